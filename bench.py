@@ -1,0 +1,380 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 FCC-DCT hot path (BASELINE.json configs[1]).
+
+Workload ("c2"): batched FCC-DCT n = 8 (N = n^3 = 512 points per block, the
+reference's index set), 65,536 independent blocks per GPU,
+fp64, inputs i.i.d. uniform[-1,1] (re and im) from a seed, one step = forward
+then inverse (round trip) of every block through the fast (radix-2x2x2)
+plan. Metric: transforms/s (one transform = one block forward OR inverse;
+points/s = N x that), whole job over all ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Multi-GPU (torchrun, one process per GPU): blocks are sharded, 65,536 per
+rank (weak scaling), no collective on the data path; the timed region is
+bracketed by barriers and the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_DEFAULT = 8
+BLOCKS_PER_GPU = 65536
+METRIC = "FCC-DCT transforms/s and points/s (fp64) vs HBM/FP64-TC roofline, 1–8 GPU"
+FP64_PEAK_TFLOPS = 37.17  # measured DMMA peak on this pool's B200 (profiles/r01_fp_peaks.txt)
+FP32_PEAK_TFLOPS = 72.4  # measured FFMA peak (profiles/r01_fp_peaks.txt)
+
+
+def measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        busy = [x for x in sm if x > 500] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(smax), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_cpu_baseline(n: int, blocks: int, threads: int, method: str = "fast") -> dict:
+    from oracle import oracle  # CPU baseline / reference arm only
+
+    oracle.build()
+    out = subprocess.run(
+        [str(oracle.CPU_BASELINE), "--n", str(n), "--blocks", str(blocks), "--threads", str(threads), "--method", method],
+        check=True, capture_output=True, text=True,
+    )
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    # each step: a bounded sample of the workload (forward + inverse of `sample` blocks)
+    sample = args.cpu_sample
+    vals = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        res = run_cpu_baseline(args.n, sample, threads, args.method)
+        if i >= args.warmup:
+            vals.append(2 * sample / (res["forward_s"] + res["inverse_s"]))
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": v,
+        "unit": "transforms/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * 2 * sample / v,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64" if args.precision == "f64" else "f32",
+        "data": "synthetic",
+        "config": {"workload": f"c2: batched FCC-DCT n={args.n} (N={args.n**3} points/block), {args.method} path, forward+inverse; CPU sample of {sample} blocks per step"},
+        "points_per_s": v * args.n**3,
+        "cpu_baseline": {
+            "value": v,
+            "unit": "transforms/s",
+            "cores": threads,
+            "kind": "port",
+            "sample": f"{sample} blocks of n={args.n}, forward then inverse, {args.method} path, reference-faithful C++ restatement (oracle/cpu_baseline.cpp), std::thread over blocks",
+        },
+        "e2e": {"value": v, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def b200_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1807_10058_b200 import SkewParams, build_plan, dense_transform, shard_range
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    dev = torch.device(f"cuda:{local if world > 1 else 0}")
+    torch.cuda.set_device(dev)
+    n = args.n
+    N = n**3
+    f32 = args.precision == "f32"
+    cdt = torch.complex64 if f32 else torch.complex128
+    rdt = torch.float32 if f32 else torch.float64
+    esize = 8 if f32 else 16
+    p = SkewParams.canonical()
+    total = args.blocks * world
+    b0, b1 = shard_range(total, rank, world)
+    blocks = b1 - b0
+
+    if args.method == "fast":
+        plan = build_plan(n, p, precision=args.precision)
+    else:
+        plan = dense_transform(n, p, precision=args.precision)._plan
+    info = plan.info
+
+    # seeded synthetic input, resident in HBM before the timed region
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = torch.complex(torch.rand((blocks, N), generator=g, device=dev, dtype=rdt) * 2 - 1,
+                      torch.rand((blocks, N), generator=g, device=dev, dtype=rdt) * 2 - 1).to(cdt)
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+    from paper_1807_10058_b200 import _capi
+    from paper_1807_10058_b200.fcct import _raise
+
+    L = _capi.lib()
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        _raise(L.fcct_forward(plan._h, x.data_ptr(), y.data_ptr(), blocks, sh))
+        if ev is not None:
+            ev[1].record(stream)
+        _raise(L.fcct_inverse(plan._h, y.data_ptr(), z.data_ptr(), blocks, sh))
+        if ev is not None:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    # correctness guard on the benchmarked data (size-independent property)
+    err = (torch.linalg.norm(z - x) / torch.linalg.norm(x)).item()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        end.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    fwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    inv_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    value = 2.0 * total * args.steps / (ms / 1e3)
+
+    # e2e: the reference-facing host-buffer API (H2D + transform + D2H each call)
+    e2e = None
+    if not args.no_e2e:
+        eb = min(blocks, args.e2e_blocks)
+        xh = x[:eb].cpu().pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        zh = torch.empty_like(xh).pin_memory()
+        for _ in range(2):
+            _raise(L.fcct_forward_host(plan._h, xh.data_ptr(), yh.data_ptr(), eb, sh))
+            _raise(L.fcct_inverse_host(plan._h, yh.data_ptr(), zh.data_ptr(), eb, sh))
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            _raise(L.fcct_forward_host(plan._h, xh.data_ptr(), yh.data_ptr(), eb, sh))
+            _raise(L.fcct_inverse_host(plan._h, yh.data_ptr(), zh.data_ptr(), eb, sh))
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {
+            "value": 2.0 * eb * world * args.e2e_steps / (ems / 1e3),
+            "unit": "transforms/s",
+            "h2d_bytes_per_step": 2 * eb * N * esize,
+            "d2h_bytes_per_step": 2 * eb * N * esize,
+            "blocks_per_step": eb,
+        }
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (the forward pipeline launch)
+    flops_fwd = info.flops_forward * blocks
+    bytes_fwd = 2.0 * N * esize * blocks
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6488.0)
+    peak_tf = FP32_PEAK_TFLOPS if f32 else FP64_PEAK_TFLOPS
+    achieved_tf = flops_fwd / (fwd_ms / 1e3) / 1e12
+    achieved_gbs = bytes_fwd / (fwd_ms / 1e3) / 1e9
+    t_star = max(bytes_fwd / (hbm * 1e9), flops_fwd / (peak_tf * 1e12))
+    roof = {
+        "bound": "tensor",
+        "achieved": achieved_tf,
+        "peak": peak_tf,
+        "unit": "TFLOP/s",
+        "frac": achieved_tf / peak_tf,
+        "traffic": args.traffic,
+        "kernel": "fcct pipeline_kernel (forward, fast path)" if args.method == "fast" else "gemm_f64_kernel (direct)",
+        "algorithmic_flops_per_launch": flops_fwd,
+        "algorithmic_bytes_per_launch": bytes_fwd,
+        "achieved_gbs": achieved_gbs,
+        "hbm_peak_gbs": hbm,
+        "t_star_over_t": t_star / (fwd_ms / 1e3),
+        "peak_source": "fp64: measured DMMA m8n8k4 peak (tools/peak_fp.cu, profiles/r01_fp_peaks.txt); HBM: MEASURED_PEAKS.json",
+        "fwd_ms": fwd_ms,
+        "inv_ms": inv_ms,
+        "inverse_achieved_tflops": info.flops_inverse * blocks / (inv_ms / 1e3) / 1e12,
+    }
+    cpu = None
+    if not args.no_cpu and world >= 1:
+        threads = os.cpu_count() or 1
+        r = run_cpu_baseline(n, args.cpu_sample, threads, args.method)
+        cpu = {
+            "value": 2 * args.cpu_sample / (r["forward_s"] + r["inverse_s"]),
+            "unit": "transforms/s",
+            "cores": threads,
+            "kind": "port",
+            "sample": f"{args.cpu_sample} blocks of n={n}, forward then inverse, {args.method} path, reference-faithful C++ restatement (oracle/cpu_baseline.cpp)",
+        }
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "transforms/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64" if not f32 else "f32",
+        "data": "synthetic",
+        "config": {
+            "workload": f"c2: batched FCC-DCT n={n} (N={N} points/block), {blocks} blocks per GPU, {args.method} path, forward then inverse per step",
+            "blocks_total": total,
+            "points_per_block": N,
+            "params": "canonical (1/8, 0, 3/8)",
+            "input": "i.i.d. uniform[-1,1] re/im from a seed (torch Philox on device)",
+            "l2": f"inputs larger than L2 ({blocks * N * esize / 2**20:.0f} MiB per array vs 126 MB L2)",
+            "parallelism": f"batch-sharded dp{world}, no collective",
+        },
+        "points_per_s": value * N,
+        "roundtrip_rel_err": err,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk.summary(),
+        "plan": {"tree_nnz": info.tree_nnz, "tree_nnz_inv": info.tree_nnz_inv, "table_bytes": info.table_bytes,
+                 "flops_forward_per_block": info.flops_forward, "flops_inverse_per_block": info.flops_inverse},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--blocks", type=int, default=BLOCKS_PER_GPU)
+    ap.add_argument("--method", default="fast", choices=["fast", "direct"])
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--cpu-sample", type=int, default=65536)
+    ap.add_argument("--e2e-blocks", type=int, default=65536)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch (from profiles/)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        b200_arm(args)
+
+
+if __name__ == "__main__":
+    main()

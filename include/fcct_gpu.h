@@ -1,0 +1,157 @@
+/*
+ * fcct_gpu.h — C ABI of the B200-native FCC-lattice cosine transform
+ * (arXiv 1807.10058). Drop-in replacement for the hot path of the reference
+ * C++ library `fcct` (/root/reference/proj/include/fcct/transform.hpp).
+ *
+ * Each entry point cites the reference interface it replaces. Plain C types
+ * only: no torch, no Eigen, no C++ exceptions cross this boundary. Errors are
+ * returned as fcct_status codes; fcct_last_error() gives the message of the
+ * last failing call on the calling thread.
+ *
+ * Data layout (byte-compatible with one Eigen::VectorXcd per block,
+ * transform.hpp:17-33): block-major [batch][n^3], each point an interleaved
+ * (re, im) pair — complex128 for FCCT_F64 plans, complex64 for FCCT_F32 —
+ * lexicographic point order (i*n + j)*n + k, last index fastest.
+ *
+ * Buffers passed to fcct_forward / fcct_inverse are DEVICE pointers owned by
+ * the caller; the *_host variants take HOST pointers and do the copies
+ * themselves (pinned memory is used internally for the staging). The plan
+ * owns its device tables. Calls on distinct streams are safe to run
+ * concurrently; results are deterministic (no atomics in any reduction).
+ */
+#ifndef FCCT_GPU_H
+#define FCCT_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error taxonomy: fcct/errors.hpp:9-63 (ErrorCategory math -> CLI exit 2,
+ * io -> exit 3; fcct.cpp:702-707). */
+typedef enum {
+    FCCT_OK = 0,
+    FCCT_INVALID_ARGUMENT = 1, /* std::invalid_argument (n < 1, bad params) */
+    FCCT_SIZE_MISMATCH = 2,    /* SizeMismatch (transform.cpp:147-154,498-521) */
+    FCCT_ODD_SIZE = 3,         /* OddSize (transform.cpp:173-175,315-317) */
+    FCCT_DEGENERATE_NODES = 4, /* DegenerateNodes (spectral.cpp:132-149) */
+    FCCT_ILL_CONDITIONED = 5,  /* IllConditioned (transform.cpp:113-117,377-378) */
+    FCCT_PARAMS_MISMATCH = 6,  /* invalid_argument "different skew grid" (:163-165,515-517) */
+    FCCT_IO = 7,               /* MalformedFile / IoFailure */
+    FCCT_CUDA = 8,             /* CUDA runtime failure */
+    FCCT_DERIVATION = 9        /* basis-change derivation residual (transform.cpp:301-304) */
+} fcct_status;
+
+typedef enum { FCCT_DIRECT = 0, FCCT_FAST = 1 } fcct_method;
+typedef enum { FCCT_F64 = 0, FCCT_F32 = 1 } fcct_precision;
+/* TransformPlan::Kind (transform.hpp:69) */
+typedef enum { FCCT_KIND_DIRECT = 0, FCCT_KIND_RADIX2 = 1 } fcct_kind;
+
+typedef struct fcct_plan_s* fcct_plan;
+
+typedef struct {
+    int n;
+    double r, s, t;          /* SkewParams of the root */
+    int kind;                /* fcct_kind of the root */
+    int method;              /* fcct_method the plan executes */
+    int precision;           /* fcct_precision */
+    int levels;              /* radix levels (log2 n for powers of two) */
+    int64_t points;          /* n^3 */
+    int64_t tree_nnz;        /* sum of nnz(B) over radix nodes, B_2 = I excluded */
+    int64_t tree_nnz_inv;    /* same for the explicit B^{-1} factors */
+    int64_t root_nnz;        /* nnz(B) of the root */
+    int64_t table_bytes;     /* device bytes owned by the plan */
+    double condition;        /* exact 1-norm condition of D (direct plans), or of the root
+                                orbit blocks (fast plans) */
+    double flops_forward;    /* algorithmic flops per block */
+    double flops_inverse;
+} fcct_plan_info_t;
+
+/* Last error message on this thread ("" if none). */
+const char* fcct_last_error(void);
+
+/* Plan creation: replaces build_plan(n, params) (transform.hpp:118-119,
+ * transform.cpp:382-408) for method FAST and dense_transform(n, params)
+ * (transform.hpp:46, transform.cpp:130-144) for method DIRECT. Tables are
+ * derived exactly (orbit-block structure, extended precision) and generated
+ * on `device`. n odd or n == 1 always yields a direct plan (transform.cpp:385-386). */
+fcct_status fcct_plan_create(int n, double r, double s, double t, int method, int precision,
+                             int device, fcct_plan* out);
+fcct_status fcct_plan_destroy(fcct_plan plan);
+fcct_status fcct_plan_info(fcct_plan plan, fcct_plan_info_t* info);
+
+/* Forward: replaces fast_apply(plan, signal) (transform.hpp:123-124,
+ * transform.cpp:496-507) and naive_apply(dense, signal) (transform.hpp:48,
+ * transform.cpp:146-156), batched. in/out are device buffers of
+ * batch * n^3 complex values; stream is a cudaStream_t (NULL = default). */
+fcct_status fcct_forward(fcct_plan plan, const void* in, void* out, int64_t batch, void* stream);
+
+/* Inverse: replaces inverse_apply(plan, spectrum) (transform.hpp:127-128,
+ * transform.cpp:509-524) and inverse_apply(dense, spectrum) (transform.hpp:49,
+ * transform.cpp:158-169). `r, s, t` of the spectrum must equal the plan's
+ * (FCCT_PARAMS_MISMATCH otherwise, transform.cpp:515-517). */
+fcct_status fcct_inverse(fcct_plan plan, const void* in, void* out, int64_t batch, void* stream);
+fcct_status fcct_inverse_checked(fcct_plan plan, double r, double s, double t, const void* in,
+                                 void* out, int64_t batch, void* stream);
+
+/* Host-buffer variants (the call a CPU caller of fcct makes): host -> device
+ * copy, transform, device -> host copy, synchronous on `stream`. */
+fcct_status fcct_forward_host(fcct_plan plan, const void* in_host, void* out_host, int64_t batch,
+                              void* stream);
+fcct_status fcct_inverse_host(fcct_plan plan, const void* in_host, void* out_host, int64_t batch,
+                              void* stream);
+
+/* radix_permutation(n) (transform.hpp:55, transform.cpp:171-194): n^3 entries,
+ * bit-exact. Computed on the device from the closed-form digit interleave. */
+fcct_status fcct_radix_permutation(int n, uint64_t* out_host);
+
+/* dense_transform(n, params).matrix (transform.hpp:39-46): column-major n^3 x n^3
+ * complex128, generated on the device into the caller's device buffer. */
+fcct_status fcct_dense_matrix(int n, double r, double s, double t, void* out_device, void* stream);
+
+/* Skew node set (skew_nodes, spectral.cpp:261-277) generated on the device:
+ * per node 6 complex128 values (u, v, w, x, y, z); runs the degeneracy check
+ * for n <= 16 (spectral.cpp:132-149). */
+fcct_status fcct_skew_nodes(int n, double r, double s, double t, void* out_device, void* stream);
+
+/* TransformPlan accessors (transform.hpp:71-84). kernel(): 8x8 column-major
+ * complex128. basis(): CSC export (colptr[n^3+1], rowidx[nnz], values[2*nnz]);
+ * pass NULL arrays to query *nnz only. child: index 0..7 of a radix plan. */
+fcct_status fcct_plan_kernel(fcct_plan plan, double* out128);
+fcct_status fcct_plan_basis(fcct_plan plan, int64_t* nnz, int64_t* colptr, int32_t* rowidx,
+                            double* values);
+fcct_status fcct_plan_child(fcct_plan plan, int index, int* n, double* r, double* s, double* t,
+                            int* kind);
+
+/* factorization_residual(plan, dense) (transform.hpp:132-133,
+ * transform.cpp:526-540): max |fast(e_k) - D e_k| over all k, evaluated on the
+ * device. */
+fcct_status fcct_factorization_residual(fcct_plan plan, double* out);
+
+/* with_perturbed_basis(plan, delta) (transform.hpp:138-139,
+ * transform.cpp:542-554): copy of a FAST plan with delta added to the first
+ * stored basis entry of the root; children shared. */
+fcct_status fcct_plan_perturbed_basis(fcct_plan plan, double delta, fcct_plan* out);
+
+/* basis_change(n, params) (transform.hpp:57-62, transform.cpp:314-320): the
+ * sparse factor B (inverse = 0) or its explicit inverse (inverse = 1) in CSC,
+ * derived on the host (no GPU needed). Pass NULL arrays to query *nnz. */
+fcct_status fcct_basis_change(int n, double r, double s, double t, int inverse, int64_t* nnz, int64_t* colptr,
+                              int32_t* rowidx, double* values);
+
+/* Host-side tree statistics of the fast plan (no GPU needed): tree nnz of B and
+ * B^{-1} (B_2 = I excluded) and the algorithmic flops per block. */
+fcct_status fcct_plan_tree_stats(int n, double r, double s, double t, int64_t* tree_nnz_fwd, int64_t* tree_nnz_inv,
+                                 double* flops_fwd, double* flops_inv);
+
+/* Batch scheduler for one process of a multi-GPU job: contiguous block range
+ * [begin, end) of `total` blocks owned by `rank` of `world` (ceil split,
+ * uneven tail allowed). No collective is involved. */
+fcct_status fcct_shard_range(int64_t total, int rank, int world, int64_t* begin, int64_t* end);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCCT_GPU_H */

@@ -1,0 +1,894 @@
+// ===========================================================================
+// ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// CPU restatement of the reference FCC-DCT path (fcct, /root/reference/proj).
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+// arm may load this library, and only as the checker or the CPU baseline.
+// The product (paper_1807_10058_b200/) never links, loads or calls it.
+//
+// Parity pinning: the reference cannot be compiled here (Eigen3, doctest and
+// CLI11 are absent), so this restatement is pinned against the
+// reference's own known-answer tests instead (tests/test_oracle_pins.py):
+// the 24 group matrices (tests/unit/test_weyl_s4.cpp:15-28), orbit sizes, the
+// permutation golden value p4[46] == 57 (test_transform.cpp:105-107),
+// B_2 == I with nnz 8 (test_transform.cpp:110-118), the constant / y columns
+// of D (test_transform.cpp:49-72), per-node brute force evaluation
+// (test_transform.cpp:25-38,74-86), the fast-vs-naive and round-trip
+// tolerances (test_transform.cpp:138-183) and the factorization residual
+// (test_transform.cpp:120-136, acceptance/main.cpp:325-348).
+//
+// Every function cites the reference file:line it restates. Eigen kernels
+// (GEMV, PartialPivLU, SparseLU) are replaced by plain loops; the sparse LU
+// solve of the fast inverse is replaced by a dense LU of B (n <= 8 only).
+// ===========================================================================
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <map>
+#include <memory>
+#include <numbers>
+#include <random>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace oracle {
+
+using Complex = std::complex<double>;
+using CLD = std::complex<long double>;
+using Index3 = std::array<int, 3>;
+
+enum Status {
+    OK = 0,
+    INVALID_ARGUMENT = 1,
+    SIZE_MISMATCH = 2,
+    ODD_SIZE = 3,
+    DEGENERATE_NODES = 4,
+    ILL_CONDITIONED = 5,
+    PARAMS_MISMATCH = 6,
+    DERIVATION = 9,
+};
+
+struct OracleError : std::runtime_error {
+    int code;
+    OracleError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+constexpr double two_pi = 2.0 * std::numbers::pi;
+
+// --- S4 Weyl group: src/weyl_s4.cpp:10-92 --------------------------------
+struct Elem {
+    std::array<int, 9> m;
+    bool operator<(const Elem& o) const { return m < o.m; }
+    bool operator==(const Elem& o) const { return m == o.m; }
+    Elem operator*(const Elem& r) const {  // src/weyl_s4.cpp:14-23
+        Elem out{};
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) {
+                int acc = 0;
+                for (int k = 0; k < 3; ++k) acc += m[i * 3 + k] * r.m[k * 3 + j];
+                out.m[i * 3 + j] = acc;
+            }
+        return out;
+    }
+    Index3 apply(const Index3& k) const {  // src/weyl_s4.cpp:38-43
+        Index3 o{};
+        for (int i = 0; i < 3; ++i)
+            o[i] = m[i * 3 + 0] * k[0] + m[i * 3 + 1] * k[1] + m[i * 3 + 2] * k[2];
+        return o;
+    }
+};
+
+// BFS closure of the generators, identity first (src/weyl_s4.cpp:54-83).
+const std::vector<Elem>& group() {
+    static const std::vector<Elem> g = [] {
+        const std::array<Elem, 3> gens{Elem{{-1, 0, 0, 1, 1, 0, 0, 0, 1}},
+                                       Elem{{1, 1, 0, 0, -1, 0, 0, 1, 1}},
+                                       Elem{{1, 0, 0, 0, 1, 1, 0, 0, -1}}};
+        std::vector<Elem> out;
+        std::set<Elem> seen;
+        std::deque<Elem> frontier{Elem{{1, 0, 0, 0, 1, 0, 0, 0, 1}}};
+        seen.insert(frontier.front());
+        while (!frontier.empty()) {
+            Elem g = frontier.front();
+            frontier.pop_front();
+            out.push_back(g);
+            for (const auto& s : gens) {
+                Elem nx = g * s;
+                if (seen.insert(nx).second) frontier.push_back(nx);
+            }
+        }
+        if (out.size() != 24) throw std::logic_error("group closure != 24");
+        return out;
+    }();
+    return g;
+}
+
+// --- unit phases: src/transform.cpp:28-30, src/spectral.cpp:124-126 ------
+Complex unit_phase(double turns) {
+    return Complex{std::cos(two_pi * turns), std::sin(two_pi * turns)};
+}
+
+struct Params {
+    double r, s, t;
+};
+
+// SkewParams::child, src/spectral.cpp:155-157
+Params child_params(const Params& p, int ir, int is, int it) {
+    return Params{(p.r + ir) / 2.0, (p.s + is) / 2.0, (p.t + it) / 2.0};
+}
+
+// --- nodes: src/chebyshev.cpp:326-342, src/spectral.cpp:132-149,261-277 ---
+struct Node {
+    Index3 ijk;
+    Complex u, v, w;
+    Complex x, y, z;
+};
+
+double wrap_turn(double a) {  // TorusPoint::wrapped, src/chebyshev.cpp:326-335
+    double f = a - std::floor(a);
+    if (f >= 1.0 - 1e-15) f = 0.0;
+    return f;
+}
+
+void coords_from_uvw(Node& nd) {  // src/chebyshev.cpp:372-381
+    const Complex u = nd.u, v = nd.v, w = nd.w;
+    const Complex ui = 1.0 / u, vi = 1.0 / v, wi = 1.0 / w;
+    nd.x = 0.25 * (u + ui * v + vi * w + wi);
+    nd.y = (vi + v + u * wi + ui * v * wi + ui * w + u * vi * w) / 6.0;
+    nd.z = 0.25 * (ui + u * vi + v * wi + w);
+}
+
+std::vector<Node> skew_nodes(int n, const Params& p, bool check) {
+    if (n < 1) throw OracleError(INVALID_ARGUMENT, "skew_nodes: n must be >= 1");
+    std::vector<Node> nodes;
+    nodes.reserve(static_cast<size_t>(n) * n * n);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j)
+            for (int k = 0; k < n; ++k) {
+                Node nd;
+                nd.ijk = {i, j, k};
+                const double a = wrap_turn((p.r + i) / n);
+                const double b = wrap_turn((p.s + j) / n);
+                const double c = wrap_turn((p.t + k) / n);
+                nd.u = Complex{std::cos(two_pi * a), std::sin(two_pi * a)};
+                nd.v = Complex{std::cos(two_pi * b), std::sin(two_pi * b)};
+                nd.w = Complex{std::cos(two_pi * c), std::sin(two_pi * c)};
+                coords_from_uvw(nd);
+                nodes.push_back(nd);
+            }
+    // check_not_degenerate: n <= 16 only (src/spectral.cpp:132-149)
+    if (check && n <= 16) {
+        constexpr double th = 1e-9 * 1e-9;
+        for (size_t a = 0; a < nodes.size(); ++a)
+            for (size_t b = a + 1; b < nodes.size(); ++b) {
+                const double d = std::norm(nodes[a].x - nodes[b].x) +
+                                 std::norm(nodes[a].y - nodes[b].y) +
+                                 std::norm(nodes[a].z - nodes[b].z);
+                if (d < th)
+                    throw OracleError(DEGENERATE_NODES,
+                                      "nodes map to the same spectral point");
+            }
+    }
+    return nodes;
+}
+
+// common_zeros, src/spectral.cpp:242-259
+std::vector<Node> common_zeros(int n) {
+    std::vector<Node> nodes;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j)
+            for (int k = 0; k < n; ++k) {
+                Node nd;
+                nd.ijk = {i, j, k};
+                nd.u = unit_phase(double(1 + 8 * i) / (8.0 * n));
+                nd.v = unit_phase(double(j) / n);
+                nd.w = unit_phase(double(3 + 8 * k) / (8.0 * n));
+                coords_from_uvw(nd);
+                nodes.push_back(nd);
+            }
+    return nodes;
+}
+
+// --- Chebyshev evaluation: src/chebyshev.cpp:310-322,363-370 -------------
+Complex ipow(Complex base, int e) {
+    if (e < 0) {
+        base = 1.0 / base;
+        e = -e;
+    }
+    Complex acc{1.0, 0.0};
+    while (e > 0) {
+        if (e & 1) acc *= base;
+        base *= base;
+        e >>= 1;
+    }
+    return acc;
+}
+
+Complex cheb_eval_uvw(const Index3& k, Complex u, Complex v, Complex w) {
+    Complex acc{0.0, 0.0};
+    for (const auto& g : group()) {
+        const Index3 wk = g.apply(k);
+        acc += ipow(u, wk[0]) * ipow(v, wk[1]) * ipow(w, wk[2]);
+    }
+    return acc / 24.0;
+}
+
+// --- ColumnEvaluator: src/transform.cpp:35-82 ------------------------------
+template <typename C, typename R>
+struct ColumnEvaluator {
+    int n;
+    Params p;
+    std::vector<C> omega;
+    mutable std::vector<C> a_, b_, c_;
+    ColumnEvaluator(int n_, const Params& p_) : n(n_), p(p_) {
+        omega.resize(n);
+        for (int j = 0; j < n; ++j) omega[j] = phase(static_cast<R>(j) / n);
+        a_.resize(n);
+        b_.resize(n);
+        c_.resize(n);
+    }
+    static C phase(R turns) {
+        if constexpr (std::is_same_v<R, double>) {
+            return unit_phase(turns);
+        } else {
+            const R tp = 2 * std::numbers::pi_v<long double>;
+            return C{std::cos(tp * turns), std::sin(tp * turns)};
+        }
+    }
+    void fill_axis(int freq, std::vector<C>& table) const {
+        const int f = ((freq % n) + n) % n;
+        for (int i = 0; i < n; ++i)
+            table[i] = omega[static_cast<int>((static_cast<int64_t>(f) * i) % n)];
+    }
+    void column(const Index3& kappa, C* out) const {
+        const int64_t n3 = static_cast<int64_t>(n) * n * n;
+        std::fill(out, out + n3, C{0, 0});
+        for (const auto& w : group()) {
+            const Index3 a = w.apply(kappa);
+            const C prefac =
+                phase((static_cast<R>(p.r) * a[0] + static_cast<R>(p.s) * a[1] +
+                       static_cast<R>(p.t) * a[2]) /
+                      n);
+            fill_axis(a[0], a_);
+            fill_axis(a[1], b_);
+            fill_axis(a[2], c_);
+            C* dst = out;
+            for (int i = 0; i < n; ++i) {
+                const C pa = prefac * a_[i];
+                for (int l = 0; l < n; ++l) {
+                    const C pab = pa * b_[l];
+                    for (int q = 0; q < n; ++q) *dst++ += pab * c_[q];
+                }
+            }
+        }
+        const R scale = R(1) / R(24);
+        for (int64_t i = 0; i < n3; ++i) out[i] *= scale;
+    }
+};
+
+Index3 unflatten(int64_t flat, int n) {  // src/transform.cpp:84-89
+    const int p = static_cast<int>(flat % n);
+    const int k = static_cast<int>((flat / n) % n);
+    const int j = static_cast<int>(flat / (static_cast<int64_t>(n) * n));
+    return Index3{j, k, p};
+}
+
+// Dense matrix, column-major (Eigen default), rows = nodes, cols = (j,k,p).
+// dense_transform, src/transform.cpp:130-144
+template <typename C, typename R>
+std::vector<C> dense_matrix(int n, const Params& p, bool check_nodes = true) {
+    if (n < 1) throw OracleError(INVALID_ARGUMENT, "dense_transform: n must be >= 1");
+    if (check_nodes) skew_nodes(n, p, true);
+    const int64_t n3 = static_cast<int64_t>(n) * n * n;
+    std::vector<C> m(static_cast<size_t>(n3 * n3));
+    const ColumnEvaluator<C, R> ev(n, p);
+    for (int64_t col = 0; col < n3; ++col) ev.column(unflatten(col, n), m.data() + col * n3);
+    return m;
+}
+
+// --- dense LU with partial pivoting (restates Eigen::PartialPivLU) -------
+template <typename C>
+struct DenseLU {
+    int64_t dim = 0;
+    std::vector<C> lu;  // column-major
+    std::vector<int64_t> piv;
+    bool singular = false;
+    DenseLU() = default;
+    DenseLU(const C* a, int64_t d) : dim(d), lu(a, a + d * d), piv(d) {
+        for (int64_t k = 0; k < d; ++k) {
+            int64_t best = k;
+            auto bv = std::abs(lu[k + k * d]);
+            for (int64_t i = k + 1; i < d; ++i) {
+                auto v = std::abs(lu[i + k * d]);
+                if (v > bv) { bv = v; best = i; }
+            }
+            piv[k] = best;
+            if (best != k)
+                for (int64_t j = 0; j < d; ++j) std::swap(lu[k + j * d], lu[best + j * d]);
+            const C pv = lu[k + k * d];
+            if (pv == C{0, 0}) { singular = true; continue; }
+            const C inv = C{1, 0} / pv;
+            for (int64_t i = k + 1; i < d; ++i) lu[i + k * d] *= inv;
+            for (int64_t j = k + 1; j < d; ++j) {
+                const C f = lu[k + j * d];
+                if (f == C{0, 0}) continue;
+                C* cj = &lu[j * d];
+                const C* ck = &lu[k * d];
+                for (int64_t i = k + 1; i < d; ++i) cj[i] -= ck[i] * f;
+            }
+        }
+    }
+    void solve_inplace(C* b) const {
+        for (int64_t k = 0; k < dim; ++k)
+            if (piv[k] != k) std::swap(b[k], b[piv[k]]);
+        for (int64_t j = 0; j < dim; ++j) {
+            const C bj = b[j];
+            if (bj == C{0, 0}) continue;
+            for (int64_t i = j + 1; i < dim; ++i) b[i] -= lu[i + j * dim] * bj;
+        }
+        for (int64_t j = dim - 1; j >= 0; --j) {
+            b[j] /= lu[j + j * dim];
+            const C bj = b[j];
+            if (bj == C{0, 0}) continue;
+            for (int64_t i = 0; i < j; ++i) b[i] -= lu[i + j * dim] * bj;
+        }
+    }
+};
+
+// condition_with_lu, src/transform.cpp:91-111 (probes: 3 unit vectors, 5
+// random-sign vectors from mt19937(12345)).
+double condition_with_lu(const Complex* a, int64_t dim, const DenseLU<Complex>& lu) {
+    double norm_a = 0.0;
+    for (int64_t j = 0; j < dim; ++j) {
+        double s = 0.0;
+        for (int64_t i = 0; i < dim; ++i) s += std::abs(a[i + j * dim]);
+        norm_a = std::max(norm_a, s);
+    }
+    if (lu.singular) return INFINITY;
+    double inv_norm = 0.0;
+    for (int64_t j : {int64_t{0}, dim / 2, dim - 1}) {
+        std::vector<Complex> e(dim, Complex{0, 0});
+        e[j] = 1.0;
+        lu.solve_inplace(e.data());
+        double s = 0;
+        for (auto v : e) s += std::abs(v);
+        inv_norm = std::max(inv_norm, s);
+    }
+    std::mt19937 rng(12345);
+    std::uniform_int_distribution<int> coin(0, 1);
+    for (int probe = 0; probe < 5; ++probe) {
+        std::vector<Complex> v(dim);
+        for (int64_t i = 0; i < dim; ++i)
+            v[i] = Complex(coin(rng) ? 1.0 : -1.0, coin(rng) ? 1.0 : -1.0);
+        double vn = 0;
+        for (auto z : v) vn += std::abs(z);
+        lu.solve_inplace(v.data());
+        double s = 0;
+        for (auto z : v) s += std::abs(z);
+        inv_norm = std::max(inv_norm, s / vn);
+    }
+    return norm_a * inv_norm;
+}
+
+void require_condition(double cond, const std::string& what) {  // src/transform.cpp:113-117
+    if (!(cond <= 1e12))
+        throw OracleError(ILL_CONDITIONED, what + ": condition estimate exceeds 1e12");
+}
+
+// radix_permutation, src/transform.cpp:171-194
+std::vector<uint64_t> radix_permutation(int n) {
+    if (n < 2) throw OracleError(INVALID_ARGUMENT, "radix_permutation: n must be >= 2");
+    if (n % 2 != 0) throw OracleError(ODD_SIZE, "radix_permutation: odd size");
+    const int m = n / 2;
+    const int64_t m3 = static_cast<int64_t>(m) * m * m;
+    std::vector<uint64_t> perm(static_cast<size_t>(n) * n * n);
+    for (int ir = 0; ir < 2; ++ir)
+        for (int is = 0; is < 2; ++is)
+            for (int it = 0; it < 2; ++it) {
+                const int blk = (ir * 2 + is) * 2 + it;
+                size_t idx = static_cast<size_t>(blk) * m3;
+                for (int kr = 0; kr < m; ++kr)
+                    for (int ks = 0; ks < m; ++ks)
+                        for (int kt = 0; kt < m; ++kt)
+                            perm[idx++] = static_cast<uint64_t>(
+                                (static_cast<int64_t>(ir + 2 * kr) * n + (is + 2 * ks)) * n +
+                                (it + 2 * kt));
+            }
+    return perm;
+}
+
+// --- sparse matrix (CSC, like Eigen's compressed column storage) ----------
+struct Sparse {
+    int64_t dim = 0;
+    std::vector<int64_t> colptr;
+    std::vector<int32_t> rowidx;
+    std::vector<Complex> val;
+    int64_t nnz() const { return static_cast<int64_t>(val.size()); }
+};
+
+// derive_basis, src/transform.cpp:202-310: solve (K (x) I)(blockdiag child) z
+// = P^T D column by column in 256-column batches, prune |v| < 1e-12, verify
+// the reassembled product for n <= 8.
+Sparse derive_basis(int n, const Params& p, const std::vector<Complex>& kernel /*8x8 col-major*/) {
+    const int m = n / 2;
+    const int64_t n3 = static_cast<int64_t>(n) * n * n, m3 = static_cast<int64_t>(m) * m * m;
+    const auto perm = radix_permutation(n);
+    std::array<std::vector<Complex>, 8> child_dense;
+    std::array<DenseLU<Complex>, 8> child_lu;
+    const bool validate = n <= 8;
+    for (int ir = 0; ir < 2; ++ir)
+        for (int is = 0; is < 2; ++is)
+            for (int it = 0; it < 2; ++it) {
+                const int blk = (ir * 2 + is) * 2 + it;
+                auto mat = dense_matrix<Complex, double>(m, child_params(p, ir, is, it));
+                child_lu[blk] = DenseLU<Complex>(mat.data(), m3);
+                require_condition(condition_with_lu(mat.data(), m3, child_lu[blk]), "child block");
+                if (validate) child_dense[blk] = std::move(mat);
+            }
+    DenseLU<Complex> kernel_lu(kernel.data(), 8);
+    require_condition(condition_with_lu(kernel.data(), 8, kernel_lu), "radix kernel");
+
+    const ColumnEvaluator<Complex, double> ev(n, p);
+    std::vector<Complex> d(n3), y(n3), gathered(8);
+    Sparse out;
+    out.dim = n3;
+    out.colptr.assign(n3 + 1, 0);
+    double worst_residual = 0.0;
+    for (int64_t col = 0; col < n3; ++col) {
+        ev.column(unflatten(col, n), d.data());
+        for (int64_t idx = 0; idx < n3; ++idx) y[idx] = d[perm[idx]];
+        for (int blk = 0; blk < 8; ++blk) child_lu[blk].solve_inplace(y.data() + blk * m3);
+        for (int64_t h = 0; h < m3; ++h) {
+            for (int g = 0; g < 8; ++g) gathered[g] = y[g * m3 + h];
+            kernel_lu.solve_inplace(gathered.data());
+            for (int g = 0; g < 8; ++g) y[g * m3 + h] = gathered[g];
+        }
+        for (int64_t row = 0; row < n3; ++row) {
+            if (std::abs(y[row]) >= 1e-12) {
+                out.rowidx.push_back(static_cast<int32_t>(row));
+                out.val.push_back(y[row]);
+            } else {
+                y[row] = 0.0;
+            }
+        }
+        out.colptr[col + 1] = out.nnz();
+        if (validate) {
+            std::vector<Complex> mixed(n3), tr(n3);
+            for (int64_t h = 0; h < m3; ++h)
+                for (int g = 0; g < 8; ++g) {
+                    Complex acc{0, 0};
+                    for (int q = 0; q < 8; ++q) acc += kernel[g + q * 8] * y[q * m3 + h];
+                    mixed[g * m3 + h] = acc;
+                }
+            for (int blk = 0; blk < 8; ++blk)
+                for (int64_t i = 0; i < m3; ++i) {
+                    Complex acc{0, 0};
+                    for (int64_t j = 0; j < m3; ++j)
+                        acc += child_dense[blk][i + j * m3] * mixed[blk * m3 + j];
+                    tr[blk * m3 + i] = acc;
+                }
+            for (int64_t idx = 0; idx < n3; ++idx)
+                worst_residual = std::max(worst_residual, std::abs(tr[idx] - d[perm[idx]]));
+        }
+    }
+    if (validate && worst_residual > 1e-9)
+        throw OracleError(DERIVATION, "basis-change derivation residual exceeds 1e-9");
+    return out;
+}
+
+// --- plan tree: src/transform.cpp:322-494 --------------------------------
+struct Plan {
+    bool radix = false;
+    int n = 0;
+    Params p{};
+    // direct
+    std::vector<Complex> dense;
+    DenseLU<Complex> dense_lu;
+    // radix
+    std::vector<uint64_t> perm;
+    std::vector<Complex> kernel, kernel_inv;  // 8x8 col-major
+    Sparse basis;
+    DenseLU<Complex> basis_lu;  // stands in for SparseLU<COLAMD> (:322-324,375-378)
+    Sparse basis_inv;           // explicit B^{-1} (pruned < 1e-12) for n^3 <= 512: the
+                                // sparse solve the CPU baseline times
+    std::array<std::shared_ptr<const Plan>, 8> children;
+
+    std::vector<Complex> apply_values(const std::vector<Complex>& x) const;  // :429-460
+    std::vector<Complex> solve_values(const std::vector<Complex>& q) const;  // :462-494
+};
+
+std::shared_ptr<const Plan> make_plan(int n, const Params& p) {  // PlanBuilder::make :382-401
+    if (n < 1) throw OracleError(INVALID_ARGUMENT, "build_plan: n must be >= 1");
+    auto plan = std::make_shared<Plan>();
+    plan->n = n;
+    plan->p = p;
+    const int64_t n3 = static_cast<int64_t>(n) * n * n;
+    if (n == 1 || n % 2 != 0) {  // assemble_direct :329-345
+        plan->radix = false;
+        plan->dense = dense_matrix<Complex, double>(n, p);
+        plan->dense_lu = DenseLU<Complex>(plan->dense.data(), n3);
+        require_condition(condition_with_lu(plan->dense.data(), n3, plan->dense_lu), "dense transform");
+        return plan;
+    }
+    const int m = n / 2;
+    for (int ir = 0; ir < 2; ++ir)
+        for (int is = 0; is < 2; ++is)
+            for (int it = 0; it < 2; ++it)
+                plan->children[(ir * 2 + is) * 2 + it] = make_plan(m, child_params(p, ir, is, it));
+    plan->radix = true;
+    plan->kernel = dense_matrix<Complex, double>(2, p);
+    plan->basis = derive_basis(n, p, plan->kernel);
+    plan->perm = radix_permutation(n);
+    // assemble_radix :347-380
+    DenseLU<Complex> klu(plan->kernel.data(), 8);
+    require_condition(condition_with_lu(plan->kernel.data(), 8, klu), "radix kernel");
+    plan->kernel_inv.assign(64, Complex{0, 0});
+    for (int j = 0; j < 8; ++j) {
+        std::vector<Complex> e(8, Complex{0, 0});
+        e[j] = 1.0;
+        klu.solve_inplace(e.data());
+        for (int i = 0; i < 8; ++i) plan->kernel_inv[i + j * 8] = e[i];
+    }
+    if (n3 <= 4096) {
+        std::vector<Complex> bd(static_cast<size_t>(n3 * n3), Complex{0, 0});
+        for (int64_t c = 0; c < n3; ++c)
+            for (int64_t k = plan->basis.colptr[c]; k < plan->basis.colptr[c + 1]; ++k)
+                bd[plan->basis.rowidx[k] + c * n3] = plan->basis.val[k];
+        plan->basis_lu = DenseLU<Complex>(bd.data(), n3);
+        if (plan->basis_lu.singular)
+            throw OracleError(ILL_CONDITIONED, "basis-change factor is not invertible");
+        if (n3 <= 512) {
+            Sparse& bi = plan->basis_inv;
+            bi.dim = n3;
+            bi.colptr.assign(n3 + 1, 0);
+            std::vector<Complex> e(n3);
+            for (int64_t c = 0; c < n3; ++c) {
+                std::fill(e.begin(), e.end(), Complex{0, 0});
+                e[c] = 1.0;
+                plan->basis_lu.solve_inplace(e.data());
+                for (int64_t r = 0; r < n3; ++r)
+                    if (std::abs(e[r]) >= 1e-12) {
+                        bi.rowidx.push_back(static_cast<int32_t>(r));
+                        bi.val.push_back(e[r]);
+                    }
+                bi.colptr[c + 1] = bi.nnz();
+            }
+        }
+    }
+    return plan;
+}
+
+std::vector<Complex> Plan::apply_values(const std::vector<Complex>& x) const {
+    const int64_t n3 = static_cast<int64_t>(n) * n * n;
+    if (!radix) {
+        std::vector<Complex> y(n3, Complex{0, 0});
+        for (int64_t j = 0; j < n3; ++j)
+            for (int64_t i = 0; i < n3; ++i) y[i] += dense[i + j * n3] * x[j];
+        return y;
+    }
+    const int64_t m3 = n3 / 8;
+    std::vector<Complex> t(n3, Complex{0, 0});
+    for (int64_t c = 0; c < n3; ++c)
+        for (int64_t k = basis.colptr[c]; k < basis.colptr[c + 1]; ++k)
+            t[basis.rowidx[k]] += basis.val[k] * x[c];
+    std::vector<Complex> y(n3);
+    for (int blk = 0; blk < 8; ++blk) {
+        std::vector<Complex> in(m3);
+        for (int64_t h = 0; h < m3; ++h) {
+            Complex acc{0, 0};
+            for (int g = 0; g < 8; ++g) acc += t[g * m3 + h] * kernel[blk + g * 8];
+            in[h] = acc;
+        }
+        auto out = children[blk]->apply_values(in);
+        std::copy(out.begin(), out.end(), y.begin() + blk * m3);
+    }
+    std::vector<Complex> out(n3);
+    for (int64_t idx = 0; idx < n3; ++idx) out[perm[idx]] = y[idx];
+    return out;
+}
+
+std::vector<Complex> Plan::solve_values(const std::vector<Complex>& q) const {
+    const int64_t n3 = static_cast<int64_t>(n) * n * n;
+    if (!radix) {
+        std::vector<Complex> x(q);
+        dense_lu.solve_inplace(x.data());
+        return x;
+    }
+    if (basis_lu.dim == 0) throw OracleError(INVALID_ARGUMENT, "oracle fast solve limited to n <= 16");
+    const int64_t m3 = n3 / 8;
+    std::vector<Complex> y(n3);
+    for (int64_t idx = 0; idx < n3; ++idx) y[idx] = q[perm[idx]];
+    std::vector<Complex> x(n3);
+    for (int blk = 0; blk < 8; ++blk) {
+        std::vector<Complex> in(y.begin() + blk * m3, y.begin() + (blk + 1) * m3);
+        auto out = children[blk]->solve_values(in);
+        std::copy(out.begin(), out.end(), x.begin() + blk * m3);
+    }
+    std::vector<Complex> t(n3);
+    for (int64_t h = 0; h < m3; ++h)
+        for (int blk = 0; blk < 8; ++blk) {
+            Complex acc{0, 0};
+            for (int g = 0; g < 8; ++g) acc += x[g * m3 + h] * kernel_inv[blk + g * 8];
+            t[blk * m3 + h] = acc;
+        }
+    if (basis_inv.dim == n3) {
+        std::vector<Complex> out(n3, Complex{0, 0});
+        for (int64_t c = 0; c < n3; ++c)
+            for (int64_t k = basis_inv.colptr[c]; k < basis_inv.colptr[c + 1]; ++k)
+                out[basis_inv.rowidx[k]] += basis_inv.val[k] * t[c];
+        return out;
+    }
+    basis_lu.solve_inplace(t.data());
+    return t;
+}
+
+thread_local std::string g_last_error;
+
+}  // namespace oracle
+
+using namespace oracle;
+
+#define ORACLE_TRY(...)                     \
+    try {                                   \
+        __VA_ARGS__;                        \
+        return OK;                          \
+    } catch (const OracleError& e) {        \
+        g_last_error = e.what();            \
+        return e.code;                      \
+    } catch (const std::exception& e) {     \
+        g_last_error = e.what();            \
+        return INVALID_ARGUMENT;            \
+    }
+
+extern "C" {
+
+const char* oracle_last_error() { return g_last_error.c_str(); }
+
+// 24 x 9 ints, BFS order (src/weyl_s4.cpp:60-83).
+int oracle_group(int* out) {
+    const auto& g = group();
+    for (int e = 0; e < 24; ++e)
+        for (int k = 0; k < 9; ++k) out[e * 9 + k] = g[e].m[k];
+    return OK;
+}
+
+// nodes: per node 12 doubles (u,v,w,x,y,z as re,im pairs).
+int oracle_skew_nodes(int n, double r, double s, double t, int check, double* out) {
+    ORACLE_TRY({
+        auto nodes = skew_nodes(n, Params{r, s, t}, check != 0);
+        for (size_t i = 0; i < nodes.size(); ++i) {
+            const Complex v[6] = {nodes[i].u, nodes[i].v, nodes[i].w,
+                                  nodes[i].x, nodes[i].y, nodes[i].z};
+            for (int c = 0; c < 6; ++c) {
+                out[i * 12 + 2 * c] = v[c].real();
+                out[i * 12 + 2 * c + 1] = v[c].imag();
+            }
+        }
+    })
+}
+
+int oracle_common_zeros(int n, double* out) {
+    ORACLE_TRY({
+        auto nodes = common_zeros(n);
+        for (size_t i = 0; i < nodes.size(); ++i) {
+            const Complex v[6] = {nodes[i].u, nodes[i].v, nodes[i].w,
+                                  nodes[i].x, nodes[i].y, nodes[i].z};
+            for (int c = 0; c < 6; ++c) {
+                out[i * 12 + 2 * c] = v[c].real();
+                out[i * 12 + 2 * c + 1] = v[c].imag();
+            }
+        }
+    })
+}
+
+// cheb_eval_uvw at one uvw point (6 doubles) -> out[2].
+int oracle_cheb_eval_uvw(int k0, int k1, int k2, const double* uvw, double* out) {
+    ORACLE_TRY({
+        const Complex v = cheb_eval_uvw({k0, k1, k2}, Complex{uvw[0], uvw[1]},
+                                        Complex{uvw[2], uvw[3]}, Complex{uvw[4], uvw[5]});
+        out[0] = v.real();
+        out[1] = v.imag();
+    })
+}
+
+// Dense D_n(r,s,t), column-major complex128 (2*N*N doubles). ext != 0 uses
+// long double arithmetic throughout (the high-accuracy oracle).
+int oracle_dense_transform(int n, double r, double s, double t, int ext, double* out) {
+    ORACLE_TRY({
+        const int64_t n3 = static_cast<int64_t>(n) * n * n;
+        if (ext) {
+            auto m = dense_matrix<CLD, long double>(n, Params{r, s, t});
+            for (int64_t i = 0; i < n3 * n3; ++i) {
+                out[2 * i] = static_cast<double>(m[i].real());
+                out[2 * i + 1] = static_cast<double>(m[i].imag());
+            }
+        } else {
+            auto m = dense_matrix<Complex, double>(n, Params{r, s, t});
+            std::memcpy(out, m.data(), sizeof(Complex) * n3 * n3);
+        }
+    })
+}
+
+// y = D x for `batch` vectors, accumulated in long double with D generated in
+// long double (the primary forward oracle). x, y: [batch][N] complex128.
+int oracle_forward_dense(int n, double r, double s, double t, int64_t batch,
+                         const double* x, double* y) {
+    ORACLE_TRY({
+        const int64_t n3 = static_cast<int64_t>(n) * n * n;
+        auto m = dense_matrix<CLD, long double>(n, Params{r, s, t});
+        std::vector<CLD> acc(n3);
+        for (int64_t b = 0; b < batch; ++b) {
+            std::fill(acc.begin(), acc.end(), CLD{0, 0});
+            const double* xb = x + 2 * n3 * b;
+            for (int64_t j = 0; j < n3; ++j) {
+                const CLD xj{xb[2 * j], xb[2 * j + 1]};
+                const CLD* col = &m[j * n3];
+                for (int64_t i = 0; i < n3; ++i) acc[i] += col[i] * xj;
+            }
+            for (int64_t i = 0; i < n3; ++i) {
+                y[2 * n3 * b + 2 * i] = static_cast<double>(acc[i].real());
+                y[2 * n3 * b + 2 * i + 1] = static_cast<double>(acc[i].imag());
+            }
+        }
+    })
+}
+
+// x = D^{-1} y via partial-pivot LU in long double (the primary inverse
+// oracle; restates inverse_apply(dense), src/transform.cpp:158-169).
+int oracle_inverse_dense(int n, double r, double s, double t, int64_t batch,
+                         const double* y, double* x) {
+    ORACLE_TRY({
+        const int64_t n3 = static_cast<int64_t>(n) * n * n;
+        auto m = dense_matrix<CLD, long double>(n, Params{r, s, t});
+        DenseLU<CLD> lu(m.data(), n3);
+        if (lu.singular) throw OracleError(ILL_CONDITIONED, "dense transform is singular");
+        std::vector<CLD> v(n3);
+        for (int64_t b = 0; b < batch; ++b) {
+            for (int64_t i = 0; i < n3; ++i)
+                v[i] = CLD{y[2 * n3 * b + 2 * i], y[2 * n3 * b + 2 * i + 1]};
+            lu.solve_inplace(v.data());
+            for (int64_t i = 0; i < n3; ++i) {
+                x[2 * n3 * b + 2 * i] = static_cast<double>(v[i].real());
+                x[2 * n3 * b + 2 * i + 1] = static_cast<double>(v[i].imag());
+            }
+        }
+    })
+}
+
+// 1-norm condition estimate of D_n (condition_estimate_1norm, :121-124).
+int oracle_condition_estimate(int n, double r, double s, double t, double* out) {
+    ORACLE_TRY({
+        const int64_t n3 = static_cast<int64_t>(n) * n * n;
+        auto m = dense_matrix<Complex, double>(n, Params{r, s, t});
+        DenseLU<Complex> lu(m.data(), n3);
+        *out = condition_with_lu(m.data(), n3, lu);
+    })
+}
+
+int oracle_condition_estimate_matrix(int64_t dim, const double* a, double* out) {
+    ORACLE_TRY({
+        const Complex* c = reinterpret_cast<const Complex*>(a);
+        DenseLU<Complex> lu(c, dim);
+        *out = condition_with_lu(c, dim, lu);
+    })
+}
+
+int oracle_radix_permutation(int n, uint64_t* out) {
+    ORACLE_TRY({
+        auto p = radix_permutation(n);
+        std::copy(p.begin(), p.end(), out);
+    })
+}
+
+// Seeded inputs exactly as tests/unit/test_transform.cpp:14-21 (libstdc++
+// mt19937 + uniform_real_distribution(-1,1), real then imaginary).
+int oracle_random_signal(int n, unsigned seed, double* out) {
+    std::mt19937 rng(seed);
+    std::uniform_real_distribution<double> unit(-1.0, 1.0);
+    const int64_t n3 = static_cast<int64_t>(n) * n * n;
+    for (int64_t i = 0; i < n3; ++i) {
+        out[2 * i] = unit(rng);
+        out[2 * i + 1] = unit(rng);
+    }
+    return OK;
+}
+
+// --- reference-faithful fast plan (handle API) ---------------------------
+void* oracle_plan_build(int n, double r, double s, double t, int* status) {
+    try {
+        auto* h = new std::shared_ptr<const Plan>(make_plan(n, Params{r, s, t}));
+        *status = OK;
+        return h;
+    } catch (const OracleError& e) {
+        g_last_error = e.what();
+        *status = e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        *status = INVALID_ARGUMENT;
+    }
+    return nullptr;
+}
+
+void oracle_plan_free(void* h) { delete static_cast<std::shared_ptr<const Plan>*>(h); }
+
+int oracle_plan_kind(void* h) { return (*static_cast<std::shared_ptr<const Plan>*>(h))->radix ? 1 : 0; }
+
+int64_t oracle_plan_basis_nnz(void* h) {
+    const auto& p = *static_cast<std::shared_ptr<const Plan>*>(h);
+    return p->radix ? p->basis.nnz() : 0;
+}
+
+// CSC export of the root basis: colptr[N+1], rowidx[nnz], val[2*nnz].
+int oracle_plan_basis(void* h, int64_t* colptr, int32_t* rowidx, double* val) {
+    const auto& p = *static_cast<std::shared_ptr<const Plan>*>(h);
+    if (!p->radix) return INVALID_ARGUMENT;
+    std::copy(p->basis.colptr.begin(), p->basis.colptr.end(), colptr);
+    std::copy(p->basis.rowidx.begin(), p->basis.rowidx.end(), rowidx);
+    std::memcpy(val, p->basis.val.data(), sizeof(Complex) * p->basis.nnz());
+    return OK;
+}
+
+// Sum of nnz over every radix node of the tree; with_b2 counts B_2 = I.
+int64_t oracle_plan_tree_nnz(void* h, int with_b2) {
+    std::function<int64_t(const Plan&)> rec = [&](const Plan& p) -> int64_t {
+        if (!p.radix) return 0;
+        int64_t s = (p.n == 2 && !with_b2) ? 0 : p.basis.nnz();
+        for (const auto& c : p.children) s += rec(*c);
+        return s;
+    };
+    return rec(**static_cast<std::shared_ptr<const Plan>*>(h));
+}
+
+int oracle_plan_apply(void* h, int64_t batch, const double* x, double* y) {
+    ORACLE_TRY({
+        const auto& p = *static_cast<std::shared_ptr<const Plan>*>(h);
+        const int64_t n3 = static_cast<int64_t>(p->n) * p->n * p->n;
+        std::vector<Complex> in(n3);
+        for (int64_t b = 0; b < batch; ++b) {
+            std::memcpy(static_cast<void*>(in.data()), x + 2 * n3 * b, sizeof(Complex) * n3);
+            auto out = p->apply_values(in);
+            std::memcpy(y + 2 * n3 * b, out.data(), sizeof(Complex) * n3);
+        }
+    })
+}
+
+int oracle_plan_solve(void* h, int64_t batch, const double* q, double* x) {
+    ORACLE_TRY({
+        const auto& p = *static_cast<std::shared_ptr<const Plan>*>(h);
+        const int64_t n3 = static_cast<int64_t>(p->n) * p->n * p->n;
+        std::vector<Complex> in(n3);
+        for (int64_t b = 0; b < batch; ++b) {
+            std::memcpy(static_cast<void*>(in.data()), q + 2 * n3 * b, sizeof(Complex) * n3);
+            auto out = p->solve_values(in);
+            std::memcpy(x + 2 * n3 * b, out.data(), sizeof(Complex) * n3);
+        }
+    })
+}
+
+// factorization_residual, src/transform.cpp:526-540 (max over unit columns).
+int oracle_plan_factorization_residual(void* h, double* out) {
+    ORACLE_TRY({
+        const auto& p = *static_cast<std::shared_ptr<const Plan>*>(h);
+        const int64_t n3 = static_cast<int64_t>(p->n) * p->n * p->n;
+        auto dense = dense_matrix<Complex, double>(p->n, p->p);
+        double worst = 0.0;
+        std::vector<Complex> e(n3, Complex{0, 0});
+        for (int64_t col = 0; col < n3; ++col) {
+            e[col] = 1.0;
+            auto lhs = p->apply_values(e);
+            for (int64_t i = 0; i < n3; ++i)
+                worst = std::max(worst, std::abs(lhs[i] - dense[i + col * n3]));
+            e[col] = 0.0;
+        }
+        *out = worst;
+    })
+}
+
+}  // extern "C"

@@ -1,0 +1,740 @@
+// C ABI of the B200 FCC-DCT (include/fcct_gpu.h). Host side: plan
+// construction (plan.cpp), stage-table compilation for the fast pipeline,
+// device uploads and kernel launches (kernels.cu). No exception crosses the
+// ABI; failures map to fcct_status codes with a thread-local message.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/fcct_gpu.h"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+namespace fcct {
+
+const int* host_group_table() {
+    static int table[24 * 9];
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const auto& g = s4_group();
+        for (int e = 0; e < 24; ++e)
+            for (int k = 0; k < 9; ++k) table[e * 9 + k] = g[e][k];
+    });
+    return table;
+}
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError : FcctError {
+    explicit CudaError(const std::string& what, cudaError_t e)
+        : FcctError(ST_CUDA, what + ": " + cudaGetErrorString(e)) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(what, e);
+}
+
+class DeviceGuard {
+public:
+    explicit DeviceGuard(int dev) {
+        ck(cudaGetDevice(&prev_), "cudaGetDevice");
+        if (prev_ != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() { cudaSetDevice(prev_); }
+
+private:
+    int prev_ = 0;
+};
+
+// Device allocation owned by a plan.
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t b) : bytes(b) { ck(cudaMalloc(&ptr, std::max<size_t>(b, 16)), "cudaMalloc"); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (ptr) cudaFree(ptr);
+    }
+};
+
+template <typename T>
+std::shared_ptr<DevBuf> upload(const std::vector<T>& v) {
+    auto b = std::make_shared<DevBuf>(v.size() * sizeof(T));
+    if (!v.empty()) ck(cudaMemcpy(b->ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    return b;
+}
+
+// Row list of a sparse stage operator on the full n^3 vector.
+struct Rows {
+    int64_t N = 0;
+    std::vector<std::vector<std::pair<int32_t, cld>>> r;
+};
+
+template <typename R>
+void push_coef(std::vector<R>& out, const cld& v) {
+    out.push_back(static_cast<R>(v.real()));
+    out.push_back(static_cast<R>(v.imag()));
+}
+
+struct PipelineTables {
+    PipelineDesc desc{};
+    std::vector<std::shared_ptr<DevBuf>> bufs;
+};
+
+// ELL packing of a sparse stage for row groups of RG rows.
+template <typename R>
+void add_sparse_stage(PipelineTables& pt, const Rows& rows, int RG, const std::vector<int32_t>* gather,
+                      const std::vector<int32_t>* scatter) {
+    const int64_t N = rows.N;
+    std::vector<int32_t> order(N);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return rows.r[a].size() > rows.r[b].size(); });
+    const int64_t ngroups = (N + RG - 1) / RG;
+    std::vector<int2> ginfo(ngroups);
+    std::vector<int32_t> grow(ngroups * RG, -1), ecol;
+    std::vector<R> ecoef;
+    for (int64_t g = 0; g < ngroups; ++g) {
+        int kmax = 0;
+        for (int rr = 0; rr < RG; ++rr) {
+            const int64_t idx = g * RG + rr;
+            if (idx < N) kmax = std::max<int>(kmax, static_cast<int>(rows.r[order[idx]].size()));
+        }
+        ginfo[g] = make_int2(static_cast<int>(ecol.size()), kmax);
+        for (int k = 0; k < kmax; ++k)
+            for (int rr = 0; rr < RG; ++rr) {
+                const int64_t idx = g * RG + rr;
+                if (idx < N && k < static_cast<int>(rows.r[order[idx]].size())) {
+                    const auto& e = rows.r[order[idx]][k];
+                    ecol.push_back(gather ? (*gather)[e.first] : e.first);
+                    push_coef(ecoef, e.second);
+                } else {
+                    ecol.push_back(0);
+                    push_coef(ecoef, cld{0, 0});
+                }
+            }
+        for (int rr = 0; rr < RG; ++rr) {
+            const int64_t idx = g * RG + rr;
+            if (idx < N) grow[g * RG + rr] = scatter ? (*scatter)[order[idx]] : order[idx];
+        }
+    }
+    auto b_ginfo = upload(ginfo), b_grow = upload(grow), b_ecol = upload(ecol), b_ecoef = upload(ecoef);
+    StageDesc& sd = pt.desc.stage[pt.desc.nstages++];
+    sd = StageDesc{};
+    sd.kind = 0;
+    sd.ngroups = static_cast<int>(ngroups);
+    sd.ginfo = static_cast<const int2*>(b_ginfo->ptr);
+    sd.grow = static_cast<const int*>(b_grow->ptr);
+    sd.ecol = static_cast<const int*>(b_ecol->ptr);
+    sd.ecoef = b_ecoef->ptr;
+    pt.bufs.insert(pt.bufs.end(), {b_ginfo, b_grow, b_ecol, b_ecoef});
+}
+
+template <typename R>
+void add_mix_stage(PipelineTables& pt, const std::vector<const PlanNode*>& nodes, bool inverse,
+                   const std::vector<int32_t>* gather, const std::vector<int32_t>* scatter) {
+    std::vector<R> K;
+    for (const PlanNode* nd : nodes)
+        for (int i = 0; i < 64; ++i) push_coef(K, inverse ? nd->Kinv[i] : nd->K[i]);
+    auto bK = upload(K);
+    StageDesc& sd = pt.desc.stage[pt.desc.nstages++];
+    sd = StageDesc{};
+    sd.kind = 1;
+    sd.nodes = static_cast<int>(nodes.size());
+    sd.m3 = static_cast<int>(cube(nodes[0]->n / 2));
+    sd.K = bK->ptr;
+    pt.bufs.push_back(bK);
+    if (gather) {
+        auto b = upload(*gather);
+        sd.gather = static_cast<const int*>(b->ptr);
+        pt.bufs.push_back(b);
+    }
+    if (scatter) {
+        auto b = upload(*scatter);
+        sd.scatter = static_cast<const int*>(b->ptr);
+        pt.bufs.push_back(b);
+    }
+}
+
+// Block-diagonal sparse operator over the nodes of one level.
+Rows level_rows(const std::vector<const PlanNode*>& nodes, int kind /*0 B, 1 Binv, 2 D, 3 Dinv*/) {
+    Rows rows;
+    const int64_t s3 = cube(nodes[0]->n);
+    rows.N = s3 * static_cast<int64_t>(nodes.size());
+    rows.r.resize(rows.N);
+    for (size_t q = 0; q < nodes.size(); ++q) {
+        const PlanNode& nd = *nodes[q];
+        const int64_t off = static_cast<int64_t>(q) * s3;
+        if (kind <= 1) {
+            const SparseLD& S = kind == 0 ? nd.B : nd.Binv;
+            for (int64_t r = 0; r < s3; ++r)
+                for (int64_t k = S.rowptr[r]; k < S.rowptr[r + 1]; ++k)
+                    rows.r[off + r].emplace_back(static_cast<int32_t>(off + S.col[k]), S.val[k]);
+        } else {
+            const auto& M = kind == 2 ? nd.D : nd.Dinv;
+            for (int64_t r = 0; r < s3; ++r)
+                for (int64_t c = 0; c < s3; ++c)
+                    rows.r[off + r].emplace_back(static_cast<int32_t>(off + c), M[r * s3 + c]);
+        }
+    }
+    return rows;
+}
+
+std::vector<int32_t> composite_order(const PlanNode& nd) {
+    // Z_s(i) = perm_s[blk*m^3 + Z_m(j)] for radix nodes, identity for direct.
+    const int64_t s3 = cube(nd.n);
+    std::vector<int32_t> z(s3);
+    if (!nd.radix) {
+        std::iota(z.begin(), z.end(), 0);
+        return z;
+    }
+    const auto sub = composite_order(*nd.children[0]);
+    const auto perm = radix_permutation(nd.n);
+    const int64_t m3 = s3 / 8;
+    for (int64_t i = 0; i < s3; ++i) z[i] = static_cast<int32_t>(perm[(i / m3) * m3 + sub[i % m3]]);
+    return z;
+}
+
+int choose_tb(int64_t N, bool f32) {
+    const int64_t row_bytes = (N + (f32 ? 2 : 1)) * (f32 ? 8 : 16);
+    for (int tb : {32, 16, 8, 4, 2, 1})
+        if (N * tb <= 8192 && 128 + tb * row_bytes <= 227 * 1024) return tb;
+    return 0;
+}
+
+template <typename R>
+void build_pipelines(const PlanNode& root, int tb, PipelineTables& fwd, PipelineTables& inv) {
+    const int RG = 32 / tb;
+    std::vector<std::vector<const PlanNode*>> levels;
+    std::vector<const PlanNode*> cur{&root};
+    while (!cur.empty() && cur[0]->radix) {
+        levels.push_back(cur);
+        std::vector<const PlanNode*> next;
+        for (const PlanNode* nd : cur)
+            for (const auto& c : nd->children) next.push_back(c.get());
+        cur = next;
+    }
+    const std::vector<const PlanNode*> leaves = cur;  // direct nodes
+    const bool dense_leaves = leaves[0]->n > 1;
+    const auto Z = composite_order(root);
+    for (auto* pt : {&fwd, &inv}) {
+        pt->desc.n = root.n;
+        pt->desc.N = static_cast<int>(cube(root.n));
+        pt->desc.tb = tb;
+        pt->desc.nstages = 0;
+    }
+    // forward: for each level B (size > 2) then K-mix; dense leaves last.
+    const int nfwd = [&] {
+        int c = 0;
+        for (auto& lv : levels) c += (lv[0]->n > 2 ? 2 : 1);
+        return c + (dense_leaves ? 1 : 0);
+    }();
+    int s = 0;
+    for (auto& lv : levels) {
+        if (lv[0]->n > 2) {
+            add_sparse_stage<R>(fwd, level_rows(lv, 0), RG, nullptr, (++s == nfwd) ? &Z : nullptr);
+        }
+        add_mix_stage<R>(fwd, lv, false, nullptr, (++s == nfwd) ? &Z : nullptr);
+    }
+    if (dense_leaves) add_sparse_stage<R>(fwd, level_rows(leaves, 2), RG, nullptr, &Z);
+    // inverse: dense leaves first, then per level (deepest first) K^{-1} mix then B^{-1}.
+    bool first = true;
+    if (dense_leaves) {
+        add_sparse_stage<R>(inv, level_rows(leaves, 3), RG, &Z, nullptr);
+        first = false;
+    }
+    for (auto it = levels.rbegin(); it != levels.rend(); ++it) {
+        add_mix_stage<R>(inv, *it, true, first ? &Z : nullptr, nullptr);
+        first = false;
+        if ((*it)[0]->n > 2) add_sparse_stage<R>(inv, level_rows(*it, 1), RG, nullptr, nullptr);
+    }
+}
+
+}  // namespace
+}  // namespace fcct
+
+using namespace fcct;
+
+struct fcct_plan_s {
+    int n = 0;
+    Params p;
+    int method = FCCT_FAST;
+    int precision = FCCT_F64;
+    int device = 0;
+    int num_sms = 148;
+    bool radix = false;
+    std::shared_ptr<const PlanNode> tree;
+    PipelineTables fwd, inv;
+    std::shared_ptr<DevBuf> Wt_fwd, Wt_inv;
+    std::vector<std::shared_ptr<DevBuf>> extra;
+    fcct_plan_info_t info{};
+    // workspace for host-buffer calls and in-place direct calls
+    std::mutex ws_mu;
+    std::shared_ptr<DevBuf> ws_in, ws_out;
+};
+
+namespace {
+
+int64_t elem_bytes(const fcct_plan_s* p) { return p->precision == FCCT_F32 ? 8 : 16; }
+
+void build_direct(fcct_plan_s* pl) {
+    const int n = pl->n;
+    const int64_t N = cube(n);
+    const bool f32 = pl->precision == FCCT_F32;
+    const size_t wbytes = static_cast<size_t>(2 * N) * (2 * N) * (f32 ? 4 : 8);
+    pl->Wt_fwd = std::make_shared<DevBuf>(wbytes);
+    pl->Wt_inv = std::make_shared<DevBuf>(wbytes);
+    ck(gen_dense_realform(n, pl->p.r, pl->p.s, pl->p.t, pl->Wt_fwd->ptr, f32, nullptr), "gen_dense_realform");
+    // orbit blocks of S_n(p)^{-1} -> device, then D^{-1} generated on the device
+    OrbitBlocks ob = orbit_blocks(n, pl->p);
+    if (!(ob.worst_condition <= 1e12))
+        throw FcctError(ST_ILL_CONDITIONED, "dense transform: orbit block condition exceeds 1e12");
+    const Orbits& orb = *ob.orb;
+    std::vector<int32_t> mem_off{0}, mem, sinv_off;
+    std::vector<double> sinv;
+    for (size_t o = 0; o < orb.members.size(); ++o) {
+        sinv_off.push_back(static_cast<int32_t>(sinv.size() / 2));
+        for (int32_t a : orb.members[o]) mem.push_back(a);
+        mem_off.push_back(static_cast<int32_t>(mem.size()));
+        for (const cld& v : ob.Sinv[o]) {
+            sinv.push_back(static_cast<double>(v.real()));
+            sinv.push_back(static_cast<double>(v.imag()));
+        }
+    }
+    auto b1 = upload(orb.orbit_of), b2 = upload(orb.pos), b3 = upload(mem_off), b4 = upload(mem),
+         b5 = upload(sinv_off), b6 = upload(sinv);
+    OrbitDev od{static_cast<const int*>(b1->ptr), static_cast<const int*>(b2->ptr),
+                static_cast<const int*>(b3->ptr), static_cast<const int*>(b4->ptr),
+                static_cast<const int*>(b5->ptr), static_cast<const double*>(b6->ptr)};
+    ck(gen_dense_inv_realform(n, od, pl->Wt_inv->ptr, f32, nullptr), "gen_dense_inv_realform");
+    ck(cudaDeviceSynchronize(), "direct table generation");
+    // exact 1-norm condition: ||D||_1 ||D^{-1}||_1 from the orbit structure is
+    // what the reference gates on (transform.cpp:329-345); estimate it on the host
+    // from the blocks: ||D||_1 <= N max|col| ... use the blocks' worst condition.
+    pl->info.condition = ob.worst_condition;
+    pl->info.table_bytes = static_cast<int64_t>(2 * wbytes);
+}
+
+void fill_info(fcct_plan_s* pl) {
+    fcct_plan_info_t& in = pl->info;
+    in.n = pl->n;
+    in.r = pl->p.r;
+    in.s = pl->p.s;
+    in.t = pl->p.t;
+    in.kind = pl->radix ? FCCT_KIND_RADIX2 : FCCT_KIND_DIRECT;
+    in.method = pl->radix ? FCCT_FAST : FCCT_DIRECT;
+    in.precision = pl->precision;
+    in.points = cube(pl->n);
+    const double N = static_cast<double>(in.points);
+    if (pl->radix) {
+        in.levels = tree_levels(pl->n);
+        in.tree_nnz = tree_nnz(*pl->tree, false, false);
+        in.tree_nnz_inv = tree_nnz(*pl->tree, true, false);
+        in.root_nnz = pl->tree->B.nnz();
+        in.flops_forward = algorithmic_flops(*pl->tree, false);
+        in.flops_inverse = algorithmic_flops(*pl->tree, true);
+        in.condition = pl->tree->condition;
+        int64_t bytes = 0;
+        for (auto* pt : {&pl->fwd, &pl->inv})
+            for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+        in.table_bytes = bytes;
+    } else {
+        in.levels = 0;
+        in.flops_forward = in.flops_inverse = 8.0 * N * N;
+    }
+}
+
+fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int device) {
+    if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "build_plan: n must be >= 1");
+    if (method != FCCT_DIRECT && method != FCCT_FAST) throw FcctError(ST_INVALID_ARGUMENT, "unknown method");
+    if (precision != FCCT_F64 && precision != FCCT_F32) throw FcctError(ST_INVALID_ARGUMENT, "unknown precision");
+    if (!std::isfinite(p.r) || !std::isfinite(p.s) || !std::isfinite(p.t))
+        throw FcctError(ST_INVALID_ARGUMENT, "grid offsets must be finite");
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) throw FcctError(ST_INVALID_ARGUMENT, "no such CUDA device");
+    DeviceGuard guard(device);
+    auto pl = std::make_unique<fcct_plan_s>();
+    pl->n = n;
+    pl->p = p;
+    pl->precision = precision;
+    pl->device = device;
+    ck(cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+    const bool f32 = precision == FCCT_F32;
+    const bool radix = method == FCCT_FAST && n % 2 == 0;
+    if (radix) {
+        pl->tree = build_tree(n, p);  // degeneracy + condition gates inside
+        const int tb = choose_tb(cube(n), f32);
+        if (tb == 0) throw FcctError(ST_INVALID_ARGUMENT, "fast pipeline: n too large for one CTA tile");
+        if (f32)
+            build_pipelines<float>(*pl->tree, tb, pl->fwd, pl->inv);
+        else
+            build_pipelines<double>(*pl->tree, tb, pl->fwd, pl->inv);
+        pl->radix = true;
+    } else {
+        check_nodes(n, p);
+        pl->radix = false;
+        build_direct(pl.get());
+    }
+    pl->method = pl->radix ? FCCT_FAST : FCCT_DIRECT;
+    fill_info(pl.get());
+    return pl.release();
+}
+
+void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st) {
+    if (batch < 0) throw FcctError(ST_SIZE_MISMATCH, "batch must be >= 0");
+    if (batch == 0) return;
+    if (!in || !out) throw FcctError(ST_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard guard(pl->device);
+    const bool f32 = pl->precision == FCCT_F32;
+    if (pl->radix) {
+        ck(launch_pipeline(inverse ? pl->inv.desc : pl->fwd.desc, f32, in, out, batch, st, pl->num_sms),
+           "fast pipeline");
+        return;
+    }
+    const int64_t N = cube(pl->n);
+    const void* W = inverse ? pl->Wt_inv->ptr : pl->Wt_fwd->ptr;
+    void* dst = out;
+    std::shared_ptr<DevBuf> tmp;
+    if (in == out) {
+        tmp = std::make_shared<DevBuf>(static_cast<size_t>(batch * N * elem_bytes(pl)));
+        dst = tmp->ptr;
+    }
+    if (f32)
+        ck(launch_gemm_f32(static_cast<const float*>(in), static_cast<const float*>(W), static_cast<float*>(dst),
+                           batch, static_cast<int>(2 * N), static_cast<int>(2 * N), st),
+           "direct gemm f32");
+    else
+        ck(launch_gemm_f64(static_cast<const double*>(in), static_cast<const double*>(W), static_cast<double*>(dst),
+                           batch, static_cast<int>(2 * N), static_cast<int>(2 * N), st),
+           "direct gemm f64");
+    if (tmp) {
+        ck(cudaMemcpyAsync(out, tmp->ptr, static_cast<size_t>(batch * N * elem_bytes(pl)), cudaMemcpyDeviceToDevice, st),
+           "copy back");
+        ck(cudaStreamSynchronize(st), "sync");
+    }
+}
+
+void run_host(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st) {
+    if (batch < 0) throw FcctError(ST_SIZE_MISMATCH, "batch must be >= 0");
+    if (batch == 0) return;
+    if (!in || !out) throw FcctError(ST_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard guard(pl->device);
+    const size_t bytes = static_cast<size_t>(batch * cube(pl->n) * elem_bytes(pl));
+    std::lock_guard<std::mutex> lock(pl->ws_mu);
+    if (!pl->ws_in || pl->ws_in->bytes < bytes) {
+        pl->ws_in = std::make_shared<DevBuf>(bytes);
+        pl->ws_out = std::make_shared<DevBuf>(bytes);
+    }
+    ck(cudaMemcpyAsync(pl->ws_in->ptr, in, bytes, cudaMemcpyHostToDevice, st), "H2D");
+    run(pl, inverse, pl->ws_in->ptr, pl->ws_out->ptr, batch, st);
+    ck(cudaMemcpyAsync(out, pl->ws_out->ptr, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+}
+
+template <typename F>
+fcct_status guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return FCCT_OK;
+    } catch (const FcctError& e) {
+        g_last_error = e.what();
+        return static_cast<fcct_status>(e.code);
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return FCCT_INVALID_ARGUMENT;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fcct_last_error(void) { return g_last_error.c_str(); }
+
+fcct_status fcct_plan_create(int n, double r, double s, double t, int method, int precision, int device,
+                             fcct_plan* out) {
+    return guarded([&] {
+        if (!out) throw FcctError(ST_INVALID_ARGUMENT, "null plan pointer");
+        *out = create_plan(n, Params{r, s, t}, method, precision, device);
+    });
+}
+
+fcct_status fcct_plan_destroy(fcct_plan plan) {
+    return guarded([&] {
+        if (!plan) return;
+        DeviceGuard guard(plan->device);
+        cudaDeviceSynchronize();
+        delete plan;
+    });
+}
+
+fcct_status fcct_plan_info(fcct_plan plan, fcct_plan_info_t* info) {
+    return guarded([&] {
+        if (!plan || !info) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        *info = plan->info;
+    });
+}
+
+fcct_status fcct_forward(fcct_plan plan, const void* in, void* out, int64_t batch, void* stream) {
+    return guarded([&] {
+        if (!plan) throw FcctError(ST_INVALID_ARGUMENT, "null plan");
+        run(plan, false, in, out, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+fcct_status fcct_inverse(fcct_plan plan, const void* in, void* out, int64_t batch, void* stream) {
+    return guarded([&] {
+        if (!plan) throw FcctError(ST_INVALID_ARGUMENT, "null plan");
+        run(plan, true, in, out, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+fcct_status fcct_inverse_checked(fcct_plan plan, double r, double s, double t, const void* in, void* out,
+                                 int64_t batch, void* stream) {
+    return guarded([&] {
+        if (!plan) throw FcctError(ST_INVALID_ARGUMENT, "null plan");
+        if (!(Params{r, s, t} == plan->p))
+            throw FcctError(ST_PARAMS_MISMATCH, "inverse_apply: spectrum was produced on a different skew grid");
+        run(plan, true, in, out, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+fcct_status fcct_forward_host(fcct_plan plan, const void* in, void* out, int64_t batch, void* stream) {
+    return guarded([&] {
+        if (!plan) throw FcctError(ST_INVALID_ARGUMENT, "null plan");
+        run_host(plan, false, in, out, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+fcct_status fcct_inverse_host(fcct_plan plan, const void* in, void* out, int64_t batch, void* stream) {
+    return guarded([&] {
+        if (!plan) throw FcctError(ST_INVALID_ARGUMENT, "null plan");
+        run_host(plan, true, in, out, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+fcct_status fcct_radix_permutation(int n, uint64_t* out_host) {
+    return guarded([&] {
+        if (n < 2) throw FcctError(ST_INVALID_ARGUMENT, "radix_permutation: n must be >= 2");
+        if (n % 2 != 0) throw FcctError(ST_ODD_SIZE, "radix_permutation: size " + std::to_string(n) + " is odd");
+        if (!out_host) throw FcctError(ST_INVALID_ARGUMENT, "null output");
+        const int64_t N = cube(n);
+        DevBuf d(static_cast<size_t>(N) * 8);
+        ck(gen_radix_permutation(n, static_cast<unsigned long long*>(d.ptr), nullptr), "radix permutation");
+        ck(cudaMemcpy(out_host, d.ptr, static_cast<size_t>(N) * 8, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+fcct_status fcct_dense_matrix(int n, double r, double s, double t, void* out_device, void* stream) {
+    return guarded([&] {
+        if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "dense_transform: n must be >= 1");
+        if (!out_device) throw FcctError(ST_INVALID_ARGUMENT, "null output");
+        check_nodes(n, Params{r, s, t});  // transform.cpp:132
+        ck(gen_dense_colmajor(n, r, s, t, static_cast<double*>(out_device), static_cast<cudaStream_t>(stream)),
+           "dense matrix");
+    });
+}
+
+fcct_status fcct_skew_nodes(int n, double r, double s, double t, void* out_device, void* stream) {
+    return guarded([&] {
+        if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "skew_nodes: n must be >= 1");
+        if (!out_device) throw FcctError(ST_INVALID_ARGUMENT, "null output");
+        DevBuf flag(sizeof(int));
+        ck(cudaMemset(flag.ptr, 0, sizeof(int)), "memset");
+        auto st = static_cast<cudaStream_t>(stream);
+        ck(gen_nodes(n, r, s, t, static_cast<double*>(out_device), static_cast<int*>(flag.ptr), st), "nodes");
+        int h = 0;
+        ck(cudaMemcpyAsync(&h, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+        if (h) throw FcctError(ST_DEGENERATE_NODES, "two nodes map to the same spectral point for n=" + std::to_string(n));
+    });
+}
+
+fcct_status fcct_plan_kernel(fcct_plan plan, double* out128) {
+    return guarded([&] {
+        if (!plan || !out128) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        if (!plan->radix) throw FcctError(ST_INVALID_ARGUMENT, "kernel(): plan is direct");
+        for (int blk = 0; blk < 8; ++blk)
+            for (int g = 0; g < 8; ++g) {
+                const cld v = plan->tree->K[blk * 8 + g];
+                out128[2 * (g * 8 + blk)] = static_cast<double>(v.real());
+                out128[2 * (g * 8 + blk) + 1] = static_cast<double>(v.imag());
+            }
+    });
+}
+
+fcct_status fcct_plan_basis(fcct_plan plan, int64_t* nnz, int64_t* colptr, int32_t* rowidx, double* values) {
+    return guarded([&] {
+        if (!plan || !nnz) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        if (!plan->radix) throw FcctError(ST_INVALID_ARGUMENT, "basis(): plan is direct");
+        const SparseLD& B = plan->tree->B;
+        *nnz = B.nnz();
+        if (!colptr || !rowidx || !values) return;
+        // CSR -> CSC (Eigen's compressed column storage, rows sorted per column)
+        const int64_t N = B.dim;
+        std::vector<int64_t> cnt(N + 1, 0);
+        for (int32_t c : B.col) cnt[c + 1]++;
+        for (int64_t c = 0; c < N; ++c) cnt[c + 1] += cnt[c];
+        std::copy(cnt.begin(), cnt.end(), colptr);
+        std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+        for (int64_t r = 0; r < N; ++r)
+            for (int64_t k = B.rowptr[r]; k < B.rowptr[r + 1]; ++k) {
+                const int64_t dst = fill[B.col[k]]++;
+                rowidx[dst] = static_cast<int32_t>(r);
+                values[2 * dst] = static_cast<double>(B.val[k].real());
+                values[2 * dst + 1] = static_cast<double>(B.val[k].imag());
+            }
+    });
+}
+
+fcct_status fcct_plan_child(fcct_plan plan, int index, int* n, double* r, double* s, double* t, int* kind) {
+    return guarded([&] {
+        if (!plan) throw FcctError(ST_INVALID_ARGUMENT, "null plan");
+        if (!plan->radix) throw FcctError(ST_INVALID_ARGUMENT, "children(): plan is direct");
+        if (index < 0 || index >= 8) throw FcctError(ST_INVALID_ARGUMENT, "child index out of range");
+        const PlanNode& c = *plan->tree->children[index];
+        if (n) *n = c.n;
+        if (r) *r = c.p.r;
+        if (s) *s = c.p.s;
+        if (t) *t = c.p.t;
+        if (kind) *kind = c.radix ? FCCT_KIND_RADIX2 : FCCT_KIND_DIRECT;
+    });
+}
+
+fcct_status fcct_factorization_residual(fcct_plan plan, double* out) {
+    return guarded([&] {
+        if (!plan || !out) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        if (plan->precision != FCCT_F64) throw FcctError(ST_INVALID_ARGUMENT, "residual needs an fp64 plan");
+        DeviceGuard guard(plan->device);
+        const int64_t N = cube(plan->n);
+        DevBuf E(static_cast<size_t>(N * N) * 16), Y(static_cast<size_t>(N * N) * 16), D(static_cast<size_t>(N * N) * 16);
+        ck(gen_identity(static_cast<int>(N), E.ptr, false, nullptr), "identity");
+        run(plan, false, E.ptr, Y.ptr, N, nullptr);
+        ck(gen_dense_colmajor(plan->n, plan->p.r, plan->p.s, plan->p.t, static_cast<double*>(D.ptr), nullptr), "dense");
+        const int nb = 512;
+        DevBuf part(nb * sizeof(double));
+        ck(residual_max(static_cast<const double*>(Y.ptr), static_cast<const double*>(D.ptr), static_cast<int>(N),
+                        static_cast<double*>(part.ptr), nb, nullptr),
+           "residual");
+        std::vector<double> h(nb);
+        ck(cudaMemcpy(h.data(), part.ptr, nb * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        *out = *std::max_element(h.begin(), h.end());
+    });
+}
+
+fcct_status fcct_plan_perturbed_basis(fcct_plan plan, double delta, fcct_plan* out) {
+    return guarded([&] {
+        if (!plan || !out) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        if (!plan->radix) throw FcctError(ST_INVALID_ARGUMENT, "with_perturbed_basis: plan has no basis factor");
+        if (plan->tree->B.nnz() == 0) throw FcctError(ST_INVALID_ARGUMENT, "with_perturbed_basis: basis is empty");
+        DeviceGuard guard(plan->device);
+        auto root = std::make_shared<PlanNode>(*plan->tree);  // children shared
+        // valuePtr()[0] of the CSC basis: column 0, smallest row (transform.cpp:550)
+        int64_t best = -1;
+        int32_t best_row = INT32_MAX;
+        for (int64_t r = 0; r < root->B.dim && best < 0; ++r)
+            for (int64_t k = root->B.rowptr[r]; k < root->B.rowptr[r + 1]; ++k)
+                if (root->B.col[k] == 0 && r < best_row) {
+                    best = k;
+                    best_row = static_cast<int32_t>(r);
+                    break;
+                }
+        if (best < 0) throw FcctError(ST_INVALID_ARGUMENT, "with_perturbed_basis: column 0 is empty");
+        root->B.val[best] += static_cast<long double>(delta);
+        auto pl = std::make_unique<fcct_plan_s>();
+        pl->n = plan->n;
+        pl->p = plan->p;
+        pl->precision = plan->precision;
+        pl->device = plan->device;
+        pl->num_sms = plan->num_sms;
+        pl->radix = true;
+        pl->tree = root;
+        const int tb = plan->fwd.desc.tb;
+        if (pl->precision == FCCT_F32)
+            build_pipelines<float>(*root, tb, pl->fwd, pl->inv);
+        else
+            build_pipelines<double>(*root, tb, pl->fwd, pl->inv);
+        pl->method = FCCT_FAST;
+        fill_info(pl.get());
+        *out = pl.release();
+    });
+}
+
+fcct_status fcct_shard_range(int64_t total, int rank, int world, int64_t* begin, int64_t* end) {
+    return guarded([&] {
+        if (total < 0 || world < 1 || rank < 0 || rank >= world || !begin || !end)
+            throw FcctError(ST_INVALID_ARGUMENT, "bad shard arguments");
+        const int64_t per = (total + world - 1) / world;
+        *begin = std::min<int64_t>(total, per * rank);
+        *end = std::min<int64_t>(total, per * (rank + 1));
+    });
+}
+
+fcct_status fcct_basis_change(int n, double r, double s, double t, int inverse, int64_t* nnz, int64_t* colptr,
+                              int32_t* rowidx, double* values) {
+    return guarded([&] {
+        if (!nnz) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        if (n < 2 || n % 2 != 0)
+            throw FcctError(ST_ODD_SIZE, "basis_change: needs an even size, got " + std::to_string(n));
+        static std::mutex mu;
+        static std::shared_ptr<const PlanNode> cached;
+        std::shared_ptr<const PlanNode> root;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            if (cached && cached->n == n && cached->p == Params{r, s, t}) root = cached;
+        }
+        if (!root) {
+            root = build_tree(n, Params{r, s, t});
+            std::lock_guard<std::mutex> lock(mu);
+            cached = root;
+        }
+        const SparseLD& B = inverse ? root->Binv : root->B;
+        *nnz = B.nnz();
+        if (!colptr || !rowidx || !values) return;
+        const int64_t N = B.dim;
+        std::vector<int64_t> cnt(N + 1, 0);
+        for (int32_t c : B.col) cnt[c + 1]++;
+        for (int64_t c = 0; c < N; ++c) cnt[c + 1] += cnt[c];
+        std::copy(cnt.begin(), cnt.end(), colptr);
+        std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+        for (int64_t row = 0; row < N; ++row)
+            for (int64_t k = B.rowptr[row]; k < B.rowptr[row + 1]; ++k) {
+                const int64_t dst = fill[B.col[k]]++;
+                rowidx[dst] = static_cast<int32_t>(row);
+                values[2 * dst] = static_cast<double>(B.val[k].real());
+                values[2 * dst + 1] = static_cast<double>(B.val[k].imag());
+            }
+    });
+}
+
+fcct_status fcct_plan_tree_stats(int n, double r, double s, double t, int64_t* tree_nnz_fwd, int64_t* tree_nnz_inv,
+                                 double* flops_fwd, double* flops_inv) {
+    return guarded([&] {
+        if (n < 2 || n % 2 != 0) throw FcctError(ST_ODD_SIZE, "tree stats: needs an even size");
+        auto root = build_tree(n, Params{r, s, t});
+        if (tree_nnz_fwd) *tree_nnz_fwd = tree_nnz(*root, false, false);
+        if (tree_nnz_inv) *tree_nnz_inv = tree_nnz(*root, true, false);
+        if (flops_fwd) *flops_fwd = algorithmic_flops(*root, false);
+        if (flops_inv) *flops_inv = algorithmic_flops(*root, true);
+    });
+}
+
+// Test hook: DMMA fragment-layout probe (device pointers).
+fcct_status fcct_debug_dmma_probe(const double* A, const double* B, double* C) {
+    return guarded([&] { ck(dmma_probe(A, B, C, nullptr), "dmma probe"); });
+}
+
+}  // extern "C"

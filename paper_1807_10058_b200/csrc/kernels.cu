@@ -1,0 +1,679 @@
+// sm_100a kernels of the B200 FCC-DCT (arXiv 1807.10058).
+//
+//  * fast pipeline  — the paper's radix-2x2x2 factorization applied stage by
+//                     stage to a tile of TB transform blocks resident in shared
+//                     memory (TMA bulk load/store, in-place two-phase stages);
+//  * direct GEMMs   — D x as a real-form GEMM on the FP64 tensor pipe (DMMA)
+//                     or FFMA for fp32;
+//  * table generation — D, D^{-1}, nodes and permutations built on the device.
+#include <algorithm>
+#include <cstdio>
+
+#include "device.cuh"
+#include "kernels.hpp"
+
+namespace fcct {
+
+using namespace dev;
+
+__constant__ int c_group[24 * 9];  // S4 in the reference's BFS order (weyl_s4.cpp:54-92)
+
+static cudaError_t upload_group() {
+    static bool done = false;
+    if (done) return cudaSuccess;
+    // BFS closure of the generators; identical to plan.cpp's s4_group (kept
+    // here as the device constant the generation kernels read).
+    extern const int* host_group_table();
+    cudaError_t e = cudaMemcpyToSymbol(c_group, host_group_table(), sizeof(int) * 24 * 9);
+    if (e == cudaSuccess) done = true;
+    return e;
+}
+
+// ===========================================================================
+// Fast pipeline
+// ===========================================================================
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kJ = 16;  // complex outputs a lane may hold per stage
+
+template <typename R, int TB>
+__device__ __forceinline__ void sparse_stage(const StageDesc& sd, C2<R>* data, int N1, int warp, int lane) {
+    constexpr int RG = 32 / TB;
+    const int rr = lane / TB, t = lane % TB;
+    C2<R>* row_t = data + t * N1;
+    const C2<R>* coef = static_cast<const C2<R>*>(sd.ecoef);
+    C2<R> acc[kJ];
+    int outpos[kJ];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+        const int g = warp + j * kWarps;
+        outpos[j] = -1;
+        acc[j].x = 0;
+        acc[j].y = 0;
+        if (g < sd.ngroups) {
+            const int2 gi = __ldg(sd.ginfo + g);
+            outpos[j] = __ldg(sd.grow + g * RG + rr);
+            C2<R> a;
+            a.x = 0;
+            a.y = 0;
+            for (int k = 0; k < gi.y; ++k) {
+                const int e = gi.x + k * RG + rr;
+                const int col = __ldg(sd.ecol + e);
+                const C2<R> c = coef[e];
+                cmac(a, c, row_t[col]);
+            }
+            acc[j] = a;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kJ; ++j)
+        if (outpos[j] >= 0) row_t[outpos[j]] = acc[j];
+    __syncthreads();
+}
+
+template <typename R, int TB>
+__device__ __forceinline__ void mix8_stage(const StageDesc& sd, C2<R>* data, int N1, int warp, int lane) {
+    constexpr int RG = 32 / TB;
+    constexpr int kItems = kJ / 8;
+    const int rr = lane / TB, t = lane % TB;
+    C2<R>* row_t = data + t * N1;
+    const C2<R>* Kall = static_cast<const C2<R>*>(sd.K);
+    const int items = sd.nodes * sd.m3;
+    C2<R> acc[kItems][8];
+    int base[kItems];
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        const int item = (warp * RG + rr) + j * (kWarps * RG);
+        base[j] = -1;
+        if (item < items) {
+            const int q = item / sd.m3, h = item - q * sd.m3;
+            base[j] = q * 8 * sd.m3 + h;
+            C2<R> x[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                int p = base[j] + g * sd.m3;
+                if (sd.gather) p = __ldg(sd.gather + p);
+                x[g] = row_t[p];
+            }
+            const C2<R>* Kq = Kall + q * 64;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                C2<R> a;
+                a.x = 0;
+                a.y = 0;
+#pragma unroll
+                for (int g = 0; g < 8; ++g) cmac(a, Kq[b * 8 + g], x[g]);
+                acc[j][b] = a;
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kItems; ++j)
+        if (base[j] >= 0) {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                int p = base[j] + b * sd.m3;
+                if (sd.scatter) p = __ldg(sd.scatter + p);
+                row_t[p] = acc[j][b];
+            }
+        }
+    __syncthreads();
+}
+
+template <typename R, int TB>
+__global__ void __launch_bounds__(kThreads, 1)
+    pipeline_kernel(const __grid_constant__ PipelineDesc d, const C2<R>* __restrict__ in, C2<R>* __restrict__ out,
+                    int64_t batch) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    C2<R>* data = reinterpret_cast<C2<R>*>(smem_raw + 128);
+    // row stride: one padding element (fp64) or two (fp32) keep every row
+    // 16-B aligned for the bulk copies and rotate the bank of consecutive rows
+    const int N = d.N, N1 = d.N + (sizeof(C2<R>) == 8 ? 2 : 1);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t ntiles = (batch + TB - 1) / TB;
+    const uint32_t row_bytes = static_cast<uint32_t>(N * sizeof(C2<R>));
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t t0 = tile * TB;
+        const int nvalid = static_cast<int>(batch - t0 < TB ? batch - t0 : TB);
+        if (threadIdx.x == 0) {
+            tma_store_wait_read0();  // previous tile's stores have read the buffer
+            mbar_arrive_expect_tx(bar, row_bytes * nvalid);
+            for (int t = 0; t < nvalid; ++t) tma_load_1d(data + t * N1, in + (t0 + t) * N, row_bytes, bar);
+            const int64_t nt = tile + gridDim.x;
+            if (nt < ntiles) {
+                const int64_t n0 = nt * TB;
+                const int nv = static_cast<int>(batch - n0 < TB ? batch - n0 : TB);
+                prefetch_l2_bulk(in + n0 * N, row_bytes * nv);
+            }
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        for (int s = 0; s < d.nstages; ++s) {
+            const StageDesc& sd = d.stage[s];
+            if (sd.kind == 0)
+                sparse_stage<R, TB>(sd, data, N1, warp, lane);
+            else
+                mix8_stage<R, TB>(sd, data, N1, warp, lane);
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int t = 0; t < nvalid; ++t) tma_store_1d(out + (t0 + t) * N, data + t * N1, row_bytes);
+            tma_store_commit();
+        }
+    }
+    if (threadIdx.x == 0) tma_store_wait0();
+}
+
+template <typename R, int TB>
+cudaError_t launch_pipeline_t(const PipelineDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st,
+                              int num_sms) {
+    const int smem = 128 + TB * (d.N + (sizeof(C2<R>) == 8 ? 2 : 1)) * static_cast<int>(sizeof(C2<R>));
+    auto kern = pipeline_kernel<R, TB>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int64_t ntiles = (batch + TB - 1) / TB;
+    const int64_t grid = std::min<int64_t>(ntiles, static_cast<int64_t>(per_sm) * num_sms);
+    kern<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(d, static_cast<const C2<R>*>(in),
+                                                               static_cast<C2<R>*>(out), batch);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int pipeline_smem_bytes(const PipelineDesc& d, bool f32) {
+    return 128 + d.tb * (d.N + (f32 ? 2 : 1)) * (f32 ? 8 : 16);
+}
+
+cudaError_t launch_pipeline(const PipelineDesc& d, bool f32, const void* in, void* out, int64_t batch,
+                            cudaStream_t st, int num_sms) {
+    if (batch <= 0) return cudaSuccess;
+#define FCCT_PIPE(TBV)                                                                   \
+    case TBV:                                                                            \
+        return f32 ? launch_pipeline_t<float, TBV>(d, in, out, batch, st, num_sms)       \
+                   : launch_pipeline_t<double, TBV>(d, in, out, batch, st, num_sms);
+    switch (d.tb) {
+        FCCT_PIPE(1)
+        FCCT_PIPE(2)
+        FCCT_PIPE(4)
+        FCCT_PIPE(8)
+        FCCT_PIPE(16)
+        FCCT_PIPE(32)
+        default:
+            return cudaErrorInvalidValue;
+    }
+#undef FCCT_PIPE
+}
+
+// ===========================================================================
+// Direct transform GEMMs (real form: C[M][Nn] = A[M][K] * Wt[Nn][K]^T)
+// ===========================================================================
+namespace {
+
+constexpr int GBM = 64, GBN = 128, GBK = 16, GLD = 20;  // GLD: padded row (doubles)
+
+__global__ void __launch_bounds__(256) gemm_f64_kernel(const double* __restrict__ A, const double* __restrict__ W,
+                                                       double* __restrict__ C, int64_t M, int Nn, int K) {
+    extern __shared__ __align__(16) double gsm[];
+    double* As = gsm;                    // [2][GBM][GLD]
+    double* Bs = gsm + 2 * GBM * GLD;    // [2][GBN][GLD]
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    const int wm = warp / 4, wn = warp % 4;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.y) * GBM;
+    const int n0 = blockIdx.x * GBN;
+    double c[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+
+    auto load_tile = [&](int buf, int k0) {
+        // A: 64 rows x 16 doubles = 512 chunks of 16B; 2 per thread
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int chunk = tid + q * 256;
+            const int r = chunk / 8, cc = chunk % 8;
+            const int64_t gr = m0 + r;
+            const int gk = k0 + cc * 2;
+            const bool ok = gr < M && gk < K;
+            cp_async16(As + (buf * GBM + r) * GLD + cc * 2, ok ? A + gr * K + gk : A, ok);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int chunk = tid + q * 256;
+            const int r = chunk / 8, cc = chunk % 8;
+            const int gn = n0 + r;
+            const int gk = k0 + cc * 2;
+            const bool ok = gn < Nn && gk < K;
+            cp_async16(Bs + (buf * GBN + r) * GLD + cc * 2, ok ? W + static_cast<int64_t>(gn) * K + gk : W, ok);
+        }
+        cp_async_commit();
+    };
+
+    const int ktiles = (K + GBK - 1) / GBK;
+    load_tile(0, 0);
+    for (int kt = 0; kt < ktiles; ++kt) {
+        const int buf = kt & 1;
+        if (kt + 1 < ktiles) {
+            load_tile(buf ^ 1, (kt + 1) * GBK);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* as = As + buf * GBM * GLD;
+        const double* bs = Bs + buf * GBN * GLD;
+#pragma unroll
+        for (int kk = 0; kk < GBK; kk += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = as[(wm * 32 + i * 8 + (lane >> 2)) * GLD + kk + (lane & 3)];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = bs[(wn * 32 + j * 8 + (lane >> 2)) * GLD + kk + (lane & 3)];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma884(c[i][j][0], c[i][j][1], a[i], b[j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t row = m0 + wm * 32 + i * 8 + (lane >> 2);
+            const int col = n0 + wn * 32 + j * 8 + 2 * (lane & 3);
+            if (row < M && col + 1 < Nn + 1) {
+                if (col + 1 < Nn) {
+                    *reinterpret_cast<double2*>(C + row * Nn + col) = make_double2(c[i][j][0], c[i][j][1]);
+                } else if (col < Nn) {
+                    C[row * Nn + col] = c[i][j][0];
+                }
+            }
+        }
+}
+
+// fp32: classic 128x128x8 SIMT tile, 8x8 outputs per thread.
+__global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A, const float* __restrict__ W,
+                                                       float* __restrict__ C, int64_t M, int Nn, int K) {
+    __shared__ __align__(16) float As[2][8][128 + 4];
+    __shared__ __align__(16) float Bs[2][8][128 + 4];
+    const int tid = threadIdx.x;
+    const int tx = tid % 16, ty = tid / 16;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.y) * 128;
+    const int n0 = blockIdx.x * 128;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    // each thread loads 4 A values and 4 B values per k-tile: row = tid/2, k = (tid%2)*4 .. +3
+    const int lr = tid / 2, lk = (tid % 2) * 4;
+    float ra[4], rb[4];
+    auto gload = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t gr = m0 + lr;
+            const int gk = k0 + lk + q;
+            ra[q] = (gr < M && gk < K) ? __ldg(A + gr * K + gk) : 0.f;
+            const int gn = n0 + lr;
+            rb[q] = (gn < Nn && gk < K) ? __ldg(W + static_cast<int64_t>(gn) * K + gk) : 0.f;
+        }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            As[buf][lk + q][lr] = ra[q];
+            Bs[buf][lk + q][lr] = rb[q];
+        }
+    };
+    const int ktiles = (K + 7) / 8;
+    gload(0);
+    sstore(0);
+    __syncthreads();
+    for (int kt = 0; kt < ktiles; ++kt) {
+        const int buf = kt & 1;
+        if (kt + 1 < ktiles) gload((kt + 1) * 8);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            float a[8], b[8];
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + ty * 4]);
+            const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
+            const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][64 + tx * 4]);
+            a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+            a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+            b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+            b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        if (kt + 1 < ktiles) sstore(buf ^ 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+        if (row >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int col = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+            if (col < Nn) C[row * Nn + col] = acc[i][j];
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_gemm_f64(const double* A, const double* Wt, double* C, int64_t M, int Nn, int K,
+                            cudaStream_t st) {
+    if (M <= 0) return cudaSuccess;
+    const int smem = 2 * (GBM + GBN) * GLD * static_cast<int>(sizeof(double));
+    cudaError_t e = cudaFuncSetAttribute(gemm_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((Nn + GBN - 1) / GBN, static_cast<unsigned>((M + GBM - 1) / GBM));
+    gemm_f64_kernel<<<grid, 256, smem, st>>>(A, Wt, C, M, Nn, K);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_f32(const float* A, const float* Wt, float* C, int64_t M, int Nn, int K,
+                            cudaStream_t st) {
+    if (M <= 0) return cudaSuccess;
+    dim3 grid((Nn + 127) / 128, static_cast<unsigned>((M + 127) / 128));
+    gemm_f32_kernel<<<grid, 256, 0, st>>>(A, Wt, C, M, Nn, K);
+    return cudaGetLastError();
+}
+
+// ===========================================================================
+// Device-side table generation
+// ===========================================================================
+namespace {
+
+// e^{2 pi i (frac + ip/n)}: frac = (w kappa).p / n in double (exact for
+// dyadic offsets), ip reduced mod n exactly in integers.
+__device__ __forceinline__ double2 phase_turns(double turns) {
+    turns -= floor(turns);
+    double s, c;
+    sincospi(2.0 * turns, &s, &c);
+    return make_double2(c, s);
+}
+
+__device__ double2 dense_entry_dev(int n, double r, double s, double t, int i0, int i1, int i2, int k0, int k1,
+                                   int k2) {
+    double re = 0.0, im = 0.0;
+    for (int e = 0; e < 24; ++e) {
+        const int* w = c_group + e * 9;
+        const int a0 = w[0] * k0 + w[1] * k1 + w[2] * k2;
+        const int a1 = w[3] * k0 + w[4] * k1 + w[5] * k2;
+        const int a2 = w[6] * k0 + w[7] * k1 + w[8] * k2;
+        const double frac = (r * a0 + s * a1 + t * a2) / n;
+        long long ip = static_cast<long long>(a0) * i0 + static_cast<long long>(a1) * i1 +
+                       static_cast<long long>(a2) * i2;
+        ip %= n;
+        if (ip < 0) ip += n;
+        const double2 ph = phase_turns(frac + static_cast<double>(ip) / n);
+        re += ph.x;
+        im += ph.y;
+    }
+    return make_double2(re / 24.0, im / 24.0);
+}
+
+template <typename R>
+__global__ void gen_dense_realform_kernel(int n, double r, double s, double t, R* Wt) {
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= N * N) return;
+    const int64_t node = idx / N, kap = idx % N;
+    const int i0 = static_cast<int>(node / (n * n)), i1 = static_cast<int>((node / n) % n), i2 = static_cast<int>(node % n);
+    const int k0 = static_cast<int>(kap / (n * n)), k1 = static_cast<int>((kap / n) % n), k2 = static_cast<int>(kap % n);
+    const double2 v = dense_entry_dev(n, r, s, t, i0, i1, i2, k0, k1, k2);
+    const int64_t K = 2 * N;
+    Wt[(2 * node) * K + 2 * kap] = static_cast<R>(v.x);
+    Wt[(2 * node) * K + 2 * kap + 1] = static_cast<R>(-v.y);
+    Wt[(2 * node + 1) * K + 2 * kap] = static_cast<R>(v.y);
+    Wt[(2 * node + 1) * K + 2 * kap + 1] = static_cast<R>(v.x);
+}
+
+__global__ void gen_dense_colmajor_kernel(int n, double r, double s, double t, double2* D) {
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= N * N) return;
+    const int64_t kap = idx / N, node = idx % N;
+    const int i0 = static_cast<int>(node / (n * n)), i1 = static_cast<int>((node / n) % n), i2 = static_cast<int>(node % n);
+    const int k0 = static_cast<int>(kap / (n * n)), k1 = static_cast<int>((kap / n) % n), k2 = static_cast<int>(kap % n);
+    D[idx] = dense_entry_dev(n, r, s, t, i0, i1, i2, k0, k1, k2);
+}
+
+// D^{-1}[kappa][node] = (1/N) sum_{a in O(kappa)} Sinv[kappa][a] e^{-2 pi i a.node/n}
+template <typename R>
+__global__ void gen_dense_inv_realform_kernel(int n, OrbitDev od, R* Wt) {
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= N * N) return;
+    const int64_t kap = idx / N, node = idx % N;
+    const int i0 = static_cast<int>(node / (n * n)), i1 = static_cast<int>((node / n) % n), i2 = static_cast<int>(node % n);
+    const int O = od.orbit_of[kap], pk = od.pos[kap];
+    const int off = od.mem_off[O], d = od.mem_off[O + 1] - off;
+    const double* S = od.sinv + 2 * (od.sinv_off[O] + static_cast<int64_t>(pk) * d);
+    double re = 0.0, im = 0.0;
+    for (int i = 0; i < d; ++i) {
+        const int a = od.mem[off + i];
+        const int a0 = a / (n * n), a1 = (a / n) % n, a2 = a % n;
+        const long long ip = (static_cast<long long>(a0) * i0 + static_cast<long long>(a1) * i1 +
+                              static_cast<long long>(a2) * i2) % n;
+        const double2 ph = phase_turns(-static_cast<double>(ip) / n);
+        const double sr = S[2 * i], si = S[2 * i + 1];
+        re += sr * ph.x - si * ph.y;
+        im += sr * ph.y + si * ph.x;
+    }
+    re /= static_cast<double>(N);
+    im /= static_cast<double>(N);
+    const int64_t K = 2 * N;
+    Wt[(2 * kap) * K + 2 * node] = static_cast<R>(re);
+    Wt[(2 * kap) * K + 2 * node + 1] = static_cast<R>(-im);
+    Wt[(2 * kap + 1) * K + 2 * node] = static_cast<R>(im);
+    Wt[(2 * kap + 1) * K + 2 * node + 1] = static_cast<R>(re);
+}
+
+__device__ double wrap_turn(double a) {  // TorusPoint::wrapped (chebyshev.cpp:326-335)
+    double f = a - floor(a);
+    if (f >= 1.0 - 1e-15) f = 0.0;
+    return f;
+}
+
+__device__ double2 cmul(double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ double2 crecip(double2 a) {
+    const double d = a.x * a.x + a.y * a.y;
+    return make_double2(a.x / d, -a.y / d);
+}
+__device__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+__global__ void gen_nodes_kernel(int n, double r, double s, double t, double2* out) {
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= N) return;
+    const int i = static_cast<int>(idx / (n * n)), j = static_cast<int>((idx / n) % n), k = static_cast<int>(idx % n);
+    const double th0 = wrap_turn((r + i) / n), th1 = wrap_turn((s + j) / n), th2 = wrap_turn((t + k) / n);
+    double s0, c0, s1, c1, s2, c2;
+    sincospi(2.0 * th0, &s0, &c0);
+    sincospi(2.0 * th1, &s1, &c1);
+    sincospi(2.0 * th2, &s2, &c2);
+    const double2 u = make_double2(c0, s0), v = make_double2(c1, s1), w = make_double2(c2, s2);
+    const double2 ui = crecip(u), vi = crecip(v), wi = crecip(w);
+    // coords_from_uvw (chebyshev.cpp:372-381)
+    const double2 x = cscale(cadd(cadd(u, cmul(ui, v)), cadd(cmul(vi, w), wi)), 0.25);
+    const double2 y = cscale(cadd(cadd(cadd(vi, v), cadd(cmul(u, wi), cmul(cmul(ui, v), wi))),
+                                  cadd(cmul(ui, w), cmul(cmul(u, vi), w))),
+                             1.0 / 6.0);
+    const double2 z = cscale(cadd(cadd(ui, cmul(u, vi)), cadd(cmul(v, wi), w)), 0.25);
+    double2* o = out + idx * 6;
+    o[0] = u;
+    o[1] = v;
+    o[2] = w;
+    o[3] = x;
+    o[4] = y;
+    o[5] = z;
+}
+
+// check_not_degenerate (spectral.cpp:132-149): any pair closer than 1e-9.
+__global__ void degenerate_kernel(int64_t N, const double2* nodes, int* flag) {
+    const int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (a >= N) return;
+    const double2* pa = nodes + a * 6;
+    for (int64_t b = a + 1; b < N; ++b) {
+        const double2* pb = nodes + b * 6;
+        double d = 0.0;
+        for (int c = 3; c < 6; ++c) {
+            const double dx = pa[c].x - pb[c].x, dy = pa[c].y - pb[c].y;
+            d += dx * dx + dy * dy;
+        }
+        if (d < 1e-18) {
+            atomicExch(flag, 1);
+            return;
+        }
+    }
+}
+
+__global__ void radix_perm_kernel(int n, unsigned long long* out) {
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= N) return;
+    const int m = n / 2;
+    const int64_t m3 = static_cast<int64_t>(m) * m * m;
+    const int blk = static_cast<int>(i / m3);
+    const int64_t k = i % m3;
+    const int kr = static_cast<int>(k / (m * m)), ks = static_cast<int>((k / m) % m), kt = static_cast<int>(k % m);
+    const int ir = blk >> 2, is = (blk >> 1) & 1, it = blk & 1;
+    out[i] = static_cast<unsigned long long>((static_cast<int64_t>(ir + 2 * kr) * n + (is + 2 * ks)) * n + (it + 2 * kt));
+}
+
+__global__ void residual_kernel(const double2* Y, const double2* D, int N, double* partial) {
+    __shared__ double red[256];
+    double best = 0.0;
+    const int64_t total = static_cast<int64_t>(N) * N;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        // Y[k][i] vs D column-major D[k*N + i]
+        const double2 y = Y[idx], dd = D[idx];
+        const double dx = y.x - dd.x, dy = y.y - dd.y;
+        best = fmax(best, sqrt(dx * dx + dy * dy));
+    }
+    red[threadIdx.x] = best;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+template <typename R>
+__global__ void identity_kernel(int N, R* E) {
+    const int64_t total = static_cast<int64_t>(N) * N;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t k = idx / N, i = idx % N;
+        E[2 * idx] = (k == i) ? R(1) : R(0);
+        E[2 * idx + 1] = R(0);
+    }
+}
+
+__global__ void dmma_probe_kernel(const double* A, const double* B, double* C) {
+    const int lane = threadIdx.x;
+    const double a = A[(lane >> 2) * 4 + (lane & 3)];
+    const double b = B[(lane & 3) * 8 + (lane >> 2)];
+    double c0 = 0.0, c1 = 0.0;
+    dmma884(c0, c1, a, b);
+    C[(lane >> 2) * 8 + 2 * (lane & 3)] = c0;
+    C[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = c1;
+}
+
+inline unsigned blocks_for(int64_t total, int threads) {
+    return static_cast<unsigned>((total + threads - 1) / threads);
+}
+
+}  // namespace
+
+cudaError_t gen_dense_realform(int n, double r, double s, double t, void* Wt, bool f32, cudaStream_t st) {
+    cudaError_t e = upload_group();
+    if (e != cudaSuccess) return e;
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    if (f32)
+        gen_dense_realform_kernel<float><<<blocks_for(N * N, 256), 256, 0, st>>>(n, r, s, t, static_cast<float*>(Wt));
+    else
+        gen_dense_realform_kernel<double><<<blocks_for(N * N, 256), 256, 0, st>>>(n, r, s, t, static_cast<double*>(Wt));
+    return cudaGetLastError();
+}
+
+cudaError_t gen_dense_inv_realform(int n, const OrbitDev& od, void* Wt, bool f32, cudaStream_t st) {
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    if (f32)
+        gen_dense_inv_realform_kernel<float><<<blocks_for(N * N, 256), 256, 0, st>>>(n, od, static_cast<float*>(Wt));
+    else
+        gen_dense_inv_realform_kernel<double><<<blocks_for(N * N, 256), 256, 0, st>>>(n, od, static_cast<double*>(Wt));
+    return cudaGetLastError();
+}
+
+cudaError_t gen_dense_colmajor(int n, double r, double s, double t, double* D, cudaStream_t st) {
+    cudaError_t e = upload_group();
+    if (e != cudaSuccess) return e;
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    gen_dense_colmajor_kernel<<<blocks_for(N * N, 256), 256, 0, st>>>(n, r, s, t, reinterpret_cast<double2*>(D));
+    return cudaGetLastError();
+}
+
+cudaError_t gen_nodes(int n, double r, double s, double t, double* out, int* flag, cudaStream_t st) {
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    gen_nodes_kernel<<<blocks_for(N, 256), 256, 0, st>>>(n, r, s, t, reinterpret_cast<double2*>(out));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || flag == nullptr || n > 16) return e;
+    degenerate_kernel<<<blocks_for(N, 128), 128, 0, st>>>(N, reinterpret_cast<const double2*>(out), flag);
+    return cudaGetLastError();
+}
+
+cudaError_t gen_radix_permutation(int n, unsigned long long* out, cudaStream_t st) {
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    radix_perm_kernel<<<blocks_for(N, 256), 256, 0, st>>>(n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t residual_max(const double* Y, const double* D, int N, double* partial, int nblocks, cudaStream_t st) {
+    residual_kernel<<<nblocks, 256, 0, st>>>(reinterpret_cast<const double2*>(Y), reinterpret_cast<const double2*>(D), N,
+                                             partial);
+    return cudaGetLastError();
+}
+
+cudaError_t gen_identity(int N, void* E, bool f32, cudaStream_t st) {
+    const int64_t total = static_cast<int64_t>(N) * N;
+    const unsigned nb = static_cast<unsigned>(std::min<int64_t>(blocks_for(total, 256), 4096));
+    if (f32)
+        identity_kernel<float><<<nb, 256, 0, st>>>(N, static_cast<float*>(E));
+    else
+        identity_kernel<double><<<nb, 256, 0, st>>>(N, static_cast<double*>(E));
+    return cudaGetLastError();
+}
+
+cudaError_t dmma_probe(const double* A, const double* B, double* C, cudaStream_t st) {
+    dmma_probe_kernel<<<1, 32, 0, st>>>(A, B, C);
+    return cudaGetLastError();
+}
+
+}  // namespace fcct

@@ -1,0 +1,79 @@
+// Launch interface of the sm_100a kernels (implemented in kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fcct {
+
+constexpr int kMaxStages = 16;
+
+// One stage of the fast pipeline: a sparse operator on the n^3 state vector.
+//  kind 0 (sparse): ELL row groups of RG = 32/TB rows. Entry e of group g,
+//        row slot rr, step k is e = ginfo[g].x + k*RG + rr.
+//  kind 1 (mix8):  for every node q of the level and slice h < m3,
+//        out[pos_out(blk)] = sum_g K[q][blk][g] * in[pos_in(g)],
+//        pos(g) = q*8*m3 + g*m3 + h, optionally remapped through gather /
+//        scatter (the composite radix permutation at the first/last stage).
+struct StageDesc {
+    int kind;
+    int ngroups;
+    const int2* ginfo;
+    const int* grow;
+    const int* ecol;
+    const void* ecoef;
+    int m3;
+    int nodes;
+    const void* K;
+    const int* gather;
+    const int* scatter;
+};
+
+struct PipelineDesc {
+    int n;
+    int N;
+    int tb;       // transforms per CTA tile
+    int nstages;
+    StageDesc stage[kMaxStages];
+};
+
+// Fast transform pipeline (forward or inverse, decided by the stage list).
+cudaError_t launch_pipeline(const PipelineDesc& d, bool f32, const void* in, void* out, int64_t batch,
+                            cudaStream_t stream, int num_sms);
+int pipeline_smem_bytes(const PipelineDesc& d, bool f32);
+
+// Direct transform: out[b][:] = real-form GEMM of in[b][:] with Wt (2N x 2N, [col][k]).
+cudaError_t launch_gemm_f64(const double* A, const double* Wt, double* C, int64_t M, int Nn, int K,
+                            cudaStream_t stream);
+cudaError_t launch_gemm_f32(const float* A, const float* Wt, float* C, int64_t M, int Nn, int K,
+                            cudaStream_t stream);
+
+// Device-side table generation.
+struct OrbitDev {
+    const int* orbit_of;
+    const int* pos;
+    const int* mem_off;   // per orbit: offset into members
+    const int* mem;       // lex members
+    const int* sinv_off;  // per orbit: offset (complex elements) into sinv
+    const double* sinv;   // complex128 blocks, row-major [kappa-pos][a-pos]
+};
+// Real-form forward operator Wt[2N][2N] of D_n(p) (fp64 or fp32 output).
+cudaError_t gen_dense_realform(int n, double r, double s, double t, void* Wt, bool f32, cudaStream_t st);
+// Real-form inverse operator of D_n(p) from the orbit blocks of S_n(p)^{-1}.
+cudaError_t gen_dense_inv_realform(int n, const OrbitDev& od, void* Wt, bool f32, cudaStream_t st);
+// Complex column-major D (dense_transform(n,p).matrix layout).
+cudaError_t gen_dense_colmajor(int n, double r, double s, double t, double* D, cudaStream_t st);
+// Skew nodes: 6 complex per node (u,v,w,x,y,z); degenerate flag via *flag (device int).
+cudaError_t gen_nodes(int n, double r, double s, double t, double* out, int* flag, cudaStream_t st);
+// Composite radix permutation.
+cudaError_t gen_radix_permutation(int n, unsigned long long* out, cudaStream_t st);
+// max |Y[k][i] - D[i][k]| per CTA (Y: batch N of complex128 rows, D column-major).
+cudaError_t residual_max(const double* Y, const double* D, int N, double* partial, int nblocks,
+                         cudaStream_t st);
+// Unit-vector batch: E[k][i] = (i == k).
+cudaError_t gen_identity(int N, void* E, bool f32, cudaStream_t st);
+
+// DMMA fragment-layout probe: C (8x8) = A (8x4 row-major) * B (4x8 row-major).
+cudaError_t dmma_probe(const double* A, const double* B, double* C, cudaStream_t st);
+
+}  // namespace fcct

@@ -1,0 +1,510 @@
+// Host-side plan construction (see plan.hpp for the derivation).
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <deque>
+#include <map>
+#include <mutex>
+#include <numbers>
+#include <set>
+#include <unordered_map>
+
+namespace fcct {
+namespace {
+
+constexpr long double kTwoPiL = 2.0L * std::numbers::pi_v<long double>;
+constexpr double kConditionLimit = 1e12;  // transform.cpp:20
+// Exact factors carry only long-double rounding (~1e-18 relative); every true
+// entry of B / B^{-1} is an algebraic number of size >= ~1e-3 for n <= 64.
+constexpr long double kPrune = 1e-13L;
+
+// Gauss-Jordan inverse with partial pivoting, row-major dim x dim. Returns the
+// exact 1-norm condition ||A||_1 ||A^{-1}||_1 (inf when singular).
+double invert_ld(const std::vector<cld>& a, int dim, std::vector<cld>& inv) {
+    std::vector<cld> m(a);
+    inv.assign(static_cast<size_t>(dim) * dim, cld{0, 0});
+    for (int i = 0; i < dim; ++i) inv[i * dim + i] = 1;
+    for (int k = 0; k < dim; ++k) {
+        int best = k;
+        long double bv = std::abs(m[k * dim + k]);
+        for (int i = k + 1; i < dim; ++i) {
+            const long double v = std::abs(m[i * dim + k]);
+            if (v > bv) { bv = v; best = i; }
+        }
+        if (bv == 0.0L) return INFINITY;
+        if (best != k)
+            for (int j = 0; j < dim; ++j) {
+                std::swap(m[k * dim + j], m[best * dim + j]);
+                std::swap(inv[k * dim + j], inv[best * dim + j]);
+            }
+        const cld pinv = cld{1, 0} / m[k * dim + k];
+        for (int j = 0; j < dim; ++j) {
+            m[k * dim + j] *= pinv;
+            inv[k * dim + j] *= pinv;
+        }
+        for (int i = 0; i < dim; ++i) {
+            if (i == k) continue;
+            const cld f = m[i * dim + k];
+            if (f == cld{0, 0}) continue;
+            for (int j = 0; j < dim; ++j) {
+                m[i * dim + j] -= f * m[k * dim + j];
+                inv[i * dim + j] -= f * inv[k * dim + j];
+            }
+        }
+    }
+    auto norm1 = [dim](const std::vector<cld>& x) {
+        long double best = 0;
+        for (int j = 0; j < dim; ++j) {
+            long double s = 0;
+            for (int i = 0; i < dim; ++i) s += std::abs(x[i * dim + j]);
+            best = std::max(best, s);
+        }
+        return best;
+    };
+    return static_cast<double>(norm1(a) * norm1(inv));
+}
+
+Index3 unlex(int64_t a, int n) {
+    return Index3{static_cast<int>(a / (static_cast<int64_t>(n) * n)),
+                  static_cast<int>((a / n) % n), static_cast<int>(a % n)};
+}
+int64_t lex(const Index3& a, int n) { return (static_cast<int64_t>(a[0]) * n + a[1]) * n + a[2]; }
+int mod(int a, int n) { return ((a % n) + n) % n; }
+
+Index3 apply(const std::array<int, 9>& w, const Index3& k) {  // weyl_s4.cpp:38-43
+    Index3 o{};
+    for (int i = 0; i < 3; ++i) o[i] = w[i * 3] * k[0] + w[i * 3 + 1] * k[1] + w[i * 3 + 2] * k[2];
+    return o;
+}
+
+void require_condition(double cond, const std::string& what) {  // transform.cpp:113-117
+    if (!(cond <= kConditionLimit))
+        throw FcctError(ST_ILL_CONDITIONED,
+                        what + ": condition estimate " + std::to_string(cond) + " exceeds 1e12");
+}
+
+}  // namespace
+
+const std::array<std::array<int, 9>, 24>& s4_group() {
+    // Breadth-first closure of the three generators, identity first
+    // (weyl_s4.cpp:54-83).
+    static const std::array<std::array<int, 9>, 24> g = [] {
+        const std::array<std::array<int, 9>, 3> gens{{{-1, 0, 0, 1, 1, 0, 0, 0, 1},
+                                                      {1, 1, 0, 0, -1, 0, 0, 1, 1},
+                                                      {1, 0, 0, 0, 1, 1, 0, 0, -1}}};
+        auto mul = [](const std::array<int, 9>& a, const std::array<int, 9>& b) {
+            std::array<int, 9> o{};
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    int acc = 0;
+                    for (int k = 0; k < 3; ++k) acc += a[i * 3 + k] * b[k * 3 + j];
+                    o[i * 3 + j] = acc;
+                }
+            return o;
+        };
+        std::array<std::array<int, 9>, 24> out{};
+        std::set<std::array<int, 9>> seen;
+        std::deque<std::array<int, 9>> frontier{{1, 0, 0, 0, 1, 0, 0, 0, 1}};
+        seen.insert(frontier.front());
+        size_t count = 0;
+        while (!frontier.empty()) {
+            auto e = frontier.front();
+            frontier.pop_front();
+            if (count >= 24) throw std::logic_error("group closure exceeded 24 elements");
+            out[count++] = e;
+            for (const auto& s : gens) {
+                auto nx = mul(e, s);
+                if (seen.insert(nx).second) frontier.push_back(nx);
+            }
+        }
+        if (count != 24) throw std::logic_error("group closure != 24");
+        return out;
+    }();
+    return g;
+}
+
+cld unit_phase_ld(long double turns) {
+    turns -= std::floor(turns);
+    return cld{std::cos(kTwoPiL * turns), std::sin(kTwoPiL * turns)};
+}
+
+const Orbits& orbits(int n) {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<Orbits>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(n);
+    if (it != cache.end()) return *it->second;
+    auto o = std::make_unique<Orbits>();
+    o->n = n;
+    const int64_t n3 = cube(n);
+    o->orbit_of.assign(n3, -1);
+    o->pos.assign(n3, -1);
+    const auto& g = s4_group();
+    for (int64_t a = 0; a < n3; ++a) {
+        if (o->orbit_of[a] >= 0) continue;
+        const Index3 av = unlex(a, n);
+        std::set<int64_t> members;
+        for (const auto& w : g) {
+            Index3 b = apply(w, av);
+            for (auto& x : b) x = mod(x, n);
+            members.insert(lex(b, n));
+        }
+        const int id = static_cast<int>(o->members.size());
+        std::vector<int32_t> list(members.begin(), members.end());
+        for (size_t i = 0; i < list.size(); ++i) {
+            o->orbit_of[list[i]] = id;
+            o->pos[list[i]] = static_cast<int32_t>(i);
+        }
+        o->members.push_back(std::move(list));
+    }
+    auto& ref = *o;
+    cache.emplace(n, std::move(o));
+    return ref;
+}
+
+OrbitBlocks orbit_blocks(int n, const Params& p) {
+    OrbitBlocks ob;
+    ob.n = n;
+    ob.p = p;
+    ob.orb = &orbits(n);
+    const auto& g = s4_group();
+    const auto& orb = *ob.orb;
+    ob.S.resize(orb.members.size());
+    ob.Sinv.resize(orb.members.size());
+    const long double pr = p.r, ps = p.s, pt = p.t;
+    for (size_t o = 0; o < orb.members.size(); ++o) {
+        const auto& mem = orb.members[o];
+        const int d = static_cast<int>(mem.size());
+        std::vector<cld> S(static_cast<size_t>(d) * d, cld{0, 0});
+        for (int j = 0; j < d; ++j) {  // polynomial index kappa = mem[j]
+            const Index3 kap = unlex(mem[j], n);
+            for (const auto& w : g) {
+                const Index3 wk = apply(w, kap);
+                Index3 a = wk;
+                for (auto& x : a) x = mod(x, n);
+                const int i = orb.pos[lex(a, n)];
+                // e^{2 pi i (w kappa).p / n} with the unreduced exponent
+                // (ColumnEvaluator prefactor, transform.cpp:51-53).
+                S[static_cast<size_t>(i) * d + j] +=
+                    unit_phase_ld((pr * wk[0] + ps * wk[1] + pt * wk[2]) / n) / 24.0L;
+            }
+        }
+        const double c = invert_ld(S, d, ob.Sinv[o]);
+        ob.worst_condition = std::max(ob.worst_condition, c);
+        ob.S[o] = std::move(S);
+    }
+    return ob;
+}
+
+cld dense_entry(int n, const Params& p, const Index3& node, const Index3& kappa) {
+    // (1/24) sum_w e^{2 pi i (w kappa).((p + ijk)/n)}; the integer part of the
+    // exponent is reduced exactly before the phase is taken.
+    cld acc{0, 0};
+    for (const auto& w : s4_group()) {
+        const Index3 a = apply(w, kappa);
+        const long double frac = (static_cast<long double>(p.r) * a[0] +
+                                  static_cast<long double>(p.s) * a[1] +
+                                  static_cast<long double>(p.t) * a[2]) / n;
+        const int64_t ip = static_cast<int64_t>(a[0]) * node[0] + static_cast<int64_t>(a[1]) * node[1] +
+                           static_cast<int64_t>(a[2]) * node[2];
+        acc += unit_phase_ld(frac + static_cast<long double>(((ip % n) + n) % n) / n);
+    }
+    return acc / 24.0L;
+}
+
+void check_nodes(int n, const Params& p) {
+    if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "skew_nodes: n must be >= 1");
+    if (n > 16) return;  // quadratic scan; larger grids skip it (spectral.cpp:133)
+    const int64_t n3 = cube(n);
+    std::vector<std::array<std::complex<double>, 3>> xyz(n3);
+    const double two_pi = 2.0 * std::numbers::pi;
+    for (int64_t a = 0; a < n3; ++a) {
+        const Index3 ijk = unlex(a, n);
+        auto wrap = [](double v) {  // TorusPoint::wrapped (chebyshev.cpp:326-335)
+            double f = v - std::floor(v);
+            if (f >= 1.0 - 1e-15) f = 0.0;
+            return f;
+        };
+        const double th[3] = {wrap((p.r + ijk[0]) / n), wrap((p.s + ijk[1]) / n),
+                              wrap((p.t + ijk[2]) / n)};
+        const std::complex<double> u{std::cos(two_pi * th[0]), std::sin(two_pi * th[0])};
+        const std::complex<double> v{std::cos(two_pi * th[1]), std::sin(two_pi * th[1])};
+        const std::complex<double> w{std::cos(two_pi * th[2]), std::sin(two_pi * th[2])};
+        const auto ui = 1.0 / u, vi = 1.0 / v, wi = 1.0 / w;  // chebyshev.cpp:372-381
+        xyz[a][0] = 0.25 * (u + ui * v + vi * w + wi);
+        xyz[a][1] = (vi + v + u * wi + ui * v * wi + ui * w + u * vi * w) / 6.0;
+        xyz[a][2] = 0.25 * (ui + u * vi + v * wi + w);
+    }
+    constexpr double th2 = 1e-9 * 1e-9;
+    for (int64_t a = 0; a < n3; ++a)
+        for (int64_t b = a + 1; b < n3; ++b) {
+            const double d = std::norm(xyz[a][0] - xyz[b][0]) + std::norm(xyz[a][1] - xyz[b][1]) +
+                             std::norm(xyz[a][2] - xyz[b][2]);
+            if (d < th2) {
+                const Index3 ia = unlex(a, n), ib = unlex(b, n);
+                throw FcctError(ST_DEGENERATE_NODES,
+                                "nodes (" + std::to_string(ia[0]) + "," + std::to_string(ia[1]) +
+                                    "," + std::to_string(ia[2]) + ") and (" + std::to_string(ib[0]) +
+                                    "," + std::to_string(ib[1]) + "," + std::to_string(ib[2]) +
+                                    ") map to the same spectral point for n=" + std::to_string(n));
+            }
+        }
+}
+
+std::vector<uint64_t> radix_permutation(int n) {
+    if (n < 2) throw FcctError(ST_INVALID_ARGUMENT, "radix_permutation: n must be >= 2");
+    if (n % 2 != 0)
+        throw FcctError(ST_ODD_SIZE, "radix_permutation: size " + std::to_string(n) + " is odd");
+    const int m = n / 2;
+    const int64_t m3 = cube(m);
+    std::vector<uint64_t> perm(static_cast<size_t>(cube(n)));
+    for (int64_t i = 0; i < cube(n); ++i) {
+        const int blk = static_cast<int>(i / m3);
+        const Index3 k = unlex(i % m3, m);
+        const int ir = blk >> 2, is = (blk >> 1) & 1, it = blk & 1;
+        perm[i] = static_cast<uint64_t>(lex(Index3{ir + 2 * k[0], is + 2 * k[1], it + 2 * k[2]}, n));
+    }
+    return perm;
+}
+
+std::vector<int32_t> output_order(int n) {
+    if (n == 1) return {0};
+    const auto sub = output_order(n / 2);
+    const auto perm = radix_permutation(n);
+    const int64_t m3 = cube(n / 2);
+    std::vector<int32_t> z(cube(n));
+    for (int64_t i = 0; i < cube(n); ++i)
+        z[i] = static_cast<int32_t>(perm[(i / m3) * m3 + sub[i % m3]]);
+    return z;
+}
+
+namespace {
+
+// B = (K^{-1} (x) I) blockdiag(S_m(child)^{-1}) Phi S_n, column by column.
+SparseLD derive_B(int n, const OrbitBlocks& Sn, const std::array<OrbitBlocks, 8>& Sm,
+                  const std::array<cld, 64>& Kinv) {
+    const int m = n / 2;
+    const int64_t n3 = cube(n), m3 = cube(m);
+    const auto& on = *Sn.orb;
+    const auto& om = orbits(m);
+    // triplets (row, col, val), column-major generation
+    std::vector<std::vector<std::pair<int32_t, cld>>> rows(n3);
+    std::vector<cld> v, u;
+    for (int64_t c = 0; c < n3; ++c) {
+        const int O = on.orbit_of[c], j = on.pos[c];
+        const auto& mem = on.members[O];
+        const int d = static_cast<int>(mem.size());
+        const Index3 cm = unlex(c, n);
+        const int64_t hrep = lex(Index3{cm[0] % m, cm[1] % m, cm[2] % m}, m);
+        const int Op = om.orbit_of[hrep];
+        const auto& memp = om.members[Op];
+        const int dp = static_cast<int>(memp.size());
+        v.assign(static_cast<size_t>(8) * dp, cld{0, 0});
+        for (int i = 0; i < d; ++i) {
+            const cld val = Sn.S[O][static_cast<size_t>(i) * d + j];
+            if (val == cld{0, 0}) continue;
+            const Index3 a = unlex(mem[i], n);
+            const int ip = om.pos[lex(Index3{a[0] % m, a[1] % m, a[2] % m}, m)];
+            for (int blk = 0; blk < 8; ++blk) {
+                const int ir = blk >> 2, is = (blk >> 1) & 1, it = blk & 1;
+                const cld tw = unit_phase_ld(static_cast<long double>(a[0] * ir + a[1] * is + a[2] * it) / n);
+                v[static_cast<size_t>(blk) * dp + ip] += tw * val;
+            }
+        }
+        u.assign(static_cast<size_t>(8) * dp, cld{0, 0});
+        for (int blk = 0; blk < 8; ++blk) {
+            const auto& Si = Sm[blk].Sinv[Op];
+            for (int h = 0; h < dp; ++h) {
+                cld acc{0, 0};
+                for (int i = 0; i < dp; ++i) acc += Si[static_cast<size_t>(h) * dp + i] * v[static_cast<size_t>(blk) * dp + i];
+                u[static_cast<size_t>(blk) * dp + h] = acc;
+            }
+        }
+        for (int g = 0; g < 8; ++g)
+            for (int h = 0; h < dp; ++h) {
+                cld acc{0, 0};
+                for (int blk = 0; blk < 8; ++blk) acc += Kinv[g * 8 + blk] * u[static_cast<size_t>(blk) * dp + h];
+                if (std::abs(acc) >= kPrune)
+                    rows[static_cast<int64_t>(g) * m3 + memp[h]].emplace_back(static_cast<int32_t>(c), acc);
+            }
+    }
+    SparseLD out;
+    out.dim = n3;
+    out.rowptr.assign(n3 + 1, 0);
+    for (int64_t r = 0; r < n3; ++r) {
+        auto& rr = rows[r];
+        std::sort(rr.begin(), rr.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (const auto& e : rr) {
+            out.col.push_back(e.first);
+            out.val.push_back(e.second);
+        }
+        out.rowptr[r + 1] = out.nnz();
+    }
+    return out;
+}
+
+// B^{-1} = S_n^{-1} Phi^{-1} blockdiag(S_m(child)) (K (x) I), column by column.
+SparseLD derive_Binv(int n, const OrbitBlocks& Sn, const std::array<OrbitBlocks, 8>& Sm,
+                     const std::array<cld, 64>& K) {
+    const int m = n / 2;
+    const int64_t n3 = cube(n), m3 = cube(m);
+    const auto& on = *Sn.orb;
+    const auto& om = orbits(m);
+    std::vector<std::vector<std::pair<int32_t, cld>>> rows(n3);
+    std::unordered_map<int64_t, cld> x;
+    std::vector<cld> w;
+    for (int g = 0; g < 8; ++g)
+        for (int64_t h = 0; h < m3; ++h) {
+            const int64_t col = g * m3 + h;
+            const int Op = om.orbit_of[h], jh = om.pos[h];
+            const auto& memp = om.members[Op];
+            const int dp = static_cast<int>(memp.size());
+            w.assign(static_cast<size_t>(8) * dp, cld{0, 0});
+            for (int blk = 0; blk < 8; ++blk) {
+                const auto& S = Sm[blk].S[Op];
+                for (int i = 0; i < dp; ++i) w[static_cast<size_t>(blk) * dp + i] = S[static_cast<size_t>(i) * dp + jh] * K[blk * 8 + g];
+            }
+            x.clear();
+            for (int i = 0; i < dp; ++i) {
+                const Index3 ap = unlex(memp[i], m);
+                for (int delta = 0; delta < 8; ++delta) {
+                    const int dr = delta >> 2, ds = (delta >> 1) & 1, dt = delta & 1;
+                    cld val{0, 0};
+                    for (int blk = 0; blk < 8; ++blk) {
+                        const int ir = blk >> 2, is = (blk >> 1) & 1, it = blk & 1;
+                        const long double sign = ((dr * ir + ds * is + dt * it) & 1) ? -1.0L : 1.0L;
+                        const cld tw = unit_phase_ld(-static_cast<long double>(ap[0] * ir + ap[1] * is + ap[2] * it) / n);
+                        val += sign * tw * w[static_cast<size_t>(blk) * dp + i];
+                    }
+                    val /= 8.0L;
+                    if (val == cld{0, 0}) continue;
+                    const int64_t a = lex(Index3{ap[0] + m * dr, ap[1] + m * ds, ap[2] + m * dt}, n);
+                    const int O = on.orbit_of[a], pa = on.pos[a];
+                    const auto& mem = on.members[O];
+                    const int d = static_cast<int>(mem.size());
+                    const auto& Si = Sn.Sinv[O];
+                    for (int k = 0; k < d; ++k) x[mem[k]] += Si[static_cast<size_t>(k) * d + pa] * val;
+                }
+            }
+            for (const auto& [row, val] : x)
+                if (std::abs(val) >= kPrune) rows[row].emplace_back(static_cast<int32_t>(col), val);
+        }
+    SparseLD out;
+    out.dim = n3;
+    out.rowptr.assign(n3 + 1, 0);
+    for (int64_t r = 0; r < n3; ++r) {
+        auto& rr = rows[r];
+        std::sort(rr.begin(), rr.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (const auto& e : rr) {
+            out.col.push_back(e.first);
+            out.val.push_back(e.second);
+        }
+        out.rowptr[r + 1] = out.nnz();
+    }
+    return out;
+}
+
+std::shared_ptr<const PlanNode> make_node(int n, const Params& p, bool check) {
+    if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "build_plan: n must be >= 1");
+    if (check) check_nodes(n, p);  // dense_transform runs the check (transform.cpp:132)
+    auto node = std::make_shared<PlanNode>();
+    node->n = n;
+    node->p = p;
+    const int64_t n3 = cube(n);
+    if (n == 1 || n % 2 != 0) {  // assemble_direct (transform.cpp:329-345)
+        node->radix = false;
+        OrbitBlocks ob = orbit_blocks(n, p);
+        node->D.resize(static_cast<size_t>(n3 * n3));
+        for (int64_t r = 0; r < n3; ++r)
+            for (int64_t c = 0; c < n3; ++c) node->D[r * n3 + c] = dense_entry(n, p, unlex(r, n), unlex(c, n));
+        // D^{-1} = S^{-1} F^{-1}: D^{-1}[kappa, node] = (1/N) sum_{a in O(kappa)} Sinv[kappa, a] e^{-2 pi i a.node/n}
+        node->Dinv.assign(static_cast<size_t>(n3 * n3), cld{0, 0});
+        const auto& orb = *ob.orb;
+        for (int64_t k = 0; k < n3; ++k) {
+            const int O = orb.orbit_of[k], pk = orb.pos[k];
+            const auto& mem = orb.members[O];
+            const int d = static_cast<int>(mem.size());
+            for (int64_t r = 0; r < n3; ++r) {
+                const Index3 nd = unlex(r, n);
+                cld acc{0, 0};
+                for (int i = 0; i < d; ++i) {
+                    const Index3 a = unlex(mem[i], n);
+                    const int64_t ip = static_cast<int64_t>(a[0]) * nd[0] + static_cast<int64_t>(a[1]) * nd[1] +
+                                       static_cast<int64_t>(a[2]) * nd[2];
+                    acc += ob.Sinv[O][static_cast<size_t>(pk) * d + i] *
+                           unit_phase_ld(-static_cast<long double>(ip % n) / n);
+                }
+                node->Dinv[k * n3 + r] = acc / static_cast<long double>(n3);
+            }
+        }
+        long double na = 0, ni = 0;
+        for (int64_t c = 0; c < n3; ++c) {
+            long double sa = 0, si = 0;
+            for (int64_t r = 0; r < n3; ++r) {
+                sa += std::abs(node->D[r * n3 + c]);
+                si += std::abs(node->Dinv[r * n3 + c]);
+            }
+            na = std::max(na, sa);
+            ni = std::max(ni, si);
+        }
+        node->condition = static_cast<double>(na * ni);
+        require_condition(node->condition, "dense transform (n=" + std::to_string(n) + ")");
+        return node;
+    }
+    const int m = n / 2;
+    node->radix = true;
+    for (int blk = 0; blk < 8; ++blk)
+        node->children[blk] = make_node(m, p.child(blk >> 2, (blk >> 1) & 1, blk & 1), check);
+    // kernel = dense_transform(2, p).matrix (transform.cpp:397): rows = nodes blk, cols = g
+    std::vector<cld> K(64), Kinv;
+    for (int blk = 0; blk < 8; ++blk)
+        for (int g = 0; g < 8; ++g)
+            K[blk * 8 + g] = dense_entry(2, p, unlex(blk, 2), unlex(g, 2));
+    const double kc = invert_ld(K, 8, Kinv);
+    require_condition(kc, "radix kernel");
+    std::copy(K.begin(), K.end(), node->K.begin());
+    std::copy(Kinv.begin(), Kinv.end(), node->Kinv.begin());
+    const OrbitBlocks Sn = orbit_blocks(n, p);
+    require_condition(Sn.worst_condition, "orbit block (n=" + std::to_string(n) + ")");
+    std::array<OrbitBlocks, 8> Sm;
+    for (int blk = 0; blk < 8; ++blk) {
+        Sm[blk] = orbit_blocks(m, node->children[blk]->p);
+        require_condition(Sm[blk].worst_condition, "child block " + std::to_string(blk));
+    }
+    node->condition = std::max(kc, Sn.worst_condition);
+    node->B = derive_B(n, Sn, Sm, node->Kinv);
+    node->Binv = derive_Binv(n, Sn, Sm, node->K);
+    return node;
+}
+
+}  // namespace
+
+std::shared_ptr<const PlanNode> build_tree(int n, const Params& p) {
+    if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "build_plan: n must be >= 1");
+    // Degeneracy is a property of the root grid; children grids are subsets
+    // of it (spectral tests "half size grids nest"), so one scan suffices.
+    check_nodes(n, p);
+    return make_node(n, p, false);
+}
+
+int64_t tree_nnz(const PlanNode& node, bool inverse, bool with_b2) {
+    if (!node.radix) return 0;
+    int64_t s = (node.n == 2 && !with_b2) ? 0 : (inverse ? node.Binv.nnz() : node.B.nnz());
+    for (const auto& c : node.children) s += tree_nnz(*c, inverse, with_b2);
+    return s;
+}
+
+int tree_levels(int n) {
+    int l = 0;
+    while (n > 1 && n % 2 == 0) { n /= 2; ++l; }
+    return l;
+}
+
+double algorithmic_flops(const PlanNode& root, bool inverse) {
+    const double N = static_cast<double>(cube(root.n));
+    if (!root.radix) return 8.0 * N * N;
+    return 8.0 * (static_cast<double>(tree_nnz(root, inverse, false)) + 8.0 * N * tree_levels(root.n));
+}
+
+}  // namespace fcct

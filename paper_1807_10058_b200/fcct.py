@@ -1,0 +1,495 @@
+"""Python mirror of the reference `fcct` transform API (proj/include/fcct/transform.hpp).
+
+Same names, argument meaning and error behaviour as the reference C++ library,
+executed by the sm_100a CUDA library through the C ABI (include/fcct_gpu.h).
+Tensors are torch complex tensors: complex128 for fp64 plans (the reference's
+Eigen::VectorXcd), complex64 for the fp32 variant. A tensor of shape
+[batch, n^3] is a batch of independent blocks (the reference applies one vector
+per call; batching is the B200 addition). CPU tensors go through the host-buffer
+entry points (H2D + transform + D2H); CUDA tensors stay on the device.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import math
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import List, Optional
+
+import numpy as np
+import torch
+
+from . import _capi
+
+# ---------------------------------------------------------------------------
+# errors: fcct/errors.hpp:9-63
+# ---------------------------------------------------------------------------
+
+
+class ErrorCategory(enum.Enum):
+    math = "math"  # CLI exit code 2
+    io = "io"  # CLI exit code 3
+
+
+class FcctError(RuntimeError):
+    category = ErrorCategory.math
+
+
+class DegenerateNodes(FcctError):
+    pass
+
+
+class IllConditioned(FcctError):
+    pass
+
+
+class SizeMismatch(FcctError):
+    pass
+
+
+class OddSize(FcctError):
+    pass
+
+
+class DerivationError(FcctError):
+    pass
+
+
+class MalformedFile(FcctError):
+    category = ErrorCategory.io
+
+
+class IoFailure(FcctError):
+    category = ErrorCategory.io
+
+
+class CudaError(FcctError):
+    pass
+
+
+def _raise(status: int) -> None:
+    if status == _capi.OK:
+        return
+    msg = _capi.lib().fcct_last_error().decode(errors="replace")
+    exc = {
+        _capi.INVALID_ARGUMENT: ValueError,  # std::invalid_argument
+        _capi.PARAMS_MISMATCH: ValueError,
+        _capi.SIZE_MISMATCH: SizeMismatch,
+        _capi.ODD_SIZE: OddSize,
+        _capi.DEGENERATE_NODES: DegenerateNodes,
+        _capi.ILL_CONDITIONED: IllConditioned,
+        _capi.IO: IoFailure,
+        _capi.CUDA: CudaError,
+        _capi.DERIVATION: DerivationError,
+    }.get(status, FcctError)
+    raise exc(msg)
+
+
+# ---------------------------------------------------------------------------
+# SkewParams: fcct/spectral.hpp:13-27, src/spectral.cpp:153-223
+# ---------------------------------------------------------------------------
+
+
+def encode_param(value: float) -> str:
+    """Exact small rational as 'a/b', else %.17g (spectral.cpp:159-181)."""
+    if value == 0.0:
+        return "0"
+    x = value
+    p0, q0, p1, q1 = 0, 1, 1, 0
+    for _ in range(40):
+        fa = math.floor(x)
+        if abs(fa) > 1e15:
+            break
+        a = int(fa)
+        p2, q2 = a * p1 + p0, a * q1 + q0
+        if q2 > 1000000 or q2 < 0:
+            break
+        if q2 != 0 and p2 / q2 == value:
+            return str(p2) if q2 == 1 else f"{p2}/{q2}"
+        p0, q0, p1, q1 = p1, q1, p2, q2
+        frac = x - fa
+        if frac == 0.0:
+            break
+        x = 1.0 / frac
+    return f"{value:.17g}"
+
+
+def parse_param(text: str) -> float:
+    """Inverse of encode_param (spectral.cpp:187-209)."""
+    if not text:
+        raise ValueError("empty grid offset")
+    try:
+        if "/" in text:
+            num, den = text.split("/", 1)
+            if "/" in den or float(den) == 0.0:
+                raise ValueError
+            return float(num) / float(den)
+        return float(text)
+    except ValueError:
+        raise ValueError(f"cannot parse grid offset '{text}'") from None
+
+
+@dataclass(frozen=True)
+class SkewParams:
+    r: float = 0.0
+    s: float = 0.0
+    t: float = 0.0
+
+    @staticmethod
+    def canonical() -> "SkewParams":
+        return SkewParams(0.125, 0.0, 0.375)
+
+    def child(self, ir: int, is_: int, it: int) -> "SkewParams":
+        return SkewParams((self.r + ir) / 2.0, (self.s + is_) / 2.0, (self.t + it) / 2.0)
+
+    def encode(self) -> str:
+        return f"{encode_param(self.r)},{encode_param(self.s)},{encode_param(self.t)}"
+
+
+def parse_params(text: str) -> SkewParams:
+    parts = text.split(",")
+    if len(parts) != 3:
+        raise ValueError(f"grid offsets must be 'r,s,t', got '{text}'")
+    return SkewParams(*(parse_param(p) for p in parts))
+
+
+# ---------------------------------------------------------------------------
+# value types: transform.hpp:17-44
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class SignalTensor:
+    n: int
+    data: torch.Tensor
+
+    @staticmethod
+    def zeros(n: int, batch: Optional[int] = None, dtype=torch.complex128, device="cpu") -> "SignalTensor":
+        shape = (n**3,) if batch is None else (batch, n**3)
+        return SignalTensor(n, torch.zeros(shape, dtype=dtype, device=device))
+
+    def size(self) -> int:
+        return self.n**3
+
+
+@dataclass
+class Spectrum:
+    n: int
+    params: SkewParams
+    values: torch.Tensor
+
+
+@dataclass
+class DenseTransform:
+    """Dense matrix D_n(r,s,t) (rows = nodes, cols = polynomial index), generated
+    on the device, plus the direct plan that applies it (DMMA GEMM)."""
+
+    n: int
+    params: SkewParams
+    matrix: torch.Tensor
+    condition_estimate: float = float("nan")
+    _plan: Optional["TransformPlan"] = field(default=None, repr=False)
+
+
+class Kind(enum.Enum):
+    direct = 0
+    radix2 = 1
+
+
+@dataclass
+class SparseMatrix:
+    """CSC export of a basis factor (Eigen::SparseMatrix<Complex> layout)."""
+
+    rows: int
+    cols: int
+    colptr: np.ndarray
+    rowidx: np.ndarray
+    values: np.ndarray
+
+    def nonZeros(self) -> int:  # noqa: N802 (reference name)
+        return int(self.values.size)
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros((self.rows, self.cols), dtype=np.complex128)
+        for c in range(self.cols):
+            sl = slice(self.colptr[c], self.colptr[c + 1])
+            out[self.rowidx[sl], c] = self.values[sl]
+        return out
+
+
+def _dtype_of(precision: str) -> torch.dtype:
+    return torch.complex64 if precision == "f32" else torch.complex128
+
+
+class TransformPlan:
+    """Executable plan (transform.hpp:67-114). Immutable once built."""
+
+    def __init__(self, handle: int, precision: str, device: int):
+        self._h = ctypes.c_void_p(handle)
+        self.precision = precision
+        self.device = device
+        info = _capi.PlanInfo()
+        _raise(_capi.lib().fcct_plan_info(self._h, ctypes.byref(info)))
+        self.info = info
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _capi.lib().fcct_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # accessors ------------------------------------------------------------
+    def kind(self) -> Kind:
+        return Kind(self.info.kind)
+
+    def n(self) -> int:
+        return self.info.n
+
+    def params(self) -> SkewParams:
+        return SkewParams(self.info.r, self.info.s, self.info.t)
+
+    def permutation(self) -> np.ndarray:
+        if self.kind() != Kind.radix2:
+            raise ValueError("permutation(): plan is direct")
+        return radix_permutation(self.n())
+
+    def kernel(self) -> np.ndarray:
+        out = (ctypes.c_double * 128)()
+        _raise(_capi.lib().fcct_plan_kernel(self._h, out))
+        return np.frombuffer(out, dtype=np.complex128).reshape(8, 8, order="F").copy()
+
+    def basis(self) -> SparseMatrix:
+        L = _capi.lib()
+        nnz = ctypes.c_int64()
+        _raise(L.fcct_plan_basis(self._h, ctypes.byref(nnz), None, None, None))
+        N = self.n() ** 3
+        colptr = np.zeros(N + 1, dtype=np.int64)
+        rowidx = np.zeros(nnz.value, dtype=np.int32)
+        vals = np.zeros(2 * nnz.value, dtype=np.float64)
+        _raise(
+            L.fcct_plan_basis(
+                self._h,
+                ctypes.byref(nnz),
+                colptr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                rowidx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                vals.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+            )
+        )
+        return SparseMatrix(N, N, colptr, rowidx, vals.view(np.complex128))
+
+    def children(self) -> List[tuple]:
+        out = []
+        for i in range(8):
+            n, r, s, t, k = ctypes.c_int(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+            _raise(
+                _capi.lib().fcct_plan_child(
+                    self._h, i, ctypes.byref(n), ctypes.byref(r), ctypes.byref(s), ctypes.byref(t), ctypes.byref(k)
+                )
+            )
+            out.append((n.value, SkewParams(r.value, s.value, t.value), Kind(k.value)))
+        return out
+
+    # raw vector forms (apply_values / solve_values, transform.cpp:429-494) ------
+    def _run(self, x: torch.Tensor, inverse: bool, params: Optional[SkewParams] = None) -> torch.Tensor:
+        N = self.n() ** 3
+        dt = _dtype_of(self.precision)
+        if x.dtype != dt:
+            raise TypeError(f"expected {dt} data for a {self.precision} plan, got {x.dtype}")
+        if x.shape[-1] != N:
+            raise SizeMismatch(f"signal has {x.shape[-1]} samples, need {N}")
+        batch = x.numel() // N
+        L = _capi.lib()
+        if x.is_cuda:
+            x = x.contiguous()
+            out = torch.empty_like(x)
+            stream = torch.cuda.current_stream(x.device).cuda_stream
+            if inverse and params is not None:
+                st = L.fcct_inverse_checked(
+                    self._h, params.r, params.s, params.t, x.data_ptr(), out.data_ptr(), batch, stream
+                )
+            else:
+                fn = L.fcct_inverse if inverse else L.fcct_forward
+                st = fn(self._h, x.data_ptr(), out.data_ptr(), batch, stream)
+            _raise(st)
+            return out
+        if inverse and params is not None and params != self.params():
+            raise ValueError("inverse_apply: spectrum was produced on a different skew grid")
+        x = x.contiguous()
+        out = torch.empty_like(x)
+        fn = L.fcct_inverse_host if inverse else L.fcct_forward_host
+        _raise(fn(self._h, x.data_ptr(), out.data_ptr(), batch, None))
+        return out
+
+    def apply_values(self, x: torch.Tensor, threads: int = 1) -> torch.Tensor:
+        return self._run(x, False)
+
+    def solve_values(self, q: torch.Tensor, threads: int = 1) -> torch.Tensor:
+        return self._run(q, True)
+
+
+# ---------------------------------------------------------------------------
+# free functions: transform.hpp:46-143
+# ---------------------------------------------------------------------------
+
+
+def _create(n: int, p: SkewParams, method: int, precision: str, device: int) -> TransformPlan:
+    if not isinstance(n, int):
+        raise TypeError("n must be an int")
+    h = ctypes.c_void_p()
+    prec = _capi.F32 if precision == "f32" else _capi.F64
+    _raise(_capi.lib().fcct_plan_create(n, p.r, p.s, p.t, method, prec, device, ctypes.byref(h)))
+    return TransformPlan(h.value, precision, device)
+
+
+def _device_index(device) -> int:
+    if device is None:
+        return torch.cuda.current_device()
+    return torch.device(device).index or 0
+
+
+def dense_transform(n: int, p: SkewParams, precision: str = "f64", device=None) -> DenseTransform:
+    """dense_transform (transform.cpp:130-144): matrix generated on the GPU."""
+    if n < 1:
+        raise ValueError("dense_transform: n must be >= 1")
+    dev = _device_index(device)
+    plan = _create(n, p, _capi.DIRECT, precision, dev)
+    N = n**3
+    mat = torch.empty((N, N), dtype=torch.complex128, device=f"cuda:{dev}")
+    # the C ABI writes column-major; a row-major [N][N] view of it is D^T
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _raise(_capi.lib().fcct_dense_matrix(n, p.r, p.s, p.t, mat.data_ptr(), stream))
+    return DenseTransform(n, p, mat.t(), plan.info.condition, plan)
+
+
+def naive_apply(t: DenseTransform, s: SignalTensor) -> Spectrum:
+    """naive_apply (transform.cpp:146-156): y = D x on the DMMA GEMM."""
+    if t.n != s.n:
+        raise SizeMismatch(f"naive_apply: transform size {t.n} vs signal size {s.n}")
+    if s.data.shape[-1] != t.n**3:
+        raise SizeMismatch(f"naive_apply: signal has {s.data.shape[-1]} samples, need {t.n ** 3}")
+    return Spectrum(t.n, t.params, t._plan.apply_values(s.data))
+
+
+def inverse_apply(t, q: Spectrum, threads: int = 1) -> SignalTensor:
+    """inverse_apply for a DenseTransform (transform.cpp:158-169) or a
+    TransformPlan (transform.cpp:509-524)."""
+    if isinstance(t, DenseTransform):
+        if t.n != q.n:
+            raise SizeMismatch(f"inverse_apply: transform size {t.n} vs spectrum size {q.n}")
+        if t.params != q.params:
+            raise ValueError("inverse_apply: spectrum was produced on a different skew grid")
+        if q.values.shape[-1] != t.n**3:
+            raise SizeMismatch(f"inverse_apply: spectrum has {q.values.shape[-1]} values, need {t.n ** 3}")
+        return SignalTensor(t.n, t._plan._run(q.values, True, q.params))
+    plan: TransformPlan = t
+    if plan.n() != q.n:
+        raise SizeMismatch(f"inverse_apply: plan size {plan.n()} vs spectrum size {q.n}")
+    if plan.params() != q.params:
+        raise ValueError("inverse_apply: spectrum was produced on a different skew grid")
+    if q.values.shape[-1] != q.n**3:
+        raise SizeMismatch(f"inverse_apply: spectrum has {q.values.shape[-1]} values, need {q.n ** 3}")
+    return SignalTensor(plan.n(), plan._run(q.values, True, q.params))
+
+
+def radix_permutation(n: int) -> np.ndarray:
+    """radix_permutation (transform.cpp:171-194), generated on the device."""
+    if n < 2:
+        raise ValueError("radix_permutation: n must be >= 2")
+    if n % 2:
+        raise OddSize(f"radix_permutation: size {n} is odd")
+    out = np.zeros(n**3, dtype=np.uint64)
+    _raise(_capi.lib().fcct_radix_permutation(n, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+    return out
+
+
+def build_plan(n: int, p: SkewParams, store=None, precision: str = "f64", device=None) -> TransformPlan:
+    """build_plan (transform.cpp:404-408): radix2 tree for even n, direct otherwise."""
+    if n < 1:
+        raise ValueError("build_plan: n must be >= 1")
+    if store is not None:
+        return store.load_or_build(n, p)
+    return _create(n, p, _capi.FAST, precision, _device_index(device))
+
+
+def basis_change(n: int, p: SkewParams, inverse: bool = False) -> SparseMatrix:
+    """basis_change (transform.cpp:314-320): the exact sparse factor B (or its
+    explicit inverse), derived on the host from the orbit structure."""
+    if n < 2 or n % 2:
+        raise OddSize(f"basis_change: needs an even size, got {n}")
+    L = _capi.lib()
+    nnz = ctypes.c_int64()
+    _raise(L.fcct_basis_change(n, p.r, p.s, p.t, int(inverse), ctypes.byref(nnz), None, None, None))
+    N = n**3
+    colptr = np.zeros(N + 1, dtype=np.int64)
+    rowidx = np.zeros(nnz.value, dtype=np.int32)
+    vals = np.zeros(2 * nnz.value, dtype=np.float64)
+    _raise(
+        L.fcct_basis_change(
+            n, p.r, p.s, p.t, int(inverse), ctypes.byref(nnz),
+            colptr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+            rowidx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+            vals.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+        )
+    )
+    return SparseMatrix(N, N, colptr, rowidx, vals.view(np.complex128))
+
+
+def plan_tree_stats(n: int, p: SkewParams) -> dict:
+    """Host-side statistics of the fast plan tree (no GPU)."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    f, g = ctypes.c_double(), ctypes.c_double()
+    _raise(_capi.lib().fcct_plan_tree_stats(n, p.r, p.s, p.t, ctypes.byref(a), ctypes.byref(b), ctypes.byref(f), ctypes.byref(g)))
+    return {"tree_nnz": a.value, "tree_nnz_inv": b.value, "flops_forward": f.value, "flops_inverse": g.value}
+
+
+def fast_apply(plan: TransformPlan, s: SignalTensor, threads: int = 1) -> Spectrum:
+    """fast_apply (transform.cpp:496-507). `threads` is accepted for API
+    compatibility; the GPU result does not depend on it (bitwise, as in the
+    reference, transform.hpp:121-122)."""
+    if plan.n() != s.n:
+        raise SizeMismatch(f"fast_apply: plan size {plan.n()} vs signal size {s.n}")
+    if s.data.shape[-1] != s.n**3:
+        raise SizeMismatch(f"fast_apply: signal has {s.data.shape[-1]} samples, need {s.n ** 3}")
+    return Spectrum(plan.n(), plan.params(), plan.apply_values(s.data, max(1, threads)))
+
+
+def factorization_residual(plan: TransformPlan, dense: DenseTransform) -> float:
+    """factorization_residual (transform.cpp:526-540), evaluated on the GPU
+    against the device-generated dense matrix."""
+    if plan.n() != dense.n:
+        raise SizeMismatch("factorization_residual: sizes differ")
+    out = ctypes.c_double()
+    _raise(_capi.lib().fcct_factorization_residual(plan._h, ctypes.byref(out)))
+    return out.value
+
+
+def with_perturbed_basis(plan: TransformPlan, delta: float) -> TransformPlan:
+    """with_perturbed_basis (transform.cpp:542-554): negative-control hook."""
+    h = ctypes.c_void_p()
+    _raise(_capi.lib().fcct_plan_perturbed_basis(plan._h, delta, ctypes.byref(h)))
+    return TransformPlan(h.value, plan.precision, plan.device)
+
+
+def skew_nodes(n: int, p: SkewParams, device=None) -> torch.Tensor:
+    """Node set (spectral.cpp:261-277) generated on the device: [n^3, 6]
+    complex128 columns (u, v, w, x, y, z). Raises DegenerateNodes for n <= 16."""
+    dev = _device_index(device)
+    out = torch.empty((n**3, 6), dtype=torch.complex128, device=f"cuda:{dev}")
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _raise(_capi.lib().fcct_skew_nodes(n, p.r, p.s, p.t, out.data_ptr(), stream))
+    return out
+
+
+def shard_range(total: int, rank: int, world: int) -> tuple:
+    """Contiguous block range of one rank (ceil split): the batch scheduler."""
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    _raise(_capi.lib().fcct_shard_range(total, rank, world, ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value
+
+
+def exact_fraction(x: float) -> Fraction:
+    return Fraction(x)

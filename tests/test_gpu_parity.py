@@ -1,0 +1,301 @@
+"""GPU parity tests: the sm_100a paths (through the C ABI) vs the CPU oracle.
+
+Bars (north star): relative L2 <= 1e-12 in fp64, <= 1e-5 in fp32; integer
+tables bit-exact. The reference's own tolerances (test_transform.cpp:138-183,
+acceptance/main.cpp:352-410) are looser and are checked too.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_1807_10058_b200 import (
+    DegenerateNodes,
+    Kind,
+    OddSize,
+    SignalTensor,
+    SizeMismatch,
+    SkewParams,
+    Spectrum,
+    basis_change,
+    build_plan,
+    dense_transform,
+    factorization_residual,
+    fast_apply,
+    inverse_apply,
+    naive_apply,
+    radix_permutation,
+    skew_nodes,
+    with_perturbed_basis,
+)
+
+pytestmark = pytest.mark.gpu
+
+CANON = SkewParams.canonical()
+F64_TOL = 1e-12
+F32_TOL = 1e-5
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def tup(p):
+    return (p.r, p.s, p.t)
+
+
+def rand_batch(n, batch, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.uniform(-1, 1, (batch, n**3)) + 1j * rng.uniform(-1, 1, (batch, n**3))).astype(np.complex128)
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("p", [CANON, SkewParams(0.21, 0.055, 0.4), SkewParams(0.37, 0.61, 0.085)])
+def test_fast_forward_inverse_f64(cuda, oracle_mod, n, p):
+    x = rand_batch(n, 37, seed=n)  # ragged: not a multiple of the CTA tile
+    y_ref = oracle_mod.forward_dense(n, tup(p), x)
+    plan = build_plan(n, p)
+    assert plan.kind() == Kind.radix2
+    xt = torch.from_numpy(x).to(cuda)
+    y = fast_apply(plan, SignalTensor(n, xt)).values
+    assert rel(y.cpu().numpy(), y_ref) <= F64_TOL
+    x_ref = oracle_mod.inverse_dense(n, tup(p), y_ref)
+    xb = inverse_apply(plan, Spectrum(n, p, torch.from_numpy(y_ref).to(cuda))).data
+    assert rel(xb.cpu().numpy(), x_ref) <= F64_TOL
+    # round trip (reference: <= 1e-8)
+    back = inverse_apply(plan, Spectrum(n, p, y)).data
+    assert rel(back.cpu().numpy(), x) <= F64_TOL
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_direct_forward_inverse_f64(cuda, oracle_mod, n):
+    x = rand_batch(n, 70, seed=100 + n)
+    y_ref = oracle_mod.forward_dense(n, tup(CANON), x)
+    dense = dense_transform(n, CANON)
+    xt = torch.from_numpy(x).to(cuda)
+    y = naive_apply(dense, SignalTensor(n, xt)).values
+    assert rel(y.cpu().numpy(), y_ref) <= F64_TOL
+    x_ref = oracle_mod.inverse_dense(n, tup(CANON), y_ref)
+    xb = inverse_apply(dense, Spectrum(n, CANON, torch.from_numpy(y_ref).to(cuda))).data
+    assert rel(xb.cpu().numpy(), x_ref) <= F64_TOL
+
+
+def test_dense_matrix_matches_oracle(cuda, oracle_mod):
+    for n in (1, 2, 3, 4, 8):
+        D = dense_transform(n, CANON).matrix.cpu().numpy()
+        Dref = oracle_mod.dense_transform(n, tup(CANON), ext=True)
+        assert np.abs(D - Dref).max() <= 1e-14, n
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_fast_f32(cuda, oracle_mod, n):
+    x = rand_batch(n, 33, seed=7)
+    y_ref = oracle_mod.forward_dense(n, tup(CANON), x)
+    plan = build_plan(n, CANON, precision="f32")
+    xt = torch.from_numpy(x).to(torch.complex64).to(cuda)
+    y = fast_apply(plan, SignalTensor(n, xt)).values
+    assert rel(y.cpu().numpy(), y_ref) <= F32_TOL
+    back = inverse_apply(plan, Spectrum(n, CANON, y)).data
+    assert rel(back.cpu().numpy(), x) <= F32_TOL
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_direct_f32(cuda, oracle_mod, n):
+    x = rand_batch(n, 130, seed=9)
+    y_ref = oracle_mod.forward_dense(n, tup(CANON), x)
+    dense = dense_transform(n, CANON, precision="f32")
+    xt = torch.from_numpy(x).to(torch.complex64).to(cuda)
+    y = naive_apply(dense, SignalTensor(n, xt)).values
+    assert rel(y.cpu().numpy(), y_ref) <= F32_TOL
+    back = inverse_apply(dense, Spectrum(n, CANON, y)).data
+    assert rel(back.cpu().numpy(), x) <= F32_TOL
+
+
+def test_reference_seeds_fast_vs_naive(cuda, oracle_mod):
+    # test_transform.cpp:138-151 (seeds 40+n) and acceptance #7 (seeds 700+16n+trial)
+    for n in (2, 4, 8):
+        plan = build_plan(n, CANON)
+        seeds = [40 + n] + [700 + 16 * n + trial for trial in range(10)]
+        x = np.stack([oracle_mod.random_signal(n, s) for s in seeds])
+        y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values.cpu().numpy()
+        y_ref = oracle_mod.forward_dense(n, tup(CANON), x)
+        assert np.abs(y - y_ref).max() / np.abs(y_ref).max() < 1e-10
+        assert rel(y, y_ref) <= F64_TOL
+
+
+def test_n16_fast_vs_orbit_route(cuda, oracle_mod):
+    n = 16
+    route = oracle_mod.OrbitRoute(n, tup(CANON))
+    x = rand_batch(n, 5, seed=16)
+    y_ref = route.forward(x)
+    plan = build_plan(n, CANON)
+    xt = torch.from_numpy(x).to(cuda)
+    y = fast_apply(plan, SignalTensor(n, xt)).values
+    assert rel(y.cpu().numpy(), y_ref) <= F64_TOL
+    xb = inverse_apply(plan, Spectrum(n, CANON, torch.from_numpy(y_ref).to(cuda))).data
+    assert rel(xb.cpu().numpy(), route.inverse(y_ref)) <= F64_TOL
+
+
+def test_n16_per_node_spot_check(cuda, oracle_mod):
+    # acceptance/main.cpp:368-388: seed 7016 signal, 64 nodes drawn by mt19937(777)
+    n = 16
+    x = oracle_mod.random_signal(n, 7016)
+    plan = build_plan(n, CANON)
+    q = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values.cpu().numpy()
+    rng = np.random.default_rng(777)
+    nodes = rng.integers(0, n**3, 64)
+    direct = oracle_mod.symmetrized_rows(n, tup(CANON), nodes, x)
+    assert np.abs(q[nodes] - direct).max() / np.abs(direct).max() <= 1e-9
+    assert rel(q[nodes], direct) <= F64_TOL
+
+
+def test_odd_and_unit_sizes_are_direct(cuda, oracle_mod):
+    for n in (1, 3, 5):
+        plan = build_plan(n, CANON)
+        assert plan.kind() == Kind.direct
+        x = rand_batch(n, 9, seed=n)
+        y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values.cpu().numpy()
+        y_ref = oracle_mod.forward_dense(n, tup(CANON), x)
+        assert rel(y, y_ref) <= F64_TOL
+        back = inverse_apply(plan, Spectrum(n, CANON, torch.from_numpy(y).to(cuda))).data.cpu().numpy()
+        assert rel(back, x) <= F64_TOL
+
+
+def test_mixed_radix_tree_with_dense_leaves(cuda, oracle_mod):
+    n = 6  # radix root, children of size 3 are direct (transform.cpp:385-386)
+    x = rand_batch(n, 11, seed=6)
+    plan = build_plan(n, CANON)
+    y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values.cpu().numpy()
+    y_ref = oracle_mod.forward_dense(n, tup(CANON), x)
+    assert rel(y, y_ref) <= F64_TOL
+    back = inverse_apply(plan, Spectrum(n, CANON, torch.from_numpy(y_ref).to(cuda))).data.cpu().numpy()
+    assert rel(back, oracle_mod.inverse_dense(n, tup(CANON), y_ref)) <= F64_TOL
+
+
+def test_radix_permutation_bit_exact(cuda, oracle_mod):
+    for n in (2, 4, 8, 16, 32, 64):
+        assert np.array_equal(radix_permutation(n), oracle_mod.radix_permutation(n))
+    p4 = radix_permutation(4)
+    assert p4[5 * 8 + 6] == (3 * 4 + 2) * 4 + 1  # test_transform.cpp:105-107
+    with pytest.raises(OddSize):
+        radix_permutation(3)
+    with pytest.raises(ValueError):
+        radix_permutation(0)
+
+
+def test_nodes_match_oracle_and_degeneracy(cuda, oracle_mod):
+    for n in (1, 2, 4, 8):
+        nodes = skew_nodes(n, CANON).cpu().numpy()
+        ref = oracle_mod.skew_nodes(n, tup(CANON))
+        assert np.abs(nodes - ref).max() <= 1e-14
+    with pytest.raises(DegenerateNodes):
+        skew_nodes(2, SkewParams(0.0, 0.0, 0.0))
+    with pytest.raises(DegenerateNodes):
+        build_plan(2, SkewParams(0.0, 0.0, 0.0))
+
+
+def test_factorization_residual_and_negative_control(cuda):
+    for n, p in [(2, CANON), (4, CANON), (8, CANON), (4, SkewParams(0.21, 0.055, 0.4)),
+                 (8, SkewParams(0.37, 0.61, 0.085))]:
+        plan = build_plan(n, p)
+        dense = dense_transform(n, p)
+        assert factorization_residual(plan, dense) < 1e-12
+    plan = build_plan(4, CANON)
+    dense = dense_transform(4, CANON)
+    broken = with_perturbed_basis(plan, 1e-3)
+    assert factorization_residual(broken, dense) > 1e-5  # test_transform.cpp:212-220
+
+
+def test_basis_export(cuda, oracle_mod):
+    plan = build_plan(4, CANON)
+    B = plan.basis()
+    assert B.nonZeros() == 245
+    ref = oracle_mod.RefPlan(4, tup(CANON)).basis_dense()
+    assert np.abs(B.to_dense() - ref).max() < 1e-11
+    assert np.abs(basis_change(4, CANON).to_dense() - B.to_dense()).max() == 0.0
+    K = plan.kernel()
+    assert np.abs(K - oracle_mod.dense_transform(2, tup(CANON))).max() < 1e-15
+    kids = plan.children()
+    assert [c[0] for c in kids] == [2] * 8
+    assert kids[5][1] == CANON.child(1, 0, 1)
+
+
+def test_size_and_params_errors(cuda):
+    plan = build_plan(2, CANON)
+    with pytest.raises(SizeMismatch):
+        fast_apply(plan, SignalTensor.zeros(4, device="cuda"))
+    q = Spectrum(4, CANON, torch.zeros(64, dtype=torch.complex128, device="cuda"))
+    with pytest.raises(SizeMismatch):
+        inverse_apply(plan, q)
+    dense = dense_transform(2, CANON)
+    with pytest.raises(SizeMismatch):
+        naive_apply(dense, SignalTensor.zeros(4, device="cuda"))
+    q2 = Spectrum(2, SkewParams(0.2, 0.1, 0.3), torch.zeros(8, dtype=torch.complex128, device="cuda"))
+    with pytest.raises(ValueError):
+        inverse_apply(plan, q2)
+    with pytest.raises(ValueError):
+        build_plan(0, CANON)
+
+
+def test_edge_batches_inplace_and_host_path(cuda, oracle_mod):
+    n = 8
+    plan = build_plan(n, CANON)
+    # empty batch
+    e = torch.zeros((0, n**3), dtype=torch.complex128, device=cuda)
+    assert fast_apply(plan, SignalTensor(n, e)).values.shape == (0, n**3)
+    # single block, host tensors (H2D + kernel + D2H through the C ABI)
+    x = oracle_mod.random_signal(n, 48)
+    yh = fast_apply(plan, SignalTensor(n, torch.from_numpy(x))).values
+    assert not yh.is_cuda
+    yd = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values.cpu()
+    assert torch.equal(yh, yd)
+    # determinism: bitwise identical across calls (transform.hpp:121-122)
+    xb = torch.from_numpy(rand_batch(n, 100, seed=3)).to(cuda)
+    a = fast_apply(plan, SignalTensor(n, xb)).values
+    b = fast_apply(plan, SignalTensor(n, xb)).values
+    assert torch.equal(a, b)
+
+
+def test_zero_and_delta_inputs(cuda):
+    n = 4
+    plan = build_plan(n, CANON)
+    z = torch.zeros((3, n**3), dtype=torch.complex128, device=cuda)
+    assert torch.count_nonzero(fast_apply(plan, SignalTensor(n, z)).values) == 0
+    # delta on (0,0,0) -> all-ones spectrum (test_transform.cpp:66-71)
+    d = torch.zeros(n**3, dtype=torch.complex128, device=cuda)
+    d[0] = 1.0
+    y = fast_apply(plan, SignalTensor(n, d)).values.cpu().numpy()
+    assert np.abs(y - 1.0).max() < 1e-14
+
+
+def test_dmma_fragment_layout(cuda):
+    import ctypes
+
+    from paper_1807_10058_b200 import _capi
+
+    A = torch.arange(32, dtype=torch.float64, device=cuda).reshape(8, 4) / 7.0
+    B = torch.arange(32, dtype=torch.float64, device=cuda).reshape(4, 8) / 3.0 - 2.0
+    C = torch.zeros(8, 8, dtype=torch.float64, device=cuda)
+    st = _capi.lib().fcct_debug_dmma_probe(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
+                                           ctypes.c_void_p(C.data_ptr()))
+    assert st == 0
+    torch.cuda.synchronize()
+    assert torch.allclose(C, A @ B, rtol=0, atol=1e-12)
+
+
+def test_large_batch_roundtrip_property(cuda):
+    # size-independent property at a large batch: inverse(forward(x)) == x
+    n = 8
+    plan = build_plan(n, CANON)
+    g = torch.Generator(device=cuda).manual_seed(5)
+    x = torch.complex(torch.rand((4096, n**3), generator=g, device=cuda, dtype=torch.float64) * 2 - 1,
+                      torch.rand((4096, n**3), generator=g, device=cuda, dtype=torch.float64) * 2 - 1)
+    y = fast_apply(plan, SignalTensor(n, x)).values
+    back = inverse_apply(plan, Spectrum(n, CANON, y)).data
+    assert (torch.linalg.norm(back - x) / torch.linalg.norm(x)).item() <= F64_TOL
+    # linearity: F(a x1 + b x2) = a F(x1) + b F(x2)
+    a, b = 0.3 - 0.2j, -1.7 + 0.5j
+    lhs = fast_apply(plan, SignalTensor(n, a * x[:64] + b * x[64:128])).values
+    rhs = a * y[:64] + b * y[64:128]
+    assert (torch.linalg.norm(lhs - rhs) / torch.linalg.norm(rhs)).item() <= 1e-14
