@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -16,6 +17,7 @@
 #include "../../include/fcct_gpu.h"
 #include "kernels.hpp"
 #include "plan.hpp"
+#include "tiling.hpp"
 
 namespace fcct {
 
@@ -91,6 +93,44 @@ struct PipelineTables {
     PipelineDesc desc{};
     std::vector<std::shared_ptr<DevBuf>> bufs;
 };
+
+struct Pipeline2Tables {
+    Pipeline2Desc desc{};
+    std::vector<std::shared_ptr<DevBuf>> bufs;
+    int64_t dmma_per_tile = 0;
+};
+
+void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
+    out.desc = Pipeline2Desc{};
+    out.desc.N = h.N;
+    out.desc.stride = h.stride;
+    out.desc.nstages = static_cast<int>(h.stages.size());
+    out.dmma_per_tile = h.dmma_per_tile;
+    if (out.desc.nstages > kMaxStages) throw FcctError(ST_INVALID_ARGUMENT, "too many stages");
+    for (size_t s = 0; s < h.stages.size(); ++s) {
+        const Stage2Host& st = h.stages[s];
+        Stage2Dev& d = out.desc.st[s];
+        d = Stage2Dev{};
+        d.kind = st.kind;
+        auto keep = [&](std::shared_ptr<DevBuf> b) {
+            out.bufs.push_back(b);
+            return b->ptr;
+        };
+        d.n_units = st.n_units;
+        d.warp_units = static_cast<const int*>(keep(upload(st.warp_units)));
+        d.u_out = static_cast<const int*>(keep(upload(st.u_out)));
+        if (st.kind == 0) {
+            d.w_base = static_cast<const int*>(keep(upload(st.w_base)));
+            d.w_count = static_cast<const int*>(keep(upload(st.w_count)));
+            d.e_slots = static_cast<const int4*>(keep(upload(st.e_slots)));
+            d.e_frag = static_cast<const double2*>(keep(upload(st.e_frag)));
+        } else {
+            d.u_node = static_cast<const int*>(keep(upload(st.u_node)));
+            d.u_in = static_cast<const int*>(keep(upload(st.u_in)));
+            d.K = static_cast<const double2*>(keep(upload(st.K)));
+        }
+    }
+}
 
 // ELL packing of a sparse stage for row groups of RG rows.
 template <typename R>
@@ -276,6 +316,8 @@ struct fcct_plan_s {
     bool radix = false;
     std::shared_ptr<const PlanNode> tree;
     PipelineTables fwd, inv;
+    bool v2 = false;  // fp64 DMMA pipeline (tiling.hpp)
+    Pipeline2Tables fwd2, inv2;
     std::shared_ptr<DevBuf> Wt_fwd, Wt_inv;
     std::vector<std::shared_ptr<DevBuf>> extra;
     fcct_plan_info_t info{};
@@ -326,6 +368,18 @@ void build_direct(fcct_plan_s* pl) {
     pl->info.table_bytes = static_cast<int64_t>(2 * wbytes);
 }
 
+void build_v2(fcct_plan_s* pl) {
+    pl->v2 = false;
+    const char* force = std::getenv("FCCT_PIPELINE");
+    if (force && std::string(force) == "v1") return;
+    if (pl->precision != FCCT_F64) return;
+    Pipeline2Host hf, hi;
+    if (!compile_pipeline2(*pl->tree, false, hf) || !compile_pipeline2(*pl->tree, true, hi)) return;
+    upload_pipeline2(hf, pl->fwd2);
+    upload_pipeline2(hi, pl->inv2);
+    pl->v2 = true;
+}
+
 void fill_info(fcct_plan_s* pl) {
     fcct_plan_info_t& in = pl->info;
     in.n = pl->n;
@@ -347,6 +401,8 @@ void fill_info(fcct_plan_s* pl) {
         in.condition = pl->tree->condition;
         int64_t bytes = 0;
         for (auto* pt : {&pl->fwd, &pl->inv})
+            for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+        for (auto* pt : {&pl->fwd2, &pl->inv2})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         in.table_bytes = bytes;
     } else {
@@ -382,6 +438,7 @@ fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int 
         else
             build_pipelines<double>(*pl->tree, tb, pl->fwd, pl->inv);
         pl->radix = true;
+        build_v2(pl.get());
     } else {
         check_nodes(n, p);
         pl->radix = false;
@@ -399,8 +456,12 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
     DeviceGuard guard(pl->device);
     const bool f32 = pl->precision == FCCT_F32;
     if (pl->radix) {
-        ck(launch_pipeline(inverse ? pl->inv.desc : pl->fwd.desc, f32, in, out, batch, st, pl->num_sms),
-           "fast pipeline");
+        if (pl->v2)
+            ck(launch_pipeline2(inverse ? pl->inv2.desc : pl->fwd2.desc, in, out, batch, st, pl->num_sms),
+               "fast pipeline v2");
+        else
+            ck(launch_pipeline(inverse ? pl->inv.desc : pl->fwd.desc, f32, in, out, batch, st, pl->num_sms),
+               "fast pipeline");
         return;
     }
     const int64_t N = cube(pl->n);
@@ -667,6 +728,7 @@ fcct_status fcct_plan_perturbed_basis(fcct_plan plan, double delta, fcct_plan* o
             build_pipelines<float>(*root, tb, pl->fwd, pl->inv);
         else
             build_pipelines<double>(*root, tb, pl->fwd, pl->inv);
+        build_v2(pl.get());
         pl->method = FCCT_FAST;
         fill_info(pl.get());
         *out = pl.release();
@@ -729,6 +791,128 @@ fcct_status fcct_plan_tree_stats(int n, double r, double s, double t, int64_t* t
         if (tree_nnz_inv) *tree_nnz_inv = tree_nnz(*root, true, false);
         if (flops_fwd) *flops_fwd = algorithmic_flops(*root, false);
         if (flops_inv) *flops_inv = algorithmic_flops(*root, true);
+    });
+}
+
+// Host emulation of the v2 DMMA pipeline tables (no GPU): applies the
+// compiled stages to `batch` blocks exactly as the kernel indexes them
+// (slots, lane-ordered fragments, unit lists). Tests the plan compiler on CPU.
+fcct_status fcct_debug_emulate_v2(int n, double r, double s, double t, int inverse, const double* in, double* out,
+                                  int64_t batch) {
+    return guarded([&] {
+        auto root = build_tree(n, Params{r, s, t});
+        Pipeline2Host h;
+        if (!compile_pipeline2(*root, inverse != 0, h))
+            throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by pipeline v2");
+        const int N = h.N;
+        std::vector<double> X(static_cast<size_t>(2) * N), Y(static_cast<size_t>(2) * N);
+        for (int64_t b = 0; b < batch; ++b) {
+            std::copy(in + 2 * N * b, in + 2 * N * (b + 1), X.begin());
+            for (const auto& st : h.stages) {
+                std::fill(Y.begin(), Y.end(), 0.0);
+                for (int w = 0; w < kWarps2; ++w)
+                    for (int j = 0; j < kUnits2; ++j) {
+                        const int u = st.warp_units[w * kUnits2 + j];
+                        if (u < 0) continue;
+                        double acc[8][2] = {};  // [n][part]
+                        auto apply = [&](const int slot[4], const double frag[64]) {
+                            for (int nn = 0; nn < 8; ++nn)
+                                for (int k = 0; k < 4; ++k) {
+                                    const int lane = nn * 4 + k;
+                                    const double tr = frag[2 * lane], ti = frag[2 * lane + 1];
+                                    const double xr = X[2 * slot[k]], xi = X[2 * slot[k] + 1];
+                                    acc[nn][0] += tr * xr - ti * xi;
+                                    acc[nn][1] += tr * xi + ti * xr;
+                                }
+                        };
+                        if (st.kind == 0) {
+                            int e0 = st.w_base[w];
+                            for (int jj = 0; jj < j; ++jj) e0 += st.w_count[w * kUnits2 + jj];
+                            const int cnt = st.w_count[w * kUnits2 + j];
+                            for (int e = e0; e < e0 + cnt; ++e) {
+                                int sl[4];
+                                for (int k = 0; k < 4; ++k) sl[k] = st.e_slots[4 * e + k] & ~(1 << 30);
+                                apply(sl, &st.e_frag[64 * e]);
+                            }
+                        } else {
+                            const int q = st.u_node[u];
+                            for (int kt = 0; kt < 2; ++kt) {
+                                int slot[4];
+                                double frag[64];
+                                for (int k = 0; k < 4; ++k) slot[k] = st.u_in[u * 8 + kt * 4 + k];
+                                for (int nn = 0; nn < 8; ++nn)
+                                    for (int k = 0; k < 4; ++k) {
+                                        frag[2 * (nn * 4 + k)] = st.K[2 * (q * 64 + nn * 8 + kt * 4 + k)];
+                                        frag[2 * (nn * 4 + k) + 1] = st.K[2 * (q * 64 + nn * 8 + kt * 4 + k) + 1];
+                                    }
+                                apply(slot, frag);
+                            }
+                        }
+                        for (int nn = 0; nn < 8; ++nn) {
+                            const int o = st.u_out[u * 8 + nn];
+                            Y[2 * o] = acc[nn][0];
+                            Y[2 * o + 1] = acc[nn][1];
+                        }
+                    }
+                std::swap(X, Y);
+            }
+            std::copy(X.begin(), X.end(), out + 2 * N * b);
+        }
+    });
+}
+
+// Bank-conflict statistics of the compiled v2 tables (host, no GPU): number of
+// 16-lane half-warp load / store requests that hit a bank twice.
+fcct_status fcct_debug_v2_stats(int n, double r, double s, double t, int inverse, int64_t* stats /* 6 */) {
+    return guarded([&] {
+        auto root = build_tree(n, Params{r, s, t});
+        Pipeline2Host h;
+        if (!compile_pipeline2(*root, inverse != 0, h))
+            throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by pipeline v2");
+        int64_t ld_req = 0, ld_conf = 0, st_req = 0, st_conf = 0;
+        const int stride = h.stride;
+        auto conflicted = [&](const int slots[4], bool store) {
+            // half-warp lanes 0-15: r = l/4 -> (t_sub, part), k = l%4
+            for (int half = 0; half < 2; ++half) {
+                bool used[16] = {};
+                bool conf = false;
+                for (int l = 16 * half; l < 16 * half + 16; ++l) {
+                    const int rr = l >> 2, k = l & 3, tsub = rr >> 1, part = rr & 1;
+                    const int slot = store ? slots[k] : slots[k];
+                    const int bank = ((tsub * stride + 2 * slot + part) % 16 + 16) % 16;
+                    if (used[bank]) conf = true;
+                    used[bank] = true;
+                }
+                (store ? st_conf : ld_conf) += conf;
+                (store ? st_req : ld_req) += 1;
+            }
+        };
+        for (const auto& st : h.stages)
+            for (int u = 0; u < st.n_units; ++u) {
+                if (st.kind == 0) {
+                    (void)u;
+                } else {
+                    for (int kt = 0; kt < 2; ++kt) conflicted(&st.u_in[u * 8 + kt * 4], false);
+                }
+                for (int par = 0; par < 2; ++par) {
+                    int sl[4];
+                    for (int k = 0; k < 4; ++k) sl[k] = st.u_out[u * 8 + 2 * k + par];
+                    conflicted(sl, true);
+                }
+            }
+        for (const auto& st : h.stages)
+            if (st.kind == 0)
+                for (size_t e = 0; e < st.e_slots.size() / 4; ++e) {
+                    int sl[4];
+                    for (int k = 0; k < 4; ++k) sl[k] = st.e_slots[4 * e + k] & ~(1 << 30);
+                    conflicted(sl, false);
+                }
+        stats[0] = ld_req;
+        stats[1] = ld_conf;
+        stats[2] = st_req;
+        stats[3] = st_conf;
+        stats[4] = h.dmma_per_tile;
+        stats[5] = static_cast<int64_t>(h.stages.size());
     });
 }
 

@@ -221,6 +221,221 @@ cudaError_t launch_pipeline(const PipelineDesc& d, bool f32, const void* in, voi
 }
 
 // ===========================================================================
+// Fast pipeline v2: every stage on the FP64 tensor pipe (DMMA m8n8k4), see
+// tiling.hpp. smem X[t][slot][part], 16 blocks, row stride 2N + 8 doubles.
+// Lane l: data row r = l/4 -> (t_sub = r/2, part = r%2), k = l%4.
+//   A fragment (data, 8 x 4): X[t = 4 mt + t_sub][slot_k][part]
+//   B fragment (table, 4 x 8): T[k][n = l/4], (Re, Im)
+//   C fragment (8 x 8):        rows r, outputs n = 2k, 2k+1
+// ===========================================================================
+namespace {
+
+constexpr int kThreads2 = 512;
+constexpr int kU2 = 4;  // units per warp
+
+__device__ __forceinline__ int pick4(const int4 v, int k) {
+    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+
+__device__ __forceinline__ double flip_unless(double v, int part) {
+    // part == 0 (re rows of the swapped operand): -x_im; part == 1: +x_re
+    return __hiloint2double(__double2hiint(v) ^ (part ? 0 : static_cast<int>(0x80000000u)), __double2loint(v));
+}
+
+constexpr int kRing = 4;                   // sparse entries in flight per warp
+constexpr int kRingBytesPerWarp = kRing * 1024;  // per entry: 32 x 16 B fragment + 32 x 16 B slots
+
+__device__ __forceinline__ void cp_async16_ca(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void store_unit(double* X, int stride, int t_sub, int part, int o0, int o1,
+                                           const double (&acc)[4][2]) {
+    double* Xw = X + t_sub * stride + part;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+        Xw[(4 * mt) * stride + 2 * o0] = acc[mt][0];
+        Xw[(4 * mt) * stride + 2 * o1] = acc[mt][1];
+    }
+}
+
+__device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int stride, int warp, int lane,
+                                       unsigned char* ring) {
+    const int r = lane >> 2, k = lane & 3;
+    const int t_sub = r >> 1, part = r & 1;
+    const int n_out = lane >> 2;
+    double acc[kU2][4][2];
+    int o0[kU2], o1[kU2];
+    const double* Xr = X + t_sub * stride + part;        // + 4 mt stride + 2 slot
+    const double* Xs = X + t_sub * stride + (1 - part);  // part-swapped
+    int units[kU2];
+#pragma unroll
+    for (int j = 0; j < kU2; ++j) {
+        units[j] = __ldg(sd.warp_units + warp * kU2 + j);
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) acc[j][mt][0] = acc[j][mt][1] = 0.0;
+        o0[j] = o1[j] = -1;
+    }
+    if (sd.kind == 0) {
+        // per-warp cp.async ring over this warp's entry stream (tiling.hpp)
+        double2* rf = reinterpret_cast<double2*>(ring + warp * kRingBytesPerWarp);
+        int4* rs = reinterpret_cast<int4*>(ring + warp * kRingBytesPerWarp + kRing * 512);
+        const int base = __ldg(sd.w_base + warp);
+        const int total = __ldg(sd.w_base + warp + 1) - base;
+        auto issue = [&](int f) {
+            if (f < total) {
+                cp_async16(rf + (f & (kRing - 1)) * 32 + lane, sd.e_frag + static_cast<size_t>(base + f) * 32 + lane,
+                           true);
+                cp_async16_ca(rs + (f & (kRing - 1)) * 32 + lane, sd.e_slots + base + f);
+            }
+            cp_async_commit();
+        };
+#pragma unroll
+        for (int i = 0; i < kRing - 1; ++i) issue(i);
+        int f = 0;
+#pragma unroll
+        for (int j = 0; j < kU2; ++j) {
+            const int cnt = __ldg(sd.w_count + warp * kU2 + j);
+            for (int e = 0; e < cnt; ++e, ++f) {
+                issue(f + kRing - 1);
+                cp_async_wait<kRing - 1>();
+                const double2 frag = rf[(f & (kRing - 1)) * 32 + lane];
+                const int4 sl = rs[(f & (kRing - 1)) * 32 + lane];
+                const int cplx = (sl.x >> 30) & 1;
+                const int slot = pick4(sl, k) & ~(1 << 30);
+                double a[4];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) a[mt] = Xr[(4 * mt) * stride + 2 * slot];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], frag.x);
+                if (cplx) {
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) a[mt] = flip_unless(Xs[(4 * mt) * stride + 2 * slot], part);
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], frag.y);
+                }
+            }
+            if (units[j] >= 0) {
+                o0[j] = __ldg(sd.u_out + units[j] * 8 + 2 * k);
+                o1[j] = __ldg(sd.u_out + units[j] * 8 + 2 * k + 1);
+            }
+        }
+        cp_async_wait<0>();
+    } else {
+        // K fragments of the next unit are prefetched into registers
+        double2 kf[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+        int ks[2] = {0, 0};
+        auto fetch = [&](int u, double2 (&f)[2], int (&sl)[2]) {
+            if (u < 0) return;
+            const double2* Kq = sd.K + __ldg(sd.u_node + u) * 64;
+#pragma unroll
+            for (int kt = 0; kt < 2; ++kt) {
+                sl[kt] = __ldg(sd.u_in + u * 8 + kt * 4 + k);
+                f[kt] = __ldg(Kq + n_out * 8 + kt * 4 + k);  // K[b = n][g]
+            }
+        };
+        fetch(units[0], kf, ks);
+#pragma unroll
+        for (int j = 0; j < kU2; ++j) {
+            double2 nf[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+            int ns[2] = {0, 0};
+            if (j + 1 < kU2) fetch(units[j + 1], nf, ns);
+            if (units[j] >= 0) {
+#pragma unroll
+                for (int kt = 0; kt < 2; ++kt) {
+                    double a[4], as[4];
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) {
+                        a[mt] = Xr[(4 * mt) * stride + 2 * ks[kt]];
+                        as[mt] = flip_unless(Xs[(4 * mt) * stride + 2 * ks[kt]], part);
+                    }
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], kf[kt].x);
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], as[mt], kf[kt].y);
+                }
+                o0[j] = __ldg(sd.u_out + units[j] * 8 + 2 * k);
+                o1[j] = __ldg(sd.u_out + units[j] * 8 + 2 * k + 1);
+            }
+            kf[0] = nf[0];
+            kf[1] = nf[1];
+            ks[0] = ns[0];
+            ks[1] = ns[1];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kU2; ++j)
+        if (o0[j] >= 0) store_unit(X, stride, t_sub, part, o0[j], o1[j], acc[j]);
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads2, 1)
+    pipeline2_kernel(const __grid_constant__ Pipeline2Desc d, const double* __restrict__ in, double* __restrict__ out,
+                     int64_t batch) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    double* X = reinterpret_cast<double*>(smem_raw + 128);
+    const int stride = d.stride;
+    unsigned char* ring = smem_raw + 128 + static_cast<size_t>(16) * stride * sizeof(double);
+    const int dimr = 2 * d.N;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    constexpr int TB = 16;
+    const int64_t ntiles = (batch + TB - 1) / TB;
+    const uint32_t row_bytes = static_cast<uint32_t>(dimr * sizeof(double));
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t t0 = tile * TB;
+        const int nvalid = static_cast<int>(batch - t0 < TB ? batch - t0 : TB);
+        if (threadIdx.x == 0) {
+            tma_store_wait_read0();
+            mbar_arrive_expect_tx(bar, row_bytes * nvalid);
+            for (int t = 0; t < nvalid; ++t) tma_load_1d(X + t * stride, in + (t0 + t) * dimr, row_bytes, bar);
+            const int64_t nt = tile + gridDim.x;
+            if (nt < ntiles) {
+                const int64_t n0 = nt * TB;
+                const int nv = static_cast<int>(batch - n0 < TB ? batch - n0 : TB);
+                prefetch_l2_bulk(in + n0 * dimr, row_bytes * nv);
+            }
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        for (int s = 0; s < d.nstages; ++s) stage2(d.st[s], X, stride, warp, lane, ring);
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int t = 0; t < nvalid; ++t) tma_store_1d(out + (t0 + t) * dimr, X + t * stride, row_bytes);
+            tma_store_commit();
+        }
+    }
+    if (threadIdx.x == 0) tma_store_wait0();
+}
+
+}  // namespace
+
+cudaError_t launch_pipeline2(const Pipeline2Desc& d, const void* in, void* out, int64_t batch, cudaStream_t st,
+                             int num_sms) {
+    if (batch <= 0) return cudaSuccess;
+    const int smem = 128 + 16 * d.stride * static_cast<int>(sizeof(double)) + 16 * kRingBytesPerWarp;
+    cudaError_t e = cudaFuncSetAttribute(pipeline2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pipeline2_kernel, kThreads2, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int64_t ntiles = (batch + 15) / 16;
+    const int64_t grid = std::min<int64_t>(ntiles, static_cast<int64_t>(per_sm) * num_sms);
+    pipeline2_kernel<<<static_cast<unsigned>(grid), kThreads2, smem, st>>>(d, static_cast<const double*>(in),
+                                                                            static_cast<double*>(out), batch);
+    return cudaGetLastError();
+}
+
+// ===========================================================================
 // Direct transform GEMMs (real form: C[M][Nn] = A[M][K] * Wt[Nn][K]^T)
 // ===========================================================================
 namespace {

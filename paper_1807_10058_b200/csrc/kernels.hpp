@@ -37,6 +37,31 @@ struct PipelineDesc {
     StageDesc stage[kMaxStages];
 };
 
+// Pipeline v2 (fp64, n <= 8): every stage on the FP64 tensor pipe, see tiling.hpp.
+struct Stage2Dev {
+    int kind;  // 0 sparse tiles, 1 mix
+    int n_units;
+    const int* warp_units;  // [16][4]
+    const int* u_out;       // [units][8]
+    const int* w_base;      // sparse: [17] warp-major entry ranges
+    const int* w_count;     // sparse: [16][4] entries per unit
+    const int4* e_slots;    // sparse: [entries] input slots of the 4 k-columns (bit 30 of .x: complex)
+    const double2* e_frag;  // sparse: [entries][32] (Re, Im) of T[k][n], lane order
+    const int* u_node;      // mix
+    const int* u_in;        // mix: [units][8]
+    const double2* K;       // mix: [nodes][8][8]
+};
+
+struct Pipeline2Desc {
+    int N;
+    int stride;  // doubles per block row in shared memory
+    int nstages;
+    Stage2Dev st[kMaxStages];
+};
+
+cudaError_t launch_pipeline2(const Pipeline2Desc& d, const void* in, void* out, int64_t batch, cudaStream_t stream,
+                             int num_sms);
+
 // Fast transform pipeline (forward or inverse, decided by the stage list).
 cudaError_t launch_pipeline(const PipelineDesc& d, bool f32, const void* in, void* out, int64_t batch,
                             cudaStream_t stream, int num_sms);
