@@ -105,6 +105,17 @@ void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
     out.desc.N = h.N;
     out.desc.stride = h.stride;
     out.desc.nstages = static_cast<int>(h.stages.size());
+    const char* ds = std::getenv("FCCT_DIRECT_STORE");
+    out.desc.direct_store = ds ? std::atoi(ds) : 0;
+    const char* sm = std::getenv("FCCT_DEBUG_STAGE_MASK");  // timing experiments only
+    out.desc.stage_mask = sm ? std::atoi(sm) : -1;
+    out.desc.timing = nullptr;
+    if (std::getenv("FCCT_DEBUG_TIMING")) {  // per-stage clock64 totals of CTA 0 (profiling aid)
+        auto b = std::make_shared<DevBuf>(sizeof(unsigned long long) * (kMaxStages + 2));
+        ck(cudaMemset(b->ptr, 0, b->bytes), "memset");
+        out.desc.timing = static_cast<unsigned long long*>(b->ptr);
+        out.bufs.push_back(b);
+    }
     out.dmma_per_tile = h.dmma_per_tile;
     if (out.desc.nstages > kMaxStages) throw FcctError(ST_INVALID_ARGUMENT, "too many stages");
     for (size_t s = 0; s < h.stages.size(); ++s) {
@@ -122,8 +133,10 @@ void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
         if (st.kind == 0) {
             d.w_base = static_cast<const int*>(keep(upload(st.w_base)));
             d.w_count = static_cast<const int*>(keep(upload(st.w_count)));
+            d.w_cplx = static_cast<const unsigned*>(keep(upload(st.w_cplx)));
             d.e_slots = static_cast<const int4*>(keep(upload(st.e_slots)));
-            d.e_frag = static_cast<const double2*>(keep(upload(st.e_frag)));
+            d.e_re = static_cast<const double*>(keep(upload(st.e_re)));
+            d.e_im = static_cast<const double*>(keep(upload(st.e_im)));
         } else {
             d.u_node = static_cast<const int*>(keep(upload(st.u_node)));
             d.u_in = static_cast<const int*>(keep(upload(st.u_in)));
@@ -832,7 +845,12 @@ fcct_status fcct_debug_emulate_v2(int n, double r, double s, double t, int inver
                             for (int e = e0; e < e0 + cnt; ++e) {
                                 int sl[4];
                                 for (int k = 0; k < 4; ++k) sl[k] = st.e_slots[4 * e + k] & ~(1 << 30);
-                                apply(sl, &st.e_frag[64 * e]);
+                                double fr[64];
+                                for (int l = 0; l < 32; ++l) {
+                                    fr[2 * l] = st.e_re[32 * e + l];
+                                    fr[2 * l + 1] = st.e_im[32 * e + l];
+                                }
+                                apply(sl, fr);
                             }
                         } else {
                             const int q = st.u_node[u];
@@ -913,6 +931,19 @@ fcct_status fcct_debug_v2_stats(int n, double r, double s, double t, int inverse
         stats[3] = st_conf;
         stats[4] = h.dmma_per_tile;
         stats[5] = static_cast<int64_t>(h.stages.size());
+    });
+}
+
+// Profiling aid: per-phase clock64 totals of CTA 0 from the last launch of a
+// plan created with FCCT_DEBUG_TIMING set (index 0 = tile load wait,
+// 1 + s = stage s). Returns the number of stages.
+fcct_status fcct_debug_timing(fcct_plan plan, int inverse, unsigned long long* out, int* nstages) {
+    return guarded([&] {
+        if (!plan || !plan->v2) throw FcctError(ST_INVALID_ARGUMENT, "plan has no v2 pipeline");
+        const auto& t = inverse ? plan->inv2 : plan->fwd2;
+        if (!t.desc.timing) throw FcctError(ST_INVALID_ARGUMENT, "FCCT_DEBUG_TIMING was not set at plan creation");
+        ck(cudaMemcpy(out, t.desc.timing, sizeof(unsigned long long) * (kMaxStages + 2), cudaMemcpyDeviceToHost), "D2H");
+        *nstages = t.desc.nstages;
     });
 }
 

@@ -233,8 +233,36 @@ namespace {
 constexpr int kThreads2 = 512;
 constexpr int kU2 = 4;  // units per warp
 
-__device__ __forceinline__ int pick4(const int4 v, int k) {
-    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+// Loads the (re, im) pair of one block at one slot (16 B, both data parts);
+// lanes of the two parts read the same address (broadcast).
+__device__ __forceinline__ double2 lds_pair(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+
+// part 0 lane: (a = re, as = -im); part 1 lane: (a = im, as = +re)
+__device__ __forceinline__ void split_pair(const double2 v, int part, double& a, double& as) {
+    if (part) {
+        a = v.y;
+        as = v.x;
+    } else {
+        a = v.x;
+        as = -v.y;
+    }
+}
+
+// Loads a double and flips its sign bit with `sign` (0 or 0x80000000).
+__device__ __forceinline__ double lds_f64_xor_hi(uint32_t addr, uint32_t sign) {
+    uint32_t lo, hi;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(lo), "=r"(hi) : "r"(addr) : "memory");
+    return __hiloint2double(static_cast<int>(hi ^ sign), static_cast<int>(lo));
 }
 
 __device__ __forceinline__ double flip_unless(double v, int part) {
@@ -242,11 +270,15 @@ __device__ __forceinline__ double flip_unless(double v, int part) {
     return __hiloint2double(__double2hiint(v) ^ (part ? 0 : static_cast<int>(0x80000000u)), __double2loint(v));
 }
 
-constexpr int kRing = 4;                   // sparse entries in flight per warp
-constexpr int kRingBytesPerWarp = kRing * 1024;  // per entry: 32 x 16 B fragment + 32 x 16 B slots
+constexpr int kRing = 8;                        // sparse entries in flight per warp
+constexpr int kRingBytesPerWarp = kRing * 640;  // per entry: 32 x (8 B Re + 8 B Im) + 32 x 4 B slot
 
-__device__ __forceinline__ void cp_async16_ca(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async8_ca(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async4_ca(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
 __device__ __forceinline__ void store_unit(double* X, int stride, int t_sub, int part, int o0, int o1,
@@ -259,8 +291,59 @@ __device__ __forceinline__ void store_unit(double* X, int stride, int t_sub, int
     }
 }
 
-__device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int stride, int warp, int lane,
-                                       unsigned char* ring) {
+// Output sink of the last stage: global rows of the tile (natural layout).
+struct TileOut {
+    double* out;  // nullptr: write back into shared memory
+    int64_t t0;
+    int nvalid;
+    int dimr;
+};
+
+__device__ __forceinline__ void store_unit_global(const TileOut& to, int t_sub, int part, int o0, int o1,
+                                                  const double (&acc)[4][2]) {
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+        const int t = 4 * mt + t_sub;
+        if (t < to.nvalid) {
+            double* row = to.out + (to.t0 + t) * to.dimr + part;
+            row[2 * o0] = acc[mt][0];
+            row[2 * o1] = acc[mt][1];
+        }
+    }
+}
+
+// Issued by thread 0 between the compute and the store phase of the last
+// stage: the shared tile is free, so the next tile's bulk load overlaps the
+// global stores of this one.
+struct NextLoad {
+    const double* in;
+    uint64_t* bar;
+    double* X;
+    int stride;
+    int dimr;
+    int64_t tile;  // next tile index (< 0: none)
+    int64_t batch;
+    int64_t after; // tile after next (L2 prefetch), < 0: none
+};
+
+__device__ __forceinline__ void issue_tile_load(const NextLoad& nl) {
+    constexpr int TB = 16;
+    const uint32_t row_bytes = static_cast<uint32_t>(nl.dimr * sizeof(double));
+    if (nl.tile >= 0) {
+        const int64_t t0 = nl.tile * TB;
+        const int nv = static_cast<int>(nl.batch - t0 < TB ? nl.batch - t0 : TB);
+        mbar_arrive_expect_tx(nl.bar, row_bytes * nv);
+        for (int t = 0; t < nv; ++t) tma_load_1d(nl.X + t * nl.stride, nl.in + (t0 + t) * nl.dimr, row_bytes, nl.bar);
+    }
+    if (nl.after >= 0) {
+        const int64_t a0 = nl.after * TB;
+        const int nv = static_cast<int>(nl.batch - a0 < TB ? nl.batch - a0 : TB);
+        prefetch_l2_bulk(nl.in + a0 * nl.dimr, row_bytes * nv);
+    }
+}
+
+__device__ __forceinline__ void stage2(const Stage2Dev sd, double* X, int stride, int warp, int lane,
+                                       unsigned char* ring, const TileOut& to, const NextLoad& nl) {
     const int r = lane >> 2, k = lane & 3;
     const int t_sub = r >> 1, part = r & 1;
     const int n_out = lane >> 2;
@@ -277,50 +360,67 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
         o0[j] = o1[j] = -1;
     }
     if (sd.kind == 0) {
-        // per-warp cp.async ring over this warp's entry stream (tiling.hpp)
-        double2* rf = reinterpret_cast<double2*>(ring + warp * kRingBytesPerWarp);
-        int4* rs = reinterpret_cast<int4*>(ring + warp * kRingBytesPerWarp + kRing * 512);
+        // This warp's entry stream (tiling.hpp) with a 2-deep register prefetch
+        // of (Re, Im, slot): every descriptor field is hoisted out of the loop
+        // and shared memory is addressed through 32-bit shared-window offsets.
         const int base = __ldg(sd.w_base + warp);
         const int total = __ldg(sd.w_base + warp + 1) - base;
-        auto issue = [&](int f) {
-            if (f < total) {
-                cp_async16(rf + (f & (kRing - 1)) * 32 + lane, sd.e_frag + static_cast<size_t>(base + f) * 32 + lane,
-                           true);
-                cp_async16_ca(rs + (f & (kRing - 1)) * 32 + lane, sd.e_slots + base + f);
-            }
-            cp_async_commit();
-        };
+        const double* __restrict__ pre = sd.e_re + static_cast<size_t>(base) * 32 + lane;
+        const double* __restrict__ pim = sd.e_im + static_cast<size_t>(base) * 32 + lane;
+        const int* __restrict__ psl = reinterpret_cast<const int*>(sd.e_slots) + static_cast<size_t>(base) * 4 + k;
+        const uint32_t xr = smem_u32(Xr), xs = smem_u32(Xs);
+        const uint32_t mstep = static_cast<uint32_t>(4 * stride * sizeof(double));
+        const uint32_t sign = part ? 0u : 0x80000000u;
+        int cnt[kU2];
 #pragma unroll
-        for (int i = 0; i < kRing - 1; ++i) issue(i);
+        for (int j = 0; j < kU2; ++j) cnt[j] = __ldg(sd.w_count + warp * kU2 + j);
+        double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0;
+        int sl0 = 0, sl1 = 0;
+        if (total > 0) {
+            re0 = __ldg(pre);
+            im0 = __ldg(pim);
+            sl0 = __ldg(psl);
+        }
+        if (total > 1) {
+            re1 = __ldg(pre + 32);
+            im1 = __ldg(pim + 32);
+            sl1 = __ldg(psl + 4);
+        }
         int f = 0;
 #pragma unroll
         for (int j = 0; j < kU2; ++j) {
-            const int cnt = __ldg(sd.w_count + warp * kU2 + j);
-            for (int e = 0; e < cnt; ++e, ++f) {
-                issue(f + kRing - 1);
-                cp_async_wait<kRing - 1>();
-                const double2 frag = rf[(f & (kRing - 1)) * 32 + lane];
-                const int4 sl = rs[(f & (kRing - 1)) * 32 + lane];
-                const int cplx = (sl.x >> 30) & 1;
-                const int slot = pick4(sl, k) & ~(1 << 30);
+            for (int e = 0; e < cnt[j]; ++e, ++f) {
+                double re2 = 0.0, im2 = 0.0;
+                int sl2 = 0;
+                if (f + 2 < total) {
+                    re2 = __ldg(pre + (f + 2) * 32);
+                    im2 = __ldg(pim + (f + 2) * 32);
+                    sl2 = __ldg(psl + (f + 2) * 4);
+                }
+                const uint32_t off = static_cast<uint32_t>(sl0 & ~(1 << 30)) * 16u;
                 double a[4];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) a[mt] = Xr[(4 * mt) * stride + 2 * slot];
+                for (int mt = 0; mt < 4; ++mt) a[mt] = lds_f64(xr + off + mt * mstep);
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], frag.x);
-                if (cplx) {
+                for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], re0);
+                if ((sl0 >> 30) & 1) {
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) a[mt] = flip_unless(Xs[(4 * mt) * stride + 2 * slot], part);
+                    for (int mt = 0; mt < 4; ++mt) a[mt] = lds_f64_xor_hi(xs + off + mt * mstep, sign);
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], frag.y);
+                    for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], im0);
                 }
+                re0 = re1;
+                im0 = im1;
+                sl0 = sl1;
+                re1 = re2;
+                im1 = im2;
+                sl1 = sl2;
             }
             if (units[j] >= 0) {
                 o0[j] = __ldg(sd.u_out + units[j] * 8 + 2 * k);
                 o1[j] = __ldg(sd.u_out + units[j] * 8 + 2 * k + 1);
             }
         }
-        cp_async_wait<0>();
     } else {
         // K fragments of the next unit are prefetched into registers
         double2 kf[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
@@ -344,11 +444,11 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
 #pragma unroll
                 for (int kt = 0; kt < 2; ++kt) {
                     double a[4], as[4];
+                    const uint32_t xq = smem_u32(X + t_sub * stride + 2 * ks[kt]);
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) {
-                        a[mt] = Xr[(4 * mt) * stride + 2 * ks[kt]];
-                        as[mt] = flip_unless(Xs[(4 * mt) * stride + 2 * ks[kt]], part);
-                    }
+                    for (int mt = 0; mt < 4; ++mt)
+                        split_pair(lds_pair(xq + mt * static_cast<uint32_t>(4 * stride * sizeof(double))), part, a[mt],
+                                   as[mt]);
 #pragma unroll
                     for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], kf[kt].x);
 #pragma unroll
@@ -364,6 +464,16 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
         }
     }
     __syncthreads();
+    if (to.out != nullptr) {
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();
+            issue_tile_load(nl);
+        }
+#pragma unroll
+        for (int j = 0; j < kU2; ++j)
+            if (o0[j] >= 0) store_unit_global(to, t_sub, part, o0[j], o1[j], acc[j]);
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < kU2; ++j)
         if (o0[j] >= 0) store_unit(X, stride, t_sub, part, o0[j], o1[j], acc[j]);
@@ -389,23 +499,53 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
     __syncthreads();
     uint32_t phase = 0;
+    if (d.direct_store) {
+        if (threadIdx.x == 0 && static_cast<int64_t>(blockIdx.x) < ntiles) {
+            const int64_t nt = blockIdx.x + gridDim.x;
+            issue_tile_load(NextLoad{in, bar, X, stride, dimr, static_cast<int64_t>(blockIdx.x), batch,
+                                     nt < ntiles ? nt : -1});
+        }
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int64_t t0 = tile * TB;
+            const int nvalid = static_cast<int>(batch - t0 < TB ? batch - t0 : TB);
+            mbar_wait(bar, phase);
+            phase ^= 1;
+            const TileOut none{nullptr, 0, 0, 0};
+            const int64_t nt = tile + gridDim.x, nn = tile + 2 * static_cast<int64_t>(gridDim.x);
+            const NextLoad nl{in, bar, X, stride, dimr, nt < ntiles ? nt : -1, batch, nn < ntiles ? nn : -1};
+            for (int s = 0; s + 1 < d.nstages; ++s) stage2(d.st[s], X, stride, warp, lane, ring, none, nl);
+            stage2(d.st[d.nstages - 1], X, stride, warp, lane, ring, TileOut{out, t0, nvalid, dimr}, nl);
+        }
+        return;
+    }
+    const TileOut none{nullptr, 0, 0, 0};
+    const NextLoad nonl{in, bar, X, stride, dimr, -1, batch, -1};
+    const bool timing = d.timing != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long tacc[kMaxStages + 2] = {};
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t t0 = tile * TB;
         const int nvalid = static_cast<int>(batch - t0 < TB ? batch - t0 : TB);
+        long long c0 = timing ? clock64() : 0;
         if (threadIdx.x == 0) {
             tma_store_wait_read0();
-            mbar_arrive_expect_tx(bar, row_bytes * nvalid);
-            for (int t = 0; t < nvalid; ++t) tma_load_1d(X + t * stride, in + (t0 + t) * dimr, row_bytes, bar);
             const int64_t nt = tile + gridDim.x;
-            if (nt < ntiles) {
-                const int64_t n0 = nt * TB;
-                const int nv = static_cast<int>(batch - n0 < TB ? batch - n0 : TB);
-                prefetch_l2_bulk(in + n0 * dimr, row_bytes * nv);
-            }
+            issue_tile_load(NextLoad{in, bar, X, stride, dimr, tile, batch, nt < ntiles ? nt : -1});
         }
         mbar_wait(bar, phase);
         phase ^= 1;
-        for (int s = 0; s < d.nstages; ++s) stage2(d.st[s], X, stride, warp, lane, ring);
+        if (timing) {
+            const long long c1 = clock64();
+            tacc[0] += c1 - c0;
+            c0 = c1;
+        }
+        for (int s = 0; s < d.nstages; ++s) {
+            if ((d.stage_mask >> s) & 1) stage2(d.st[s], X, stride, warp, lane, ring, none, nonl);
+            if (timing) {
+                const long long c1 = clock64();
+                tacc[1 + s] += c1 - c0;
+                c0 = c1;
+            }
+        }
         fence_proxy_async_smem();
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -414,6 +554,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
     }
     if (threadIdx.x == 0) tma_store_wait0();
+    if (timing)
+        for (int i = 0; i < kMaxStages + 2; ++i) d.timing[i] = tacc[i];
 }
 
 }  // namespace

@@ -45,8 +45,10 @@ struct Stage2Dev {
     const int* u_out;       // [units][8]
     const int* w_base;      // sparse: [17] warp-major entry ranges
     const int* w_count;     // sparse: [16][4] entries per unit
+    const unsigned* w_cplx; // sparse: [16][4] complex-entry bitmask of the warp stream
     const int4* e_slots;    // sparse: [entries] input slots of the 4 k-columns (bit 30 of .x: complex)
-    const double2* e_frag;  // sparse: [entries][32] (Re, Im) of T[k][n], lane order
+    const double* e_re;     // sparse: [entries][32] Re T[k][n], lane order
+    const double* e_im;     // sparse: [entries][32] Im T[k][n] (fetched for complex tiles only)
     const int* u_node;      // mix
     const int* u_in;        // mix: [units][8]
     const double2* K;       // mix: [nodes][8][8]
@@ -56,6 +58,9 @@ struct Pipeline2Desc {
     int N;
     int stride;  // doubles per block row in shared memory
     int nstages;
+    int direct_store;  // 1: last stage stores to global from registers; 0: smem + TMA bulk store
+    int stage_mask;    // debug/timing only: stages with a cleared bit are skipped
+    unsigned long long* timing;  // debug: CTA 0 accumulates clock64 per phase (nullptr: off)
     Stage2Dev st[kMaxStages];
 };
 

@@ -78,6 +78,15 @@ Index3 apply(const std::array<int, 9>& w, const Index3& k) {  // weyl_s4.cpp:38-
     return o;
 }
 
+// Exact factors are algebraic numbers of size >= ~1e-3; a real or imaginary
+// component below 1e-15 is long-double rounding noise (e.g. cos(pi/2) or the
+// imaginary part of an entry that is real in exact arithmetic) and is snapped
+// to zero so real coefficients stay real.
+cld snap(const cld& v) {
+    constexpr long double eps = 1e-15L;
+    return cld{std::fabs(v.real()) < eps ? 0.0L : v.real(), std::fabs(v.imag()) < eps ? 0.0L : v.imag()};
+}
+
 void require_condition(double cond, const std::string& what) {  // transform.cpp:113-117
     if (!(cond <= kConditionLimit))
         throw FcctError(ST_ILL_CONDITIONED,
@@ -326,7 +335,7 @@ SparseLD derive_B(int n, const OrbitBlocks& Sn, const std::array<OrbitBlocks, 8>
                 cld acc{0, 0};
                 for (int blk = 0; blk < 8; ++blk) acc += Kinv[g * 8 + blk] * u[static_cast<size_t>(blk) * dp + h];
                 if (std::abs(acc) >= kPrune)
-                    rows[static_cast<int64_t>(g) * m3 + memp[h]].emplace_back(static_cast<int32_t>(c), acc);
+                    rows[static_cast<int64_t>(g) * m3 + memp[h]].emplace_back(static_cast<int32_t>(c), snap(acc));
             }
     }
     SparseLD out;
@@ -388,7 +397,7 @@ SparseLD derive_Binv(int n, const OrbitBlocks& Sn, const std::array<OrbitBlocks,
                 }
             }
             for (const auto& [row, val] : x)
-                if (std::abs(val) >= kPrune) rows[row].emplace_back(static_cast<int32_t>(col), val);
+                if (std::abs(val) >= kPrune) rows[row].emplace_back(static_cast<int32_t>(col), snap(val));
         }
     SparseLD out;
     out.dim = n3;
@@ -463,8 +472,10 @@ std::shared_ptr<const PlanNode> make_node(int n, const Params& p, bool check) {
             K[blk * 8 + g] = dense_entry(2, p, unlex(blk, 2), unlex(g, 2));
     const double kc = invert_ld(K, 8, Kinv);
     require_condition(kc, "radix kernel");
-    std::copy(K.begin(), K.end(), node->K.begin());
-    std::copy(Kinv.begin(), Kinv.end(), node->Kinv.begin());
+    for (int i = 0; i < 64; ++i) {
+        node->K[i] = snap(K[i]);
+        node->Kinv[i] = snap(Kinv[i]);
+    }
     const OrbitBlocks Sn = orbit_blocks(n, p);
     require_condition(Sn.worst_condition, "orbit block (n=" + std::to_string(n) + ")");
     std::array<OrbitBlocks, 8> Sm;

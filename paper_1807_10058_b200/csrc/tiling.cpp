@@ -301,24 +301,63 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, Pipeline2Host& out) {
     out.n = n;
     out.N = N;
     out.stride = 2 * N + 8;
+    struct Entry {
+        std::array<int32_t, 4> slots;
+        std::array<double, 32> re, im;
+        bool cplx;
+    };
     for (int s = 0; s < S; ++s) {
         const auto& L = logical[s];
         Stage2Host st;
-        st.kind = L.kind;
         st.n_units = static_cast<int>(unit_outs[s].size());
         std::vector<int64_t> cost(st.n_units, 0);
         for (int u = 0; u < st.n_units; ++u)
             for (int i = 0; i < 8; ++i) st.u_out.push_back(lam[s + 1][unit_outs[s][u][i]]);
+        // Leaf-level mixes (one slice per node, a distinct K per unit) go
+        // through the entry ring like sparse stages: their K tables would
+        // otherwise stream from L2 with only one unit of prefetch.
+        const bool leaf_mix = false && L.kind == 1 && L.nodes[0]->n == 2;  // measured slower than the mix path
+        std::vector<std::vector<Entry>> uent(st.n_units);
         if (L.kind == 0) {
             const Tiling& T = tilings[s];
             for (int u = 0; u < st.n_units; ++u)
                 for (const auto& [kt, vals] : T.tiles[u]) {
-                    int cplx = 0;
-                    for (int l = 0; l < 32; ++l) cplx |= vals[2 * l + 1] != 0.0;
-                    cost[u] += cplx ? 2 : 1;
-                    st.dmma_per_tile += 4 * (cplx ? 2 : 1);
+                    Entry e{};
+                    e.cplx = false;
+                    for (int l = 0; l < 32; ++l) {
+                        e.re[l] = vals[2 * l];
+                        e.im[l] = vals[2 * l + 1];
+                        e.cplx |= e.im[l] != 0.0;
+                    }
+                    for (int k = 0; k < 4; ++k) e.slots[k] = lam[s][T.col_order[kt * 4 + k]];
+                    uent[u].push_back(e);
+                }
+        } else if (leaf_mix) {
+            for (size_t q = 0; q < L.nodes.size(); ++q) {
+                const auto& Kq = L.inverse ? L.nodes[q]->Kinv : L.nodes[q]->K;
+                for (int kt = 0; kt < 2; ++kt) {
+                    Entry e{};
+                    e.cplx = false;
+                    for (int l = 0; l < 32; ++l) {
+                        const int nn = l / 4, k = l % 4;  // T[k][n] = K[b = n][g = 4 kt + k]
+                        e.re[l] = static_cast<double>(Kq[nn * 8 + kt * 4 + k].real());
+                        e.im[l] = static_cast<double>(Kq[nn * 8 + kt * 4 + k].imag());
+                        e.cplx |= e.im[l] != 0.0;
+                    }
+                    for (int k = 0; k < 4; ++k) e.slots[k] = lam[s][static_cast<int32_t>(q) * 8 + kt * 4 + k];
+                    uent[q].push_back(e);
+                }
+            }
+        }
+        if (L.kind == 0 || leaf_mix) {
+            st.kind = 0;
+            for (int u = 0; u < st.n_units; ++u)
+                for (const auto& e : uent[u]) {
+                    cost[u] += e.cplx ? 2 : 1;
+                    st.dmma_per_tile += 4 * (e.cplx ? 2 : 1);
                 }
         } else {
+            st.kind = 1;
             const int s3 = static_cast<int>(cube(L.nodes[0]->n)), m3 = s3 / 8;
             for (size_t q = 0; q < L.nodes.size(); ++q) {
                 const auto& Kq = L.inverse ? L.nodes[q]->Kinv : L.nodes[q]->K;
@@ -350,26 +389,24 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, Pipeline2Host& out) {
             st.warp_units[best * kUnits2 + cnt[best]++] = u;
             load[best] += cost[u];
         }
-        if (L.kind == 0) {
-            const Tiling& T = tilings[s];
+        if (st.kind == 0) {
             st.w_base.assign(kWarps2 + 1, 0);
             st.w_count.assign(kWarps2 * kUnits2, 0);
+            st.w_cplx.assign(kWarps2 * 4, 0u);
             int32_t flat = 0;
             for (int w = 0; w < kWarps2; ++w) {
                 st.w_base[w] = flat;
                 for (int j = 0; j < kUnits2; ++j) {
                     const int u = st.warp_units[w * kUnits2 + j];
                     if (u < 0) continue;
-                    st.w_count[w * kUnits2 + j] = static_cast<int32_t>(T.tiles[u].size());
-                    for (const auto& [kt, vals] : T.tiles[u]) {
-                        int cplx = 0;
-                        for (int l = 0; l < 32; ++l) cplx |= vals[2 * l + 1] != 0.0;
-                        for (int k = 0; k < 4; ++k) {
-                            int32_t slot = lam[s][T.col_order[kt * 4 + k]];
-                            if (k == 0 && cplx) slot |= 1 << 30;
-                            st.e_slots.push_back(slot);
-                        }
-                        st.e_frag.insert(st.e_frag.end(), vals.begin(), vals.end());
+                    st.w_count[w * kUnits2 + j] = static_cast<int32_t>(uent[u].size());
+                    for (const auto& e : uent[u]) {
+                        for (int k = 0; k < 4; ++k) st.e_slots.push_back(e.slots[k] | (e.cplx ? (1 << 30) : 0));
+                        st.e_re.insert(st.e_re.end(), e.re.begin(), e.re.end());
+                        st.e_im.insert(st.e_im.end(), e.im.begin(), e.im.end());
+                        const int fw = flat - st.w_base[w];
+                        if (fw >= 128) return false;
+                        if (e.cplx) st.w_cplx[w * 4 + fw / 32] |= 1u << (fw % 32);
                         ++flat;
                     }
                 }

@@ -42,8 +42,10 @@ struct Stage2Host {
     // unit j of warp w has w_count[w][j] of them.
     std::vector<int32_t> w_base;      // [kWarps2 + 1]
     std::vector<int32_t> w_count;     // [kWarps2][kUnits2]
-    std::vector<int32_t> e_slots;     // [n_entries][4] input slot of k-column; bit 30 of [0] = complex
-    std::vector<double> e_frag;       // [n_entries][32][2] (Re, Im) of T[k][n], lane order
+    std::vector<uint32_t> w_cplx;     // [kWarps2][4]: bit f = flat entry f of the warp is complex (<= 128 entries)
+    std::vector<int32_t> e_slots;     // [n_entries][4] input slot of k-column; bit 30 = complex tile
+    std::vector<double> e_re;         // [n_entries][32] Re T[k][n], lane order
+    std::vector<double> e_im;         // [n_entries][32] Im T[k][n] (zeros for real tiles, never fetched)
     // mix
     std::vector<int32_t> u_node;      // [n_units]
     std::vector<int32_t> u_in;        // [n_units][8] input slot of input g

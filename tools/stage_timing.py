@@ -1,0 +1,32 @@
+"""Per-stage clock64 breakdown of the fp64 fast pipeline (CTA 0), profiling aid."""
+import ctypes
+import os
+import sys
+from pathlib import Path
+
+os.environ["FCCT_DEBUG_TIMING"] = "1"
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1807_10058_b200 import SkewParams, _capi, build_plan  # noqa: E402
+from paper_1807_10058_b200.fcct import _raise  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+blocks = 65536
+plan = build_plan(n, SkewParams.canonical())
+x = torch.randn(blocks, n**3, dtype=torch.complex128, device="cuda")
+y = torch.empty_like(x)
+L = _capi.lib()
+for inv in (0, 1):
+    fn = L.fcct_inverse if inv else L.fcct_forward
+    for _ in range(3):
+        _raise(fn(plan._h, x.data_ptr(), y.data_ptr(), blocks, None))
+    torch.cuda.synchronize()
+    buf = (ctypes.c_ulonglong * 18)()
+    ns = ctypes.c_int()
+    _raise(L.fcct_debug_timing(plan._h, inv, buf, ctypes.byref(ns)))
+    t = np.array(buf[: ns.value + 1], dtype=np.float64)
+    tot = t.sum()
+    print(("inverse" if inv else "forward"), "total Mcycles (CTA 0)", round(tot / 1e6, 3),
+          " ".join(f"{'load' if i == 0 else 's%d' % (i - 1)}={100 * v / tot:.1f}%" for i, v in enumerate(t)))
