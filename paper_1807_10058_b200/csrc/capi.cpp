@@ -102,6 +102,8 @@ struct Pipeline2Tables {
 
 void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
     out.desc = Pipeline2Desc{};
+    out.desc.tb = h.shape.tb;
+    out.desc.warps = h.shape.warps;
     out.desc.N = h.N;
     out.desc.stride = h.stride;
     out.desc.nstages = static_cast<int>(h.stages.size());
@@ -118,31 +120,44 @@ void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
     }
     out.dmma_per_tile = h.dmma_per_tile;
     if (out.desc.nstages > kMaxStages) throw FcctError(ST_INVALID_ARGUMENT, "too many stages");
+    std::vector<unsigned char> arena;
+    auto put = [&](const void* data, size_t bytes) -> int {
+        if (bytes == 0) return -1;
+        const size_t off = (arena.size() + 15) & ~size_t{15};
+        arena.resize(off + bytes);
+        std::memcpy(arena.data() + off, data, bytes);
+        return static_cast<int>(off);
+    };
+    auto keep = [&](std::shared_ptr<DevBuf> b) {
+        out.bufs.push_back(b);
+        return b->ptr;
+    };
+    constexpr size_t kArenaK = 16 * 1024;  // K tables up to this size go to shared memory
     for (size_t s = 0; s < h.stages.size(); ++s) {
         const Stage2Host& st = h.stages[s];
         Stage2Dev& d = out.desc.st[s];
         d = Stage2Dev{};
         d.kind = st.kind;
-        auto keep = [&](std::shared_ptr<DevBuf> b) {
-            out.bufs.push_back(b);
-            return b->ptr;
-        };
         d.n_units = st.n_units;
-        d.warp_units = static_cast<const int*>(keep(upload(st.warp_units)));
-        d.u_out = static_cast<const int*>(keep(upload(st.u_out)));
+        d.o_warp_units = put(st.warp_units.data(), st.warp_units.size() * 4);
+        d.o_u_out = put(st.u_out.data(), st.u_out.size() * 4);
+        d.o_w_base = d.o_w_count = d.o_e_slots = d.o_u_node = d.o_u_in = d.o_K = -1;
         if (st.kind == 0) {
-            d.w_base = static_cast<const int*>(keep(upload(st.w_base)));
-            d.w_count = static_cast<const int*>(keep(upload(st.w_count)));
-            d.w_cplx = static_cast<const unsigned*>(keep(upload(st.w_cplx)));
-            d.e_slots = static_cast<const int4*>(keep(upload(st.e_slots)));
+            d.o_w_base = put(st.w_base.data(), st.w_base.size() * 4);
+            d.o_w_count = put(st.w_count.data(), st.w_count.size() * 4);
+            d.o_e_slots = put(st.e_slots.data(), st.e_slots.size() * 4);
             d.e_re = static_cast<const double*>(keep(upload(st.e_re)));
             d.e_im = static_cast<const double*>(keep(upload(st.e_im)));
         } else {
-            d.u_node = static_cast<const int*>(keep(upload(st.u_node)));
-            d.u_in = static_cast<const int*>(keep(upload(st.u_in)));
+            d.o_u_node = put(st.u_node.data(), st.u_node.size() * 4);
+            d.o_u_in = put(st.u_in.data(), st.u_in.size() * 4);
             d.K = static_cast<const double2*>(keep(upload(st.K)));
+            if (st.K.size() * sizeof(double) <= kArenaK) d.o_K = put(st.K.data(), st.K.size() * sizeof(double));
         }
     }
+    arena.resize((arena.size() + 15) & ~size_t{15});
+    out.desc.arena_bytes = static_cast<int>(arena.size());
+    out.desc.arena = static_cast<const uint4*>(keep(upload(arena)));
 }
 
 // ELL packing of a sparse stage for row groups of RG rows.
@@ -386,8 +401,11 @@ void build_v2(fcct_plan_s* pl) {
     const char* force = std::getenv("FCCT_PIPELINE");
     if (force && std::string(force) == "v1") return;
     if (pl->precision != FCCT_F64) return;
+    Shape2 shape;  // default: 16 blocks x 16 warps, one CTA per SM
+    if (const char* sh = std::getenv("FCCT_V2_SHAPE"); sh && std::string(sh) == "8x8")
+        shape = Shape2{8, 8, 8};  // two CTAs per SM (tuning experiment)
     Pipeline2Host hf, hi;
-    if (!compile_pipeline2(*pl->tree, false, hf) || !compile_pipeline2(*pl->tree, true, hi)) return;
+    if (!compile_pipeline2(*pl->tree, false, shape, hf) || !compile_pipeline2(*pl->tree, true, shape, hi)) return;
     upload_pipeline2(hf, pl->fwd2);
     upload_pipeline2(hi, pl->inv2);
     pl->v2 = true;
@@ -815,9 +833,10 @@ fcct_status fcct_debug_emulate_v2(int n, double r, double s, double t, int inver
     return guarded([&] {
         auto root = build_tree(n, Params{r, s, t});
         Pipeline2Host h;
-        if (!compile_pipeline2(*root, inverse != 0, h))
+        if (!compile_pipeline2(*root, inverse != 0, Shape2{}, h))
             throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by pipeline v2");
         const int N = h.N;
+        const int kWarps2 = h.shape.warps, kUnits2 = h.shape.units;
         std::vector<double> X(static_cast<size_t>(2) * N), Y(static_cast<size_t>(2) * N);
         for (int64_t b = 0; b < batch; ++b) {
             std::copy(in + 2 * N * b, in + 2 * N * (b + 1), X.begin());
@@ -885,7 +904,7 @@ fcct_status fcct_debug_v2_stats(int n, double r, double s, double t, int inverse
     return guarded([&] {
         auto root = build_tree(n, Params{r, s, t});
         Pipeline2Host h;
-        if (!compile_pipeline2(*root, inverse != 0, h))
+        if (!compile_pipeline2(*root, inverse != 0, Shape2{}, h))
             throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by pipeline v2");
         int64_t ld_req = 0, ld_conf = 0, st_req = 0, st_conf = 0;
         const int stride = h.stride;

@@ -8,6 +8,7 @@
 //  * table generation — D, D^{-1}, nodes and permutations built on the device.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "kernels.hpp"
@@ -230,8 +231,7 @@ cudaError_t launch_pipeline(const PipelineDesc& d, bool f32, const void* in, voi
 // ===========================================================================
 namespace {
 
-constexpr int kThreads2 = 512;
-constexpr int kU2 = 4;  // units per warp
+// CTA shapes: <TB blocks, WARPS warps>; units per warp U = 64 / WARPS
 
 __device__ __forceinline__ double lds_f64(uint32_t addr) {
     double v;
@@ -270,9 +270,6 @@ __device__ __forceinline__ double flip_unless(double v, int part) {
     return __hiloint2double(__double2hiint(v) ^ (part ? 0 : static_cast<int>(0x80000000u)), __double2loint(v));
 }
 
-constexpr int kRing = 8;                        // sparse entries in flight per warp
-constexpr int kRingBytesPerWarp = kRing * 640;  // per entry: 32 x (8 B Re + 8 B Im) + 32 x 4 B slot
-
 __device__ __forceinline__ void cp_async8_ca(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -281,11 +278,12 @@ __device__ __forceinline__ void cp_async4_ca(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
+template <int MT>
 __device__ __forceinline__ void store_unit(double* X, int stride, int t_sub, int part, int o0, int o1,
-                                           const double (&acc)[4][2]) {
+                                           const double (&acc)[MT][2]) {
     double* Xw = X + t_sub * stride + part;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
+    for (int mt = 0; mt < MT; ++mt) {
         Xw[(4 * mt) * stride + 2 * o0] = acc[mt][0];
         Xw[(4 * mt) * stride + 2 * o1] = acc[mt][1];
     }
@@ -299,10 +297,11 @@ struct TileOut {
     int dimr;
 };
 
+template <int MT>
 __device__ __forceinline__ void store_unit_global(const TileOut& to, int t_sub, int part, int o0, int o1,
-                                                  const double (&acc)[4][2]) {
+                                                  const double (&acc)[MT][2]) {
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
+    for (int mt = 0; mt < MT; ++mt) {
         const int t = 4 * mt + t_sub;
         if (t < to.nvalid) {
             double* row = to.out + (to.t0 + t) * to.dimr + part;
@@ -326,8 +325,8 @@ struct NextLoad {
     int64_t after; // tile after next (L2 prefetch), < 0: none
 };
 
+template <int TB>
 __device__ __forceinline__ void issue_tile_load(const NextLoad& nl) {
-    constexpr int TB = 16;
     const uint32_t row_bytes = static_cast<uint32_t>(nl.dimr * sizeof(double));
     if (nl.tile >= 0) {
         const int64_t t0 = nl.tile * TB;
@@ -342,49 +341,58 @@ __device__ __forceinline__ void issue_tile_load(const NextLoad& nl) {
     }
 }
 
-__device__ __forceinline__ void stage2(const Stage2Dev sd, double* X, int stride, int warp, int lane,
-                                       unsigned char* ring, const TileOut& to, const NextLoad& nl) {
+__constant__ int d_debug_flags;  // timing experiments only (bit 0: skip sparse fragment loads)
+
+template <int TB, int WARPS>
+__device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int stride, int warp, int lane,
+                                       const unsigned char* arena, const TileOut& to, const NextLoad& nl) {
     const int r = lane >> 2, k = lane & 3;
     const int t_sub = r >> 1, part = r & 1;
     const int n_out = lane >> 2;
-    double acc[kU2][4][2];
+    constexpr int kU2 = 64 / WARPS;  // units per warp
+    constexpr int MT = TB / 4;       // m-tiles (8 data rows each) per unit
+    double acc[kU2][MT][2];
     int o0[kU2], o1[kU2];
     const double* Xr = X + t_sub * stride + part;        // + 4 mt stride + 2 slot
     const double* Xs = X + t_sub * stride + (1 - part);  // part-swapped
+    const int* __restrict__ s_units = reinterpret_cast<const int*>(arena + sd.o_warp_units);
+    const int* __restrict__ s_uout = reinterpret_cast<const int*>(arena + sd.o_u_out);
     int units[kU2];
 #pragma unroll
     for (int j = 0; j < kU2; ++j) {
-        units[j] = __ldg(sd.warp_units + warp * kU2 + j);
+        units[j] = s_units[warp * kU2 + j];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) acc[j][mt][0] = acc[j][mt][1] = 0.0;
+        for (int mt = 0; mt < MT; ++mt) acc[j][mt][0] = acc[j][mt][1] = 0.0;
         o0[j] = o1[j] = -1;
     }
     if (sd.kind == 0) {
         // This warp's entry stream (tiling.hpp) with a 2-deep register prefetch
         // of (Re, Im, slot): every descriptor field is hoisted out of the loop
         // and shared memory is addressed through 32-bit shared-window offsets.
-        const int base = __ldg(sd.w_base + warp);
-        const int total = __ldg(sd.w_base + warp + 1) - base;
+        const int* __restrict__ s_wbase = reinterpret_cast<const int*>(arena + sd.o_w_base);
+        const int* __restrict__ s_wcount = reinterpret_cast<const int*>(arena + sd.o_w_count);
+        const int base = s_wbase[warp];
+        const int total = s_wbase[warp + 1] - base;
         const double* __restrict__ pre = sd.e_re + static_cast<size_t>(base) * 32 + lane;
         const double* __restrict__ pim = sd.e_im + static_cast<size_t>(base) * 32 + lane;
-        const int* __restrict__ psl = reinterpret_cast<const int*>(sd.e_slots) + static_cast<size_t>(base) * 4 + k;
+        const int* __restrict__ psl = reinterpret_cast<const int*>(arena + sd.o_e_slots) + base * 4 + k;
         const uint32_t xr = smem_u32(Xr), xs = smem_u32(Xs);
         const uint32_t mstep = static_cast<uint32_t>(4 * stride * sizeof(double));
         const uint32_t sign = part ? 0u : 0x80000000u;
         int cnt[kU2];
 #pragma unroll
-        for (int j = 0; j < kU2; ++j) cnt[j] = __ldg(sd.w_count + warp * kU2 + j);
+        for (int j = 0; j < kU2; ++j) cnt[j] = s_wcount[warp * kU2 + j];
         double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0;
         int sl0 = 0, sl1 = 0;
         if (total > 0) {
             re0 = __ldg(pre);
             im0 = __ldg(pim);
-            sl0 = __ldg(psl);
+            sl0 = psl[0];
         }
         if (total > 1) {
             re1 = __ldg(pre + 32);
             im1 = __ldg(pim + 32);
-            sl1 = __ldg(psl + 4);
+            sl1 = psl[4];
         }
         int f = 0;
 #pragma unroll
@@ -393,21 +401,26 @@ __device__ __forceinline__ void stage2(const Stage2Dev sd, double* X, int stride
                 double re2 = 0.0, im2 = 0.0;
                 int sl2 = 0;
                 if (f + 2 < total) {
-                    re2 = __ldg(pre + (f + 2) * 32);
-                    im2 = __ldg(pim + (f + 2) * 32);
-                    sl2 = __ldg(psl + (f + 2) * 4);
+                    if (!(d_debug_flags & 1)) {
+                        re2 = __ldg(pre + (f + 2) * 32);
+                        im2 = __ldg(pim + (f + 2) * 32);
+                    } else {
+                        re2 = 0.5;
+                        im2 = 0.25;
+                    }
+                    sl2 = psl[(f + 2) * 4];
                 }
                 const uint32_t off = static_cast<uint32_t>(sl0 & ~(1 << 30)) * 16u;
-                double a[4];
+                double a[MT];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) a[mt] = lds_f64(xr + off + mt * mstep);
+                for (int mt = 0; mt < MT; ++mt) a[mt] = lds_f64(xr + off + mt * mstep);
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], re0);
+                for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], re0);
                 if ((sl0 >> 30) & 1) {
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) a[mt] = lds_f64_xor_hi(xs + off + mt * mstep, sign);
+                    for (int mt = 0; mt < MT; ++mt) a[mt] = lds_f64_xor_hi(xs + off + mt * mstep, sign);
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], im0);
+                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], im0);
                 }
                 re0 = re1;
                 im0 = im1;
@@ -417,8 +430,8 @@ __device__ __forceinline__ void stage2(const Stage2Dev sd, double* X, int stride
                 sl1 = sl2;
             }
             if (units[j] >= 0) {
-                o0[j] = __ldg(sd.u_out + units[j] * 8 + 2 * k);
-                o1[j] = __ldg(sd.u_out + units[j] * 8 + 2 * k + 1);
+                o0[j] = s_uout[units[j] * 8 + 2 * k];
+                o1[j] = s_uout[units[j] * 8 + 2 * k + 1];
             }
         }
     } else {
@@ -427,11 +440,13 @@ __device__ __forceinline__ void stage2(const Stage2Dev sd, double* X, int stride
         int ks[2] = {0, 0};
         auto fetch = [&](int u, double2 (&f)[2], int (&sl)[2]) {
             if (u < 0) return;
-            const double2* Kq = sd.K + __ldg(sd.u_node + u) * 64;
+            const int* s_unode = reinterpret_cast<const int*>(arena + sd.o_u_node);
+            const double2* Kbase = sd.o_K >= 0 ? reinterpret_cast<const double2*>(arena + sd.o_K) : sd.K;
+            const double2* Kq = Kbase + s_unode[u] * 64;
 #pragma unroll
             for (int kt = 0; kt < 2; ++kt) {
-                sl[kt] = __ldg(sd.u_in + u * 8 + kt * 4 + k);
-                f[kt] = __ldg(Kq + n_out * 8 + kt * 4 + k);  // K[b = n][g]
+                sl[kt] = reinterpret_cast<const int*>(arena + sd.o_u_in)[u * 8 + kt * 4 + k];
+                f[kt] = Kq[n_out * 8 + kt * 4 + k];  // K[b = n][g]
             }
         };
         fetch(units[0], kf, ks);
@@ -443,19 +458,19 @@ __device__ __forceinline__ void stage2(const Stage2Dev sd, double* X, int stride
             if (units[j] >= 0) {
 #pragma unroll
                 for (int kt = 0; kt < 2; ++kt) {
-                    double a[4], as[4];
+                    double a[MT], as[MT];
                     const uint32_t xq = smem_u32(X + t_sub * stride + 2 * ks[kt]);
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt)
+                    for (int mt = 0; mt < MT; ++mt)
                         split_pair(lds_pair(xq + mt * static_cast<uint32_t>(4 * stride * sizeof(double))), part, a[mt],
                                    as[mt]);
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], kf[kt].x);
+                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], kf[kt].x);
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], as[mt], kf[kt].y);
+                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], as[mt], kf[kt].y);
                 }
-                o0[j] = __ldg(sd.u_out + units[j] * 8 + 2 * k);
-                o1[j] = __ldg(sd.u_out + units[j] * 8 + 2 * k + 1);
+                o0[j] = s_uout[units[j] * 8 + 2 * k];
+                o1[j] = s_uout[units[j] * 8 + 2 * k + 1];
             }
             kf[0] = nf[0];
             kf[1] = nf[1];
@@ -467,7 +482,7 @@ __device__ __forceinline__ void stage2(const Stage2Dev sd, double* X, int stride
     if (to.out != nullptr) {
         if (threadIdx.x == 0) {
             fence_proxy_async_smem();
-            issue_tile_load(nl);
+            issue_tile_load<TB>(nl);
         }
 #pragma unroll
         for (int j = 0; j < kU2; ++j)
@@ -480,29 +495,33 @@ __device__ __forceinline__ void stage2(const Stage2Dev sd, double* X, int stride
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kThreads2, 1)
+template <int TB, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
     pipeline2_kernel(const __grid_constant__ Pipeline2Desc d, const double* __restrict__ in, double* __restrict__ out,
                      int64_t batch) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     double* X = reinterpret_cast<double*>(smem_raw + 128);
     const int stride = d.stride;
-    unsigned char* ring = smem_raw + 128 + static_cast<size_t>(16) * stride * sizeof(double);
+    unsigned char* arena = smem_raw + 128 + static_cast<size_t>(TB) * stride * sizeof(double);
     const int dimr = 2 * d.N;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    constexpr int TB = 16;
     const int64_t ntiles = (batch + TB - 1) / TB;
     const uint32_t row_bytes = static_cast<uint32_t>(dimr * sizeof(double));
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
     }
+    {  // per-CTA copy of the small stage tables (identical for every tile)
+        uint4* dst = reinterpret_cast<uint4*>(arena);
+        for (int i = threadIdx.x; i < d.arena_bytes / 16; i += blockDim.x) dst[i] = __ldg(d.arena + i);
+    }
     __syncthreads();
     uint32_t phase = 0;
     if (d.direct_store) {
         if (threadIdx.x == 0 && static_cast<int64_t>(blockIdx.x) < ntiles) {
             const int64_t nt = blockIdx.x + gridDim.x;
-            issue_tile_load(NextLoad{in, bar, X, stride, dimr, static_cast<int64_t>(blockIdx.x), batch,
+            issue_tile_load<TB>(NextLoad{in, bar, X, stride, dimr, static_cast<int64_t>(blockIdx.x), batch,
                                      nt < ntiles ? nt : -1});
         }
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -513,15 +532,16 @@ __global__ void __launch_bounds__(kThreads2, 1)
             const TileOut none{nullptr, 0, 0, 0};
             const int64_t nt = tile + gridDim.x, nn = tile + 2 * static_cast<int64_t>(gridDim.x);
             const NextLoad nl{in, bar, X, stride, dimr, nt < ntiles ? nt : -1, batch, nn < ntiles ? nn : -1};
-            for (int s = 0; s + 1 < d.nstages; ++s) stage2(d.st[s], X, stride, warp, lane, ring, none, nl);
-            stage2(d.st[d.nstages - 1], X, stride, warp, lane, ring, TileOut{out, t0, nvalid, dimr}, nl);
+            for (int s = 0; s + 1 < d.nstages; ++s) stage2<TB, WARPS>(d.st[s], X, stride, warp, lane, arena, none, nl);
+            stage2<TB, WARPS>(d.st[d.nstages - 1], X, stride, warp, lane, arena, TileOut{out, t0, nvalid, dimr}, nl);
         }
         return;
     }
     const TileOut none{nullptr, 0, 0, 0};
     const NextLoad nonl{in, bar, X, stride, dimr, -1, batch, -1};
     const bool timing = d.timing != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-    unsigned long long tacc[kMaxStages + 2] = {};
+    __shared__ unsigned long long tacc[kMaxStages + 2];
+    if (threadIdx.x < kMaxStages + 2) tacc[threadIdx.x] = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t t0 = tile * TB;
         const int nvalid = static_cast<int>(batch - t0 < TB ? batch - t0 : TB);
@@ -529,7 +549,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         if (threadIdx.x == 0) {
             tma_store_wait_read0();
             const int64_t nt = tile + gridDim.x;
-            issue_tile_load(NextLoad{in, bar, X, stride, dimr, tile, batch, nt < ntiles ? nt : -1});
+            issue_tile_load<TB>(NextLoad{in, bar, X, stride, dimr, tile, batch, nt < ntiles ? nt : -1});
         }
         mbar_wait(bar, phase);
         phase ^= 1;
@@ -539,7 +559,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             c0 = c1;
         }
         for (int s = 0; s < d.nstages; ++s) {
-            if ((d.stage_mask >> s) & 1) stage2(d.st[s], X, stride, warp, lane, ring, none, nonl);
+            if ((d.stage_mask >> s) & 1) stage2<TB, WARPS>(d.st[s], X, stride, warp, lane, arena, none, nonl);
             if (timing) {
                 const long long c1 = clock64();
                 tacc[1 + s] += c1 - c0;
@@ -560,21 +580,37 @@ __global__ void __launch_bounds__(kThreads2, 1)
 
 }  // namespace
 
+template <int TB, int WARPS>
+cudaError_t launch_pipeline2_t(const Pipeline2Desc& d, const void* in, void* out, int64_t batch, cudaStream_t st,
+                               int num_sms) {
+    const int smem = 128 + TB * d.stride * static_cast<int>(sizeof(double)) + d.arena_bytes;
+    auto kern = pipeline2_kernel<TB, WARPS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int64_t ntiles = (batch + TB - 1) / TB;
+    const int64_t grid = std::min<int64_t>(ntiles, static_cast<int64_t>(per_sm) * num_sms);
+    kern<<<static_cast<unsigned>(grid), WARPS * 32, smem, st>>>(d, static_cast<const double*>(in),
+                                                                 static_cast<double*>(out), batch);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pipeline2(const Pipeline2Desc& d, const void* in, void* out, int64_t batch, cudaStream_t st,
                              int num_sms) {
     if (batch <= 0) return cudaSuccess;
-    const int smem = 128 + 16 * d.stride * static_cast<int>(sizeof(double)) + 16 * kRingBytesPerWarp;
-    cudaError_t e = cudaFuncSetAttribute(pipeline2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pipeline2_kernel, kThreads2, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const int64_t ntiles = (batch + 15) / 16;
-    const int64_t grid = std::min<int64_t>(ntiles, static_cast<int64_t>(per_sm) * num_sms);
-    pipeline2_kernel<<<static_cast<unsigned>(grid), kThreads2, smem, st>>>(d, static_cast<const double*>(in),
-                                                                            static_cast<double*>(out), batch);
-    return cudaGetLastError();
+    static int flags_set = -1;
+    const char* dbg = std::getenv("FCCT_DEBUG_FLAGS");
+    const int flags = dbg ? std::atoi(dbg) : 0;
+    if (flags != flags_set) {
+        cudaMemcpyToSymbol(d_debug_flags, &flags, sizeof(int));
+        flags_set = flags;
+    }
+    if (d.tb == 16 && d.warps == 16) return launch_pipeline2_t<16, 16>(d, in, out, batch, st, num_sms);
+    if (d.tb == 8 && d.warps == 8) return launch_pipeline2_t<8, 8>(d, in, out, batch, st, num_sms);
+    return cudaErrorInvalidValue;
 }
 
 // ===========================================================================

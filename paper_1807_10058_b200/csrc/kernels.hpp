@@ -38,23 +38,30 @@ struct PipelineDesc {
 };
 
 // Pipeline v2 (fp64, n <= 8): every stage on the FP64 tensor pipe, see tiling.hpp.
+// Small per-stage tables live in a per-CTA shared-memory arena (copied once
+// per kernel, they are identical for every tile): fields named o_* are byte
+// offsets into it (-1: absent). Fragment values and large K tables stay global.
 struct Stage2Dev {
     int kind;  // 0 sparse tiles, 1 mix
     int n_units;
-    const int* warp_units;  // [16][4]
-    const int* u_out;       // [units][8]
-    const int* w_base;      // sparse: [17] warp-major entry ranges
-    const int* w_count;     // sparse: [16][4] entries per unit
-    const unsigned* w_cplx; // sparse: [16][4] complex-entry bitmask of the warp stream
-    const int4* e_slots;    // sparse: [entries] input slots of the 4 k-columns (bit 30 of .x: complex)
-    const double* e_re;     // sparse: [entries][32] Re T[k][n], lane order
-    const double* e_im;     // sparse: [entries][32] Im T[k][n] (fetched for complex tiles only)
-    const int* u_node;      // mix
-    const int* u_in;        // mix: [units][8]
-    const double2* K;       // mix: [nodes][8][8]
+    int o_warp_units;  // int [warps][units]
+    int o_u_out;       // int [units][8]
+    int o_w_base;      // sparse: int [warps + 1] warp-major entry ranges
+    int o_w_count;     // sparse: int [warps][units]
+    int o_e_slots;     // sparse: int [entries][4] input slots (bit 30: complex tile)
+    int o_u_node;      // mix: int [units]
+    int o_u_in;        // mix: int [units][8]
+    int o_K;           // mix: double2 [nodes][8][8] when small enough, else -1
+    const double* e_re;  // sparse: [entries][32] Re T[k][n], lane order (global)
+    const double* e_im;  // sparse: [entries][32] Im T[k][n] (global)
+    const double2* K;    // mix: global copy of the K tables
 };
 
 struct Pipeline2Desc {
+    const uint4* arena;  // global image of the shared-memory table arena
+    int arena_bytes;     // multiple of 16
+    int tb;     // blocks per tile (16 or 8)
+    int warps;  // warps per CTA (16 or 8)
     int N;
     int stride;  // doubles per block row in shared memory
     int nstages;

@@ -189,7 +189,8 @@ struct Logical {
 
 }  // namespace
 
-bool compile_pipeline2(const PlanNode& root, bool inverse, Pipeline2Host& out) {
+bool compile_pipeline2(const PlanNode& root, bool inverse, const Shape2& shape, Pipeline2Host& out) {
+    const int kWarps2 = shape.warps, kUnits2 = shape.units;
     if (!root.radix || root.n > 8) return false;
     std::vector<std::vector<const PlanNode*>> levels;
     std::vector<const PlanNode*> cur{&root};
@@ -298,6 +299,7 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, Pipeline2Host& out) {
     }
 
     out = Pipeline2Host{};
+    out.shape = shape;
     out.n = n;
     out.N = N;
     out.stride = 2 * N + 8;
@@ -354,7 +356,7 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, Pipeline2Host& out) {
             for (int u = 0; u < st.n_units; ++u)
                 for (const auto& e : uent[u]) {
                     cost[u] += e.cplx ? 2 : 1;
-                    st.dmma_per_tile += 4 * (e.cplx ? 2 : 1);
+                    st.dmma_per_tile += (shape.tb / 4) * (e.cplx ? 2 : 1);
                 }
         } else {
             st.kind = 1;
@@ -372,7 +374,7 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, Pipeline2Host& out) {
                 }
             }
             for (int u = 0; u < st.n_units; ++u) cost[u] = 4;
-            st.dmma_per_tile += static_cast<int64_t>(st.n_units) * 16;
+            st.dmma_per_tile += static_cast<int64_t>(st.n_units) * 4 * (shape.tb / 4);
         }
         // LPT assignment of units to warps, at most kUnits2 per warp
         std::vector<int32_t> order(st.n_units);

@@ -28,21 +28,25 @@
 
 namespace fcct {
 
-constexpr int kTB2 = 16;       // transform blocks per CTA tile
-constexpr int kWarps2 = 16;    // warps per CTA
-constexpr int kUnits2 = 4;     // units per warp per stage
+// CTA shape: `tb` blocks per tile (4 data rows per block pair -> tb/4 m-tiles
+// per unit), `warps` warps per CTA, at most `units` units per warp per stage.
+struct Shape2 {
+    int tb = 16;
+    int warps = 16;
+    int units = 4;
+};
 
 struct Stage2Host {
     int kind = 0;  // 0 sparse (tiles), 1 mix (8x8 complex per unit)
     int n_units = 0;
-    std::vector<int32_t> warp_units;  // [kWarps2][kUnits2] unit index or -1
+    std::vector<int32_t> warp_units;  // [warps][units] unit index or -1
     std::vector<int32_t> u_out;       // [n_units][8] output slot of output n
     // sparse: entries stored warp-major (the per-warp stream the kernel's
     // cp.async ring walks): warp w owns entries [w_base[w], w_base[w+1]),
     // unit j of warp w has w_count[w][j] of them.
-    std::vector<int32_t> w_base;      // [kWarps2 + 1]
-    std::vector<int32_t> w_count;     // [kWarps2][kUnits2]
-    std::vector<uint32_t> w_cplx;     // [kWarps2][4]: bit f = flat entry f of the warp is complex (<= 128 entries)
+    std::vector<int32_t> w_base;      // [warps + 1]
+    std::vector<int32_t> w_count;     // [warps][units]
+    std::vector<uint32_t> w_cplx;     // [warps][4]: bit f = flat entry f of the warp is complex (<= 128 entries)
     std::vector<int32_t> e_slots;     // [n_entries][4] input slot of k-column; bit 30 = complex tile
     std::vector<double> e_re;         // [n_entries][32] Re T[k][n], lane order
     std::vector<double> e_im;         // [n_entries][32] Im T[k][n] (zeros for real tiles, never fetched)
@@ -54,6 +58,7 @@ struct Stage2Host {
 };
 
 struct Pipeline2Host {
+    Shape2 shape;
     int n = 0;
     int N = 0;
     int stride = 0;  // doubles per block row in smem (2N + 8)
@@ -63,6 +68,6 @@ struct Pipeline2Host {
 
 // Builds the stage list for a full radix tree (every leaf n == 1, n <= 8).
 // Returns false when the tree is not supported (odd leaves, n > 8).
-bool compile_pipeline2(const PlanNode& root, bool inverse, Pipeline2Host& out);
+bool compile_pipeline2(const PlanNode& root, bool inverse, const Shape2& shape, Pipeline2Host& out);
 
 }  // namespace fcct
