@@ -345,7 +345,8 @@ __constant__ int d_debug_flags;  // timing experiments only (bit 0: skip sparse 
 
 template <int TB, int WARPS>
 __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int stride, int warp, int lane,
-                                       const unsigned char* arena, const TileOut& to, const NextLoad& nl) {
+                                       const unsigned char* arena, const TileOut& to, const NextLoad& nl,
+                                       unsigned long long* tcomp = nullptr) {
     const int r = lane >> 2, k = lane & 3;
     const int t_sub = r >> 1, part = r & 1;
     const int n_out = lane >> 2;
@@ -376,9 +377,6 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
         const double* __restrict__ pre = sd.e_re + static_cast<size_t>(base) * 32 + lane;
         const double* __restrict__ pim = sd.e_im + static_cast<size_t>(base) * 32 + lane;
         const int* __restrict__ psl = reinterpret_cast<const int*>(arena + sd.o_e_slots) + base * 4 + k;
-        const uint32_t xr = smem_u32(Xr), xs = smem_u32(Xs);
-        const uint32_t mstep = static_cast<uint32_t>(4 * stride * sizeof(double));
-        const uint32_t sign = part ? 0u : 0x80000000u;
         int cnt[kU2];
 #pragma unroll
         for (int j = 0; j < kU2; ++j) cnt[j] = s_wcount[warp * kU2 + j];
@@ -394,6 +392,13 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
             im1 = __ldg(pim + 32);
             sl1 = psl[4];
         }
+        // operand double-buffering: the next entry's data rows are loaded
+        // (plain, schedulable shared loads) before this entry's DMMAs issue
+        const double* __restrict__ xrow = reinterpret_cast<const double*>(X) + t_sub * stride + part;
+        const int mrow = 4 * stride;
+        double a_c[MT], a_n[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) a_c[mt] = xrow[mt * mrow + 2 * (sl0 & ~(1 << 30))];
         int f = 0;
 #pragma unroll
         for (int j = 0; j < kU2; ++j) {
@@ -410,18 +415,22 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
                     }
                     sl2 = psl[(f + 2) * 4];
                 }
-                const uint32_t off = static_cast<uint32_t>(sl0 & ~(1 << 30)) * 16u;
-                double a[MT];
+                if (f + 1 < total) {
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt) a[mt] = lds_f64(xr + off + mt * mstep);
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], re0);
-                if ((sl0 >> 30) & 1) {
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) a[mt] = lds_f64_xor_hi(xs + off + mt * mstep, sign);
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], im0);
+                    for (int mt = 0; mt < MT; ++mt) a_n[mt] = xrow[mt * mrow + 2 * (sl1 & ~(1 << 30))];
                 }
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a_c[mt], re0);
+                if ((sl0 >> 30) & 1) {
+                    const double* __restrict__ xsw = xrow + (part ? -1 : 1) + 2 * (sl0 & ~(1 << 30));
+                    double as[MT];
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) as[mt] = part ? xsw[mt * mrow] : -xsw[mt * mrow];
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], as[mt], im0);
+                }
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) a_c[mt] = a_n[mt];
                 re0 = re1;
                 im0 = im1;
                 sl0 = sl1;
@@ -456,18 +465,23 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
             int ns[2] = {0, 0};
             if (j + 1 < kU2) fetch(units[j + 1], nf, ns);
             if (units[j] >= 0) {
+                const double2* __restrict__ xrow = reinterpret_cast<const double2*>(X + t_sub * stride);
+                const int mrow2 = 2 * stride;  // 4 blocks, in double2 units
+                double a[2][MT], as[2][MT];
+#pragma unroll
+                for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const double2 v = xrow[mt * mrow2 + ks[kt]];
+                        a[kt][mt] = part ? v.y : v.x;
+                        as[kt][mt] = part ? v.x : -v.y;
+                    }
 #pragma unroll
                 for (int kt = 0; kt < 2; ++kt) {
-                    double a[MT], as[MT];
-                    const uint32_t xq = smem_u32(X + t_sub * stride + 2 * ks[kt]);
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt)
-                        split_pair(lds_pair(xq + mt * static_cast<uint32_t>(4 * stride * sizeof(double))), part, a[mt],
-                                   as[mt]);
+                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[kt][mt], kf[kt].x);
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[mt], kf[kt].x);
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], as[mt], kf[kt].y);
+                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], as[kt][mt], kf[kt].y);
                 }
                 o0[j] = s_uout[units[j] * 8 + 2 * k];
                 o1[j] = s_uout[units[j] * 8 + 2 * k + 1];
@@ -479,6 +493,7 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
         }
     }
     __syncthreads();
+    if (tcomp != nullptr) *tcomp = clock64();
     if (to.out != nullptr) {
         if (threadIdx.x == 0) {
             fence_proxy_async_smem();
@@ -559,10 +574,13 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
             c0 = c1;
         }
         for (int s = 0; s < d.nstages; ++s) {
-            if ((d.stage_mask >> s) & 1) stage2<TB, WARPS>(d.st[s], X, stride, warp, lane, arena, none, nonl);
+            __shared__ unsigned long long tmid;
+            if ((d.stage_mask >> s) & 1)
+                stage2<TB, WARPS>(d.st[s], X, stride, warp, lane, arena, none, nonl, timing ? &tmid : nullptr);
             if (timing) {
                 const long long c1 = clock64();
-                tacc[1 + s] += c1 - c0;
+                tacc[1 + s] += tmid - c0;              // compute phase (to the mid barrier)
+                tacc[1 + kMaxStages / 2 + s] += c1 - tmid;  // store phase + final barrier
                 c0 = c1;
             }
         }

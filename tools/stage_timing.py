@@ -26,7 +26,10 @@ for inv in (0, 1):
     buf = (ctypes.c_ulonglong * 18)()
     ns = ctypes.c_int()
     _raise(L.fcct_debug_timing(plan._h, inv, buf, ctypes.byref(ns)))
-    t = np.array(buf[: ns.value + 1], dtype=np.float64)
-    tot = t.sum()
-    print(("inverse" if inv else "forward"), "total Mcycles (CTA 0)", round(tot / 1e6, 3),
-          " ".join(f"{'load' if i == 0 else 's%d' % (i - 1)}={100 * v / tot:.1f}%" for i, v in enumerate(t)))
+    t = np.array(buf[:], dtype=np.float64)
+    S = ns.value
+    comp = t[1 : 1 + S]
+    store = t[9 : 9 + S]
+    tot = t[0] + comp.sum() + store.sum()
+    print(("inverse" if inv else "forward"), "total Mcycles (CTA 0)", round(tot / 1e6, 3), f"load={100 * t[0] / tot:.1f}%",
+          " ".join(f"s{i}=({100 * comp[i] / tot:.1f}% + {100 * store[i] / tot:.1f}%)" for i in range(S)))
