@@ -329,6 +329,105 @@ void build_pipelines(const PlanNode& root, int tb, PipelineTables& fwd, Pipeline
     }
 }
 
+struct GlobalTables {
+    GlobalPipelineDesc desc{};
+    std::vector<std::shared_ptr<DevBuf>> bufs;
+};
+
+template <typename R>
+void add_global_sparse(GlobalTables& gt, const Rows& rows, const std::vector<int32_t>* gather,
+                       const std::vector<int32_t>* scatter) {
+    std::vector<int64_t> rowptr(rows.N + 1, 0);
+    std::vector<int32_t> col;
+    std::vector<R> coef;
+    for (int64_t r = 0; r < rows.N; ++r) {
+        for (const auto& e : rows.r[r]) {
+            col.push_back(gather ? (*gather)[e.first] : e.first);
+            push_coef(coef, e.second);
+        }
+        rowptr[r + 1] = static_cast<int64_t>(col.size());
+    }
+    GStage& st = gt.desc.st[gt.desc.nstages++];
+    st = GStage{};
+    st.kind = 0;
+    auto b1 = upload(rowptr), b2 = upload(col), b3 = upload(coef);
+    st.rowptr = static_cast<const int64_t*>(b1->ptr);
+    st.col = static_cast<const int*>(b2->ptr);
+    st.coef = b3->ptr;
+    gt.bufs.insert(gt.bufs.end(), {b1, b2, b3});
+    if (scatter) {
+        auto b4 = upload(*scatter);
+        st.out_row = static_cast<const int*>(b4->ptr);
+        gt.bufs.push_back(b4);
+    }
+}
+
+template <typename R>
+void add_global_mix(GlobalTables& gt, const std::vector<const PlanNode*>& nodes, bool inverse,
+                    const std::vector<int32_t>* gather, const std::vector<int32_t>* scatter) {
+    std::vector<R> K;
+    for (const PlanNode* nd : nodes)
+        for (int i = 0; i < 64; ++i) push_coef(K, inverse ? nd->Kinv[i] : nd->K[i]);
+    GStage& st = gt.desc.st[gt.desc.nstages++];
+    st = GStage{};
+    st.kind = 1;
+    st.nodes = static_cast<int>(nodes.size());
+    st.m3 = static_cast<int>(cube(nodes[0]->n / 2));
+    auto bK = upload(K);
+    st.K = bK->ptr;
+    gt.bufs.push_back(bK);
+    if (gather) {
+        auto b = upload(*gather);
+        st.gather = static_cast<const int*>(b->ptr);
+        gt.bufs.push_back(b);
+    }
+    if (scatter) {
+        auto b = upload(*scatter);
+        st.scatter = static_cast<const int*>(b->ptr);
+        gt.bufs.push_back(b);
+    }
+}
+
+// Stage lists of the global multi-pass pipeline (same order as build_pipelines).
+template <typename R>
+void build_global_pipelines(const PlanNode& root, GlobalTables& fwd, GlobalTables& inv) {
+    std::vector<std::vector<const PlanNode*>> levels;
+    std::vector<const PlanNode*> cur{&root};
+    while (!cur.empty() && cur[0]->radix) {
+        levels.push_back(cur);
+        std::vector<const PlanNode*> next;
+        for (const PlanNode* nd : cur)
+            for (const auto& c : nd->children) next.push_back(c.get());
+        cur = next;
+    }
+    const std::vector<const PlanNode*> leaves = cur;
+    const bool dense_leaves = leaves[0]->n > 1;
+    const auto Z = composite_order(root);
+    for (auto* gt : {&fwd, &inv}) {
+        gt->desc.N = static_cast<int>(cube(root.n));
+        gt->desc.nstages = 0;
+    }
+    int nfwd = dense_leaves ? 1 : 0;
+    for (auto& lv : levels) nfwd += lv[0]->n > 2 ? 2 : 1;
+    if (nfwd > kMaxStages) throw FcctError(ST_INVALID_ARGUMENT, "too many stages");
+    int s = 0;
+    for (auto& lv : levels) {
+        if (lv[0]->n > 2) add_global_sparse<R>(fwd, level_rows(lv, 0), nullptr, (++s == nfwd) ? &Z : nullptr);
+        add_global_mix<R>(fwd, lv, false, nullptr, (++s == nfwd) ? &Z : nullptr);
+    }
+    if (dense_leaves) add_global_sparse<R>(fwd, level_rows(leaves, 2), nullptr, &Z);
+    bool first = true;
+    if (dense_leaves) {
+        add_global_sparse<R>(inv, level_rows(leaves, 3), &Z, nullptr);
+        first = false;
+    }
+    for (auto it = levels.rbegin(); it != levels.rend(); ++it) {
+        add_global_mix<R>(inv, *it, true, first ? &Z : nullptr, nullptr);
+        first = false;
+        if ((*it)[0]->n > 2) add_global_sparse<R>(inv, level_rows(*it, 1), nullptr, nullptr);
+    }
+}
+
 }  // namespace
 }  // namespace fcct
 
@@ -346,6 +445,10 @@ struct fcct_plan_s {
     PipelineTables fwd, inv;
     bool v2 = false;  // fp64 DMMA pipeline (tiling.hpp)
     Pipeline2Tables fwd2, inv2;
+    bool global = false;  // global-memory multi-pass pipeline
+    GlobalTables gfwd, ginv;
+    std::shared_ptr<DevBuf> scratch0, scratch1;
+    std::mutex scratch_mu;
     std::shared_ptr<DevBuf> Wt_fwd, Wt_inv;
     std::vector<std::shared_ptr<DevBuf>> extra;
     fcct_plan_info_t info{};
@@ -411,6 +514,33 @@ void build_v2(fcct_plan_s* pl) {
     pl->v2 = true;
 }
 
+// Picks the executor of a fast plan: the fp64 DMMA pipeline (n <= 8), else
+// the shared-memory tile interpreter (one block's state fits a CTA tile),
+// else the global-memory multi-pass pipeline. FCCT_PIPELINE=v1|v2|global
+// forces one for experiments.
+void build_fast_paths(fcct_plan_s* pl) {
+    const char* force = std::getenv("FCCT_PIPELINE");
+    const std::string f = force ? force : "";
+    const bool f32 = pl->precision == FCCT_F32;
+    if (f.empty() || f == "v2") build_v2(pl);
+    if (pl->v2) return;
+    const int tb = choose_tb(cube(pl->n), f32);
+    const bool tile_ok = tb > 0 && cube(pl->n) <= 4096;
+    if (f == "global" || (f != "v1" && !tile_ok)) {
+        if (f32)
+            build_global_pipelines<float>(*pl->tree, pl->gfwd, pl->ginv);
+        else
+            build_global_pipelines<double>(*pl->tree, pl->gfwd, pl->ginv);
+        pl->global = true;
+        return;
+    }
+    if (tb == 0) throw FcctError(ST_INVALID_ARGUMENT, "fast pipeline: n too large for one CTA tile");
+    if (f32)
+        build_pipelines<float>(*pl->tree, tb, pl->fwd, pl->inv);
+    else
+        build_pipelines<double>(*pl->tree, tb, pl->fwd, pl->inv);
+}
+
 void fill_info(fcct_plan_s* pl) {
     fcct_plan_info_t& in = pl->info;
     in.n = pl->n;
@@ -434,6 +564,8 @@ void fill_info(fcct_plan_s* pl) {
         for (auto* pt : {&pl->fwd, &pl->inv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->fwd2, &pl->inv2})
+            for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+        for (auto* pt : {&pl->gfwd, &pl->ginv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         in.table_bytes = bytes;
     } else {
@@ -462,14 +594,8 @@ fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int 
     const bool radix = method == FCCT_FAST && n % 2 == 0;
     if (radix) {
         pl->tree = build_tree(n, p);  // degeneracy + condition gates inside
-        const int tb = choose_tb(cube(n), f32);
-        if (tb == 0) throw FcctError(ST_INVALID_ARGUMENT, "fast pipeline: n too large for one CTA tile");
-        if (f32)
-            build_pipelines<float>(*pl->tree, tb, pl->fwd, pl->inv);
-        else
-            build_pipelines<double>(*pl->tree, tb, pl->fwd, pl->inv);
         pl->radix = true;
-        build_v2(pl.get());
+        build_fast_paths(pl.get());
     } else {
         check_nodes(n, p);
         pl->radix = false;
@@ -487,10 +613,23 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
     DeviceGuard guard(pl->device);
     const bool f32 = pl->precision == FCCT_F32;
     if (pl->radix) {
-        if (pl->v2)
+        if (pl->v2) {
             ck(launch_pipeline2(inverse ? pl->inv2.desc : pl->fwd2.desc, in, out, batch, st, pl->num_sms),
                "fast pipeline v2");
-        else
+        } else if (pl->global) {
+            const size_t bytes = static_cast<size_t>(batch * cube(pl->n) * elem_bytes(pl));
+            std::lock_guard<std::mutex> lock(pl->scratch_mu);
+            if (!pl->scratch0 || pl->scratch0->bytes < bytes) {
+                ck(cudaStreamSynchronize(st), "sync");
+                pl->scratch0 = std::make_shared<DevBuf>(bytes);
+                pl->scratch1 = std::make_shared<DevBuf>(bytes);
+            }
+            ck(launch_global_pipeline(inverse ? pl->ginv.desc : pl->gfwd.desc, f32, in, out, pl->scratch0->ptr,
+                                      pl->scratch1->ptr, batch, st),
+               "global pipeline");
+            // the plan-owned scratch serialises calls on this path
+            ck(cudaStreamSynchronize(st), "sync");
+        } else
             ck(launch_pipeline(inverse ? pl->inv.desc : pl->fwd.desc, f32, in, out, batch, st, pl->num_sms),
                "fast pipeline");
         return;
@@ -754,12 +893,7 @@ fcct_status fcct_plan_perturbed_basis(fcct_plan plan, double delta, fcct_plan* o
         pl->num_sms = plan->num_sms;
         pl->radix = true;
         pl->tree = root;
-        const int tb = plan->fwd.desc.tb;
-        if (pl->precision == FCCT_F32)
-            build_pipelines<float>(*root, tb, pl->fwd, pl->inv);
-        else
-            build_pipelines<double>(*root, tb, pl->fwd, pl->inv);
-        build_v2(pl.get());
+        build_fast_paths(pl.get());
         pl->method = FCCT_FAST;
         fill_info(pl.get());
         *out = pl.release();

@@ -632,6 +632,90 @@ cudaError_t launch_pipeline2(const Pipeline2Desc& d, const void* in, void* out, 
 }
 
 // ===========================================================================
+// Global-memory multi-pass pipeline (one launch per stage)
+// ===========================================================================
+namespace {
+
+template <typename R>
+__global__ void gstage_sparse_kernel(const GStage st, int N, const C2<R>* __restrict__ x, C2<R>* __restrict__ y) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (r >= N) return;
+    const int64_t b = blockIdx.y;
+    const C2<R>* xb = x + b * N;
+    const C2<R>* coef = static_cast<const C2<R>*>(st.coef);
+    C2<R> acc;
+    acc.x = 0;
+    acc.y = 0;
+    const int64_t e1 = __ldg(st.rowptr + r + 1);
+    for (int64_t e = __ldg(st.rowptr + r); e < e1; ++e) cmac(acc, coef[e], xb[__ldg(st.col + e)]);
+    const int64_t o = st.out_row ? __ldg(st.out_row + r) : r;
+    y[b * N + o] = acc;
+}
+
+template <typename R>
+__global__ void gstage_mix_kernel(const GStage st, int N, const C2<R>* __restrict__ x, C2<R>* __restrict__ y) {
+    const int64_t item = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (item >= static_cast<int64_t>(st.nodes) * st.m3) return;
+    const int64_t b = blockIdx.y;
+    const int q = static_cast<int>(item / st.m3), h = static_cast<int>(item % st.m3);
+    const int64_t base = static_cast<int64_t>(q) * 8 * st.m3 + h;
+    const C2<R>* Kq = static_cast<const C2<R>*>(st.K) + static_cast<int64_t>(q) * 64;
+    C2<R> in[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        int64_t p = base + static_cast<int64_t>(g) * st.m3;
+        if (st.gather) p = __ldg(st.gather + p);
+        in[g] = x[b * N + p];
+    }
+#pragma unroll
+    for (int bo = 0; bo < 8; ++bo) {
+        C2<R> acc;
+        acc.x = 0;
+        acc.y = 0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) cmac(acc, Kq[bo * 8 + g], in[g]);
+        int64_t p = base + static_cast<int64_t>(bo) * st.m3;
+        if (st.scatter) p = __ldg(st.scatter + p);
+        y[b * N + p] = acc;
+    }
+}
+
+template <typename R>
+cudaError_t launch_global_t(const GlobalPipelineDesc& d, const void* in, void* out, void* s0, void* s1, int64_t batch,
+                            cudaStream_t stream) {
+    const C2<R>* src = static_cast<const C2<R>*>(in);
+    for (int s = 0; s < d.nstages; ++s) {
+        C2<R>* dst = (s + 1 == d.nstages) ? static_cast<C2<R>*>(out) : static_cast<C2<R>*>(s % 2 ? s1 : s0);
+        const GStage& st = d.st[s];
+        for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+            const unsigned nb = static_cast<unsigned>(std::min<int64_t>(65535, batch - b0));
+            const int64_t off = b0 * d.N;
+            if (st.kind == 0) {
+                dim3 grid(static_cast<unsigned>((d.N + 255) / 256), nb);
+                gstage_sparse_kernel<R><<<grid, 256, 0, stream>>>(st, d.N, src + off, dst + off);
+            } else {
+                const int64_t items = static_cast<int64_t>(st.nodes) * st.m3;
+                dim3 grid(static_cast<unsigned>((items + 255) / 256), nb);
+                gstage_mix_kernel<R><<<grid, 256, 0, stream>>>(st, d.N, src + off, dst + off);
+            }
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
+        src = dst;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace
+
+cudaError_t launch_global_pipeline(const GlobalPipelineDesc& d, bool f32, const void* in, void* out, void* scratch0,
+                                   void* scratch1, int64_t batch, cudaStream_t stream) {
+    if (batch <= 0) return cudaSuccess;
+    return f32 ? launch_global_t<float>(d, in, out, scratch0, scratch1, batch, stream)
+               : launch_global_t<double>(d, in, out, scratch0, scratch1, batch, stream);
+}
+
+// ===========================================================================
 // Direct transform GEMMs (real form: C[M][Nn] = A[M][K] * Wt[Nn][K]^T)
 // ===========================================================================
 namespace {

@@ -74,6 +74,29 @@ struct Pipeline2Desc {
 cudaError_t launch_pipeline2(const Pipeline2Desc& d, const void* in, void* out, int64_t batch, cudaStream_t stream,
                              int num_sms);
 
+// Global-memory multi-pass pipeline (any full radix tree; used when a block's
+// state does not fit one CTA tile, e.g. n = 32, 64): one launch per stage.
+struct GStage {
+    int kind;              // 0 CSR sparse, 1 mix8
+    const int64_t* rowptr; // sparse
+    const int* col;        // sparse (gather folded in for the first inverse stage)
+    const void* coef;      // sparse: complex values
+    const int* out_row;    // sparse: output position of row r (scatter folded in), nullptr = identity
+    int nodes, m3;         // mix
+    const void* K;         // mix: [nodes][8][8] complex, row-major [b][g]
+    const int* gather;     // mix: input position map or nullptr
+    const int* scatter;    // mix: output position map or nullptr
+};
+
+struct GlobalPipelineDesc {
+    int N;
+    int nstages;
+    GStage st[kMaxStages];
+};
+
+cudaError_t launch_global_pipeline(const GlobalPipelineDesc& d, bool f32, const void* in, void* out, void* scratch0,
+                                   void* scratch1, int64_t batch, cudaStream_t stream);
+
 // Fast transform pipeline (forward or inverse, decided by the stage list).
 cudaError_t launch_pipeline(const PipelineDesc& d, bool f32, const void* in, void* out, int64_t batch,
                             cudaStream_t stream, int num_sms);

@@ -4,10 +4,12 @@
 #include <algorithm>
 #include <cmath>
 #include <deque>
+#include <future>
 #include <map>
 #include <mutex>
 #include <numbers>
 #include <set>
+#include <thread>
 #include <unordered_map>
 
 namespace fcct {
@@ -290,6 +292,49 @@ std::vector<int32_t> output_order(int n) {
 
 namespace {
 
+struct Triplet {
+    int32_t row, col;
+    cld val;
+};
+
+// Runs body(c0, c1, out) over column ranges on hardware threads and returns
+// the rows of the resulting sparse matrix (sorted by column within a row).
+template <typename Body>
+SparseLD columns_parallel(int64_t n3, Body body) {
+    const int nt = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(std::thread::hardware_concurrency(), n3 / 512)));
+    std::vector<std::vector<Triplet>> parts(nt);
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nt; ++w)
+        pool.emplace_back([&, w] { body(n3 * w / nt, n3 * (w + 1) / nt, parts[w]); });
+    for (auto& t : pool) t.join();
+    SparseLD out;
+    out.dim = n3;
+    out.rowptr.assign(n3 + 1, 0);
+    int64_t total = 0;
+    for (const auto& p : parts) {
+        total += static_cast<int64_t>(p.size());
+        for (const auto& t : p) out.rowptr[t.row + 1]++;
+    }
+    for (int64_t r = 0; r < n3; ++r) out.rowptr[r + 1] += out.rowptr[r];
+    out.col.resize(total);
+    out.val.resize(total);
+    std::vector<int64_t> fill(out.rowptr.begin(), out.rowptr.end() - 1);
+    for (const auto& p : parts)  // parts are in column order, so rows stay column-sorted
+        for (const auto& t : p) {
+            const int64_t dst = fill[t.row]++;
+            out.col[dst] = t.col;
+            out.val[dst] = t.val;
+        }
+    return out;
+}
+
+std::vector<cld> roots_of_unity(int n) {  // e^{2 pi i j / n}
+    std::vector<cld> r(n);
+    for (int j = 0; j < n; ++j) r[j] = unit_phase_ld(static_cast<long double>(j) / n);
+    return r;
+}
+
 // B = (K^{-1} (x) I) blockdiag(S_m(child)^{-1}) Phi S_n, column by column.
 SparseLD derive_B(int n, const OrbitBlocks& Sn, const std::array<OrbitBlocks, 8>& Sm,
                   const std::array<cld, 64>& Kinv) {
@@ -297,60 +342,50 @@ SparseLD derive_B(int n, const OrbitBlocks& Sn, const std::array<OrbitBlocks, 8>
     const int64_t n3 = cube(n), m3 = cube(m);
     const auto& on = *Sn.orb;
     const auto& om = orbits(m);
-    // triplets (row, col, val), column-major generation
-    std::vector<std::vector<std::pair<int32_t, cld>>> rows(n3);
-    std::vector<cld> v, u;
-    for (int64_t c = 0; c < n3; ++c) {
-        const int O = on.orbit_of[c], j = on.pos[c];
-        const auto& mem = on.members[O];
-        const int d = static_cast<int>(mem.size());
-        const Index3 cm = unlex(c, n);
-        const int64_t hrep = lex(Index3{cm[0] % m, cm[1] % m, cm[2] % m}, m);
-        const int Op = om.orbit_of[hrep];
-        const auto& memp = om.members[Op];
-        const int dp = static_cast<int>(memp.size());
-        v.assign(static_cast<size_t>(8) * dp, cld{0, 0});
-        for (int i = 0; i < d; ++i) {
-            const cld val = Sn.S[O][static_cast<size_t>(i) * d + j];
-            if (val == cld{0, 0}) continue;
-            const Index3 a = unlex(mem[i], n);
-            const int ip = om.pos[lex(Index3{a[0] % m, a[1] % m, a[2] % m}, m)];
+    const auto root = roots_of_unity(n);
+    return columns_parallel(n3, [&](int64_t c0, int64_t c1, std::vector<Triplet>& out) {
+        std::vector<cld> v, u;
+        for (int64_t c = c0; c < c1; ++c) {
+            const int O = on.orbit_of[c], j = on.pos[c];
+            const auto& mem = on.members[O];
+            const int d = static_cast<int>(mem.size());
+            const Index3 cm = unlex(c, n);
+            const int64_t hrep = lex(Index3{cm[0] % m, cm[1] % m, cm[2] % m}, m);
+            const int Op = om.orbit_of[hrep];
+            const auto& memp = om.members[Op];
+            const int dp = static_cast<int>(memp.size());
+            v.assign(static_cast<size_t>(8) * dp, cld{0, 0});
+            for (int i = 0; i < d; ++i) {
+                const cld val = Sn.S[O][static_cast<size_t>(i) * d + j];
+                if (val == cld{0, 0}) continue;
+                const Index3 a = unlex(mem[i], n);
+                const int ip = om.pos[lex(Index3{a[0] % m, a[1] % m, a[2] % m}, m)];
+                for (int blk = 0; blk < 8; ++blk) {
+                    const int ir = blk >> 2, is = (blk >> 1) & 1, it = blk & 1;
+                    v[static_cast<size_t>(blk) * dp + ip] += root[(a[0] * ir + a[1] * is + a[2] * it) % n] * val;
+                }
+            }
+            u.assign(static_cast<size_t>(8) * dp, cld{0, 0});
             for (int blk = 0; blk < 8; ++blk) {
-                const int ir = blk >> 2, is = (blk >> 1) & 1, it = blk & 1;
-                const cld tw = unit_phase_ld(static_cast<long double>(a[0] * ir + a[1] * is + a[2] * it) / n);
-                v[static_cast<size_t>(blk) * dp + ip] += tw * val;
+                const auto& Si = Sm[blk].Sinv[Op];
+                for (int h = 0; h < dp; ++h) {
+                    cld acc{0, 0};
+                    for (int i = 0; i < dp; ++i)
+                        acc += Si[static_cast<size_t>(h) * dp + i] * v[static_cast<size_t>(blk) * dp + i];
+                    u[static_cast<size_t>(blk) * dp + h] = acc;
+                }
             }
+            for (int g = 0; g < 8; ++g)
+                for (int h = 0; h < dp; ++h) {
+                    cld acc{0, 0};
+                    for (int blk = 0; blk < 8; ++blk)
+                        acc += Kinv[g * 8 + blk] * u[static_cast<size_t>(blk) * dp + h];
+                    if (std::abs(acc) >= kPrune)
+                        out.push_back({static_cast<int32_t>(static_cast<int64_t>(g) * m3 + memp[h]),
+                                       static_cast<int32_t>(c), snap(acc)});
+                }
         }
-        u.assign(static_cast<size_t>(8) * dp, cld{0, 0});
-        for (int blk = 0; blk < 8; ++blk) {
-            const auto& Si = Sm[blk].Sinv[Op];
-            for (int h = 0; h < dp; ++h) {
-                cld acc{0, 0};
-                for (int i = 0; i < dp; ++i) acc += Si[static_cast<size_t>(h) * dp + i] * v[static_cast<size_t>(blk) * dp + i];
-                u[static_cast<size_t>(blk) * dp + h] = acc;
-            }
-        }
-        for (int g = 0; g < 8; ++g)
-            for (int h = 0; h < dp; ++h) {
-                cld acc{0, 0};
-                for (int blk = 0; blk < 8; ++blk) acc += Kinv[g * 8 + blk] * u[static_cast<size_t>(blk) * dp + h];
-                if (std::abs(acc) >= kPrune)
-                    rows[static_cast<int64_t>(g) * m3 + memp[h]].emplace_back(static_cast<int32_t>(c), snap(acc));
-            }
-    }
-    SparseLD out;
-    out.dim = n3;
-    out.rowptr.assign(n3 + 1, 0);
-    for (int64_t r = 0; r < n3; ++r) {
-        auto& rr = rows[r];
-        std::sort(rr.begin(), rr.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-        for (const auto& e : rr) {
-            out.col.push_back(e.first);
-            out.val.push_back(e.second);
-        }
-        out.rowptr[r + 1] = out.nnz();
-    }
-    return out;
+    });
 }
 
 // B^{-1} = S_n^{-1} Phi^{-1} blockdiag(S_m(child)) (K (x) I), column by column.
@@ -360,21 +395,25 @@ SparseLD derive_Binv(int n, const OrbitBlocks& Sn, const std::array<OrbitBlocks,
     const int64_t n3 = cube(n), m3 = cube(m);
     const auto& on = *Sn.orb;
     const auto& om = orbits(m);
-    std::vector<std::vector<std::pair<int32_t, cld>>> rows(n3);
-    std::unordered_map<int64_t, cld> x;
-    std::vector<cld> w;
-    for (int g = 0; g < 8; ++g)
-        for (int64_t h = 0; h < m3; ++h) {
-            const int64_t col = g * m3 + h;
+    const auto root = roots_of_unity(n);
+    return columns_parallel(n3, [&](int64_t c0, int64_t c1, std::vector<Triplet>& out) {
+        std::vector<cld> x(n3, cld{0, 0});  // dense scratch + touched list
+        std::vector<char> hit(n3, 0);
+        std::vector<int32_t> touched;
+        std::vector<cld> w;
+        for (int64_t col = c0; col < c1; ++col) {
+            const int g = static_cast<int>(col / m3);
+            const int64_t h = col % m3;
             const int Op = om.orbit_of[h], jh = om.pos[h];
             const auto& memp = om.members[Op];
             const int dp = static_cast<int>(memp.size());
             w.assign(static_cast<size_t>(8) * dp, cld{0, 0});
             for (int blk = 0; blk < 8; ++blk) {
                 const auto& S = Sm[blk].S[Op];
-                for (int i = 0; i < dp; ++i) w[static_cast<size_t>(blk) * dp + i] = S[static_cast<size_t>(i) * dp + jh] * K[blk * 8 + g];
+                for (int i = 0; i < dp; ++i)
+                    w[static_cast<size_t>(blk) * dp + i] = S[static_cast<size_t>(i) * dp + jh] * K[blk * 8 + g];
             }
-            x.clear();
+            touched.clear();
             for (int i = 0; i < dp; ++i) {
                 const Index3 ap = unlex(memp[i], m);
                 for (int delta = 0; delta < 8; ++delta) {
@@ -383,7 +422,7 @@ SparseLD derive_Binv(int n, const OrbitBlocks& Sn, const std::array<OrbitBlocks,
                     for (int blk = 0; blk < 8; ++blk) {
                         const int ir = blk >> 2, is = (blk >> 1) & 1, it = blk & 1;
                         const long double sign = ((dr * ir + ds * is + dt * it) & 1) ? -1.0L : 1.0L;
-                        const cld tw = unit_phase_ld(-static_cast<long double>(ap[0] * ir + ap[1] * is + ap[2] * it) / n);
+                        const cld tw = std::conj(root[(ap[0] * ir + ap[1] * is + ap[2] * it) % n]);
                         val += sign * tw * w[static_cast<size_t>(blk) * dp + i];
                     }
                     val /= 8.0L;
@@ -393,25 +432,23 @@ SparseLD derive_Binv(int n, const OrbitBlocks& Sn, const std::array<OrbitBlocks,
                     const auto& mem = on.members[O];
                     const int d = static_cast<int>(mem.size());
                     const auto& Si = Sn.Sinv[O];
-                    for (int k = 0; k < d; ++k) x[mem[k]] += Si[static_cast<size_t>(k) * d + pa] * val;
+                    for (int k = 0; k < d; ++k) {
+                        const int32_t r = mem[k];
+                        if (!hit[r]) {
+                            hit[r] = 1;
+                            touched.push_back(r);
+                        }
+                        x[r] += Si[static_cast<size_t>(k) * d + pa] * val;
+                    }
                 }
             }
-            for (const auto& [row, val] : x)
-                if (std::abs(val) >= kPrune) rows[row].emplace_back(static_cast<int32_t>(col), snap(val));
+            for (int32_t r : touched) {
+                if (std::abs(x[r]) >= kPrune) out.push_back({r, static_cast<int32_t>(col), snap(x[r])});
+                x[r] = cld{0, 0};
+                hit[r] = 0;
+            }
         }
-    SparseLD out;
-    out.dim = n3;
-    out.rowptr.assign(n3 + 1, 0);
-    for (int64_t r = 0; r < n3; ++r) {
-        auto& rr = rows[r];
-        std::sort(rr.begin(), rr.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-        for (const auto& e : rr) {
-            out.col.push_back(e.first);
-            out.val.push_back(e.second);
-        }
-        out.rowptr[r + 1] = out.nnz();
-    }
-    return out;
+    });
 }
 
 std::shared_ptr<const PlanNode> make_node(int n, const Params& p, bool check) {
@@ -463,8 +500,17 @@ std::shared_ptr<const PlanNode> make_node(int n, const Params& p, bool check) {
     }
     const int m = n / 2;
     node->radix = true;
-    for (int blk = 0; blk < 8; ++blk)
-        node->children[blk] = make_node(m, p.child(blk >> 2, (blk >> 1) & 1, blk & 1), check);
+    if (m >= 8) {  // independent subtrees: build them concurrently
+        std::array<std::future<std::shared_ptr<const PlanNode>>, 8> fut;
+        for (int blk = 0; blk < 8; ++blk)
+            fut[blk] = std::async(std::launch::async, [&, blk] {
+                return make_node(m, p.child(blk >> 2, (blk >> 1) & 1, blk & 1), check);
+            });
+        for (int blk = 0; blk < 8; ++blk) node->children[blk] = fut[blk].get();
+    } else {
+        for (int blk = 0; blk < 8; ++blk)
+            node->children[blk] = make_node(m, p.child(blk >> 2, (blk >> 1) & 1, blk & 1), check);
+    }
     // kernel = dense_transform(2, p).matrix (transform.cpp:397): rows = nodes blk, cols = g
     std::vector<cld> K(64), Kinv;
     for (int blk = 0; blk < 8; ++blk)
