@@ -110,6 +110,95 @@ def run_cpu_baseline(n: int, blocks: int, threads: int, method: str = "fast") ->
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
+CONFIGS = {
+    # BASELINE.json configs restated on the reference's n^3 index set
+    "c2": dict(n=8, blocks=65536, scaling="weak", desc="batched FCC-DCT n=8, 65,536 blocks per GPU, i.i.d. U[-1,1] re/im"),
+    "c3": dict(n=16, blocks=16384, scaling="weak",
+               desc="batched FCC-DCT n=16, 16,384 blocks per GPU, 8 seeded Gaussian blobs (sigma U[0.05,0.3] x extent) + N(0,0.01) noise at the FCC node coordinates"),
+    "c4": dict(n=64, blocks=1, scaling="weak", desc="single FCC-DCT n=64 (262,144 points), i.i.d. U[-1,1] re/im"),
+    "c5": dict(n=8, blocks=185193, scaling="strong",
+               desc="whole volume: 57^3 = 185,193 n=8 FCC blocks (~512^3 CC equivalent), 4-octave seeded Perlin noise in [0,1], sharded across GPUs"),
+}
+
+
+def node_real_coords(n, dev):
+    """Real coordinates ((x+z)/2, Re y, (x-z)/(2i)) of the canonical skew nodes
+    (real_coords, chebyshev.cpp:383-393), from the device-generated node set."""
+    from paper_1807_10058_b200 import SkewParams, skew_nodes
+
+    nodes = skew_nodes(n, SkewParams.canonical(), device=dev)
+    x, y, z = nodes[:, 3], nodes[:, 4], nodes[:, 5]
+    return torch_stack_real([(0.5 * (x + z)).real, y.real, ((x - z) / 2j).real])
+
+
+def torch_stack_real(cols):
+    import torch
+
+    return torch.stack(cols, dim=1)
+
+
+def gaussian_blobs(n, blocks, gen, dev, dtype):
+    import torch
+
+    pos = node_real_coords(n, dev).to(dtype)  # [N, 3]
+    lo, hi = pos.min(0).values, pos.max(0).values
+    ext = (hi - lo).max()
+    out = torch.zeros((blocks, n**3), dtype=dtype, device=dev)
+    for _ in range(8):
+        c = lo + (hi - lo) * torch.rand((blocks, 3), generator=gen, device=dev, dtype=dtype)
+        sig = ext * (0.05 + 0.25 * torch.rand((blocks, 1), generator=gen, device=dev, dtype=dtype))
+        amp = torch.rand((blocks, 1), generator=gen, device=dev, dtype=dtype)
+        d2 = ((pos[None, :, :] - c[:, None, :]) ** 2).sum(-1)
+        out += amp * torch.exp(-0.5 * d2 / sig**2)
+    out += 0.1 * torch.randn((blocks, n**3), generator=gen, device=dev, dtype=dtype)
+    return out
+
+
+def perlin_volume(n, b0, b1, side, gen_seed, dev, dtype):
+    """4-octave gradient noise in [0,1] at block-local positions
+    (bx + (i+1/2)/n, by + (j+1/2)/n, bz + (k+1/2)/n) of blocks [b0, b1) of a side^3 volume."""
+    import torch
+
+    g = torch.Generator(device="cpu").manual_seed(gen_seed)
+    perm = torch.randperm(256, generator=g)
+    perm = torch.cat([perm, perm]).to(dev)
+    grads = torch.nn.functional.normalize(torch.randn((256, 3), generator=g), dim=1).to(dev, dtype)
+    bid = torch.arange(b0, b1, device=dev)
+    bx, by, bz = bid // (side * side), (bid // side) % side, bid % side
+    ii = torch.arange(n, device=dev, dtype=dtype)
+    off = (ii + 0.5) / n
+    P = torch.stack(torch.meshgrid(off, off, off, indexing="ij"), dim=-1).reshape(-1, 3)  # [N, 3]
+    pts = torch.stack([bx, by, bz], dim=1).to(dtype)[:, None, :] + P[None, :, :]  # [B, N, 3]
+
+    def fade(t):
+        return t * t * t * (t * (t * 6 - 15) + 10)
+
+    def noise(p):
+        pi = torch.floor(p).long()
+        pf = p - pi
+        u = fade(pf)
+        res = 0
+        for dx in (0, 1):
+            for dy in (0, 1):
+                for dz in (0, 1):
+                    h = perm[(perm[(perm[(pi[..., 0] + dx) & 255] + pi[..., 1] + dy) & 255] + pi[..., 2] + dz) & 255]
+                    d = pf - torch.tensor([dx, dy, dz], device=dev, dtype=dtype)
+                    dot = (grads[h] * d).sum(-1)
+                    w = (u[..., 0] if dx else 1 - u[..., 0]) * (u[..., 1] if dy else 1 - u[..., 1]) * (
+                        u[..., 2] if dz else 1 - u[..., 2])
+                    res = res + w * dot
+        return res
+
+    field = 0
+    amp, freq, norm = 1.0, 1.0 / 8.0, 0.0
+    for _ in range(4):
+        field = field + amp * noise(pts * freq)
+        norm += amp
+        amp *= 0.5
+        freq *= 2.0
+    return (0.5 + 0.5 * field / norm).clamp(0, 1)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -121,9 +210,15 @@ def reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    cfg = CONFIGS[args.config]
+    args.n = args.n if args.n is not None else cfg["n"]
+    args.precision = args.precision or ("f32" if args.config == "c5" else "f64")
+    if args.n > 16:
+        print(json.dumps({"impl": "reference", "unavailable": f"n={args.n}: the reference-faithful plan derivation needs dense child LUs of (n/2)^3 (~137 GB at n=64, SURVEY.md §0.6)"}), flush=True)
+        return
     threads = os.cpu_count() or 1
     # each step: a bounded sample of the workload (forward + inverse of `sample` blocks)
-    sample = args.cpu_sample
+    sample = min(args.cpu_sample, max(1, 2**25 // args.n**3))
     vals = []
     res = None
     for i in range(args.warmup + args.steps):
@@ -145,7 +240,7 @@ def reference_arm(args):
         "vs_baseline": None,
         "dtype": "f64" if args.precision == "f64" else "f32",
         "data": "synthetic",
-        "config": {"workload": f"c2: batched FCC-DCT n={args.n} (N={args.n**3} points/block), {args.method} path, forward+inverse; CPU sample of {sample} blocks per step"},
+        "config": {"workload": f"{args.config}: {cfg['desc']}; n={args.n} (N={args.n**3} points/block), {args.method} path, forward+inverse; CPU sample of {sample} blocks per step"},
         "points_per_s": v * args.n**3,
         "cpu_baseline": {
             "value": v,
@@ -171,14 +266,19 @@ def b200_arm(args):
         dist.init_process_group("nccl", init_method="env://")
     dev = torch.device(f"cuda:{local if world > 1 else 0}")
     torch.cuda.set_device(dev)
-    n = args.n
+    cfg = CONFIGS[args.config]
+    n = args.n if args.n is not None else cfg["n"]
     N = n**3
+    if args.config == "c5" and args.precision is None:
+        args.precision = "f32"
+    args.precision = args.precision or "f64"
     f32 = args.precision == "f32"
     cdt = torch.complex64 if f32 else torch.complex128
     rdt = torch.float32 if f32 else torch.float64
     esize = 8 if f32 else 16
     p = SkewParams.canonical()
-    total = args.blocks * world
+    per_gpu = args.blocks if args.blocks is not None else cfg["blocks"]
+    total = per_gpu if cfg["scaling"] == "strong" else per_gpu * world
     b0, b1 = shard_range(total, rank, world)
     blocks = b1 - b0
 
@@ -190,8 +290,14 @@ def b200_arm(args):
 
     # seeded synthetic input, resident in HBM before the timed region
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    x = torch.complex(torch.rand((blocks, N), generator=g, device=dev, dtype=rdt) * 2 - 1,
-                      torch.rand((blocks, N), generator=g, device=dev, dtype=rdt) * 2 - 1).to(cdt)
+    if args.config == "c3":
+        x = gaussian_blobs(n, blocks, g, dev, rdt).to(cdt)
+    elif args.config == "c5":
+        side = round(total ** (1.0 / 3.0))
+        x = perlin_volume(n, b0, b1, side, 5, dev, rdt).to(cdt)
+    else:
+        x = torch.complex(torch.rand((blocks, N), generator=g, device=dev, dtype=rdt) * 2 - 1,
+                          torch.rand((blocks, N), generator=g, device=dev, dtype=rdt) * 2 - 1).to(cdt)
     y = torch.empty_like(x)
     z = torch.empty_like(x)
     stream = torch.cuda.current_stream(dev)
@@ -242,7 +348,7 @@ def b200_arm(args):
     # e2e: the reference-facing host-buffer API (H2D + transform + D2H each call)
     e2e = None
     if not args.no_e2e:
-        eb = min(blocks, args.e2e_blocks)
+        eb = max(1, min(blocks, args.e2e_blocks))
         xh = x[:eb].cpu().pin_memory()
         yh = torch.empty_like(xh).pin_memory()
         zh = torch.empty_like(xh).pin_memory()
@@ -307,13 +413,14 @@ def b200_arm(args):
     cpu = None
     if not args.no_cpu and world >= 1:
         threads = os.cpu_count() or 1
-        r = run_cpu_baseline(n, args.cpu_sample, threads, args.method)
-        cpu = {
-            "value": 2 * args.cpu_sample / (r["forward_s"] + r["inverse_s"]),
+        sample = min(args.cpu_sample, max(1, 2**24 // N))
+        r = run_cpu_baseline(n, sample, threads, args.method) if n <= 16 else None
+        cpu = None if r is None else {
+            "value": 2 * sample / (r["forward_s"] + r["inverse_s"]),
             "unit": "transforms/s",
             "cores": threads,
             "kind": "port",
-            "sample": f"{args.cpu_sample} blocks of n={n}, forward then inverse, {args.method} path, reference-faithful C++ restatement (oracle/cpu_baseline.cpp)",
+            "sample": f"{sample} blocks of n={n}, forward then inverse, {args.method} path, reference-faithful C++ restatement (oracle/cpu_baseline.cpp)",
         }
     line = {
         "metric": METRIC,
@@ -324,17 +431,19 @@ def b200_arm(args):
         "warmup": args.warmup,
         "ms_per_step": ms / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": cfg["scaling"],
         "vs_baseline": None,
         "dtype": "f64" if not f32 else "f32",
         "data": "synthetic",
         "config": {
-            "workload": f"c2: batched FCC-DCT n={n} (N={N} points/block), {blocks} blocks per GPU, {args.method} path, forward then inverse per step",
+            "workload": f"{args.config}: {cfg['desc']}; n={n} (N={N} points/block), {blocks} blocks on rank 0, {args.method} path, forward then inverse per step",
             "blocks_total": total,
             "points_per_block": N,
             "params": "canonical (1/8, 0, 3/8)",
-            "input": "i.i.d. uniform[-1,1] re/im from a seed (torch Philox on device)",
-            "l2": f"inputs larger than L2 ({blocks * N * esize / 2**20:.0f} MiB per array vs 126 MB L2)",
+            "input": cfg["desc"] + " (seeded, generated on device)",
+            "l2": (f"inputs larger than L2 ({blocks * N * esize / 2**20:.0f} MiB per array vs 126 MB L2)"
+                   if blocks * N * esize > 126e6 else
+                   f"input {blocks * N * esize / 2**20:.1f} MiB is L2-resident (single-transform latency config)"),
             "parallelism": f"batch-sharded dp{world}, no collective",
         },
         "points_per_s": value * N,
@@ -358,10 +467,11 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEFAULT)
-    ap.add_argument("--blocks", type=int, default=BLOCKS_PER_GPU)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--blocks", type=int, default=None)
     ap.add_argument("--method", default="fast", choices=["fast", "direct"])
-    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--precision", default=None, choices=["f64", "f32"])
     ap.add_argument("--cpu-sample", type=int, default=65536)
     ap.add_argument("--e2e-blocks", type=int, default=65536)
     ap.add_argument("--e2e-steps", type=int, default=3)
