@@ -388,7 +388,10 @@ def b200_arm(args):
     bytes_fwd = 2.0 * N * esize * blocks
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6488.0)
-    peak_tf = FP32_PEAK_TFLOPS if f32 else FP64_PEAK_TFLOPS
+    # the roofline of the pipe that executes the plan: the FP64 tensor pipe for
+    # the DMMA executors (fp32 plans there keep fp64 arithmetic, complex64 I/O)
+    on_fp64_pipe = (not f32) or info.executor == 2
+    peak_tf = FP64_PEAK_TFLOPS if on_fp64_pipe else FP32_PEAK_TFLOPS
     achieved_tf = flops_fwd / (fwd_ms / 1e3) / 1e12
     achieved_gbs = bytes_fwd / (fwd_ms / 1e3) / 1e9
     t_star = max(bytes_fwd / (hbm * 1e9), flops_fwd / (peak_tf * 1e12))
@@ -399,13 +402,15 @@ def b200_arm(args):
         "unit": "TFLOP/s",
         "frac": achieved_tf / peak_tf,
         "traffic": args.traffic,
-        "kernel": "fcct pipeline_kernel (forward, fast path)" if args.method == "fast" else "gemm_f64_kernel (direct)",
+        "kernel": {0: "gemm_f64_kernel / gemm_f32_kernel (direct)", 1: "pipeline_kernel (tile interpreter)",
+                   2: "pipeline2_kernel (FP64 tensor pipe)", 3: "gstage_* kernels (global multi-pass)"}[info.executor],
         "algorithmic_flops_per_launch": flops_fwd,
         "algorithmic_bytes_per_launch": bytes_fwd,
         "achieved_gbs": achieved_gbs,
         "hbm_peak_gbs": hbm,
         "t_star_over_t": t_star / (fwd_ms / 1e3),
-        "peak_source": "fp64: measured DMMA m8n8k4 peak (tools/peak_fp.cu, profiles/r01_fp_peaks.txt); HBM: MEASURED_PEAKS.json",
+        "peak_source": ("measured DMMA m8n8k4 f64 peak" if on_fp64_pipe else "measured FFMA fp32 peak")
+                       + " (tools/peak_fp.cu, profiles/r01_fp_peaks.txt); HBM: MEASURED_PEAKS.json",
         "fwd_ms": fwd_ms,
         "inv_ms": inv_ms,
         "inverse_achieved_tflops": info.flops_inverse * blocks / (inv_ms / 1e3) / 1e12,

@@ -46,6 +46,7 @@ class PlanInfo(ctypes.Structure):
         ("condition", c_double),
         ("flops_forward", c_double),
         ("flops_inverse", c_double),
+        ("executor", c_int),
     ]
 
 

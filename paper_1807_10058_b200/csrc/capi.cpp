@@ -503,7 +503,6 @@ void build_v2(fcct_plan_s* pl) {
     pl->v2 = false;
     const char* force = std::getenv("FCCT_PIPELINE");
     if (force && std::string(force) == "v1") return;
-    if (pl->precision != FCCT_F64) return;
     Shape2 shape;  // default: 16 blocks x 16 warps, one CTA per SM
     if (const char* sh = std::getenv("FCCT_V2_SHAPE"); sh && std::string(sh) == "8x8")
         shape = Shape2{8, 8, 8};  // two CTAs per SM (tuning experiment)
@@ -511,6 +510,10 @@ void build_v2(fcct_plan_s* pl) {
     if (!compile_pipeline2(*pl->tree, false, shape, hf) || !compile_pipeline2(*pl->tree, true, shape, hi)) return;
     upload_pipeline2(hf, pl->fwd2);
     upload_pipeline2(hi, pl->inv2);
+    // fp32 plans: complex64 in HBM, fp64 arithmetic in the tile (the FP64 tensor
+    // pipe has no fp32 kind; TF32 would miss the 1e-5 bar)
+    pl->fwd2.desc.io_f32 = pl->inv2.desc.io_f32 = pl->precision == FCCT_F32 ? 1 : 0;
+    if (pl->fwd2.desc.io_f32) pl->fwd2.desc.direct_store = pl->inv2.desc.direct_store = 0;
     pl->v2 = true;
 }
 
@@ -551,6 +554,7 @@ void fill_info(fcct_plan_s* pl) {
     in.method = pl->radix ? FCCT_FAST : FCCT_DIRECT;
     in.precision = pl->precision;
     in.points = cube(pl->n);
+    in.executor = !pl->radix ? 0 : (pl->v2 ? 2 : (pl->global ? 3 : 1));
     const double N = static_cast<double>(in.points);
     if (pl->radix) {
         in.levels = tree_levels(pl->n);

@@ -512,8 +512,10 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
 
 template <int TB, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
-    pipeline2_kernel(const __grid_constant__ Pipeline2Desc d, const double* __restrict__ in, double* __restrict__ out,
+    pipeline2_kernel(const __grid_constant__ Pipeline2Desc d, const void* __restrict__ in_raw, void* __restrict__ out_raw,
                      int64_t batch) {
+    const double* __restrict__ in = static_cast<const double*>(in_raw);
+    double* __restrict__ out = static_cast<double*>(out_raw);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     double* X = reinterpret_cast<double*>(smem_raw + 128);
@@ -561,13 +563,36 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
         const int64_t t0 = tile * TB;
         const int nvalid = static_cast<int>(batch - t0 < TB ? batch - t0 : TB);
         long long c0 = timing ? clock64() : 0;
-        if (threadIdx.x == 0) {
-            tma_store_wait_read0();
-            const int64_t nt = tile + gridDim.x;
-            issue_tile_load<TB>(NextLoad{in, bar, X, stride, dimr, tile, batch, nt < ntiles ? nt : -1});
+        if (d.io_f32) {
+            // complex64 rows -> fp64 tile (coalesced float4 loads, 2 points each)
+            const float4* src = reinterpret_cast<const float4*>(in_raw) + t0 * (d.N / 2);
+            const int per_row = d.N / 2;
+            for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
+                const int t = i / per_row, q = i - t * per_row;
+                const float4 v = __ldg(src + static_cast<int64_t>(t) * per_row + q);
+                double2* xr = reinterpret_cast<double2*>(X + t * stride) + 2 * q;
+                xr[0] = make_double2(v.x, v.y);
+                xr[1] = make_double2(v.z, v.w);
+            }
+            if (threadIdx.x == 0) {
+                const int64_t nt = tile + gridDim.x;
+                if (nt < ntiles) {
+                    const int64_t n0 = nt * TB;
+                    const int nv = static_cast<int>(batch - n0 < TB ? batch - n0 : TB);
+                    prefetch_l2_bulk(reinterpret_cast<const float*>(in_raw) + n0 * dimr,
+                                     static_cast<uint32_t>(nv * dimr * sizeof(float)));
+                }
+            }
+            __syncthreads();
+        } else {
+            if (threadIdx.x == 0) {
+                tma_store_wait_read0();
+                const int64_t nt = tile + gridDim.x;
+                issue_tile_load<TB>(NextLoad{in, bar, X, stride, dimr, tile, batch, nt < ntiles ? nt : -1});
+            }
+            mbar_wait(bar, phase);
+            phase ^= 1;
         }
-        mbar_wait(bar, phase);
-        phase ^= 1;
         if (timing) {
             const long long c1 = clock64();
             tacc[0] += c1 - c0;
@@ -583,6 +608,19 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
                 tacc[1 + kMaxStages / 2 + s] += c1 - tmid;  // store phase + final barrier
                 c0 = c1;
             }
+        }
+        if (d.io_f32) {
+            float4* dst = reinterpret_cast<float4*>(out_raw) + t0 * (d.N / 2);
+            const int per_row = d.N / 2;
+            for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
+                const int t = i / per_row, q = i - t * per_row;
+                const double2* xr = reinterpret_cast<const double2*>(X + t * stride) + 2 * q;
+                const double2 a = xr[0], b = xr[1];
+                dst[static_cast<int64_t>(t) * per_row + q] = make_float4(static_cast<float>(a.x), static_cast<float>(a.y),
+                                                                       static_cast<float>(b.x), static_cast<float>(b.y));
+            }
+            __syncthreads();
+            continue;
         }
         fence_proxy_async_smem();
         __syncthreads();
@@ -611,8 +649,7 @@ cudaError_t launch_pipeline2_t(const Pipeline2Desc& d, const void* in, void* out
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (batch + TB - 1) / TB;
     const int64_t grid = std::min<int64_t>(ntiles, static_cast<int64_t>(per_sm) * num_sms);
-    kern<<<static_cast<unsigned>(grid), WARPS * 32, smem, st>>>(d, static_cast<const double*>(in),
-                                                                 static_cast<double*>(out), batch);
+    kern<<<static_cast<unsigned>(grid), WARPS * 32, smem, st>>>(d, in, out, batch);
     return cudaGetLastError();
 }
 

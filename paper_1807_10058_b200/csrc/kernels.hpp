@@ -66,6 +66,7 @@ struct Pipeline2Desc {
     int stride;  // doubles per block row in shared memory
     int nstages;
     int direct_store;  // 1: last stage stores to global from registers; 0: smem + TMA bulk store
+    int io_f32;        // 1: global data is complex64 (converted to/from fp64 at tile load/store)
     int stage_mask;    // debug/timing only: stages with a cleared bit are skipped
     unsigned long long* timing;  // debug: CTA 0 accumulates clock64 per phase (nullptr: off)
     Stage2Dev st[kMaxStages];
