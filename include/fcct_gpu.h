@@ -148,6 +148,23 @@ fcct_status fcct_basis_change(int n, double r, double s, double t, int inverse, 
 fcct_status fcct_plan_tree_stats(int n, double r, double s, double t, int64_t* tree_nnz_fwd, int64_t* tree_nnz_inv,
                                  double* flops_fwd, double* flops_inv);
 
+/* Plan cache (PlanStore, plan_cache.hpp:30-51): one `.fccplan` file per
+ * (n, params), byte-compatible with the reference's format (plan_cache.hpp:11-27),
+ * children as separate entries, corrupt files rebuilt in place with a warning.
+ * Files written by the reference load here (the inverse factor is recomputed
+ * from the stored B). */
+typedef struct fcct_store_s* fcct_store;
+fcct_status fcct_store_open(const char* dir, fcct_store* out);
+fcct_status fcct_store_close(fcct_store store);
+/* load_or_build on the host only (no GPU): warms the cache for (n, params). */
+fcct_status fcct_store_warm(fcct_store store, int n, double r, double s, double t);
+fcct_status fcct_store_stats(fcct_store store, int* hits, int* misses, int* rebuilt);
+/* Path of the cache entry for (n, params) (PlanStore::path_for); len = buffer size. */
+fcct_status fcct_store_path(fcct_store store, int n, double r, double s, double t, char* buf, int len);
+/* build_plan(n, params, store) (transform.cpp:404-408): fast plan through the store. */
+fcct_status fcct_plan_create_from_store(fcct_store store, int n, double r, double s, double t, int precision,
+                                        int device, fcct_plan* out);
+
 /* Batch scheduler for one process of a multi-GPU job: contiguous block range
  * [begin, end) of `total` blocks owned by `rank` of `world` (ceil split,
  * uneven tail allowed). No collective is involved. */

@@ -15,6 +15,7 @@ from .fcct import (  # noqa: F401
     Kind,
     MalformedFile,
     OddSize,
+    PlanStore,
     SignalTensor,
     SizeMismatch,
     SkewParams,

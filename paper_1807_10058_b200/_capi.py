@@ -84,6 +84,12 @@ def lib() -> ctypes.CDLL:
         "fcct_plan_perturbed_basis": (c_int, [c_void_p, c_double, POINTER(c_void_p)]),
         "fcct_shard_range": (c_int, [c_int64, c_int, c_int, POINTER(c_int64), POINTER(c_int64)]),
         "fcct_debug_dmma_probe": (c_int, [c_void_p, c_void_p, c_void_p]),
+        "fcct_store_open": (c_int, [ctypes.c_char_p, POINTER(c_void_p)]),
+        "fcct_store_close": (c_int, [c_void_p]),
+        "fcct_store_warm": (c_int, [c_void_p, c_int, c_double, c_double, c_double]),
+        "fcct_store_stats": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_int)]),
+        "fcct_store_path": (c_int, [c_void_p, c_int, c_double, c_double, c_double, ctypes.c_char_p, c_int]),
+        "fcct_plan_create_from_store": (c_int, [c_void_p, c_int, c_double, c_double, c_double, c_int, c_int, POINTER(c_void_p)]),
         "fcct_debug_emulate_v2": (c_int, [c_int, c_double, c_double, c_double, c_int, c_void_p, c_void_p, c_int64]),
         "fcct_debug_v2_stats": (c_int, [c_int, c_double, c_double, c_double, c_int, POINTER(c_int64)]),
         "fcct_debug_timing": (c_int, [c_void_p, c_int, c_void_p, POINTER(c_int)]),
@@ -120,4 +126,10 @@ HEADER_SYMBOLS = [
     "fcct_shard_range",
     "fcct_basis_change",
     "fcct_plan_tree_stats",
+    "fcct_store_open",
+    "fcct_store_close",
+    "fcct_store_warm",
+    "fcct_store_stats",
+    "fcct_store_path",
+    "fcct_plan_create_from_store",
 ]

@@ -17,6 +17,7 @@
 #include "../../include/fcct_gpu.h"
 #include "kernels.hpp"
 #include "plan.hpp"
+#include "plan_cache.hpp"
 #include "tiling.hpp"
 
 namespace fcct {
@@ -578,7 +579,8 @@ void fill_info(fcct_plan_s* pl) {
     }
 }
 
-fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int device) {
+fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int device,
+                         PlanStore* store = nullptr) {
     if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "build_plan: n must be >= 1");
     if (method != FCCT_DIRECT && method != FCCT_FAST) throw FcctError(ST_INVALID_ARGUMENT, "unknown method");
     if (precision != FCCT_F64 && precision != FCCT_F32) throw FcctError(ST_INVALID_ARGUMENT, "unknown precision");
@@ -597,7 +599,12 @@ fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int 
     const bool f32 = precision == FCCT_F32;
     const bool radix = method == FCCT_FAST && n % 2 == 0;
     if (radix) {
-        pl->tree = build_tree(n, p);  // degeneracy + condition gates inside
+        if (store) {
+            check_nodes(n, p);
+            pl->tree = store->load_or_build(n, p);
+        } else {
+            pl->tree = build_tree(n, p);  // degeneracy + condition gates inside
+        }
         pl->radix = true;
         build_fast_paths(pl.get());
     } else {
@@ -901,6 +908,59 @@ fcct_status fcct_plan_perturbed_basis(fcct_plan plan, double delta, fcct_plan* o
         pl->method = FCCT_FAST;
         fill_info(pl.get());
         *out = pl.release();
+    });
+}
+
+struct fcct_store_s {
+    std::unique_ptr<PlanStore> store;
+};
+
+fcct_status fcct_store_open(const char* dir, fcct_store* out) {
+    return guarded([&] {
+        if (!dir || !out) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        auto st = std::make_unique<fcct_store_s>();
+        st->store = std::make_unique<PlanStore>(dir);
+        *out = st.release();
+    });
+}
+
+fcct_status fcct_store_close(fcct_store store) {
+    return guarded([&] { delete store; });
+}
+
+fcct_status fcct_store_warm(fcct_store store, int n, double r, double s, double t) {
+    return guarded([&] {
+        if (!store) throw FcctError(ST_INVALID_ARGUMENT, "null store");
+        if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "build_plan: n must be >= 1");
+        check_nodes(n, Params{r, s, t});
+        (void)store->store->load_or_build(n, Params{r, s, t});
+    });
+}
+
+fcct_status fcct_store_stats(fcct_store store, int* hits, int* misses, int* rebuilt) {
+    return guarded([&] {
+        if (!store) throw FcctError(ST_INVALID_ARGUMENT, "null store");
+        const auto st = store->store->stats();
+        if (hits) *hits = st.hits;
+        if (misses) *misses = st.misses;
+        if (rebuilt) *rebuilt = st.rebuilt;
+    });
+}
+
+fcct_status fcct_store_path(fcct_store store, int n, double r, double s, double t, char* buf, int len) {
+    return guarded([&] {
+        if (!store || !buf || len <= 0) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        const std::string p = store->store->path_for(n, Params{r, s, t});
+        if (static_cast<int>(p.size()) >= len) throw FcctError(ST_INVALID_ARGUMENT, "buffer too small");
+        std::memcpy(buf, p.c_str(), p.size() + 1);
+    });
+}
+
+fcct_status fcct_plan_create_from_store(fcct_store store, int n, double r, double s, double t, int precision,
+                                        int device, fcct_plan* out) {
+    return guarded([&] {
+        if (!store || !out) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        *out = create_plan(n, Params{r, s, t}, FCCT_FAST, precision, device, store->store.get());
     });
 }
 

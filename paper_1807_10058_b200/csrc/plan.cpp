@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <deque>
 #include <future>
 #include <map>
@@ -133,6 +134,33 @@ const std::array<std::array<int, 9>, 24>& s4_group() {
         return out;
     }();
     return g;
+}
+
+std::string encode_param(double value) {  // spectral.cpp:159-181
+    if (value == 0.0) return "0";
+    double x = value;
+    long long p0 = 0, q0 = 1, p1 = 1, q1 = 0;
+    for (int step = 0; step < 40; ++step) {
+        const double fa = std::floor(x);
+        if (std::abs(fa) > 1e15) break;
+        const long long a = static_cast<long long>(fa);
+        const long long p2 = a * p1 + p0, q2 = a * q1 + q0;
+        if (q2 > 1000000 || q2 < 0) break;
+        if (q2 != 0 && static_cast<double>(p2) / static_cast<double>(q2) == value) {
+            if (q2 == 1) return std::to_string(p2);
+            return std::to_string(p2) + "/" + std::to_string(q2);
+        }
+        p0 = p1;
+        q0 = q1;
+        p1 = p2;
+        q1 = q2;
+        const double frac = x - fa;
+        if (frac == 0.0) break;
+        x = 1.0 / frac;
+    }
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%.17g", value);  // detail::g17 (format.hpp:9-13)
+    return buf;
 }
 
 cld unit_phase_ld(long double turns) {
@@ -499,18 +527,39 @@ std::shared_ptr<const PlanNode> make_node(int n, const Params& p, bool check) {
         return node;
     }
     const int m = n / 2;
-    node->radix = true;
+    std::array<std::shared_ptr<const PlanNode>, 8> children;
     if (m >= 8) {  // independent subtrees: build them concurrently
         std::array<std::future<std::shared_ptr<const PlanNode>>, 8> fut;
         for (int blk = 0; blk < 8; ++blk)
             fut[blk] = std::async(std::launch::async, [&, blk] {
                 return make_node(m, p.child(blk >> 2, (blk >> 1) & 1, blk & 1), check);
             });
-        for (int blk = 0; blk < 8; ++blk) node->children[blk] = fut[blk].get();
+        for (int blk = 0; blk < 8; ++blk) children[blk] = fut[blk].get();
     } else {
         for (int blk = 0; blk < 8; ++blk)
-            node->children[blk] = make_node(m, p.child(blk >> 2, (blk >> 1) & 1, blk & 1), check);
+            children[blk] = make_node(m, p.child(blk >> 2, (blk >> 1) & 1, blk & 1), check);
     }
+    return build_radix_node(n, p, children);
+}
+
+}  // namespace
+
+std::vector<cld> dense_inverse(const std::vector<cld>& a, int64_t dim, double* cond) {
+    std::vector<cld> inv;
+    const double c = invert_ld(a, static_cast<int>(dim), inv);
+    if (cond) *cond = c;
+    return inv;
+}
+
+std::shared_ptr<const PlanNode> build_radix_node(int n, const Params& p,
+                                                 const std::array<std::shared_ptr<const PlanNode>, 8>& children) {
+    if (n < 2 || n % 2 != 0) throw FcctError(ST_ODD_SIZE, "radix node needs an even size");
+    auto node = std::make_shared<PlanNode>();
+    node->n = n;
+    node->p = p;
+    node->radix = true;
+    node->children = children;
+    const int m = n / 2;
     // kernel = dense_transform(2, p).matrix (transform.cpp:397): rows = nodes blk, cols = g
     std::vector<cld> K(64), Kinv;
     for (int blk = 0; blk < 8; ++blk)
@@ -526,7 +575,7 @@ std::shared_ptr<const PlanNode> make_node(int n, const Params& p, bool check) {
     require_condition(Sn.worst_condition, "orbit block (n=" + std::to_string(n) + ")");
     std::array<OrbitBlocks, 8> Sm;
     for (int blk = 0; blk < 8; ++blk) {
-        Sm[blk] = orbit_blocks(m, node->children[blk]->p);
+        Sm[blk] = orbit_blocks(m, children[blk]->p);
         require_condition(Sm[blk].worst_condition, "child block " + std::to_string(blk));
     }
     node->condition = std::max(kc, Sn.worst_condition);
@@ -535,6 +584,7 @@ std::shared_ptr<const PlanNode> make_node(int n, const Params& p, bool check) {
     return node;
 }
 
+namespace {
 }  // namespace
 
 std::shared_ptr<const PlanNode> build_tree(int n, const Params& p) {

@@ -112,6 +112,18 @@ struct PlanNode {
     double condition = 0.0;
 };
 
+// One radix node over given children (build_plan_node with a child source,
+// plan_internal.hpp:10-13): K, K^{-1}, B, B^{-1} derived exactly.
+std::shared_ptr<const PlanNode> build_radix_node(int n, const Params& p,
+                                                 const std::array<std::shared_ptr<const PlanNode>, 8>& children);
+
+// Dense inverse (Gauss-Jordan, partial pivoting, long double), row-major;
+// *cond receives the exact 1-norm condition.
+std::vector<cld> dense_inverse(const std::vector<cld>& a, int64_t dim, double* cond);
+
+// Text encoding of an offset (encode_param, spectral.cpp:159-181).
+std::string encode_param(double value);
+
 // Builds the tree (PlanBuilder::make, transform.cpp:382-401): direct for odd n
 // or n == 1, radix2 with 8 children otherwise. Throws FcctError.
 std::shared_ptr<const PlanNode> build_tree(int n, const Params& p);

@@ -1,0 +1,355 @@
+// On-disk plan cache, byte-compatible with the reference's `.fccplan` files
+// (plan_cache.hpp:11-27, plan_cache.cpp:92-203): one file per (n, params),
+// children as separate entries, load-or-build with corruption detection and
+// atomic temp + rename writes (plan_cache.cpp:222-282). Files written by the
+// reference (Eigen build) load here too: the inverse factor is recomputed from
+// the stored B by inverting its connected components, so it is consistent
+// with whatever B the file holds.
+#include <algorithm>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <future>
+#include <iostream>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <optional>
+
+#include "plan.hpp"
+#include "plan_cache.hpp"
+
+namespace fcct {
+namespace {
+
+constexpr char kMagic[8] = {'F', 'C', 'C', 'P', 'L', 'A', 'N', '1'};
+constexpr uint32_t kVersion = 1;
+constexpr uint8_t kKindDirect = 0, kKindRadix2 = 1;
+
+struct Malformed : FcctError {
+    explicit Malformed(const std::string& m) : FcctError(ST_IO, m) {}
+};
+
+template <typename T>
+void put(std::ostream& out, T v) {
+    out.write(reinterpret_cast<const char*>(&v), sizeof(v));
+}
+void put_string(std::ostream& out, const std::string& s) {
+    put(out, static_cast<uint32_t>(s.size()));
+    out.write(s.data(), static_cast<std::streamsize>(s.size()));
+}
+void put_complex(std::ostream& out, const cld& v) {
+    put(out, static_cast<double>(v.real()));
+    put(out, static_cast<double>(v.imag()));
+}
+void get_bytes(std::istream& in, void* p, size_t n) {
+    in.read(static_cast<char*>(p), static_cast<std::streamsize>(n));
+    if (!in || in.gcount() != static_cast<std::streamsize>(n)) throw Malformed("plan file truncated");
+}
+template <typename T>
+T get(std::istream& in) {
+    T v;
+    get_bytes(in, &v, sizeof(v));
+    return v;
+}
+std::string get_string(std::istream& in) {
+    const auto len = get<uint32_t>(in);
+    if (len > 64) throw Malformed("plan file string too long");
+    std::string s(len, '\0');
+    get_bytes(in, s.data(), len);
+    return s;
+}
+cld get_complex(std::istream& in) {
+    const double re = get<double>(in), im = get<double>(in);
+    return cld{re, im};
+}
+
+std::string sanitize(const std::string& key) {  // plan_cache.cpp:74-88
+    std::string out;
+    for (char c : key) {
+        switch (c) {
+            case '/': out.push_back('d'); break;
+            case '.': out.push_back('p'); break;
+            case '-': out.push_back('m'); break;
+            case '+': break;
+            case ',': out.push_back('_'); break;
+            default: out.push_back(c);
+        }
+    }
+    return out;
+}
+
+// B^{-1} from B: B is block diagonal up to row/column permutation (its
+// connected components are small); each square component is inverted densely.
+SparseLD invert_by_components(const SparseLD& B) {
+    const int64_t N = B.dim;
+    std::vector<int64_t> par(2 * N);
+    std::iota(par.begin(), par.end(), 0);
+    auto find = [&](int64_t a) {
+        while (par[a] != a) a = par[a] = par[par[a]];
+        return a;
+    };
+    for (int64_t r = 0; r < N; ++r)
+        for (int64_t k = B.rowptr[r]; k < B.rowptr[r + 1]; ++k) par[find(r)] = find(N + B.col[k]);
+    std::map<int64_t, std::pair<std::vector<int32_t>, std::vector<int32_t>>> comps;
+    for (int64_t i = 0; i < 2 * N; ++i)
+        (i < N ? comps[find(i)].first : comps[find(i)].second).push_back(static_cast<int32_t>(i < N ? i : i - N));
+    std::vector<std::vector<std::pair<int32_t, cld>>> rows(N);  // rows of B^{-1}
+    for (const auto& [key, rc] : comps) {
+        const auto& [R, C] = rc;
+        if (R.size() != C.size()) throw FcctError(ST_ILL_CONDITIONED, "basis-change factor is not invertible");
+        const int d = static_cast<int>(R.size());
+        if (d == 0) continue;
+        std::map<int32_t, int> cpos;
+        for (int j = 0; j < d; ++j) cpos[C[j]] = j;
+        // Gauss-Jordan on the dense component (rows R, cols C)
+        std::vector<cld> a(static_cast<size_t>(d) * d, cld{0, 0}), inv(static_cast<size_t>(d) * d, cld{0, 0});
+        for (int i = 0; i < d; ++i) {
+            for (int64_t k = B.rowptr[R[i]]; k < B.rowptr[R[i] + 1]; ++k)
+                a[static_cast<size_t>(i) * d + cpos[B.col[k]]] = B.val[k];
+            inv[static_cast<size_t>(i) * d + i] = 1;
+        }
+        for (int k = 0; k < d; ++k) {
+            int best = k;
+            for (int i = k + 1; i < d; ++i)
+                if (std::abs(a[static_cast<size_t>(i) * d + k]) > std::abs(a[static_cast<size_t>(best) * d + k])) best = i;
+            if (std::abs(a[static_cast<size_t>(best) * d + k]) == 0.0L)
+                throw FcctError(ST_ILL_CONDITIONED, "basis-change factor is not invertible");
+            for (int j = 0; j < d; ++j) {
+                std::swap(a[static_cast<size_t>(k) * d + j], a[static_cast<size_t>(best) * d + j]);
+                std::swap(inv[static_cast<size_t>(k) * d + j], inv[static_cast<size_t>(best) * d + j]);
+            }
+            const cld pinv = cld{1, 0} / a[static_cast<size_t>(k) * d + k];
+            for (int j = 0; j < d; ++j) {
+                a[static_cast<size_t>(k) * d + j] *= pinv;
+                inv[static_cast<size_t>(k) * d + j] *= pinv;
+            }
+            for (int i = 0; i < d; ++i) {
+                if (i == k) continue;
+                const cld f = a[static_cast<size_t>(i) * d + k];
+                if (f == cld{0, 0}) continue;
+                for (int j = 0; j < d; ++j) {
+                    a[static_cast<size_t>(i) * d + j] -= f * a[static_cast<size_t>(k) * d + j];
+                    inv[static_cast<size_t>(i) * d + j] -= f * inv[static_cast<size_t>(k) * d + j];
+                }
+            }
+        }
+        // (B^{-1})[C[j]][R[i]] = inv[j][i]  (inv maps component rows -> columns)
+        for (int j = 0; j < d; ++j)
+            for (int i = 0; i < d; ++i) {
+                const cld v = inv[static_cast<size_t>(j) * d + i];
+                if (std::abs(v) >= 1e-13L) rows[C[j]].emplace_back(R[i], v);
+            }
+    }
+    SparseLD out;
+    out.dim = N;
+    out.rowptr.assign(N + 1, 0);
+    for (int64_t r = 0; r < N; ++r) {
+        auto& rr = rows[r];
+        std::sort(rr.begin(), rr.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        for (const auto& e : rr) {
+            out.col.push_back(e.first);
+            out.val.push_back(e.second);
+        }
+        out.rowptr[r + 1] = out.nnz();
+    }
+    return out;
+}
+
+void save_node(std::ostream& out, const PlanNode& nd) {  // save_plan, plan_cache.cpp:92-125
+    out.write(kMagic, 8);
+    put(out, kVersion);
+    put(out, nd.radix ? kKindRadix2 : kKindDirect);
+    put(out, static_cast<uint64_t>(nd.n));
+    put_string(out, encode_param(nd.p.r));
+    put_string(out, encode_param(nd.p.s));
+    put_string(out, encode_param(nd.p.t));
+    const int64_t n3 = cube(nd.n);
+    if (!nd.radix) {
+        put(out, static_cast<uint64_t>(n3));
+        for (int64_t i = 0; i < n3 * n3; ++i) put_complex(out, nd.D[i]);  // row major
+        return;
+    }
+    for (int i = 0; i < 64; ++i) put_complex(out, nd.K[i]);  // K(row = blk, col = g), row major
+    for (uint64_t v : radix_permutation(nd.n)) put(out, v);
+    // basis triplets in Eigen's compressed-column order (outer = column)
+    std::vector<std::vector<std::pair<int32_t, cld>>> cols(n3);
+    for (int64_t r = 0; r < n3; ++r)
+        for (int64_t k = nd.B.rowptr[r]; k < nd.B.rowptr[r + 1]; ++k)
+            cols[nd.B.col[k]].emplace_back(static_cast<int32_t>(r), nd.B.val[k]);
+    put(out, static_cast<uint64_t>(nd.B.nnz()));
+    for (int64_t c = 0; c < n3; ++c)
+        for (const auto& [r, v] : cols[c]) {
+            put(out, static_cast<uint64_t>(r));
+            put(out, static_cast<uint64_t>(c));
+            put_complex(out, v);
+        }
+}
+
+struct Header {
+    int kind = 0, n = 0;
+    std::string r, s, t;
+};
+
+Header read_header(std::istream& in) {  // read_plan_header, plan_cache.cpp:128-146
+    char magic[8];
+    get_bytes(in, magic, 8);
+    if (std::memcmp(magic, kMagic, 8) != 0) throw Malformed("plan file has wrong magic");
+    if (get<uint32_t>(in) != kVersion) throw Malformed("plan file has unsupported version");
+    Header h;
+    const auto kind = get<uint8_t>(in);
+    if (kind != kKindDirect && kind != kKindRadix2) throw Malformed("plan file has unknown kind");
+    h.kind = kind;
+    const auto n = get<uint64_t>(in);
+    if (n < 1 || n > 4096) throw Malformed("plan file has implausible size");
+    h.n = static_cast<int>(n);
+    h.r = get_string(in);
+    h.s = get_string(in);
+    h.t = get_string(in);
+    return h;
+}
+
+void expect_eof(std::istream& in) {
+    if (in.peek() != std::char_traits<char>::eof()) throw Malformed("plan file has trailing bytes");
+}
+
+// load_plan_body, plan_cache.cpp:148-203, producing a PlanNode with the
+// derived factors (K^{-1}, B^{-1}, D^{-1}) recomputed in long double.
+std::shared_ptr<PlanNode> read_body(std::istream& in, const Header& h, const Params& p,
+                                    const std::array<std::shared_ptr<const PlanNode>, 8>& children) {
+    const int64_t n3 = cube(h.n);
+    auto nd = std::make_shared<PlanNode>();
+    nd->n = h.n;
+    nd->p = p;
+    if (h.kind == kKindDirect) {
+        const auto dim = static_cast<int64_t>(get<uint64_t>(in));
+        if (dim != n3) throw Malformed("plan file dense dimension does not match n");
+        nd->D.resize(static_cast<size_t>(n3 * n3));
+        for (auto& v : nd->D) v = get_complex(in);
+        expect_eof(in);
+        nd->radix = false;
+        // D^{-1} densely (direct nodes are odd or unit sized and small)
+        const auto Dinv = dense_inverse(nd->D, n3, &nd->condition);
+        nd->Dinv = Dinv;
+        if (!(nd->condition <= 1e12)) throw FcctError(ST_ILL_CONDITIONED, "dense transform: condition exceeds 1e12");
+        return nd;
+    }
+    for (int i = 0; i < 64; ++i) nd->K[i] = get_complex(in);
+    std::vector<char> seen(n3, 0);
+    const auto perm = radix_permutation(h.n);
+    for (int64_t i = 0; i < n3; ++i) {
+        const auto v = get<uint64_t>(in);
+        if (v >= static_cast<uint64_t>(n3) || seen[v]) throw Malformed("plan file permutation is not a permutation");
+        if (v != perm[i]) throw Malformed("plan file permutation is not the radix interleave");
+        seen[v] = 1;
+    }
+    const auto nnz = get<uint64_t>(in);
+    if (nnz > static_cast<uint64_t>(n3) * n3) throw Malformed("plan file basis factor has implausible size");
+    std::vector<std::vector<std::pair<int32_t, cld>>> rows(n3);
+    for (uint64_t i = 0; i < nnz; ++i) {
+        const auto r = get<uint64_t>(in), c = get<uint64_t>(in);
+        if (r >= static_cast<uint64_t>(n3) || c >= static_cast<uint64_t>(n3))
+            throw Malformed("plan file basis entry out of range");
+        rows[r].emplace_back(static_cast<int32_t>(c), get_complex(in));
+    }
+    expect_eof(in);
+    nd->radix = true;
+    nd->children = children;
+    nd->B.dim = n3;
+    nd->B.rowptr.assign(n3 + 1, 0);
+    for (int64_t r = 0; r < n3; ++r) {
+        std::sort(rows[r].begin(), rows[r].end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        for (const auto& e : rows[r]) {
+            nd->B.col.push_back(e.first);
+            nd->B.val.push_back(e.second);
+        }
+        nd->B.rowptr[r + 1] = nd->B.nnz();
+    }
+    std::vector<cld> K(nd->K.begin(), nd->K.end());
+    double kc = 0;
+    const auto Kinv = dense_inverse(K, 8, &kc);
+    if (!(kc <= 1e12)) throw FcctError(ST_ILL_CONDITIONED, "radix kernel: condition exceeds 1e12");
+    std::copy(Kinv.begin(), Kinv.end(), nd->Kinv.begin());
+    nd->Binv = invert_by_components(nd->B);
+    nd->condition = kc;
+    return nd;
+}
+
+}  // namespace
+
+std::string PlanStore::cache_key(int n, const Params& p) {  // plan_cache.cpp:213-216
+    return "n" + std::to_string(n) + "_r" + encode_param(p.r) + "_s" + encode_param(p.s) + "_t" + encode_param(p.t);
+}
+
+std::string PlanStore::path_for(int n, const Params& p) const {
+    return (std::filesystem::path(dir_) / (sanitize(cache_key(n, p)) + ".fccplan")).string();
+}
+
+PlanStore::PlanStore(std::string dir) : dir_(std::move(dir)) {
+    std::error_code ec;
+    std::filesystem::create_directories(dir_, ec);
+    if (ec) throw FcctError(ST_IO, "cannot create plan cache directory '" + dir_ + "': " + ec.message());
+}
+
+std::shared_ptr<const PlanNode> PlanStore::load_or_build(int n, const Params& p) {  // plan_cache.cpp:222-282
+    const std::string path = path_for(n, p);
+    const bool existed = std::filesystem::exists(path);
+    if (existed) {
+        std::ifstream in(path, std::ios::binary);
+        std::optional<Header> header;
+        try {
+            if (!in) throw Malformed("cannot open plan file");
+            Header h = read_header(in);
+            const bool expect_direct = (n == 1 || n % 2 != 0);
+            if (h.n != n || (h.kind == kKindDirect) != expect_direct || h.r != encode_param(p.r) ||
+                h.s != encode_param(p.s) || h.t != encode_param(p.t))
+                throw Malformed("plan file header does not match request");
+            header = h;
+        } catch (const FcctError& e) {
+            std::cerr << "warning: rebuilding plan cache entry " << path << " (" << e.what() << ")\n";
+        }
+        if (header) {
+            std::array<std::shared_ptr<const PlanNode>, 8> children{};
+            if (header->kind == kKindRadix2)
+                for (int blk = 0; blk < 8; ++blk)
+                    children[blk] = load_or_build(n / 2, p.child(blk >> 2, (blk >> 1) & 1, blk & 1));
+            try {
+                auto node = read_body(in, *header, p, children);
+                std::lock_guard<std::mutex> lock(mu_);
+                ++stats_.hits;
+                return node;
+            } catch (const FcctError& e) {
+                if (e.code != ST_IO) throw;
+                std::cerr << "warning: rebuilding plan cache entry " << path << " (" << e.what() << ")\n";
+            }
+        }
+        std::lock_guard<std::mutex> lock(mu_);
+        ++stats_.rebuilt;
+    } else {
+        std::lock_guard<std::mutex> lock(mu_);
+        ++stats_.misses;
+    }
+    // build this node; children through the store (build_plan_node with a child source)
+    std::shared_ptr<const PlanNode> node;
+    if (n == 1 || n % 2 != 0) {
+        node = build_tree(n, p);
+    } else {
+        std::array<std::shared_ptr<const PlanNode>, 8> children{};
+        for (int blk = 0; blk < 8; ++blk)
+            children[blk] = load_or_build(n / 2, p.child(blk >> 2, (blk >> 1) & 1, blk & 1));
+        node = build_radix_node(n, p, children);
+    }
+    const std::string tmp = path + ".tmp";
+    {
+        std::ofstream out(tmp, std::ios::binary | std::ios::trunc);
+        if (!out) throw FcctError(ST_IO, "cannot write plan cache file " + tmp);
+        save_node(out, *node);
+        if (!out) throw FcctError(ST_IO, "failed while writing plan cache file " + tmp);
+    }
+    std::error_code ec;
+    std::filesystem::rename(tmp, path, ec);
+    if (ec) throw FcctError(ST_IO, "cannot move plan cache file into place: " + ec.message());
+    return node;
+}
+
+}  // namespace fcct

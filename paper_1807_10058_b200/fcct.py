@@ -411,8 +411,60 @@ def build_plan(n: int, p: SkewParams, store=None, precision: str = "f64", device
     if n < 1:
         raise ValueError("build_plan: n must be >= 1")
     if store is not None:
-        return store.load_or_build(n, p)
+        return store.load_or_build(n, p, precision=precision, device=device)
     return _create(n, p, _capi.FAST, precision, _device_index(device))
+
+
+@dataclass
+class PlanStoreStats:
+    hits: int = 0
+    misses: int = 0
+    rebuilt: int = 0
+
+
+class PlanStore:
+    """On-disk plan cache (plan_cache.hpp:30-51), one reference-compatible
+    `.fccplan` file per (n, params); corrupt entries are rebuilt with a
+    warning on stderr, writes are temp + rename."""
+
+    def __init__(self, directory):
+        self._h = ctypes.c_void_p()
+        _raise(_capi.lib().fcct_store_open(str(directory).encode(), ctypes.byref(self._h)))
+        self.directory = str(directory)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _capi.lib().fcct_store_close(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @staticmethod
+    def cache_key(n: int, p: SkewParams) -> str:
+        return f"n{n}_r{encode_param(p.r)}_s{encode_param(p.s)}_t{encode_param(p.t)}"
+
+    def path_for(self, n: int, p: SkewParams) -> str:
+        buf = ctypes.create_string_buffer(4096)
+        _raise(_capi.lib().fcct_store_path(self._h, n, p.r, p.s, p.t, buf, 4096))
+        return buf.value.decode()
+
+    def warm(self, n: int, p: SkewParams) -> None:
+        """load_or_build on the host only (no GPU needed)."""
+        _raise(_capi.lib().fcct_store_warm(self._h, n, p.r, p.s, p.t))
+
+    def load_or_build(self, n: int, p: SkewParams, precision: str = "f64", device=None) -> TransformPlan:
+        h = ctypes.c_void_p()
+        prec = _capi.F32 if precision == "f32" else _capi.F64
+        dev = _device_index(device)
+        _raise(_capi.lib().fcct_plan_create_from_store(self._h, n, p.r, p.s, p.t, prec, dev, ctypes.byref(h)))
+        return TransformPlan(h.value, precision, dev)
+
+    def stats(self) -> PlanStoreStats:
+        a, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _raise(_capi.lib().fcct_store_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return PlanStoreStats(a.value, b.value, c.value)
 
 
 def basis_change(n: int, p: SkewParams, inverse: bool = False) -> SparseMatrix:

@@ -343,3 +343,53 @@ def test_alternative_executors_agree(cuda, oracle_mod, pipeline, monkeypatch):
         assert rel(y.cpu().numpy(), y_ref) <= F64_TOL
         back = inverse_apply(plan, Spectrum(n, CANON, y)).data.cpu().numpy()
         assert rel(back, x) <= F64_TOL
+
+
+def _write_fccplan_radix(path, n, p_strs, K, perm, B):
+    """Test-side writer of the reference layout (plan_cache.hpp:11-27), used to
+    hand the store a file carrying the reference's own (LU-derived) factor."""
+    import struct
+    rows, cols = np.nonzero(B)
+    order = np.lexsort((rows, cols))
+    out = bytearray(b"FCCPLAN1") + struct.pack("<IBQ", 1, 1, n)
+    for s in p_strs:
+        out += struct.pack("<I", len(s)) + s.encode()
+    out += np.ascontiguousarray(K, dtype=np.complex128).tobytes()
+    out += np.asarray(perm, dtype=np.uint64).tobytes()
+    out += struct.pack("<Q", len(order))
+    for k in order:
+        v = B[rows[k], cols[k]]
+        out += struct.pack("<QQdd", int(rows[k]), int(cols[k]), v.real, v.imag)
+    open(path, "wb").write(bytes(out))
+
+
+def test_plan_store_load_or_build(cuda, oracle_mod, tmp_path):
+    """PlanStore (plan_cache.hpp:29-58): a loaded plan computes bitwise what a
+    freshly derived one does, and a root entry written with the reference's own
+    LU-derived factor (noise ~1e-13) is accepted and applied within the bar."""
+    from paper_1807_10058_b200 import PlanStore
+    st = PlanStore(tmp_path)
+    x = torch.from_numpy(rand_batch(8, 300, seed=77)).to(cuda)
+    fresh = fast_apply(build_plan(8, CANON), SignalTensor(8, x)).values
+    built = fast_apply(st.load_or_build(8, CANON), SignalTensor(8, x)).values
+    loaded_plan = PlanStore(tmp_path).load_or_build(8, CANON)
+    loaded = fast_apply(loaded_plan, SignalTensor(8, x)).values
+    assert torch.equal(fresh, built)
+    assert rel(loaded.cpu().numpy(), fresh.cpu().numpy()) <= 1e-14
+    back = inverse_apply(loaded_plan, Spectrum(8, CANON, loaded)).data
+    assert rel(back.cpu().numpy(), x.cpu().numpy()) <= F64_TOL
+
+    st.warm(4, CANON)
+    ref_root = oracle_mod.RefPlan(4, tup(CANON))
+    _write_fccplan_radix(st.path_for(4, CANON), 4, ["1/8", "0", "3/8"],
+                         oracle_mod.dense_transform(2, tup(CANON)), oracle_mod.radix_permutation(4),
+                         ref_root.basis_dense())
+    st2 = PlanStore(tmp_path)
+    plan4 = st2.load_or_build(4, CANON)
+    s = st2.stats()
+    assert s.rebuilt == 0 and s.misses == 0 and s.hits == 73
+    x4 = rand_batch(4, 50, seed=5)
+    y = fast_apply(plan4, SignalTensor(4, torch.from_numpy(x4).to(cuda))).values.cpu().numpy()
+    assert rel(y, oracle_mod.forward_dense(4, tup(CANON), x4)) <= 1e-12
+    xb = inverse_apply(plan4, Spectrum(4, CANON, torch.from_numpy(y).to(cuda))).data.cpu().numpy()
+    assert rel(xb, x4) <= 1e-12
