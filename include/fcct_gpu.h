@@ -41,7 +41,9 @@ typedef enum {
     FCCT_PARAMS_MISMATCH = 6,  /* invalid_argument "different skew grid" (:163-165,515-517) */
     FCCT_IO = 7,               /* MalformedFile / IoFailure */
     FCCT_CUDA = 8,             /* CUDA runtime failure */
-    FCCT_DERIVATION = 9        /* basis-change derivation residual (transform.cpp:301-304) */
+    FCCT_DERIVATION = 9,       /* basis-change derivation residual (transform.cpp:301-304) */
+    FCCT_MALFORMED = 10,       /* MalformedFile (errors.hpp:52-56), io category */
+    FCCT_SIZE_MISMATCH_IO = 11 /* SizeMismatch(..., ErrorCategory::io): a file promises another length */
 } fcct_status;
 
 typedef enum { FCCT_DIRECT = 0, FCCT_FAST = 1 } fcct_method;
@@ -104,6 +106,21 @@ fcct_status fcct_forward_host(fcct_plan plan, const void* in_host, void* out_hos
                               void* stream);
 fcct_status fcct_inverse_host(fcct_plan plan, const void* in_host, void* out_host, int64_t batch,
                               void* stream);
+
+/* Real-sample I/O (the steps either side of the path, voxel_io.hpp:40-46).
+ * fcct_forward_real replaces z_transform (voxel_io.cpp:178-186) followed by
+ * fast_apply / naive_apply: `in_real` holds [batch][n^3] real samples (f64,
+ * or f32 for an FCCT_F32 plan) and `out` the complex spectrum. fcct_inverse_real
+ * replaces inverse_apply followed by grid_from_signal (voxel_io.cpp:188-198):
+ * `out_real` receives the real parts only. The fast fp64/fp32 pipeline fuses
+ * the (de)complexification into its tile load/store, halving the bytes moved
+ * on the real side. */
+fcct_status fcct_forward_real(fcct_plan plan, const void* in_real, void* out, int64_t batch, void* stream);
+fcct_status fcct_inverse_real(fcct_plan plan, const void* in, void* out_real, int64_t batch, void* stream);
+fcct_status fcct_forward_real_host(fcct_plan plan, const void* in_real_host, void* out_host, int64_t batch,
+                                   void* stream);
+fcct_status fcct_inverse_real_host(fcct_plan plan, const void* in_host, void* out_real_host, int64_t batch,
+                                   void* stream);
 
 /* radix_permutation(n) (transform.hpp:55, transform.cpp:171-194): n^3 entries,
  * bit-exact. Computed on the device from the closed-form digit interleave. */
@@ -169,6 +186,48 @@ fcct_status fcct_plan_create_from_store(fcct_store store, int n, double r, doubl
  * [begin, end) of `total` blocks owned by `rank` of `world` (ceil split,
  * uneven tail allowed). No collective is involved. */
 fcct_status fcct_shard_range(int64_t total, int rank, int world, int64_t* begin, int64_t* end);
+
+/* ---------------------------------------------------------------------------
+ * I/O either side of the path. Host buffers; text
+ * outputs go to `path`, where NULL or "-" means stdout (fcct.cpp:44-54).
+ * ------------------------------------------------------------------------- */
+
+/* parse_params / SkewParams::encode (spectral.cpp:79-128): "r,s,t" with
+ * fields "a/b" or decimals. encode writes at most `len` bytes incl. the NUL. */
+fcct_status fcct_parse_params(const char* text, double* r, double* s, double* t);
+fcct_status fcct_encode_params(double r, double s, double t, char* buf, int64_t len);
+
+/* export_nodes_csv of skew_nodes(n, params) (spectral.cpp:155-188; CLI `zeros`):
+ * "i,j,k,x,y,z" + one %.17g row per node. DEGENERATE_NODES as skew_nodes. */
+fcct_status fcct_export_nodes_csv(int n, double r, double s, double t, const char* path);
+
+/* export_geometry (voxel_io.cpp:330-334): "dx,dy,dz" + the 14 FCC shifts. */
+fcct_status fcct_export_geometry(const char* path);
+
+/* export_spectrum (voxel_io.cpp:238-261): `values_host` is one spectrum of n^3
+ * complex128 values; writes "# n=.. params=..", the column header
+ * "i,j,k,x,y,z,re,im,magnitude" and one %.17g row per node. */
+fcct_status fcct_export_spectrum(int n, double r, double s, double t, const void* values_host, const char* path);
+
+/* load_spectrum_csv (voxel_io.cpp:263-328). With values_host == NULL only the
+ * header is read (n and params returned); otherwise the whole file is checked
+ * and n^3 complex128 values written (capacity counts points). Errors: IO
+ * (cannot open), MALFORMED (header / row problems), SIZE_MISMATCH_IO (row count). */
+fcct_status fcct_load_spectrum_csv(const char* path, int* n, double* r, double* s, double* t, void* values_host,
+                                   int64_t capacity);
+
+/* load_grid / save_grid (voxel_io.cpp:158-176): ".json" paths hold one JSON
+ * object {"metadata":{..},"n":..,"values":[..]}; other paths a little-endian
+ * f64 payload plus a ".json" sidecar. metadata travels as a JSON object of
+ * strings. values_host == NULL reads n (and metadata) only. */
+fcct_status fcct_grid_load(const char* path, int* n, double* values_host, int64_t capacity, char* metadata_json,
+                           int64_t metadata_len);
+fcct_status fcct_grid_save(const char* path, int n, const double* values_host, const char* metadata_json);
+
+/* synthetic_sword (voxel_io.cpp:200-236), n >= 8: writes n^3 samples in {0,1}
+ * (metadata {"solid":"sword"}); occupancy_checksum (:336-344): FNV-1a 64. */
+fcct_status fcct_synthetic_sword(int n, double* values_host);
+fcct_status fcct_occupancy_checksum(const double* values_host, int64_t count, uint64_t* out);
 
 #ifdef __cplusplus
 }

@@ -13,8 +13,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libfcct_b200.so"
-SOURCES = ["kernels.cu", "capi.cpp", "plan.cpp", "tiling.cpp", "plan_cache.cpp"]
-HEADERS = ["kernels.hpp", "device.cuh", "plan.hpp", "tiling.hpp", "plan_cache.hpp"]
+SOURCES = ["kernels.cu", "capi.cpp", "plan.cpp", "tiling.cpp", "plan_cache.cpp", "voxel_io.cpp"]
+HEADERS = ["kernels.hpp", "device.cuh", "plan.hpp", "tiling.hpp", "plan_cache.hpp", "voxel_io.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3",

@@ -19,6 +19,8 @@ PARAMS_MISMATCH = 6
 IO = 7
 CUDA = 8
 DERIVATION = 9
+MALFORMED = 10
+SIZE_MISMATCH_IO = 11
 
 DIRECT = 0
 FAST = 1
@@ -74,6 +76,10 @@ def lib() -> ctypes.CDLL:
         "fcct_inverse_checked": (c_int, [c_void_p, c_double, c_double, c_double, c_void_p, c_void_p, c_int64, c_void_p]),
         "fcct_forward_host": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
         "fcct_inverse_host": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
+        "fcct_forward_real": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
+        "fcct_inverse_real": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
+        "fcct_forward_real_host": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
+        "fcct_inverse_real_host": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
         "fcct_radix_permutation": (c_int, [c_int, POINTER(c_uint64)]),
         "fcct_dense_matrix": (c_int, [c_int, c_double, c_double, c_double, c_void_p, c_void_p]),
         "fcct_skew_nodes": (c_int, [c_int, c_double, c_double, c_double, c_void_p, c_void_p]),
@@ -85,6 +91,16 @@ def lib() -> ctypes.CDLL:
         "fcct_shard_range": (c_int, [c_int64, c_int, c_int, POINTER(c_int64), POINTER(c_int64)]),
         "fcct_debug_dmma_probe": (c_int, [c_void_p, c_void_p, c_void_p]),
         "fcct_store_open": (c_int, [ctypes.c_char_p, POINTER(c_void_p)]),
+        "fcct_parse_params": (c_int, [ctypes.c_char_p, POINTER(c_double), POINTER(c_double), POINTER(c_double)]),
+        "fcct_encode_params": (c_int, [c_double, c_double, c_double, ctypes.c_char_p, c_int64]),
+        "fcct_export_nodes_csv": (c_int, [c_int, c_double, c_double, c_double, ctypes.c_char_p]),
+        "fcct_export_geometry": (c_int, [ctypes.c_char_p]),
+        "fcct_export_spectrum": (c_int, [c_int, c_double, c_double, c_double, c_void_p, ctypes.c_char_p]),
+        "fcct_load_spectrum_csv": (c_int, [ctypes.c_char_p, POINTER(c_int), POINTER(c_double), POINTER(c_double), POINTER(c_double), c_void_p, c_int64]),
+        "fcct_grid_load": (c_int, [ctypes.c_char_p, POINTER(c_int), c_void_p, c_int64, ctypes.c_char_p, c_int64]),
+        "fcct_grid_save": (c_int, [ctypes.c_char_p, c_int, c_void_p, ctypes.c_char_p]),
+        "fcct_synthetic_sword": (c_int, [c_int, c_void_p]),
+        "fcct_occupancy_checksum": (c_int, [c_void_p, c_int64, POINTER(ctypes.c_uint64)]),
         "fcct_store_close": (c_int, [c_void_p]),
         "fcct_store_warm": (c_int, [c_void_p, c_int, c_double, c_double, c_double]),
         "fcct_store_stats": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_int)]),
@@ -115,6 +131,10 @@ HEADER_SYMBOLS = [
     "fcct_inverse_checked",
     "fcct_forward_host",
     "fcct_inverse_host",
+    "fcct_forward_real",
+    "fcct_inverse_real",
+    "fcct_forward_real_host",
+    "fcct_inverse_real_host",
     "fcct_radix_permutation",
     "fcct_dense_matrix",
     "fcct_skew_nodes",
@@ -126,6 +146,16 @@ HEADER_SYMBOLS = [
     "fcct_shard_range",
     "fcct_basis_change",
     "fcct_plan_tree_stats",
+    "fcct_parse_params",
+    "fcct_encode_params",
+    "fcct_export_nodes_csv",
+    "fcct_export_geometry",
+    "fcct_export_spectrum",
+    "fcct_load_spectrum_csv",
+    "fcct_grid_load",
+    "fcct_grid_save",
+    "fcct_synthetic_sword",
+    "fcct_occupancy_checksum",
     "fcct_store_open",
     "fcct_store_close",
     "fcct_store_warm",

@@ -19,6 +19,7 @@
 #include "plan.hpp"
 #include "plan_cache.hpp"
 #include "tiling.hpp"
+#include "voxel_io.hpp"
 
 namespace fcct {
 
@@ -456,6 +457,9 @@ struct fcct_plan_s {
     // workspace for host-buffer calls and in-place direct calls
     std::mutex ws_mu;
     std::shared_ptr<DevBuf> ws_in, ws_out;
+    // complex staging for real-I/O calls on executors without fused real I/O
+    std::mutex ws_real_mu;
+    std::shared_ptr<DevBuf> ws_real;
 };
 
 namespace {
@@ -685,6 +689,57 @@ void run_host(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t 
     ck(cudaStreamSynchronize(st), "sync");
 }
 
+// Real-sample I/O: forward takes real samples (z_transform, voxel_io.cpp:178-186),
+// inverse returns real parts (grid_from_signal, voxel_io.cpp:188-198). The v2
+// pipeline fuses both into its tile load / store; the other executors stage
+// through a complex workspace.
+void run_real(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st) {
+    if (batch < 0) throw FcctError(ST_SIZE_MISMATCH, "batch must be >= 0");
+    if (batch == 0) return;
+    if (!in || !out) throw FcctError(ST_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard guard(pl->device);
+    const bool f32 = pl->precision == FCCT_F32;
+    if (pl->radix && pl->v2) {
+        Pipeline2Desc d = inverse ? pl->inv2.desc : pl->fwd2.desc;
+        (inverse ? d.real_out : d.real_in) = 1;
+        ck(launch_pipeline2(d, in, out, batch, st, pl->num_sms), "fast pipeline v2 (real I/O)");
+        return;
+    }
+    const int64_t count = batch * cube(pl->n);
+    const size_t bytes = static_cast<size_t>(count * elem_bytes(pl));
+    std::lock_guard<std::mutex> lock(pl->ws_real_mu);
+    if (!pl->ws_real || pl->ws_real->bytes < bytes) {
+        ck(cudaStreamSynchronize(st), "sync");
+        pl->ws_real = std::make_shared<DevBuf>(bytes);
+    }
+    if (inverse) {
+        run(pl, true, in, pl->ws_real->ptr, batch, st);
+        ck(launch_real_part(pl->ws_real->ptr, out, count, f32, st), "real part");
+    } else {
+        ck(launch_complexify(in, pl->ws_real->ptr, count, f32, st), "complexify");
+        run(pl, false, pl->ws_real->ptr, out, batch, st);
+    }
+    ck(cudaStreamSynchronize(st), "sync");  // the plan-owned workspace serialises calls on this path
+}
+
+void run_real_host(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st) {
+    if (batch < 0) throw FcctError(ST_SIZE_MISMATCH, "batch must be >= 0");
+    if (batch == 0) return;
+    if (!in || !out) throw FcctError(ST_INVALID_ARGUMENT, "null buffer");
+    DeviceGuard guard(pl->device);
+    const size_t cbytes = static_cast<size_t>(batch * cube(pl->n) * elem_bytes(pl));
+    const size_t in_bytes = inverse ? cbytes : cbytes / 2, out_bytes = inverse ? cbytes / 2 : cbytes;
+    std::lock_guard<std::mutex> lock(pl->ws_mu);
+    if (!pl->ws_in || pl->ws_in->bytes < cbytes) {
+        pl->ws_in = std::make_shared<DevBuf>(cbytes);
+        pl->ws_out = std::make_shared<DevBuf>(cbytes);
+    }
+    ck(cudaMemcpyAsync(pl->ws_in->ptr, in, in_bytes, cudaMemcpyHostToDevice, st), "H2D");
+    run_real(pl, inverse, pl->ws_in->ptr, pl->ws_out->ptr, batch, st);
+    ck(cudaMemcpyAsync(out, pl->ws_out->ptr, out_bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+}
+
 template <typename F>
 fcct_status guarded(F&& f) {
     try {
@@ -765,6 +820,34 @@ fcct_status fcct_inverse_host(fcct_plan plan, const void* in, void* out, int64_t
     return guarded([&] {
         if (!plan) throw FcctError(ST_INVALID_ARGUMENT, "null plan");
         run_host(plan, true, in, out, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+fcct_status fcct_forward_real(fcct_plan plan, const void* in_real, void* out, int64_t batch, void* stream) {
+    return guarded([&] {
+        if (!plan) throw FcctError(ST_INVALID_ARGUMENT, "null plan");
+        run_real(plan, false, in_real, out, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+fcct_status fcct_inverse_real(fcct_plan plan, const void* in, void* out_real, int64_t batch, void* stream) {
+    return guarded([&] {
+        if (!plan) throw FcctError(ST_INVALID_ARGUMENT, "null plan");
+        run_real(plan, true, in, out_real, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+fcct_status fcct_forward_real_host(fcct_plan plan, const void* in_real, void* out, int64_t batch, void* stream) {
+    return guarded([&] {
+        if (!plan) throw FcctError(ST_INVALID_ARGUMENT, "null plan");
+        run_real_host(plan, false, in_real, out, batch, static_cast<cudaStream_t>(stream));
+    });
+}
+
+fcct_status fcct_inverse_real_host(fcct_plan plan, const void* in, void* out_real, int64_t batch, void* stream) {
+    return guarded([&] {
+        if (!plan) throw FcctError(ST_INVALID_ARGUMENT, "null plan");
+        run_real_host(plan, true, in, out_real, batch, static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1167,6 +1250,106 @@ fcct_status fcct_debug_timing(fcct_plan plan, int inverse, unsigned long long* o
 // Test hook: DMMA fragment-layout probe (device pointers).
 fcct_status fcct_debug_dmma_probe(const double* A, const double* B, double* C) {
     return guarded([&] { ck(dmma_probe(A, B, C, nullptr), "dmma probe"); });
+}
+
+
+// ---------------------------------------------------------------------------
+// I/O either side of the path (voxel_io.hpp, spectral.cpp)
+// ---------------------------------------------------------------------------
+namespace {
+void copy_string(const std::string& v, char* buf, int64_t len) {
+    if (!buf || len <= static_cast<int64_t>(v.size()))
+        throw FcctError(ST_INVALID_ARGUMENT, "string buffer too small (need " + std::to_string(v.size() + 1) + " bytes)");
+    std::memcpy(buf, v.c_str(), v.size() + 1);
+}
+std::string path_arg(const char* path) { return path ? std::string(path) : std::string("-"); }
+}  // namespace
+
+fcct_status fcct_parse_params(const char* text, double* r, double* s, double* t) {
+    return guarded([&] {
+        if (!text || !r || !s || !t) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        const Params p = io::parse_params(text);
+        *r = p.r;
+        *s = p.s;
+        *t = p.t;
+    });
+}
+
+fcct_status fcct_encode_params(double r, double s, double t, char* buf, int64_t len) {
+    return guarded([&] { copy_string(io::encode_params(Params{r, s, t}), buf, len); });
+}
+
+fcct_status fcct_export_nodes_csv(int n, double r, double s, double t, const char* path) {
+    return guarded([&] { io::write_text(path_arg(path), io::nodes_csv(n, Params{r, s, t})); });
+}
+
+fcct_status fcct_export_geometry(const char* path) {
+    return guarded([&] { io::write_text(path_arg(path), io::geometry_csv()); });
+}
+
+fcct_status fcct_export_spectrum(int n, double r, double s, double t, const void* values_host, const char* path) {
+    return guarded([&] {
+        if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "skew_nodes: n must be >= 1");
+        if (!values_host) throw FcctError(ST_INVALID_ARGUMENT, "null values");
+        io::write_text(path_arg(path),
+                       io::spectrum_csv(n, Params{r, s, t}, static_cast<const std::complex<double>*>(values_host)));
+    });
+}
+
+fcct_status fcct_load_spectrum_csv(const char* path, int* n, double* r, double* s, double* t, void* values_host,
+                                   int64_t capacity) {
+    return guarded([&] {
+        if (!path || !n || !r || !s || !t) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        const io::SpectrumFile f = io::load_spectrum_csv(path, values_host == nullptr);
+        *n = f.n;
+        *r = f.p.r;
+        *s = f.p.s;
+        *t = f.p.t;
+        if (!values_host) return;
+        if (capacity < cube(f.n)) throw FcctError(ST_SIZE_MISMATCH, "values buffer holds fewer than n^3 points");
+        std::memcpy(values_host, f.values.data(), f.values.size() * sizeof(std::complex<double>));
+    });
+}
+
+fcct_status fcct_grid_load(const char* path, int* n, double* values_host, int64_t capacity, char* metadata_json,
+                           int64_t metadata_len) {
+    return guarded([&] {
+        if (!path || !n) throw FcctError(ST_INVALID_ARGUMENT, "null argument");
+        const io::Grid g = io::load_grid(path);
+        *n = g.n;
+        if (metadata_json) copy_string(io::metadata_json(g.metadata), metadata_json, metadata_len);
+        if (!values_host) return;
+        if (capacity < cube(g.n)) throw FcctError(ST_SIZE_MISMATCH, "values buffer holds fewer than n^3 samples");
+        std::memcpy(values_host, g.values.data(), g.values.size() * sizeof(double));
+    });
+}
+
+fcct_status fcct_grid_save(const char* path, int n, const double* values_host, const char* metadata_json) {
+    return guarded([&] {
+        if (!path) throw FcctError(ST_INVALID_ARGUMENT, "null path");
+        if (n < 1) throw FcctError(ST_SIZE_MISMATCH, "grid size must be >= 1");
+        if (!values_host) throw FcctError(ST_INVALID_ARGUMENT, "null values");
+        io::Grid g;
+        g.n = n;
+        g.values.assign(values_host, values_host + cube(n));
+        g.metadata = io::parse_metadata_json(metadata_json ? metadata_json : "");
+        io::save_grid(g, path);
+    });
+}
+
+fcct_status fcct_synthetic_sword(int n, double* values_host) {
+    return guarded([&] {
+        if (!values_host) throw FcctError(ST_INVALID_ARGUMENT, "null values");
+        const io::Grid g = io::synthetic_sword(n);
+        std::memcpy(values_host, g.values.data(), g.values.size() * sizeof(double));
+    });
+}
+
+fcct_status fcct_occupancy_checksum(const double* values_host, int64_t count, uint64_t* out) {
+    return guarded([&] {
+        if ((!values_host && count > 0) || !out || count < 0) throw FcctError(ST_INVALID_ARGUMENT, "bad argument");
+        *out = io::occupancy_checksum(values_host, count);
+    });
 }
 
 }  // extern "C"

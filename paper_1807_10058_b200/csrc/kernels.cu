@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
     }
     __syncthreads();
     uint32_t phase = 0;
-    if (d.direct_store) {
+    if (d.direct_store && !d.real_in && !d.real_out) {
         if (threadIdx.x == 0 && static_cast<int64_t>(blockIdx.x) < ntiles) {
             const int64_t nt = blockIdx.x + gridDim.x;
             issue_tile_load<TB>(NextLoad{in, bar, X, stride, dimr, static_cast<int64_t>(blockIdx.x), batch,
@@ -563,7 +563,45 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
         const int64_t t0 = tile * TB;
         const int nvalid = static_cast<int>(batch - t0 < TB ? batch - t0 : TB);
         long long c0 = timing ? clock64() : 0;
-        if (d.io_f32) {
+        if (d.real_in) {
+            // z_transform fused into the load: real rows -> (re, 0) pairs of the fp64 tile
+            if (threadIdx.x == 0) tma_store_wait_read0();  // the previous tile's bulk store has read X
+            __syncthreads();
+            if (d.io_f32) {
+                const int per_row = d.N / 4;
+                const float4* src = reinterpret_cast<const float4*>(in_raw) + t0 * per_row;
+                for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
+                    const int t = i / per_row, q = i - t * per_row;
+                    const float4 v = __ldg(src + static_cast<int64_t>(t) * per_row + q);
+                    double2* xr = reinterpret_cast<double2*>(X + t * stride) + 4 * q;
+                    xr[0] = make_double2(v.x, 0.0);
+                    xr[1] = make_double2(v.y, 0.0);
+                    xr[2] = make_double2(v.z, 0.0);
+                    xr[3] = make_double2(v.w, 0.0);
+                }
+            } else {
+                const int per_row = d.N / 2;
+                const double2* src = reinterpret_cast<const double2*>(in_raw) + t0 * per_row;
+                for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
+                    const int t = i / per_row, q = i - t * per_row;
+                    const double2 v = __ldg(src + static_cast<int64_t>(t) * per_row + q);
+                    double2* xr = reinterpret_cast<double2*>(X + t * stride) + 2 * q;
+                    xr[0] = make_double2(v.x, 0.0);
+                    xr[1] = make_double2(v.y, 0.0);
+                }
+            }
+            if (threadIdx.x == 0) {
+                const int64_t nt = tile + gridDim.x;
+                if (nt < ntiles) {
+                    const int64_t n0 = nt * TB;
+                    const int nv = static_cast<int>(batch - n0 < TB ? batch - n0 : TB);
+                    const size_t eb = d.io_f32 ? sizeof(float) : sizeof(double);
+                    prefetch_l2_bulk(static_cast<const char*>(in_raw) + n0 * d.N * eb,
+                                     static_cast<uint32_t>(nv * d.N * eb));
+                }
+            }
+            __syncthreads();
+        } else if (d.io_f32) {
             // complex64 rows -> fp64 tile (coalesced float4 loads, 2 points each)
             const float4* src = reinterpret_cast<const float4*>(in_raw) + t0 * (d.N / 2);
             const int per_row = d.N / 2;
@@ -608,6 +646,30 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
                 tacc[1 + kMaxStages / 2 + s] += c1 - tmid;  // store phase + final barrier
                 c0 = c1;
             }
+        }
+        if (d.real_out) {
+            // grid_from_signal fused into the store: real parts only
+            if (d.io_f32) {
+                const int per_row = d.N / 4;
+                float4* dst = reinterpret_cast<float4*>(out_raw) + t0 * per_row;
+                for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
+                    const int t = i / per_row, q = i - t * per_row;
+                    const double* xr = X + t * stride + 8 * q;
+                    dst[static_cast<int64_t>(t) * per_row + q] =
+                        make_float4(static_cast<float>(xr[0]), static_cast<float>(xr[2]), static_cast<float>(xr[4]),
+                                    static_cast<float>(xr[6]));
+                }
+            } else {
+                const int per_row = d.N / 2;
+                double2* dst = reinterpret_cast<double2*>(out_raw) + t0 * per_row;
+                for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
+                    const int t = i / per_row, q = i - t * per_row;
+                    const double* xr = X + t * stride + 4 * q;
+                    dst[static_cast<int64_t>(t) * per_row + q] = make_double2(xr[0], xr[2]);
+                }
+            }
+            __syncthreads();
+            continue;
         }
         if (d.io_f32) {
             float4* dst = reinterpret_cast<float4*>(out_raw) + t0 * (d.N / 2);
@@ -666,6 +728,55 @@ cudaError_t launch_pipeline2(const Pipeline2Desc& d, const void* in, void* out, 
     if (d.tb == 16 && d.warps == 16) return launch_pipeline2_t<16, 16>(d, in, out, batch, st, num_sms);
     if (d.tb == 8 && d.warps == 8) return launch_pipeline2_t<8, 8>(d, in, out, batch, st, num_sms);
     return cudaErrorInvalidValue;
+}
+
+namespace {
+
+template <typename R>
+__global__ void complexify_kernel(const R* __restrict__ in, C2<R>* __restrict__ out, int64_t count) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        C2<R> v;
+        v.x = __ldg(in + i);
+        v.y = 0;
+        out[i] = v;
+    }
+}
+
+template <typename R>
+__global__ void real_part_kernel(const C2<R>* __restrict__ in, R* __restrict__ out, int64_t count) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = in[i].x;
+}
+
+unsigned elementwise_grid(int64_t count) {
+    const int64_t blocks = (count + 255) / 256;
+    return static_cast<unsigned>(blocks < 148 * 32 ? (blocks > 0 ? blocks : 1) : 148 * 32);
+}
+
+}  // namespace
+
+cudaError_t launch_complexify(const void* in_real, void* out_cplx, int64_t count, bool f32, cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    if (f32)
+        complexify_kernel<float><<<elementwise_grid(count), 256, 0, st>>>(static_cast<const float*>(in_real),
+                                                                          static_cast<C2<float>*>(out_cplx), count);
+    else
+        complexify_kernel<double><<<elementwise_grid(count), 256, 0, st>>>(static_cast<const double*>(in_real),
+                                                                           static_cast<C2<double>*>(out_cplx), count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_real_part(const void* in_cplx, void* out_real, int64_t count, bool f32, cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    if (f32)
+        real_part_kernel<float><<<elementwise_grid(count), 256, 0, st>>>(static_cast<const C2<float>*>(in_cplx),
+                                                                         static_cast<float*>(out_real), count);
+    else
+        real_part_kernel<double><<<elementwise_grid(count), 256, 0, st>>>(static_cast<const C2<double>*>(in_cplx),
+                                                                          static_cast<double*>(out_real), count);
+    return cudaGetLastError();
 }
 
 // ===========================================================================

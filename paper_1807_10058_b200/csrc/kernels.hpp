@@ -67,6 +67,8 @@ struct Pipeline2Desc {
     int nstages;
     int direct_store;  // 1: last stage stores to global from registers; 0: smem + TMA bulk store
     int io_f32;        // 1: global data is complex64 (converted to/from fp64 at tile load/store)
+    int real_in;       // 1: input rows are real samples (z_transform fused into the tile load)
+    int real_out;      // 1: only real parts are stored (grid_from_signal fused into the tile store)
     int stage_mask;    // debug/timing only: stages with a cleared bit are skipped
     unsigned long long* timing;  // debug: CTA 0 accumulates clock64 per phase (nullptr: off)
     Stage2Dev st[kMaxStages];
@@ -74,6 +76,11 @@ struct Pipeline2Desc {
 
 cudaError_t launch_pipeline2(const Pipeline2Desc& d, const void* in, void* out, int64_t batch, cudaStream_t stream,
                              int num_sms);
+
+// z_transform / grid_from_signal for executors without fused real I/O:
+// real[count] -> complex[count] (zero imaginary parts) and back (real parts).
+cudaError_t launch_complexify(const void* in_real, void* out_cplx, int64_t count, bool f32, cudaStream_t st);
+cudaError_t launch_real_part(const void* in_cplx, void* out_real, int64_t count, bool f32, cudaStream_t st);
 
 // Global-memory multi-pass pipeline (any full radix tree; used when a block's
 // state does not fit one CTA tile, e.g. n = 32, 64): one launch per stage.

@@ -252,15 +252,14 @@ cld dense_entry(int n, const Params& p, const Index3& node, const Index3& kappa)
     return acc / 24.0L;
 }
 
-void check_nodes(int n, const Params& p) {
+std::vector<std::array<std::complex<double>, 3>> node_coords(int n, const Params& p) {
     if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "skew_nodes: n must be >= 1");
-    if (n > 16) return;  // quadratic scan; larger grids skip it (spectral.cpp:133)
     const int64_t n3 = cube(n);
     std::vector<std::array<std::complex<double>, 3>> xyz(n3);
     const double two_pi = 2.0 * std::numbers::pi;
     for (int64_t a = 0; a < n3; ++a) {
         const Index3 ijk = unlex(a, n);
-        auto wrap = [](double v) {  // TorusPoint::wrapped (chebyshev.cpp:326-335)
+        auto wrap = [](double v) {  // TorusPoint::wrapped (chebyshev.cpp:30-39)
             double f = v - std::floor(v);
             if (f >= 1.0 - 1e-15) f = 0.0;
             return f;
@@ -270,11 +269,19 @@ void check_nodes(int n, const Params& p) {
         const std::complex<double> u{std::cos(two_pi * th[0]), std::sin(two_pi * th[0])};
         const std::complex<double> v{std::cos(two_pi * th[1]), std::sin(two_pi * th[1])};
         const std::complex<double> w{std::cos(two_pi * th[2]), std::sin(two_pi * th[2])};
-        const auto ui = 1.0 / u, vi = 1.0 / v, wi = 1.0 / w;  // chebyshev.cpp:372-381
+        const auto ui = 1.0 / u, vi = 1.0 / v, wi = 1.0 / w;  // coords_from_uvw (chebyshev.cpp:76-85)
         xyz[a][0] = 0.25 * (u + ui * v + vi * w + wi);
         xyz[a][1] = (vi + v + u * wi + ui * v * wi + ui * w + u * vi * w) / 6.0;
         xyz[a][2] = 0.25 * (ui + u * vi + v * wi + w);
     }
+    return xyz;
+}
+
+void check_nodes(int n, const Params& p) {
+    if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "skew_nodes: n must be >= 1");
+    if (n > 16) return;  // quadratic scan; larger grids skip it (spectral.cpp:27)
+    const int64_t n3 = cube(n);
+    const auto xyz = node_coords(n, p);
     constexpr double th2 = 1e-9 * 1e-9;
     for (int64_t a = 0; a < n3; ++a)
         for (int64_t b = a + 1; b < n3; ++b) {

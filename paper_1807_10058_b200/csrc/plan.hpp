@@ -43,6 +43,8 @@ enum Status {
     ST_IO = 7,
     ST_CUDA = 8,
     ST_DERIVATION = 9,
+    ST_MALFORMED = 10,        // MalformedFile (io category)
+    ST_SIZE_MISMATCH_IO = 11, // SizeMismatch(..., ErrorCategory::io)
 };
 
 struct FcctError : std::runtime_error {
@@ -137,6 +139,10 @@ std::vector<int32_t> output_order(int n);
 
 // Dense D_n(p) entry (ColumnEvaluator semantics, transform.cpp:35-82).
 cld dense_entry(int n, const Params& p, const Index3& node, const Index3& kappa);
+
+// Spectral coordinates (x, y, z) of the skew nodes in lexicographic order
+// (skew_nodes + coords_from_uvw, spectral.cpp:155-171, chebyshev.cpp:30-85).
+std::vector<std::array<std::complex<double>, 3>> node_coords(int n, const Params& p);
 
 // Node degeneracy check (check_not_degenerate, spectral.cpp:132-149), n <= 16.
 void check_nodes(int n, const Params& p);

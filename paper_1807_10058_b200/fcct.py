@@ -11,6 +11,8 @@ entry points (H2D + transform + D2H); CUDA tensors stay on the device.
 from __future__ import annotations
 
 import ctypes
+import json
+import os
 import enum
 import math
 from dataclasses import dataclass, field
@@ -82,8 +84,13 @@ def _raise(status: int) -> None:
         _capi.IO: IoFailure,
         _capi.CUDA: CudaError,
         _capi.DERIVATION: DerivationError,
+        _capi.MALFORMED: MalformedFile,
+        _capi.SIZE_MISMATCH_IO: SizeMismatch,
     }.get(status, FcctError)
-    raise exc(msg)
+    err = exc(msg)
+    if status == _capi.SIZE_MISMATCH_IO:
+        err.category = ErrorCategory.io  # SizeMismatch(..., ErrorCategory::io)
+    raise err
 
 
 # ---------------------------------------------------------------------------
@@ -161,6 +168,10 @@ def parse_params(text: str) -> SkewParams:
 
 @dataclass
 class SignalTensor:
+    """Samples at the nodes, [..., n^3]. `data` is complex, or real (float64 /
+    float32) when produced by z_transform: the identity complexification
+    (voxel_io.cpp:178-186) is then fused into the device tile load."""
+
     n: int
     data: torch.Tensor
 
@@ -220,6 +231,10 @@ class SparseMatrix:
 
 def _dtype_of(precision: str) -> torch.dtype:
     return torch.complex64 if precision == "f32" else torch.complex128
+
+
+def _real_dtype_of(precision: str) -> torch.dtype:
+    return torch.float32 if precision == "f32" else torch.float64
 
 
 class TransformPlan:
@@ -294,20 +309,30 @@ class TransformPlan:
         return out
 
     # raw vector forms (apply_values / solve_values, transform.cpp:429-494) ------
-    def _run(self, x: torch.Tensor, inverse: bool, params: Optional[SkewParams] = None) -> torch.Tensor:
+    def _run(
+        self, x: torch.Tensor, inverse: bool, params: Optional[SkewParams] = None, real_out: bool = False
+    ) -> torch.Tensor:
         N = self.n() ** 3
         dt = _dtype_of(self.precision)
-        if x.dtype != dt:
-            raise TypeError(f"expected {dt} data for a {self.precision} plan, got {x.dtype}")
+        rdt = _real_dtype_of(self.precision)
+        real_in = not inverse and x.dtype == rdt
+        if x.dtype != dt and not real_in:
+            raise TypeError(f"expected {dt} (or {rdt} real samples) for a {self.precision} plan, got {x.dtype}")
         if x.shape[-1] != N:
             raise SizeMismatch(f"signal has {x.shape[-1]} samples, need {N}")
+        if inverse and params is not None and params != self.params():
+            raise ValueError("inverse_apply: spectrum was produced on a different skew grid")
         batch = x.numel() // N
         L = _capi.lib()
+        x = x.contiguous()
+        out = torch.empty(x.shape, dtype=rdt if real_out else dt, device=x.device)
         if x.is_cuda:
-            x = x.contiguous()
-            out = torch.empty_like(x)
             stream = torch.cuda.current_stream(x.device).cuda_stream
-            if inverse and params is not None:
+            if real_in:
+                st = L.fcct_forward_real(self._h, x.data_ptr(), out.data_ptr(), batch, stream)
+            elif real_out:
+                st = L.fcct_inverse_real(self._h, x.data_ptr(), out.data_ptr(), batch, stream)
+            elif inverse and params is not None:
                 st = L.fcct_inverse_checked(
                     self._h, params.r, params.s, params.t, x.data_ptr(), out.data_ptr(), batch, stream
                 )
@@ -316,11 +341,12 @@ class TransformPlan:
                 st = fn(self._h, x.data_ptr(), out.data_ptr(), batch, stream)
             _raise(st)
             return out
-        if inverse and params is not None and params != self.params():
-            raise ValueError("inverse_apply: spectrum was produced on a different skew grid")
-        x = x.contiguous()
-        out = torch.empty_like(x)
-        fn = L.fcct_inverse_host if inverse else L.fcct_forward_host
+        if real_in:
+            fn = L.fcct_forward_real_host
+        elif real_out:
+            fn = L.fcct_inverse_real_host
+        else:
+            fn = L.fcct_inverse_host if inverse else L.fcct_forward_host
         _raise(fn(self._h, x.data_ptr(), out.data_ptr(), batch, None))
         return out
 
@@ -374,9 +400,12 @@ def naive_apply(t: DenseTransform, s: SignalTensor) -> Spectrum:
     return Spectrum(t.n, t.params, t._plan.apply_values(s.data))
 
 
-def inverse_apply(t, q: Spectrum, threads: int = 1) -> SignalTensor:
+def inverse_apply(t, q: Spectrum, threads: int = 1, real_output: bool = False) -> SignalTensor:
     """inverse_apply for a DenseTransform (transform.cpp:158-169) or a
-    TransformPlan (transform.cpp:509-524)."""
+    TransformPlan (transform.cpp:509-524).
+
+    real_output=True fuses grid_from_signal (voxel_io.cpp:188-198) into the
+    device store: the returned SignalTensor carries only the real parts."""
     if isinstance(t, DenseTransform):
         if t.n != q.n:
             raise SizeMismatch(f"inverse_apply: transform size {t.n} vs spectrum size {q.n}")
@@ -384,7 +413,7 @@ def inverse_apply(t, q: Spectrum, threads: int = 1) -> SignalTensor:
             raise ValueError("inverse_apply: spectrum was produced on a different skew grid")
         if q.values.shape[-1] != t.n**3:
             raise SizeMismatch(f"inverse_apply: spectrum has {q.values.shape[-1]} values, need {t.n ** 3}")
-        return SignalTensor(t.n, t._plan._run(q.values, True, q.params))
+        return SignalTensor(t.n, t._plan._run(q.values, True, q.params, real_out=real_output))
     plan: TransformPlan = t
     if plan.n() != q.n:
         raise SizeMismatch(f"inverse_apply: plan size {plan.n()} vs spectrum size {q.n}")
@@ -392,7 +421,7 @@ def inverse_apply(t, q: Spectrum, threads: int = 1) -> SignalTensor:
         raise ValueError("inverse_apply: spectrum was produced on a different skew grid")
     if q.values.shape[-1] != q.n**3:
         raise SizeMismatch(f"inverse_apply: spectrum has {q.values.shape[-1]} values, need {q.n ** 3}")
-    return SignalTensor(plan.n(), plan._run(q.values, True, q.params))
+    return SignalTensor(plan.n(), plan._run(q.values, True, q.params, real_out=real_output))
 
 
 def radix_permutation(n: int) -> np.ndarray:
@@ -545,3 +574,122 @@ def shard_range(total: int, rank: int, world: int) -> tuple:
 
 def exact_fraction(x: float) -> Fraction:
     return Fraction(x)
+
+
+# ---------------------------------------------------------------------------
+# I/O either side of the path: voxel_io.hpp, spectral.cpp:173-188 (native, C ABI)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class VoxelGrid:
+    """VoxelGrid (voxel_io.hpp:16-22): real samples on an n^3 grid."""
+
+    n: int
+    values: np.ndarray
+    metadata: dict = field(default_factory=dict)
+
+    def size(self) -> int:
+        return self.n**3
+
+
+def _path(p) -> Optional[bytes]:
+    return None if p is None else os.fsencode(p)
+
+
+def load_grid(path) -> VoxelGrid:
+    """load_grid (voxel_io.cpp:158-164): JSON for '.json' paths, raw + sidecar otherwise."""
+    L = _capi.lib()
+    n = ctypes.c_int()
+    _raise(L.fcct_grid_load(_path(path), ctypes.byref(n), None, 0, None, 0))
+    vals = np.empty(n.value**3, dtype=np.float64)
+    meta = ctypes.create_string_buffer(1 << 16)
+    _raise(L.fcct_grid_load(_path(path), ctypes.byref(n), vals.ctypes.data, vals.size, meta, len(meta)))
+    return VoxelGrid(n.value, vals, json.loads(meta.value.decode()))
+
+
+def save_grid(grid: VoxelGrid, path) -> None:
+    """save_grid (voxel_io.cpp:166-176)."""
+    vals = np.ascontiguousarray(grid.values, dtype=np.float64)
+    if vals.size != grid.n**3 or grid.n < 1:
+        raise SizeMismatch(f"grid carries {vals.size} values for n={grid.n}")
+    meta = json.dumps(grid.metadata or {}, sort_keys=True).encode()
+    _raise(_capi.lib().fcct_grid_save(_path(path), grid.n, vals.ctypes.data, meta))
+
+
+def z_transform(grid: VoxelGrid, device=None) -> SignalTensor:
+    """z_transform (voxel_io.cpp:178-186). The identity complexification is
+    not materialised: the SignalTensor carries the real samples and the fast /
+    direct apply fuses (re, 0) into its device tile load (fcct_forward_real)."""
+    if grid.n < 1 or np.asarray(grid.values).size != grid.n**3:
+        raise SizeMismatch(f"grid carries {np.asarray(grid.values).size} values for n={grid.n}")
+    data = torch.from_numpy(np.ascontiguousarray(grid.values, dtype=np.float64))
+    if device is not None:
+        data = data.to(device)
+    return SignalTensor(grid.n, data)
+
+
+def grid_from_signal(s: SignalTensor) -> VoxelGrid:
+    """grid_from_signal (voxel_io.cpp:188-198): real parts of one signal."""
+    if s.data.shape[-1] != s.n**3 or s.data.numel() != s.n**3:
+        raise SizeMismatch(f"signal carries {s.data.numel()} samples for n={s.n}")
+    d = s.data.detach().cpu()
+    vals = (d.real if d.is_complex() else d).to(torch.float64).numpy().copy()
+    return VoxelGrid(s.n, vals.reshape(-1))
+
+
+def synthetic_sword(n: int) -> VoxelGrid:
+    """synthetic_sword (voxel_io.cpp:200-236)."""
+    vals = np.empty(max(n, 0) ** 3, dtype=np.float64)
+    _raise(_capi.lib().fcct_synthetic_sword(n, vals.ctypes.data if vals.size else None))
+    return VoxelGrid(n, vals, {"solid": "sword"})
+
+
+def occupancy_checksum(grid: VoxelGrid) -> int:
+    """occupancy_checksum (voxel_io.cpp:336-344): FNV-1a 64 over '0'/'1' bytes."""
+    vals = np.ascontiguousarray(grid.values, dtype=np.float64)
+    out = ctypes.c_uint64()
+    _raise(_capi.lib().fcct_occupancy_checksum(vals.ctypes.data if vals.size else None, vals.size, ctypes.byref(out)))
+    return out.value
+
+
+def _spectrum_host(spec: Spectrum) -> np.ndarray:
+    v = spec.values.detach()
+    if v.numel() != spec.n**3:
+        raise SizeMismatch("spectrum value count does not match node count")
+    return np.ascontiguousarray(v.cpu().to(torch.complex128).numpy().reshape(-1))
+
+
+def export_spectrum(spec: Spectrum, path=None, params: Optional[SkewParams] = None) -> None:
+    """export_spectrum (voxel_io.cpp:238-261) to `path` (None / '-' = stdout).
+    `params` stands for the node grid's offsets: they must match the spectrum's."""
+    if params is not None and params != spec.params:
+        raise ValueError("export_spectrum: spectrum and node grid use different offsets")
+    vals = _spectrum_host(spec)
+    p = spec.params
+    _raise(_capi.lib().fcct_export_spectrum(spec.n, p.r, p.s, p.t, vals.ctypes.data, _path(path)))
+
+
+def load_spectrum_csv(path) -> Spectrum:
+    """load_spectrum_csv (voxel_io.cpp:263-328): MalformedFile / IoFailure /
+    SizeMismatch(io) exactly where the reference raises them."""
+    L = _capi.lib()
+    n, r, s_, t = ctypes.c_int(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    _raise(L.fcct_load_spectrum_csv(_path(path), ctypes.byref(n), ctypes.byref(r), ctypes.byref(s_), ctypes.byref(t), None, 0))
+    vals = np.empty(n.value**3, dtype=np.complex128)
+    _raise(
+        L.fcct_load_spectrum_csv(
+            _path(path), ctypes.byref(n), ctypes.byref(r), ctypes.byref(s_), ctypes.byref(t), vals.ctypes.data, vals.size
+        )
+    )
+    return Spectrum(n.value, SkewParams(r.value, s_.value, t.value), torch.from_numpy(vals))
+
+
+def export_nodes_csv(n: int, p: SkewParams, path=None) -> None:
+    """export_nodes_csv(skew_nodes(n, p)) (spectral.cpp:155-188; CLI `zeros`)."""
+    _raise(_capi.lib().fcct_export_nodes_csv(n, p.r, p.s, p.t, _path(path)))
+
+
+def export_geometry(path=None) -> None:
+    """export_geometry (voxel_io.cpp:330-334): the 14 FCC shift vectors."""
+    _raise(_capi.lib().fcct_export_geometry(_path(path)))

@@ -393,3 +393,39 @@ def test_plan_store_load_or_build(cuda, oracle_mod, tmp_path):
     assert rel(y, oracle_mod.forward_dense(4, tup(CANON), x4)) <= 1e-12
     xb = inverse_apply(plan4, Spectrum(4, CANON, torch.from_numpy(y).to(cuda))).data.cpu().numpy()
     assert rel(xb, x4) <= 1e-12
+
+
+@pytest.mark.parametrize("n,method,precision", [(4, "fast", "f64"), (8, "fast", "f64"), (8, "fast", "f32"),
+                                                (16, "fast", "f64"), (8, "direct", "f64"), (3, "fast", "f64"),
+                                                (8, "direct", "f32")])
+def test_real_io_fused_matches_complex_path(cuda, oracle_mod, n, method, precision):
+    """z_transform fused into the tile load (fcct_forward_real) and
+    grid_from_signal fused into the store (fcct_inverse_real) give bitwise
+    the complex path's results (voxel_io.cpp:178-198)."""
+    from paper_1807_10058_b200 import z_transform, grid_from_signal, VoxelGrid
+    rdt = torch.float32 if precision == "f32" else torch.float64
+    cdt = torch.complex64 if precision == "f32" else torch.complex128
+    plan = build_plan(n, CANON, precision=precision) if method == "fast" else \
+        dense_transform(n, CANON, precision=precision)._plan
+    rng = np.random.default_rng(n)
+    xr = torch.from_numpy(rng.uniform(-1, 1, (53, n**3))).to(rdt).to(cuda)  # ragged batch
+    xc = torch.complex(xr, torch.zeros_like(xr)).to(cdt)
+    y_real = plan.apply_values(xr)
+    y_cplx = plan.apply_values(xc)
+    assert y_real.dtype == cdt and torch.equal(y_real, y_cplx)
+    back_c = plan._run(y_cplx, True)
+    back_r = plan._run(y_cplx, True, real_out=True)
+    assert back_r.dtype == rdt and torch.equal(back_r, back_c.real.contiguous())
+    # host-buffer variants
+    assert torch.equal(plan.apply_values(xr.cpu()), y_cplx.cpu())
+    assert torch.equal(plan._run(y_cplx.cpu(), True, real_out=True), back_c.real.cpu())
+    if precision == "f64":
+        ref = oracle_mod.forward_dense(n, tup(CANON), xc.cpu().numpy())
+        assert rel(y_real.cpu().numpy(), ref) <= F64_TOL
+        # the public path: z_transform -> fast_apply -> inverse_apply(real) -> grid
+        g = VoxelGrid(n, rng.uniform(0, 1, n**3))
+        s = z_transform(g, device=cuda)
+        spec = fast_apply(plan, s) if method == "fast" else Spectrum(n, CANON, plan.apply_values(s.data))
+        back = inverse_apply(plan, spec, real_output=True) if method == "fast" else \
+            SignalTensor(n, plan._run(spec.values, True, real_out=True))
+        assert np.abs(grid_from_signal(back).values - g.values).max() <= 1e-12
