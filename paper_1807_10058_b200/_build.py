@@ -13,6 +13,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libfcct_b200.so"
+CLI = LIB_DIR / "fcct"  # command-line front end (csrc/cli.cpp), a client of the C ABI
 SOURCES = ["kernels.cu", "capi.cpp", "plan.cpp", "tiling.cpp", "plan_cache.cpp", "voxel_io.cpp"]
 HEADERS = ["kernels.hpp", "device.cuh", "plan.hpp", "tiling.hpp", "plan_cache.hpp", "voxel_io.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -36,16 +37,36 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
-    LIB_DIR.mkdir(exist_ok=True)
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [NVCC, *FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
+def _cli_stale() -> bool:
+    if not CLI.exists():
+        return True
+    t = CLI.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in [CSRC / "cli.cpp", LIB, PKG.parent / "include" / "fcct_gpu.h"])
+
+
+def build_cli(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not _cli_stale():
+        return CLI
+    tmp = CLI.with_suffix(".tmp")
+    cmd = ["g++", "-O2", "-std=c++20", "-Wall", str(CSRC / "cli.cpp"), "-o", str(tmp), f"-L{LIB_DIR}", "-lfcct_b200",
+           "-Wl,-rpath,$ORIGIN"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, CLI)
+    return CLI
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if force or _stale():
+        LIB_DIR.mkdir(exist_ok=True)
+        tmp = LIB.with_suffix(".so.tmp")
+        cmd = [NVCC, *FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, LIB)
+    build_cli(force=force, verbose=verbose)
     return LIB
 
 

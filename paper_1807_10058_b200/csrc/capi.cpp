@@ -307,12 +307,12 @@ void build_pipelines(const PlanNode& root, int tb, PipelineTables& fwd, Pipeline
     // forward: for each level B (size > 2) then K-mix; dense leaves last.
     const int nfwd = [&] {
         int c = 0;
-        for (auto& lv : levels) c += (lv[0]->n > 2 ? 2 : 1);
+        for (auto& lv : levels) c += (level_identity(lv, false) ? 1 : 2);
         return c + (dense_leaves ? 1 : 0);
     }();
     int s = 0;
     for (auto& lv : levels) {
-        if (lv[0]->n > 2) {
+        if (!level_identity(lv, false)) {
             add_sparse_stage<R>(fwd, level_rows(lv, 0), RG, nullptr, (++s == nfwd) ? &Z : nullptr);
         }
         add_mix_stage<R>(fwd, lv, false, nullptr, (++s == nfwd) ? &Z : nullptr);
@@ -327,7 +327,7 @@ void build_pipelines(const PlanNode& root, int tb, PipelineTables& fwd, Pipeline
     for (auto it = levels.rbegin(); it != levels.rend(); ++it) {
         add_mix_stage<R>(inv, *it, true, first ? &Z : nullptr, nullptr);
         first = false;
-        if ((*it)[0]->n > 2) add_sparse_stage<R>(inv, level_rows(*it, 1), RG, nullptr, nullptr);
+        if (!level_identity(*it, true)) add_sparse_stage<R>(inv, level_rows(*it, 1), RG, nullptr, nullptr);
     }
 }
 
@@ -410,11 +410,11 @@ void build_global_pipelines(const PlanNode& root, GlobalTables& fwd, GlobalTable
         gt->desc.nstages = 0;
     }
     int nfwd = dense_leaves ? 1 : 0;
-    for (auto& lv : levels) nfwd += lv[0]->n > 2 ? 2 : 1;
+    for (auto& lv : levels) nfwd += level_identity(lv, false) ? 1 : 2;
     if (nfwd > kMaxStages) throw FcctError(ST_INVALID_ARGUMENT, "too many stages");
     int s = 0;
     for (auto& lv : levels) {
-        if (lv[0]->n > 2) add_global_sparse<R>(fwd, level_rows(lv, 0), nullptr, (++s == nfwd) ? &Z : nullptr);
+        if (!level_identity(lv, false)) add_global_sparse<R>(fwd, level_rows(lv, 0), nullptr, (++s == nfwd) ? &Z : nullptr);
         add_global_mix<R>(fwd, lv, false, nullptr, (++s == nfwd) ? &Z : nullptr);
     }
     if (dense_leaves) add_global_sparse<R>(fwd, level_rows(leaves, 2), nullptr, &Z);
@@ -426,7 +426,7 @@ void build_global_pipelines(const PlanNode& root, GlobalTables& fwd, GlobalTable
     for (auto it = levels.rbegin(); it != levels.rend(); ++it) {
         add_global_mix<R>(inv, *it, true, first ? &Z : nullptr, nullptr);
         first = false;
-        if ((*it)[0]->n > 2) add_global_sparse<R>(inv, level_rows(*it, 1), nullptr, nullptr);
+        if (!level_identity(*it, true)) add_global_sparse<R>(inv, level_rows(*it, 1), nullptr, nullptr);
     }
 }
 
@@ -456,7 +456,14 @@ struct fcct_plan_s {
     fcct_plan_info_t info{};
     // workspace for host-buffer calls and in-place direct calls
     std::mutex ws_mu;
-    std::shared_ptr<DevBuf> ws_in, ws_out;
+    std::shared_ptr<DevBuf> ws_in[2], ws_out[2];
+    cudaStream_t hs[2] = {nullptr, nullptr};  // host-path copy/compute streams
+    cudaEvent_t hev = nullptr;
+    ~fcct_plan_s() {
+        for (auto& h : hs)
+            if (h) cudaStreamDestroy(h);
+        if (hev) cudaEventDestroy(hev);
+    }
     // complex staging for real-I/O calls on executors without fused real I/O
     std::mutex ws_real_mu;
     std::shared_ptr<DevBuf> ws_real;
@@ -672,21 +679,61 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
     }
 }
 
-void run_host(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st) {
+void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st);
+void run_real(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st);
+
+// Host-buffer calls: the batch is cut into chunks that alternate between two
+// streams, so the H2D copy of one chunk, the transform of the previous one
+// and the D2H copy of the one before overlap (both copy directions run at
+// once over PCIe / C2C; pinned host buffers give fully asynchronous DMA).
+void run_host_any(fcct_plan_s* pl, bool inverse, bool real_io, const void* in, void* out, int64_t batch,
+                  cudaStream_t st) {
     if (batch < 0) throw FcctError(ST_SIZE_MISMATCH, "batch must be >= 0");
     if (batch == 0) return;
     if (!in || !out) throw FcctError(ST_INVALID_ARGUMENT, "null buffer");
     DeviceGuard guard(pl->device);
-    const size_t bytes = static_cast<size_t>(batch * cube(pl->n) * elem_bytes(pl));
+    const int64_t N = cube(pl->n), eb = elem_bytes(pl);
+    const int64_t in_eb = (real_io && !inverse) ? eb / 2 : eb, out_eb = (real_io && inverse) ? eb / 2 : eb;
+    const int64_t block_bytes = N * eb;
+    // ~32 MB chunks (at least 8 per call when the batch is large), whole blocks
+    int64_t chunk = std::max<int64_t>(1, (int64_t{32} << 20) / block_bytes);
+    chunk = std::min(chunk, std::max<int64_t>(1, (batch + 7) / 8));
+    chunk = std::min(chunk, batch);
+    const size_t ws_bytes = static_cast<size_t>(chunk * block_bytes);
     std::lock_guard<std::mutex> lock(pl->ws_mu);
-    if (!pl->ws_in || pl->ws_in->bytes < bytes) {
-        pl->ws_in = std::make_shared<DevBuf>(bytes);
-        pl->ws_out = std::make_shared<DevBuf>(bytes);
+    for (int k = 0; k < 2; ++k) {
+        if (!pl->hs[k]) ck(cudaStreamCreateWithFlags(&pl->hs[k], cudaStreamNonBlocking), "stream");
+        if (!pl->ws_in[k] || pl->ws_in[k]->bytes < ws_bytes) {
+            pl->ws_in[k] = std::make_shared<DevBuf>(ws_bytes);
+            pl->ws_out[k] = std::make_shared<DevBuf>(ws_bytes);
+        }
     }
-    ck(cudaMemcpyAsync(pl->ws_in->ptr, in, bytes, cudaMemcpyHostToDevice, st), "H2D");
-    run(pl, inverse, pl->ws_in->ptr, pl->ws_out->ptr, batch, st);
-    ck(cudaMemcpyAsync(out, pl->ws_out->ptr, bytes, cudaMemcpyDeviceToHost, st), "D2H");
-    ck(cudaStreamSynchronize(st), "sync");
+    if (!pl->hev) ck(cudaEventCreateWithFlags(&pl->hev, cudaEventDisableTiming), "event");
+    // work already queued on the caller's stream comes first
+    ck(cudaEventRecord(pl->hev, st), "event record");
+    for (auto h : pl->hs) ck(cudaStreamWaitEvent(h, pl->hev, 0), "stream wait");
+    const char* src = static_cast<const char*>(in);
+    char* dst = static_cast<char*>(out);
+    int c = 0;
+    for (int64_t off = 0; off < batch; off += chunk, ++c) {
+        const int64_t nb = std::min(chunk, batch - off);
+        cudaStream_t h = pl->hs[c & 1];
+        void* wi = pl->ws_in[c & 1]->ptr;
+        void* wo = pl->ws_out[c & 1]->ptr;
+        ck(cudaMemcpyAsync(wi, src + off * N * in_eb, static_cast<size_t>(nb * N * in_eb), cudaMemcpyHostToDevice, h),
+           "H2D");
+        if (real_io)
+            run_real(pl, inverse, wi, wo, nb, h);
+        else
+            run(pl, inverse, wi, wo, nb, h);
+        ck(cudaMemcpyAsync(dst + off * N * out_eb, wo, static_cast<size_t>(nb * N * out_eb), cudaMemcpyDeviceToHost, h),
+           "D2H");
+    }
+    for (auto h : pl->hs) ck(cudaStreamSynchronize(h), "sync");
+}
+
+void run_host(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st) {
+    run_host_any(pl, inverse, false, in, out, batch, st);
 }
 
 // Real-sample I/O: forward takes real samples (z_transform, voxel_io.cpp:178-186),
@@ -723,21 +770,7 @@ void run_real(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t 
 }
 
 void run_real_host(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st) {
-    if (batch < 0) throw FcctError(ST_SIZE_MISMATCH, "batch must be >= 0");
-    if (batch == 0) return;
-    if (!in || !out) throw FcctError(ST_INVALID_ARGUMENT, "null buffer");
-    DeviceGuard guard(pl->device);
-    const size_t cbytes = static_cast<size_t>(batch * cube(pl->n) * elem_bytes(pl));
-    const size_t in_bytes = inverse ? cbytes : cbytes / 2, out_bytes = inverse ? cbytes / 2 : cbytes;
-    std::lock_guard<std::mutex> lock(pl->ws_mu);
-    if (!pl->ws_in || pl->ws_in->bytes < cbytes) {
-        pl->ws_in = std::make_shared<DevBuf>(cbytes);
-        pl->ws_out = std::make_shared<DevBuf>(cbytes);
-    }
-    ck(cudaMemcpyAsync(pl->ws_in->ptr, in, in_bytes, cudaMemcpyHostToDevice, st), "H2D");
-    run_real(pl, inverse, pl->ws_in->ptr, pl->ws_out->ptr, batch, st);
-    ck(cudaMemcpyAsync(out, pl->ws_out->ptr, out_bytes, cudaMemcpyDeviceToHost, st), "D2H");
-    ck(cudaStreamSynchronize(st), "sync");
+    run_host_any(pl, inverse, true, in, out, batch, st);
 }
 
 template <typename F>
@@ -979,6 +1012,7 @@ fcct_status fcct_plan_perturbed_basis(fcct_plan plan, double delta, fcct_plan* o
                 }
         if (best < 0) throw FcctError(ST_INVALID_ARGUMENT, "with_perturbed_basis: column 0 is empty");
         root->B.val[best] += static_cast<long double>(delta);
+        root->Binv = invert_sparse(root->B);  // the reference refactors the perturbed basis (transform.cpp:551-553)
         auto pl = std::make_unique<fcct_plan_s>();
         pl->n = plan->n;
         pl->p = plan->p;

@@ -621,4 +621,13 @@ double algorithmic_flops(const PlanNode& root, bool inverse) {
     return 8.0 * (static_cast<double>(tree_nnz(root, inverse, false)) + 8.0 * N * tree_levels(root.n));
 }
 
+bool basis_is_identity(const SparseLD& B) {
+    if (B.nnz() != B.dim) return false;
+    for (int64_t r = 0; r < B.dim; ++r)
+        if (B.rowptr[r + 1] - B.rowptr[r] != 1 || B.col[B.rowptr[r]] != r ||
+            std::abs(B.val[B.rowptr[r]] - cld{1, 0}) > 1e-15L)  // derivation rounding only
+            return false;
+    return true;
+}
+
 }  // namespace fcct

@@ -119,6 +119,20 @@ struct PlanNode {
 std::shared_ptr<const PlanNode> build_radix_node(int n, const Params& p,
                                                  const std::array<std::shared_ptr<const PlanNode>, 8>& children);
 
+// B^{-1} by connected components of B, each inverted densely in long double
+// (plan_cache.cpp): used for a loaded or a perturbed basis factor.
+SparseLD invert_sparse(const SparseLD& B);
+
+// True when B is the identity (entries within 1e-15 of 1, derivation rounding). B_2 = I holds for every offset, so the
+// executors skip that stage; a perturbed B_2 (with_perturbed_basis) is applied.
+bool basis_is_identity(const SparseLD& B);
+
+inline bool level_identity(const std::vector<const PlanNode*>& level, bool inverse) {
+    for (const PlanNode* nd : level)
+        if (!basis_is_identity(inverse ? nd->Binv : nd->B)) return false;
+    return true;
+}
+
 // Dense inverse (Gauss-Jordan, partial pivoting, long double), row-major;
 // *cond receives the exact 1-norm condition.
 std::vector<cld> dense_inverse(const std::vector<cld>& a, int64_t dim, double* cond);

@@ -352,4 +352,6 @@ std::shared_ptr<const PlanNode> PlanStore::load_or_build(int n, const Params& p)
     return node;
 }
 
+SparseLD invert_sparse(const SparseLD& B) { return invert_by_components(B); }
+
 }  // namespace fcct

@@ -231,13 +231,13 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, const Shape2& shape, 
     std::vector<Logical> logical;
     if (!inverse) {
         for (auto& lv : levels) {
-            if (lv[0]->n > 2) logical.push_back(sparse_level(lv, false));
+            if (!level_identity(lv, false)) logical.push_back(sparse_level(lv, false));
             logical.push_back(mix_level(lv, false));
         }
     } else {
         for (auto it = levels.rbegin(); it != levels.rend(); ++it) {
             logical.push_back(mix_level(*it, true));
-            if ((*it)[0]->n > 2) logical.push_back(sparse_level(*it, true));
+            if (!level_identity(*it, true)) logical.push_back(sparse_level(*it, true));
         }
     }
     const int S = static_cast<int>(logical.size());

@@ -205,6 +205,15 @@ def test_factorization_residual_and_negative_control(cuda):
     dense = dense_transform(4, CANON)
     broken = with_perturbed_basis(plan, 1e-3)
     assert factorization_residual(broken, dense) > 1e-5  # test_transform.cpp:212-220
+    # B_2 = I is skipped by the executors only while it is the identity (CLI verify --n-max 2 --perturb-b)
+    for n in (2, 8):
+        broken = with_perturbed_basis(build_plan(n, CANON), 1e-3)
+        assert factorization_residual(broken, dense_transform(n, CANON)) > 1e-5
+        # the perturbed plan stays self-consistent: its inverse undoes its forward
+        x = torch.from_numpy(rand_batch(n, 3, seed=2)).to(cuda)
+        y = fast_apply(broken, SignalTensor(n, x)).values
+        back = inverse_apply(broken, Spectrum(n, CANON, y)).data
+        assert rel(back.cpu().numpy(), x.cpu().numpy()) <= 1e-12
 
 
 def test_basis_export(cuda, oracle_mod):
