@@ -113,9 +113,10 @@ void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
     out.desc.direct_store = ds ? std::atoi(ds) : 0;
     const char* sm = std::getenv("FCCT_DEBUG_STAGE_MASK");  // timing experiments only
     out.desc.stage_mask = sm ? std::atoi(sm) : -1;
+    out.desc.ring = 1;  // sparse-stage table entries stream through the per-warp cp.async ring
     out.desc.timing = nullptr;
     if (std::getenv("FCCT_DEBUG_TIMING")) {  // per-stage clock64 totals of CTA 0 (profiling aid)
-        auto b = std::make_shared<DevBuf>(sizeof(unsigned long long) * (kMaxStages + 2));
+        auto b = std::make_shared<DevBuf>(sizeof(unsigned long long) * (kMaxStages + 2 + kMaxStages * 16));
         ck(cudaMemset(b->ptr, 0, b->bytes), "memset");
         out.desc.timing = static_cast<unsigned long long*>(b->ptr);
         out.bufs.push_back(b);
@@ -135,21 +136,32 @@ void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
         return b->ptr;
     };
     constexpr size_t kArenaK = 16 * 1024;  // K tables up to this size go to shared memory
+    const char* gs = std::getenv("FCCT_V2_GROUP_SYNC");  // A/B switch: 0 = CTA-wide barriers only
+    const bool group_sync = gs ? std::atoi(gs) != 0 : true;
     for (size_t s = 0; s < h.stages.size(); ++s) {
         const Stage2Host& st = h.stages[s];
         Stage2Dev& d = out.desc.st[s];
         d = Stage2Dev{};
         d.kind = st.kind;
         d.n_units = st.n_units;
+        d.sync_mid = group_sync ? st.sync_mid : 0;
+        d.sync_end = group_sync ? st.sync_end : 0;
         d.o_warp_units = put(st.warp_units.data(), st.warp_units.size() * 4);
         d.o_u_out = put(st.u_out.data(), st.u_out.size() * 4);
-        d.o_w_base = d.o_w_count = d.o_e_slots = d.o_u_node = d.o_u_in = d.o_K = -1;
+        d.o_w_base = d.o_w_count = d.o_w_ccount = d.o_e_slots = d.o_u_node = d.o_u_in = d.o_K = -1;
         if (st.kind == 0) {
             d.o_w_base = put(st.w_base.data(), st.w_base.size() * 4);
             d.o_w_count = put(st.w_count.data(), st.w_count.size() * 4);
+            d.o_w_ccount = put(st.w_ccount.data(), st.w_ccount.size() * 4);
             d.o_e_slots = put(st.e_slots.data(), st.e_slots.size() * 4);
             d.e_re = static_cast<const double*>(keep(upload(st.e_re)));
             d.e_im = static_cast<const double*>(keep(upload(st.e_im)));
+            std::vector<double> ri(2 * st.e_re.size());
+            for (size_t q = 0; q < st.e_re.size(); ++q) {
+                ri[2 * q] = st.e_re[q];
+                ri[2 * q + 1] = st.e_im[q];
+            }
+            d.e_ri = static_cast<const double2*>(keep(upload(ri)));
         } else {
             d.o_u_node = put(st.u_node.data(), st.u_node.size() * 4);
             d.o_u_in = put(st.u_in.data(), st.u_in.size() * 4);
@@ -1215,6 +1227,48 @@ fcct_status fcct_debug_emulate_v2(int n, double r, double s, double t, int inver
 
 // Bank-conflict statistics of the compiled v2 tables (host, no GPU): number of
 // 16-lane half-warp load / store requests that hit a bank twice.
+// Per-stage work of the compiled v2 pipeline (profiling aid): for each stage
+// kind, DMMA per tile, the busiest warp's DMMA and the busiest SM sub-partition's
+// DMMA (warps w, w+4, w+8, w+12 share one tensor pipe).
+fcct_status fcct_debug_v2_stage_stats(int n, double r, double s, double t, int inverse, int64_t* out /* 4*16 */,
+                                      int* nstages) {
+    return guarded([&] {
+        auto root = build_tree(n, Params{r, s, t});
+        Pipeline2Host h;
+        if (!compile_pipeline2(*root, inverse != 0, Shape2{}, h))
+            throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by pipeline v2");
+        const int W = h.shape.warps, U = h.shape.units, MT = h.shape.tb / 4;
+        *nstages = static_cast<int>(h.stages.size());
+        for (size_t si = 0; si < h.stages.size(); ++si) {
+            const auto& st = h.stages[si];
+            std::vector<int64_t> per_warp(W, 0);
+            for (int w = 0; w < W; ++w) {
+                if (st.kind == 0) {
+                    for (int e = st.w_base[w]; e < st.w_base[w + 1]; ++e)
+                        per_warp[w] += MT * (((st.e_slots[4 * e] >> 30) & 1) ? 2 : 1);
+                } else {
+                    for (int j = 0; j < U; ++j)
+                        if (st.warp_units[w * U + j] >= 0) per_warp[w] += 4 * MT;
+                }
+            }
+            int64_t tot = 0, mx = 0, sp = 0;
+            for (int w = 0; w < W; ++w) {
+                tot += per_warp[w];
+                mx = std::max(mx, per_warp[w]);
+            }
+            for (int q = 0; q < 4; ++q) {
+                int64_t acc = 0;
+                for (int w = q; w < W; w += 4) acc += per_warp[w];
+                sp = std::max(sp, acc);
+            }
+            out[4 * si + 0] = st.kind;
+            out[4 * si + 1] = tot;
+            out[4 * si + 2] = mx;
+            out[4 * si + 3] = sp;
+        }
+    });
+}
+
 fcct_status fcct_debug_v2_stats(int n, double r, double s, double t, int inverse, int64_t* stats /* 6 */) {
     return guarded([&] {
         auto root = build_tree(n, Params{r, s, t});
@@ -1276,7 +1330,9 @@ fcct_status fcct_debug_timing(fcct_plan plan, int inverse, unsigned long long* o
         if (!plan || !plan->v2) throw FcctError(ST_INVALID_ARGUMENT, "plan has no v2 pipeline");
         const auto& t = inverse ? plan->inv2 : plan->fwd2;
         if (!t.desc.timing) throw FcctError(ST_INVALID_ARGUMENT, "FCCT_DEBUG_TIMING was not set at plan creation");
-        ck(cudaMemcpy(out, t.desc.timing, sizeof(unsigned long long) * (kMaxStages + 2), cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(out, t.desc.timing, sizeof(unsigned long long) * (kMaxStages + 2 + kMaxStages * 16),
+                      cudaMemcpyDeviceToHost),
+           "D2H");
         *nstages = t.desc.nstages;
     });
 }

@@ -265,6 +265,17 @@ __device__ __forceinline__ double lds_f64_xor_hi(uint32_t addr, uint32_t sign) {
     return __hiloint2double(static_cast<int>(hi ^ sign), static_cast<int>(lo));
 }
 
+// v with its sign bit xor-ed by `s` (0 or 0x80000000) on the integer pipe: a
+// plain negation compiles to DADD, which competes with DMMA for the FP64 pipe.
+__device__ __forceinline__ double xor_hi(double v, uint32_t s) {
+    uint32_t lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(v));
+    asm("xor.b32 %0, %0, %1;" : "+r"(hi) : "r"(s));
+    double o;
+    asm("mov.b64 %0, {%1, %2};" : "=d"(o) : "r"(lo), "r"(hi));
+    return o;
+}
+
 __device__ __forceinline__ double flip_unless(double v, int part) {
     // part == 0 (re rows of the swapped operand): -x_im; part == 1: +x_re
     return __hiloint2double(__double2hiint(v) ^ (part ? 0 : static_cast<int>(0x80000000u)), __double2loint(v));
@@ -343,19 +354,61 @@ __device__ __forceinline__ void issue_tile_load(const NextLoad& nl) {
 
 __constant__ int d_debug_flags;  // timing experiments only (bit 0: skip sparse fragment loads)
 
+constexpr int kRing = 4;  // table entries in flight per warp (cp.async ring depth)
+
+// Stage barrier: the whole CTA, or only the warp group of one root child
+// (named barrier 1 + group, WARPS/8 warps) when the stage keeps every group's
+// data inside its own slot range.
+template <int WARPS>
+__device__ __forceinline__ void stage_sync(int group_scope, int warp) {
+    if (group_scope) {
+        constexpr int wpg = WARPS / 8;
+        asm volatile("bar.sync %0, %1;\n" ::"r"(1 + warp / wpg), "r"(32 * wpg) : "memory");
+    } else {
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void sts128(uint32_t addr, double a, double b) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
+
+// One stage of the fast pipeline on the FP64 tensor pipe.
+//
+// The complex stage operator is applied in real form: for an 8-block m-tile
+// the DMMA A operand is an 8 x 4 fragment of real parts (a_re) or imaginary
+// parts (a_im) of 4 input slots; the B operand is a 4 x 8 table tile T = Tr +
+// i Ti; the C accumulators are the real and imaginary outputs:
+//     C_re += a_re Tr - a_im Ti,   C_im += a_re Ti + a_im Tr
+// (real tiles skip the Ti terms). One 16-byte shared load per lane returns a
+// slot's (re, im) pair, i.e. both A fragments, and one 16-byte store writes an
+// output's (re, im): every shared access moves unique data, conflict-free for
+// the edge-coloured slot layouts (tiling.cpp), and no operand needs a sign flip
+// or a part select except -Ti, one integer xor per table entry.
+// Per-warp table-entry ring (kRing x 32 lanes x 16 B in shared memory).
+struct RingCtx {
+    double2* ring;
+};
+
 template <int TB, int WARPS>
 __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int stride, int warp, int lane,
                                        const unsigned char* arena, const TileOut& to, const NextLoad& nl,
-                                       unsigned long long* tcomp = nullptr) {
+                                       unsigned long long* tcomp, RingCtx& rc, unsigned long long* wt = nullptr) {
+    const long long wt0 = wt != nullptr ? clock64() : 0;
     const int r = lane >> 2, k = lane & 3;
-    const int t_sub = r >> 1, part = r & 1;
-    const int n_out = lane >> 2;
     constexpr int kU2 = 64 / WARPS;  // units per warp
-    constexpr int MT = TB / 4;       // m-tiles (8 data rows each) per unit
-    double acc[kU2][MT][2];
+    constexpr int MT = TB / 8;       // m-tiles (8 blocks each)
+    double2* ring = rc.ring;
+    double acc[kU2][MT][2][2];       // [unit][m-tile][re, im][c0, c1]
     int o0[kU2], o1[kU2];
-    const double* Xr = X + t_sub * stride + part;        // + 4 mt stride + 2 slot
-    const double* Xs = X + t_sub * stride + (1 - part);  // part-swapped
+    const uint32_t xb = smem_u32(X) + static_cast<uint32_t>(r * stride) * 8u;  // block r of m-tile 0
+    const uint32_t mstep = static_cast<uint32_t>(8 * stride) * 8u;             // next m-tile (8 blocks)
     const int* __restrict__ s_units = reinterpret_cast<const int*>(arena + sd.o_warp_units);
     const int* __restrict__ s_uout = reinterpret_cast<const int*>(arena + sd.o_u_out);
     int units[kU2];
@@ -363,136 +416,114 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
     for (int j = 0; j < kU2; ++j) {
         units[j] = s_units[warp * kU2 + j];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) acc[j][mt][0] = acc[j][mt][1] = 0.0;
+        for (int mt = 0; mt < MT; ++mt) acc[j][mt][0][0] = acc[j][mt][0][1] = acc[j][mt][1][0] = acc[j][mt][1][1] = 0.0;
         o0[j] = o1[j] = -1;
     }
     if (sd.kind == 0) {
-        // This warp's entry stream (tiling.hpp) with a 2-deep register prefetch
-        // of (Re, Im, slot): every descriptor field is hoisted out of the loop
-        // and shared memory is addressed through 32-bit shared-window offsets.
+        // This warp's entry stream (tiling.hpp): (Re, Im) of the table tiles
+        // stream through a kRing-deep per-warp cp.async ring (each lane copies
+        // and reads back only its own 16 bytes: no warp synchronisation). Per
+        // unit the real tiles come first, then the complex ones, so both
+        // loops are branch-free (a predicated-off DMMA would still take its
+        // tensor-pipe slot).
         const int* __restrict__ s_wbase = reinterpret_cast<const int*>(arena + sd.o_w_base);
         const int* __restrict__ s_wcount = reinterpret_cast<const int*>(arena + sd.o_w_count);
+        const int* __restrict__ s_wccount = reinterpret_cast<const int*>(arena + sd.o_w_ccount);
         const int base = s_wbase[warp];
         const int total = s_wbase[warp + 1] - base;
-        const double* __restrict__ pre = sd.e_re + static_cast<size_t>(base) * 32 + lane;
-        const double* __restrict__ pim = sd.e_im + static_cast<size_t>(base) * 32 + lane;
         const int* __restrict__ psl = reinterpret_cast<const int*>(arena + sd.o_e_slots) + base * 4 + k;
-        int cnt[kU2];
+        const uint32_t rs = smem_u32(ring + warp * kRing * 32 + lane);
+        const double2* __restrict__ pri = sd.e_ri + static_cast<size_t>(base) * 32 + lane;
 #pragma unroll
-        for (int j = 0; j < kU2; ++j) cnt[j] = s_wcount[warp * kU2 + j];
-        double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0;
-        int sl0 = 0, sl1 = 0;
-        if (total > 0) {
-            re0 = __ldg(pre);
-            im0 = __ldg(pim);
-            sl0 = psl[0];
+        for (int q = 0; q < kRing - 1; ++q) {
+            if (q < total)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(rs + q * 512), "l"(pri + q * 32)
+                             : "memory");
+            cp_async_commit();
         }
-        if (total > 1) {
-            re1 = __ldg(pre + 32);
-            im1 = __ldg(pim + 32);
-            sl1 = psl[4];
-        }
-        // operand double-buffering: the next entry's data rows are loaded
-        // (plain, schedulable shared loads) before this entry's DMMAs issue
-        const double* __restrict__ xrow = reinterpret_cast<const double*>(X) + t_sub * stride + part;
-        const int mrow = 4 * stride;
-        double a_c[MT], a_n[MT];
+        // issues entry f + kRing - 1, loads entry f's A fragments and table tile
+        auto next = [&](int f, double2 (&a)[MT]) -> double2 {
+            const int q = f + kRing - 1;
+            if (q < total)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(rs + (q & (kRing - 1)) * 512),
+                             "l"(pri + q * 32)
+                             : "memory");
+            cp_async_commit();
+            const uint32_t xa = xb + static_cast<uint32_t>(psl[f * 4] & ~(1 << 30)) * 16u;
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) a_c[mt] = xrow[mt * mrow + 2 * (sl0 & ~(1 << 30))];
+            for (int mt = 0; mt < MT; ++mt) a[mt] = lds128(xa + mt * mstep);
+            cp_async_wait<kRing - 1>();
+            return lds128(rs + (f & (kRing - 1)) * 512);
+        };
         int f = 0;
 #pragma unroll
         for (int j = 0; j < kU2; ++j) {
-            for (int e = 0; e < cnt[j]; ++e, ++f) {
-                double re2 = 0.0, im2 = 0.0;
-                int sl2 = 0;
-                if (f + 2 < total) {
-                    if (!(d_debug_flags & 1)) {
-                        re2 = __ldg(pre + (f + 2) * 32);
-                        im2 = __ldg(pim + (f + 2) * 32);
-                    } else {
-                        re2 = 0.5;
-                        im2 = 0.25;
-                    }
-                    sl2 = psl[(f + 2) * 4];
+            const int nc = s_wccount[warp * kU2 + j];
+            const int nr = s_wcount[warp * kU2 + j] - nc;
+            for (int e = 0; e < nr; ++e, ++f) {
+                double2 a[MT];
+                const double2 t = next(f, a);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    dmma884(acc[j][mt][0][0], acc[j][mt][0][1], a[mt].x, t.x);
+                    dmma884(acc[j][mt][1][0], acc[j][mt][1][1], a[mt].y, t.x);
                 }
-                if (f + 1 < total) {
+            }
+            for (int e = 0; e < nc; ++e, ++f) {
+                double2 a[MT];
+                const double2 t = next(f, a);
+                const double nti = xor_hi(t.y, 0x80000000u);
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) a_n[mt] = xrow[mt * mrow + 2 * (sl1 & ~(1 << 30))];
+                for (int mt = 0; mt < MT; ++mt) {
+                    dmma884(acc[j][mt][0][0], acc[j][mt][0][1], a[mt].x, t.x);
+                    dmma884(acc[j][mt][1][0], acc[j][mt][1][1], a[mt].y, t.x);
+                    dmma884(acc[j][mt][0][0], acc[j][mt][0][1], a[mt].y, nti);
+                    dmma884(acc[j][mt][1][0], acc[j][mt][1][1], a[mt].x, t.y);
                 }
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a_c[mt], re0);
-                if ((sl0 >> 30) & 1) {
-                    const double* __restrict__ xsw = xrow + (part ? -1 : 1) + 2 * (sl0 & ~(1 << 30));
-                    double as[MT];
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) as[mt] = part ? xsw[mt * mrow] : -xsw[mt * mrow];
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], as[mt], im0);
-                }
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) a_c[mt] = a_n[mt];
-                re0 = re1;
-                im0 = im1;
-                sl0 = sl1;
-                re1 = re2;
-                im1 = im2;
-                sl1 = sl2;
             }
             if (units[j] >= 0) {
                 o0[j] = s_uout[units[j] * 8 + 2 * k];
                 o1[j] = s_uout[units[j] * 8 + 2 * k + 1];
             }
         }
+        cp_async_wait<0>();
     } else {
-        // K fragments of the next unit are prefetched into registers
-        double2 kf[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-        int ks[2] = {0, 0};
-        auto fetch = [&](int u, double2 (&f)[2], int (&sl)[2]) {
-            if (u < 0) return;
-            const int* s_unode = reinterpret_cast<const int*>(arena + sd.o_u_node);
-            const double2* Kbase = sd.o_K >= 0 ? reinterpret_cast<const double2*>(arena + sd.o_K) : sd.K;
-            const double2* Kq = Kbase + s_unode[u] * 64;
-#pragma unroll
-            for (int kt = 0; kt < 2; ++kt) {
-                sl[kt] = reinterpret_cast<const int*>(arena + sd.o_u_in)[u * 8 + kt * 4 + k];
-                f[kt] = Kq[n_out * 8 + kt * 4 + k];  // K[b = n][g]
-            }
-        };
-        fetch(units[0], kf, ks);
+        // 8x8 complex K per unit (B fragment: K[b = n][g = 4 kt + k]); the next
+        // unit's K fragments and input slots are prefetched into registers
+        const int* __restrict__ s_unode = reinterpret_cast<const int*>(arena + sd.o_u_node);
+        const int* __restrict__ s_uin = reinterpret_cast<const int*>(arena + sd.o_u_in);
+        const bool k_smem = sd.o_K >= 0;
+        const double2* __restrict__ Ks = reinterpret_cast<const double2*>(arena + (k_smem ? sd.o_K : 0));
+        const int kidx = r * 8 + k;  // K[b = r][g = k] (+ 4 kt)
 #pragma unroll
         for (int j = 0; j < kU2; ++j) {
-            double2 nf[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-            int ns[2] = {0, 0};
-            if (j + 1 < kU2) fetch(units[j + 1], nf, ns);
-            if (units[j] >= 0) {
-                const double2* __restrict__ xrow = reinterpret_cast<const double2*>(X + t_sub * stride);
-                const int mrow2 = 2 * stride;  // 4 blocks, in double2 units
-                double a[2][MT], as[2][MT];
+            if (units[j] < 0) continue;
+            const int u = units[j];
+            const int node = s_unode[u] * 64 + kidx;
 #pragma unroll
-                for (int kt = 0; kt < 2; ++kt)
+            for (int kt = 0; kt < 2; ++kt) {
+                const int slot = s_uin[u * 8 + kt * 4 + k];
+                const double2 kf = k_smem ? Ks[node + kt * 4] : __ldg(sd.K + node + kt * 4);
+                const uint32_t xa = xb + static_cast<uint32_t>(slot) * 16u;
+                double2 a[MT];
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) {
-                        const double2 v = xrow[mt * mrow2 + ks[kt]];
-                        a[kt][mt] = part ? v.y : v.x;
-                        as[kt][mt] = part ? v.x : -v.y;
-                    }
+                for (int mt = 0; mt < MT; ++mt) a[mt] = lds128(xa + mt * mstep);
+                const double nki = xor_hi(kf.y, 0x80000000u);
 #pragma unroll
-                for (int kt = 0; kt < 2; ++kt) {
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], a[kt][mt], kf[kt].x);
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[j][mt][0], acc[j][mt][1], as[kt][mt], kf[kt].y);
+                for (int mt = 0; mt < MT; ++mt) {
+                    dmma884(acc[j][mt][0][0], acc[j][mt][0][1], a[mt].x, kf.x);
+                    dmma884(acc[j][mt][1][0], acc[j][mt][1][1], a[mt].y, kf.x);
+                    dmma884(acc[j][mt][0][0], acc[j][mt][0][1], a[mt].y, nki);
+                    dmma884(acc[j][mt][1][0], acc[j][mt][1][1], a[mt].x, kf.y);
                 }
-                o0[j] = s_uout[units[j] * 8 + 2 * k];
-                o1[j] = s_uout[units[j] * 8 + 2 * k + 1];
             }
-            kf[0] = nf[0];
-            kf[1] = nf[1];
-            ks[0] = ns[0];
-            ks[1] = ns[1];
+            o0[j] = s_uout[u * 8 + 2 * k];
+            o1[j] = s_uout[u * 8 + 2 * k + 1];
         }
     }
-    __syncthreads();
+    if (wt != nullptr && lane == 0)
+        atomicAdd(wt + warp, static_cast<unsigned long long>(clock64() - wt0));
+    stage_sync<WARPS>(sd.sync_mid, warp);
     if (tcomp != nullptr) *tcomp = clock64();
     if (to.out != nullptr) {
         if (threadIdx.x == 0) {
@@ -501,13 +532,29 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
         }
 #pragma unroll
         for (int j = 0; j < kU2; ++j)
-            if (o0[j] >= 0) store_unit_global(to, t_sub, part, o0[j], o1[j], acc[j]);
+            if (o0[j] >= 0) {
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const int t = 8 * mt + r;
+                    if (t < to.nvalid) {
+                        double2* row = reinterpret_cast<double2*>(to.out + (to.t0 + t) * to.dimr);
+                        row[o0[j]] = make_double2(acc[j][mt][0][0], acc[j][mt][1][0]);
+                        row[o1[j]] = make_double2(acc[j][mt][0][1], acc[j][mt][1][1]);
+                    }
+                }
+            }
         return;
     }
 #pragma unroll
     for (int j = 0; j < kU2; ++j)
-        if (o0[j] >= 0) store_unit(X, stride, t_sub, part, o0[j], o1[j], acc[j]);
-    __syncthreads();
+        if (o0[j] >= 0) {
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                sts128(xb + mt * mstep + static_cast<uint32_t>(o0[j]) * 16u, acc[j][mt][0][0], acc[j][mt][1][0]);
+                sts128(xb + mt * mstep + static_cast<uint32_t>(o1[j]) * 16u, acc[j][mt][0][1], acc[j][mt][1][1]);
+            }
+        }
+    stage_sync<WARPS>(sd.sync_end, warp);
 }
 
 template <int TB, int WARPS>
@@ -521,6 +568,8 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
     double* X = reinterpret_cast<double*>(smem_raw + 128);
     const int stride = d.stride;
     unsigned char* arena = smem_raw + 128 + static_cast<size_t>(TB) * stride * sizeof(double);
+    double2* ring = d.ring ? reinterpret_cast<double2*>(arena + d.arena_bytes) : nullptr;
+    RingCtx rc{ring};
     const int dimr = 2 * d.N;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t ntiles = (batch + TB - 1) / TB;
@@ -549,8 +598,9 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
             const TileOut none{nullptr, 0, 0, 0};
             const int64_t nt = tile + gridDim.x, nn = tile + 2 * static_cast<int64_t>(gridDim.x);
             const NextLoad nl{in, bar, X, stride, dimr, nt < ntiles ? nt : -1, batch, nn < ntiles ? nn : -1};
-            for (int s = 0; s + 1 < d.nstages; ++s) stage2<TB, WARPS>(d.st[s], X, stride, warp, lane, arena, none, nl);
-            stage2<TB, WARPS>(d.st[d.nstages - 1], X, stride, warp, lane, arena, TileOut{out, t0, nvalid, dimr}, nl);
+            for (int s = 0; s + 1 < d.nstages; ++s) stage2<TB, WARPS>(d.st[s], X, stride, warp, lane, arena, none, nl, nullptr, rc);
+            stage2<TB, WARPS>(d.st[d.nstages - 1], X, stride, warp, lane, arena, TileOut{out, t0, nvalid, dimr}, nl,
+                              nullptr, rc);
         }
         return;
     }
@@ -639,7 +689,8 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
         for (int s = 0; s < d.nstages; ++s) {
             __shared__ unsigned long long tmid;
             if ((d.stage_mask >> s) & 1)
-                stage2<TB, WARPS>(d.st[s], X, stride, warp, lane, arena, none, nonl, timing ? &tmid : nullptr);
+                stage2<TB, WARPS>(d.st[s], X, stride, warp, lane, arena, none, nonl, timing ? &tmid : nullptr, rc,
+                                  (d.timing != nullptr && blockIdx.x == 0) ? d.timing + kMaxStages + 2 + s * 16 : nullptr);
             if (timing) {
                 const long long c1 = clock64();
                 tacc[1 + s] += tmid - c0;              // compute phase (to the mid barrier)
@@ -701,7 +752,8 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
 template <int TB, int WARPS>
 cudaError_t launch_pipeline2_t(const Pipeline2Desc& d, const void* in, void* out, int64_t batch, cudaStream_t st,
                                int num_sms) {
-    const int smem = 128 + TB * d.stride * static_cast<int>(sizeof(double)) + d.arena_bytes;
+    const int smem = 128 + TB * d.stride * static_cast<int>(sizeof(double)) + d.arena_bytes +
+                     (d.ring ? WARPS * kRing * 32 * static_cast<int>(sizeof(double2)) : 0);
     auto kern = pipeline2_kernel<TB, WARPS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -711,6 +763,9 @@ cudaError_t launch_pipeline2_t(const Pipeline2Desc& d, const void* in, void* out
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (batch + TB - 1) / TB;
     const int64_t grid = std::min<int64_t>(ntiles, static_cast<int64_t>(per_sm) * num_sms);
+    if (std::getenv("FCCT_DEBUG_LAUNCH"))
+        std::fprintf(stderr, "pipeline2<%d,%d>: smem %d B (arena %d), %d CTA/SM, grid %lld\n", TB, WARPS, smem,
+                     d.arena_bytes, per_sm, static_cast<long long>(grid));
     kern<<<static_cast<unsigned>(grid), WARPS * 32, smem, st>>>(d, in, out, batch);
     return cudaGetLastError();
 }

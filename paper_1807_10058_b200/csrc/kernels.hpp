@@ -48,13 +48,17 @@ struct Stage2Dev {
     int o_u_out;       // int [units][8]
     int o_w_base;      // sparse: int [warps + 1] warp-major entry ranges
     int o_w_count;     // sparse: int [warps][units]
+    int o_w_ccount;    // sparse: int [warps][units] complex entries (after the real ones)
     int o_e_slots;     // sparse: int [entries][4] input slots (bit 30: complex tile)
     int o_u_node;      // mix: int [units]
     int o_u_in;        // mix: int [units][8]
     int o_K;           // mix: double2 [nodes][8][8] when small enough, else -1
     const double* e_re;  // sparse: [entries][32] Re T[k][n], lane order (global)
     const double* e_im;  // sparse: [entries][32] Im T[k][n] (global)
+    const double2* e_ri; // sparse: [entries][32] (Re, Im) interleaved: the cp.async ring's source
     const double2* K;    // mix: global copy of the K tables
+    int sync_mid;        // barrier between compute and store: 0 CTA, 1 warp group (root child)
+    int sync_end;        // barrier after the store: 0 CTA, 1 warp group
 };
 
 struct Pipeline2Desc {
@@ -69,6 +73,7 @@ struct Pipeline2Desc {
     int io_f32;        // 1: global data is complex64 (converted to/from fp64 at tile load/store)
     int real_in;       // 1: input rows are real samples (z_transform fused into the tile load)
     int real_out;      // 1: only real parts are stored (grid_from_signal fused into the tile store)
+    int ring;          // 1: sparse-stage table entries stream through a per-warp cp.async ring in smem
     int stage_mask;    // debug/timing only: stages with a cleared bit are skipped
     unsigned long long* timing;  // debug: CTA 0 accumulates clock64 per phase (nullptr: off)
     Stage2Dev st[kMaxStages];

@@ -148,6 +148,30 @@ Tiling tile_rows(int N, const Rows& rows) {
     return T;
 }
 
+// Block-diagonal operator (one diagonal block of size s3 per node): every
+// node is tiled on its own, so units and k-tiles never straddle two nodes and
+// the k-tiles of node q are exactly [q s3/4, (q+1) s3/4).
+Tiling tile_rows_nodes(int N, const Rows& rows, int s3) {
+    if (s3 >= N) return tile_rows(N, rows);
+    Tiling T;
+    T.tiles.resize(N / 8);
+    for (int q = 0; q < N / s3; ++q) {
+        const int off = q * s3;
+        Rows sub(s3);
+        for (int r = 0; r < s3; ++r)
+            for (const auto& [c, v] : rows[off + r]) {
+                if (c < off || c >= off + s3) throw FcctError(ST_INVALID_ARGUMENT, "tiling: operator is not block diagonal");
+                sub[r].emplace_back(c - off, v);
+            }
+        const Tiling t = tile_rows(s3, sub);
+        for (int32_t r : t.row_order) T.row_order.push_back(off + r);
+        for (int32_t c : t.col_order) T.col_order.push_back(off + c);
+        for (int m = 0; m < s3 / 8; ++m)
+            for (const auto& [kt, vals] : t.tiles[m]) T.tiles[off / 8 + m].emplace_back(off / 4 + kt, vals);
+    }
+    return T;
+}
+
 // Proper 4-edge-colouring of a 4-regular bipartite multigraph given as edges
 // (left, right); returns the colour of every edge. Peels 4 perfect matchings
 // (each exists by König's theorem) found with Kuhn's augmenting paths.
@@ -185,6 +209,7 @@ struct Logical {
     Rows rows;                           // sparse
     std::vector<const PlanNode*> nodes;  // mix
     bool inverse = false;
+    int s3 = 0;                          // points per node of this level
 };
 
 }  // namespace
@@ -212,6 +237,7 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, const Shape2& shape, 
         L.kind = 0;
         L.rows.resize(N);
         const int64_t s3 = cube(lv[0]->n);
+        L.s3 = static_cast<int>(s3);
         for (size_t q = 0; q < lv.size(); ++q) {
             const SparseLD& S = inv ? lv[q]->Binv : lv[q]->B;
             const int64_t off = static_cast<int64_t>(q) * s3;
@@ -226,6 +252,7 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, const Shape2& shape, 
         L.kind = 1;
         L.nodes = lv;
         L.inverse = inv;
+        L.s3 = static_cast<int>(cube(lv[0]->n));
         return L;
     };
     std::vector<Logical> logical;
@@ -241,6 +268,11 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, const Shape2& shape, 
         }
     }
     const int S = static_cast<int>(logical.size());
+    // a stage is group-local when its level has more than one node (n > 2:
+    // every node lies inside one root child)
+    std::vector<char> local(S, 0);
+    if (n >= 4)
+        for (int s = 0; s < S; ++s) local[s] = logical[s].s3 * 8 <= N;
 
     // Units: for each stage, its units' 8 output positions and k-tiles' 4 input positions.
     std::vector<Tiling> tilings(S);
@@ -249,7 +281,7 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, const Shape2& shape, 
     for (int s = 0; s < S; ++s) {
         auto& L = logical[s];
         if (L.kind == 0) {
-            tilings[s] = tile_rows(N, L.rows);
+            tilings[s] = tile_rows_nodes(N, L.rows, L.s3);
             const auto& T = tilings[s];
             for (int m = 0; m < N / 8; ++m) {
                 std::array<int32_t, 8> o{};
@@ -376,24 +408,40 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, const Shape2& shape, 
             for (int u = 0; u < st.n_units; ++u) cost[u] = 4;
             st.dmma_per_tile += static_cast<int64_t>(st.n_units) * 4 * (shape.tb / 4);
         }
-        // LPT assignment of units to warps, at most kUnits2 per warp
+        // LPT assignment of units to warps, at most kUnits2 per warp. In a
+        // group-local stage (a level below the root: every unit lives inside
+        // one root child's N/8 positions) the units of child c go to warp
+        // group c only, so the group can run the stage on its own barrier.
         std::vector<int32_t> order(st.n_units);
         std::iota(order.begin(), order.end(), 0);
         std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
         st.warp_units.assign(kWarps2 * kUnits2, -1);
         std::vector<int64_t> load(kWarps2, 0);
         std::vector<int> cnt(kWarps2, 0);
+        const bool grouped = local[s] && kWarps2 % 8 == 0;
+        const int wpg = kWarps2 / 8;
         for (int32_t u : order) {
             int best = -1;
-            for (int w = 0; w < kWarps2; ++w)
+            const int g = unit_outs[s][u][0] / (N / 8);
+            for (int w = 0; w < kWarps2; ++w) {
+                if (grouped && w / wpg != g) continue;
                 if (cnt[w] < kUnits2 && (best < 0 || load[w] < load[best])) best = w;
+            }
             if (best < 0) return false;
             st.warp_units[best * kUnits2 + cnt[best]++] = u;
             load[best] += cost[u];
         }
+        // barrier scope between compute and store (sync_mid) and after the
+        // store (sync_end): a warp group suffices when the group's inputs and
+        // outputs stay inside its own slot range [c N/8, (c+1) N/8)
+        const bool in_closed = grouped && s >= 1;
+        const bool out_closed = grouped && s + 1 <= S - 1 && local[s + 1];
+        st.sync_mid = (in_closed && out_closed) ? 1 : 0;
+        st.sync_end = out_closed ? 1 : 0;
         if (st.kind == 0) {
             st.w_base.assign(kWarps2 + 1, 0);
             st.w_count.assign(kWarps2 * kUnits2, 0);
+            st.w_ccount.assign(kWarps2 * kUnits2, 0);
             st.w_cplx.assign(kWarps2 * 4, 0u);
             int32_t flat = 0;
             for (int w = 0; w < kWarps2; ++w) {
@@ -402,6 +450,13 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, const Shape2& shape, 
                     const int u = st.warp_units[w * kUnits2 + j];
                     if (u < 0) continue;
                     st.w_count[w * kUnits2 + j] = static_cast<int32_t>(uent[u].size());
+                    // real tiles first, complex after: the kernel runs one
+                    // branch-free loop for each kind
+                    std::stable_sort(uent[u].begin(), uent[u].end(),
+                                     [](const Entry& a, const Entry& b) { return a.cplx < b.cplx; });
+                    int32_t nc = 0;
+                    for (const auto& e : uent[u]) nc += e.cplx ? 1 : 0;
+                    st.w_ccount[w * kUnits2 + j] = nc;
                     for (const auto& e : uent[u]) {
                         for (int k = 0; k < 4; ++k) st.e_slots.push_back(e.slots[k] | (e.cplx ? (1 << 30) : 0));
                         st.e_re.insert(st.e_re.end(), e.re.begin(), e.re.end());

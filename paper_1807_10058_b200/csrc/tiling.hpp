@@ -46,6 +46,7 @@ struct Stage2Host {
     // unit j of warp w has w_count[w][j] of them.
     std::vector<int32_t> w_base;      // [warps + 1]
     std::vector<int32_t> w_count;     // [warps][units]
+    std::vector<int32_t> w_ccount;    // [warps][units] complex entries (stored after the real ones)
     std::vector<uint32_t> w_cplx;     // [warps][4]: bit f = flat entry f of the warp is complex (<= 128 entries)
     std::vector<int32_t> e_slots;     // [n_entries][4] input slot of k-column; bit 30 = complex tile
     std::vector<double> e_re;         // [n_entries][32] Re T[k][n], lane order
@@ -55,6 +56,8 @@ struct Stage2Host {
     std::vector<int32_t> u_in;        // [n_units][8] input slot of input g
     std::vector<double> K;            // [nodes][8 b][8 g][2]
     int64_t dmma_per_tile = 0;        // DMMA.884 per 16-block tile
+    int sync_mid = 0;                 // barrier between compute and store: 0 CTA, 1 warp group
+    int sync_end = 0;                 // barrier after the store: 0 CTA, 1 warp group
 };
 
 struct Pipeline2Host {

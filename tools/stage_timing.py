@@ -13,7 +13,7 @@ from paper_1807_10058_b200 import SkewParams, _capi, build_plan  # noqa: E402
 from paper_1807_10058_b200.fcct import _raise  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-blocks = 65536
+blocks = int(sys.argv[2]) if len(sys.argv) > 2 else 65536
 plan = build_plan(n, SkewParams.canonical())
 x = torch.randn(blocks, n**3, dtype=torch.complex128, device="cuda")
 y = torch.empty_like(x)
@@ -23,7 +23,7 @@ for inv in (0, 1):
     for _ in range(3):
         _raise(fn(plan._h, x.data_ptr(), y.data_ptr(), blocks, None))
     torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * 18)()
+    buf = (ctypes.c_ulonglong * (18 + 16 * 16))()
     ns = ctypes.c_int()
     _raise(L.fcct_debug_timing(plan._h, inv, buf, ctypes.byref(ns)))
     t = np.array(buf[:], dtype=np.float64)
@@ -33,3 +33,8 @@ for inv in (0, 1):
     tot = t[0] + comp.sum() + store.sum()
     print(("inverse" if inv else "forward"), "total Mcycles (CTA 0)", round(tot / 1e6, 3), f"load={100 * t[0] / tot:.1f}%",
           " ".join(f"s{i}=({100 * comp[i] / tot:.1f}% + {100 * store[i] / tot:.1f}%)" for i in range(S)))
+    if len(sys.argv) > 3:  # per-warp compute-phase cycles per tile (CTA 0)
+        tiles = (blocks + 16 * 148 - 1) // (16 * 148)
+        for i in range(S):
+            w = t[18 + 16 * i: 18 + 16 * i + 16] / tiles
+            print(f"   s{i} per-warp compute cyc/tile: min {w.min():.0f} mean {w.mean():.0f} max {w.max():.0f}  stage {comp[i] / tiles:.0f}")
