@@ -138,6 +138,10 @@ void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
     constexpr size_t kArenaK = 16 * 1024;  // K tables up to this size go to shared memory
     const char* gs = std::getenv("FCCT_V2_GROUP_SYNC");  // A/B switch: 0 = CTA-wide barriers only
     const bool group_sync = gs ? std::atoi(gs) != 0 : true;
+    const char* ns = std::getenv("FCCT_V2_NAT_SHIFT");  // A/B switch: 0 = unshifted natural rows
+    const bool nat_shift = ns ? std::atoi(ns) != 0 : true;
+    out.desc.shift_in = nat_shift ? 2 * h.shift_in : 0;
+    out.desc.shift_out = nat_shift ? 2 * h.shift_out : 0;
     for (size_t s = 0; s < h.stages.size(); ++s) {
         const Stage2Host& st = h.stages[s];
         Stage2Dev& d = out.desc.st[s];
@@ -146,6 +150,8 @@ void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
         d.n_units = st.n_units;
         d.sync_mid = group_sync ? st.sync_mid : 0;
         d.sync_end = group_sync ? st.sync_end : 0;
+        d.ld_shift = (s == 0 && nat_shift) ? 16 * h.shift_in : 0;
+        d.st_shift = (s + 1 == h.stages.size() && nat_shift) ? 16 * h.shift_out : 0;
         d.o_warp_units = put(st.warp_units.data(), st.warp_units.size() * 4);
         d.o_u_out = put(st.u_out.data(), st.u_out.size() * 4);
         d.o_w_base = d.o_w_count = d.o_w_ccount = d.o_e_slots = d.o_u_node = d.o_u_in = d.o_K = -1;
@@ -1265,6 +1271,44 @@ fcct_status fcct_debug_v2_stage_stats(int n, double r, double s, double t, int i
             out[4 * si + 1] = tot;
             out[4 * si + 2] = mx;
             out[4 * si + 3] = sp;
+            // shared-memory wavefronts of one m-tile's 16-byte accesses (4 lanes
+            // k x 2 rows per 8-lane phase; 16-byte bank group = (4 row + slot) mod 8)
+            auto wavefronts = [](const int32_t* slots) {
+                int64_t wf = 0;
+                for (int ph = 0; ph < 4; ++ph) {
+                    int cnt[8] = {};
+                    for (int rr = 0; rr < 2; ++rr)
+                        for (int kk = 0; kk < 4; ++kk) cnt[(4 * (2 * ph + rr) + (slots[kk] & ~(1 << 30))) & 7]++;
+                    int m = 0;
+                    for (int b = 0; b < 8; ++b) m = std::max(m, cnt[b]);
+                    wf += m;
+                }
+                return wf;
+            };
+            int64_t ld = 0, ld_ideal = 0, stw = 0, st_ideal = 0;
+            if (st.kind == 0) {
+                for (size_t e = 0; e < st.e_slots.size() / 4; ++e) {
+                    ld += wavefronts(&st.e_slots[4 * e]);
+                    ld_ideal += 4;
+                }
+            } else {
+                for (int u = 0; u < st.n_units; ++u)
+                    for (int kt = 0; kt < 2; ++kt) {
+                        ld += wavefronts(&st.u_in[u * 8 + kt * 4]);
+                        ld_ideal += 4;
+                    }
+            }
+            for (int u = 0; u < st.n_units; ++u)
+                for (int par = 0; par < 2; ++par) {
+                    int32_t sl[4];
+                    for (int kk = 0; kk < 4; ++kk) sl[kk] = st.u_out[u * 8 + 2 * kk + par];
+                    stw += wavefronts(sl);
+                    st_ideal += 4;
+                }
+            out[64 + 4 * si + 0] = ld;
+            out[64 + 4 * si + 1] = ld_ideal;
+            out[64 + 4 * si + 2] = stw;
+            out[64 + 4 * si + 3] = st_ideal;
         }
     });
 }

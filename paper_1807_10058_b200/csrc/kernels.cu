@@ -330,6 +330,7 @@ struct NextLoad {
     uint64_t* bar;
     double* X;
     int stride;
+    int shift;     // doubles added to odd rows (natural input layout)
     int dimr;
     int64_t tile;  // next tile index (< 0: none)
     int64_t batch;
@@ -343,7 +344,8 @@ __device__ __forceinline__ void issue_tile_load(const NextLoad& nl) {
         const int64_t t0 = nl.tile * TB;
         const int nv = static_cast<int>(nl.batch - t0 < TB ? nl.batch - t0 : TB);
         mbar_arrive_expect_tx(nl.bar, row_bytes * nv);
-        for (int t = 0; t < nv; ++t) tma_load_1d(nl.X + t * nl.stride, nl.in + (t0 + t) * nl.dimr, row_bytes, nl.bar);
+        for (int t = 0; t < nv; ++t)
+            tma_load_1d(nl.X + t * nl.stride + ((t & 1) ? nl.shift : 0), nl.in + (t0 + t) * nl.dimr, row_bytes, nl.bar);
     }
     if (nl.after >= 0) {
         const int64_t a0 = nl.after * TB;
@@ -408,6 +410,8 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
     double acc[kU2][MT][2][2];       // [unit][m-tile][re, im][c0, c1]
     int o0[kU2], o1[kU2];
     const uint32_t xb = smem_u32(X) + static_cast<uint32_t>(r * stride) * 8u;  // block r of m-tile 0
+    const uint32_t xl = xb + ((r & 1) ? sd.ld_shift : 0);                         // A-load base
+    const uint32_t xsb = xb + ((r & 1) ? sd.st_shift : 0);                        // store base
     const uint32_t mstep = static_cast<uint32_t>(8 * stride) * 8u;             // next m-tile (8 blocks)
     const int* __restrict__ s_units = reinterpret_cast<const int*>(arena + sd.o_warp_units);
     const int* __restrict__ s_uout = reinterpret_cast<const int*>(arena + sd.o_u_out);
@@ -449,7 +453,7 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
                              "l"(pri + q * 32)
                              : "memory");
             cp_async_commit();
-            const uint32_t xa = xb + static_cast<uint32_t>(psl[f * 4] & ~(1 << 30)) * 16u;
+            const uint32_t xa = xl + static_cast<uint32_t>(psl[f * 4] & ~(1 << 30)) * 16u;
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) a[mt] = lds128(xa + mt * mstep);
             cp_async_wait<kRing - 1>();
@@ -504,7 +508,7 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
             for (int kt = 0; kt < 2; ++kt) {
                 const int slot = s_uin[u * 8 + kt * 4 + k];
                 const double2 kf = k_smem ? Ks[node + kt * 4] : __ldg(sd.K + node + kt * 4);
-                const uint32_t xa = xb + static_cast<uint32_t>(slot) * 16u;
+                const uint32_t xa = xl + static_cast<uint32_t>(slot) * 16u;
                 double2 a[MT];
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) a[mt] = lds128(xa + mt * mstep);
@@ -550,8 +554,8 @@ __device__ __forceinline__ void stage2(const Stage2Dev& sd, double* X, int strid
         if (o0[j] >= 0) {
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-                sts128(xb + mt * mstep + static_cast<uint32_t>(o0[j]) * 16u, acc[j][mt][0][0], acc[j][mt][1][0]);
-                sts128(xb + mt * mstep + static_cast<uint32_t>(o1[j]) * 16u, acc[j][mt][0][1], acc[j][mt][1][1]);
+                sts128(xsb + mt * mstep + static_cast<uint32_t>(o0[j]) * 16u, acc[j][mt][0][0], acc[j][mt][1][0]);
+                sts128(xsb + mt * mstep + static_cast<uint32_t>(o1[j]) * 16u, acc[j][mt][0][1], acc[j][mt][1][1]);
             }
         }
     stage_sync<WARPS>(sd.sync_end, warp);
@@ -587,7 +591,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
     if (d.direct_store && !d.real_in && !d.real_out) {
         if (threadIdx.x == 0 && static_cast<int64_t>(blockIdx.x) < ntiles) {
             const int64_t nt = blockIdx.x + gridDim.x;
-            issue_tile_load<TB>(NextLoad{in, bar, X, stride, dimr, static_cast<int64_t>(blockIdx.x), batch,
+            issue_tile_load<TB>(NextLoad{in, bar, X, stride, d.shift_in, dimr, static_cast<int64_t>(blockIdx.x), batch,
                                      nt < ntiles ? nt : -1});
         }
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -597,7 +601,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
             phase ^= 1;
             const TileOut none{nullptr, 0, 0, 0};
             const int64_t nt = tile + gridDim.x, nn = tile + 2 * static_cast<int64_t>(gridDim.x);
-            const NextLoad nl{in, bar, X, stride, dimr, nt < ntiles ? nt : -1, batch, nn < ntiles ? nn : -1};
+            const NextLoad nl{in, bar, X, stride, d.shift_in, dimr, nt < ntiles ? nt : -1, batch, nn < ntiles ? nn : -1};
             for (int s = 0; s + 1 < d.nstages; ++s) stage2<TB, WARPS>(d.st[s], X, stride, warp, lane, arena, none, nl, nullptr, rc);
             stage2<TB, WARPS>(d.st[d.nstages - 1], X, stride, warp, lane, arena, TileOut{out, t0, nvalid, dimr}, nl,
                               nullptr, rc);
@@ -605,7 +609,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
         return;
     }
     const TileOut none{nullptr, 0, 0, 0};
-    const NextLoad nonl{in, bar, X, stride, dimr, -1, batch, -1};
+    const NextLoad nonl{in, bar, X, stride, d.shift_in, dimr, -1, batch, -1};
     const bool timing = d.timing != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
     __shared__ unsigned long long tacc[kMaxStages + 2];
     if (threadIdx.x < kMaxStages + 2) tacc[threadIdx.x] = 0;
@@ -623,7 +627,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
                 for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
                     const int t = i / per_row, q = i - t * per_row;
                     const float4 v = __ldg(src + static_cast<int64_t>(t) * per_row + q);
-                    double2* xr = reinterpret_cast<double2*>(X + t * stride) + 4 * q;
+                    double2* xr = reinterpret_cast<double2*>(X + t * stride + ((t & 1) ? d.shift_in : 0)) + 4 * q;
                     xr[0] = make_double2(v.x, 0.0);
                     xr[1] = make_double2(v.y, 0.0);
                     xr[2] = make_double2(v.z, 0.0);
@@ -635,7 +639,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
                 for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
                     const int t = i / per_row, q = i - t * per_row;
                     const double2 v = __ldg(src + static_cast<int64_t>(t) * per_row + q);
-                    double2* xr = reinterpret_cast<double2*>(X + t * stride) + 2 * q;
+                    double2* xr = reinterpret_cast<double2*>(X + t * stride + ((t & 1) ? d.shift_in : 0)) + 2 * q;
                     xr[0] = make_double2(v.x, 0.0);
                     xr[1] = make_double2(v.y, 0.0);
                 }
@@ -658,7 +662,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
             for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
                 const int t = i / per_row, q = i - t * per_row;
                 const float4 v = __ldg(src + static_cast<int64_t>(t) * per_row + q);
-                double2* xr = reinterpret_cast<double2*>(X + t * stride) + 2 * q;
+                double2* xr = reinterpret_cast<double2*>(X + t * stride + ((t & 1) ? d.shift_in : 0)) + 2 * q;
                 xr[0] = make_double2(v.x, v.y);
                 xr[1] = make_double2(v.z, v.w);
             }
@@ -676,7 +680,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
             if (threadIdx.x == 0) {
                 tma_store_wait_read0();
                 const int64_t nt = tile + gridDim.x;
-                issue_tile_load<TB>(NextLoad{in, bar, X, stride, dimr, tile, batch, nt < ntiles ? nt : -1});
+                issue_tile_load<TB>(NextLoad{in, bar, X, stride, d.shift_in, dimr, tile, batch, nt < ntiles ? nt : -1});
             }
             mbar_wait(bar, phase);
             phase ^= 1;
@@ -705,7 +709,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
                 float4* dst = reinterpret_cast<float4*>(out_raw) + t0 * per_row;
                 for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
                     const int t = i / per_row, q = i - t * per_row;
-                    const double* xr = X + t * stride + 8 * q;
+                    const double* xr = X + t * stride + ((t & 1) ? d.shift_out : 0) + 8 * q;
                     dst[static_cast<int64_t>(t) * per_row + q] =
                         make_float4(static_cast<float>(xr[0]), static_cast<float>(xr[2]), static_cast<float>(xr[4]),
                                     static_cast<float>(xr[6]));
@@ -715,7 +719,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
                 double2* dst = reinterpret_cast<double2*>(out_raw) + t0 * per_row;
                 for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
                     const int t = i / per_row, q = i - t * per_row;
-                    const double* xr = X + t * stride + 4 * q;
+                    const double* xr = X + t * stride + ((t & 1) ? d.shift_out : 0) + 4 * q;
                     dst[static_cast<int64_t>(t) * per_row + q] = make_double2(xr[0], xr[2]);
                 }
             }
@@ -727,7 +731,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
             const int per_row = d.N / 2;
             for (int i = threadIdx.x; i < nvalid * per_row; i += blockDim.x) {
                 const int t = i / per_row, q = i - t * per_row;
-                const double2* xr = reinterpret_cast<const double2*>(X + t * stride) + 2 * q;
+                const double2* xr = reinterpret_cast<const double2*>(X + t * stride + ((t & 1) ? d.shift_out : 0)) + 2 * q;
                 const double2 a = xr[0], b = xr[1];
                 dst[static_cast<int64_t>(t) * per_row + q] = make_float4(static_cast<float>(a.x), static_cast<float>(a.y),
                                                                        static_cast<float>(b.x), static_cast<float>(b.y));
@@ -738,7 +742,8 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
         fence_proxy_async_smem();
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int t = 0; t < nvalid; ++t) tma_store_1d(out + (t0 + t) * dimr, X + t * stride, row_bytes);
+            for (int t = 0; t < nvalid; ++t)
+                tma_store_1d(out + (t0 + t) * dimr, X + t * stride + ((t & 1) ? d.shift_out : 0), row_bytes);
             tma_store_commit();
         }
     }

@@ -59,6 +59,8 @@ struct Stage2Dev {
     const double2* K;    // mix: global copy of the K tables
     int sync_mid;        // barrier between compute and store: 0 CTA, 1 warp group (root child)
     int sync_end;        // barrier after the store: 0 CTA, 1 warp group
+    int ld_shift;        // bytes added to the A-load address of odd block rows (natural input layout)
+    int st_shift;        // bytes added to the store address of odd block rows (natural output layout)
 };
 
 struct Pipeline2Desc {
@@ -74,6 +76,8 @@ struct Pipeline2Desc {
     int real_in;       // 1: input rows are real samples (z_transform fused into the tile load)
     int real_out;      // 1: only real parts are stored (grid_from_signal fused into the tile store)
     int ring;          // 1: sparse-stage table entries stream through a per-warp cp.async ring in smem
+    int shift_in;      // doubles: odd block rows of the natural input tile start this far into their row
+    int shift_out;     // doubles: same for the natural output tile (spreads the leaf mix's banks)
     int stage_mask;    // debug/timing only: stages with a cleared bit are skipped
     unsigned long long* timing;  // debug: CTA 0 accumulates clock64 per phase (nullptr: off)
     Stage2Dev st[kMaxStages];

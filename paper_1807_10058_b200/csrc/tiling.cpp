@@ -2,6 +2,7 @@
 #include "tiling.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <array>
 #include <functional>
 #include <map>
@@ -473,6 +474,8 @@ bool compile_pipeline2(const PlanNode& root, bool inverse, const Shape2& shape, 
         out.dmma_per_tile += st.dmma_per_tile;
         out.stages.push_back(std::move(st));
     }
+    out.shift_in = logical.front().kind == 1 ? 1 : 0;
+    out.shift_out = logical.back().kind == 1 ? 1 : 0;
     return true;
 }
 

@@ -67,6 +67,10 @@ struct Pipeline2Host {
     int stride = 0;  // doubles per block row in smem (2N + 8)
     std::vector<Stage2Host> stages;
     int64_t dmma_per_tile = 0;
+    // natural-layout row shift (in 16-byte slots) of odd block rows: a leaf
+    // mix touches 8 natural positions that share their residue mod 4, so odd
+    // rows are moved by one slot to spread them over twice the banks
+    int shift_in = 0, shift_out = 0;
 };
 
 // Builds the stage list for a full radix tree (every leaf n == 1, n <= 8).
