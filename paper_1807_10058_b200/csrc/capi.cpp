@@ -1233,6 +1233,23 @@ fcct_status fcct_debug_emulate_v2(int n, double r, double s, double t, int inver
 
 // Bank-conflict statistics of the compiled v2 tables (host, no GPU): number of
 // 16-lane half-warp load / store requests that hit a bank twice.
+// Input slots (4 per table entry) of one sparse stage of the compiled v2
+// pipeline (profiling / layout experiments). Returns the entry count.
+fcct_status fcct_debug_v2_entry_slots(int n, double r, double s, double t, int inverse, int stage, int32_t* out,
+                                      int64_t cap, int64_t* count) {
+    return guarded([&] {
+        auto root = build_tree(n, Params{r, s, t});
+        Pipeline2Host h;
+        if (!compile_pipeline2(*root, inverse != 0, Shape2{}, h))
+            throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by pipeline v2");
+        if (stage < 0 || stage >= static_cast<int>(h.stages.size())) throw FcctError(ST_INVALID_ARGUMENT, "bad stage");
+        const auto& st = h.stages[stage];
+        *count = static_cast<int64_t>(st.e_slots.size() / 4);
+        if (out && cap >= static_cast<int64_t>(st.e_slots.size()))
+            std::memcpy(out, st.e_slots.data(), st.e_slots.size() * 4);
+    });
+}
+
 // Per-stage work of the compiled v2 pipeline (profiling aid): for each stage
 // kind, DMMA per tile, the busiest warp's DMMA and the busiest SM sub-partition's
 // DMMA (warps w, w+4, w+8, w+12 share one tensor pipe).

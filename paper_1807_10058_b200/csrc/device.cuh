@@ -68,6 +68,31 @@ __device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk
 __device__ __forceinline__ void tma_store_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
+template <int N>
+__device__ __forceinline__ void tma_store_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+// wait until at most n (0..15) of this thread's most recent bulk groups still read shared memory
+__device__ __forceinline__ void tma_store_wait_read_n(int n) {
+    switch (n) {
+        case 0: tma_store_wait_read<0>(); break;
+        case 1: tma_store_wait_read<1>(); break;
+        case 2: tma_store_wait_read<2>(); break;
+        case 3: tma_store_wait_read<3>(); break;
+        case 4: tma_store_wait_read<4>(); break;
+        case 5: tma_store_wait_read<5>(); break;
+        case 6: tma_store_wait_read<6>(); break;
+        case 7: tma_store_wait_read<7>(); break;
+        case 8: tma_store_wait_read<8>(); break;
+        case 9: tma_store_wait_read<9>(); break;
+        case 10: tma_store_wait_read<10>(); break;
+        case 11: tma_store_wait_read<11>(); break;
+        case 12: tma_store_wait_read<12>(); break;
+        case 13: tma_store_wait_read<13>(); break;
+        case 14: tma_store_wait_read<14>(); break;
+        default: tma_store_wait_read<15>(); break;
+    }
+}
 __device__ __forceinline__ void tma_store_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");

@@ -678,9 +678,23 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
             __syncthreads();
         } else {
             if (threadIdx.x == 0) {
-                tma_store_wait_read0();
-                const int64_t nt = tile + gridDim.x;
-                issue_tile_load<TB>(NextLoad{in, bar, X, stride, d.shift_in, dimr, tile, batch, nt < ntiles ? nt : -1});
+                // the previous tile left row by row (one bulk group per row):
+                // each row of this tile is loaded as soon as the copy engine
+                // has read that row out, so the stores and loads overlap
+                const int nv = nvalid;
+                mbar_arrive_expect_tx(bar, row_bytes * nv);
+#pragma unroll
+                for (int t = 0; t < TB; ++t) {
+                    if (t >= nv) break;
+                    tma_store_wait_read_n(TB - 1 - t);
+                    tma_load_1d(X + t * stride + ((t & 1) ? d.shift_in : 0), in + (t0 + t) * dimr, row_bytes, bar);
+                }
+                const int64_t na = tile + gridDim.x;
+                if (na < ntiles) {
+                    const int64_t a0 = na * TB;
+                    const int nva = static_cast<int>(batch - a0 < TB ? batch - a0 : TB);
+                    prefetch_l2_bulk(in + a0 * dimr, row_bytes * nva);
+                }
             }
             mbar_wait(bar, phase);
             phase ^= 1;
@@ -742,9 +756,13 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
         fence_proxy_async_smem();
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int t = 0; t < nvalid; ++t)
-                tma_store_1d(out + (t0 + t) * dimr, X + t * stride + ((t & 1) ? d.shift_out : 0), row_bytes);
-            tma_store_commit();
+            // one bulk group per row, and always TB groups (empty ones for a
+            // ragged last tile) so the next tile's per-row waits line up
+            for (int t = 0; t < TB; ++t) {
+                if (t < nvalid)
+                    tma_store_1d(out + (t0 + t) * dimr, X + t * stride + ((t & 1) ? d.shift_out : 0), row_bytes);
+                tma_store_commit();
+            }
         }
     }
     if (threadIdx.x == 0) tma_store_wait0();
