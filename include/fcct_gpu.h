@@ -70,7 +70,8 @@ typedef struct {
     double flops_forward;    /* algorithmic flops per block */
     double flops_inverse;
     int executor;            /* 0 direct GEMM, 1 tile interpreter, 2 FP64-tensor-pipe
-                                pipeline, 3 global-memory multi-pass pipeline */
+                                pipeline, 3 global-memory multi-pass pipeline,
+                                4 two-level (n = 16: root pass + eight n = 8 pipelines) */
 } fcct_plan_info_t;
 
 /* Last error message on this thread ("" if none). */

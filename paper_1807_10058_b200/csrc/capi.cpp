@@ -96,6 +96,11 @@ struct PipelineTables {
     std::vector<std::shared_ptr<DevBuf>> bufs;
 };
 
+struct RootTables {
+    RootDesc desc{};
+    std::vector<std::shared_ptr<DevBuf>> bufs;
+};
+
 struct Pipeline2Tables {
     Pipeline2Desc desc{};
     std::vector<std::shared_ptr<DevBuf>> bufs;
@@ -108,6 +113,7 @@ void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
     out.desc.warps = h.shape.warps;
     out.desc.N = h.N;
     out.desc.stride = h.stride;
+    out.desc.row_in = out.desc.row_out = 2 * static_cast<int64_t>(h.N);
     out.desc.nstages = static_cast<int>(h.stages.size());
     const char* ds = std::getenv("FCCT_DIRECT_STORE");
     out.desc.direct_store = ds ? std::atoi(ds) : 0;
@@ -465,6 +471,9 @@ struct fcct_plan_s {
     PipelineTables fwd, inv;
     bool v2 = false;  // fp64 DMMA pipeline (tiling.hpp)
     Pipeline2Tables fwd2, inv2;
+    bool two_level = false;  // n = 16: root pass + eight n = 8 child pipelines
+    RootTables rfwd, rinv;
+    Pipeline2Tables cfwd[8], cinv[8];
     bool global = false;  // global-memory multi-pass pipeline
     GlobalTables gfwd, ginv;
     std::shared_ptr<DevBuf> scratch0, scratch1;
@@ -547,6 +556,115 @@ void build_v2(fcct_plan_s* pl) {
     pl->v2 = true;
 }
 
+// Two-level executor (n = 16): the root B and K run as one SIMT pass over a
+// child-major scratch, the eight n = 8 children on the DMMA pipeline (each
+// reading and writing its 512-point slice of every block), and one gather
+// applies the radix permutation. Inverse: gather, children, root pass.
+void build_root_ell(const SparseLD& S, int N, RootTables& rt, RootDesc& d) {
+    const int m3 = N / 8;
+    std::vector<int> width(8, 0);
+    for (int g = 0; g < 8; ++g)
+        for (int h = 0; h < m3; ++h) {
+            const int64_t row = static_cast<int64_t>(g) * m3 + h;
+            width[g] = std::max<int>(width[g], static_cast<int>(S.rowptr[row + 1] - S.rowptr[row]));
+        }
+    d.ell_off[0] = 0;
+    for (int g = 0; g < 8; ++g) d.ell_off[g + 1] = d.ell_off[g] + width[g] * m3;
+    std::vector<int32_t> col(d.ell_off[8], 0);
+    std::vector<double> val(2 * static_cast<size_t>(d.ell_off[8]), 0.0);
+    for (int g = 0; g < 8; ++g)
+        for (int h = 0; h < m3; ++h) {
+            const int64_t row = static_cast<int64_t>(g) * m3 + h;
+            int e = 0;
+            for (int64_t k = S.rowptr[row]; k < S.rowptr[row + 1]; ++k, ++e) {
+                const int64_t idx = d.ell_off[g] + static_cast<int64_t>(e) * m3 + h;
+                col[idx] = S.col[k];
+                val[2 * idx] = static_cast<double>(S.val[k].real());
+                val[2 * idx + 1] = static_cast<double>(S.val[k].imag());
+            }
+        }
+    auto bc = upload(col);
+    auto bv = upload(val);
+    rt.bufs.insert(rt.bufs.end(), {bc, bv});
+    d.col = static_cast<const int*>(bc->ptr);
+    d.val = static_cast<const double2*>(bv->ptr);
+}
+
+void build_two_level(fcct_plan_s* pl) {
+    const PlanNode& root = *pl->tree;
+    if (root.n != 16) return;
+    for (const auto& c : root.children)
+        if (!c->radix || c->n != 8) return;
+    const int N = static_cast<int>(cube(root.n)), m3 = N / 8;
+    const auto perm64 = radix_permutation(root.n);
+    std::vector<int32_t> perm(N), pinv(N);
+    for (int i = 0; i < N; ++i) {
+        perm[i] = static_cast<int32_t>(perm64[i]);
+        pinv[perm[i]] = i;
+    }
+    for (int dir = 0; dir < 2; ++dir) {
+        const bool inv = dir == 1;
+        RootTables& rt = inv ? pl->rinv : pl->rfwd;
+        rt = RootTables{};
+        RootDesc& d = rt.desc;
+        d.N = N;
+        d.m3 = m3;
+        d.lgN = 0;
+        while ((1 << d.lgN) < N) ++d.lgN;
+        build_root_ell(inv ? root.Binv : root.B, N, rt, d);
+        std::vector<double> K(128);
+        const auto& Kq = inv ? root.Kinv : root.K;
+        for (int i = 0; i < 64; ++i) {
+            K[2 * i] = static_cast<double>(Kq[i].real());
+            K[2 * i + 1] = static_cast<double>(Kq[i].imag());
+        }
+        auto bk = upload(K), bp = upload(perm), bi = upload(pinv);
+        rt.bufs.insert(rt.bufs.end(), {bk, bp, bi});
+        d.K = static_cast<const double2*>(bk->ptr);
+        d.perm = static_cast<const int*>(bp->ptr);
+        d.pinv = static_cast<const int*>(bi->ptr);
+    }
+    for (int c = 0; c < 8; ++c) {
+        Pipeline2Host hf, hi;
+        if (!compile_pipeline2(*root.children[c], false, Shape2{}, hf) ||
+            !compile_pipeline2(*root.children[c], true, Shape2{}, hi))
+            return;
+        upload_pipeline2(hf, pl->cfwd[c]);
+        upload_pipeline2(hi, pl->cinv[c]);
+        for (auto* t : {&pl->cfwd[c], &pl->cinv[c]}) t->desc.row_in = t->desc.row_out = 2 * static_cast<int64_t>(N);
+    }
+    pl->two_level = true;
+}
+
+// in_mode / out_mode of the natural side: 0 complex128, 1 complex64, 2 real f64, 3 real f32
+void run_two_level(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, void* out, int out_mode, int64_t batch,
+                   cudaStream_t st) {
+    const int64_t N = cube(pl->n), m3 = N / 8;
+    const size_t bytes = static_cast<size_t>(batch * N * 16);
+    std::lock_guard<std::mutex> lock(pl->scratch_mu);
+    if (!pl->scratch0 || pl->scratch0->bytes < bytes) {
+        ck(cudaStreamSynchronize(st), "sync");
+        pl->scratch0 = std::make_shared<DevBuf>(bytes);
+        pl->scratch1 = std::make_shared<DevBuf>(bytes);
+    }
+    double* s1 = static_cast<double*>(pl->scratch0->ptr);
+    double* s2 = static_cast<double*>(pl->scratch1->ptr);
+    if (!inverse) {
+        ck(launch_root_forward(pl->rfwd.desc, in, in_mode, s1, batch, st, pl->num_sms), "root pass");
+        for (int c = 0; c < 8; ++c)
+            ck(launch_pipeline2(pl->cfwd[c].desc, s1 + 2 * c * m3, s2 + 2 * c * m3, batch, st, pl->num_sms),
+               "child pipeline");
+        ck(launch_child_to_natural(pl->rfwd.desc, s2, out, out_mode, batch, st), "radix permutation");
+    } else {
+        ck(launch_natural_to_child(pl->rinv.desc, in, in_mode, s1, batch, st), "radix permutation");
+        for (int c = 0; c < 8; ++c)
+            ck(launch_pipeline2(pl->cinv[c].desc, s1 + 2 * c * m3, s2 + 2 * c * m3, batch, st, pl->num_sms),
+               "child pipeline");
+        ck(launch_root_inverse(pl->rinv.desc, s2, out, out_mode, batch, st, pl->num_sms), "root pass");
+    }
+    ck(cudaStreamSynchronize(st), "sync");  // the plan-owned scratch serialises calls on this path
+}
+
 // Picks the executor of a fast plan: the fp64 DMMA pipeline (n <= 8), else
 // the shared-memory tile interpreter (one block's state fits a CTA tile),
 // else the global-memory multi-pass pipeline. FCCT_PIPELINE=v1|v2|global
@@ -557,6 +675,8 @@ void build_fast_paths(fcct_plan_s* pl) {
     const bool f32 = pl->precision == FCCT_F32;
     if (f.empty() || f == "v2") build_v2(pl);
     if (pl->v2) return;
+    if (f.empty() || f == "two") build_two_level(pl);
+    if (pl->two_level) return;
     const int tb = choose_tb(cube(pl->n), f32);
     const bool tile_ok = tb > 0 && cube(pl->n) <= 4096;
     if (f == "global" || (f != "v1" && !tile_ok)) {
@@ -584,7 +704,7 @@ void fill_info(fcct_plan_s* pl) {
     in.method = pl->radix ? FCCT_FAST : FCCT_DIRECT;
     in.precision = pl->precision;
     in.points = cube(pl->n);
-    in.executor = !pl->radix ? 0 : (pl->v2 ? 2 : (pl->global ? 3 : 1));
+    in.executor = !pl->radix ? 0 : (pl->v2 ? 2 : (pl->two_level ? 4 : (pl->global ? 3 : 1)));
     const double N = static_cast<double>(in.points);
     if (pl->radix) {
         in.levels = tree_levels(pl->n);
@@ -601,6 +721,11 @@ void fill_info(fcct_plan_s* pl) {
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->gfwd, &pl->ginv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+        for (auto* pt : {&pl->rfwd, &pl->rinv})
+            for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+        for (int c = 0; c < 8; ++c)
+            for (auto* pt : {&pl->cfwd[c], &pl->cinv[c]})
+                for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         in.table_bytes = bytes;
     } else {
         in.levels = 0;
@@ -653,6 +778,10 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
     DeviceGuard guard(pl->device);
     const bool f32 = pl->precision == FCCT_F32;
     if (pl->radix) {
+        if (pl->two_level) {
+            run_two_level(pl, inverse, in, f32 ? 1 : 0, out, f32 ? 1 : 0, batch, st);
+            return;
+        }
         if (pl->v2) {
             ck(launch_pipeline2(inverse ? pl->inv2.desc : pl->fwd2.desc, in, out, batch, st, pl->num_sms),
                "fast pipeline v2");
@@ -764,6 +893,11 @@ void run_real(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t 
     if (!in || !out) throw FcctError(ST_INVALID_ARGUMENT, "null buffer");
     DeviceGuard guard(pl->device);
     const bool f32 = pl->precision == FCCT_F32;
+    if (pl->radix && pl->two_level) {
+        const int cm = f32 ? 1 : 0, rm = f32 ? 3 : 2;
+        run_two_level(pl, inverse, in, inverse ? cm : rm, out, inverse ? rm : cm, batch, st);
+        return;
+    }
     if (pl->radix && pl->v2) {
         Pipeline2Desc d = inverse ? pl->inv2.desc : pl->fwd2.desc;
         (inverse ? d.real_out : d.real_in) = 1;

@@ -687,13 +687,16 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
                 for (int t = 0; t < TB; ++t) {
                     if (t >= nv) break;
                     tma_store_wait_read_n(TB - 1 - t);
-                    tma_load_1d(X + t * stride + ((t & 1) ? d.shift_in : 0), in + (t0 + t) * dimr, row_bytes, bar);
+                    tma_load_1d(X + t * stride + ((t & 1) ? d.shift_in : 0), in + (t0 + t) * d.row_in, row_bytes, bar);
                 }
                 const int64_t na = tile + gridDim.x;
                 if (na < ntiles) {
                     const int64_t a0 = na * TB;
                     const int nva = static_cast<int>(batch - a0 < TB ? batch - a0 : TB);
-                    prefetch_l2_bulk(in + a0 * dimr, row_bytes * nva);
+                    if (d.row_in == dimr)
+                        prefetch_l2_bulk(in + a0 * dimr, row_bytes * nva);
+                    else
+                        for (int t = 0; t < nva; ++t) prefetch_l2_bulk(in + (a0 + t) * d.row_in, row_bytes);
                 }
             }
             mbar_wait(bar, phase);
@@ -760,7 +763,7 @@ __global__ void __launch_bounds__(WARPS * 32, 512 / (WARPS * 32))
             // ragged last tile) so the next tile's per-row waits line up
             for (int t = 0; t < TB; ++t) {
                 if (t < nvalid)
-                    tma_store_1d(out + (t0 + t) * dimr, X + t * stride + ((t & 1) ? d.shift_out : 0), row_bytes);
+                    tma_store_1d(out + (t0 + t) * d.row_out, X + t * stride + ((t & 1) ? d.shift_out : 0), row_bytes);
                 tma_store_commit();
             }
         }
@@ -854,6 +857,201 @@ cudaError_t launch_real_part(const void* in_cplx, void* out_real, int64_t count,
     else
         real_part_kernel<double><<<elementwise_grid(count), 256, 0, st>>>(static_cast<const C2<double>*>(in_cplx),
                                                                           static_cast<double*>(out_real), count);
+    return cudaGetLastError();
+}
+
+// ===========================================================================
+// Two-level executor: root pass (SIMT FP64), children on pipeline2
+// ===========================================================================
+namespace {
+
+__device__ __forceinline__ double2 load_point(int mode, const void* __restrict__ src, int64_t i) {
+    if (mode == 0) return __ldg(static_cast<const double2*>(src) + i);
+    if (mode == 1) {
+        const float2 f = __ldg(static_cast<const float2*>(src) + i);
+        return make_double2(f.x, f.y);
+    }
+    if (mode == 2) return make_double2(__ldg(static_cast<const double*>(src) + i), 0.0);
+    return make_double2(__ldg(static_cast<const float*>(src) + i), 0.0);
+}
+
+__device__ __forceinline__ void store_point(int mode, void* __restrict__ dst, int64_t i, double2 v) {
+    if (mode == 0)
+        static_cast<double2*>(dst)[i] = v;
+    else if (mode == 1)
+        static_cast<float2*>(dst)[i] = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+    else if (mode == 2)
+        static_cast<double*>(dst)[i] = v.x;
+    else
+        static_cast<float*>(dst)[i] = static_cast<float>(v.x);
+}
+
+__device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+}
+
+constexpr int kRootBlk = 3;  // blocks per CTA pass: each table entry serves kRootBlk blocks
+
+// Sparse rows of one ELL group for the kRootBlk blocks held in shared memory.
+__device__ __forceinline__ void root_rows(const RootDesc& d, int g, int h, const double2* xs, double2 (&acc)[kRootBlk]) {
+    // unrolled so that several entries' table loads (L2) are in flight at once
+#pragma unroll 8
+    for (int idx = d.ell_off[g] + h; idx < d.ell_off[g + 1]; idx += d.m3) {
+        const int c = __ldg(d.col + idx);
+        const double2 v = __ldg(d.val + idx);
+#pragma unroll
+        for (int b = 0; b < kRootBlk; ++b) cfma(acc[b], v, xs[(b << d.lgN) + c]);
+    }
+}
+
+__global__ void __launch_bounds__(512, 1)
+    root_forward_kernel(const RootDesc d, const void* __restrict__ x, int in_mode, double2* __restrict__ z,
+                        int64_t batch) {
+    extern __shared__ double2 xs[];  // [kRootBlk][N]
+    __shared__ double2 Ks[64];
+    if (threadIdx.x < 64) Ks[threadIdx.x] = d.K[threadIdx.x];
+    for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * kRootBlk; b0 < batch;
+         b0 += static_cast<int64_t>(gridDim.x) * kRootBlk) {
+        const int nb = static_cast<int>(batch - b0 < kRootBlk ? batch - b0 : kRootBlk);
+        __syncthreads();
+        for (int i = threadIdx.x; i < (nb << d.lgN); i += blockDim.x) xs[i] = load_point(in_mode, x, (b0 << d.lgN) + i);
+        __syncthreads();
+        for (int h = threadIdx.x; h < d.m3; h += blockDim.x) {
+            double2 t[kRootBlk][8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                double2 acc[kRootBlk];
+#pragma unroll
+                for (int b = 0; b < kRootBlk; ++b) acc[b] = make_double2(0.0, 0.0);
+                root_rows(d, g, h, xs, acc);
+#pragma unroll
+                for (int b = 0; b < kRootBlk; ++b) t[b][g] = acc[b];
+            }
+            // K-mix: z[c m3 + h] = sum_g K[c][g] t[g]
+#pragma unroll
+            for (int b = 0; b < kRootBlk; ++b)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    if (b >= nb) break;
+                    double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) cfma(s, Ks[c * 8 + g], t[b][g]);
+                    z[((b0 + b) << d.lgN) + c * d.m3 + h] = s;
+                }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(512, 1)
+    root_inverse_kernel(const RootDesc d, const double2* __restrict__ z, void* __restrict__ y, int out_mode,
+                        int64_t batch) {
+    extern __shared__ double2 xs[];  // [kRootBlk][N]
+    __shared__ double2 Ks[64];
+    if (threadIdx.x < 64) Ks[threadIdx.x] = d.K[threadIdx.x];
+    for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * kRootBlk; b0 < batch;
+         b0 += static_cast<int64_t>(gridDim.x) * kRootBlk) {
+        const int nb = static_cast<int>(batch - b0 < kRootBlk ? batch - b0 : kRootBlk);
+        __syncthreads();
+        for (int i = threadIdx.x; i < (nb << d.lgN); i += blockDim.x) xs[i] = __ldg(z + (b0 << d.lgN) + i);
+        __syncthreads();
+        // K^{-1} unmix in place: every thread owns positions g m3 + h of its h
+        for (int h = threadIdx.x; h < d.m3; h += blockDim.x)
+#pragma unroll 1
+            for (int b = 0; b < nb; ++b) {
+                double2 u[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) u[c] = xs[(b << d.lgN) + c * d.m3 + h];
+#pragma unroll 1
+                for (int g = 0; g < 8; ++g) {  // not unrolled: the 64 K values would be hoisted into registers
+                    double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) cfma(s, Ks[g * 8 + c], u[c]);
+                    xs[(b << d.lgN) + g * d.m3 + h] = s;
+                }
+            }
+        __syncthreads();
+        // B^{-1}: natural rows j m3 + h
+        for (int h = threadIdx.x; h < d.m3; h += blockDim.x)
+#pragma unroll 1
+            for (int j = 0; j < 8; ++j) {
+                double2 acc[kRootBlk];
+#pragma unroll
+                for (int b = 0; b < kRootBlk; ++b) acc[b] = make_double2(0.0, 0.0);
+                root_rows(d, j, h, xs, acc);
+#pragma unroll
+                for (int b = 0; b < kRootBlk; ++b)
+                    if (b < nb) store_point(out_mode, y, ((b0 + b) << d.lgN) + j * d.m3 + h, acc[b]);
+            }
+    }
+}
+
+__global__ void child_to_natural_kernel(const RootDesc d, const double2* __restrict__ src, void* __restrict__ dst,
+                                        int out_mode, int64_t total) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t b = i >> d.lgN;
+        const int P = static_cast<int>(i & (d.N - 1));
+        store_point(out_mode, dst, i, __ldg(src + (b << d.lgN) + __ldg(d.pinv + P)));
+    }
+}
+
+__global__ void natural_to_child_kernel(const RootDesc d, const void* __restrict__ src, int in_mode,
+                                        double2* __restrict__ dst, int64_t total) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t b = i >> d.lgN;
+        const int q = static_cast<int>(i & (d.N - 1));
+        dst[i] = load_point(in_mode, src, (b << d.lgN) + __ldg(d.perm + q));
+    }
+}
+
+unsigned root_grid(int64_t batch, int num_sms) {
+    const int64_t passes = (batch + kRootBlk - 1) / kRootBlk;
+    return static_cast<unsigned>(std::min<int64_t>(passes, num_sms));
+}
+
+}  // namespace
+
+cudaError_t launch_root_forward(const RootDesc& d, const void* x, int in_mode, double* z, int64_t batch,
+                                cudaStream_t st, int num_sms) {
+    if (batch <= 0) return cudaSuccess;
+    const int smem = kRootBlk * d.N * static_cast<int>(sizeof(double2));
+    cudaError_t e = cudaFuncSetAttribute(root_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    root_forward_kernel<<<root_grid(batch, num_sms), 512, smem, st>>>(d, x, in_mode, reinterpret_cast<double2*>(z),
+                                                                      batch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_root_inverse(const RootDesc& d, const double* z, void* y, int out_mode, int64_t batch,
+                                cudaStream_t st, int num_sms) {
+    if (batch <= 0) return cudaSuccess;
+    const int smem = kRootBlk * d.N * static_cast<int>(sizeof(double2));
+    cudaError_t e = cudaFuncSetAttribute(root_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    root_inverse_kernel<<<root_grid(batch, num_sms), 512, smem, st>>>(d, reinterpret_cast<const double2*>(z), y,
+                                                                      out_mode, batch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_child_to_natural(const RootDesc& d, const double* src, void* dst, int out_mode, int64_t batch,
+                                    cudaStream_t st) {
+    const int64_t total = batch << d.lgN;
+    if (total <= 0) return cudaSuccess;
+    child_to_natural_kernel<<<elementwise_grid(total), 256, 0, st>>>(d, reinterpret_cast<const double2*>(src), dst,
+                                                                     out_mode, total);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_natural_to_child(const RootDesc& d, const void* src, int in_mode, double* dst, int64_t batch,
+                                    cudaStream_t st) {
+    const int64_t total = batch << d.lgN;
+    if (total <= 0) return cudaSuccess;
+    natural_to_child_kernel<<<elementwise_grid(total), 256, 0, st>>>(d, src, in_mode, reinterpret_cast<double2*>(dst),
+                                                                     total);
     return cudaGetLastError();
 }
 

@@ -75,6 +75,8 @@ struct Pipeline2Desc {
     int io_f32;        // 1: global data is complex64 (converted to/from fp64 at tile load/store)
     int real_in;       // 1: input rows are real samples (z_transform fused into the tile load)
     int real_out;      // 1: only real parts are stored (grid_from_signal fused into the tile store)
+    int64_t row_in;    // doubles between consecutive block rows of the input (2N when dense)
+    int64_t row_out;   // same for the output (the two-level executor runs children in place of a parent)
     int ring;          // 1: sparse-stage table entries stream through a per-warp cp.async ring in smem
     int shift_in;      // doubles: odd block rows of the natural input tile start this far into their row
     int shift_out;     // doubles: same for the natural output tile (spreads the leaf mix's banks)
@@ -85,6 +87,31 @@ struct Pipeline2Desc {
 
 cudaError_t launch_pipeline2(const Pipeline2Desc& d, const void* in, void* out, int64_t batch, cudaStream_t stream,
                              int num_sms);
+
+// Two-level executor (n = 16): the root level runs as its own pass, the eight
+// n = 8 children on pipeline2 (row-strided into a child-major scratch).
+// Root tables: ELL per unit h (m3 = N / 8 units); entries of output row
+// g m3 + h (forward B) or j m3 + h (inverse B^-1) at [off[g] + e * m3 + h].
+struct RootDesc {
+    int N, m3, lgN;
+    int ell_off[9];           // prefix offsets (in entries) of the 8 row groups; ell_off[8] = total
+    const int* col;           // [entries] input column (padding: 0 with value 0)
+    const double2* val;       // [entries]
+    const double2* K;         // [8][8] K (forward) or K^{-1} (inverse), row-major
+    const int* perm;          // [N] radix permutation: child-major index c m3 + j -> natural position
+    const int* pinv;          // [N] its inverse
+};
+// forward: x (natural, mode 0 c128 / 1 c64 / 2 r64 / 3 r32) -> z child-major c128
+cudaError_t launch_root_forward(const RootDesc& d, const void* x, int in_mode, double* z, int64_t batch,
+                                cudaStream_t st, int num_sms);
+// inverse: z child-major c128 -> y natural (out_mode as above)
+cudaError_t launch_root_inverse(const RootDesc& d, const double* z, void* y, int out_mode, int64_t batch,
+                                cudaStream_t st, int num_sms);
+// child-major c128 <-> natural (mode conversions on the natural side)
+cudaError_t launch_child_to_natural(const RootDesc& d, const double* src, void* dst, int out_mode, int64_t batch,
+                                    cudaStream_t st);
+cudaError_t launch_natural_to_child(const RootDesc& d, const void* src, int in_mode, double* dst, int64_t batch,
+                                    cudaStream_t st);
 
 // z_transform / grid_from_signal for executors without fused real I/O:
 // real[count] -> complex[count] (zero imaginary parts) and back (real parts).
