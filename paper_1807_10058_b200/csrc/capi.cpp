@@ -474,6 +474,8 @@ struct fcct_plan_s {
     bool two_level = false;  // n = 16: root pass + eight n = 8 child pipelines
     RootTables rfwd, rinv;
     Pipeline2Tables cfwd[8], cinv[8];
+    cudaStream_t cs[4] = {nullptr, nullptr, nullptr, nullptr};  // child pipelines run concurrently
+    cudaEvent_t cev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     bool global = false;  // global-memory multi-pass pipeline
     GlobalTables gfwd, ginv;
     std::shared_ptr<DevBuf> scratch0, scratch1;
@@ -489,6 +491,10 @@ struct fcct_plan_s {
     ~fcct_plan_s() {
         for (auto& h : hs)
             if (h) cudaStreamDestroy(h);
+        for (auto& h : cs)
+            if (h) cudaStreamDestroy(h);
+        for (auto& e : cev)
+            if (e) cudaEventDestroy(e);
         if (hev) cudaEventDestroy(hev);
     }
     // complex staging for real-I/O calls on executors without fused real I/O
@@ -560,6 +566,11 @@ void build_v2(fcct_plan_s* pl) {
 // child-major scratch, the eight n = 8 children on the DMMA pipeline (each
 // reading and writing its 512-point slice of every block), and one gather
 // applies the radix permutation. Inverse: gather, children, root pass.
+// ELL layout of the root-level rows, 8 groups g of m3 rows g m3 + h (thread h
+// handles row g m3 + h of every group). Within each warp's 32 rows the entries
+// of every step are reordered so the 8 lanes of each quarter-warp gather
+// x[col] from distinct 16-byte bank groups (col mod 8) where possible; padding
+// entries (value 0) take a free bank group too.
 void build_root_ell(const SparseLD& S, int N, RootTables& rt, RootDesc& d) {
     const int m3 = N / 8;
     std::vector<int> width(8, 0);
@@ -573,14 +584,42 @@ void build_root_ell(const SparseLD& S, int N, RootTables& rt, RootDesc& d) {
     std::vector<int32_t> col(d.ell_off[8], 0);
     std::vector<double> val(2 * static_cast<size_t>(d.ell_off[8]), 0.0);
     for (int g = 0; g < 8; ++g)
-        for (int h = 0; h < m3; ++h) {
-            const int64_t row = static_cast<int64_t>(g) * m3 + h;
-            int e = 0;
-            for (int64_t k = S.rowptr[row]; k < S.rowptr[row + 1]; ++k, ++e) {
-                const int64_t idx = d.ell_off[g] + static_cast<int64_t>(e) * m3 + h;
-                col[idx] = S.col[k];
-                val[2 * idx] = static_cast<double>(S.val[k].real());
-                val[2 * idx + 1] = static_cast<double>(S.val[k].imag());
+        for (int h0 = 0; h0 < m3; h0 += 8) {  // one quarter-warp phase: lanes h0 .. h0+7
+            const int lanes = std::min(8, m3 - h0);
+            std::vector<std::vector<int64_t>> left(lanes);  // remaining entry indices per lane
+            for (int l = 0; l < lanes; ++l) {
+                const int64_t row = static_cast<int64_t>(g) * m3 + h0 + l;
+                for (int64_t k = S.rowptr[row]; k < S.rowptr[row + 1]; ++k) left[l].push_back(k);
+            }
+            for (int e = 0; e < width[g]; ++e) {
+                unsigned used = 0;
+                std::vector<int64_t> pick(lanes, -1);
+                for (int l = 0; l < lanes; ++l) {  // distinct bank groups first
+                    for (size_t q = 0; q < left[l].size(); ++q)
+                        if (!(used & (1u << (S.col[left[l][q]] & 7)))) {
+                            pick[l] = left[l][q];
+                            left[l].erase(left[l].begin() + static_cast<std::ptrdiff_t>(q));
+                            break;
+                        }
+                    if (pick[l] >= 0) used |= 1u << (S.col[pick[l]] & 7);
+                }
+                for (int l = 0; l < lanes; ++l) {
+                    const int64_t idx = d.ell_off[g] + static_cast<int64_t>(e) * m3 + h0 + l;
+                    if (pick[l] < 0 && !left[l].empty()) {  // a conflicting entry is better than a later step
+                        pick[l] = left[l].front();
+                        left[l].erase(left[l].begin());
+                    }
+                    if (pick[l] >= 0) {
+                        col[idx] = S.col[pick[l]];
+                        val[2 * idx] = static_cast<double>(S.val[pick[l]].real());
+                        val[2 * idx + 1] = static_cast<double>(S.val[pick[l]].imag());
+                    } else {  // padding: any position with a free bank group
+                        int b = 0;
+                        while (b < 7 && (used & (1u << b))) ++b;
+                        used |= 1u << b;
+                        col[idx] = b;
+                    }
+                }
             }
         }
     auto bc = upload(col);
@@ -649,17 +688,29 @@ void run_two_level(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, v
     }
     double* s1 = static_cast<double*>(pl->scratch0->ptr);
     double* s2 = static_cast<double*>(pl->scratch1->ptr);
+    for (int k = 0; k < 4; ++k)
+        if (!pl->cs[k]) ck(cudaStreamCreateWithFlags(&pl->cs[k], cudaStreamNonBlocking), "stream");
+    for (int k = 0; k < 5; ++k)
+        if (!pl->cev[k]) ck(cudaEventCreateWithFlags(&pl->cev[k], cudaEventDisableTiming), "event");
+    // the eight child pipelines on four streams: one launch's tail overlaps the next one's start
+    auto children = [&](Pipeline2Tables* tabs) {
+        ck(cudaEventRecord(pl->cev[4], st), "event");
+        for (int k = 0; k < 4; ++k) ck(cudaStreamWaitEvent(pl->cs[k], pl->cev[4], 0), "wait");
+        for (int c = 0; c < 8; ++c)
+            ck(launch_pipeline2(tabs[c].desc, s1 + 2 * c * m3, s2 + 2 * c * m3, batch, pl->cs[c & 3], pl->num_sms),
+               "child pipeline");
+        for (int k = 0; k < 4; ++k) {
+            ck(cudaEventRecord(pl->cev[k], pl->cs[k]), "event");
+            ck(cudaStreamWaitEvent(st, pl->cev[k], 0), "wait");
+        }
+    };
     if (!inverse) {
         ck(launch_root_forward(pl->rfwd.desc, in, in_mode, s1, batch, st, pl->num_sms), "root pass");
-        for (int c = 0; c < 8; ++c)
-            ck(launch_pipeline2(pl->cfwd[c].desc, s1 + 2 * c * m3, s2 + 2 * c * m3, batch, st, pl->num_sms),
-               "child pipeline");
+        children(pl->cfwd);
         ck(launch_child_to_natural(pl->rfwd.desc, s2, out, out_mode, batch, st), "radix permutation");
     } else {
         ck(launch_natural_to_child(pl->rinv.desc, in, in_mode, s1, batch, st), "radix permutation");
-        for (int c = 0; c < 8; ++c)
-            ck(launch_pipeline2(pl->cinv[c].desc, s1 + 2 * c * m3, s2 + 2 * c * m3, batch, st, pl->num_sms),
-               "child pipeline");
+        children(pl->cinv);
         ck(launch_root_inverse(pl->rinv.desc, s2, out, out_mode, batch, st, pl->num_sms), "root pass");
     }
     ck(cudaStreamSynchronize(st), "sync");  // the plan-owned scratch serialises calls on this path

@@ -897,13 +897,22 @@ constexpr int kRootBlk = 3;  // blocks per CTA pass: each table entry serves kRo
 
 // Sparse rows of one ELL group for the kRootBlk blocks held in shared memory.
 __device__ __forceinline__ void root_rows(const RootDesc& d, int g, int h, const double2* xs, double2 (&acc)[kRootBlk]) {
-    // unrolled so that several entries' table loads (L2) are in flight at once
-#pragma unroll 8
-    for (int idx = d.ell_off[g] + h; idx < d.ell_off[g + 1]; idx += d.m3) {
-        const int c = __ldg(d.col + idx);
-        const double2 v = __ldg(d.val + idx);
+    // entries are fetched 8 at a time into registers before any is used, so
+    // eight table loads (L2) are in flight per thread
+    const int e_end = d.ell_off[g + 1];
+    for (int base = d.ell_off[g] + h; base < e_end; base += 8 * d.m3) {
+        int c[8];
+        double2 v[8];
 #pragma unroll
-        for (int b = 0; b < kRootBlk; ++b) cfma(acc[b], v, xs[(b << d.lgN) + c]);
+        for (int u = 0; u < 8; ++u) {
+            const int idx = base + u * d.m3;
+            c[u] = idx < e_end ? __ldg(d.col + idx) : 0;
+            v[u] = idx < e_end ? __ldg(d.val + idx) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int b = 0; b < kRootBlk; ++b) cfma(acc[b], v[u], xs[(b << d.lgN) + c[u]]);
     }
 }
 
@@ -912,12 +921,34 @@ __global__ void __launch_bounds__(512, 1)
                         int64_t batch) {
     extern __shared__ double2 xs[];  // [kRootBlk][N]
     __shared__ double2 Ks[64];
+    __shared__ uint64_t bar;
     if (threadIdx.x < 64) Ks[threadIdx.x] = d.K[threadIdx.x];
-    for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * kRootBlk; b0 < batch;
-         b0 += static_cast<int64_t>(gridDim.x) * kRootBlk) {
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    uint32_t phase = 0;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kRootBlk;
+    for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * kRootBlk; b0 < batch; b0 += step) {
         const int nb = static_cast<int>(batch - b0 < kRootBlk ? batch - b0 : kRootBlk);
         __syncthreads();
-        for (int i = threadIdx.x; i < (nb << d.lgN); i += blockDim.x) xs[i] = load_point(in_mode, x, (b0 << d.lgN) + i);
+        if (in_mode == 0) {  // complex128 blocks are contiguous: one bulk copy, next pass prefetched into L2
+            if (threadIdx.x == 0) {
+                const uint32_t bytes = static_cast<uint32_t>(nb) << (d.lgN + 4);
+                mbar_arrive_expect_tx(&bar, bytes);
+                tma_load_1d(xs, static_cast<const double2*>(x) + (b0 << d.lgN), bytes, &bar);
+                const int64_t nx = b0 + step;
+                if (nx < batch) {
+                    const int nn = static_cast<int>(batch - nx < kRootBlk ? batch - nx : kRootBlk);
+                    prefetch_l2_bulk(static_cast<const double2*>(x) + (nx << d.lgN), static_cast<uint32_t>(nn) << (d.lgN + 4));
+                }
+            }
+            mbar_wait(&bar, phase);
+            phase ^= 1;
+        } else {
+#pragma unroll 8
+            for (int i = threadIdx.x; i < (nb << d.lgN); i += blockDim.x) xs[i] = load_point(in_mode, x, (b0 << d.lgN) + i);
+        }
         __syncthreads();
         for (int h = threadIdx.x; h < d.m3; h += blockDim.x) {
             double2 t[kRootBlk][8];
@@ -950,12 +981,29 @@ __global__ void __launch_bounds__(512, 1)
                         int64_t batch) {
     extern __shared__ double2 xs[];  // [kRootBlk][N]
     __shared__ double2 Ks[64];
+    __shared__ uint64_t bar;
     if (threadIdx.x < 64) Ks[threadIdx.x] = d.K[threadIdx.x];
-    for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * kRootBlk; b0 < batch;
-         b0 += static_cast<int64_t>(gridDim.x) * kRootBlk) {
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    uint32_t phase = 0;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kRootBlk;
+    for (int64_t b0 = static_cast<int64_t>(blockIdx.x) * kRootBlk; b0 < batch; b0 += step) {
         const int nb = static_cast<int>(batch - b0 < kRootBlk ? batch - b0 : kRootBlk);
         __syncthreads();
-        for (int i = threadIdx.x; i < (nb << d.lgN); i += blockDim.x) xs[i] = __ldg(z + (b0 << d.lgN) + i);
+        if (threadIdx.x == 0) {
+            const uint32_t bytes = static_cast<uint32_t>(nb) << (d.lgN + 4);
+            mbar_arrive_expect_tx(&bar, bytes);
+            tma_load_1d(xs, z + (b0 << d.lgN), bytes, &bar);
+            const int64_t nx = b0 + step;
+            if (nx < batch) {
+                const int nn = static_cast<int>(batch - nx < kRootBlk ? batch - nx : kRootBlk);
+                prefetch_l2_bulk(z + (nx << d.lgN), static_cast<uint32_t>(nn) << (d.lgN + 4));
+            }
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1;
         __syncthreads();
         // K^{-1} unmix in place: every thread owns positions g m3 + h of its h
         for (int h = threadIdx.x; h < d.m3; h += blockDim.x)
