@@ -354,7 +354,6 @@ __device__ __forceinline__ void issue_tile_load(const NextLoad& nl) {
     }
 }
 
-__constant__ int d_debug_flags;  // timing experiments only (bit 0: skip sparse fragment loads)
 
 constexpr int kRing = 4;  // table entries in flight per warp (cp.async ring depth)
 
@@ -799,13 +798,6 @@ cudaError_t launch_pipeline2_t(const Pipeline2Desc& d, const void* in, void* out
 cudaError_t launch_pipeline2(const Pipeline2Desc& d, const void* in, void* out, int64_t batch, cudaStream_t st,
                              int num_sms) {
     if (batch <= 0) return cudaSuccess;
-    static int flags_set = -1;
-    const char* dbg = std::getenv("FCCT_DEBUG_FLAGS");
-    const int flags = dbg ? std::atoi(dbg) : 0;
-    if (flags != flags_set) {
-        cudaMemcpyToSymbol(d_debug_flags, &flags, sizeof(int));
-        flags_set = flags;
-    }
     if (d.tb == 16 && d.warps == 16) return launch_pipeline2_t<16, 16>(d, in, out, batch, st, num_sms);
     if (d.tb == 8 && d.warps == 8) return launch_pipeline2_t<8, 8>(d, in, out, batch, st, num_sms);
     return cudaErrorInvalidValue;
