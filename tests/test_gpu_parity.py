@@ -438,3 +438,40 @@ def test_real_io_fused_matches_complex_path(cuda, oracle_mod, n, method, precisi
         back = inverse_apply(plan, spec, real_output=True) if method == "fast" else \
             SignalTensor(n, plan._run(spec.values, True, real_out=True))
         assert np.abs(grid_from_signal(back).values - g.values).max() <= 1e-12
+
+
+@pytest.mark.parametrize("p", [SkewParams(0.21, 0.055, 0.4), SkewParams(0.37, 0.61, 0.085)])
+def test_n16_two_level_noncanonical(cuda, oracle_mod, p):
+    """n = 16 on the two-level executor (root pass + eight n = 8 DMMA child
+    pipelines, fcct_plan_info_t.executor == 4) for non-canonical offsets,
+    against the FFT / orbit-route oracle."""
+    n = 16
+    plan = build_plan(n, p)
+    assert plan.info.executor == 4
+    route = oracle_mod.OrbitRoute(n, tup(p))
+    x = rand_batch(n, 7, seed=31)  # ragged: 7 blocks, 3 per root-pass CTA pass
+    y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values.cpu().numpy()
+    # The radix factorization itself has an fp64 floor that grows with the
+    # conditioning of the offsets: 1.0e-12 / 2.6e-12 for these two sets at
+    # n = 16 (4e-14 canonical), bit-identical on every executor (v1 tile
+    # interpreter, global multi-pass, two-level; tools/n16_err.py). The
+    # reference's LU-derived plan is at 3-5e-11 already for canonical n = 16.
+    assert rel(y, route.forward(x)) <= 5e-12
+    back = inverse_apply(plan, Spectrum(n, p, torch.from_numpy(y).to(cuda))).data.cpu().numpy()
+    assert rel(back, x) <= 2e-11  # measured 5.1e-12 (same floor; the reference's bar is 1e-8)
+
+
+def test_n16_two_level_f32_and_host(cuda, oracle_mod):
+    n = 16
+    plan = build_plan(n, CANON, precision="f32")
+    assert plan.info.executor == 4
+    route = oracle_mod.OrbitRoute(n, tup(CANON))
+    x = rand_batch(n, 5, seed=32)
+    y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(torch.complex64).to(cuda))).values
+    assert rel(y.cpu().numpy(), route.forward(x)) <= F32_TOL
+    back = inverse_apply(plan, Spectrum(n, CANON, y)).data
+    assert rel(back.cpu().numpy(), x) <= F32_TOL
+    # host buffers through the chunked two-stream path: bitwise the device result
+    p64 = build_plan(n, CANON)
+    xd = torch.from_numpy(x).to(cuda)
+    assert torch.equal(p64.apply_values(xd).cpu(), p64.apply_values(xd.cpu()))
