@@ -99,12 +99,36 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(smax), "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def run_cpu_baseline(n: int, blocks: int, threads: int, method: str = "fast") -> dict:
+def profiled_traffic(cfg_name: str, f32: bool, executor: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one forward pipeline2
+    launch from the committed `ncu --set full` capture (profiles/
+    r01_pipeline2_raw.csv, c2 fp64: tools/prof_run.py, 65,536 blocks), or None
+    when the run is not that configuration."""
+    if cfg_name != "c2" or f32 or executor != 2:
+        return None
+    path = Path(__file__).resolve().parent / "profiles" / "r01_pipeline2_raw.csv"
+    try:
+        import csv
+
+        rows = list(csv.reader(open(path)))
+        hdr, units, vals = rows[0], rows[1], rows[2]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(name)
+            tot += float(vals[i]) * scale[units[i]]
+        return tot
+    except (OSError, ValueError, KeyError, IndexError):
+        return None
+
+
+def run_cpu_baseline(n: int, blocks: int, threads: int, method: str = "fast", min_seconds: float = 0.0) -> dict:
     from oracle import oracle  # CPU baseline / reference arm only
 
     oracle.build()
     out = subprocess.run(
-        [str(oracle.CPU_BASELINE), "--n", str(n), "--blocks", str(blocks), "--threads", str(threads), "--method", method],
+        [str(oracle.CPU_BASELINE), "--n", str(n), "--blocks", str(blocks), "--threads", str(threads), "--method", method,
+         "--min-seconds", str(min_seconds)],
         check=True, capture_output=True, text=True,
     )
     return json.loads(out.stdout.strip().splitlines()[-1])
@@ -401,7 +425,7 @@ def b200_arm(args):
         "peak": peak_tf,
         "unit": "TFLOP/s",
         "frac": achieved_tf / peak_tf,
-        "traffic": args.traffic,
+        "traffic": args.traffic if args.traffic is not None else profiled_traffic(args.config, f32, info.executor),
         "kernel": {0: "gemm_f64_kernel / gemm_f32_kernel (direct)", 1: "pipeline_kernel (tile interpreter)",
                    2: "pipeline2_kernel (FP64 tensor pipe)", 3: "gstage_* kernels (global multi-pass)",
                    4: "root pass + 8 x pipeline2_kernel (two-level, FP64 tensor pipe)"}[info.executor],
@@ -420,13 +444,14 @@ def b200_arm(args):
     if not args.no_cpu and world >= 1:
         threads = os.cpu_count() or 1
         sample = min(args.cpu_sample, max(1, 2**24 // N))
-        r = run_cpu_baseline(n, sample, threads, args.method) if n <= 16 else None
+        r = run_cpu_baseline(n, sample, threads, args.method, args.cpu_seconds) if n <= 16 else None
         cpu = None if r is None else {
             "value": 2 * sample / (r["forward_s"] + r["inverse_s"]),
             "unit": "transforms/s",
             "cores": threads,
             "kind": "port",
-            "sample": f"{sample} blocks of n={n}, forward then inverse, {args.method} path, reference-faithful C++ restatement (oracle/cpu_baseline.cpp)",
+            "sample": f"{sample} blocks of n={n}, forward then inverse, {args.method} path, repeated {r.get('reps', 1)}x "
+                      f"(>= {args.cpu_seconds:g} s of CPU work), reference-faithful C++ restatement (oracle/cpu_baseline.cpp)",
         }
     line = {
         "metric": METRIC,
@@ -479,6 +504,7 @@ def main():
     ap.add_argument("--method", default="fast", choices=["fast", "direct"])
     ap.add_argument("--precision", default=None, choices=["f64", "f32"])
     ap.add_argument("--cpu-sample", type=int, default=65536)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="minimum CPU work of the cpu_baseline leg")
     ap.add_argument("--e2e-blocks", type=int, default=65536)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")

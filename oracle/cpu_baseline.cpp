@@ -41,11 +41,13 @@ int main(int argc, char** argv) {
     int64_t blocks = 4096;
     int threads = static_cast<int>(std::thread::hardware_concurrency());
     const char* method = "fast";
+    double min_seconds = 0.0;  // repeat the timed passes until this much CPU time has elapsed
     for (int i = 1; i < argc; ++i) {
         if (!std::strcmp(argv[i], "--n") && i + 1 < argc) n = std::atoi(argv[++i]);
         else if (!std::strcmp(argv[i], "--blocks") && i + 1 < argc) blocks = std::atoll(argv[++i]);
         else if (!std::strcmp(argv[i], "--threads") && i + 1 < argc) threads = std::atoi(argv[++i]);
         else if (!std::strcmp(argv[i], "--method") && i + 1 < argc) method = argv[++i];
+        else if (!std::strcmp(argv[i], "--min-seconds") && i + 1 < argc) min_seconds = std::atof(argv[++i]);
     }
     const Params p{0.125, 0.0, 0.375};
     const int64_t n3 = static_cast<int64_t>(n) * n * n;
@@ -86,20 +88,27 @@ int main(int argc, char** argv) {
     };
     // warm-up
     parallel_for(std::min<int64_t>(blocks, threads), threads, [&](int64_t b) { fwd(b); inv(b); });
-    auto ta = std::chrono::steady_clock::now();
-    parallel_for(blocks, threads, fwd);
-    auto tb = std::chrono::steady_clock::now();
-    parallel_for(blocks, threads, inv);
-    auto tc = std::chrono::steady_clock::now();
+    double fs = 0.0, is = 0.0;
+    int reps = 0;
+    do {
+        const auto ta = std::chrono::steady_clock::now();
+        parallel_for(blocks, threads, fwd);
+        const auto tb = std::chrono::steady_clock::now();
+        parallel_for(blocks, threads, inv);
+        const auto tc = std::chrono::steady_clock::now();
+        fs += std::chrono::duration<double>(tb - ta).count();
+        is += std::chrono::duration<double>(tc - tb).count();
+        ++reps;
+    } while (fs + is < min_seconds);
+    fs /= reps;
+    is /= reps;
     double err = 0, scale = 0;
     for (int64_t i = 0; i < blocks * n3; ++i) {
         err = std::max(err, std::abs(z[i] - x[i]));
         scale = std::max(scale, std::abs(x[i]));
     }
-    const double fs = std::chrono::duration<double>(tb - ta).count();
-    const double is = std::chrono::duration<double>(tc - tb).count();
     std::printf("{\"n\": %d, \"method\": \"%s\", \"blocks\": %ld, \"threads\": %d, \"plan_s\": %.6g, "
-                "\"forward_s\": %.6g, \"inverse_s\": %.6g, \"roundtrip_rel_err\": %.3g}\n",
-                n, method, static_cast<long>(blocks), threads, plan_s, fs, is, err / scale);
+                "\"forward_s\": %.6g, \"inverse_s\": %.6g, \"reps\": %d, \"roundtrip_rel_err\": %.3g}\n",
+                n, method, static_cast<long>(blocks), threads, plan_s, fs, is, reps, err / scale);
     return 0;
 }
