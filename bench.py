@@ -136,6 +136,7 @@ def run_cpu_baseline(n: int, blocks: int, threads: int, method: str = "fast", mi
 
 CONFIGS = {
     # BASELINE.json configs restated on the reference's n^3 index set
+    "c1": dict(n=4, blocks=1, scaling="weak", desc="single FCC-DCT n=4 (64 points), i.i.d. U[-1,1] re/im (latency config)"),
     "c2": dict(n=8, blocks=65536, scaling="weak", desc="batched FCC-DCT n=8, 65,536 blocks per GPU, i.i.d. U[-1,1] re/im"),
     "c3": dict(n=16, blocks=16384, scaling="weak",
                desc="batched FCC-DCT n=16, 16,384 blocks per GPU, 8 seeded Gaussian blobs (sigma U[0.05,0.3] x extent) + N(0,0.01) noise at the FCC node coordinates"),
@@ -314,16 +315,26 @@ def b200_arm(args):
 
     # seeded synthetic input, resident in HBM before the timed region
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    # real fields (c3, c5) enter and leave as real samples: z_transform / grid_from_signal
+    # fused into the device pipelines, as the reference CLI uses them (fcct.cpp:95-129)
+    real_io = args.real_io if args.real_io is not None else args.config in ("c3", "c5")
     if args.config == "c3":
-        x = gaussian_blobs(n, blocks, g, dev, rdt).to(cdt)
+        x = gaussian_blobs(n, blocks, g, dev, rdt)
     elif args.config == "c5":
         side = round(total ** (1.0 / 3.0))
-        x = perlin_volume(n, b0, b1, side, 5, dev, rdt).to(cdt)
+        x = perlin_volume(n, b0, b1, side, 5, dev, rdt)
     else:
         x = torch.complex(torch.rand((blocks, N), generator=g, device=dev, dtype=rdt) * 2 - 1,
                           torch.rand((blocks, N), generator=g, device=dev, dtype=rdt) * 2 - 1).to(cdt)
-    y = torch.empty_like(x)
+    if not x.is_complex() and not real_io:
+        x = x.to(cdt)
+    if x.is_complex() and real_io:
+        x = x.real.contiguous()
+    y = torch.empty((blocks, N), dtype=cdt, device=dev)
     z = torch.empty_like(x)
+    fwd_fn = "fcct_forward_real" if real_io else "fcct_forward"
+    inv_fn = "fcct_inverse_real" if real_io else "fcct_inverse"
+    in_esize = esize // 2 if real_io else esize
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
     from paper_1807_10058_b200 import _capi
@@ -334,10 +345,10 @@ def b200_arm(args):
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        _raise(L.fcct_forward(plan._h, x.data_ptr(), y.data_ptr(), blocks, sh))
+        _raise(getattr(L, fwd_fn)(plan._h, x.data_ptr(), y.data_ptr(), blocks, sh))
         if ev is not None:
             ev[1].record(stream)
-        _raise(L.fcct_inverse(plan._h, y.data_ptr(), z.data_ptr(), blocks, sh))
+        _raise(getattr(L, inv_fn)(plan._h, y.data_ptr(), z.data_ptr(), blocks, sh))
         if ev is not None:
             ev[2].record(stream)
 
@@ -374,19 +385,21 @@ def b200_arm(args):
     if not args.no_e2e:
         eb = max(1, min(blocks, args.e2e_blocks))
         xh = x[:eb].cpu().pin_memory()
-        yh = torch.empty_like(xh).pin_memory()
+        yh = torch.empty((eb, N), dtype=cdt).pin_memory()
         zh = torch.empty_like(xh).pin_memory()
+        fwd_host = getattr(L, fwd_fn + "_host")
+        inv_host = getattr(L, inv_fn + "_host")
         for _ in range(2):
-            _raise(L.fcct_forward_host(plan._h, xh.data_ptr(), yh.data_ptr(), eb, sh))
-            _raise(L.fcct_inverse_host(plan._h, yh.data_ptr(), zh.data_ptr(), eb, sh))
+            _raise(fwd_host(plan._h, xh.data_ptr(), yh.data_ptr(), eb, sh))
+            _raise(inv_host(plan._h, yh.data_ptr(), zh.data_ptr(), eb, sh))
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(dev)
         e0.record(stream)
         for _ in range(args.e2e_steps):
-            _raise(L.fcct_forward_host(plan._h, xh.data_ptr(), yh.data_ptr(), eb, sh))
-            _raise(L.fcct_inverse_host(plan._h, yh.data_ptr(), zh.data_ptr(), eb, sh))
+            _raise(fwd_host(plan._h, xh.data_ptr(), yh.data_ptr(), eb, sh))
+            _raise(inv_host(plan._h, yh.data_ptr(), zh.data_ptr(), eb, sh))
         e1.record(stream)
         torch.cuda.synchronize(dev)
         ems = e0.elapsed_time(e1)
@@ -397,8 +410,8 @@ def b200_arm(args):
         e2e = {
             "value": 2.0 * eb * world * args.e2e_steps / (ems / 1e3),
             "unit": "transforms/s",
-            "h2d_bytes_per_step": 2 * eb * N * esize,
-            "d2h_bytes_per_step": 2 * eb * N * esize,
+            "h2d_bytes_per_step": eb * N * (in_esize + esize),
+            "d2h_bytes_per_step": eb * N * (esize + in_esize),
             "blocks_per_step": eb,
         }
 
@@ -409,7 +422,7 @@ def b200_arm(args):
 
     # roofline of the dominant kernel (the forward pipeline launch)
     flops_fwd = info.flops_forward * blocks
-    bytes_fwd = 2.0 * N * esize * blocks
+    bytes_fwd = float(N * (in_esize + esize) * blocks)
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6488.0)
     # the roofline of the pipe that executes the plan: the FP64 tensor pipe for
@@ -471,6 +484,8 @@ def b200_arm(args):
             "blocks_total": total,
             "points_per_block": N,
             "params": "canonical (1/8, 0, 3/8)",
+            "io": ("real samples in and out (z_transform / grid_from_signal fused into the device pipeline)"
+                   if real_io else "complex in and out"),
             "input": cfg["desc"] + " (seeded, generated on device)",
             "l2": (f"inputs larger than L2 ({blocks * N * esize / 2**20:.0f} MiB per array vs 126 MB L2)"
                    if blocks * N * esize > 126e6 else
@@ -505,6 +520,7 @@ def main():
     ap.add_argument("--precision", default=None, choices=["f64", "f32"])
     ap.add_argument("--cpu-sample", type=int, default=65536)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="minimum CPU work of the cpu_baseline leg")
+    ap.add_argument("--real-io", type=int, default=None, help="1/0: real samples in and out (default: c3 and c5)")
     ap.add_argument("--e2e-blocks", type=int, default=65536)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")

@@ -9,11 +9,55 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "device.cuh"
 #include "kernels.hpp"
 
 namespace fcct {
+
+namespace {
+// Per (device, kernel, dynamic smem) cache of the smem attribute and the
+// occupancy query: both are host round trips that would otherwise cost
+// microseconds on every launch (the latency of single-transform calls).
+cudaError_t prepare_launch(const void* kern, int threads, int smem, int* per_sm) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int, int>, int> cache;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const auto key = std::make_tuple(dev, kern, threads, smem);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        const auto it = cache.find(key);
+        if (it != cache.end()) {
+            if (per_sm) *per_sm = it->second;
+            return cudaSuccess;
+        }
+    }
+    // the attribute is raised to the device maximum once per kernel, so any
+    // cached smem size stays launchable whatever was prepared last
+    int max_optin = 0;
+    e = cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa{};
+    e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    const int dyn_max = max_optin - static_cast<int>(fa.sharedSizeBytes);
+    if (smem > dyn_max) return cudaErrorInvalidConfiguration;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    cache[key] = occ;
+    if (per_sm) *per_sm = occ;
+    return cudaSuccess;
+}
+}  // namespace
 
 using namespace dev;
 
@@ -182,10 +226,8 @@ cudaError_t launch_pipeline_t(const PipelineDesc& d, const void* in, void* out, 
                               int num_sms) {
     const int smem = 128 + TB * (d.N + (sizeof(C2<R>) == 8 ? 2 : 1)) * static_cast<int>(sizeof(C2<R>));
     auto kern = pipeline_kernel<R, TB>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+    cudaError_t e = prepare_launch(reinterpret_cast<const void*>(kern), kThreads, smem, &per_sm);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (batch + TB - 1) / TB;
@@ -780,17 +822,12 @@ cudaError_t launch_pipeline2_t(const Pipeline2Desc& d, const void* in, void* out
     const int smem = 128 + TB * d.stride * static_cast<int>(sizeof(double)) + d.arena_bytes +
                      (d.ring ? WARPS * kRing * 32 * static_cast<int>(sizeof(double2)) : 0);
     auto kern = pipeline2_kernel<TB, WARPS>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem);
+    cudaError_t e = prepare_launch(reinterpret_cast<const void*>(kern), WARPS * 32, smem, &per_sm);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int64_t ntiles = (batch + TB - 1) / TB;
     const int64_t grid = std::min<int64_t>(ntiles, static_cast<int64_t>(per_sm) * num_sms);
-    if (std::getenv("FCCT_DEBUG_LAUNCH"))
-        std::fprintf(stderr, "pipeline2<%d,%d>: smem %d B (arena %d), %d CTA/SM, grid %lld\n", TB, WARPS, smem,
-                     d.arena_bytes, per_sm, static_cast<long long>(grid));
     kern<<<static_cast<unsigned>(grid), WARPS * 32, smem, st>>>(d, in, out, batch);
     return cudaGetLastError();
 }
@@ -1059,7 +1096,7 @@ cudaError_t launch_root_forward(const RootDesc& d, const void* x, int in_mode, d
                                 cudaStream_t st, int num_sms) {
     if (batch <= 0) return cudaSuccess;
     const int smem = kRootBlk * d.N * static_cast<int>(sizeof(double2));
-    cudaError_t e = cudaFuncSetAttribute(root_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = prepare_launch(reinterpret_cast<const void*>(root_forward_kernel), 512, smem, nullptr);
     if (e != cudaSuccess) return e;
     root_forward_kernel<<<root_grid(batch, num_sms), 512, smem, st>>>(d, x, in_mode, reinterpret_cast<double2*>(z),
                                                                       batch);
@@ -1070,7 +1107,7 @@ cudaError_t launch_root_inverse(const RootDesc& d, const double* z, void* y, int
                                 cudaStream_t st, int num_sms) {
     if (batch <= 0) return cudaSuccess;
     const int smem = kRootBlk * d.N * static_cast<int>(sizeof(double2));
-    cudaError_t e = cudaFuncSetAttribute(root_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = prepare_launch(reinterpret_cast<const void*>(root_inverse_kernel), 512, smem, nullptr);
     if (e != cudaSuccess) return e;
     root_inverse_kernel<<<root_grid(batch, num_sms), 512, smem, st>>>(d, reinterpret_cast<const double2*>(z), y,
                                                                       out_mode, batch);
@@ -1345,7 +1382,7 @@ cudaError_t launch_gemm_f64(const double* A, const double* Wt, double* C, int64_
                             cudaStream_t st) {
     if (M <= 0) return cudaSuccess;
     const int smem = 2 * (GBM + GBN) * GLD * static_cast<int>(sizeof(double));
-    cudaError_t e = cudaFuncSetAttribute(gemm_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = prepare_launch(reinterpret_cast<const void*>(gemm_f64_kernel), 256, smem, nullptr);
     if (e != cudaSuccess) return e;
     dim3 grid((Nn + GBN - 1) / GBN, static_cast<unsigned>((M + GBM - 1) / GBM));
     gemm_f64_kernel<<<grid, 256, smem, st>>>(A, Wt, C, M, Nn, K);
