@@ -413,6 +413,59 @@ struct Sparse {
     int64_t nnz() const { return static_cast<int64_t>(val.size()); }
 };
 
+// Explicit inverse of a sparse matrix that is block diagonal up to a row and
+// column permutation: every connected component is inverted densely (LU with
+// partial pivoting); entries below 1e-12 are pruned.
+Sparse inverse_by_blocks(const Sparse& B) {
+    const int64_t n = B.dim;
+    std::vector<int64_t> par(2 * n);
+    for (int64_t i = 0; i < 2 * n; ++i) par[i] = i;
+    auto find = [&](int64_t a) {
+        while (par[a] != a) a = par[a] = par[par[a]];
+        return a;
+    };
+    for (int64_t c = 0; c < n; ++c)
+        for (int64_t k = B.colptr[c]; k < B.colptr[c + 1]; ++k) par[find(B.rowidx[k])] = find(n + c);
+    std::map<int64_t, std::pair<std::vector<int64_t>, std::vector<int64_t>>> comps;  // rows, cols
+    for (int64_t i = 0; i < 2 * n; ++i) (i < n ? comps[find(i)].first : comps[find(i)].second).push_back(i < n ? i : i - n);
+    // B^{-1} maps rows of B to its columns: entry (col_j, row_i) of the inverse block
+    std::vector<std::vector<std::pair<int32_t, Complex>>> cols(n);  // columns of B^{-1}
+    for (const auto& [key, rc] : comps) {
+        const auto& R = rc.first;
+        const auto& C = rc.second;
+        if (R.size() != C.size()) throw OracleError(ILL_CONDITIONED, "basis-change factor is not invertible");
+        const int64_t d = static_cast<int64_t>(R.size());
+        if (d == 0) continue;
+        std::map<int64_t, int64_t> rpos;
+        for (int64_t i = 0; i < d; ++i) rpos[R[i]] = i;
+        std::vector<Complex> a(static_cast<size_t>(d * d), Complex{0, 0});  // column-major block of B
+        for (int64_t j = 0; j < d; ++j)
+            for (int64_t k = B.colptr[C[j]]; k < B.colptr[C[j] + 1]; ++k) a[rpos[B.rowidx[k]] + j * d] = B.val[k];
+        DenseLU<Complex> lu(a.data(), d);
+        if (lu.singular) throw OracleError(ILL_CONDITIONED, "basis-change factor is not invertible");
+        std::vector<Complex> e(static_cast<size_t>(d));
+        for (int64_t i = 0; i < d; ++i) {  // column R[i] of B^{-1}: solve B_blk z = e_i
+            std::fill(e.begin(), e.end(), Complex{0, 0});
+            e[i] = 1.0;
+            lu.solve_inplace(e.data());
+            for (int64_t j = 0; j < d; ++j)
+                if (std::abs(e[j]) >= 1e-12) cols[R[i]].emplace_back(static_cast<int32_t>(C[j]), e[j]);
+        }
+    }
+    Sparse inv;
+    inv.dim = n;
+    inv.colptr.assign(n + 1, 0);
+    for (int64_t c = 0; c < n; ++c) {
+        std::sort(cols[c].begin(), cols[c].end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        for (const auto& [r, v] : cols[c]) {
+            inv.rowidx.push_back(r);
+            inv.val.push_back(v);
+        }
+        inv.colptr[c + 1] = inv.nnz();
+    }
+    return inv;
+}
+
 // derive_basis, src/transform.cpp:202-310: solve (K (x) I)(blockdiag child) z
 // = P^T D column by column in 256-column batches, prune |v| < 1e-12, verify
 // the reassembled product for n <= 8.
@@ -536,7 +589,13 @@ std::shared_ptr<const Plan> make_plan(int n, const Params& p) {  // PlanBuilder:
         klu.solve_inplace(e.data());
         for (int i = 0; i < 8; ++i) plan->kernel_inv[i + j * 8] = e[i];
     }
-    if (n3 <= 4096) {
+    if (n3 > 512 && n3 <= 4096) {
+        // SparseLU (transform.cpp:322-324,375-378) factors B along its sparse
+        // structure; B is block diagonal up to a permutation (blocks <= 48 x 48
+        // for the canonical offsets), so the same work is done here by
+        // inverting each connected block with a dense partial-pivot LU.
+        plan->basis_inv = inverse_by_blocks(plan->basis);
+    } else if (n3 <= 512) {
         std::vector<Complex> bd(static_cast<size_t>(n3 * n3), Complex{0, 0});
         for (int64_t c = 0; c < n3; ++c)
             for (int64_t k = plan->basis.colptr[c]; k < plan->basis.colptr[c + 1]; ++k)
@@ -544,7 +603,7 @@ std::shared_ptr<const Plan> make_plan(int n, const Params& p) {  // PlanBuilder:
         plan->basis_lu = DenseLU<Complex>(bd.data(), n3);
         if (plan->basis_lu.singular)
             throw OracleError(ILL_CONDITIONED, "basis-change factor is not invertible");
-        if (n3 <= 512) {
+        {
             Sparse& bi = plan->basis_inv;
             bi.dim = n3;
             bi.colptr.assign(n3 + 1, 0);
@@ -601,7 +660,8 @@ std::vector<Complex> Plan::solve_values(const std::vector<Complex>& q) const {
         dense_lu.solve_inplace(x.data());
         return x;
     }
-    if (basis_lu.dim == 0) throw OracleError(INVALID_ARGUMENT, "oracle fast solve limited to n <= 16");
+    if (basis_lu.dim == 0 && basis_inv.dim != n3)
+        throw OracleError(INVALID_ARGUMENT, "oracle fast solve limited to n <= 16");
     const int64_t m3 = n3 / 8;
     std::vector<Complex> y(n3);
     for (int64_t idx = 0; idx < n3; ++idx) y[idx] = q[perm[idx]];
