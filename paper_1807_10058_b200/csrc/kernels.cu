@@ -975,6 +975,15 @@ __global__ void __launch_bounds__(512, 1)
             mbar_wait(&bar, phase);
             phase ^= 1;
         } else {
+            if (threadIdx.x == 0) {  // the next pass's samples into L2
+                const int64_t nx = b0 + step;
+                const int esz = in_mode == 1 ? 8 : (in_mode == 2 ? 8 : 4);
+                if (nx < batch) {
+                    const int nn = static_cast<int>(batch - nx < kRootBlk ? batch - nx : kRootBlk);
+                    prefetch_l2_bulk(static_cast<const char*>(x) + (nx << d.lgN) * esz,
+                                     static_cast<uint32_t>(nn) * (static_cast<uint32_t>(esz) << d.lgN));
+                }
+            }
 #pragma unroll 8
             for (int i = threadIdx.x; i < (nb << d.lgN); i += blockDim.x) xs[i] = load_point(in_mode, x, (b0 << d.lgN) + i);
         }
