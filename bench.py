@@ -422,7 +422,12 @@ def b200_arm(args):
 
     # roofline of the dominant kernel (the forward pipeline launch)
     flops_fwd = info.flops_forward * blocks
-    bytes_fwd = float(N * (in_esize + esize) * blocks)
+    # algorithmic bytes of one forward launch: the data once in and once out, plus
+    # the plan tables streamed once (about half of table_bytes, which counts both
+    # directions) — negligible for batched configs, dominant for a single n = 64
+    data_bytes = float(N * (in_esize + esize) * blocks)
+    table_bytes_fwd = 0.5 * float(info.table_bytes)
+    bytes_fwd = data_bytes + table_bytes_fwd
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6488.0)
     # the roofline of the pipe that executes the plan: the FP64 tensor pipe for
@@ -432,18 +437,21 @@ def b200_arm(args):
     achieved_tf = flops_fwd / (fwd_ms / 1e3) / 1e12
     achieved_gbs = bytes_fwd / (fwd_ms / 1e3) / 1e9
     t_star = max(bytes_fwd / (hbm * 1e9), flops_fwd / (peak_tf * 1e12))
+    hbm_bound = bytes_fwd / (hbm * 1e9) > flops_fwd / (peak_tf * 1e12)
     roof = {
-        "bound": "tensor",
-        "achieved": achieved_tf,
-        "peak": peak_tf,
-        "unit": "TFLOP/s",
-        "frac": achieved_tf / peak_tf,
+        "bound": "hbm" if hbm_bound else "tensor",
+        "achieved": achieved_gbs if hbm_bound else achieved_tf,
+        "peak": hbm if hbm_bound else peak_tf,
+        "unit": "GB/s" if hbm_bound else "TFLOP/s",
+        "frac": (achieved_gbs / hbm) if hbm_bound else (achieved_tf / peak_tf),
         "traffic": args.traffic if args.traffic is not None else profiled_traffic(args.config, f32, info.executor),
         "kernel": {0: "gemm_f64_kernel / gemm_f32_kernel (direct)", 1: "pipeline_kernel (tile interpreter)",
                    2: "pipeline2_kernel (FP64 tensor pipe)", 3: "gstage_* kernels (global multi-pass)",
                    4: "root pass + 8 x pipeline2_kernel (two-level, FP64 tensor pipe)"}[info.executor],
         "algorithmic_flops_per_launch": flops_fwd,
         "algorithmic_bytes_per_launch": bytes_fwd,
+        "table_bytes_per_launch": table_bytes_fwd,
+        "achieved_tflops": achieved_tf,
         "achieved_gbs": achieved_gbs,
         "hbm_peak_gbs": hbm,
         "t_star_over_t": t_star / (fwd_ms / 1e3),
