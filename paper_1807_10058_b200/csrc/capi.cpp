@@ -363,29 +363,47 @@ struct GlobalTables {
 template <typename R>
 void add_global_sparse(GlobalTables& gt, const Rows& rows, const std::vector<int32_t>* gather,
                        const std::vector<int32_t>* scatter) {
-    std::vector<int64_t> rowptr(rows.N + 1, 0);
-    std::vector<int32_t> col;
-    std::vector<R> coef;
-    for (int64_t r = 0; r < rows.N; ++r) {
-        for (const auto& e : rows.r[r]) {
-            col.push_back(gather ? (*gather)[e.first] : e.first);
-            push_coef(coef, e.second);
+    // sliced ELL: rows sorted by length (the output position map absorbs the
+    // order), slices of 32 rows padded to their longest row, entries stored
+    // [slice][e][lane] so every warp-wide table load is one contiguous 512 B
+    // (complex128) run
+    const int64_t N = rows.N;
+    std::vector<int32_t> order(N);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return rows.r[a].size() > rows.r[b].size(); });
+    const int64_t nslices = (N + 31) / 32;
+    std::vector<int64_t> slice_off(nslices + 1, 0);
+    for (int64_t sl = 0; sl < nslices; ++sl) {
+        size_t w = 0;
+        for (int64_t l = 0; l < 32 && sl * 32 + l < N; ++l) w = std::max(w, rows.r[order[sl * 32 + l]].size());
+        slice_off[sl + 1] = slice_off[sl] + static_cast<int64_t>(w) * 32;
+    }
+    std::vector<int32_t> col(slice_off[nslices], 0);
+    std::vector<R> coef(2 * slice_off[nslices], R(0));
+    std::vector<int32_t> out_row(N);
+    for (int64_t i = 0; i < N; ++i) {
+        const int64_t sl = i / 32, lane = i % 32;
+        const auto& row = rows.r[order[i]];
+        for (size_t e = 0; e < row.size(); ++e) {
+            const int64_t idx = slice_off[sl] + static_cast<int64_t>(e) * 32 + lane;
+            col[idx] = gather ? (*gather)[row[e].first] : row[e].first;
+            std::vector<R> c;
+            push_coef(c, row[e].second);
+            coef[2 * idx] = c[0];
+            coef[2 * idx + 1] = c[1];
         }
-        rowptr[r + 1] = static_cast<int64_t>(col.size());
+        out_row[i] = scatter ? (*scatter)[order[i]] : order[i];
     }
     GStage& st = gt.desc.st[gt.desc.nstages++];
     st = GStage{};
     st.kind = 0;
-    auto b1 = upload(rowptr), b2 = upload(col), b3 = upload(coef);
+    auto b1 = upload(slice_off), b2 = upload(col), b3 = upload(coef), b4 = upload(out_row);
     st.rowptr = static_cast<const int64_t*>(b1->ptr);
     st.col = static_cast<const int*>(b2->ptr);
     st.coef = b3->ptr;
-    gt.bufs.insert(gt.bufs.end(), {b1, b2, b3});
-    if (scatter) {
-        auto b4 = upload(*scatter);
-        st.out_row = static_cast<const int*>(b4->ptr);
-        gt.bufs.push_back(b4);
-    }
+    st.out_row = static_cast<const int*>(b4->ptr);
+    gt.bufs.insert(gt.bufs.end(), {b1, b2, b3, b4});
 }
 
 template <typename R>

@@ -1156,9 +1156,11 @@ __global__ void gstage_sparse_kernel(const GStage st, int N, const C2<R>* __rest
     C2<R> acc;
     acc.x = 0;
     acc.y = 0;
-    const int64_t e1 = __ldg(st.rowptr + r + 1);
-    for (int64_t e = __ldg(st.rowptr + r); e < e1; ++e) cmac(acc, coef[e], xb[__ldg(st.col + e)]);
-    const int64_t o = st.out_row ? __ldg(st.out_row + r) : r;
+    const int64_t sl = r >> 5;
+    const int64_t e0 = __ldg(st.rowptr + sl) + (r & 31), e1 = __ldg(st.rowptr + sl + 1);
+#pragma unroll 4
+    for (int64_t e = e0; e < e1; e += 32) cmac(acc, coef[e], xb[__ldg(st.col + e)]);
+    const int64_t o = __ldg(st.out_row + r);
     y[b * N + o] = acc;
 }
 

@@ -121,8 +121,8 @@ cudaError_t launch_real_part(const void* in_cplx, void* out_real, int64_t count,
 // Global-memory multi-pass pipeline (any full radix tree; used when a block's
 // state does not fit one CTA tile, e.g. n = 32, 64): one launch per stage.
 struct GStage {
-    int kind;              // 0 CSR sparse, 1 mix8
-    const int64_t* rowptr; // sparse
+    int kind;              // 0 sparse (sliced ELL), 1 mix8
+    const int64_t* rowptr; // sparse: slice offsets [N / 32 + 1] (entries of slice s at rowptr[s] + e 32 + lane)
     const int* col;        // sparse (gather folded in for the first inverse stage)
     const void* coef;      // sparse: complex values
     const int* out_row;    // sparse: output position of row r (scatter folded in), nullptr = identity
