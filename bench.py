@@ -432,7 +432,7 @@ def b200_arm(args):
     hbm = peaks.get("hbm_gbs", 6488.0)
     # the roofline of the pipe that executes the plan: the FP64 tensor pipe for
     # the DMMA executors (fp32 plans there keep fp64 arithmetic, complex64 I/O)
-    on_fp64_pipe = (not f32) or info.executor in (2, 4)
+    on_fp64_pipe = (not f32) or info.executor in (2, 4, 5)
     peak_tf = FP64_PEAK_TFLOPS if on_fp64_pipe else FP32_PEAK_TFLOPS
     achieved_tf = flops_fwd / (fwd_ms / 1e3) / 1e12
     achieved_gbs = bytes_fwd / (fwd_ms / 1e3) / 1e9
@@ -447,7 +447,8 @@ def b200_arm(args):
         "traffic": args.traffic if args.traffic is not None else profiled_traffic(args.config, f32, info.executor),
         "kernel": {0: "gemm_f64_kernel / gemm_f32_kernel (direct)", 1: "pipeline_kernel (tile interpreter)",
                    2: "pipeline2_kernel (FP64 tensor pipe)", 3: "gstage_* kernels (global multi-pass)",
-                   4: "root pass + 8 x pipeline2_kernel (two-level, FP64 tensor pipe)"}[info.executor],
+                   4: "root pass + 8 x pipeline2_kernel (two-level, FP64 tensor pipe)",
+                   5: "orbit_fft_kernel (S_n on the FP64 tensor pipe + radix-2 FFT)"}[info.executor],
         "algorithmic_flops_per_launch": flops_fwd,
         "algorithmic_bytes_per_launch": bytes_fwd,
         "table_bytes_per_launch": table_bytes_fwd,

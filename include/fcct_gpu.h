@@ -71,7 +71,8 @@ typedef struct {
     double flops_inverse;
     int executor;            /* 0 direct GEMM, 1 tile interpreter, 2 FP64-tensor-pipe
                                 pipeline, 3 global-memory multi-pass pipeline,
-                                4 two-level (n = 16: root pass + eight n = 8 pipelines) */
+                                4 two-level (n = 16: root pass + eight n = 8 pipelines),
+                                5 orbit-FFT (the radix tree telescoped to S_n + radix-2 FFT) */
 } fcct_plan_info_t;
 
 /* Last error message on this thread ("" if none). */

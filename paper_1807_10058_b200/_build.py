@@ -14,8 +14,8 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libfcct_b200.so"
 CLI = LIB_DIR / "fcct"  # command-line front end (csrc/cli.cpp), a client of the C ABI
-SOURCES = ["kernels.cu", "capi.cpp", "plan.cpp", "tiling.cpp", "plan_cache.cpp", "voxel_io.cpp"]
-HEADERS = ["kernels.hpp", "device.cuh", "plan.hpp", "tiling.hpp", "plan_cache.hpp", "voxel_io.hpp"]
+SOURCES = ["kernels.cu", "orbit_fft.cu", "orbit_fft_host.cpp", "capi.cpp", "plan.cpp", "tiling.cpp", "plan_cache.cpp", "voxel_io.cpp"]
+HEADERS = ["kernels.hpp", "orbit_fft.hpp", "device.cuh", "plan.hpp", "tiling.hpp", "plan_cache.hpp", "voxel_io.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3",
@@ -60,8 +60,23 @@ def build_cli(force: bool = False, verbose: bool = False) -> Path:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if force or _stale():
         LIB_DIR.mkdir(exist_ok=True)
+        obj_dir = LIB_DIR / "obj"
+        obj_dir.mkdir(exist_ok=True)
+        # one translation unit per nvcc process, all in parallel, then one link
+        compile_flags = [f for f in FLAGS if f != "-shared"]
+        procs, objs = [], []
+        for s in SOURCES:
+            obj = obj_dir / (s + ".o")
+            cmd = [NVCC, *compile_flags, "-c", str(CSRC / s), "-o", str(obj)]
+            if verbose:
+                print(" ".join(cmd))
+            procs.append((s, subprocess.Popen(cmd)))
+            objs.append(str(obj))
+        failed = [s for s, p in procs if p.wait() != 0]
+        if failed:
+            raise subprocess.CalledProcessError(1, f"nvcc {' '.join(failed)}")
         tmp = LIB.with_suffix(".so.tmp")
-        cmd = [NVCC, *FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
+        cmd = [NVCC, *FLAGS, "-o", str(tmp), *objs]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

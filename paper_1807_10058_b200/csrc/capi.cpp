@@ -16,6 +16,7 @@
 
 #include "../../include/fcct_gpu.h"
 #include "kernels.hpp"
+#include "orbit_fft.hpp"
 #include "plan.hpp"
 #include "plan_cache.hpp"
 #include "tiling.hpp"
@@ -100,6 +101,29 @@ struct RootTables {
     RootDesc desc{};
     std::vector<std::shared_ptr<DevBuf>> bufs;
 };
+
+// Orbit-FFT executor (orbit_fft.hpp): register-resident base-change tiles.
+struct OrbitFftTables {
+    OrbitFftDesc desc{};
+    std::vector<std::shared_ptr<DevBuf>> bufs;
+    int64_t tiles = 0;
+};
+
+void upload_orbit_fft(const OrbitFftHost& h, OrbitFftTables& out) {
+    out = OrbitFftTables{};
+    auto bt = upload(h.table), bm = upload(h.meta), bn = upload(h.ntiles);
+    out.bufs = {bt, bm, bn};
+    OrbitFftDesc& d = out.desc;
+    d.n = h.n;
+    d.N = h.N;
+    d.dir = h.dir;
+    d.groups = h.groups;
+    d.tmax = h.tmax;
+    d.table = static_cast<const double2*>(bt->ptr);
+    d.meta = static_cast<const int2*>(bm->ptr);
+    d.ntiles = static_cast<const int*>(bn->ptr);
+    out.tiles = h.tiles;
+}
 
 struct Pipeline2Tables {
     Pipeline2Desc desc{};
@@ -487,6 +511,8 @@ struct fcct_plan_s {
     bool radix = false;
     std::shared_ptr<const PlanNode> tree;
     PipelineTables fwd, inv;
+    bool offt = false;  // orbit-FFT executor (telescoped radix tree, orbit_fft.hpp)
+    OrbitFftTables ofwd, ofinv;
     bool v2 = false;  // fp64 DMMA pipeline (tiling.hpp)
     Pipeline2Tables fwd2, inv2;
     bool two_level = false;  // n = 16: root pass + eight n = 8 child pipelines
@@ -734,14 +760,71 @@ void run_two_level(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, v
     ck(cudaStreamSynchronize(st), "sync");  // the plan-owned scratch serialises calls on this path
 }
 
-// Picks the executor of a fast plan: the fp64 DMMA pipeline (n <= 8), else
-// the shared-memory tile interpreter (one block's state fits a CTA tile),
-// else the global-memory multi-pass pipeline. FCCT_PIPELINE=v1|v2|global
-// forces one for experiments.
+// max |a - b| over the union of the two sparsity patterns
+long double sparse_max_diff(const SparseLD& a, const SparseLD& b) {
+    if (a.dim != b.dim) return 1e300L;
+    long double worst = 0;
+    std::vector<cld> row(static_cast<size_t>(a.dim), cld{0, 0});
+    for (int64_t r = 0; r < a.dim; ++r) {
+        for (int64_t k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) row[a.col[k]] += a.val[k];
+        for (int64_t k = b.rowptr[r]; k < b.rowptr[r + 1]; ++k) row[b.col[k]] -= b.val[k];
+        for (int64_t k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) {
+            worst = std::max(worst, std::abs(row[a.col[k]]));
+            row[a.col[k]] = cld{0, 0};
+        }
+        for (int64_t k = b.rowptr[r]; k < b.rowptr[r + 1]; ++k) {
+            worst = std::max(worst, std::abs(row[b.col[k]]));
+            row[b.col[k]] = cld{0, 0};
+        }
+    }
+    return worst;
+}
+
+// True when every factor of `a` equals the exact derivation `b` to within
+// `tol` (a tree loaded from a plan file, or one built here). A perturbed or
+// foreign factor keeps the plan on the stage-by-stage executors, which apply
+// the tree's factors as they are (with_perturbed_basis, transform.cpp:542-554).
+bool tree_matches(const PlanNode& a, const PlanNode& b, long double tol) {
+    if (a.n != b.n || a.radix != b.radix) return false;
+    if (!a.radix) {
+        if (a.D.size() != b.D.size()) return false;
+        for (size_t i = 0; i < a.D.size(); ++i)
+            if (std::abs(a.D[i] - b.D[i]) > tol) return false;
+        return true;
+    }
+    for (int i = 0; i < 64; ++i)
+        if (std::abs(a.K[i] - b.K[i]) > tol) return false;
+    if (sparse_max_diff(a.B, b.B) > tol) return false;
+    for (int c = 0; c < 8; ++c)
+        if (!tree_matches(*a.children[c], *b.children[c], tol)) return false;
+    return true;
+}
+
+// Orbit-FFT executor for n = 4, 8: the radix tree telescoped to S_n then the
+// radix-2 FFT (orbit_fft.hpp). Valid when the plan's tree is the exact
+// factorisation of D_n(p) (it then represents F_n S_n(p) exactly).
+void build_orbit_fft(fcct_plan_s* pl) {
+    pl->offt = false;
+    if (pl->n != 4 && pl->n != 8) return;
+    if (!tree_matches(*pl->tree, *build_tree(pl->n, pl->p), 1e-9L)) return;
+    OrbitFftHost hf, hi;
+    if (!compile_orbit_fft(pl->n, pl->p, false, hf) || !compile_orbit_fft(pl->n, pl->p, true, hi)) return;
+    upload_orbit_fft(hf, pl->ofwd);
+    upload_orbit_fft(hi, pl->ofinv);
+    pl->offt = true;
+}
+
+// Picks the executor of a fast plan: the orbit-FFT executor (n = 4, 8), the
+// fp64 DMMA stage pipeline (n <= 8, stage by stage through the tree), the
+// two-level executor (n = 16), the shared-memory tile interpreter (one
+// block's state fits a CTA tile), else the global-memory multi-pass pipeline.
+// FCCT_PIPELINE=orbit|v2|two|v1|global forces one (A/B runs, parity tests).
 void build_fast_paths(fcct_plan_s* pl) {
     const char* force = std::getenv("FCCT_PIPELINE");
     const std::string f = force ? force : "";
     const bool f32 = pl->precision == FCCT_F32;
+    if (f.empty() || f == "orbit") build_orbit_fft(pl);
+    if (pl->offt) return;
     if (f.empty() || f == "v2") build_v2(pl);
     if (pl->v2) return;
     if (f.empty() || f == "two") build_two_level(pl);
@@ -773,7 +856,7 @@ void fill_info(fcct_plan_s* pl) {
     in.method = pl->radix ? FCCT_FAST : FCCT_DIRECT;
     in.precision = pl->precision;
     in.points = cube(pl->n);
-    in.executor = !pl->radix ? 0 : (pl->v2 ? 2 : (pl->two_level ? 4 : (pl->global ? 3 : 1)));
+    in.executor = !pl->radix ? 0 : (pl->offt ? 5 : (pl->v2 ? 2 : (pl->two_level ? 4 : (pl->global ? 3 : 1))));
     const double N = static_cast<double>(in.points);
     if (pl->radix) {
         in.levels = tree_levels(pl->n);
@@ -787,6 +870,8 @@ void fill_info(fcct_plan_s* pl) {
         for (auto* pt : {&pl->fwd, &pl->inv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->fwd2, &pl->inv2})
+            for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+        for (auto* pt : {&pl->ofwd, &pl->ofinv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->gfwd, &pl->ginv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
@@ -849,6 +934,12 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
     if (pl->radix) {
         if (pl->two_level) {
             run_two_level(pl, inverse, in, f32 ? 1 : 0, out, f32 ? 1 : 0, batch, st);
+            return;
+        }
+        if (pl->offt) {
+            const int m = f32 ? OF_C64 : OF_C128;
+            ck(launch_orbit_fft(inverse ? pl->ofinv.desc : pl->ofwd.desc, m, m, in, out, batch, st, pl->num_sms),
+               "orbit-FFT executor");
             return;
         }
         if (pl->v2) {
@@ -965,6 +1056,13 @@ void run_real(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t 
     if (pl->radix && pl->two_level) {
         const int cm = f32 ? 1 : 0, rm = f32 ? 3 : 2;
         run_two_level(pl, inverse, in, inverse ? cm : rm, out, inverse ? rm : cm, batch, st);
+        return;
+    }
+    if (pl->radix && pl->offt) {
+        const int cm = f32 ? OF_C64 : OF_C128, rm = f32 ? OF_R32 : OF_R64;
+        ck(launch_orbit_fft(inverse ? pl->ofinv.desc : pl->ofwd.desc, inverse ? cm : rm, inverse ? rm : cm, in, out,
+                            batch, st, pl->num_sms),
+           "orbit-FFT executor (real I/O)");
         return;
     }
     if (pl->radix && pl->v2) {
@@ -1364,6 +1462,17 @@ fcct_status fcct_plan_tree_stats(int n, double r, double s, double t, int64_t* t
 // Host emulation of the v2 DMMA pipeline tables (no GPU): applies the
 // compiled stages to `batch` blocks exactly as the kernel indexes them
 // (slots, lane-ordered fragments, unit lists). Tests the plan compiler on CPU.
+// Host emulation of the orbit-FFT executor's compiled tables (CPU tests).
+fcct_status fcct_debug_emulate_orbit_fft(int n, double r, double s, double t, int inverse, const double* in,
+                                         double* out, int64_t batch) {
+    return guarded([&] {
+        OrbitFftHost h;
+        if (!compile_orbit_fft(n, Params{r, s, t}, inverse != 0, h))
+            throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by the orbit-FFT executor");
+        emulate_orbit_fft(h, in, out, batch);
+    });
+}
+
 fcct_status fcct_debug_emulate_v2(int n, double r, double s, double t, int inverse, const double* in, double* out,
                                   int64_t batch) {
     return guarded([&] {

@@ -1,0 +1,182 @@
+// Host side of the orbit-FFT executor (orbit_fft.hpp): compiles the orbit
+// blocks of S_n(p) (or S_n(p)^{-1} / n^3) into register-resident DMMA tiles.
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <numbers>
+
+#include "orbit_fft.hpp"
+#include "plan.hpp"
+
+namespace fcct {
+
+namespace {
+
+struct Chain {  // one n-tile (8 output rows) of one orbit block and its k-tiles
+    int orbit;
+    int nt;
+    int kts;
+};
+
+}  // namespace
+
+bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h) {
+    if (n != 4 && n != 8) return false;
+    const int N = static_cast<int>(cube(n));
+    const int tmax_bound = n == 8 ? kOfTmax8 : kOfTmax4;
+    OrbitBlocks ob = orbit_blocks(n, p);
+    if (!(ob.worst_condition <= 1e12))
+        throw FcctError(ST_ILL_CONDITIONED, "orbit-FFT plan: orbit block condition exceeds 1e12");
+    const Orbits& orb = *ob.orb;
+    std::vector<Chain> chains;
+    for (int o = 0; o < static_cast<int>(orb.members.size()); ++o) {
+        const int s = static_cast<int>(orb.members[o].size());
+        for (int nt = 0; nt < (s + 7) / 8; ++nt) chains.push_back(Chain{o, nt, (s + 3) / 4});
+    }
+    // longest chains first onto the least loaded warp (LPT); ties keep orbit order
+    std::stable_sort(chains.begin(), chains.end(), [](const Chain& a, const Chain& b) { return a.kts > b.kts; });
+    std::vector<std::vector<Chain>> per_warp(kOfWarps);
+    std::vector<int> load(kOfWarps, 0);
+    for (const Chain& c : chains) {
+        const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+        per_warp[w].push_back(c);
+        load[w] += c.kts;
+    }
+    const int tmax = *std::max_element(load.begin(), load.end());
+    if (tmax > tmax_bound) return false;
+    h = OrbitFftHost{};
+    h.n = n;
+    h.N = N;
+    h.dir = inverse ? 1 : 0;
+    h.groups = 512 / N >= 1 ? 512 / N : 1;
+    h.tmax = tmax;
+    h.table.assign(static_cast<size_t>(kOfWarps) * tmax * 32 * 2, 0.0);
+    h.meta.assign(static_cast<size_t>(kOfWarps) * tmax * 4 * 2, 0);
+    h.ntiles.assign(kOfWarps, 0);
+    const long double scale = inverse ? 1.0L / N : 1.0L;
+    for (int w = 0; w < kOfWarps; ++w) {
+        int t = 0;
+        for (const Chain& c : per_warp[w]) {
+            const auto& mem = orb.members[c.orbit];
+            const int s = static_cast<int>(mem.size());
+            const std::vector<cld>& M = inverse ? ob.Sinv[c.orbit] : ob.S[c.orbit];  // [row][col], s x s
+            // positions: forward reads natural kappa, writes swizzled a; inverse the reverse
+            auto in_pos = [&](int col) { return inverse ? of_swizzle(mem[col], n) : mem[col]; };
+            auto out_pos = [&](int row) { return inverse ? mem[row] : of_swizzle(mem[row], n); };
+            for (int kt = 0; kt < c.kts; ++kt, ++t) {
+                for (int l = 0; l < 32; ++l) {
+                    const int row = 8 * c.nt + l / 4, col = 4 * kt + l % 4;
+                    cld v{0, 0};
+                    if (row < s && col < s) v = M[static_cast<size_t>(row) * s + col] * scale;
+                    const size_t e = ((static_cast<size_t>(w) * tmax + t) * 32 + l) * 2;
+                    h.table[e] = static_cast<double>(v.real());
+                    h.table[e + 1] = static_cast<double>(v.imag());
+                }
+                const int flags = (kt == 0 ? 1 : 0) | (kt == c.kts - 1 ? 2 : 0);
+                for (int k = 0; k < 4; ++k) {
+                    const int col = 4 * kt + k;
+                    const int ip = in_pos(col < s ? col : 0);
+                    const int r0 = 8 * c.nt + 2 * k, r1 = r0 + 1;
+                    const int o0 = r0 < s ? out_pos(r0) : 0xFFFF, o1 = r1 < s ? out_pos(r1) : 0xFFFF;
+                    const size_t e = ((static_cast<size_t>(w) * tmax + t) * 4 + k) * 2;
+                    h.meta[e] = ip | (flags << 16);
+                    h.meta[e + 1] = o0 | (o1 << 16);
+                }
+                ++h.tiles;
+            }
+        }
+        h.ntiles[w] = t;
+    }
+    return true;
+}
+
+namespace {
+
+using cd = std::complex<double>;
+
+// v[q] <- sum_p v[p] e^{sign 2 pi i p q / n} along one axis of an n^3 cube
+// stored at positions pos(i, j, k).
+template <typename Pos>
+void dft_axis(std::vector<cd>& buf, int n, int axis, int sign, Pos pos) {
+    std::vector<cd> line(n), res(n);
+    for (int u = 0; u < n; ++u)
+        for (int v = 0; v < n; ++v) {
+            auto at = [&](int x) {
+                int ijk[3];
+                ijk[axis] = x;
+                ijk[axis == 0 ? 1 : 0] = u;
+                ijk[axis == 2 ? 1 : 2] = v;
+                return pos(ijk[0], ijk[1], ijk[2]);
+            };
+            for (int x = 0; x < n; ++x) line[x] = buf[at(x)];
+            for (int q = 0; q < n; ++q) {
+                cd acc{0, 0};
+                for (int x = 0; x < n; ++x) {
+                    const double ang = sign * 2.0 * std::numbers::pi * ((x * q) % n) / n;
+                    acc += line[x] * cd{std::cos(ang), std::sin(ang)};
+                }
+                res[q] = acc;
+            }
+            for (int x = 0; x < n; ++x) buf[at(x)] = res[x];
+        }
+}
+
+}  // namespace
+
+void emulate_orbit_fft(const OrbitFftHost& h, const double* in, double* out, int64_t batch) {
+    const int n = h.n, N = h.N;
+    auto swz = [&](int i, int j, int k) { return of_swizzle((i * n + j) * n + k, n); };
+    std::vector<cd> y(N), x(N);
+    for (int64_t b = 0; b < batch; ++b) {
+        const double* src = in + b * 2 * N;
+        double* dst = out + b * 2 * N;
+        auto base_change = [&](const std::vector<cd>& from, std::vector<cd>& to) {
+            for (int w = 0; w < kOfWarps; ++w) {
+                cd acc[8];
+                for (int t = 0; t < h.ntiles[w]; ++t) {
+                    const int32_t* m = &h.meta[(static_cast<size_t>(w) * h.tmax + t) * 8];
+                    const int flags = m[0] >> 16;
+                    if (flags & 1)
+                        for (auto& a : acc) a = cd{0, 0};
+                    for (int l = 0; l < 32; ++l) {
+                        const int k = l % 4, col_n = l / 4;
+                        const size_t e = ((static_cast<size_t>(w) * h.tmax + t) * 32 + l) * 2;
+                        acc[col_n] += cd{h.table[e], h.table[e + 1]} * from[m[2 * k] & 0xFFFF];
+                    }
+                    if (flags & 2)
+                        for (int k = 0; k < 4; ++k) {
+                            const int o0 = m[2 * k + 1] & 0xFFFF, o1 = (m[2 * k + 1] >> 16) & 0xFFFF;
+                            if (o0 != 0xFFFF) to[o0] = acc[2 * k];
+                            if (o1 != 0xFFFF) to[o1] = acc[2 * k + 1];
+                        }
+                }
+            }
+        };
+        for (int a = 0; a < N; ++a) x[a] = cd{src[2 * a], src[2 * a + 1]};
+        if (h.dir == 0) {
+            base_change(x, y);  // y at swizzled positions
+            for (int axis = 2; axis >= 0; --axis) dft_axis(y, n, axis, +1, swz);
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j)
+                    for (int k = 0; k < n; ++k) {
+                        const cd v = y[swz(i, j, k)];
+                        const int a = (i * n + j) * n + k;
+                        dst[2 * a] = v.real();
+                        dst[2 * a + 1] = v.imag();
+                    }
+        } else {
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j)
+                    for (int k = 0; k < n; ++k) y[swz(i, j, k)] = x[(i * n + j) * n + k];
+            for (int axis = 0; axis < 3; ++axis) dft_axis(y, n, axis, -1, swz);
+            std::vector<cd> o(N);
+            base_change(y, o);
+            for (int a = 0; a < N; ++a) {
+                dst[2 * a] = o[a].real();
+                dst[2 * a + 1] = o[a].imag();
+            }
+        }
+    }
+}
+
+}  // namespace fcct

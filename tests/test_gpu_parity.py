@@ -475,3 +475,58 @@ def test_n16_two_level_f32_and_host(cuda, oracle_mod):
     p64 = build_plan(n, CANON)
     xd = torch.from_numpy(x).to(cuda)
     assert torch.equal(p64.apply_values(xd).cpu(), p64.apply_values(xd.cpu()))
+
+
+@pytest.mark.parametrize("pipeline", ["orbit", "v2"])
+@pytest.mark.parametrize("n", [4, 8])
+def test_orbit_fft_and_stage_executors(cuda, oracle_mod, pipeline, n, monkeypatch):
+    """The orbit-FFT executor (the radix tree telescoped to S_n(p) + radix-2 FFT,
+    executor 5, default for n = 4, 8) and the stage-by-stage DMMA pipeline
+    (executor 2) both reproduce the dense oracle: fp64 (<= 1e-12), fp32 I/O
+    (<= 1e-5), fused real-sample I/O bitwise equal to the complex path, on a
+    ragged batch, canonical and non-dyadic offsets."""
+    monkeypatch.setenv("FCCT_PIPELINE", pipeline)
+    want = 5 if pipeline == "orbit" else 2
+    for p in (CANON, SkewParams(0.21, 0.055, 0.4)):
+        x = rand_batch(n, 45, seed=7 * n)
+        y_ref = oracle_mod.forward_dense(n, tup(p), x)
+        x_ref = oracle_mod.inverse_dense(n, tup(p), y_ref)
+        plan = build_plan(n, p)
+        assert plan.info.executor == want
+        y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values
+        assert rel(y.cpu().numpy(), y_ref) <= F64_TOL
+        xb = inverse_apply(plan, Spectrum(n, p, torch.from_numpy(y_ref).to(cuda))).data
+        assert rel(xb.cpu().numpy(), x_ref) <= F64_TOL
+        p32 = build_plan(n, p, precision="f32")
+        assert p32.info.executor == want
+        y32 = fast_apply(p32, SignalTensor(n, torch.from_numpy(x).to(torch.complex64).to(cuda))).values
+        assert rel(y32.cpu().numpy(), y_ref) <= F32_TOL
+        b32 = inverse_apply(p32, Spectrum(n, p, y32)).data
+        assert rel(b32.cpu().numpy(), x) <= F32_TOL
+        for pl, rdt in ((plan, torch.float64), (p32, torch.float32)):
+            xr = torch.from_numpy(x.real.copy()).to(rdt).to(cuda)
+            yr = pl.apply_values(xr)
+            assert torch.equal(yr, pl.apply_values(torch.complex(xr, torch.zeros_like(xr))))
+            assert torch.equal(pl._run(yr, True, real_out=True), pl._run(yr, True).real.contiguous())
+
+
+def test_orbit_fft_full_batch_properties(cuda, oracle_mod):
+    """c2 at full size (65,536 blocks of n = 8): round trip, linearity and
+    oracle rows on a sample of blocks; repeated calls are bitwise identical."""
+    n, B = 8, 65536
+    plan = build_plan(n, CANON)
+    assert plan.info.executor == 5
+    g = torch.Generator(device=cuda).manual_seed(2)
+    x = torch.complex(torch.rand(B, n**3, device=cuda, dtype=torch.float64, generator=g) * 2 - 1,
+                      torch.rand(B, n**3, device=cuda, dtype=torch.float64, generator=g) * 2 - 1)
+    y = plan.apply_values(x)
+    y2 = plan.apply_values(x)
+    assert torch.equal(y, y2)
+    back = plan._run(y, True)
+    assert float(torch.linalg.norm(back - x) / torch.linalg.norm(x)) <= F64_TOL
+    idx = torch.tensor([0, 1, 4097, 33333, B - 1], device=cuda)
+    ref = oracle_mod.forward_dense(n, tup(CANON), x[idx].cpu().numpy())
+    assert rel(y[idx].cpu().numpy(), ref) <= F64_TOL
+    ya = plan.apply_values(2.0 * x[:1024] - 0.5j * x[1024:2048])
+    lin = 2.0 * y[:1024] - 0.5j * y[1024:2048]
+    assert float(torch.linalg.norm(ya - lin) / torch.linalg.norm(lin)) <= F64_TOL

@@ -91,6 +91,27 @@ def test_compiled_dmma_tables_emulated(n, p):
     assert np.linalg.norm(xi - xr) / np.linalg.norm(xr) < 1e-12
 
 
+@pytest.mark.parametrize("n", [4, 8])
+@pytest.mark.parametrize("p", [CANON, P2])
+def test_orbit_fft_tables_emulated(n, p):
+    """The orbit-FFT executor's compiled tables (register-resident DMMA tiles of
+    S_n(p) / S_n(p)^{-1} n^-3, swizzled FFT positions), emulated on the host as
+    the kernel indexes them, then the radix-2 FFT: D_n(p) = F_n S_n(p) against
+    the long-double dense oracle, both directions."""
+    L = _capi.lib()
+    rng = np.random.default_rng(10 + n)
+    x = rng.uniform(-1, 1, (3, n**3)) + 1j * rng.uniform(-1, 1, (3, n**3))
+    y = np.zeros_like(x)
+    pt = (p.r, p.s, p.t)
+    assert L.fcct_debug_emulate_orbit_fft(n, *pt, 0, x.ctypes.data, y.ctypes.data, 3) == 0
+    yr = oracle.forward_dense(n, pt, x)
+    assert np.linalg.norm(y - yr) / np.linalg.norm(yr) < 1e-13
+    xi = np.zeros_like(x)
+    assert L.fcct_debug_emulate_orbit_fft(n, *pt, 1, yr.ctypes.data, xi.ctypes.data, 3) == 0
+    xr = oracle.inverse_dense(n, pt, yr)
+    assert np.linalg.norm(xi - xr) / np.linalg.norm(xr) < 1e-13
+
+
 def test_compiled_layouts_are_conflict_free_inside():
     # Only the first stage (natural layout from the TMA load) and the last stage
     # (natural output layout) may see shared-memory bank conflicts.
