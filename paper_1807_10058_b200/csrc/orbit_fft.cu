@@ -125,37 +125,54 @@ __device__ __forceinline__ double neg_hi(double v) {  // -v on the integer pipe 
 }
 
 // Base change on the FP64 tensor pipe: C[block][out] += A[block][in] T[in][out]
-// over this warp's register-resident tiles, for each 8-block group.
+// over this warp's register-resident tiles (every warp runs exactly TMAX,
+// padded with zero tiles), for each 8-block group. The four real products go
+// to four independent accumulator pairs (two DMMA chains per accumulator
+// instead of four), and the next tile's metadata and A fragment are loaded
+// before this tile's DMMAs.
 template <int TMAX, int G, int SM, int DM>
-__device__ __forceinline__ void base_change(const double2 (&tab)[TMAX], const int2* __restrict__ meta_w, int nt_w,
+__device__ __forceinline__ void base_change(const double2 (&tab)[TMAX], const int2* __restrict__ meta_w,
                                             const char* src, int srow, char* dst, int drow, int r, int k) {
     constexpr bool real_src = SM == OF_R64 || SM == OF_R32;
 #pragma unroll 1
     for (int g = 0; g < G; ++g) {
         const char* s_row = src + (8 * g + r) * srow;
         char* d_row = dst + (8 * g + r) * drow;
-        double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+        double rr0 = 0.0, rr1 = 0.0, ri0 = 0.0, ri1 = 0.0;  // a_re Tr, -a_im Ti  -> Re
+        double ir0 = 0.0, ir1 = 0.0, ii0 = 0.0, ii1 = 0.0;  // a_re Ti,  a_im Tr  -> Im
+        int2 m = meta_w[k];
+        double ar, ai;
+        load_elem<SM>(s_row, m.x & 0xFFFF, ar, ai);
 #pragma unroll
         for (int t = 0; t < TMAX; ++t) {
-            if (t < nt_w) {
-                const int2 m = meta_w[t * 4 + k];
-                if (m.x & (1 << 16)) cr0 = cr1 = ci0 = ci1 = 0.0;
-                double ar, ai;
-                load_elem<SM>(s_row, m.x & 0xFFFF, ar, ai);
-                dmma884(cr0, cr1, ar, tab[t].x);
-                dmma884(ci0, ci1, ar, tab[t].y);
-                if constexpr (!real_src) {
-                    // -a_im Ti: the sign goes on the data (a table-side negation is
-                    // loop invariant and the compiler would keep TMAX of them live)
-                    dmma884(cr0, cr1, neg_hi(ai), tab[t].y);
-                    dmma884(ci0, ci1, ai, tab[t].x);
-                }
-                if (m.x & (2 << 16)) {
-                    const int o0 = m.y & 0xFFFF, o1 = (m.y >> 16) & 0xFFFF;
-                    if (o0 != 0xFFFF) store_elem<DM>(d_row, o0, cr0, ci0);
-                    if (o1 != 0xFFFF) store_elem<DM>(d_row, o1, cr1, ci1);
-                }
+            int2 mn = m;
+            double arn = 0.0, ain = 0.0;
+            if (t + 1 < TMAX) {
+                mn = meta_w[(t + 1) * 4 + k];
+                load_elem<SM>(s_row, mn.x & 0xFFFF, arn, ain);
             }
+            dmma884(rr0, rr1, ar, tab[t].x);
+            dmma884(ir0, ir1, ar, tab[t].y);
+            if constexpr (!real_src) {
+                // -a_im Ti: the sign goes on the data (a table-side negation is
+                // loop invariant and the compiler would keep TMAX of them live)
+                dmma884(ri0, ri1, neg_hi(ai), tab[t].y);
+                dmma884(ii0, ii1, ai, tab[t].x);
+            }
+            if (m.x & (2 << 16)) {  // chain end (warp-uniform)
+                const int o0 = m.y & 0xFFFF, o1 = (m.y >> 16) & 0xFFFF;
+                if constexpr (real_src) {
+                    if (o0 != 0xFFFF) store_elem<DM>(d_row, o0, rr0, ir0);
+                    if (o1 != 0xFFFF) store_elem<DM>(d_row, o1, rr1, ir1);
+                } else {
+                    if (o0 != 0xFFFF) store_elem<DM>(d_row, o0, rr0 + ri0, ir0 + ii0);
+                    if (o1 != 0xFFFF) store_elem<DM>(d_row, o1, rr1 + ri1, ir1 + ii1);
+                }
+                rr0 = rr1 = ri0 = ri1 = ir0 = ir1 = ii0 = ii1 = 0.0;
+            }
+            m = mn;
+            ar = arn;
+            ai = ain;
         }
     }
 }
@@ -193,8 +210,12 @@ struct OfCfg {
     static constexpr int G = 512 / N >= 1 ? 512 / N : 1;
     static constexpr int TB = 8 * G;
     static constexpr int EB = mode_bytes(MI) > mode_bytes(MO) ? mode_bytes(MI) : mode_bytes(MO);
-    static constexpr int XROW = N * EB + 16;  // 16-byte rotation of the bank groups per block row
-    static constexpr int YROW = (N + 1) * 16;
+    // Block rows rotate by 4 elements of the base change's access width: the 8
+    // lanes of a quarter-warp (2 blocks x 4 members with positions distinct
+    // mod 4, orbit_fft_host.cpp) then hit distinct banks. X is read by the
+    // forward base change (MI) and written by the inverse one (MO).
+    static constexpr int XROW = N * EB + 4 * mode_bytes(DIR == 0 ? MI : MO);
+    static constexpr int YROW = (N + 4) * 16;
     static constexpr int META = kOfWarps * TMAX * 4 * 8;
     static constexpr int SMEM = 128 + META + 2 * TB * XROW + TB * YROW;
 };
@@ -216,10 +237,9 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
 #pragma unroll
     for (int t = 0; t < TMAX; ++t)
         tab[t] = t < d.tmax ? __ldg(d.table + (static_cast<size_t>(warp) * d.tmax + t) * 32 + lane) : make_double2(0, 0);
-    const int nt_w = __ldg(d.ntiles + warp);
-    for (int i = tid; i < kOfWarps * d.tmax * 4; i += blockDim.x) {
-        const int w = i / (d.tmax * 4), rest = i - w * d.tmax * 4;
-        meta_s[w * TMAX * 4 + rest] = __ldg(d.meta + i);
+    for (int i = tid; i < kOfWarps * TMAX * 4; i += blockDim.x) {  // tiles beyond d.tmax: zero padding
+        const int w = i / (TMAX * 4), rest = i - w * TMAX * 4;
+        meta_s[i] = rest < d.tmax * 4 ? __ldg(d.meta + w * d.tmax * 4 + rest) : make_int2(0, -1);
     }
     if (tid == 0) {
         mbar_init(bar, 1);
@@ -259,7 +279,7 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
         mbar_wait(bar + buf, (phases >> buf) & 1);
         phases ^= 1u << buf;
         if constexpr (DIR == 0) {
-            base_change<TMAX, G, MI, OF_C128>(tab, meta_w, nt_w, X, C::XROW, Y, C::YROW, r, k);
+            base_change<TMAX, G, MI, OF_C128>(tab, meta_w, X, C::XROW, Y, C::YROW, r, k);
             __syncthreads();
             if (tid == 0) {
                 const int64_t nx = tile + 2 * static_cast<int64_t>(gridDim.x);
@@ -279,7 +299,7 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
             __syncthreads();
             fft_pass<NN, -1, TB, 2, OF_C128, OF_C128>(Y, C::YROW, false, Y, C::YROW, false, TB);
             __syncthreads();
-            base_change<TMAX, G, OF_C128, MO>(tab, meta_w, nt_w, Y, C::YROW, X, C::XROW, r, k);
+            base_change<TMAX, G, OF_C128, MO>(tab, meta_w, Y, C::YROW, X, C::XROW, r, k);
             fence_proxy_async_smem();
             __syncthreads();
             if (tid == 0) {

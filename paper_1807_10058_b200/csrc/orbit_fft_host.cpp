@@ -1,6 +1,7 @@
 // Host side of the orbit-FFT executor (orbit_fft.hpp): compiles the orbit
 // blocks of S_n(p) (or S_n(p)^{-1} / n^3) into register-resident DMMA tiles.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <complex>
 #include <numbers>
@@ -12,11 +13,46 @@ namespace fcct {
 
 namespace {
 
-struct Chain {  // one n-tile (8 output rows) of one orbit block and its k-tiles
+// One n-tile (8 output rows) of one orbit block and its k-tiles (4 input
+// columns each); -1 marks a padding row / column (zero table entries).
+struct Chain {
     int orbit;
-    int nt;
-    int kts;
+    std::array<int, 8> rows;
+    std::vector<std::array<int, 4>> ktiles;
 };
+
+// Partitions members (indices 0..s-1) into groups of <= 4 whose positions are
+// distinct mod 4 wherever the residues allow: with a block-row rotation of 4
+// bank groups (orbit_fft.cu) the 8 lanes of a quarter-warp (2 blocks x 4
+// members) then touch 8 distinct bank groups.
+std::vector<std::array<int, 4>> residue_groups(const std::vector<int>& pos) {
+    std::array<std::vector<int>, 4> bucket;
+    for (int m = 0; m < static_cast<int>(pos.size()); ++m) bucket[pos[m] & 3].push_back(m);
+    auto by_size = [&] {
+        std::array<int, 4> order{0, 1, 2, 3};
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return bucket[x].size() > bucket[y].size(); });
+        return order;
+    };
+    std::vector<std::array<int, 4>> groups;
+    for (int left = static_cast<int>(pos.size()); left > 0;) {
+        const int want = std::min(4, left);
+        std::array<int, 4> g{-1, -1, -1, -1};
+        int filled = 0;
+        for (int q : by_size())  // one member from each residue class first
+            if (filled < want && !bucket[q].empty()) {
+                g[filled++] = bucket[q].back();
+                bucket[q].pop_back();
+            }
+        while (filled < want) {  // then the largest classes (a conflict, but no extra tile)
+            const int q = by_size()[0];
+            g[filled++] = bucket[q].back();
+            bucket[q].pop_back();
+        }
+        left -= want;
+        groups.push_back(g);
+    }
+    return groups;
+}
 
 }  // namespace
 
@@ -28,19 +64,39 @@ bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h) {
     if (!(ob.worst_condition <= 1e12))
         throw FcctError(ST_ILL_CONDITIONED, "orbit-FFT plan: orbit block condition exceeds 1e12");
     const Orbits& orb = *ob.orb;
+    // positions: forward reads natural kappa and writes swizzled a; inverse the reverse
+    auto in_pos = [&](int lex) { return inverse ? of_swizzle(lex, n) : lex; };
+    auto out_pos = [&](int lex) { return inverse ? lex : of_swizzle(lex, n); };
     std::vector<Chain> chains;
     for (int o = 0; o < static_cast<int>(orb.members.size()); ++o) {
-        const int s = static_cast<int>(orb.members[o].size());
-        for (int nt = 0; nt < (s + 7) / 8; ++nt) chains.push_back(Chain{o, nt, (s + 3) / 4});
+        const auto& mem = orb.members[o];
+        std::vector<int> ip, op;
+        for (int m : mem) {
+            ip.push_back(in_pos(m));
+            op.push_back(out_pos(m));
+        }
+        const auto kt = residue_groups(ip);
+        const auto rg = residue_groups(op);
+        // n-tile = two row groups: the first on the even output columns (the
+        // lanes' first store), the second on the odd ones (the second store)
+        for (size_t g = 0; g < rg.size(); g += 2) {
+            Chain c{o, {}, kt};
+            for (int k = 0; k < 4; ++k) {
+                c.rows[2 * k] = rg[g][k];
+                c.rows[2 * k + 1] = g + 1 < rg.size() ? rg[g + 1][k] : -1;
+            }
+            chains.push_back(std::move(c));
+        }
     }
     // longest chains first onto the least loaded warp (LPT); ties keep orbit order
-    std::stable_sort(chains.begin(), chains.end(), [](const Chain& a, const Chain& b) { return a.kts > b.kts; });
-    std::vector<std::vector<Chain>> per_warp(kOfWarps);
+    std::stable_sort(chains.begin(), chains.end(),
+                     [](const Chain& a, const Chain& b) { return a.ktiles.size() > b.ktiles.size(); });
+    std::vector<std::vector<const Chain*>> per_warp(kOfWarps);
     std::vector<int> load(kOfWarps, 0);
     for (const Chain& c : chains) {
         const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-        per_warp[w].push_back(c);
-        load[w] += c.kts;
+        per_warp[w].push_back(&c);
+        load[w] += static_cast<int>(c.ktiles.size());
     }
     const int tmax = *std::max_element(load.begin(), load.end());
     if (tmax > tmax_bound) return false;
@@ -50,34 +106,35 @@ bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h) {
     h.dir = inverse ? 1 : 0;
     h.groups = 512 / N >= 1 ? 512 / N : 1;
     h.tmax = tmax;
+    // every warp runs exactly tmax tiles: the padding tiles are zero, flagged
+    // neither chain start nor end, and read slot 0 (no per-tile branch remains)
     h.table.assign(static_cast<size_t>(kOfWarps) * tmax * 32 * 2, 0.0);
     h.meta.assign(static_cast<size_t>(kOfWarps) * tmax * 4 * 2, 0);
-    h.ntiles.assign(kOfWarps, 0);
+    for (size_t e = 1; e < h.meta.size(); e += 2) h.meta[e] = 0xFFFF | (0xFFFF << 16);
+    h.ntiles.assign(kOfWarps, tmax);
     const long double scale = inverse ? 1.0L / N : 1.0L;
     for (int w = 0; w < kOfWarps; ++w) {
         int t = 0;
-        for (const Chain& c : per_warp[w]) {
-            const auto& mem = orb.members[c.orbit];
+        for (const Chain* c : per_warp[w]) {
+            const auto& mem = orb.members[c->orbit];
             const int s = static_cast<int>(mem.size());
-            const std::vector<cld>& M = inverse ? ob.Sinv[c.orbit] : ob.S[c.orbit];  // [row][col], s x s
-            // positions: forward reads natural kappa, writes swizzled a; inverse the reverse
-            auto in_pos = [&](int col) { return inverse ? of_swizzle(mem[col], n) : mem[col]; };
-            auto out_pos = [&](int row) { return inverse ? mem[row] : of_swizzle(mem[row], n); };
-            for (int kt = 0; kt < c.kts; ++kt, ++t) {
+            const std::vector<cld>& M = inverse ? ob.Sinv[c->orbit] : ob.S[c->orbit];  // [row][col], s x s
+            const int kts = static_cast<int>(c->ktiles.size());
+            for (int kt = 0; kt < kts; ++kt, ++t) {
+                const auto& cols = c->ktiles[kt];
                 for (int l = 0; l < 32; ++l) {
-                    const int row = 8 * c.nt + l / 4, col = 4 * kt + l % 4;
+                    const int row = c->rows[l / 4], col = cols[l % 4];
                     cld v{0, 0};
-                    if (row < s && col < s) v = M[static_cast<size_t>(row) * s + col] * scale;
+                    if (row >= 0 && col >= 0) v = M[static_cast<size_t>(row) * s + col] * scale;
                     const size_t e = ((static_cast<size_t>(w) * tmax + t) * 32 + l) * 2;
                     h.table[e] = static_cast<double>(v.real());
                     h.table[e + 1] = static_cast<double>(v.imag());
                 }
-                const int flags = (kt == 0 ? 1 : 0) | (kt == c.kts - 1 ? 2 : 0);
+                const int flags = (kt == 0 ? 1 : 0) | (kt == kts - 1 ? 2 : 0);
                 for (int k = 0; k < 4; ++k) {
-                    const int col = 4 * kt + k;
-                    const int ip = in_pos(col < s ? col : 0);
-                    const int r0 = 8 * c.nt + 2 * k, r1 = r0 + 1;
-                    const int o0 = r0 < s ? out_pos(r0) : 0xFFFF, o1 = r1 < s ? out_pos(r1) : 0xFFFF;
+                    const int ip = in_pos(mem[cols[k] >= 0 ? cols[k] : cols[0]]);
+                    const int r0 = c->rows[2 * k], r1 = c->rows[2 * k + 1];
+                    const int o0 = r0 >= 0 ? out_pos(mem[r0]) : 0xFFFF, o1 = r1 >= 0 ? out_pos(mem[r1]) : 0xFFFF;
                     const size_t e = ((static_cast<size_t>(w) * tmax + t) * 4 + k) * 2;
                     h.meta[e] = ip | (flags << 16);
                     h.meta[e + 1] = o0 | (o1 << 16);
@@ -85,7 +142,6 @@ bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h) {
                 ++h.tiles;
             }
         }
-        h.ntiles[w] = t;
     }
     return true;
 }
