@@ -119,6 +119,7 @@ void upload_orbit_fft(const OrbitFftHost& h, OrbitFftTables& out) {
     d.dir = h.dir;
     d.groups = h.groups;
     d.tmax = h.tmax;
+    d.warps = h.warps;
     d.table = static_cast<const double2*>(bt->ptr);
     d.meta = static_cast<const int2*>(bm->ptr);
     d.ntiles = static_cast<const int*>(bn->ptr);
@@ -807,8 +808,12 @@ void build_orbit_fft(fcct_plan_s* pl) {
     pl->offt = false;
     if (pl->n != 4 && pl->n != 8) return;
     if (!tree_matches(*pl->tree, *build_tree(pl->n, pl->p), 1e-9L)) return;
+    // default: the warp-specialised kernel (12 base-change + 4 FFT warps);
+    // FCCT_OFFT_WS=0 selects the phased one (16 warps alternate both roles)
+    const char* ws = std::getenv("FCCT_OFFT_WS");
+    const int warps = (ws && std::string(ws) == "0") ? kOfWarps : kOfBcWarps;
     OrbitFftHost hf, hi;
-    if (!compile_orbit_fft(pl->n, pl->p, false, hf) || !compile_orbit_fft(pl->n, pl->p, true, hi)) return;
+    if (!compile_orbit_fft(pl->n, pl->p, false, hf, warps) || !compile_orbit_fft(pl->n, pl->p, true, hi, warps)) return;
     upload_orbit_fft(hf, pl->ofwd);
     upload_orbit_fft(hi, pl->ofinv);
     pl->offt = true;
@@ -1467,7 +1472,7 @@ fcct_status fcct_debug_emulate_orbit_fft(int n, double r, double s, double t, in
                                          double* out, int64_t batch) {
     return guarded([&] {
         OrbitFftHost h;
-        if (!compile_orbit_fft(n, Params{r, s, t}, inverse != 0, h))
+        if (!compile_orbit_fft(n, Params{r, s, t}, inverse != 0, h, kOfBcWarps))
             throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by the orbit-FFT executor");
         emulate_orbit_fft(h, in, out, batch);
     });

@@ -312,6 +312,253 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
     if (DIR == 1 && tid == 0) tma_store_wait0();
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised kernel: warps 0..11 run the base change (register-resident
+// table split 12 ways), warps 12..15 the FFT line passes, on different tiles
+// at the same time, handing tiles over through named barriers.
+//   forward: three tile buffers rotate as input in(j) = -j mod 3 and FFT
+//            buffer f(j) = 1 - j mod 3; the FFT group reloads f(j) with tile
+//            j + 2 once FFT(j) is done (in(j + 2) == f(j)).
+//   inverse: the FFT group reads tile j from HBM (first pass) into y(j mod 3);
+//            the base change writes its rows straight to HBM.
+// Named barriers: 1..3 "tile j ready" (j mod 3), 4..6 "y(j mod 3) free"
+// (inverse), 7 base-change group, 8 FFT group.
+// ---------------------------------------------------------------------------
+constexpr int kOfFftThreads = (kOfWarps - kOfBcWarps) * 32;
+static_assert(kOfFftThreads == 128, "FFT group: warps 12..15, one per SMSP");
+constexpr int kOfBcThreads = kOfBcWarps * 32;
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+// Base change with two accumulator pairs and no fragment prefetch (the
+// specialised kernel's base-change warps keep 25 table tiles in registers).
+// Rows of blocks >= nvalid are not stored (the inverse writes to HBM).
+template <int TMAX, int G, int SM, int DM>
+__device__ __forceinline__ void base_change_lean(const double2 (&tab)[TMAX], const int2* __restrict__ meta_w, int nt_w,
+                                                 const char* src, int srow, char* dst, int64_t drow, int r, int k,
+                                                 int nvalid) {
+    constexpr bool real_src = SM == OF_R64 || SM == OF_R32;
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+        const char* s_row = src + (8 * g + r) * srow;
+        char* d_row = dst + (8 * g + r) * drow;
+        const bool live = 8 * g + r < nvalid;
+        double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < TMAX; ++t) {
+            if (t >= nt_w) break;  // warp-uniform
+            // no fragment prefetch: with 25 register-resident tiles it spills (measured slower)
+            const int2 m = meta_w[t * 4 + k];
+            double ar, ai;
+            load_elem<SM>(s_row, m.x & 0xFFFF, ar, ai);
+            dmma884(cr0, cr1, ar, tab[t].x);
+            dmma884(ci0, ci1, ar, tab[t].y);
+            if constexpr (!real_src) {
+                dmma884(cr0, cr1, neg_hi(ai), tab[t].y);
+                dmma884(ci0, ci1, ai, tab[t].x);
+            }
+            if (m.x & (2 << 16)) {  // chain end (warp-uniform)
+                const int o0 = m.y & 0xFFFF, o1 = (m.y >> 16) & 0xFFFF;
+                if (live && o0 != 0xFFFF) store_elem<DM>(d_row, o0, cr0, ci0);
+                if (live && o1 != 0xFFFF) store_elem<DM>(d_row, o1, cr1, ci1);
+                cr0 = cr1 = ci0 = ci1 = 0.0;
+            }
+        }
+    }
+}
+
+// One FFT pass by the FFT group (128 threads), two lines per step for ILP.
+// Lines of blocks >= nvalid neither load from nor store to a natural
+// (global) side.
+template <int NN, int SIGN, int TB, int AX, int SRCM, int DSTM>
+__device__ __forceinline__ void fft_pass_group(int ft, const char* src, int64_t srow, bool src_nat, char* dst,
+                                               int64_t drow, bool dst_nat, int nvalid) {
+    constexpr int L = TB * NN * NN;
+    constexpr int P = 2;
+    static_assert(L % (P * kOfFftThreads) == 0, "lines per FFT thread");
+#pragma unroll 1
+    for (int base = ft; base < L; base += P * kOfFftThreads) {
+        double2 v[P][NN];
+        int bb[P], hh[P], ll[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const int line = base + q * kOfFftThreads;
+            bb[q] = line / (NN * NN);
+            const int l = line % (NN * NN);
+            hh[q] = l / NN;
+            ll[q] = l % NN;
+        }
+        auto pos = [&](int q, int x, bool natural) {
+            const int hi = hh[q], lo = ll[q];
+            const int i = AX == 0 ? x : hi, j = AX == 0 ? hi : (AX == 1 ? x : lo), kk = AX == 2 ? x : lo;
+            return (i * NN + j) * NN + (natural ? kk : (kk ^ (j & (NN - 1))));
+        };
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const char* sp = src + bb[q] * srow;
+            const bool ok = !src_nat || bb[q] < nvalid;
+#pragma unroll
+            for (int x = 0; x < NN; ++x) {
+                if (ok)
+                    load_elem<SRCM>(sp, pos(q, x, src_nat), v[q][x].x, v[q][x].y);
+                else
+                    v[q][x] = make_double2(0.0, 0.0);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < P; ++q) fft_line<NN, SIGN>(v[q]);
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            if (dst_nat && bb[q] >= nvalid) continue;
+            char* dp = dst + bb[q] * drow;
+#pragma unroll
+            for (int x = 0; x < NN; ++x) store_elem<DSTM>(dp, pos(q, x, dst_nat), v[q][x].x, v[q][x].y);
+        }
+    }
+}
+
+template <int NN, int DIR, int MI, int MO, int TMAX>
+struct OfWsCfg {
+    static constexpr int N = NN * NN * NN;
+    static constexpr int G = 512 / N >= 1 ? 512 / N : 1;
+    static constexpr int TB = 8 * G;
+    static constexpr int XROW = N * mode_bytes(MI) + 4 * mode_bytes(MI);  // forward input rows (see OfCfg)
+    static constexpr int YROW = (N + 4) * 16;
+    static constexpr int BUF = ((TB * (XROW > YROW ? XROW : YROW)) + 127) / 128 * 128;
+    static constexpr int META = kOfBcWarps * TMAX * 4 * 8;
+    static constexpr int SMEM = 128 + META + 3 * BUF;
+};
+
+template <int NN, int DIR, int MI, int MO, int TMAX>
+__global__ void __launch_bounds__(kOfWarps * 32, 1)
+    orbit_fft_ws_kernel(const __grid_constant__ OrbitFftDesc d, const void* __restrict__ in, void* __restrict__ out,
+                        int64_t batch) {
+    using C = OfWsCfg<NN, DIR, MI, MO, TMAX>;
+    constexpr int N = C::N, TB = C::TB, G = C::G;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // [3] tile-buffer loads (forward)
+    int2* meta_s = reinterpret_cast<int2*>(smem + 128);
+    char* buf0 = reinterpret_cast<char*>(smem + 128 + C::META);
+    auto buf = [&](int b) { return buf0 + b * C::BUF; };
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int64_t ntiles = (batch + TB - 1) / TB;
+    constexpr uint32_t in_row = N * mode_bytes(MI), out_row = N * mode_bytes(MO);
+    for (int i = tid; i < kOfBcWarps * TMAX * 4; i += blockDim.x) {  // tiles beyond d.tmax: zero padding
+        const int w = i / (TMAX * 4), rest = i - w * TMAX * 4;
+        meta_s[i] = rest < d.tmax * 4 ? __ldg(d.meta + w * d.tmax * 4 + rest) : make_int2(0, -1);
+    }
+    if (tid == 0) {
+        for (int b = 0; b < 3; ++b) mbar_init(bar + b, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto tile_of = [&](int j) { return static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(j) * gridDim.x; };
+    auto nvalid_of = [&](int64_t tile) { return static_cast<int>(batch - tile * TB < TB ? batch - tile * TB : TB); };
+    auto issue_load = [&](int b, int64_t tile) {  // forward: raw input rows -> buffer b (X layout)
+        const int64_t t0 = tile * TB;
+        const int nv = nvalid_of(tile);
+        mbar_arrive_expect_tx(bar + b, in_row * nv);
+        const char* src = static_cast<const char*>(in) + t0 * in_row;
+        for (int q = 0; q < nv; ++q)
+            tma_load_1d(buf(b) + q * C::XROW, src + static_cast<int64_t>(q) * in_row, in_row, bar + b);
+    };
+    if constexpr (DIR == 0) {
+        if (tid == 0) {
+            if (tile_of(0) < ntiles) issue_load(0, tile_of(0));
+            if (tile_of(1) < ntiles) issue_load(2, tile_of(1));
+        }
+    }
+    if (warp < kOfBcWarps) {
+        // ---------------- base-change group ----------------
+        const int lane = tid & 31, r = lane >> 2, k = lane & 3;
+        double2 tab[TMAX];
+#pragma unroll
+        for (int t = 0; t < TMAX; ++t)
+            tab[t] = t < d.tmax ? __ldg(d.table + (static_cast<size_t>(warp) * d.tmax + t) * 32 + lane)
+                                : make_double2(0, 0);
+        const int2* meta_w = meta_s + warp * TMAX * 4;
+        const int nt_w = __ldg(d.ntiles + warp);
+        for (int j = 0; tile_of(j) < ntiles; ++j) {
+            const int64_t tile = tile_of(j);
+            const int nvalid = nvalid_of(tile);
+            if constexpr (DIR == 0) {
+                const int bi = (3 - j % 3) % 3, bf = (4 - j % 3) % 3;
+                mbar_wait(bar + bi, (j / 3) & 1);
+                if (j > 0) named_sync(7, kOfBcThreads);  // BC(j - 1) has read buffer bf (= in(j - 1))
+                base_change_lean<TMAX, G, MI, OF_C128>(tab, meta_w, nt_w, buf(bi), C::XROW, buf(bf), C::YROW, r, k, TB);
+                named_arrive(1 + j % 3, kOfWarps * 32);  // tile j's spectrum-side buffer is ready
+            } else {
+                named_sync(1 + j % 3, kOfWarps * 32);    // FFT(j) has filled y(j mod 3)
+                char* dst = static_cast<char*>(out) + tile * TB * static_cast<int64_t>(out_row);
+                base_change_lean<TMAX, G, OF_C128, MO>(tab, meta_w, nt_w, buf(j % 3), C::YROW, dst, out_row, r, k, nvalid);
+                named_arrive(4 + j % 3, kOfWarps * 32);  // y(j mod 3) may be refilled
+            }
+        }
+    } else {
+        // ---------------- FFT group ----------------
+        const int ft = tid - kOfBcWarps * 32;
+        for (int j = 0; tile_of(j) < ntiles; ++j) {
+            const int64_t tile = tile_of(j);
+            const int nvalid = nvalid_of(tile);
+            if constexpr (DIR == 0) {
+                const int bf = (4 - j % 3) % 3;
+                char* Y = buf(bf);
+                named_sync(1 + j % 3, kOfWarps * 32);
+                fft_pass_group<NN, +1, TB, 2, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, TB);
+                named_sync(8, kOfFftThreads);
+                fft_pass_group<NN, +1, TB, 1, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, TB);
+                named_sync(8, kOfFftThreads);
+                fft_pass_group<NN, +1, TB, 0, OF_C128, MO>(ft, Y, C::YROW, false,
+                                                          static_cast<char*>(out) + tile * TB * static_cast<int64_t>(out_row),
+                                                          out_row, true, nvalid);
+                named_sync(8, kOfFftThreads);
+                if (ft == 0 && tile_of(j + 2) < ntiles) {  // f(j) becomes in(j + 2)
+                    fence_proxy_async_smem();
+                    issue_load(bf, tile_of(j + 2));
+                }
+            } else {
+                char* Y = buf(j % 3);
+                if (ft == 0 && tile_of(j + 2) < ntiles)
+                    prefetch_l2_bulk(static_cast<const char*>(in) + tile_of(j + 2) * TB * static_cast<int64_t>(in_row),
+                                     in_row * nvalid_of(tile_of(j + 2)));
+                if (j >= 3) named_sync(4 + j % 3, kOfWarps * 32);  // BC(j - 3) has read y(j mod 3)
+                fft_pass_group<NN, -1, TB, 0, MI, OF_C128>(ft, static_cast<const char*>(in) + tile * TB * static_cast<int64_t>(in_row),
+                                                          in_row, true, Y, C::YROW, false, nvalid);
+                named_sync(8, kOfFftThreads);
+                fft_pass_group<NN, -1, TB, 1, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, TB);
+                named_sync(8, kOfFftThreads);
+                fft_pass_group<NN, -1, TB, 2, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, TB);
+                named_arrive(1 + j % 3, kOfWarps * 32);
+            }
+        }
+    }
+}
+
+template <int NN, int DIR, int MI, int MO, int TMAX>
+cudaError_t launch_ws_t(const OrbitFftDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st,
+                        int num_sms) {
+    using C = OfWsCfg<NN, DIR, MI, MO, TMAX>;
+    auto kern = orbit_fft_ws_kernel<NN, DIR, MI, MO, TMAX>;
+    static thread_local int prepared_dev = -1;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (prepared_dev != dev) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        prepared_dev = dev;
+    }
+    const int64_t ntiles = (batch + C::TB - 1) / C::TB;
+    const int64_t grid = std::min<int64_t>(ntiles, num_sms);
+    kern<<<static_cast<unsigned>(grid), kOfWarps * 32, C::SMEM, st>>>(d, in, out, batch);
+    return cudaGetLastError();
+}
+
 template <int NN, int DIR, int MI, int MO, int TMAX>
 cudaError_t launch_t(const OrbitFftDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st, int num_sms) {
     using C = OfCfg<NN, DIR, MI, MO, TMAX>;
@@ -331,20 +578,22 @@ cudaError_t launch_t(const OrbitFftDesc& d, const void* in, void* out, int64_t b
     return cudaGetLastError();
 }
 
-template <int NN, int TMAX>
+template <int NN, int TMAX, bool WS>
 cudaError_t launch_n(const OrbitFftDesc& d, int mi, int mo, const void* in, void* out, int64_t batch, cudaStream_t st,
                      int num_sms) {
-    if (d.dir == 0) {
-        if (mi == OF_C128 && mo == OF_C128) return launch_t<NN, 0, OF_C128, OF_C128, TMAX>(d, in, out, batch, st, num_sms);
-        if (mi == OF_R64 && mo == OF_C128) return launch_t<NN, 0, OF_R64, OF_C128, TMAX>(d, in, out, batch, st, num_sms);
-        if (mi == OF_C64 && mo == OF_C64) return launch_t<NN, 0, OF_C64, OF_C64, TMAX>(d, in, out, batch, st, num_sms);
-        if (mi == OF_R32 && mo == OF_C64) return launch_t<NN, 0, OF_R32, OF_C64, TMAX>(d, in, out, batch, st, num_sms);
-    } else {
-        if (mi == OF_C128 && mo == OF_C128) return launch_t<NN, 1, OF_C128, OF_C128, TMAX>(d, in, out, batch, st, num_sms);
-        if (mi == OF_C128 && mo == OF_R64) return launch_t<NN, 1, OF_C128, OF_R64, TMAX>(d, in, out, batch, st, num_sms);
-        if (mi == OF_C64 && mo == OF_C64) return launch_t<NN, 1, OF_C64, OF_C64, TMAX>(d, in, out, batch, st, num_sms);
-        if (mi == OF_C64 && mo == OF_R32) return launch_t<NN, 1, OF_C64, OF_R32, TMAX>(d, in, out, batch, st, num_sms);
-    }
+#define OF_L(DIRV, MIV, MOV)                                                                     \
+    if (d.dir == DIRV && mi == MIV && mo == MOV)                                                 \
+        return WS ? launch_ws_t<NN, DIRV, MIV, MOV, TMAX>(d, in, out, batch, st, num_sms)        \
+                  : launch_t<NN, DIRV, MIV, MOV, TMAX>(d, in, out, batch, st, num_sms);
+    OF_L(0, OF_C128, OF_C128)
+    OF_L(0, OF_R64, OF_C128)
+    OF_L(0, OF_C64, OF_C64)
+    OF_L(0, OF_R32, OF_C64)
+    OF_L(1, OF_C128, OF_C128)
+    OF_L(1, OF_C128, OF_R64)
+    OF_L(1, OF_C64, OF_C64)
+    OF_L(1, OF_C64, OF_R32)
+#undef OF_L
     return cudaErrorInvalidValue;
 }
 
@@ -353,8 +602,15 @@ cudaError_t launch_n(const OrbitFftDesc& d, int mi, int mo, const void* in, void
 cudaError_t launch_orbit_fft(const OrbitFftDesc& d, int in_mode, int out_mode, const void* in, void* out,
                              int64_t batch, cudaStream_t st, int num_sms) {
     if (batch <= 0) return cudaSuccess;
-    if (d.n == 8 && d.tmax <= kOfTmax8) return launch_n<8, kOfTmax8>(d, in_mode, out_mode, in, out, batch, st, num_sms);
-    if (d.n == 4 && d.tmax <= kOfTmax4) return launch_n<4, kOfTmax4>(d, in_mode, out_mode, in, out, batch, st, num_sms);
+    if (d.warps == kOfBcWarps) {
+        if (d.n == 8 && d.tmax <= kOfWsTmax8)
+            return launch_n<8, kOfWsTmax8, true>(d, in_mode, out_mode, in, out, batch, st, num_sms);
+        if (d.n == 4 && d.tmax <= kOfWsTmax4)
+            return launch_n<4, kOfWsTmax4, true>(d, in_mode, out_mode, in, out, batch, st, num_sms);
+        return cudaErrorInvalidValue;
+    }
+    if (d.n == 8 && d.tmax <= kOfTmax8) return launch_n<8, kOfTmax8, false>(d, in_mode, out_mode, in, out, batch, st, num_sms);
+    if (d.n == 4 && d.tmax <= kOfTmax4) return launch_n<4, kOfTmax4, false>(d, in_mode, out_mode, in, out, batch, st, num_sms);
     return cudaErrorInvalidValue;
 }
 

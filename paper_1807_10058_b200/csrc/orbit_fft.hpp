@@ -27,8 +27,17 @@
 namespace fcct {
 
 constexpr int kOfWarps = 16;   // warps per CTA (one CTA per SM)
+// Phased kernel: all 16 warps run the base change, then the FFT passes.
 constexpr int kOfTmax8 = 19;   // register-resident table tiles per warp, n = 8
 constexpr int kOfTmax4 = 4;    // n = 4
+// Warp-specialised kernel: 12 base-change warps (the register-resident table
+// split 12 ways) and 4 FFT warps that run the previous tile's line passes
+// concurrently, through three rotating tile buffers. Warp w runs on SMSP
+// w % 4: each SMSP carries 3 base-change warps and 1 FFT warp. (Measured:
+// 14 + 2 warps leaves the FFT group the bottleneck, 0.397 vs 0.311 ms.)
+constexpr int kOfBcWarps = 12;
+constexpr int kOfWsTmax8 = 25;
+constexpr int kOfWsTmax4 = 4;
 
 // I/O element modes of the global rows (same codes as the two-level executor).
 enum OfMode { OF_C128 = 0, OF_C64 = 1, OF_R64 = 2, OF_R32 = 3 };
@@ -39,6 +48,7 @@ struct OrbitFftDesc {
     int dir = 0;      // 0 forward (S then FFT+), 1 inverse (FFT- then S^{-1}/N)
     int groups = 1;   // 8-block m-tile groups per CTA tile (tile = 8 * groups blocks)
     int tmax = 0;     // table tiles per warp (<= the kernel's compile-time bound)
+    int warps = kOfWarps;  // base-change warps the table is split over (16 phased, 12 specialised)
     // B fragments of the orbit-block operator, [warp][tmax][32 lanes] (Re, Im):
     // lane l holds M[row 8 nt + l/4][col 4 kt + l%4] of its tile (0 outside the block)
     const double2* table = nullptr;
@@ -50,7 +60,7 @@ struct OrbitFftDesc {
 
 // Host image of the tables (also what the CPU emulation runs).
 struct OrbitFftHost {
-    int n = 0, N = 0, dir = 0, groups = 1, tmax = 0;
+    int n = 0, N = 0, dir = 0, groups = 1, tmax = 0, warps = kOfWarps;
     std::vector<double> table;    // [warp][tmax][32][2]
     std::vector<int32_t> meta;    // [warp][tmax][4][2]
     std::vector<int32_t> ntiles;  // [warp]
@@ -70,7 +80,7 @@ inline int of_swizzle(int a, int n) {
 
 // Compiles the orbit-block operator of S_n(p) (forward) or S_n(p)^{-1} / n^3
 // (inverse) into per-warp DMMA tiles. Returns false when n is not supported.
-bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h);
+bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h, int warps = kOfWarps);
 
 // Host emulation of the kernel's arithmetic on the compiled tables (tests):
 // in/out complex128 rows [batch][N].

@@ -5,6 +5,8 @@
 #include <cmath>
 #include <complex>
 #include <numbers>
+#include <cstdio>
+#include <cstdlib>
 
 #include "orbit_fft.hpp"
 #include "plan.hpp"
@@ -56,10 +58,12 @@ std::vector<std::array<int, 4>> residue_groups(const std::vector<int>& pos) {
 
 }  // namespace
 
-bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h) {
+bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h, int warps) {
     if (n != 4 && n != 8) return false;
+    if (warps != kOfWarps && warps != kOfBcWarps) return false;
     const int N = static_cast<int>(cube(n));
-    const int tmax_bound = n == 8 ? kOfTmax8 : kOfTmax4;
+    const bool ws = warps == kOfBcWarps;
+    const int tmax_bound = n == 8 ? (ws ? kOfWsTmax8 : kOfTmax8) : (ws ? kOfWsTmax4 : kOfTmax4);
     OrbitBlocks ob = orbit_blocks(n, p);
     if (!(ob.worst_condition <= 1e12))
         throw FcctError(ST_ILL_CONDITIONED, "orbit-FFT plan: orbit block condition exceeds 1e12");
@@ -88,17 +92,45 @@ bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h) {
             chains.push_back(std::move(c));
         }
     }
-    // longest chains first onto the least loaded warp (LPT); ties keep orbit order
+    // longest chains first onto the least loaded warp (LPT); ties keep orbit order.
+    // Specialised kernel: balance the FP64 pipe of each SMSP first (SMSPs 2 and
+    // 3 also run an FFT warp: its butterflies are worth ~14 DMMA tile steps per
+    // tile), then the warps inside each SMSP.
     std::stable_sort(chains.begin(), chains.end(),
                      [](const Chain& a, const Chain& b) { return a.ktiles.size() > b.ktiles.size(); });
-    std::vector<std::vector<const Chain*>> per_warp(kOfWarps);
-    std::vector<int> load(kOfWarps, 0);
-    for (const Chain& c : chains) {
-        const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-        per_warp[w].push_back(&c);
-        load[w] += static_cast<int>(c.ktiles.size());
+    std::vector<std::vector<const Chain*>> per_warp(warps);
+    std::vector<int> load(warps, 0);
+    if (ws) {
+        const int fft_steps = n == 8 ? 14 : 0;
+        std::array<double, 4> sm_load{};
+        std::array<int, 4> sm_warps{};
+        for (int w = 0; w < warps; ++w) ++sm_warps[w % 4];
+        for (int q = 0; q < 4; ++q)
+            if (sm_warps[q] < (warps + 3) / 4) sm_load[q] = fft_steps * sm_warps[q];  // hosts an FFT warp
+        for (const Chain& c : chains) {
+            // least loaded SMSP (its FP64 pipe is shared by its warps), then its least loaded warp
+            int q = 0;
+            for (int x = 1; x < 4; ++x)
+                if (sm_load[x] < sm_load[q]) q = x;
+            int w = q;
+            for (int x = q; x < warps; x += 4)
+                if (load[x] < load[w]) w = x;
+            per_warp[w].push_back(&c);
+            load[w] += static_cast<int>(c.ktiles.size());
+            sm_load[q] += static_cast<double>(c.ktiles.size());
+        }
+    } else {
+        for (const Chain& c : chains) {
+            const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+            per_warp[w].push_back(&c);
+            load[w] += static_cast<int>(c.ktiles.size());
+        }
     }
     const int tmax = *std::max_element(load.begin(), load.end());
+    if (std::getenv("FCCT_DEBUG_OFFT_LOAD")) {
+        for (int w = 0; w < warps; ++w) fprintf(stderr, "%d ", load[w]);
+        fprintf(stderr, "\n");
+    }
     if (tmax > tmax_bound) return false;
     h = OrbitFftHost{};
     h.n = n;
@@ -106,14 +138,15 @@ bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h) {
     h.dir = inverse ? 1 : 0;
     h.groups = 512 / N >= 1 ? 512 / N : 1;
     h.tmax = tmax;
+    h.warps = warps;
     // every warp runs exactly tmax tiles: the padding tiles are zero, flagged
     // neither chain start nor end, and read slot 0 (no per-tile branch remains)
-    h.table.assign(static_cast<size_t>(kOfWarps) * tmax * 32 * 2, 0.0);
-    h.meta.assign(static_cast<size_t>(kOfWarps) * tmax * 4 * 2, 0);
+    h.table.assign(static_cast<size_t>(warps) * tmax * 32 * 2, 0.0);
+    h.meta.assign(static_cast<size_t>(warps) * tmax * 4 * 2, 0);
     for (size_t e = 1; e < h.meta.size(); e += 2) h.meta[e] = 0xFFFF | (0xFFFF << 16);
-    h.ntiles.assign(kOfWarps, tmax);
+    h.ntiles.assign(warps, tmax);  // set to each warp's real count below
     const long double scale = inverse ? 1.0L / N : 1.0L;
-    for (int w = 0; w < kOfWarps; ++w) {
+    for (int w = 0; w < warps; ++w) {
         int t = 0;
         for (const Chain* c : per_warp[w]) {
             const auto& mem = orb.members[c->orbit];
@@ -142,6 +175,7 @@ bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h) {
                 ++h.tiles;
             }
         }
+        h.ntiles[w] = t;
     }
     return true;
 }
@@ -187,7 +221,7 @@ void emulate_orbit_fft(const OrbitFftHost& h, const double* in, double* out, int
         const double* src = in + b * 2 * N;
         double* dst = out + b * 2 * N;
         auto base_change = [&](const std::vector<cd>& from, std::vector<cd>& to) {
-            for (int w = 0; w < kOfWarps; ++w) {
+            for (int w = 0; w < h.warps; ++w) {
                 cd acc[8];
                 for (int t = 0; t < h.ntiles[w]; ++t) {
                     const int32_t* m = &h.meta[(static_cast<size_t>(w) * h.tmax + t) * 8];

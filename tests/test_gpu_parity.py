@@ -477,7 +477,7 @@ def test_n16_two_level_f32_and_host(cuda, oracle_mod):
     assert torch.equal(p64.apply_values(xd).cpu(), p64.apply_values(xd.cpu()))
 
 
-@pytest.mark.parametrize("pipeline", ["orbit", "v2"])
+@pytest.mark.parametrize("pipeline", ["orbit", "orbit-phased", "v2"])
 @pytest.mark.parametrize("n", [4, 8])
 def test_orbit_fft_and_stage_executors(cuda, oracle_mod, pipeline, n, monkeypatch):
     """The orbit-FFT executor (the radix tree telescoped to S_n(p) + radix-2 FFT,
@@ -485,8 +485,9 @@ def test_orbit_fft_and_stage_executors(cuda, oracle_mod, pipeline, n, monkeypatc
     (executor 2) both reproduce the dense oracle: fp64 (<= 1e-12), fp32 I/O
     (<= 1e-5), fused real-sample I/O bitwise equal to the complex path, on a
     ragged batch, canonical and non-dyadic offsets."""
-    monkeypatch.setenv("FCCT_PIPELINE", pipeline)
-    want = 5 if pipeline == "orbit" else 2
+    monkeypatch.setenv("FCCT_PIPELINE", pipeline.split("-")[0])
+    monkeypatch.setenv("FCCT_OFFT_WS", "0" if pipeline == "orbit-phased" else "1")
+    want = 5 if pipeline.startswith("orbit") else 2
     for p in (CANON, SkewParams(0.21, 0.055, 0.4)):
         x = rand_batch(n, 45, seed=7 * n)
         y_ref = oracle_mod.forward_dense(n, tup(p), x)
