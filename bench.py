@@ -100,13 +100,15 @@ class ClockSampler:
 
 
 def profiled_traffic(cfg_name: str, f32: bool, executor: int):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one forward pipeline2
-    launch from the committed `ncu --set full` capture (profiles/
-    r01_pipeline2_raw.csv, c2 fp64: tools/prof_run.py, 65,536 blocks), or None
-    when the run is not that configuration."""
-    if cfg_name != "c2" or f32 or executor != 2:
+    """dram__bytes_read.sum + dram__bytes_write.sum of one forward launch of the
+    dominant kernel from the committed `ncu --set full` capture (c2 fp64,
+    tools/prof_run.py, 65,536 blocks): profiles/r01_orbit_fft_ws_raw.csv for
+    the orbit-FFT executor, profiles/r01_pipeline2_raw.csv for the stage
+    pipeline; None when the run is not that configuration."""
+    files = {2: "r01_pipeline2_raw.csv", 5: "r01_orbit_fft_ws_raw.csv"}
+    if cfg_name != "c2" or f32 or executor not in files:
         return None
-    path = Path(__file__).resolve().parent / "profiles" / "r01_pipeline2_raw.csv"
+    path = Path(__file__).resolve().parent / "profiles" / files[executor]
     try:
         import csv
 
@@ -448,7 +450,7 @@ def b200_arm(args):
         "kernel": {0: "gemm_f64_kernel / gemm_f32_kernel (direct)", 1: "pipeline_kernel (tile interpreter)",
                    2: "pipeline2_kernel (FP64 tensor pipe)", 3: "gstage_* kernels (global multi-pass)",
                    4: "root pass + 8 x pipeline2_kernel (two-level, FP64 tensor pipe)",
-                   5: "orbit_fft_kernel (S_n on the FP64 tensor pipe + radix-2 FFT)"}[info.executor],
+                   5: "orbit_fft_ws_kernel (S_n on the FP64 tensor pipe + radix-2 FFT, warp-specialised)"}[info.executor],
         "algorithmic_flops_per_launch": flops_fwd,
         "algorithmic_bytes_per_launch": bytes_fwd,
         "table_bytes_per_launch": table_bytes_fwd,
@@ -462,6 +464,14 @@ def b200_arm(args):
         "inv_ms": inv_ms,
         "inverse_achieved_tflops": info.flops_inverse * blocks / (inv_ms / 1e3) / 1e12,
     }
+    if info.exec_flops_forward > 0:
+        # what the executor really issues on the FP64 pipes (the orbit-FFT route
+        # telescopes the tree: fewer flops than SURVEY.md's algorithmic count)
+        exec_tf = info.exec_flops_forward * blocks / (fwd_ms / 1e3) / 1e12
+        roof["executed_flops_per_launch"] = info.exec_flops_forward * blocks
+        roof["executed_tflops"] = exec_tf
+        roof["executed_frac_of_fp64_peak"] = exec_tf / peak_tf
+        roof["hbm_frac"] = achieved_gbs / hbm
     cpu = None
     if not args.no_cpu and world >= 1:
         threads = os.cpu_count() or 1

@@ -73,6 +73,10 @@ typedef struct {
                                 pipeline, 3 global-memory multi-pass pipeline,
                                 4 two-level (n = 16: root pass + eight n = 8 pipelines),
                                 5 orbit-FFT (the radix tree telescoped to S_n + radix-2 FFT) */
+    double exec_flops_forward; /* flops the executor issues on the FP64 pipes per block (tensor-core
+                                  tiles including their zero padding, plus FFT butterflies); 0 when
+                                  equal to the algorithmic count */
+    double exec_flops_inverse;
 } fcct_plan_info_t;
 
 /* Last error message on this thread ("" if none). */

@@ -49,6 +49,8 @@ class PlanInfo(ctypes.Structure):
         ("flops_forward", c_double),
         ("flops_inverse", c_double),
         ("executor", c_int),
+        ("exec_flops_forward", c_double),
+        ("exec_flops_inverse", c_double),
     ]
 
 

@@ -107,6 +107,7 @@ struct OrbitFftTables {
     OrbitFftDesc desc{};
     std::vector<std::shared_ptr<DevBuf>> bufs;
     int64_t tiles = 0;
+    double exec_flops = 0;
 };
 
 void upload_orbit_fft(const OrbitFftHost& h, OrbitFftTables& out) {
@@ -120,10 +121,12 @@ void upload_orbit_fft(const OrbitFftHost& h, OrbitFftTables& out) {
     d.groups = h.groups;
     d.tmax = h.tmax;
     d.warps = h.warps;
+    d.in_stride = d.out_stride = 0;
     d.table = static_cast<const double2*>(bt->ptr);
     d.meta = static_cast<const int2*>(bm->ptr);
     d.ntiles = static_cast<const int*>(bn->ptr);
     out.tiles = h.tiles;
+    out.exec_flops = h.exec_flops();
 }
 
 struct Pipeline2Tables {
@@ -519,6 +522,8 @@ struct fcct_plan_s {
     bool two_level = false;  // n = 16: root pass + eight n = 8 child pipelines
     RootTables rfwd, rinv;
     Pipeline2Tables cfwd[8], cinv[8];
+    bool child_offt = false;  // the eight n = 8 children run on the orbit-FFT executor
+    OrbitFftTables ocfwd[8], ocinv[8];
     cudaStream_t cs[4] = {nullptr, nullptr, nullptr, nullptr};  // child pipelines run concurrently
     cudaEvent_t cev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     bool global = false;  // global-memory multi-pass pipeline
@@ -674,6 +679,8 @@ void build_root_ell(const SparseLD& S, int N, RootTables& rt, RootDesc& d) {
     d.val = static_cast<const double2*>(bv->ptr);
 }
 
+bool tree_matches(const PlanNode& a, const PlanNode& b, long double tol);
+
 void build_two_level(fcct_plan_s* pl) {
     const PlanNode& root = *pl->tree;
     if (root.n != 16) return;
@@ -708,7 +715,23 @@ void build_two_level(fcct_plan_s* pl) {
         d.perm = static_cast<const int*>(bp->ptr);
         d.pinv = static_cast<const int*>(bi->ptr);
     }
-    for (int c = 0; c < 8; ++c) {
+    // children: the orbit-FFT executor when every child is the exact n = 8 tree
+    // (FCCT_CHILD_PIPELINE=v2 keeps them on the stage pipeline)
+    const char* cp = std::getenv("FCCT_CHILD_PIPELINE");
+    pl->child_offt = !(cp && std::string(cp) == "v2");
+    for (int c = 0; c < 8 && pl->child_offt; ++c) {
+        const PlanNode& ch = *root.children[c];
+        OrbitFftHost hf, hi;
+        if (!tree_matches(ch, *build_tree(8, ch.p), 1e-9L) || !compile_orbit_fft(8, ch.p, false, hf, kOfBcWarps) ||
+            !compile_orbit_fft(8, ch.p, true, hi, kOfBcWarps)) {
+            pl->child_offt = false;
+            break;
+        }
+        upload_orbit_fft(hf, pl->ocfwd[c]);
+        upload_orbit_fft(hi, pl->ocinv[c]);
+        for (auto* t : {&pl->ocfwd[c], &pl->ocinv[c]}) t->desc.in_stride = t->desc.out_stride = 16 * static_cast<int64_t>(N);
+    }
+    for (int c = 0; c < 8 && !pl->child_offt; ++c) {
         Pipeline2Host hf, hi;
         if (!compile_pipeline2(*root.children[c], false, Shape2{}, hf) ||
             !compile_pipeline2(*root.children[c], true, Shape2{}, hi))
@@ -741,9 +764,16 @@ void run_two_level(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, v
     auto children = [&](Pipeline2Tables* tabs) {
         ck(cudaEventRecord(pl->cev[4], st), "event");
         for (int k = 0; k < 4; ++k) ck(cudaStreamWaitEvent(pl->cs[k], pl->cev[4], 0), "wait");
-        for (int c = 0; c < 8; ++c)
-            ck(launch_pipeline2(tabs[c].desc, s1 + 2 * c * m3, s2 + 2 * c * m3, batch, pl->cs[c & 3], pl->num_sms),
-               "child pipeline");
+        const bool inv = tabs == pl->cinv;
+        for (int c = 0; c < 8; ++c) {
+            if (pl->child_offt)
+                ck(launch_orbit_fft(inv ? pl->ocinv[c].desc : pl->ocfwd[c].desc, OF_C128, OF_C128, s1 + 2 * c * m3,
+                                    s2 + 2 * c * m3, batch, pl->cs[c & 3], pl->num_sms),
+                   "child orbit-FFT");
+            else
+                ck(launch_pipeline2(tabs[c].desc, s1 + 2 * c * m3, s2 + 2 * c * m3, batch, pl->cs[c & 3], pl->num_sms),
+                   "child pipeline");
+        }
         for (int k = 0; k < 4; ++k) {
             ck(cudaEventRecord(pl->cev[k], pl->cs[k]), "event");
             ck(cudaStreamWaitEvent(st, pl->cev[k], 0), "wait");
@@ -871,6 +901,10 @@ void fill_info(fcct_plan_s* pl) {
         in.flops_forward = algorithmic_flops(*pl->tree, false);
         in.flops_inverse = algorithmic_flops(*pl->tree, true);
         in.condition = pl->tree->condition;
+        if (pl->offt) {
+            in.exec_flops_forward = pl->ofwd.exec_flops;
+            in.exec_flops_inverse = pl->ofinv.exec_flops;
+        }
         int64_t bytes = 0;
         for (auto* pt : {&pl->fwd, &pl->inv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
@@ -882,9 +916,12 @@ void fill_info(fcct_plan_s* pl) {
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->rfwd, &pl->rinv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
-        for (int c = 0; c < 8; ++c)
+        for (int c = 0; c < 8; ++c) {
             for (auto* pt : {&pl->cfwd[c], &pl->cinv[c]})
                 for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+            for (auto* pt : {&pl->ocfwd[c], &pl->ocinv[c]})
+                for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+        }
         in.table_bytes = bytes;
     } else {
         in.levels = 0;

@@ -448,6 +448,9 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
     const int tid = threadIdx.x, warp = tid >> 5;
     const int64_t ntiles = (batch + TB - 1) / TB;
     constexpr uint32_t in_row = N * mode_bytes(MI), out_row = N * mode_bytes(MO);
+    // bytes between consecutive block rows (a strided batch: the two-level
+    // executor runs its eight children on 512-point slices of n = 16 blocks)
+    const int64_t in_stride = d.in_stride ? d.in_stride : in_row, out_stride = d.out_stride ? d.out_stride : out_row;
     for (int i = tid; i < kOfBcWarps * TMAX * 4; i += blockDim.x) {  // tiles beyond d.tmax: zero padding
         const int w = i / (TMAX * 4), rest = i - w * TMAX * 4;
         meta_s[i] = rest < d.tmax * 4 ? __ldg(d.meta + w * d.tmax * 4 + rest) : make_int2(0, -1);
@@ -463,9 +466,8 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
         const int64_t t0 = tile * TB;
         const int nv = nvalid_of(tile);
         mbar_arrive_expect_tx(bar + b, in_row * nv);
-        const char* src = static_cast<const char*>(in) + t0 * in_row;
-        for (int q = 0; q < nv; ++q)
-            tma_load_1d(buf(b) + q * C::XROW, src + static_cast<int64_t>(q) * in_row, in_row, bar + b);
+        const char* src = static_cast<const char*>(in) + t0 * in_stride;
+        for (int q = 0; q < nv; ++q) tma_load_1d(buf(b) + q * C::XROW, src + q * in_stride, in_row, bar + b);
     };
     if constexpr (DIR == 0) {
         if (tid == 0) {
@@ -494,8 +496,9 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                 named_arrive(1 + j % 3, kOfWarps * 32);  // tile j's spectrum-side buffer is ready
             } else {
                 named_sync(1 + j % 3, kOfWarps * 32);    // FFT(j) has filled y(j mod 3)
-                char* dst = static_cast<char*>(out) + tile * TB * static_cast<int64_t>(out_row);
-                base_change_lean<TMAX, G, OF_C128, MO>(tab, meta_w, nt_w, buf(j % 3), C::YROW, dst, out_row, r, k, nvalid);
+                char* dst = static_cast<char*>(out) + tile * TB * out_stride;
+                base_change_lean<TMAX, G, OF_C128, MO>(tab, meta_w, nt_w, buf(j % 3), C::YROW, dst, out_stride, r, k,
+                                                       nvalid);
                 named_arrive(4 + j % 3, kOfWarps * 32);  // y(j mod 3) may be refilled
             }
         }
@@ -514,8 +517,8 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                 fft_pass_group<NN, +1, TB, 1, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, TB);
                 named_sync(8, kOfFftThreads);
                 fft_pass_group<NN, +1, TB, 0, OF_C128, MO>(ft, Y, C::YROW, false,
-                                                          static_cast<char*>(out) + tile * TB * static_cast<int64_t>(out_row),
-                                                          out_row, true, nvalid);
+                                                          static_cast<char*>(out) + tile * TB * out_stride,
+                                                          out_stride, true, nvalid);
                 named_sync(8, kOfFftThreads);
                 if (ft == 0 && tile_of(j + 2) < ntiles) {  // f(j) becomes in(j + 2)
                     fence_proxy_async_smem();
@@ -523,12 +526,11 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                 }
             } else {
                 char* Y = buf(j % 3);
-                if (ft == 0 && tile_of(j + 2) < ntiles)
-                    prefetch_l2_bulk(static_cast<const char*>(in) + tile_of(j + 2) * TB * static_cast<int64_t>(in_row),
-                                     in_row * nvalid_of(tile_of(j + 2)));
+                if (ft < TB && tile_of(j + 2) < ntiles && ft < nvalid_of(tile_of(j + 2)))  // one row per thread
+                    prefetch_l2_bulk(static_cast<const char*>(in) + (tile_of(j + 2) * TB + ft) * in_stride, in_row);
                 if (j >= 3) named_sync(4 + j % 3, kOfWarps * 32);  // BC(j - 3) has read y(j mod 3)
-                fft_pass_group<NN, -1, TB, 0, MI, OF_C128>(ft, static_cast<const char*>(in) + tile * TB * static_cast<int64_t>(in_row),
-                                                          in_row, true, Y, C::YROW, false, nvalid);
+                fft_pass_group<NN, -1, TB, 0, MI, OF_C128>(ft, static_cast<const char*>(in) + tile * TB * in_stride,
+                                                          in_stride, true, Y, C::YROW, false, nvalid);
                 named_sync(8, kOfFftThreads);
                 fft_pass_group<NN, -1, TB, 1, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, TB);
                 named_sync(8, kOfFftThreads);

@@ -49,6 +49,8 @@ struct OrbitFftDesc {
     int groups = 1;   // 8-block m-tile groups per CTA tile (tile = 8 * groups blocks)
     int tmax = 0;     // table tiles per warp (<= the kernel's compile-time bound)
     int warps = kOfWarps;  // base-change warps the table is split over (16 phased, 12 specialised)
+    int64_t in_stride = 0;   // bytes between input block rows (0: dense rows); specialised kernel only
+    int64_t out_stride = 0;  // bytes between output block rows (0: dense rows)
     // B fragments of the orbit-block operator, [warp][tmax][32 lanes] (Re, Im):
     // lane l holds M[row 8 nt + l/4][col 4 kt + l%4] of its tile (0 outside the block)
     const double2* table = nullptr;
@@ -65,6 +67,9 @@ struct OrbitFftHost {
     std::vector<int32_t> meta;    // [warp][tmax][4][2]
     std::vector<int32_t> ntiles;  // [warp]
     int64_t tiles = 0;            // DMMA tiles (4 x 8) over all warps
+    // FP64-pipe flops per block: DMMA tiles (4 real products each, 8 blocks per
+    // m-tile, zero padding included) plus the radix-2 butterflies
+    double exec_flops() const;
 };
 
 struct PlanNode;

@@ -180,6 +180,22 @@ bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h, in
     return true;
 }
 
+double OrbitFftHost::exec_flops() const {
+    const double dmma = static_cast<double>(tiles) * 4.0 * 512.0 / 8.0;
+    // radix-2 line of n points: (n/2) log2 n butterflies of 2 complex add/sub
+    // (4 flops each) plus 6 flops per twiddle other than 1 and +-i
+    int lg = 0;
+    while ((1 << lg) < n) ++lg;
+    double twiddles = 0;
+    for (int half = n / 2; half >= 1; half /= 2)
+        for (int j = 0; j < half; ++j) {
+            const int e = j * (n / (2 * half));
+            if (e != 0 && 4 * e != n) twiddles += n / (2 * half);
+        }
+    const double line = (n / 2.0) * lg * 4.0 + 6.0 * twiddles;
+    return dmma + 3.0 * n * n * line;
+}
+
 namespace {
 
 using cd = std::complex<double>;
