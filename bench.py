@@ -472,6 +472,11 @@ def b200_arm(args):
         roof["executed_tflops"] = exec_tf
         roof["executed_frac_of_fp64_peak"] = exec_tf / peak_tf
         roof["hbm_frac"] = achieved_gbs / hbm
+        t_exec = max(bytes_fwd / (hbm * 1e9), info.exec_flops_forward * blocks / (peak_tf * 1e12))
+        roof["executed_t_star_over_t"] = t_exec / (fwd_ms / 1e3)
+        roof["note"] = ("achieved/frac use SURVEY.md 8(d)'s algorithmic flops of the stage-by-stage tree; the "
+                        "orbit-FFT executor telescopes the tree and issues executed_flops_per_launch, so against "
+                        "its own work the bound is max(HBM bytes, executed flops) -> executed_t_star_over_t")
     cpu = None
     if not args.no_cpu and world >= 1:
         threads = os.cpu_count() or 1
