@@ -434,7 +434,7 @@ def b200_arm(args):
     hbm = peaks.get("hbm_gbs", 6488.0)
     # the roofline of the pipe that executes the plan: the FP64 tensor pipe for
     # the DMMA executors (fp32 plans there keep fp64 arithmetic, complex64 I/O)
-    on_fp64_pipe = (not f32) or info.executor in (2, 4, 5)
+    on_fp64_pipe = (not f32) or info.executor in (2, 4, 5, 6)
     peak_tf = FP64_PEAK_TFLOPS if on_fp64_pipe else FP32_PEAK_TFLOPS
     achieved_tf = flops_fwd / (fwd_ms / 1e3) / 1e12
     achieved_gbs = bytes_fwd / (fwd_ms / 1e3) / 1e9
@@ -450,7 +450,9 @@ def b200_arm(args):
         "kernel": {0: "gemm_f64_kernel / gemm_f32_kernel (direct)", 1: "pipeline_kernel (tile interpreter)",
                    2: "pipeline2_kernel (FP64 tensor pipe)", 3: "gstage_* kernels (global multi-pass)",
                    4: "root pass + 8 x pipeline2_kernel (two-level, FP64 tensor pipe)",
-                   5: "orbit_fft_ws_kernel (S_n on the FP64 tensor pipe + radix-2 FFT, warp-specialised)"}[info.executor],
+                   5: "orbit_fft_ws_kernel (S_n on the FP64 tensor pipe + radix-2 FFT, warp-specialised)",
+                   6: "orbit16_base_kernel + fft_cube_kernel (two-pass orbit-FFT: S_n on the FP64 tensor pipe, "
+                      "then the n^3 FFT)"}[info.executor],
         "algorithmic_flops_per_launch": flops_fwd,
         "algorithmic_bytes_per_launch": bytes_fwd,
         "table_bytes_per_launch": table_bytes_fwd,

@@ -72,7 +72,8 @@ typedef struct {
     int executor;            /* 0 direct GEMM, 1 tile interpreter, 2 FP64-tensor-pipe
                                 pipeline, 3 global-memory multi-pass pipeline,
                                 4 two-level (n = 16: root pass + eight n = 8 pipelines),
-                                5 orbit-FFT (the radix tree telescoped to S_n + radix-2 FFT) */
+                                5 orbit-FFT (the radix tree telescoped to S_n + radix-2 FFT),
+                                6 two-pass orbit-FFT (n = 16: S_n pass + cube FFT pass) */
     double exec_flops_forward; /* flops the executor issues on the FP64 pipes per block (tensor-core
                                   tiles including their zero padding, plus FFT butterflies); 0 when
                                   equal to the algorithmic count */

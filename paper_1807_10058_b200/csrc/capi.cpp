@@ -16,6 +16,7 @@
 
 #include "../../include/fcct_gpu.h"
 #include "kernels.hpp"
+#include "orbit16.hpp"
 #include "orbit_fft.hpp"
 #include "plan.hpp"
 #include "plan_cache.hpp"
@@ -126,6 +127,33 @@ void upload_orbit_fft(const OrbitFftHost& h, OrbitFftTables& out) {
     d.meta = static_cast<const int2*>(bm->ptr);
     d.ntiles = static_cast<const int*>(bn->ptr);
     out.tiles = h.tiles;
+    out.exec_flops = h.exec_flops();
+}
+
+// Two-pass orbit-FFT executor (n = 16, orbit16.hpp).
+struct Orbit16Tables {
+    Orbit16Desc desc{};
+    std::vector<std::shared_ptr<DevBuf>> bufs;
+    double exec_flops = 0;
+};
+
+void upload_orbit16(const Orbit16Host& h, Orbit16Tables& out) {
+    out = Orbit16Tables{};
+    auto bt = upload(h.table), bm = upload(h.tile_meta), bo = upload(h.out_pos), bg = upload(h.gather),
+         bc = upload(h.chunk_slots), bz = upload(h.zperm);
+    out.bufs = {bt, bm, bo, bg, bc, bz};
+    Orbit16Desc& d = out.desc;
+    d.n = h.n;
+    d.N = h.N;
+    d.dir = h.dir;
+    d.nchunks = h.nchunks;
+    d.tmax = h.tmax;
+    d.table = static_cast<const double2*>(bt->ptr);
+    d.tile_meta = static_cast<const int*>(bm->ptr);
+    d.out_pos = static_cast<const int*>(bo->ptr);
+    d.gather = static_cast<const int*>(bg->ptr);
+    d.chunk_slots = static_cast<const int*>(bc->ptr);
+    d.zperm = static_cast<const int*>(bz->ptr);
     out.exec_flops = h.exec_flops();
 }
 
@@ -517,6 +545,8 @@ struct fcct_plan_s {
     PipelineTables fwd, inv;
     bool offt = false;  // orbit-FFT executor (telescoped radix tree, orbit_fft.hpp)
     OrbitFftTables ofwd, ofinv;
+    bool o16 = false;  // two-pass orbit-FFT executor (n = 16, orbit16.hpp)
+    Orbit16Tables o16fwd, o16inv;
     bool v2 = false;  // fp64 DMMA pipeline (tiling.hpp)
     Pipeline2Tables fwd2, inv2;
     bool two_level = false;  // n = 16: root pass + eight n = 8 child pipelines
@@ -743,6 +773,29 @@ void build_two_level(fcct_plan_s* pl) {
     pl->two_level = true;
 }
 
+// Two-pass orbit-FFT executor: forward S_n (pass A) then F_n (pass B) through a
+// complex128 scratch z; inverse F_n^{-1} then S_n^{-1} / n^3.
+void run_o16(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, void* out, int out_mode, int64_t batch,
+             cudaStream_t st) {
+    const size_t bytes = static_cast<size_t>(batch * cube(pl->n) * 16);
+    std::lock_guard<std::mutex> lock(pl->scratch_mu);
+    if (!pl->scratch0 || pl->scratch0->bytes < bytes) {
+        ck(cudaStreamSynchronize(st), "sync");
+        pl->scratch0 = std::make_shared<DevBuf>(bytes);
+    }
+    void* z = pl->scratch0->ptr;
+    if (!inverse) {
+        ck(launch_orbit16_base(pl->o16fwd.desc, in_mode, OF_C128, in, z, batch, st, pl->num_sms), "orbit base change");
+        ck(launch_fft_cube(pl->n, +1, OF_C128, out_mode, z, out, batch, pl->o16fwd.desc.zperm, st, pl->num_sms),
+           "cube FFT");
+    } else {
+        ck(launch_fft_cube(pl->n, -1, in_mode, OF_C128, in, z, batch, pl->o16inv.desc.zperm, st, pl->num_sms),
+           "cube FFT");
+        ck(launch_orbit16_base(pl->o16inv.desc, OF_C128, out_mode, z, out, batch, st, pl->num_sms), "orbit base change");
+    }
+    ck(cudaStreamSynchronize(st), "sync");  // the plan-owned scratch serialises calls on this path
+}
+
 // in_mode / out_mode of the natural side: 0 complex128, 1 complex64, 2 real f64, 3 real f32
 void run_two_level(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, void* out, int out_mode, int64_t batch,
                    cudaStream_t st) {
@@ -860,6 +913,17 @@ void build_fast_paths(fcct_plan_s* pl) {
     const bool f32 = pl->precision == FCCT_F32;
     if (f.empty() || f == "orbit") build_orbit_fft(pl);
     if (pl->offt) return;
+    if (f.empty() || f == "orbit") {  // n = 16: the two-pass orbit-FFT executor
+        pl->o16 = false;
+        Orbit16Host hf, hi;
+        if (pl->n == 16 && tree_matches(*pl->tree, *build_tree(pl->n, pl->p), 1e-9L) &&
+            compile_orbit16(pl->n, pl->p, false, hf) && compile_orbit16(pl->n, pl->p, true, hi)) {
+            upload_orbit16(hf, pl->o16fwd);
+            upload_orbit16(hi, pl->o16inv);
+            pl->o16 = true;
+            return;
+        }
+    }
     if (f.empty() || f == "v2") build_v2(pl);
     if (pl->v2) return;
     if (f.empty() || f == "two") build_two_level(pl);
@@ -891,7 +955,8 @@ void fill_info(fcct_plan_s* pl) {
     in.method = pl->radix ? FCCT_FAST : FCCT_DIRECT;
     in.precision = pl->precision;
     in.points = cube(pl->n);
-    in.executor = !pl->radix ? 0 : (pl->offt ? 5 : (pl->v2 ? 2 : (pl->two_level ? 4 : (pl->global ? 3 : 1))));
+    in.executor = !pl->radix ? 0
+                             : (pl->offt ? 5 : (pl->o16 ? 6 : (pl->v2 ? 2 : (pl->two_level ? 4 : (pl->global ? 3 : 1)))));
     const double N = static_cast<double>(in.points);
     if (pl->radix) {
         in.levels = tree_levels(pl->n);
@@ -905,12 +970,18 @@ void fill_info(fcct_plan_s* pl) {
             in.exec_flops_forward = pl->ofwd.exec_flops;
             in.exec_flops_inverse = pl->ofinv.exec_flops;
         }
+        if (pl->o16) {
+            in.exec_flops_forward = pl->o16fwd.exec_flops;
+            in.exec_flops_inverse = pl->o16inv.exec_flops;
+        }
         int64_t bytes = 0;
         for (auto* pt : {&pl->fwd, &pl->inv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->fwd2, &pl->inv2})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->ofwd, &pl->ofinv})
+            for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+        for (auto* pt : {&pl->o16fwd, &pl->o16inv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->gfwd, &pl->ginv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
@@ -976,6 +1047,10 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
     if (pl->radix) {
         if (pl->two_level) {
             run_two_level(pl, inverse, in, f32 ? 1 : 0, out, f32 ? 1 : 0, batch, st);
+            return;
+        }
+        if (pl->o16) {
+            run_o16(pl, inverse, in, f32 ? OF_C64 : OF_C128, out, f32 ? OF_C64 : OF_C128, batch, st);
             return;
         }
         if (pl->offt) {
@@ -1098,6 +1173,11 @@ void run_real(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t 
     if (pl->radix && pl->two_level) {
         const int cm = f32 ? 1 : 0, rm = f32 ? 3 : 2;
         run_two_level(pl, inverse, in, inverse ? cm : rm, out, inverse ? rm : cm, batch, st);
+        return;
+    }
+    if (pl->radix && pl->o16) {
+        const int cm = f32 ? OF_C64 : OF_C128, rm = f32 ? OF_R32 : OF_R64;
+        run_o16(pl, inverse, in, inverse ? cm : rm, out, inverse ? rm : cm, batch, st);
         return;
     }
     if (pl->radix && pl->offt) {
@@ -1504,6 +1584,17 @@ fcct_status fcct_plan_tree_stats(int n, double r, double s, double t, int64_t* t
 // Host emulation of the v2 DMMA pipeline tables (no GPU): applies the
 // compiled stages to `batch` blocks exactly as the kernel indexes them
 // (slots, lane-ordered fragments, unit lists). Tests the plan compiler on CPU.
+// Host emulation of the two-pass orbit-FFT executor's tables (n = 16, CPU tests).
+fcct_status fcct_debug_emulate_orbit16(int n, double r, double s, double t, int inverse, const double* in, double* out,
+                                       int64_t batch) {
+    return guarded([&] {
+        Orbit16Host h;
+        if (!compile_orbit16(n, Params{r, s, t}, inverse != 0, h))
+            throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by the two-pass orbit-FFT executor");
+        emulate_orbit16(h, in, out, batch);
+    });
+}
+
 // Host emulation of the orbit-FFT executor's compiled tables (CPU tests).
 fcct_status fcct_debug_emulate_orbit_fft(int n, double r, double s, double t, int inverse, const double* in,
                                          double* out, int64_t batch) {

@@ -1,0 +1,412 @@
+// Two-pass orbit-FFT executor (orbit16.hpp): pass A, the orbit-block base
+// change on the FP64 tensor pipe over gathered chunks of 8 blocks; pass B, the
+// radix-2 3D FFT per block.
+#include <algorithm>
+
+#include "device.cuh"
+#include "orbit16.hpp"
+#include "orbit_fft.hpp"
+
+namespace fcct {
+
+using namespace dev;
+
+namespace {
+
+__host__ __device__ constexpr int eb_of(int m) { return m == OF_C128 ? 16 : (m == OF_R32 ? 4 : 8); }
+
+template <int M>
+__device__ __forceinline__ void ld_el(const char* base, int idx, double& re, double& im) {
+    if constexpr (M == OF_C128) {
+        const double2 v = *reinterpret_cast<const double2*>(base + static_cast<size_t>(idx) * 16);
+        re = v.x;
+        im = v.y;
+    } else if constexpr (M == OF_C64) {
+        const float2 v = *reinterpret_cast<const float2*>(base + static_cast<size_t>(idx) * 8);
+        re = v.x;
+        im = v.y;
+    } else if constexpr (M == OF_R64) {
+        re = *reinterpret_cast<const double*>(base + static_cast<size_t>(idx) * 8);
+        im = 0.0;
+    } else {
+        re = *reinterpret_cast<const float*>(base + static_cast<size_t>(idx) * 4);
+        im = 0.0;
+    }
+}
+
+template <int M>
+__device__ __forceinline__ void st_el(char* base, int idx, double re, double im) {
+    if constexpr (M == OF_C128) {
+        *reinterpret_cast<double2*>(base + static_cast<size_t>(idx) * 16) = make_double2(re, im);
+    } else if constexpr (M == OF_C64) {
+        *reinterpret_cast<float2*>(base + static_cast<size_t>(idx) * 8) =
+            make_float2(static_cast<float>(re), static_cast<float>(im));
+    } else if constexpr (M == OF_R64) {
+        *reinterpret_cast<double*>(base + static_cast<size_t>(idx) * 8) = re;
+    } else {
+        *reinterpret_cast<float*>(base + static_cast<size_t>(idx) * 4) = static_cast<float>(re);
+    }
+}
+
+__device__ __forceinline__ double neg_hi16(double v) {
+    return __hiloint2double(__double2hiint(v) ^ static_cast<int>(0x80000000u), __double2loint(v));
+}
+
+// cp.async of 4, 8 or 16 bytes with zero fill when !valid
+template <int BYTES>
+__device__ __forceinline__ void cp_async_n(void* dst, const void* src, bool valid) {
+    const int sz = valid ? BYTES : 0;
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(sz) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES), "r"(sz)
+                     : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Pass A: base change. One persistent CTA per SM (16 warps), 8 blocks per
+// group, chunks of <= kO16Chunk member slots. Stage slot (s, b) at element
+// index s * 8 + (b ^ 2 (s & 3)): the quarter-warp of a fragment load (2 blocks
+// x 4 slots of one k-tile) touches 8 distinct bank groups for every element
+// size (16, 8 and 4 bytes), and the gather's 8 lanes of one slot too.
+// ---------------------------------------------------------------------------
+constexpr int kRingA = 4;  // operator tiles in flight per warp (L2 latency)
+
+template <int DIR, int MI, int MO>
+__global__ void __launch_bounds__(kO16Warps * 32, 1)
+    orbit16_base_kernel(const __grid_constant__ Orbit16Desc d, const void* __restrict__ in, void* __restrict__ out,
+                        int64_t batch) {
+    constexpr int SM = DIR == 0 ? MI : OF_C128;  // stage element (the z side is complex128)
+    constexpr int DM = DIR == 0 ? OF_C128 : MO;
+    constexpr int SEB = eb_of(SM);
+    constexpr bool REAL = SM == OF_R64 || SM == OF_R32;
+    constexpr int SBUF = kO16Chunk * 8 * SEB;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int N = d.N, tmax = d.tmax, nch = d.nchunks;
+    // shared: stage[2] | gather lists | tile metadata | output positions (all chunks, copied once)
+    char* stage = reinterpret_cast<char*>(smem);
+    int* g_s = reinterpret_cast<int*>(smem + 2 * SBUF);
+    int* tm_s = g_s + nch * kO16Chunk;
+    int* op_s = tm_s + nch * kO16Warps * tmax;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, k = lane & 3;
+    for (int i = tid; i < nch * kO16Chunk; i += blockDim.x) g_s[i] = __ldg(d.gather + i);
+    for (int i = tid; i < nch * kO16Warps * tmax; i += blockDim.x) tm_s[i] = __ldg(d.tile_meta + i);
+    for (int i = tid; i < nch * kO16Warps * tmax * 4; i += blockDim.x) op_s[i] = __ldg(d.out_pos + i);
+    const int64_t in_row = static_cast<int64_t>(N) * eb_of(DIR == 0 ? MI : OF_C128);
+    const int64_t out_row = static_cast<int64_t>(N) * eb_of(DM);
+    const int64_t ngroups = (batch + 7) / 8;
+    __syncthreads();
+    // stream of (group, chunk) work items of this CTA
+    const int64_t items = (ngroups > blockIdx.x ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0) * nch;
+    int gc = 0;            // chunk of the next gather
+    int64_t ggrp = blockIdx.x;  // group of the next gather
+    auto gather = [&](int64_t item) {
+        char* st = stage + (item & 1) * SBUF;
+        const int c = gc;
+        const int64_t grp = ggrp;
+        if (++gc == nch) {
+            gc = 0;
+            ggrp += gridDim.x;
+        }
+        // thread tid copies block b = tid & 7 of slots s = tid / 8 + 64 e: its
+        // block, source row and bank xor are fixed, only the slot advances
+        const int b = tid & 7, s0 = tid >> 3;
+        const int* gl = g_s + c * kO16Chunk + s0;
+        const bool bvalid = b < batch - grp * 8;
+        const char* srow = static_cast<const char*>(in) + (grp * 8 + (bvalid ? b : 0)) * in_row;
+        char* dst = st + (s0 * 8 + (b ^ (2 * (s0 & 3)))) * SEB;
+#pragma unroll
+        for (int e = 0; e < kO16Chunk * 8 / (kO16Warps * 32); ++e) {
+            const int p = gl[e * 64];
+            if (p >= 0 || (s0 & 3) != 0)  // slots of an unused k-tile are never read
+                cp_async_n<SEB>(dst + e * 64 * 8 * SEB, srow + static_cast<int64_t>(p > 0 ? p : 0) * SEB,
+                                p >= 0 && bvalid);
+        }
+        cp_async_commit();
+    };
+    // operator tile stream of this warp (chunk-major, tmax tiles per chunk),
+    // kRingA fragments in flight, loaded L2-only (they are read once per group)
+    int tc = 0, tt = 0;  // chunk / tile of the next fragment load
+    const double2* tbase = d.table + static_cast<size_t>(warp) * tmax * 32 + lane;
+    const double2* tp = tbase;
+    auto next_tile = [&]() {
+        const double2 v = __ldcg(tp);
+        tp += 32;
+        if (++tt == tmax) {  // warp-uniform: next chunk's segment of this warp, or wrap
+            tt = 0;
+            if (++tc == nch) {
+                tc = 0;
+                tp = tbase;
+            } else {
+                tp += static_cast<size_t>(kO16Warps - 1) * tmax * 32;
+            }
+        }
+        return v;
+    };
+    const int lane_off = (8 * k + (r ^ (2 * k))) * SEB;  // this lane's element of a k-tile's 32 slots
+    double2 ring[kRingA];
+#pragma unroll
+    for (int q = 0; q < kRingA; ++q) ring[q] = next_tile();
+    if (items > 0) gather(0);
+    int c = 0;
+    int64_t grp = blockIdx.x;
+    for (int64_t item = 0; item < items; ++item) {
+        if (item + 1 < items) {
+            gather(item + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();  // the chunk's stage is complete
+        const char* st = stage + (item & 1) * SBUF;
+        const int64_t nv = batch - grp * 8;
+        const bool live = r < nv;
+        char* d_row = static_cast<char*>(out) + (grp * 8 + r) * out_row;
+        const int* tm = tm_s + (c * kO16Warps + warp) * tmax;
+        const int* op = op_s + (c * kO16Warps + warp) * tmax * 4;
+        double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+        for (int t0 = 0; t0 < tmax; t0 += kRingA) {
+#pragma unroll
+            for (int q = 0; q < kRingA; ++q) {
+                const int t = t0 + q;
+                const double2 tb = ring[q];
+                ring[q] = next_tile();  // kRingA tiles ahead
+                const int m = tm[t];
+                if (!(m & (1 << 17))) continue;  // padding tile (warp-uniform)
+                double ar, ai;
+                ld_el<SM>(st + (m & 0xFFFF) * (32 * SEB) + lane_off, 0, ar, ai);
+                dmma884(cr0, cr1, ar, tb.x);
+                dmma884(ci0, ci1, ar, tb.y);
+                if constexpr (!REAL) {
+                    dmma884(cr0, cr1, neg_hi16(ai), tb.y);
+                    dmma884(ci0, ci1, ai, tb.x);
+                }
+                if (m & (1 << 16)) {  // chain end
+                    const int o = op[t * 4 + k];
+                    const int o0 = o & 0xFFFF, o1 = (o >> 16) & 0xFFFF;
+                    if (live && o0 != 0xFFFF) st_el<DM>(d_row, o0, cr0, ci0);
+                    if (live && o1 != 0xFFFF) st_el<DM>(d_row, o1, cr1, ci1);
+                    cr0 = cr1 = ci0 = ci1 = 0.0;
+                }
+            }
+        }
+        if (++c == nch) {
+            c = 0;
+            grp += gridDim.x;
+        }
+        __syncthreads();  // every warp is done with this stage before it is refilled
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pass B: 3D radix-2 FFT of NN^3 points per block. 256 threads, one line of
+// NN points per thread per pass; the tile is loaded by cp.async (complex128
+// input) into the (k ^ j)-swizzled layout, the block after next is prefetched.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr double c16(int e) {
+    switch (e & 15) {
+        case 0: return 1.0;
+        case 1: return 0.92387953251128675613;
+        case 2: return 0.70710678118654752440;
+        case 3: return 0.38268343236508977173;
+        case 4: return 0.0;
+        case 5: return -0.38268343236508977173;
+        case 6: return -0.70710678118654752440;
+        case 7: return -0.92387953251128675613;
+        case 8: return -1.0;
+        case 9: return -0.92387953251128675613;
+        case 10: return -0.70710678118654752440;
+        case 11: return -0.38268343236508977173;
+        case 12: return 0.0;
+        case 13: return 0.38268343236508977173;
+        case 14: return 0.70710678118654752440;
+        default: return 0.92387953251128675613;
+    }
+}
+__host__ __device__ constexpr int brev(int q, int nn) {
+    int r = 0;
+    for (int b = 1; b < nn; b <<= 1) {
+        r = (r << 1) | (q & 1);
+        q >>= 1;
+    }
+    return r;
+}
+template <int NN, int SIGN>
+__device__ __forceinline__ double2 twid(double2 d, int e) {
+    if (e == 0) return d;
+    if (4 * e == NN) return SIGN > 0 ? make_double2(-d.y, d.x) : make_double2(d.y, -d.x);
+    const double c = c16(e * (16 / NN)), s = SIGN * c16(e * (16 / NN) - 4);
+    return make_double2(fma(d.x, c, -d.y * s), fma(d.x, s, d.y * c));
+}
+template <int NN, int SIGN>
+__device__ __forceinline__ void fft_line16(double2 (&v)[NN]) {
+#pragma unroll
+    for (int half = NN / 2; half >= 1; half >>= 1) {
+#pragma unroll
+        for (int st = 0; st < NN; st += 2 * half) {
+#pragma unroll
+            for (int j = 0; j < half; ++j) {
+                const double2 a = v[st + j], b = v[st + j + half];
+                v[st + j] = make_double2(a.x + b.x, a.y + b.y);
+                v[st + j + half] = twid<NN, SIGN>(make_double2(a.x - b.x, a.y - b.y), j * (NN / (2 * half)));
+            }
+        }
+    }
+    double2 t[NN];
+#pragma unroll
+    for (int q = 0; q < NN; ++q) t[q] = v[brev(q, NN)];
+#pragma unroll
+    for (int q = 0; q < NN; ++q) v[q] = t[q];
+}
+
+constexpr int kFftThreads = 256;
+
+template <int NN, int SIGN, int MI, int MO>
+__global__ void __launch_bounds__(kFftThreads, 1)
+    fft_cube_kernel(const void* __restrict__ in, void* __restrict__ out, int64_t batch, const int* __restrict__ zperm) {
+    constexpr int N = NN * NN * NN, LINES = NN * NN;
+    static_assert(LINES == kFftThreads, "one line per thread per pass");
+    extern __shared__ __align__(128) unsigned char smem[];
+    double2* buf = reinterpret_cast<double2*>(smem);  // [2][N], swizzled
+    int* zp = reinterpret_cast<int*>(smem + 2 * N * 16);  // orbit-order index of each natural position
+    for (int a = threadIdx.x; a < N; a += kFftThreads) zp[a] = __ldg(zperm + a);
+    __syncthreads();
+    const int tid = threadIdx.x, hi = tid / NN, lo = tid % NN;
+    auto swz = [](int i, int j, int k) { return (i * NN + j) * NN + (k ^ (j & (NN - 1))); };
+    auto load = [&](int b, int64_t blk) {  // natural rows -> swizzled tile
+        double2* X = buf + b * N;
+        const char* src = static_cast<const char*>(in) + blk * static_cast<int64_t>(N) * eb_of(MI);
+        for (int a = tid; a < N; a += kFftThreads) {
+            const int k = a % NN, j = (a / NN) % NN, i = a / (NN * NN);
+            if constexpr (SIGN > 0) {  // forward: z in orbit order
+                cp_async_n<16>(X + swz(i, j, k), src + static_cast<int64_t>(zp[a]) * 16, true);
+            } else if constexpr (MI == OF_C128) {
+                cp_async_n<16>(X + swz(i, j, k), src + static_cast<int64_t>(a) * 16, true);
+            } else {
+                double re, im;
+                ld_el<MI>(src, a, re, im);
+                X[swz(i, j, k)] = make_double2(re, im);
+            }
+        }
+        cp_async_commit();
+    };
+    int it = 0;
+    if (static_cast<int64_t>(blockIdx.x) < batch) load(0, blockIdx.x);
+    for (int64_t blk = blockIdx.x; blk < batch; blk += gridDim.x, ++it) {
+        const int64_t nx = blk + gridDim.x;
+        if (nx < batch) {
+            load((it + 1) & 1, nx);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        double2* X = buf + (it & 1) * N;
+        double2 v[NN];
+        // k axis: line (i, j) = (hi, lo)
+#pragma unroll
+        for (int x = 0; x < NN; ++x) v[x] = X[swz(hi, lo, x)];
+        fft_line16<NN, SIGN>(v);
+#pragma unroll
+        for (int x = 0; x < NN; ++x) X[swz(hi, lo, x)] = v[x];
+        __syncthreads();
+        // j axis: line (i, k) = (hi, lo)
+#pragma unroll
+        for (int x = 0; x < NN; ++x) v[x] = X[swz(hi, x, lo)];
+        fft_line16<NN, SIGN>(v);
+#pragma unroll
+        for (int x = 0; x < NN; ++x) X[swz(hi, x, lo)] = v[x];
+        __syncthreads();
+        // i axis: line (j, k) = (hi, lo), stored to HBM (lanes vary k: coalesced)
+#pragma unroll
+        for (int x = 0; x < NN; ++x) v[x] = X[swz(x, hi, lo)];
+        fft_line16<NN, SIGN>(v);
+        char* dst = static_cast<char*>(out) + blk * static_cast<int64_t>(N) * eb_of(MO);
+#pragma unroll
+        for (int x = 0; x < NN; ++x) {
+            const int a = (x * NN + hi) * NN + lo;
+            st_el<MO>(dst, SIGN > 0 ? a : zp[a], v[x].x, v[x].y);  // inverse: z in orbit order
+        }
+        __syncthreads();  // the buffer is refilled two blocks later
+    }
+}
+
+template <int DIR, int MI, int MO>
+cudaError_t launch_a(const Orbit16Desc& d, const void* in, void* out, int64_t batch, cudaStream_t st, int num_sms) {
+    constexpr int SM = DIR == 0 ? MI : OF_C128;
+    const int smem = 2 * kO16Chunk * 8 * eb_of(SM) + d.nchunks * kO16Chunk * 4 + d.nchunks * kO16Warps * d.tmax * 5 * 4;
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    auto kern = orbit16_base_kernel<DIR, MI, MO>;
+    static thread_local int prepared = -1;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (prepared != dev) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        prepared = dev;
+    }
+    const int64_t groups = (batch + 7) / 8;
+    kern<<<static_cast<unsigned>(std::min<int64_t>(groups, num_sms)), kO16Warps * 32, smem, st>>>(d, in, out, batch);
+    return cudaGetLastError();
+}
+
+template <int NN, int SIGN, int MI, int MO>
+cudaError_t launch_b(const void* in, void* out, int64_t batch, const int* zperm, cudaStream_t st, int num_sms) {
+    const int smem = 2 * NN * NN * NN * 16 + NN * NN * NN * 4;
+    auto kern = fft_cube_kernel<NN, SIGN, MI, MO>;
+    static thread_local int prepared = -1;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (prepared != dev) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        prepared = dev;
+    }
+    kern<<<static_cast<unsigned>(std::min<int64_t>(batch, num_sms)), kFftThreads, smem, st>>>(in, out, batch, zperm);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_orbit16_base(const Orbit16Desc& d, int in_mode, int out_mode, const void* in, void* out,
+                                int64_t batch, cudaStream_t st, int num_sms) {
+    if (batch <= 0) return cudaSuccess;
+    if (d.tmax % kRingA != 0) return cudaErrorInvalidValue;  // the ring stays chunk-aligned
+    if (d.dir == 0 && out_mode == OF_C128) {
+        switch (in_mode) {
+            case OF_C128: return launch_a<0, OF_C128, OF_C128>(d, in, out, batch, st, num_sms);
+            case OF_C64: return launch_a<0, OF_C64, OF_C128>(d, in, out, batch, st, num_sms);
+            case OF_R64: return launch_a<0, OF_R64, OF_C128>(d, in, out, batch, st, num_sms);
+            case OF_R32: return launch_a<0, OF_R32, OF_C128>(d, in, out, batch, st, num_sms);
+        }
+    }
+    if (d.dir == 1 && in_mode == OF_C128) {
+        switch (out_mode) {
+            case OF_C128: return launch_a<1, OF_C128, OF_C128>(d, in, out, batch, st, num_sms);
+            case OF_C64: return launch_a<1, OF_C128, OF_C64>(d, in, out, batch, st, num_sms);
+            case OF_R64: return launch_a<1, OF_C128, OF_R64>(d, in, out, batch, st, num_sms);
+            case OF_R32: return launch_a<1, OF_C128, OF_R32>(d, in, out, batch, st, num_sms);
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_fft_cube(int n, int sign, int in_mode, int out_mode, const void* in, void* out, int64_t batch,
+                            const int* zperm, cudaStream_t st, int num_sms) {
+    if (batch <= 0) return cudaSuccess;
+    if (n != 16) return cudaErrorInvalidValue;
+    // forward: z (complex128) -> y (c128 / c64); inverse: y (c128 / c64) -> z (complex128)
+    if (sign > 0 && in_mode == OF_C128) {
+        if (out_mode == OF_C128) return launch_b<16, +1, OF_C128, OF_C128>(in, out, batch, zperm, st, num_sms);
+        if (out_mode == OF_C64) return launch_b<16, +1, OF_C128, OF_C64>(in, out, batch, zperm, st, num_sms);
+    }
+    if (sign < 0 && out_mode == OF_C128) {
+        if (in_mode == OF_C128) return launch_b<16, -1, OF_C128, OF_C128>(in, out, batch, zperm, st, num_sms);
+        if (in_mode == OF_C64) return launch_b<16, -1, OF_C64, OF_C128>(in, out, batch, zperm, st, num_sms);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace fcct

@@ -349,11 +349,15 @@ __device__ __forceinline__ void base_change_lean(const double2 (&tab)[TMAX], con
         char* d_row = dst + (8 * g + r) * drow;
         const bool live = 8 * g + r < nvalid;
         double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+        int2 mn = meta_w[k];
 #pragma unroll
         for (int t = 0; t < TMAX; ++t) {
             if (t >= nt_w) break;  // warp-uniform
-            // no fragment prefetch: with 25 register-resident tiles it spills (measured slower)
-            const int2 m = meta_w[t * 4 + k];
+            // the next tile's metadata is loaded one step ahead (2 registers), so the
+            // fragment load does not wait behind a dependent metadata load; a full
+            // fragment prefetch spills with 25 register-resident tiles (measured slower)
+            const int2 m = mn;
+            if (t + 1 < TMAX) mn = meta_w[(t + 1) * 4 + k];
             double ar, ai;
             load_elem<SM>(s_row, m.x & 0xFFFF, ar, ai);
             dmma884(cr0, cr1, ar, tab[t].x);

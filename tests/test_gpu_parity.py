@@ -441,10 +441,11 @@ def test_real_io_fused_matches_complex_path(cuda, oracle_mod, n, method, precisi
 
 
 @pytest.mark.parametrize("p", [SkewParams(0.21, 0.055, 0.4), SkewParams(0.37, 0.61, 0.085)])
-def test_n16_two_level_noncanonical(cuda, oracle_mod, p):
-    """n = 16 on the two-level executor (root pass + eight n = 8 DMMA child
-    pipelines, fcct_plan_info_t.executor == 4) for non-canonical offsets,
+def test_n16_two_level_noncanonical(cuda, oracle_mod, p, monkeypatch):
+    """n = 16 on the two-level executor (root pass + eight n = 8 child
+    transforms, fcct_plan_info_t.executor == 4) for non-canonical offsets,
     against the FFT / orbit-route oracle."""
+    monkeypatch.setenv("FCCT_PIPELINE", "two")
     n = 16
     plan = build_plan(n, p)
     assert plan.info.executor == 4
@@ -461,7 +462,8 @@ def test_n16_two_level_noncanonical(cuda, oracle_mod, p):
     assert rel(back, x) <= 2e-11  # measured 5.1e-12 (same floor; the reference's bar is 1e-8)
 
 
-def test_n16_two_level_f32_and_host(cuda, oracle_mod):
+def test_n16_two_level_f32_and_host(cuda, oracle_mod, monkeypatch):
+    monkeypatch.setenv("FCCT_PIPELINE", "two")
     n = 16
     plan = build_plan(n, CANON, precision="f32")
     assert plan.info.executor == 4
@@ -531,3 +533,40 @@ def test_orbit_fft_full_batch_properties(cuda, oracle_mod):
     ya = plan.apply_values(2.0 * x[:1024] - 0.5j * x[1024:2048])
     lin = 2.0 * y[:1024] - 0.5j * y[1024:2048]
     assert float(torch.linalg.norm(ya - lin) / torch.linalg.norm(lin)) <= F64_TOL
+
+
+@pytest.mark.parametrize("p", [CANON, SkewParams(0.21, 0.055, 0.4), SkewParams(0.37, 0.61, 0.085)])
+def test_n16_two_pass_orbit_fft(cuda, oracle_mod, p):
+    """n = 16 on the two-pass orbit-FFT executor (executor 6: S_16(p) on the
+    FP64 tensor pipe over gathered 8-block chunks, then the 16^3 FFT) against
+    the FFT / orbit-route oracle, ragged batch; fp32 I/O; fused real I/O
+    bitwise equal to the complex path; host buffers; acceptance #7 node rows."""
+    n = 16
+    plan = build_plan(n, p)
+    assert plan.info.executor == 6
+    route = oracle_mod.OrbitRoute(n, tup(p))
+    x = rand_batch(n, 11, seed=61)  # ragged: 8 + 3 blocks
+    y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values
+    y_ref = route.forward(x)
+    assert rel(y.cpu().numpy(), y_ref) <= F64_TOL
+    xb = inverse_apply(plan, Spectrum(n, p, torch.from_numpy(y_ref).to(cuda))).data
+    assert rel(xb.cpu().numpy(), route.inverse(y_ref)) <= F64_TOL
+    back = inverse_apply(plan, Spectrum(n, p, y)).data
+    assert rel(back.cpu().numpy(), x) <= F64_TOL
+    nodes = np.random.default_rng(777).integers(0, n**3, 16)
+    direct = oracle_mod.symmetrized_rows(n, tup(p), nodes, x[0])
+    assert np.abs(y.cpu().numpy()[0, nodes] - direct).max() / np.abs(direct).max() <= 1e-12
+    # host buffers: bitwise the device path
+    assert torch.equal(plan.apply_values(torch.from_numpy(x)), y.cpu())
+    # real samples in / real parts out, fused: bitwise the complex path
+    xr = torch.from_numpy(x.real.copy()).to(cuda)
+    yr = plan.apply_values(xr)
+    assert torch.equal(yr, plan.apply_values(torch.complex(xr, torch.zeros_like(xr))))
+    assert torch.equal(plan._run(yr, True, real_out=True), plan._run(yr, True).real.contiguous())
+    # fp32 I/O (complex64 in HBM, fp64 arithmetic)
+    p32 = build_plan(n, p, precision="f32")
+    assert p32.info.executor == 6
+    y32 = fast_apply(p32, SignalTensor(n, torch.from_numpy(x).to(torch.complex64).to(cuda))).values
+    assert rel(y32.cpu().numpy(), y_ref) <= F32_TOL
+    b32 = inverse_apply(p32, Spectrum(n, p, y32)).data
+    assert rel(b32.cpu().numpy(), x) <= F32_TOL

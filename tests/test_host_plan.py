@@ -112,6 +112,27 @@ def test_orbit_fft_tables_emulated(n, p):
     assert np.linalg.norm(xi - xr) / np.linalg.norm(xr) < 1e-13
 
 
+@pytest.mark.parametrize("p", [CANON, P2])
+def test_orbit16_tables_emulated(p):
+    """The two-pass orbit-FFT executor (n = 16): chunked orbit-block tables of
+    pass A emulated as the kernel indexes them (gather slots, per-warp tiles,
+    chain ends, natural output positions) plus the cube FFT, against the FFT /
+    orbit-route oracle (the n = 16 dense oracle is too slow for a CPU test)."""
+    n = 16
+    L = _capi.lib()
+    rng = np.random.default_rng(16)
+    x = rng.uniform(-1, 1, (2, n**3)) + 1j * rng.uniform(-1, 1, (2, n**3))
+    pt = (p.r, p.s, p.t)
+    route = oracle.OrbitRoute(n, pt)
+    y = np.zeros_like(x)
+    assert L.fcct_debug_emulate_orbit16(n, *pt, 0, x.ctypes.data, y.ctypes.data, 2) == 0
+    yr = route.forward(x)
+    assert np.linalg.norm(y - yr) / np.linalg.norm(yr) < 1e-13
+    xi = np.zeros_like(x)
+    assert L.fcct_debug_emulate_orbit16(n, *pt, 1, yr.ctypes.data, xi.ctypes.data, 2) == 0
+    assert np.linalg.norm(xi - x) / np.linalg.norm(x) < 1e-13
+
+
 def test_compiled_layouts_are_conflict_free_inside():
     # Only the first stage (natural layout from the TMA load) and the last stage
     # (natural output layout) may see shared-memory bank conflicts.
