@@ -262,21 +262,25 @@ __device__ __forceinline__ void fft_line16(double2 (&v)[NN]) {
 constexpr int kFftThreads = 256;
 
 template <int NN, int SIGN, int MI, int MO>
-__global__ void __launch_bounds__(kFftThreads, 1)
+__global__ void __launch_bounds__(kFftThreads, 2)
     fft_cube_kernel(const void* __restrict__ in, void* __restrict__ out, int64_t batch, const int* __restrict__ zperm) {
     constexpr int N = NN * NN * NN, LINES = NN * NN;
     static_assert(LINES == kFftThreads, "one line per thread per pass");
+    // one 64 KB tile and the orbit-order permutation per CTA, two CTAs per SM:
+    // the block after this one is prefetched into L2 while the tile is transformed
     extern __shared__ __align__(128) unsigned char smem[];
-    double2* buf = reinterpret_cast<double2*>(smem);  // [2][N], swizzled
-    int* zp = reinterpret_cast<int*>(smem + 2 * N * 16);  // orbit-order index of each natural position
-    for (int a = threadIdx.x; a < N; a += kFftThreads) zp[a] = __ldg(zperm + a);
-    __syncthreads();
+    double2* X = reinterpret_cast<double2*>(smem);
+    int* zp = reinterpret_cast<int*>(smem + N * 16);
     const int tid = threadIdx.x, hi = tid / NN, lo = tid % NN;
+    for (int a = tid; a < N; a += kFftThreads) zp[a] = __ldg(zperm + a);
+    __syncthreads();
     auto swz = [](int i, int j, int k) { return (i * NN + j) * NN + (k ^ (j & (NN - 1))); };
-    auto load = [&](int b, int64_t blk) {  // natural rows -> swizzled tile
-        double2* X = buf + b * N;
-        const char* src = static_cast<const char*>(in) + blk * static_cast<int64_t>(N) * eb_of(MI);
-        for (int a = tid; a < N; a += kFftThreads) {
+    constexpr int64_t in_row = int64_t{N} * eb_of(MI), out_row = int64_t{N} * eb_of(MO);
+    for (int64_t blk = blockIdx.x; blk < batch; blk += gridDim.x) {
+        const int64_t nx = blk + gridDim.x;
+        if (tid == 0 && nx < batch) prefetch_l2_bulk(static_cast<const char*>(in) + nx * in_row, static_cast<uint32_t>(in_row));
+        const char* src = static_cast<const char*>(in) + blk * in_row;
+        for (int a = tid; a < N; a += kFftThreads) {  // natural (or orbit-ordered z) -> swizzled tile
             const int k = a % NN, j = (a / NN) % NN, i = a / (NN * NN);
             if constexpr (SIGN > 0) {  // forward: z in orbit order
                 cp_async_n<16>(X + swz(i, j, k), src + static_cast<int64_t>(zp[a]) * 16, true);
@@ -289,19 +293,8 @@ __global__ void __launch_bounds__(kFftThreads, 1)
             }
         }
         cp_async_commit();
-    };
-    int it = 0;
-    if (static_cast<int64_t>(blockIdx.x) < batch) load(0, blockIdx.x);
-    for (int64_t blk = blockIdx.x; blk < batch; blk += gridDim.x, ++it) {
-        const int64_t nx = blk + gridDim.x;
-        if (nx < batch) {
-            load((it + 1) & 1, nx);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+        cp_async_wait<0>();
         __syncthreads();
-        double2* X = buf + (it & 1) * N;
         double2 v[NN];
         // k axis: line (i, j) = (hi, lo)
 #pragma unroll
@@ -321,13 +314,13 @@ __global__ void __launch_bounds__(kFftThreads, 1)
 #pragma unroll
         for (int x = 0; x < NN; ++x) v[x] = X[swz(x, hi, lo)];
         fft_line16<NN, SIGN>(v);
-        char* dst = static_cast<char*>(out) + blk * static_cast<int64_t>(N) * eb_of(MO);
+        char* dst = static_cast<char*>(out) + blk * out_row;
 #pragma unroll
         for (int x = 0; x < NN; ++x) {
             const int a = (x * NN + hi) * NN + lo;
             st_el<MO>(dst, SIGN > 0 ? a : zp[a], v[x].x, v[x].y);  // inverse: z in orbit order
         }
-        __syncthreads();  // the buffer is refilled two blocks later
+        __syncthreads();  // the tile is refilled by the next block
     }
 }
 
@@ -353,7 +346,7 @@ cudaError_t launch_a(const Orbit16Desc& d, const void* in, void* out, int64_t ba
 
 template <int NN, int SIGN, int MI, int MO>
 cudaError_t launch_b(const void* in, void* out, int64_t batch, const int* zperm, cudaStream_t st, int num_sms) {
-    const int smem = 2 * NN * NN * NN * 16 + NN * NN * NN * 4;
+    const int smem = NN * NN * NN * (16 + 4);
     auto kern = fft_cube_kernel<NN, SIGN, MI, MO>;
     static thread_local int prepared = -1;
     int dev = 0;
@@ -364,7 +357,8 @@ cudaError_t launch_b(const void* in, void* out, int64_t batch, const int* zperm,
         if (e != cudaSuccess) return e;
         prepared = dev;
     }
-    kern<<<static_cast<unsigned>(std::min<int64_t>(batch, num_sms)), kFftThreads, smem, st>>>(in, out, batch, zperm);
+    kern<<<static_cast<unsigned>(std::min<int64_t>(batch, 2 * static_cast<int64_t>(num_sms))), kFftThreads, smem, st>>>(
+        in, out, batch, zperm);
     return cudaGetLastError();
 }
 
