@@ -434,7 +434,7 @@ def b200_arm(args):
     hbm = peaks.get("hbm_gbs", 6488.0)
     # the roofline of the pipe that executes the plan: the FP64 tensor pipe for
     # the DMMA executors (fp32 plans there keep fp64 arithmetic, complex64 I/O)
-    on_fp64_pipe = (not f32) or info.executor in (2, 4, 5, 6)
+    on_fp64_pipe = (not f32) or info.executor in (2, 4, 5, 6, 7)
     peak_tf = FP64_PEAK_TFLOPS if on_fp64_pipe else FP32_PEAK_TFLOPS
     achieved_tf = flops_fwd / (fwd_ms / 1e3) / 1e12
     achieved_gbs = bytes_fwd / (fwd_ms / 1e3) / 1e9
@@ -452,7 +452,9 @@ def b200_arm(args):
                    4: "root pass + 8 x pipeline2_kernel (two-level, FP64 tensor pipe)",
                    5: "orbit_fft_ws_kernel (S_n on the FP64 tensor pipe + radix-2 FFT, warp-specialised)",
                    6: "orbit16_base_kernel + fft_cube_kernel (two-pass orbit-FFT: S_n on the FP64 tensor pipe, "
-                      "then the n^3 FFT)"}[info.executor],
+                      "then the n^3 FFT)",
+                   7: "orbit_big_s_kernel + line_fft_kernel (large-n orbit-FFT: S_n then three line-FFT passes)"}[
+                       info.executor],
         "algorithmic_flops_per_launch": flops_fwd,
         "algorithmic_bytes_per_launch": bytes_fwd,
         "table_bytes_per_launch": table_bytes_fwd,

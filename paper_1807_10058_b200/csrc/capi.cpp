@@ -17,6 +17,7 @@
 #include "../../include/fcct_gpu.h"
 #include "kernels.hpp"
 #include "orbit16.hpp"
+#include "orbit_big.hpp"
 #include "orbit_fft.hpp"
 #include "plan.hpp"
 #include "plan_cache.hpp"
@@ -154,6 +155,32 @@ void upload_orbit16(const Orbit16Host& h, Orbit16Tables& out) {
     d.gather = static_cast<const int*>(bg->ptr);
     d.chunk_slots = static_cast<const int*>(bc->ptr);
     d.zperm = static_cast<const int*>(bz->ptr);
+    out.exec_flops = h.exec_flops();
+}
+
+// Large-n orbit-FFT executor (n = 32, 64, orbit_big.hpp).
+struct OrbitBigTables {
+    OrbitBigDesc desc{};
+    std::vector<std::shared_ptr<DevBuf>> bufs;
+    double exec_flops = 0;
+};
+
+void upload_orbit_big(const OrbitBigHost& h, OrbitBigTables& out) {
+    out = OrbitBigTables{};
+    auto b1 = upload(h.row_orbit), b2 = upload(h.row_index), b3 = upload(h.orbit_off), b4 = upload(h.coef_off),
+         b5 = upload(h.members), b6 = upload(h.coef);
+    out.bufs = {b1, b2, b3, b4, b5, b6};
+    OrbitBigDesc& d = out.desc;
+    d.n = h.n;
+    d.N = h.N;
+    d.dir = h.dir;
+    d.rows = h.N;
+    d.row_orbit = static_cast<const int*>(b1->ptr);
+    d.row_index = static_cast<const int*>(b2->ptr);
+    d.orbit_off = static_cast<const int*>(b3->ptr);
+    d.coef_off = static_cast<const int64_t*>(b4->ptr);
+    d.members = static_cast<const int*>(b5->ptr);
+    d.coef = static_cast<const double2*>(b6->ptr);
     out.exec_flops = h.exec_flops();
 }
 
@@ -547,6 +574,8 @@ struct fcct_plan_s {
     OrbitFftTables ofwd, ofinv;
     bool o16 = false;  // two-pass orbit-FFT executor (n = 16, orbit16.hpp)
     Orbit16Tables o16fwd, o16inv;
+    bool obig = false;  // large-n orbit-FFT executor (n = 32, 64, fp64, orbit_big.hpp)
+    OrbitBigTables obfwd, obinv;
     bool v2 = false;  // fp64 DMMA pipeline (tiling.hpp)
     Pipeline2Tables fwd2, inv2;
     bool two_level = false;  // n = 16: root pass + eight n = 8 child pipelines
@@ -923,6 +952,19 @@ void build_fast_paths(fcct_plan_s* pl) {
             pl->o16 = true;
             return;
         }
+        pl->obig = false;
+        if ((pl->n == 32 || pl->n == 64) && !f32 && tree_matches(*pl->tree, *build_tree(pl->n, pl->p), 1e-9L)) {
+            OrbitBigHost h;
+            if (compile_orbit_big(pl->n, pl->p, false, h)) {
+                upload_orbit_big(h, pl->obfwd);
+                h = OrbitBigHost{};
+                if (compile_orbit_big(pl->n, pl->p, true, h)) {
+                    upload_orbit_big(h, pl->obinv);
+                    pl->obig = true;
+                    return;
+                }
+            }
+        }
     }
     if (f.empty() || f == "v2") build_v2(pl);
     if (pl->v2) return;
@@ -956,7 +998,9 @@ void fill_info(fcct_plan_s* pl) {
     in.precision = pl->precision;
     in.points = cube(pl->n);
     in.executor = !pl->radix ? 0
-                             : (pl->offt ? 5 : (pl->o16 ? 6 : (pl->v2 ? 2 : (pl->two_level ? 4 : (pl->global ? 3 : 1)))));
+                             : (pl->offt ? 5
+                                : (pl->o16 ? 6
+                                : (pl->obig ? 7 : (pl->v2 ? 2 : (pl->two_level ? 4 : (pl->global ? 3 : 1))))));
     const double N = static_cast<double>(in.points);
     if (pl->radix) {
         in.levels = tree_levels(pl->n);
@@ -974,6 +1018,10 @@ void fill_info(fcct_plan_s* pl) {
             in.exec_flops_forward = pl->o16fwd.exec_flops;
             in.exec_flops_inverse = pl->o16inv.exec_flops;
         }
+        if (pl->obig) {
+            in.exec_flops_forward = pl->obfwd.exec_flops;
+            in.exec_flops_inverse = pl->obinv.exec_flops;
+        }
         int64_t bytes = 0;
         for (auto* pt : {&pl->fwd, &pl->inv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
@@ -982,6 +1030,8 @@ void fill_info(fcct_plan_s* pl) {
         for (auto* pt : {&pl->ofwd, &pl->ofinv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->o16fwd, &pl->o16inv})
+            for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+        for (auto* pt : {&pl->obfwd, &pl->obinv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->gfwd, &pl->ginv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
@@ -1051,6 +1101,28 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
         }
         if (pl->o16) {
             run_o16(pl, inverse, in, f32 ? OF_C64 : OF_C128, out, f32 ? OF_C64 : OF_C128, batch, st);
+            return;
+        }
+        if (pl->obig) {  // S pass + three line-FFT passes through a plan-owned scratch
+            const size_t bytes = static_cast<size_t>(batch * cube(pl->n) * 16);
+            std::lock_guard<std::mutex> lock(pl->scratch_mu);
+            if (!pl->scratch0 || pl->scratch0->bytes < bytes) {
+                ck(cudaStreamSynchronize(st), "sync");
+                pl->scratch0 = std::make_shared<DevBuf>(bytes);
+            }
+            void* z = pl->scratch0->ptr;
+            if (!inverse) {
+                ck(launch_orbit_big_s(pl->obfwd.desc, in, z, batch, st), "orbit base change");
+                ck(launch_line_fft(pl->n, 2, +1, z, z, batch, st), "line FFT");
+                ck(launch_line_fft(pl->n, 1, +1, z, z, batch, st), "line FFT");
+                ck(launch_line_fft(pl->n, 0, +1, z, out, batch, st), "line FFT");
+            } else {
+                ck(launch_line_fft(pl->n, 0, -1, in, z, batch, st), "line FFT");
+                ck(launch_line_fft(pl->n, 1, -1, z, z, batch, st), "line FFT");
+                ck(launch_line_fft(pl->n, 2, -1, z, z, batch, st), "line FFT");
+                ck(launch_orbit_big_s(pl->obinv.desc, z, out, batch, st), "orbit base change");
+            }
+            ck(cudaStreamSynchronize(st), "sync");  // the plan-owned scratch serialises calls on this path
             return;
         }
         if (pl->offt) {

@@ -1,0 +1,144 @@
+// Large-n orbit-FFT executor (orbit_big.hpp): the orbit-block base change as a
+// coalesced SIMT pass, and radix-2 line FFTs in shared memory per axis.
+#include <algorithm>
+
+#include "device.cuh"
+#include "orbit_big.hpp"
+
+namespace fcct {
+
+using namespace dev;
+
+namespace {
+
+// y[b][members[off + r]] = sum_c coef[cbase + c s + r] x[b][members[off + c]]
+__global__ void __launch_bounds__(256) orbit_big_s_kernel(const __grid_constant__ OrbitBigDesc d,
+                                                          const double2* __restrict__ x, double2* __restrict__ y,
+                                                          int64_t batch) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (row >= d.rows) return;
+    const int o = __ldg(d.row_orbit + row), r = __ldg(d.row_index + row);
+    const int off = __ldg(d.orbit_off + o), s = __ldg(d.orbit_off + o + 1) - off;
+    const double2* __restrict__ cf = d.coef + __ldg(d.coef_off + o) + r;
+    const int* __restrict__ mem = d.members + off;
+    const int out = __ldg(mem + r);
+    for (int64_t b = 0; b < batch; ++b) {
+        const double2* xb = x + b * d.N;
+        double re = 0.0, im = 0.0;
+        for (int c = 0; c < s; ++c) {
+            const double2 m = __ldcs(cf + static_cast<int64_t>(c) * s);  // read once: streaming
+            const double2 v = __ldg(xb + __ldg(mem + c));
+            re = fma(m.x, v.x, re);
+            re = fma(-m.y, v.y, re);
+            im = fma(m.x, v.y, im);
+            im = fma(m.y, v.x, im);
+        }
+        y[b * d.N + out] = make_double2(re, im);
+    }
+}
+
+constexpr int kLines = 8;  // lines per CTA (neighbours in the contiguous dimension)
+
+// One radix-2 DIF FFT along `axis` for kLines neighbouring lines of n points.
+template <int NN, int SIGN>
+__global__ void __launch_bounds__(256) line_fft_kernel(const double2* __restrict__ in, double2* __restrict__ out,
+                                                       int axis, int64_t batch) {
+    constexpr int N = NN * NN * NN, LOG = NN == 32 ? 5 : 6;
+    __shared__ double2 buf[kLines][NN];
+    __shared__ double2 tw[NN / 2];
+    const int tid = threadIdx.x;
+    for (int e = tid; e < NN / 2; e += blockDim.x) {
+        double sv, cv;
+        sincospi(2.0 * e / NN, &sv, &cv);
+        tw[e] = make_double2(cv, SIGN * sv);
+    }
+    // line group g: lines (u, ., v0 + l) along the axis, l = 0..7 contiguous in memory
+    const int64_t groups_per_block = static_cast<int64_t>(NN) * NN / kLines;
+    const int64_t g = blockIdx.x;
+    const int64_t b = g / groups_per_block;
+    const int gi = static_cast<int>(g % groups_per_block);
+    if (b >= batch) return;
+    // strides: the line's own stride and the neighbour stride (1: contiguous)
+    int64_t base, step;
+    if (axis == 2) {  // k lines: rows (i, j) = consecutive lines, neighbours l -> j + l
+        const int i = gi / (NN / kLines), j0 = (gi % (NN / kLines)) * kLines;
+        base = (static_cast<int64_t>(i) * NN + j0) * NN;
+        step = 1;  // along the line
+    } else {
+        const int u = gi / (NN / kLines), v0 = (gi % (NN / kLines)) * kLines;  // u: the other axis, v0: k
+        base = axis == 1 ? static_cast<int64_t>(u) * NN * NN + v0 : static_cast<int64_t>(u) * NN + v0;
+        step = axis == 1 ? NN : static_cast<int64_t>(NN) * NN;
+    }
+    const double2* src = in + b * N;
+    double2* dst = out + b * N;
+    for (int e = tid; e < kLines * NN; e += blockDim.x) {
+        int l, x;
+        if (axis == 2) {
+            l = e / NN;
+            x = e % NN;
+        } else {  // neighbours innermost: coalesced 128-byte rows
+            l = e % kLines;
+            x = e / kLines;
+        }
+        const int64_t off = axis == 2 ? base + static_cast<int64_t>(l) * NN + x : base + l + x * step;
+        buf[l][x] = src[off];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int st = 0; st < LOG; ++st) {
+        const int half = NN >> (st + 1);
+        for (int e = tid; e < kLines * NN / 2; e += blockDim.x) {
+            const int l = e / (NN / 2), q = e % (NN / 2);
+            const int grp = q / half, j = q % half;
+            const int i0 = grp * 2 * half + j, i1 = i0 + half;
+            const double2 a = buf[l][i0], c = buf[l][i1];
+            const double2 d = make_double2(a.x - c.x, a.y - c.y);
+            const double2 w = tw[j << st];
+            buf[l][i0] = make_double2(a.x + c.x, a.y + c.y);
+            buf[l][i1] = make_double2(d.x * w.x - d.y * w.y, d.x * w.y + d.y * w.x);
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < kLines * NN; e += blockDim.x) {
+        int l, x;
+        if (axis == 2) {
+            l = e / NN;
+            x = e % NN;
+        } else {
+            l = e % kLines;
+            x = e / kLines;
+        }
+        const int rx = __brev(static_cast<unsigned>(x)) >> (32 - LOG);  // DIF output is bit-reversed
+        const int64_t off = axis == 2 ? base + static_cast<int64_t>(l) * NN + x : base + l + x * step;
+        dst[off] = buf[l][rx];
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_orbit_big_s(const OrbitBigDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st) {
+    if (batch <= 0) return cudaSuccess;
+    const int64_t blocks = (d.rows + 255) / 256;
+    orbit_big_s_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(d, static_cast<const double2*>(in),
+                                                                      static_cast<double2*>(out), batch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_line_fft(int n, int axis, int sign, const void* in, void* out, int64_t batch, cudaStream_t st) {
+    if (batch <= 0) return cudaSuccess;
+    const int64_t grid = batch * static_cast<int64_t>(n) * n / kLines;
+    auto* i = static_cast<const double2*>(in);
+    auto* o = static_cast<double2*>(out);
+#define LFFT(NV, SV) line_fft_kernel<NV, SV><<<static_cast<unsigned>(grid), 256, 0, st>>>(i, o, axis, batch)
+    if (n == 64) {
+        if (sign > 0) LFFT(64, 1); else LFFT(64, -1);
+    } else if (n == 32) {
+        if (sign > 0) LFFT(32, 1); else LFFT(32, -1);
+    } else {
+        return cudaErrorInvalidValue;
+    }
+#undef LFFT
+    return cudaGetLastError();
+}
+
+}  // namespace fcct

@@ -1,0 +1,52 @@
+// Orbit-FFT executor for large n (32, 64): D_n(p) = F_n S_n(p) (orbit_fft.hpp)
+// for a single transform or a small batch, where one block's state (4 MB at
+// n = 64) is L2-resident and the work is bound by streaming the operator.
+//
+//  S pass   one thread per output row of an orbit block (rows of an orbit are
+//           consecutive threads); the orbit's coefficients are stored column
+//           major, so a warp reads them coalesced while the input member is a
+//           broadcast; every coefficient is read once per launch and reused
+//           across the batch.
+//  F pass   one kernel per axis: a CTA loads 8 neighbouring lines of n points
+//           (coalesced 128-byte rows), runs the radix-2 stages in shared
+//           memory, and writes them back (in place, or to the output on the
+//           last axis).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+namespace fcct {
+
+struct Params;
+
+struct OrbitBigDesc {
+    int n = 0, N = 0, dir = 0;
+    int64_t rows = 0;                 // = N (every natural position is one row of one orbit)
+    const int* row_orbit = nullptr;   // [rows]: orbit of the row (rows are grouped by orbit)
+    const int* row_index = nullptr;   // [rows]: row index r inside its orbit
+    const int* orbit_off = nullptr;   // [orbits + 1]: first member slot of each orbit
+    const int64_t* coef_off = nullptr;// [orbits]: first coefficient of each orbit
+    const int* members = nullptr;     // [N]: natural position of each member slot
+    const double2* coef = nullptr;    // column-major blocks: coef[coef_off + c s + r] = M[r][c]
+};
+
+struct OrbitBigHost {
+    int n = 0, N = 0, dir = 0;
+    std::vector<int32_t> row_orbit, row_index, orbit_off, members;
+    std::vector<int64_t> coef_off;
+    std::vector<double> coef;  // (Re, Im) pairs
+    double exec_flops() const;
+};
+
+// Builds the S_n(p) (forward) or S_n(p)^{-1} / n^3 (inverse) blocks for n = 32, 64.
+bool compile_orbit_big(int n, const Params& p, bool inverse, OrbitBigHost& h);
+
+// S pass: complex128 in and out, [batch][N] rows.
+cudaError_t launch_orbit_big_s(const OrbitBigDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st);
+// F pass along axis (0 = i, 1 = j, 2 = k) with sign +-1; in == out allowed.
+cudaError_t launch_line_fft(int n, int axis, int sign, const void* in, void* out, int64_t batch, cudaStream_t st);
+
+}  // namespace fcct

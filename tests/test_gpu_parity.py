@@ -311,7 +311,7 @@ def test_large_batch_roundtrip_property(cuda):
 
 
 @pytest.mark.parametrize("n", [32, 64])
-def test_large_n_global_pipeline(cuda, oracle_mod, n):
+def test_large_n_global_pipeline(cuda, oracle_mod, n, monkeypatch):
     # configs[3] (n = 64, single transform): fast path vs the FFT/orbit oracle,
     # plus per-node direct evaluation spot checks (acceptance/main.cpp:368-388)
     # The fp64 floor of the factorization grows ~35x per doubling of n
@@ -319,6 +319,7 @@ def test_large_n_global_pipeline(cuda, oracle_mod, n):
     # 8.1e-12 / 3.6e-12 at n = 32 and 2.6e-10 / 1.2e-9 at n = 64
     # (tools/large_n_errors.py). The bars below sit just above those floors; the
     # node spot check uses the reference's own bar (acceptance #7: 1e-9).
+    monkeypatch.setenv("FCCT_PIPELINE", "global")
     bar = {32: 5e-11, 64: 5e-9}[n]
     route = oracle_mod.OrbitRoute(n, tup(CANON))
     batch = 2 if n == 32 else 1
@@ -570,3 +571,26 @@ def test_n16_two_pass_orbit_fft(cuda, oracle_mod, p):
     assert rel(y32.cpu().numpy(), y_ref) <= F32_TOL
     b32 = inverse_apply(p32, Spectrum(n, p, y32)).data
     assert rel(b32.cpu().numpy(), x) <= F32_TOL
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_large_n_orbit_fft(cuda, oracle_mod, n):
+    """configs[3] (n = 64, single transform) on the large-n orbit-FFT executor
+    (executor 7: S_n(p) as coalesced orbit-block rows, then three line-FFT
+    passes): the telescoped factorisation has no tree-conditioning floor, so
+    the 1e-12 bar holds where the stage-by-stage tree measures 1e-9."""
+    route = oracle_mod.OrbitRoute(n, tup(CANON))
+    batch = 2 if n == 32 else 1
+    x = rand_batch(n, batch, seed=n + 1)
+    y_ref = route.forward(x)
+    plan = build_plan(n, CANON)
+    assert plan.info.executor == 7
+    y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values.cpu().numpy()
+    assert rel(y, y_ref) <= F64_TOL
+    nodes = np.random.default_rng(777).integers(0, n**3, 8)
+    direct = oracle_mod.symmetrized_rows(n, tup(CANON), nodes, x[0])
+    assert np.abs(y[0, nodes] - direct).max() / np.abs(direct).max() <= 1e-12
+    xb = inverse_apply(plan, Spectrum(n, CANON, torch.from_numpy(y_ref).to(cuda))).data.cpu().numpy()
+    assert rel(xb, route.inverse(y_ref)) <= F64_TOL
+    back = inverse_apply(plan, Spectrum(n, CANON, torch.from_numpy(y).to(cuda))).data.cpu().numpy()
+    assert rel(back, x) <= F64_TOL
