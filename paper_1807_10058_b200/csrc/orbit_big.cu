@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(256) orbit_big_s_kernel(const __grid_constant_
     for (int64_t b = 0; b < batch; ++b) {
         const double2* xb = x + b * d.N;
         double re = 0.0, im = 0.0;
+#pragma unroll 4
         for (int c = 0; c < s; ++c) {
             const double2 m = __ldcs(cf + static_cast<int64_t>(c) * s);  // read once: streaming
             const double2 v = __ldg(xb + __ldg(mem + c));
@@ -114,6 +115,98 @@ __global__ void __launch_bounds__(256) line_fft_kernel(const double2* __restrict
     }
 }
 
+// 64-point lines as 8 x 8: thread t (0..7) of a line takes x[t + 8 m], runs
+// an 8-point DFT over m, multiplies by w64^{t q}, exchanges through shared
+// memory, and runs the 8-point DFT over t: X[q + 8 u] = sum_t w8^{t u} w64^{t q}
+// sum_m w8^{m q} x[t + 8 m]. 32 lines per CTA (8 threads each), two barriers.
+template <int SIGN>
+__device__ __forceinline__ void dft8(double2 (&v)[8]) {
+    // radix-2 DIF on 8 points, output in natural order
+    const double h = 0.70710678118654752440;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const double2 a = v[j], b = v[j + 4];
+        v[j] = make_double2(a.x + b.x, a.y + b.y);
+        double2 d = make_double2(a.x - b.x, a.y - b.y);
+        if (j == 1) d = make_double2(h * (d.x - SIGN * d.y), h * (d.y + SIGN * d.x));
+        if (j == 2) d = SIGN > 0 ? make_double2(-d.y, d.x) : make_double2(d.y, -d.x);
+        if (j == 3) d = make_double2(h * (-d.x - SIGN * d.y), h * (-d.y + SIGN * d.x));
+        v[j + 4] = d;
+    }
+#pragma unroll
+    for (int g = 0; g < 8; g += 4)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const double2 a = v[g + j], b = v[g + j + 2];
+            v[g + j] = make_double2(a.x + b.x, a.y + b.y);
+            double2 d = make_double2(a.x - b.x, a.y - b.y);
+            if (j == 1) d = SIGN > 0 ? make_double2(-d.y, d.x) : make_double2(d.y, -d.x);
+            v[g + j + 2] = d;
+        }
+#pragma unroll
+    for (int g = 0; g < 8; g += 2) {
+        const double2 a = v[g], b = v[g + 1];
+        v[g] = make_double2(a.x + b.x, a.y + b.y);
+        v[g + 1] = make_double2(a.x - b.x, a.y - b.y);
+    }
+    double2 t[8];
+    constexpr int br[8] = {0, 4, 2, 6, 1, 5, 3, 7};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = v[br[q]];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = t[q];
+}
+
+template <int SIGN>
+__global__ void __launch_bounds__(256) line_fft64_kernel(const double2* __restrict__ in, double2* __restrict__ out,
+                                                         int axis, int64_t batch) {
+    constexpr int NN = 64, N = NN * NN * NN, LPC = 32;  // lines per CTA
+    __shared__ double2 ex[LPC][8][9];                   // [line][t][q], padded
+    __shared__ double2 tw[NN];                          // w64^e
+    const int tid = threadIdx.x, t = tid & 7, li = tid >> 3;  // 8 threads per line
+    if (tid < NN) {
+        double sv, cv;
+        sincospi(2.0 * tid / NN, &sv, &cv);
+        tw[tid] = make_double2(cv, SIGN * sv);
+    }
+    __syncthreads();
+    const int64_t line = static_cast<int64_t>(blockIdx.x) * LPC + li;  // global line id
+    const int64_t b = line / (NN * NN);
+    if (b >= batch) return;
+    const int gi = static_cast<int>(line % (NN * NN));
+    // line start and stride along the axis; neighbouring lines are adjacent in
+    // the contiguous dimension for the i and j axes (coalesced across li)
+    int64_t base, step;
+    if (axis == 2) {
+        base = static_cast<int64_t>(gi) * NN;
+        step = 1;
+    } else if (axis == 1) {
+        base = static_cast<int64_t>(gi / NN) * NN * NN + gi % NN;
+        step = NN;
+    } else {
+        base = gi;
+        step = static_cast<int64_t>(NN) * NN;
+    }
+    const double2* src = in + b * N + base;
+    double2* dst = out + b * N + base;
+    double2 v[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) v[m] = src[(t + 8 * m) * step];
+    dft8<SIGN>(v);  // over m -> q
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const double2 w = tw[t * q];  // t q < 64
+        ex[li][t][q] = make_double2(v[q].x * w.x - v[q].y * w.y, v[q].x * w.y + v[q].y * w.x);
+    }
+    __syncwarp();
+    // thread t now takes q = t: the 8 values over t' (the second DFT's input)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = ex[li][u][t];
+    dft8<SIGN>(v);  // over t' -> u: X[t + 8 u]
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dst[(t + 8 * u) * step] = v[u];
+}
+
 }  // namespace
 
 cudaError_t launch_orbit_big_s(const OrbitBigDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st) {
@@ -130,8 +223,12 @@ cudaError_t launch_line_fft(int n, int axis, int sign, const void* in, void* out
     auto* i = static_cast<const double2*>(in);
     auto* o = static_cast<double2*>(out);
 #define LFFT(NV, SV) line_fft_kernel<NV, SV><<<static_cast<unsigned>(grid), 256, 0, st>>>(i, o, axis, batch)
-    if (n == 64) {
-        if (sign > 0) LFFT(64, 1); else LFFT(64, -1);
+    if (n == 64) {  // 8 x 8 decomposition, 32 lines per CTA
+        const int64_t g64 = batch * 64 * 64 / 32;
+        if (sign > 0)
+            line_fft64_kernel<1><<<static_cast<unsigned>(g64), 256, 0, st>>>(i, o, axis, batch);
+        else
+            line_fft64_kernel<-1><<<static_cast<unsigned>(g64), 256, 0, st>>>(i, o, axis, batch);
     } else if (n == 32) {
         if (sign > 0) LFFT(32, 1); else LFFT(32, -1);
     } else {
