@@ -343,8 +343,9 @@ __device__ __forceinline__ void base_change_lean(const double2 (&tab)[TMAX], con
                                                  const char* src, int srow, char* dst, int64_t drow, int r, int k,
                                                  int nvalid) {
     constexpr bool real_src = SM == OF_R64 || SM == OF_R32;
+    const int groups = (nvalid + 7) / 8 < G ? (nvalid + 7) / 8 : G;  // 8-block groups holding live blocks
 #pragma unroll 1
-    for (int g = 0; g < G; ++g) {
+    for (int g = 0; g < groups; ++g) {
         const char* s_row = src + (8 * g + r) * srow;
         char* d_row = dst + (8 * g + r) * drow;
         const bool live = 8 * g + r < nvalid;
@@ -385,8 +386,11 @@ __device__ __forceinline__ void fft_pass_group(int ft, const char* src, int64_t 
     constexpr int L = TB * NN * NN;
     constexpr int P = 2;
     static_assert(L % (P * kOfFftThreads) == 0, "lines per FFT thread");
+    // lines of blocks >= nvalid are skipped altogether (a ragged or single-block
+    // tile: the c1 latency config transforms 1 of the 64 blocks of an n = 4 tile)
+    const int Lv = nvalid * NN * NN < L ? nvalid * NN * NN : L;
 #pragma unroll 1
-    for (int base = ft; base < L; base += P * kOfFftThreads) {
+    for (int base = ft; base < Lv; base += P * kOfFftThreads) {
         double2 v[P][NN];
         int bb[P], hh[P], ll[P];
 #pragma unroll
@@ -405,7 +409,7 @@ __device__ __forceinline__ void fft_pass_group(int ft, const char* src, int64_t 
 #pragma unroll
         for (int q = 0; q < P; ++q) {
             const char* sp = src + bb[q] * srow;
-            const bool ok = !src_nat || bb[q] < nvalid;
+            const bool ok = !src_nat || bb[q] < nvalid;  // shared-memory sides stay unconditional
 #pragma unroll
             for (int x = 0; x < NN; ++x) {
                 if (ok)
@@ -496,7 +500,8 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                 const int bi = (3 - j % 3) % 3, bf = (4 - j % 3) % 3;
                 mbar_wait(bar + bi, (j / 3) & 1);
                 if (j > 0) named_sync(7, kOfBcThreads);  // BC(j - 1) has read buffer bf (= in(j - 1))
-                base_change_lean<TMAX, G, MI, OF_C128>(tab, meta_w, nt_w, buf(bi), C::XROW, buf(bf), C::YROW, r, k, TB);
+                base_change_lean<TMAX, G, MI, OF_C128>(tab, meta_w, nt_w, buf(bi), C::XROW, buf(bf), C::YROW, r, k,
+                                                       nvalid_of(tile));
                 named_arrive(1 + j % 3, kOfWarps * 32);  // tile j's spectrum-side buffer is ready
             } else {
                 named_sync(1 + j % 3, kOfWarps * 32);    // FFT(j) has filled y(j mod 3)
@@ -516,9 +521,9 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                 const int bf = (4 - j % 3) % 3;
                 char* Y = buf(bf);
                 named_sync(1 + j % 3, kOfWarps * 32);
-                fft_pass_group<NN, +1, TB, 2, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, TB);
+                fft_pass_group<NN, +1, TB, 2, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
                 named_sync(8, kOfFftThreads);
-                fft_pass_group<NN, +1, TB, 1, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, TB);
+                fft_pass_group<NN, +1, TB, 1, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
                 named_sync(8, kOfFftThreads);
                 fft_pass_group<NN, +1, TB, 0, OF_C128, MO>(ft, Y, C::YROW, false,
                                                           static_cast<char*>(out) + tile * TB * out_stride,
@@ -536,9 +541,9 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                 fft_pass_group<NN, -1, TB, 0, MI, OF_C128>(ft, static_cast<const char*>(in) + tile * TB * in_stride,
                                                           in_stride, true, Y, C::YROW, false, nvalid);
                 named_sync(8, kOfFftThreads);
-                fft_pass_group<NN, -1, TB, 1, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, TB);
+                fft_pass_group<NN, -1, TB, 1, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
                 named_sync(8, kOfFftThreads);
-                fft_pass_group<NN, -1, TB, 2, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, TB);
+                fft_pass_group<NN, -1, TB, 2, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
                 named_arrive(1 + j % 3, kOfWarps * 32);
             }
         }
