@@ -70,7 +70,7 @@ __device__ __forceinline__ void cp_async_n(void* dst, const void* src, bool vali
 // x 4 slots of one k-tile) touches 8 distinct bank groups for every element
 // size (16, 8 and 4 bytes), and the gather's 8 lanes of one slot too.
 // ---------------------------------------------------------------------------
-constexpr int kRingA = 4;  // operator tiles in flight per warp (L2 latency)
+constexpr int kRingA = kO16Wrap;  // operator tiles in flight per warp (L2 latency)
 
 template <int DIR, int MI, int MO>
 __global__ void __launch_bounds__(kO16Warps * 32, 1)
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kO16Warps * 32, 1)
     const int N = d.N, tmax = d.tmax, nch = d.nchunks;
     // shared: stage[2] | gather lists | tile metadata | output positions (all chunks, copied once)
     char* stage = reinterpret_cast<char*>(smem);
-    int* g_s = reinterpret_cast<int*>(smem + 2 * SBUF);
+    int* g_s = reinterpret_cast<int*>(smem + 3 * SBUF);
     int* tm_s = g_s + nch * kO16Chunk;
     int* op_s = tm_s + nch * kO16Warps * tmax;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = lane >> 2, k = lane & 3;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kO16Warps * 32, 1)
     int gc = 0;            // chunk of the next gather
     int64_t ggrp = blockIdx.x;  // group of the next gather
     auto gather = [&](int64_t item) {
-        char* st = stage + (item & 1) * SBUF;
+        char* st = stage + (item % 3) * SBUF;
         const int c = gc;
         const int64_t grp = ggrp;
         if (++gc == nch) {
@@ -126,75 +126,82 @@ __global__ void __launch_bounds__(kO16Warps * 32, 1)
     };
     // operator tile stream of this warp (chunk-major, tmax tiles per chunk),
     // kRingA fragments in flight, loaded L2-only (they are read once per group)
-    int tc = 0, tt = 0;  // chunk / tile of the next fragment load
-    const double2* tbase = d.table + static_cast<size_t>(warp) * tmax * 32 + lane;
+    // this warp's operator tiles are contiguous over the chunks, followed by
+    // copies of its first kRingA tiles: the look-ahead reads tp[32 q] and the
+    // pointer resets once per group
+    const double2* tbase = d.table + static_cast<size_t>(warp) * (static_cast<size_t>(nch) * tmax + kRingA) * 32 + lane;
     const double2* tp = tbase;
-    auto next_tile = [&]() {
-        const double2 v = __ldcg(tp);
-        tp += 32;
-        if (++tt == tmax) {  // warp-uniform: next chunk's segment of this warp, or wrap
-            tt = 0;
-            if (++tc == nch) {
-                tc = 0;
-                tp = tbase;
-            } else {
-                tp += static_cast<size_t>(kO16Warps - 1) * tmax * 32;
-            }
-        }
-        return v;
-    };
     const int lane_off = (8 * k + (r ^ (2 * k))) * SEB;  // this lane's element of a k-tile's 32 slots
     double2 ring[kRingA];
 #pragma unroll
-    for (int q = 0; q < kRingA; ++q) ring[q] = next_tile();
+    for (int q = 0; q < kRingA; ++q) ring[q] = __ldcg(tp + q * 32);
+    tp += kRingA * 32;
+    // three stage buffers: chunk item + 2 is gathered while item is computed,
+    // one barrier per chunk
     if (items > 0) gather(0);
+    if (items > 1) gather(1); else cp_async_commit();
     int c = 0;
     int64_t grp = blockIdx.x;
     for (int64_t item = 0; item < items; ++item) {
-        if (item + 1 < items) {
-            gather(item + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();  // the chunk's stage is complete
-        const char* st = stage + (item & 1) * SBUF;
+        cp_async_wait<1>();  // this thread's copies of chunk `item` have landed
+        __syncthreads();     // ... everyone's; and every warp is done with chunk item - 1
+        if (item + 2 < items)
+            gather(item + 2);  // into the buffer chunk item - 1 used
+        else
+            cp_async_commit();  // keep one group per iteration
+        const char* st = stage + (item % 3) * SBUF;
         const int64_t nv = batch - grp * 8;
         const bool live = r < nv;
         char* d_row = static_cast<char*>(out) + (grp * 8 + r) * out_row;
         const int* tm = tm_s + (c * kO16Warps + warp) * tmax;
         const int* op = op_s + (c * kO16Warps + warp) * tmax * 4;
         double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+        // software pipeline: metadata two tiles ahead, the fragment one tile ahead
+        auto frag = [&](int m, double& ar, double& ai) {
+            if (m & (1 << 17))
+                ld_el<SM>(st + (m & 0xFFFF) * (32 * SEB) + lane_off, 0, ar, ai);
+            else
+                ar = ai = 0.0;
+        };
+        int m_cur = tm[0], m_nxt = tmax > 1 ? tm[1] : 0;
+        double ar, ai;
+        frag(m_cur, ar, ai);
         for (int t0 = 0; t0 < tmax; t0 += kRingA) {
 #pragma unroll
             for (int q = 0; q < kRingA; ++q) {
                 const int t = t0 + q;
                 const double2 tb = ring[q];
-                ring[q] = next_tile();  // kRingA tiles ahead
-                const int m = tm[t];
-                if (!(m & (1 << 17))) continue;  // padding tile (warp-uniform)
-                double ar, ai;
-                ld_el<SM>(st + (m & 0xFFFF) * (32 * SEB) + lane_off, 0, ar, ai);
-                dmma884(cr0, cr1, ar, tb.x);
-                dmma884(ci0, ci1, ar, tb.y);
-                if constexpr (!REAL) {
-                    dmma884(cr0, cr1, neg_hi16(ai), tb.y);
-                    dmma884(ci0, ci1, ai, tb.x);
+                ring[q] = __ldcg(tp + q * 32);  // kRingA tiles ahead
+                const int m_nn = t + 2 < tmax ? tm[t + 2] : 0;
+                double arn, ain;
+                frag(m_nxt, arn, ain);
+                if (m_cur & (1 << 17)) {  // real tile (padding tiles close each warp's list)
+                    dmma884(cr0, cr1, ar, tb.x);
+                    dmma884(ci0, ci1, ar, tb.y);
+                    if constexpr (!REAL) {
+                        dmma884(cr0, cr1, neg_hi16(ai), tb.y);
+                        dmma884(ci0, ci1, ai, tb.x);
+                    }
+                    if (m_cur & (1 << 16)) {  // chain end
+                        const int o = op[t * 4 + k];
+                        const int o0 = o & 0xFFFF, o1 = (o >> 16) & 0xFFFF;
+                        if (live && o0 != 0xFFFF) st_el<DM>(d_row, o0, cr0, ci0);
+                        if (live && o1 != 0xFFFF) st_el<DM>(d_row, o1, cr1, ci1);
+                        cr0 = cr1 = ci0 = ci1 = 0.0;
+                    }
                 }
-                if (m & (1 << 16)) {  // chain end
-                    const int o = op[t * 4 + k];
-                    const int o0 = o & 0xFFFF, o1 = (o >> 16) & 0xFFFF;
-                    if (live && o0 != 0xFFFF) st_el<DM>(d_row, o0, cr0, ci0);
-                    if (live && o1 != 0xFFFF) st_el<DM>(d_row, o1, cr1, ci1);
-                    cr0 = cr1 = ci0 = ci1 = 0.0;
-                }
+                m_cur = m_nxt;
+                m_nxt = m_nn;
+                ar = arn;
+                ai = ain;
             }
+            tp += kRingA * 32;
         }
         if (++c == nch) {
             c = 0;
             grp += gridDim.x;
+            tp = tbase + kRingA * 32;  // the ring holds the group's first tiles (the wrap copies)
         }
-        __syncthreads();  // every warp is done with this stage before it is refilled
     }
 }
 
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(kFftThreads, 2)
 template <int DIR, int MI, int MO>
 cudaError_t launch_a(const Orbit16Desc& d, const void* in, void* out, int64_t batch, cudaStream_t st, int num_sms) {
     constexpr int SM = DIR == 0 ? MI : OF_C128;
-    const int smem = 2 * kO16Chunk * 8 * eb_of(SM) + d.nchunks * kO16Chunk * 4 + d.nchunks * kO16Warps * d.tmax * 5 * 4;
+    const int smem = 3 * kO16Chunk * 8 * eb_of(SM) + d.nchunks * kO16Chunk * 4 + d.nchunks * kO16Warps * d.tmax * 5 * 4;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     auto kern = orbit16_base_kernel<DIR, MI, MO>;
     static thread_local int prepared = -1;

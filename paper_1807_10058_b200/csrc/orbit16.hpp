@@ -29,12 +29,13 @@ struct Params;
 constexpr int kO16Warps = 16;
 constexpr int kO16Chunk = 256;  // member slots per chunk (4 per k-tile)
 constexpr int kO16Tmax = 16;    // tiles per warp per chunk
+constexpr int kO16Wrap = 4;     // operator tiles in flight per warp (the stream's look-ahead)
 
 struct Orbit16Desc {
     int n = 0, N = 0, dir = 0;
     int nchunks = 0;
     int tmax = 0;                      // tiles per warp per chunk (<= kO16Tmax)
-    const double2* table = nullptr;    // [chunk][warp][tmax][32] B fragments (Re, Im)
+    const double2* table = nullptr;    // [warp][chunk * tmax + kO16Wrap][32] B fragments (Re, Im)
     const int* tile_meta = nullptr;    // [chunk][warp][tmax]: k-tile index | chain end << 16 | valid << 17
     const int* out_pos = nullptr;      // [chunk][warp][tmax][4]: natural positions o(2k) | o(2k+1) << 16 (0xFFFF none)
     const int* gather = nullptr;       // [chunk][kO16Chunk]: natural position of each slot (-1: zero padding)

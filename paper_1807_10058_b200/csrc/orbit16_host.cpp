@@ -72,7 +72,11 @@ bool compile_orbit16(int n, const Params& p, bool inverse, Orbit16Host& h) {
     h.dir = inverse ? 1 : 0;
     h.nchunks = nchunks;
     h.tmax = tmax;
-    h.table.assign(static_cast<size_t>(nchunks) * kO16Warps * tmax * 32 * 2, 0.0);
+    // operator tiles per warp, contiguous over the chunks ([warp][chunk][tmax]),
+    // plus kO16Wrap copies of the warp's first tiles: the kernel streams them
+    // with a fixed look-ahead and no per-tile wrap logic
+    const size_t per_warp_tiles = static_cast<size_t>(nchunks) * tmax + kO16Wrap;
+    h.table.assign(kO16Warps * per_warp_tiles * 32 * 2, 0.0);
     h.tile_meta.assign(static_cast<size_t>(nchunks) * kO16Warps * tmax, 0);
     h.out_pos.assign(static_cast<size_t>(nchunks) * kO16Warps * tmax * 4, -1);
     h.gather.assign(static_cast<size_t>(nchunks) * kO16Chunk, -1);
@@ -106,12 +110,13 @@ bool compile_orbit16(int n, const Params& p, bool inverse, Orbit16Host& h) {
                 const std::vector<cld>& M = inverse ? ob.Sinv[ch.orbit] : ob.S[ch.orbit];  // [row][col], s x s
                 for (int q = 0; q < ch.kts; ++q, ++t) {
                     const size_t ti = (static_cast<size_t>(c) * kO16Warps + w) * tmax + t;
+                    const size_t tt = w * per_warp_tiles + static_cast<size_t>(c) * tmax + t;  // table position
                     for (int l = 0; l < 32; ++l) {
                         const int row = 8 * ch.nt + l / 4, col = 4 * q + l % 4;
                         cld v{0, 0};
                         if (row < s && col < s) v = M[static_cast<size_t>(row) * s + col] * scale;
-                        h.table[(ti * 32 + l) * 2] = static_cast<double>(v.real());
-                        h.table[(ti * 32 + l) * 2 + 1] = static_cast<double>(v.imag());
+                        h.table[(tt * 32 + l) * 2] = static_cast<double>(v.real());
+                        h.table[(tt * 32 + l) * 2 + 1] = static_cast<double>(v.imag());
                     }
                     const bool end = q == ch.kts - 1;
                     h.tile_meta[ti] = (ch.kt0 + q) | (end ? 1 << 16 : 0) | (1 << 17);
@@ -127,6 +132,11 @@ bool compile_orbit16(int n, const Params& p, bool inverse, Orbit16Host& h) {
             }
         }
     }
+    for (int w = 0; w < kO16Warps; ++w)  // wrap copies
+        for (int t = 0; t < kO16Wrap; ++t)
+            for (int e = 0; e < 64; ++e)
+                h.table[((w * per_warp_tiles + nchunks * tmax + t) * 32) * 2 + e] =
+                    h.table[((w * per_warp_tiles + t) * 32) * 2 + e];
     return true;
 }
 
@@ -198,8 +208,9 @@ void emulate_orbit16(const Orbit16Host& h, const double* in, double* out, int64_
                     const int m = h.tile_meta[ti];
                     if (!(m & (1 << 17))) continue;
                     const int kt = m & 0xFFFF;
+                    const size_t tt = w * (static_cast<size_t>(h.nchunks) * h.tmax + kO16Wrap) + c * h.tmax + t;
                     for (int l = 0; l < 32; ++l)
-                        acc[l / 4] += cd{h.table[(ti * 32 + l) * 2], h.table[(ti * 32 + l) * 2 + 1]} * stage[4 * kt + l % 4];
+                        acc[l / 4] += cd{h.table[(tt * 32 + l) * 2], h.table[(tt * 32 + l) * 2 + 1]} * stage[4 * kt + l % 4];
                     if (m & (1 << 16)) {
                         for (int k = 0; k < 4; ++k) {
                             const int o0 = h.out_pos[ti * 4 + k] & 0xFFFF, o1 = (h.out_pos[ti * 4 + k] >> 16) & 0xFFFF;
