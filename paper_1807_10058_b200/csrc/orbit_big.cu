@@ -25,14 +25,28 @@ __global__ void __launch_bounds__(256) orbit_big_s_kernel(const __grid_constant_
     for (int64_t b = 0; b < batch; ++b) {
         const double2* xb = x + b * d.N;
         double re = 0.0, im = 0.0;
+        if (s == 24) {  // free orbits (almost every row at n = 64): all 24 coefficient loads in flight at once
+            double2 m[24];
+#pragma unroll
+            for (int c = 0; c < 24; ++c) m[c] = __ldcs(cf + c * 24);
+#pragma unroll
+            for (int c = 0; c < 24; ++c) {
+                const double2 v = __ldg(xb + __ldg(mem + c));
+                re = fma(m[c].x, v.x, re);
+                re = fma(-m[c].y, v.y, re);
+                im = fma(m[c].x, v.y, im);
+                im = fma(m[c].y, v.x, im);
+            }
+        } else {
 #pragma unroll 4
-        for (int c = 0; c < s; ++c) {
-            const double2 m = __ldcs(cf + static_cast<int64_t>(c) * s);  // read once: streaming
-            const double2 v = __ldg(xb + __ldg(mem + c));
-            re = fma(m.x, v.x, re);
-            re = fma(-m.y, v.y, re);
-            im = fma(m.x, v.y, im);
-            im = fma(m.y, v.x, im);
+            for (int c = 0; c < s; ++c) {
+                const double2 m = __ldcs(cf + static_cast<int64_t>(c) * s);  // read once: streaming
+                const double2 v = __ldg(xb + __ldg(mem + c));
+                re = fma(m.x, v.x, re);
+                re = fma(-m.y, v.y, re);
+                im = fma(m.x, v.y, im);
+                im = fma(m.y, v.x, im);
+            }
         }
         y[b * d.N + out] = make_double2(re, im);
     }
