@@ -812,6 +812,10 @@ void run_o16(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, void* o
         ck(cudaStreamSynchronize(st), "sync");
         pl->scratch0 = std::make_shared<DevBuf>(bytes);
     }
+    if (inverse && (!pl->scratch1 || pl->scratch1->bytes < bytes)) {
+        ck(cudaStreamSynchronize(st), "sync");
+        pl->scratch1 = std::make_shared<DevBuf>(bytes);
+    }
     void* z = pl->scratch0->ptr;
     if (!inverse) {
         ck(launch_orbit16_base(pl->o16fwd.desc, in_mode, OF_C128, in, z, batch, st, pl->num_sms), "orbit base change");
@@ -820,7 +824,12 @@ void run_o16(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, void* o
     } else {
         ck(launch_fft_cube(pl->n, -1, in_mode, OF_C128, in, z, batch, pl->o16inv.desc.zperm, st, pl->num_sms),
            "cube FFT");
-        ck(launch_orbit16_base(pl->o16inv.desc, OF_C128, out_mode, z, out, batch, st, pl->num_sms), "orbit base change");
+        // rows in orbit order (contiguous stores), then back to natural positions
+        ck(launch_orbit16_base(pl->o16inv.desc, OF_C128, out_mode, z, pl->scratch1->ptr, batch, st, pl->num_sms),
+           "orbit base change");
+        ck(launch_unpermute(out_mode, pl->scratch1->ptr, out, static_cast<int>(cube(pl->n)), batch,
+                            pl->o16inv.desc.zperm, st, pl->num_sms),
+           "orbit-order rows to natural");
     }
     ck(cudaStreamSynchronize(st), "sync");  // the plan-owned scratch serialises calls on this path
 }

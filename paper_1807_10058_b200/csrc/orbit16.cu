@@ -369,7 +369,43 @@ cudaError_t launch_b(const void* in, void* out, int64_t batch, const int* zperm,
     return cudaGetLastError();
 }
 
+// out[b][a] = in[b][zperm[a]]: the inverse base change's orbit-ordered rows
+// back to natural positions (coalesced stores, gathers within one row)
+template <int M>
+__global__ void __launch_bounds__(256) unpermute_kernel(const char* __restrict__ in, char* __restrict__ out, int N,
+                                                        int64_t batch, const int* __restrict__ zperm) {
+    constexpr int EB = eb_of(M);
+    const int64_t total = batch * N;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t b = i / N;
+        const int a = static_cast<int>(i - b * N);
+        const char* row = in + b * N * EB;
+        if constexpr (EB == 16)
+            reinterpret_cast<double2*>(out)[i] = reinterpret_cast<const double2*>(row)[__ldg(zperm + a)];
+        else if constexpr (EB == 8)
+            reinterpret_cast<double*>(out)[i] = reinterpret_cast<const double*>(row)[__ldg(zperm + a)];
+        else
+            reinterpret_cast<float*>(out)[i] = reinterpret_cast<const float*>(row)[__ldg(zperm + a)];
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_unpermute(int mode, const void* in, void* out, int N, int64_t batch, const int* zperm,
+                             cudaStream_t st, int num_sms) {
+    if (batch <= 0) return cudaSuccess;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((batch * N + 255) / 256, 8 * int64_t{num_sms}));
+    auto* i = static_cast<const char*>(in);
+    auto* o = static_cast<char*>(out);
+    switch (mode) {
+        case OF_C128: unpermute_kernel<OF_C128><<<grid, 256, 0, st>>>(i, o, N, batch, zperm); break;
+        case OF_C64: unpermute_kernel<OF_C64><<<grid, 256, 0, st>>>(i, o, N, batch, zperm); break;
+        case OF_R64: unpermute_kernel<OF_R64><<<grid, 256, 0, st>>>(i, o, N, batch, zperm); break;
+        default: unpermute_kernel<OF_R32><<<grid, 256, 0, st>>>(i, o, N, batch, zperm); break;
+    }
+    return cudaGetLastError();
+}
 
 cudaError_t launch_orbit16_base(const Orbit16Desc& d, int in_mode, int out_mode, const void* in, void* out,
                                 int64_t batch, cudaStream_t st, int num_sms) {

@@ -37,7 +37,7 @@ struct Orbit16Desc {
     int tmax = 0;                      // tiles per warp per chunk (<= kO16Tmax)
     const double2* table = nullptr;    // [warp][chunk * tmax + kO16Wrap][32] B fragments (Re, Im)
     const int* tile_meta = nullptr;    // [chunk][warp][tmax]: k-tile index | chain end << 16 | valid << 17
-    const int* out_pos = nullptr;      // [chunk][warp][tmax][4]: natural positions o(2k) | o(2k+1) << 16 (0xFFFF none)
+    const int* out_pos = nullptr;      // [chunk][warp][tmax][4]: orbit-order positions o(2k) | o(2k+1) << 16 (0xFFFF none)
     const int* gather = nullptr;       // [chunk][kO16Chunk]: natural position of each slot (-1: zero padding)
     const int* chunk_slots = nullptr;  // [chunk]: slots used
     const int* zperm = nullptr;        // [N]: orbit-order index of natural position a in z
@@ -62,6 +62,9 @@ void emulate_orbit16(const Orbit16Host& h, const double* in, double* out, int64_
 // Pass A: in/out modes as OfMode (orbit_fft.hpp); the z side is complex128.
 cudaError_t launch_orbit16_base(const Orbit16Desc& d, int in_mode, int out_mode, const void* in, void* out,
                                 int64_t batch, cudaStream_t st, int num_sms);
+// Inverse epilogue: rows stored in orbit order by pass A -> natural positions.
+cudaError_t launch_unpermute(int mode, const void* in, void* out, int N, int64_t batch, const int* zperm,
+                             cudaStream_t st, int num_sms);
 // Pass B: sign +1 (forward F_n) or -1 (F_n^{-1} without the 1/n^3, folded into pass A).
 // zperm: the z side (forward input / inverse output, complex128) is in orbit
 // order, z[zperm[a]] holding natural position a.

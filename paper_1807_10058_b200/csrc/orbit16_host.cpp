@@ -122,8 +122,9 @@ bool compile_orbit16(int n, const Params& p, bool inverse, Orbit16Host& h) {
                     h.tile_meta[ti] = (ch.kt0 + q) | (end ? 1 << 16 : 0) | (1 << 17);
                     for (int k = 0; k < 4; ++k) {
                         const int r0 = 8 * ch.nt + 2 * k, r1 = r0 + 1;
-                        // forward: z in orbit order; inverse: x natural
-                        auto op = [&](int row) { return row < s ? (inverse ? mem[row] : zside(mem[row])) : 0xFFFF; };
+                        // both directions store in orbit order (contiguous runs): forward
+                        // z, inverse x (un-permuted by a coalesced pass afterwards)
+                        auto op = [&](int row) { return row < s ? zside(mem[row]) : 0xFFFF; };
                         const int o0 = op(r0), o1 = op(r1);
                         h.out_pos[ti * 4 + k] = o0 | (o1 << 16);
                     }
@@ -222,12 +223,12 @@ void emulate_orbit16(const Orbit16Host& h, const double* in, double* out, int64_
                 }
             }
         }
-        if (h.dir == 0) {  // z in orbit order -> natural, then the FFT
+        {  // z (forward) / x (inverse) in orbit order -> natural
             std::vector<cd> t(N);
             for (int a = 0; a < N; ++a) t[a] = z[h.zperm[a]];
             z = t;
-            dft3(z, h.n, +1);
         }
+        if (h.dir == 0) dft3(z, h.n, +1);
         for (int a = 0; a < N; ++a) {
             out[2 * (b * N + a)] = z[a].real();
             out[2 * (b * N + a) + 1] = z[a].imag();
