@@ -1201,7 +1201,10 @@ void run_host_any(fcct_plan_s* pl, bool inverse, bool real_io, const void* in, v
     const int64_t in_eb = (real_io && !inverse) ? eb / 2 : eb, out_eb = (real_io && inverse) ? eb / 2 : eb;
     const int64_t block_bytes = N * eb;
     // ~32 MB chunks (at least 8 per call when the batch is large), whole blocks
-    int64_t chunk = std::max<int64_t>(1, (int64_t{32} << 20) / block_bytes);
+    // chunk size: FCCT_HOST_CHUNK_MB (default 32 MB), at least 8 chunks per call
+    int64_t chunk_mb = 32;
+    if (const char* e = std::getenv("FCCT_HOST_CHUNK_MB")) chunk_mb = std::max<int64_t>(1, std::atoll(e));
+    int64_t chunk = std::max<int64_t>(1, (chunk_mb << 20) / block_bytes);
     chunk = std::min(chunk, std::max<int64_t>(1, (batch + 7) / 8));
     chunk = std::min(chunk, batch);
     const size_t ws_bytes = static_cast<size_t>(chunk * block_bytes);
