@@ -124,6 +124,25 @@ def profiled_traffic(cfg_name: str, f32: bool, executor: int):
         return None
 
 
+def launches_per_call(info):
+    """Kernels one forward / one inverse call launches on each executor
+    (fcct_plan_info_t.executor): orbit-FFT 1; two-pass n = 16: base change +
+    cube FFT (+ un-permute on the inverse); large n: S pass + 3 line passes;
+    two-level: root pass + 8 children + permutation; stage pipelines and the
+    direct GEMM: 1 (global multi-pass: one per stage, ~levels * 2 + 1)."""
+    ex = info.executor
+    if ex == 6:
+        return (2, 3)
+    if ex == 7:
+        return (4, 4)
+    if ex == 4:
+        return (10, 10)
+    if ex == 3:
+        k = 2 * info.levels + 1
+        return (k, k)
+    return (1, 1)
+
+
 def run_cpu_baseline(n: int, blocks: int, threads: int, method: str = "fast", min_seconds: float = 0.0) -> dict:
     from oracle import oracle  # CPU baseline / reference arm only
 
@@ -525,7 +544,7 @@ def b200_arm(args):
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": args.steps * sum(launches_per_call(info)),
         "clocks": clk.summary(),
         "plan": {"tree_nnz": info.tree_nnz, "tree_nnz_inv": info.tree_nnz_inv, "table_bytes": info.table_bytes,
                  "flops_forward_per_block": info.flops_forward, "flops_inverse_per_block": info.flops_inverse},
