@@ -589,6 +589,9 @@ struct fcct_plan_s {
     GlobalTables gfwd, ginv;
     std::shared_ptr<DevBuf> scratch0, scratch1;
     std::mutex scratch_mu;
+    // stream-ordered ownership of the scratch: recorded after the last kernel
+    // of a call that used it; the next call's stream waits on it (no host sync)
+    cudaEvent_t scratch_ev = nullptr;
     std::shared_ptr<DevBuf> Wt_fwd, Wt_inv;
     std::vector<std::shared_ptr<DevBuf>> extra;
     fcct_plan_info_t info{};
@@ -605,6 +608,7 @@ struct fcct_plan_s {
         for (auto& e : cev)
             if (e) cudaEventDestroy(e);
         if (hev) cudaEventDestroy(hev);
+        if (scratch_ev) cudaEventDestroy(scratch_ev);
     }
     // complex staging for real-I/O calls on executors without fused real I/O
     std::mutex ws_real_mu;
@@ -614,6 +618,19 @@ struct fcct_plan_s {
 namespace {
 
 int64_t elem_bytes(const fcct_plan_s* p) { return p->precision == FCCT_F32 ? 8 : 16; }
+
+// The plan-owned scratch (z / ping-pong buffers) is shared by every call on the
+// plan: a call holds scratch_mu while it enqueues, makes its stream wait for
+// the previous user's last kernel, and records its own last kernel. Calls on
+// one stream stay asynchronous; calls on different streams are ordered on the
+// device, not by blocking the host.
+void scratch_acquire(fcct_plan_s* pl, cudaStream_t st) {
+    if (!pl->scratch_ev)
+        ck(cudaEventCreateWithFlags(&pl->scratch_ev, cudaEventDisableTiming), "event");
+    else
+        ck(cudaStreamWaitEvent(st, pl->scratch_ev, 0), "scratch wait");
+}
+void scratch_release(fcct_plan_s* pl, cudaStream_t st) { ck(cudaEventRecord(pl->scratch_ev, st), "scratch record"); }
 
 void build_direct(fcct_plan_s* pl) {
     const int n = pl->n;
@@ -817,6 +834,7 @@ void run_o16(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, void* o
         pl->scratch1 = std::make_shared<DevBuf>(bytes);
     }
     void* z = pl->scratch0->ptr;
+    scratch_acquire(pl, st);
     if (!inverse) {
         ck(launch_orbit16_base(pl->o16fwd.desc, in_mode, OF_C128, in, z, batch, st, pl->num_sms), "orbit base change");
         ck(launch_fft_cube(pl->n, +1, OF_C128, out_mode, z, out, batch, pl->o16fwd.desc.zperm, st, pl->num_sms),
@@ -831,7 +849,7 @@ void run_o16(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, void* o
                             pl->o16inv.desc.zperm, st, pl->num_sms),
            "orbit-order rows to natural");
     }
-    ck(cudaStreamSynchronize(st), "sync");  // the plan-owned scratch serialises calls on this path
+    scratch_release(pl, st);
 }
 
 // in_mode / out_mode of the natural side: 0 complex128, 1 complex64, 2 real f64, 3 real f32
@@ -845,6 +863,7 @@ void run_two_level(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, v
         pl->scratch0 = std::make_shared<DevBuf>(bytes);
         pl->scratch1 = std::make_shared<DevBuf>(bytes);
     }
+    scratch_acquire(pl, st);
     double* s1 = static_cast<double*>(pl->scratch0->ptr);
     double* s2 = static_cast<double*>(pl->scratch1->ptr);
     for (int k = 0; k < 4; ++k)
@@ -879,7 +898,7 @@ void run_two_level(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, v
         children(pl->cinv);
         ck(launch_root_inverse(pl->rinv.desc, s2, out, out_mode, batch, st, pl->num_sms), "root pass");
     }
-    ck(cudaStreamSynchronize(st), "sync");  // the plan-owned scratch serialises calls on this path
+    scratch_release(pl, st);
 }
 
 // max |a - b| over the union of the two sparsity patterns
@@ -1120,6 +1139,7 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
                 pl->scratch0 = std::make_shared<DevBuf>(bytes);
             }
             void* z = pl->scratch0->ptr;
+            scratch_acquire(pl, st);
             if (!inverse) {
                 ck(launch_orbit_big_s(pl->obfwd.desc, in, z, batch, st), "orbit base change");
                 ck(launch_line_fft(pl->n, 2, +1, z, z, batch, st), "line FFT");
@@ -1131,7 +1151,7 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
                 ck(launch_line_fft(pl->n, 2, -1, z, z, batch, st), "line FFT");
                 ck(launch_orbit_big_s(pl->obinv.desc, z, out, batch, st), "orbit base change");
             }
-            ck(cudaStreamSynchronize(st), "sync");  // the plan-owned scratch serialises calls on this path
+            scratch_release(pl, st);
             return;
         }
         if (pl->offt) {
@@ -1151,11 +1171,11 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
                 pl->scratch0 = std::make_shared<DevBuf>(bytes);
                 pl->scratch1 = std::make_shared<DevBuf>(bytes);
             }
+            scratch_acquire(pl, st);
             ck(launch_global_pipeline(inverse ? pl->ginv.desc : pl->gfwd.desc, f32, in, out, pl->scratch0->ptr,
                                       pl->scratch1->ptr, batch, st),
                "global pipeline");
-            // the plan-owned scratch serialises calls on this path
-            ck(cudaStreamSynchronize(st), "sync");
+            scratch_release(pl, st);
         } else
             ck(launch_pipeline(inverse ? pl->inv.desc : pl->fwd.desc, f32, in, out, batch, st, pl->num_sms),
                "fast pipeline");
