@@ -1688,6 +1688,17 @@ fcct_status fcct_plan_tree_stats(int n, double r, double s, double t, int64_t* t
 // Host emulation of the v2 DMMA pipeline tables (no GPU): applies the
 // compiled stages to `batch` blocks exactly as the kernel indexes them
 // (slots, lane-ordered fragments, unit lists). Tests the plan compiler on CPU.
+// Host emulation of the large-n orbit-FFT executor's tables (n = 32, 64, CPU tests).
+fcct_status fcct_debug_emulate_orbit_big(int n, double r, double s, double t, int inverse, const double* in,
+                                         double* out, int64_t batch) {
+    return guarded([&] {
+        OrbitBigHost h;
+        if (!compile_orbit_big(n, Params{r, s, t}, inverse != 0, h))
+            throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by the large-n orbit-FFT executor");
+        emulate_orbit_big(h, in, out, batch);
+    });
+}
+
 // Host emulation of the two-pass orbit-FFT executor's tables (n = 16, CPU tests).
 fcct_status fcct_debug_emulate_orbit16(int n, double r, double s, double t, int inverse, const double* in, double* out,
                                        int64_t batch) {

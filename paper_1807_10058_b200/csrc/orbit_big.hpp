@@ -44,6 +44,9 @@ struct OrbitBigHost {
 // Builds the S_n(p) (forward) or S_n(p)^{-1} / n^3 (inverse) blocks for n = 32, 64.
 bool compile_orbit_big(int n, const Params& p, bool inverse, OrbitBigHost& h);
 
+// Host emulation of both passes on the compiled tables (CPU tests), complex128 rows.
+void emulate_orbit_big(const OrbitBigHost& h, const double* in, double* out, int64_t batch);
+
 // S pass: complex128 in and out, [batch][N] rows.
 cudaError_t launch_orbit_big_s(const OrbitBigDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st);
 // F pass along axis (0 = i, 1 = j, 2 = k) with sign +-1; in == out allowed.

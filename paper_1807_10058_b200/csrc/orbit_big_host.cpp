@@ -2,6 +2,8 @@
 // of S_n(p) / S_n(p)^{-1} as column-major coefficient blocks, one row per
 // natural position.
 #include <cmath>
+#include <complex>
+#include <numbers>
 
 #include "orbit_big.hpp"
 #include "plan.hpp"
@@ -67,6 +69,57 @@ double OrbitBigHost::exec_flops() const {
             if (e != 0 && 4 * e != n) twiddles += n / (2 * half);
         }
     return 8.0 * cmacs + 3.0 * n * n * ((n / 2.0) * lg * 4.0 + 6.0 * twiddles);
+}
+
+// Host emulation (CPU tests): the S pass exactly as the kernel indexes the
+// coefficient blocks, then the three axis DFTs. in / out: complex128 rows.
+void emulate_orbit_big(const OrbitBigHost& h, const double* in, double* out, int64_t batch) {
+    using cd = std::complex<double>;
+    const int n = h.n, N = h.N;
+    auto dft3 = [&](std::vector<cd>& v, int sign) {
+        std::vector<cd> line(n), res(n);
+        for (int axis = 0; axis < 3; ++axis)
+            for (int u = 0; u < n; ++u)
+                for (int w = 0; w < n; ++w) {
+                    auto at = [&](int x) {
+                        int ijk[3];
+                        ijk[axis] = x;
+                        ijk[axis == 0 ? 1 : 0] = u;
+                        ijk[axis == 2 ? 1 : 2] = w;
+                        return (ijk[0] * n + ijk[1]) * n + ijk[2];
+                    };
+                    for (int x = 0; x < n; ++x) line[x] = v[at(x)];
+                    for (int q = 0; q < n; ++q) {
+                        cd acc{0, 0};
+                        for (int x = 0; x < n; ++x) {
+                            const double ang = sign * 2.0 * std::numbers::pi * ((x * q) % n) / n;
+                            acc += line[x] * cd{std::cos(ang), std::sin(ang)};
+                        }
+                        res[q] = acc;
+                    }
+                    for (int x = 0; x < n; ++x) v[at(x)] = res[x];
+                }
+    };
+    std::vector<cd> x(N), y(N);
+    for (int64_t b = 0; b < batch; ++b) {
+        for (int a = 0; a < N; ++a) x[a] = cd{in[2 * (b * N + a)], in[2 * (b * N + a) + 1]};
+        if (h.dir == 1) dft3(x, -1);
+        for (int row = 0; row < N; ++row) {
+            const int o = h.row_orbit[row], r = h.row_index[row];
+            const int off = h.orbit_off[o], s = h.orbit_off[o + 1] - off;
+            cd acc{0, 0};
+            for (int c = 0; c < s; ++c) {
+                const size_t e = static_cast<size_t>(h.coef_off[o] + static_cast<int64_t>(c) * s + r);
+                acc += cd{h.coef[2 * e], h.coef[2 * e + 1]} * x[h.members[off + c]];
+            }
+            y[h.members[off + r]] = acc;
+        }
+        if (h.dir == 0) dft3(y, +1);
+        for (int a = 0; a < N; ++a) {
+            out[2 * (b * N + a)] = y[a].real();
+            out[2 * (b * N + a) + 1] = y[a].imag();
+        }
+    }
 }
 
 }  // namespace fcct

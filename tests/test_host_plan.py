@@ -133,6 +133,25 @@ def test_orbit16_tables_emulated(p):
     assert np.linalg.norm(xi - x) / np.linalg.norm(x) < 1e-13
 
 
+@pytest.mark.parametrize("p", [CANON, P2])
+def test_orbit_big_tables_emulated(p):
+    """The large-n orbit-FFT executor (n = 32): column-major orbit-block rows of
+    S_n(p) / S_n(p)^{-1} n^-3 emulated as the kernel indexes them, plus the three
+    axis DFTs, against the FFT / orbit-route oracle."""
+    n = 32
+    L = _capi.lib()
+    x = np.random.default_rng(32).uniform(-1, 1, (1, n**3)) + 1j * np.random.default_rng(33).uniform(-1, 1, (1, n**3))
+    pt = (p.r, p.s, p.t)
+    route = oracle.OrbitRoute(n, pt)
+    y = np.zeros_like(x)
+    assert L.fcct_debug_emulate_orbit_big(n, *pt, 0, x.ctypes.data, y.ctypes.data, 1) == 0
+    yr = route.forward(x)
+    assert np.linalg.norm(y - yr) / np.linalg.norm(yr) < 1e-13
+    xi = np.zeros_like(x)
+    assert L.fcct_debug_emulate_orbit_big(n, *pt, 1, yr.ctypes.data, xi.ctypes.data, 1) == 0
+    assert np.linalg.norm(xi - x) / np.linalg.norm(x) < 1e-13
+
+
 def test_compiled_layouts_are_conflict_free_inside():
     # Only the first stage (natural layout from the TMA load) and the last stage
     # (natural output layout) may see shared-memory bank conflicts.
