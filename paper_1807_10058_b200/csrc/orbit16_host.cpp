@@ -30,17 +30,45 @@ bool compile_orbit16(int n, const Params& p, bool inverse, Orbit16Host& h) {
     if (!(ob.worst_condition <= 1e12))
         throw FcctError(ST_ILL_CONDITIONED, "orbit-FFT plan: orbit block condition exceeds 1e12");
     const Orbits& orb = *ob.orb;
-    // chunks of whole orbits, <= kO16Chunk slots (4 per k-tile)
-    std::vector<std::vector<int>> chunk_orbits(1);
-    int used = 0;
-    for (int o = 0; o < static_cast<int>(orb.members.size()); ++o) {
-        const int need = 4 * ((static_cast<int>(orb.members[o].size()) + 3) / 4);
-        if (used + need > kO16Chunk) {
-            chunk_orbits.emplace_back();
-            used = 0;
+    // chunks of whole orbits, <= kO16Chunk slots (4 per k-tile), formed
+    // greedily so that orbits whose members share 32-byte sectors (four
+    // consecutive positions: real f64 input) land in the same chunk: a chunk's
+    // gather then reads each sector once instead of once per chunk touching it
+    const int norb = static_cast<int>(orb.members.size());
+    auto need = [&](int o) { return 4 * ((static_cast<int>(orb.members[o].size()) + 3) / 4); };
+    std::vector<std::vector<int>> orb_keys(norb);
+    for (int o = 0; o < norb; ++o) {
+        for (int m : orb.members[o]) orb_keys[o].push_back(m >> 2);
+        std::sort(orb_keys[o].begin(), orb_keys[o].end());
+        orb_keys[o].erase(std::unique(orb_keys[o].begin(), orb_keys[o].end()), orb_keys[o].end());
+    }
+    std::vector<std::vector<int>> chunk_orbits;
+    std::vector<char> taken(norb, 0);
+    std::vector<int> key_hits(N / 4 + 1, 0);
+    for (int left = norb; left > 0;) {
+        chunk_orbits.emplace_back();
+        std::fill(key_hits.begin(), key_hits.end(), 0);
+        int used = 0;
+        while (true) {
+            int best = -1, best_score = -1;
+            for (int o = 0; o < norb; ++o) {
+                if (taken[o] || used + need(o) > kO16Chunk) continue;
+                int score = 0;
+                for (int key : orb_keys[o]) score += key_hits[key] ? 1 : 0;
+                // shared sectors first, then larger orbits, then orbit order
+                score = score * 64 + static_cast<int>(orb.members[o].size());
+                if (score > best_score) {
+                    best_score = score;
+                    best = o;
+                }
+            }
+            if (best < 0) break;
+            taken[best] = 1;
+            --left;
+            used += need(best);
+            chunk_orbits.back().push_back(best);
+            for (int key : orb_keys[best]) key_hits[key] = 1;
         }
-        chunk_orbits.back().push_back(o);
-        used += need;
     }
     const int nchunks = static_cast<int>(chunk_orbits.size());
     std::vector<std::vector<std::vector<Chain16>>> per_warp(nchunks, std::vector<std::vector<Chain16>>(kO16Warps));
