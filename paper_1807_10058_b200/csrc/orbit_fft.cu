@@ -477,10 +477,12 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
         const char* src = static_cast<const char*>(in) + t0 * in_stride;
         for (int q = 0; q < nv; ++q) tma_load_1d(buf(b) + q * C::XROW, src + q * in_stride, in_row, bar + b);
     };
-    if constexpr (DIR == 0) {
-        if (tid == 0) {
+    if (tid == 0) {
+        if constexpr (DIR == 0) {
             if (tile_of(0) < ntiles) issue_load(0, tile_of(0));
             if (tile_of(1) < ntiles) issue_load(2, tile_of(1));
+        } else {  // inverse: buffer 0 is the input tile, buffers 1 and 2 alternate as y(j mod 2)
+            if (tile_of(0) < ntiles) issue_load(0, tile_of(0));
         }
     }
     if (warp < kOfBcWarps) {
@@ -504,11 +506,11 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                                                        nvalid_of(tile));
                 named_arrive(1 + j % 3, kOfWarps * 32);  // tile j's spectrum-side buffer is ready
             } else {
-                named_sync(1 + j % 3, kOfWarps * 32);    // FFT(j) has filled y(j mod 3)
+                named_sync(1 + j % 2, kOfWarps * 32);    // FFT(j) has filled y(j mod 2)
                 char* dst = static_cast<char*>(out) + tile * TB * out_stride;
-                base_change_lean<TMAX, G, OF_C128, MO>(tab, meta_w, nt_w, buf(j % 3), C::YROW, dst, out_stride, r, k,
-                                                       nvalid);
-                named_arrive(4 + j % 3, kOfWarps * 32);  // y(j mod 3) may be refilled
+                base_change_lean<TMAX, G, OF_C128, MO>(tab, meta_w, nt_w, buf(1 + j % 2), C::YROW, dst, out_stride, r,
+                                                       k, nvalid);
+                named_arrive(4 + j % 2, kOfWarps * 32);  // y(j mod 2) may be refilled
             }
         }
     } else {
@@ -534,17 +536,24 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                     issue_load(bf, tile_of(j + 2));
                 }
             } else {
-                char* Y = buf(j % 3);
+                // the input tile arrives by TMA in buffer 0 (natural rows): the
+                // first pass reads shared memory, and buffer 0 is reloaded with
+                // tile j + 1 as soon as that pass is done
+                char* Y = buf(1 + j % 2);
                 if (ft < TB && tile_of(j + 2) < ntiles && ft < nvalid_of(tile_of(j + 2)))  // one row per thread
                     prefetch_l2_bulk(static_cast<const char*>(in) + (tile_of(j + 2) * TB + ft) * in_stride, in_row);
-                if (j >= 3) named_sync(4 + j % 3, kOfWarps * 32);  // BC(j - 3) has read y(j mod 3)
-                fft_pass_group<NN, -1, TB, 0, MI, OF_C128>(ft, static_cast<const char*>(in) + tile * TB * in_stride,
-                                                          in_stride, true, Y, C::YROW, false, nvalid);
+                mbar_wait(bar, j & 1);
+                if (j >= 2) named_sync(4 + j % 2, kOfWarps * 32);  // BC(j - 2) has read y(j mod 2)
+                fft_pass_group<NN, -1, TB, 0, MI, OF_C128>(ft, buf(0), C::XROW, true, Y, C::YROW, false, nvalid);
                 named_sync(8, kOfFftThreads);
+                if (ft == 0 && tile_of(j + 1) < ntiles) {
+                    fence_proxy_async_smem();
+                    issue_load(0, tile_of(j + 1));
+                }
                 fft_pass_group<NN, -1, TB, 1, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
                 named_sync(8, kOfFftThreads);
                 fft_pass_group<NN, -1, TB, 2, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
-                named_arrive(1 + j % 3, kOfWarps * 32);
+                named_arrive(1 + j % 2, kOfWarps * 32);
             }
         }
     }
