@@ -275,38 +275,6 @@ namespace {
 
 // CTA shapes: <TB blocks, WARPS warps>; units per warp U = 64 / WARPS
 
-__device__ __forceinline__ double lds_f64(uint32_t addr) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr) : "memory");
-    return v;
-}
-
-// Loads the (re, im) pair of one block at one slot (16 B, both data parts);
-// lanes of the two parts read the same address (broadcast).
-__device__ __forceinline__ double2 lds_pair(uint32_t addr) {
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
-    return v;
-}
-
-// part 0 lane: (a = re, as = -im); part 1 lane: (a = im, as = +re)
-__device__ __forceinline__ void split_pair(const double2 v, int part, double& a, double& as) {
-    if (part) {
-        a = v.y;
-        as = v.x;
-    } else {
-        a = v.x;
-        as = -v.y;
-    }
-}
-
-// Loads a double and flips its sign bit with `sign` (0 or 0x80000000).
-__device__ __forceinline__ double lds_f64_xor_hi(uint32_t addr, uint32_t sign) {
-    uint32_t lo, hi;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(lo), "=r"(hi) : "r"(addr) : "memory");
-    return __hiloint2double(static_cast<int>(hi ^ sign), static_cast<int>(lo));
-}
-
 // v with its sign bit xor-ed by `s` (0 or 0x80000000) on the integer pipe: a
 // plain negation compiles to DADD, which competes with DMMA for the FP64 pipe.
 __device__ __forceinline__ double xor_hi(double v, uint32_t s) {
@@ -316,19 +284,6 @@ __device__ __forceinline__ double xor_hi(double v, uint32_t s) {
     double o;
     asm("mov.b64 %0, {%1, %2};" : "=d"(o) : "r"(lo), "r"(hi));
     return o;
-}
-
-__device__ __forceinline__ double flip_unless(double v, int part) {
-    // part == 0 (re rows of the swapped operand): -x_im; part == 1: +x_re
-    return __hiloint2double(__double2hiint(v) ^ (part ? 0 : static_cast<int>(0x80000000u)), __double2loint(v));
-}
-
-__device__ __forceinline__ void cp_async8_ca(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-
-__device__ __forceinline__ void cp_async4_ca(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
 template <int MT>
