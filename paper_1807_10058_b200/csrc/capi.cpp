@@ -569,6 +569,7 @@ struct fcct_plan_s {
     int num_sms = 148;
     bool radix = false;
     std::shared_ptr<const PlanNode> tree;
+    bool tree_exact = false;  // built here by build_tree: the exact factorisation by construction
     PipelineTables fwd, inv;
     bool offt = false;  // orbit-FFT executor (telescoped radix tree, orbit_fft.hpp)
     OrbitFftTables ofwd, ofinv;
@@ -941,13 +942,20 @@ bool tree_matches(const PlanNode& a, const PlanNode& b, long double tol) {
     return true;
 }
 
+// The orbit-FFT executors compute F_n S_n(p), i.e. the exact factorisation: a
+// tree built here is exact by construction; a loaded (PlanStore) or perturbed
+// tree is compared against a fresh derivation.
+bool tree_is_exact(const fcct_plan_s* pl) {
+    return pl->tree_exact || tree_matches(*pl->tree, *build_tree(pl->n, pl->p), 1e-9L);
+}
+
 // Orbit-FFT executor for n = 4, 8: the radix tree telescoped to S_n then the
 // radix-2 FFT (orbit_fft.hpp). Valid when the plan's tree is the exact
 // factorisation of D_n(p) (it then represents F_n S_n(p) exactly).
 void build_orbit_fft(fcct_plan_s* pl) {
     pl->offt = false;
     if (pl->n != 4 && pl->n != 8) return;
-    if (!tree_matches(*pl->tree, *build_tree(pl->n, pl->p), 1e-9L)) return;
+    if (!tree_is_exact(pl)) return;
     // default: the warp-specialised kernel (12 base-change + 4 FFT warps);
     // FCCT_OFFT_WS=0 selects the phased one (16 warps alternate both roles)
     const char* ws = std::getenv("FCCT_OFFT_WS");
@@ -973,7 +981,7 @@ void build_fast_paths(fcct_plan_s* pl) {
     if (f.empty() || f == "orbit") {  // n = 16: the two-pass orbit-FFT executor
         pl->o16 = false;
         Orbit16Host hf, hi;
-        if (pl->n == 16 && tree_matches(*pl->tree, *build_tree(pl->n, pl->p), 1e-9L) &&
+        if (pl->n == 16 && tree_is_exact(pl) &&
             compile_orbit16(pl->n, pl->p, false, hf) && compile_orbit16(pl->n, pl->p, true, hi)) {
             upload_orbit16(hf, pl->o16fwd);
             upload_orbit16(hi, pl->o16inv);
@@ -981,7 +989,7 @@ void build_fast_paths(fcct_plan_s* pl) {
             return;
         }
         pl->obig = false;
-        if ((pl->n == 32 || pl->n == 64) && !f32 && tree_matches(*pl->tree, *build_tree(pl->n, pl->p), 1e-9L)) {
+        if ((pl->n == 32 || pl->n == 64) && !f32 && tree_is_exact(pl)) {
             OrbitBigHost h;
             if (compile_orbit_big(pl->n, pl->p, false, h)) {
                 upload_orbit_big(h, pl->obfwd);
@@ -1103,6 +1111,7 @@ fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int 
             pl->tree = store->load_or_build(n, p);
         } else {
             pl->tree = build_tree(n, p);  // degeneracy + condition gates inside
+            pl->tree_exact = true;
         }
         pl->radix = true;
         build_fast_paths(pl.get());
