@@ -322,10 +322,19 @@ __global__ void __launch_bounds__(kFftThreads, 2)
         for (int x = 0; x < NN; ++x) v[x] = X[swz(x, hi, lo)];
         fft_line16<NN, SIGN>(v);
         char* dst = static_cast<char*>(out) + blk * out_row;
+        if constexpr (SIGN > 0) {
 #pragma unroll
-        for (int x = 0; x < NN; ++x) {
-            const int a = (x * NN + hi) * NN + lo;
-            st_el<MO>(dst, SIGN > 0 ? a : zp[a], v[x].x, v[x].y);  // inverse: z in orbit order
+            for (int x = 0; x < NN; ++x) st_el<MO>(dst, (x * NN + hi) * NN + lo, v[x].x, v[x].y);
+        } else {
+            // inverse: z is stored in orbit order; the lines go back into the
+            // tile at their orbit-order slots first, then the row leaves in
+            // contiguous 16-byte stores
+            __syncthreads();  // every line of the i pass has been read
+#pragma unroll
+            for (int x = 0; x < NN; ++x) X[zp[(x * NN + hi) * NN + lo]] = v[x];
+            __syncthreads();
+            double2* d2 = reinterpret_cast<double2*>(dst);
+            for (int a = tid; a < N; a += kFftThreads) d2[a] = X[a];
         }
         __syncthreads();  // the tile is refilled by the next block
     }
