@@ -287,10 +287,10 @@ __global__ void __launch_bounds__(kFftThreads, 2)
         const int64_t nx = blk + gridDim.x;
         if (tid == 0 && nx < batch) prefetch_l2_bulk(static_cast<const char*>(in) + nx * in_row, static_cast<uint32_t>(in_row));
         const char* src = static_cast<const char*>(in) + blk * in_row;
-        for (int a = tid; a < N; a += kFftThreads) {  // natural (or orbit-ordered z) -> swizzled tile
+        for (int a = tid; a < N; a += kFftThreads) {  // natural (or orbit-ordered z) -> tile
             const int k = a % NN, j = (a / NN) % NN, i = a / (NN * NN);
-            if constexpr (SIGN > 0) {  // forward: z in orbit order
-                cp_async_n<16>(X + swz(i, j, k), src + static_cast<int64_t>(zp[a]) * 16, true);
+            if constexpr (SIGN > 0) {  // forward: z (orbit order) copied contiguously; un-permuted by the k pass
+                cp_async_n<16>(X + a, src + static_cast<int64_t>(a) * 16, true);
             } else if constexpr (MI == OF_C128) {
                 cp_async_n<16>(X + swz(i, j, k), src + static_cast<int64_t>(a) * 16, true);
             } else {
@@ -304,8 +304,14 @@ __global__ void __launch_bounds__(kFftThreads, 2)
         __syncthreads();
         double2 v[NN];
         // k axis: line (i, j) = (hi, lo)
+        if constexpr (SIGN > 0) {  // the tile holds z in orbit order: gather, then write the swizzled layout
 #pragma unroll
-        for (int x = 0; x < NN; ++x) v[x] = X[swz(hi, lo, x)];
+            for (int x = 0; x < NN; ++x) v[x] = X[zp[(hi * NN + lo) * NN + x]];
+            __syncthreads();  // every line has been read before the tile is rewritten
+        } else {
+#pragma unroll
+            for (int x = 0; x < NN; ++x) v[x] = X[swz(hi, lo, x)];
+        }
         fft_line16<NN, SIGN>(v);
 #pragma unroll
         for (int x = 0; x < NN; ++x) X[swz(hi, lo, x)] = v[x];
