@@ -92,7 +92,7 @@ bool compile_orbit16(int n, const Params& p, bool inverse, Orbit16Host& h) {
         }
         tmax = std::max(tmax, *std::max_element(load.begin(), load.end()));
     }
-    tmax = (tmax + 3) / 4 * 4;  // the kernel's operator ring (4 deep) stays chunk-aligned
+    tmax = (tmax + kO16Wrap - 1) / kO16Wrap * kO16Wrap;  // the kernel's operator ring stays chunk-aligned
     if (tmax > kO16Tmax) return false;
     h = Orbit16Host{};
     h.n = n;
