@@ -29,7 +29,7 @@ struct Params;
 constexpr int kO16Warps = 16;
 constexpr int kO16Chunk = 256;  // member slots per chunk (4 per k-tile)
 constexpr int kO16Tmax = 16;    // tiles per warp per chunk
-constexpr int kO16Wrap = 6;     // operator tiles in flight per warp (the stream's look-ahead)
+constexpr int kO16Wrap = 12;    // operator tiles in flight per warp (the stream's look-ahead)
 
 struct Orbit16Desc {
     int n = 0, N = 0, dir = 0;
