@@ -15,6 +15,7 @@ ap.add_argument("--blocks", type=int, default=65536)
 ap.add_argument("--method", default="fast")
 ap.add_argument("--precision", default="f64")
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--real", action="store_true", help="real samples in and out (fcct_forward_real / fcct_inverse_real)")
 a = ap.parse_args()
 p = SkewParams.canonical()
 plan = build_plan(a.n, p, precision=a.precision) if a.method == "fast" else dense_transform(a.n, p, precision=a.precision)._plan
@@ -22,8 +23,14 @@ dt = torch.complex64 if a.precision == "f32" else torch.complex128
 x = torch.randn(a.blocks, a.n**3, dtype=dt, device="cuda")
 y = torch.empty_like(x)
 L = _capi.lib()
+if a.real:
+    x = torch.randn(a.blocks, a.n**3, dtype=torch.float32 if a.precision == "f32" else torch.float64, device="cuda")
 for _ in range(a.reps):
-    _raise(L.fcct_forward(plan._h, x.data_ptr(), y.data_ptr(), a.blocks, None))
-    _raise(L.fcct_inverse(plan._h, y.data_ptr(), x.data_ptr(), a.blocks, None))
+    if a.real:
+        _raise(L.fcct_forward_real(plan._h, x.data_ptr(), y.data_ptr(), a.blocks, None))
+        _raise(L.fcct_inverse_real(plan._h, y.data_ptr(), x.data_ptr(), a.blocks, None))
+    else:
+        _raise(L.fcct_forward(plan._h, x.data_ptr(), y.data_ptr(), a.blocks, None))
+        _raise(L.fcct_inverse(plan._h, y.data_ptr(), x.data_ptr(), a.blocks, None))
 torch.cuda.synchronize()
 print("ok")
