@@ -100,8 +100,10 @@ __global__ void __launch_bounds__(kO16Warps * 32, 1)
     const int64_t items = (ngroups > blockIdx.x ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0) * nch;
     int gc = 0;            // chunk of the next gather
     int64_t ggrp = blockIdx.x;  // group of the next gather
-    auto gather = [&](int64_t item) {
-        char* st = stage + (item % 3) * SBUF;
+    int gbuf = 0;  // stage buffer of the next gather (rotates 0, 1, 2)
+    auto gather = [&]() {
+        char* st = stage + gbuf * SBUF;
+        gbuf = gbuf == 2 ? 0 : gbuf + 1;
         const int c = gc;
         const int64_t grp = ggrp;
         if (++gc == nch) {
@@ -115,9 +117,15 @@ __global__ void __launch_bounds__(kO16Warps * 32, 1)
         const bool bvalid = b < batch - grp * 8;
         const char* srow = static_cast<const char*>(in) + (grp * 8 + (bvalid ? b : 0)) * in_row;
         char* dst = st + (s0 * 8 + (b ^ (2 * (s0 & 3)))) * SEB;
+        // all list entries first: each cp.async is a compiler memory barrier,
+        // a load between two of them would wait out its full latency
+        constexpr int E = kO16Chunk * 8 / (kO16Warps * 32);
+        int pe[E];
 #pragma unroll
-        for (int e = 0; e < kO16Chunk * 8 / (kO16Warps * 32); ++e) {
-            const int p = gl[e * 64];
+        for (int e = 0; e < E; ++e) pe[e] = gl[e * 64];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int p = pe[e];
             if (p >= 0 || (s0 & 3) != 0)  // slots of an unused k-tile are never read
                 cp_async_n<SEB>(dst + e * 64 * 8 * SEB, srow + static_cast<int64_t>(p > 0 ? p : 0) * SEB,
                                 p >= 0 && bvalid);
@@ -138,18 +146,19 @@ __global__ void __launch_bounds__(kO16Warps * 32, 1)
     tp += kRingA * 32;
     // three stage buffers: chunk item + 2 is gathered while item is computed,
     // one barrier per chunk
-    if (items > 0) gather(0);
-    if (items > 1) gather(1); else cp_async_commit();
-    int c = 0;
+    if (items > 0) gather();
+    if (items > 1) gather(); else cp_async_commit();
+    int c = 0, cbuf = 0;
     int64_t grp = blockIdx.x;
     for (int64_t item = 0; item < items; ++item) {
         cp_async_wait<1>();  // this thread's copies of chunk `item` have landed
         __syncthreads();     // ... everyone's; and every warp is done with chunk item - 1
         if (item + 2 < items)
-            gather(item + 2);  // into the buffer chunk item - 1 used
+            gather();  // chunk item + 2, into the buffer chunk item - 1 used
         else
             cp_async_commit();  // keep one group per iteration
-        const char* st = stage + (item % 3) * SBUF;
+        const char* st = stage + cbuf * SBUF;
+        cbuf = cbuf == 2 ? 0 : cbuf + 1;
         const int64_t nv = batch - grp * 8;
         const bool live = r < nv;
         char* d_row = static_cast<char*>(out) + (grp * 8 + r) * out_row;
