@@ -563,7 +563,18 @@ def test_n16_two_pass_orbit_fft(cuda, oracle_mod, p):
     xr = torch.from_numpy(x.real.copy()).to(cuda)
     yr = plan.apply_values(xr)
     assert torch.equal(yr, plan.apply_values(torch.complex(xr, torch.zeros_like(xr))))
-    assert torch.equal(plan._run(yr, True, real_out=True), plan._run(yr, True).real.contiguous())
+    xr_back = plan._run(yr, True, real_out=True)
+    assert torch.equal(xr_back, plan._run(yr, True).real.contiguous())
+    # real output at an 8-byte (not 16-byte) aligned address: the un-permute's
+    # element-per-thread kernel, bitwise the row-staged one
+    import ctypes
+    from paper_1807_10058_b200 import _capi
+    from paper_1807_10058_b200.fcct import _raise
+    buf = torch.zeros(yr.shape[0] * n**3 + 1, dtype=torch.float64, device=cuda)
+    _raise(_capi.lib().fcct_inverse_real(plan._h, ctypes.c_void_p(yr.data_ptr()), ctypes.c_void_p(buf.data_ptr() + 8),
+                                         yr.shape[0], None))
+    torch.cuda.synchronize()
+    assert torch.equal(buf[1:].view(yr.shape[0], n**3), xr_back)
     # fp32 I/O (complex64 in HBM, fp64 arithmetic)
     p32 = build_plan(n, p, precision="f32")
     assert p32.info.executor == 6
