@@ -24,3 +24,34 @@ def test_reference_arm_json_line():
     assert line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port"
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_own_arm_json_line():
+    """bench.py's own arm on a small config: one JSON line with the contract's
+    keys, the roofline and cpu_baseline objects, an e2e through host buffers,
+    clocks sampled under load and a nonzero count of this repo's launches."""
+    out = subprocess.run(
+        [sys.executable, str(ROOT / "bench.py"), "--config", "c1", "--steps", "3", "--warmup", "3",
+         "--cpu-seconds", "0.5", "--cpu-sample", "64", "--e2e-blocks", "64", "--e2e-steps", "2"],
+        check=True, capture_output=True, text=True, cwd=ROOT,
+    )
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+                "clocks", "gpu_launches"):
+        assert key in line, key
+    assert line["n_gpus"] == 1 and line["steps"] == 3 and line["value"] > 0
+    assert "workload" in line["config"]
+    roof = line["roofline"]
+    for key in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert key in roof, key
+    assert roof["bound"] in ("hbm", "tensor") and roof["peak"] > 0
+    assert abs(roof["frac"] - roof["achieved"] / roof["peak"]) < 1e-9
+    cpu = line["cpu_baseline"]
+    assert cpu["value"] > 0 and cpu["kind"] in ("port", "reference") and cpu["cores"] >= 1
+    e2e = line["e2e"]
+    assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
+    assert line["gpu_launches"] > 0
+    assert line["clocks"]["sm_max_mhz"] > 0
