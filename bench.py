@@ -100,27 +100,37 @@ class ClockSampler:
 
 
 def profiled_traffic(cfg_name: str, f32: bool, executor: int):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one forward launch of the
-    dominant kernel from the committed `ncu --set full` capture (c2 fp64,
-    tools/prof_run.py, 65,536 blocks): profiles/r01_orbit_fft_ws_raw.csv for
-    the orbit-FFT executor, profiles/r01_pipeline2_raw.csv for the stage
-    pipeline; None when the run is not that configuration."""
-    files = {2: "r01_pipeline2_raw.csv", 5: "r01_orbit_fft_ws_raw.csv"}
-    if cfg_name != "c2" or f32 or executor not in files:
+    """dram__bytes_read.sum + dram__bytes_write.sum of one forward call of the
+    dominant kernel(s) from the committed `ncu --set full` captures; None when
+    the run is not a captured configuration.
+    c2 fp64 (tools/prof_run.py, 65,536 blocks): profiles/r01_orbit_fft_ws_raw.csv
+    (orbit-FFT executor) or profiles/r01_pipeline2_raw.csv (stage pipeline).
+    c3 (16,384 blocks, real f64 input): the forward base change from
+    profiles/r01_orbit16_passA_raw.csv (`prof_run.py --n 16 --real`) plus the
+    forward cube FFT from profiles/r01_orbit16_raw.csv (z is complex128 either way)."""
+    parts = {
+        ("c2", 2): [("r01_pipeline2_raw.csv", None)],
+        ("c2", 5): [("r01_orbit_fft_ws_raw.csv", None)],
+        ("c3", 6): [("r01_orbit16_passA_raw.csv", "orbit16_base_kernel<0, 2, 0>"),
+                    ("r01_orbit16_raw.csv", "fft_cube_kernel<16, 1,")],
+    }.get((cfg_name, executor))
+    if f32 or parts is None:
         return None
-    path = Path(__file__).resolve().parent / "profiles" / files[executor]
     try:
         import csv
 
-        rows = list(csv.reader(open(path)))
-        hdr, units, vals = rows[0], rows[1], rows[2]
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         tot = 0.0
-        for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            i = hdr.index(name)
-            tot += float(vals[i]) * scale[units[i]]
+        for fname, kernel in parts:
+            rows = list(csv.reader(open(Path(__file__).resolve().parent / "profiles" / fname)))
+            hdr, units = rows[0], rows[1]
+            ki = hdr.index("Kernel Name")
+            vals = next(r for r in rows[2:] if kernel is None or kernel in r[ki])
+            for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                i = hdr.index(name)
+                tot += float(vals[i]) * scale[units[i]]
         return tot
-    except (OSError, ValueError, KeyError, IndexError):
+    except (OSError, ValueError, KeyError, IndexError, StopIteration):
         return None
 
 
@@ -487,6 +497,10 @@ def b200_arm(args):
         "inv_ms": inv_ms,
         "inverse_achieved_tflops": info.flops_inverse * blocks / (inv_ms / 1e3) / 1e12,
     }
+    if info.executor == 6 and roof["traffic"] is not None:
+        roof["traffic_note"] = ("two kernels per forward call: the base change writes z (complex128, orbit order) "
+                                "and the cube FFT reads it back, 2 x 16 B per point by design on top of the "
+                                "algorithmic bytes (ncu: pass A 0.57 + 1.02 GB, pass B 1.13 + 1.03 GB)")
     if info.exec_flops_forward > 0:
         # what the executor really issues on the FP64 pipes (the orbit-FFT route
         # telescopes the tree: fewer flops than SURVEY.md's algorithmic count)
