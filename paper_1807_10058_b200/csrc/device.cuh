@@ -101,6 +101,13 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// --- programmatic dependent launch ---------------------------------------
+// pdl_wait: block until the preceding kernel in the stream has completed and
+// its memory is visible (a no-op without the launch attribute); pdl_trigger:
+// let the next kernel's CTAs be scheduled (their prologue overlaps this tail)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // --- cp.async 16B with zero fill ----------------------------------------
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
     const int sz = valid ? 16 : 0;

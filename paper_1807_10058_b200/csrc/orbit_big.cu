@@ -15,13 +15,17 @@ namespace {
 __global__ void __launch_bounds__(256) orbit_big_s_kernel(const __grid_constant__ OrbitBigDesc d,
                                                           const double2* __restrict__ x, double2* __restrict__ y,
                                                           int64_t batch) {
+    // no early trigger: this grid runs in several waves, and dependents
+    // scheduled during them slowed the forward (60 vs 50 us at n = 64)
     const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (row >= d.rows) return;
+    // plan tables (constant) before the wait; x is the previous kernel's output
     const int o = __ldg(d.row_orbit + row), r = __ldg(d.row_index + row);
     const int off = __ldg(d.orbit_off + o), s = __ldg(d.orbit_off + o + 1) - off;
     const double2* __restrict__ cf = d.coef + __ldg(d.coef_off + o) + r;
     const int* __restrict__ mem = d.members + off;
     const int out = __ldg(mem + r);
+    pdl_wait();
     for (int64_t b = 0; b < batch; ++b) {
         const double2* xb = x + b * d.N;
         double re = 0.0, im = 0.0;
@@ -62,11 +66,13 @@ __global__ void __launch_bounds__(256) line_fft_kernel(const double2* __restrict
     __shared__ double2 buf[kLines][NN];
     __shared__ double2 tw[NN / 2];
     const int tid = threadIdx.x;
+    pdl_trigger();
     for (int e = tid; e < NN / 2; e += blockDim.x) {
         double sv, cv;
         sincospi(2.0 * e / NN, &sv, &cv);
         tw[e] = make_double2(cv, SIGN * sv);
     }
+    pdl_wait();  // the twiddles overlap the previous kernel's tail
     // line group g: lines (u, ., v0 + l) along the axis, l = 0..7 contiguous in memory
     const int64_t groups_per_block = static_cast<int64_t>(NN) * NN / kLines;
     const int64_t g = blockIdx.x;
@@ -178,12 +184,14 @@ __global__ void __launch_bounds__(256) line_fft64_kernel(const double2* __restri
     __shared__ double2 ex[LPC][8][9];                   // [line][t][q], padded
     __shared__ double2 tw[NN];                          // w64^e
     const int tid = threadIdx.x, t = tid & 7, li = tid >> 3;  // 8 threads per line
+    pdl_trigger();
     if (tid < NN) {
         double sv, cv;
         sincospi(2.0 * tid / NN, &sv, &cv);
         tw[tid] = make_double2(cv, SIGN * sv);
     }
     __syncthreads();
+    pdl_wait();  // the twiddles overlap the previous kernel's tail
     const int64_t line = static_cast<int64_t>(blockIdx.x) * LPC + li;  // global line id
     const int64_t b = line / (NN * NN);
     if (b >= batch) return;
@@ -221,14 +229,39 @@ __global__ void __launch_bounds__(256) line_fft64_kernel(const double2* __restri
     for (int u = 0; u < 8; ++u) dst[(t + 8 * u) * step] = v[u];
 }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FCCT_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// launch with programmatic stream serialisation: the kernel may start while
+// the previous one in the stream drains; it waits (pdl_wait) before touching
+// that kernel's output
+template <typename... P, typename... A>
+cudaError_t launch_pdl(void (*kern)(P...), unsigned grid, unsigned block, cudaStream_t st, A... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<P>(args)...);
+}
+
 }  // namespace
 
 cudaError_t launch_orbit_big_s(const OrbitBigDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st) {
     if (batch <= 0) return cudaSuccess;
     const int64_t blocks = (d.rows + 255) / 256;
-    orbit_big_s_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(d, static_cast<const double2*>(in),
-                                                                      static_cast<double2*>(out), batch);
-    return cudaGetLastError();
+    return launch_pdl(orbit_big_s_kernel, static_cast<unsigned>(blocks), 256, st, d, static_cast<const double2*>(in),
+                      static_cast<double2*>(out), batch);
 }
 
 cudaError_t launch_line_fft(int n, int axis, int sign, const void* in, void* out, int64_t batch, cudaStream_t st) {
@@ -236,20 +269,15 @@ cudaError_t launch_line_fft(int n, int axis, int sign, const void* in, void* out
     const int64_t grid = batch * static_cast<int64_t>(n) * n / kLines;
     auto* i = static_cast<const double2*>(in);
     auto* o = static_cast<double2*>(out);
-#define LFFT(NV, SV) line_fft_kernel<NV, SV><<<static_cast<unsigned>(grid), 256, 0, st>>>(i, o, axis, batch)
     if (n == 64) {  // 8 x 8 decomposition, 32 lines per CTA
-        const int64_t g64 = batch * 64 * 64 / 32;
-        if (sign > 0)
-            line_fft64_kernel<1><<<static_cast<unsigned>(g64), 256, 0, st>>>(i, o, axis, batch);
-        else
-            line_fft64_kernel<-1><<<static_cast<unsigned>(g64), 256, 0, st>>>(i, o, axis, batch);
-    } else if (n == 32) {
-        if (sign > 0) LFFT(32, 1); else LFFT(32, -1);
-    } else {
-        return cudaErrorInvalidValue;
+        const unsigned g64 = static_cast<unsigned>(batch * 64 * 64 / 32);
+        return sign > 0 ? launch_pdl(line_fft64_kernel<1>, g64, 256, st, i, o, axis, batch)
+                        : launch_pdl(line_fft64_kernel<-1>, g64, 256, st, i, o, axis, batch);
     }
-#undef LFFT
-    return cudaGetLastError();
+    if (n == 32)
+        return sign > 0 ? launch_pdl(line_fft_kernel<32, 1>, static_cast<unsigned>(grid), 256, st, i, o, axis, batch)
+                        : launch_pdl(line_fft_kernel<32, -1>, static_cast<unsigned>(grid), 256, st, i, o, axis, batch);
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace fcct
