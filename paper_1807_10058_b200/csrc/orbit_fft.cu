@@ -14,6 +14,7 @@
 // The base-change operator is register resident: each warp owns a fixed set
 // of DMMA tiles (<= TMAX) for the whole kernel, so no table traffic remains.
 #include <algorithm>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "orbit_fft.hpp"
@@ -454,6 +455,7 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
     char* buf0 = reinterpret_cast<char*>(smem + 128 + C::META);
     auto buf = [&](int b) { return buf0 + b * C::BUF; };
     const int tid = threadIdx.x, warp = tid >> 5;
+    pdl_trigger();  // one CTA per SM: the next launch's CTAs take SMs as these exit
     const int64_t ntiles = (batch + TB - 1) / TB;
     constexpr uint32_t in_row = N * mode_bytes(MI), out_row = N * mode_bytes(MO);
     // bytes between consecutive block rows (a strided batch: the two-level
@@ -477,17 +479,21 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
         const char* src = static_cast<const char*>(in) + t0 * in_stride;
         for (int q = 0; q < nv; ++q) tma_load_1d(buf(b) + q * C::XROW, src + q * in_stride, in_row, bar + b);
     };
-    if (tid == 0) {
-        if constexpr (DIR == 0) {
-            if (tile_of(0) < ntiles) issue_load(0, tile_of(0));
-            if (tile_of(1) < ntiles) issue_load(2, tile_of(1));
-        } else {  // inverse: buffer 0 is the input tile, buffers 1 and 2 alternate as y(j mod 2)
-            if (tile_of(0) < ntiles) issue_load(0, tile_of(0));
-        }
-    }
     if (warp < kOfBcWarps) {
         // ---------------- base-change group ----------------
         const int lane = tid & 31, r = lane >> 2, k = lane & 3;
+        // the previous kernel's output (this launch's input, or a buffer this
+        // launch writes) only after the wait; the input tile is requested first,
+        // the resident operator tiles load while it is in flight
+        pdl_wait();
+        if (tid == 0) {
+            if constexpr (DIR == 0) {
+                if (tile_of(0) < ntiles) issue_load(0, tile_of(0));
+                if (tile_of(1) < ntiles) issue_load(2, tile_of(1));
+            } else {  // inverse: buffer 0 is the input tile, buffers 1 and 2 alternate as y(j mod 2)
+                if (tile_of(0) < ntiles) issue_load(0, tile_of(0));
+            }
+        }
         double2 tab[TMAX];
 #pragma unroll
         for (int t = 0; t < TMAX; ++t)
@@ -515,6 +521,7 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
         }
     } else {
         // ---------------- FFT group ----------------
+        pdl_wait();
         const int ft = tid - kOfBcWarps * 32;
         for (int j = 0; tile_of(j) < ntiles; ++j) {
             const int64_t tile = tile_of(j);
@@ -575,8 +582,23 @@ cudaError_t launch_ws_t(const OrbitFftDesc& d, const void* in, void* out, int64_
     }
     const int64_t ntiles = (batch + C::TB - 1) / C::TB;
     const int64_t grid = std::min<int64_t>(ntiles, num_sms);
-    kern<<<static_cast<unsigned>(grid), kOfWarps * 32, C::SMEM, st>>>(d, in, out, batch);
-    return cudaGetLastError();
+    // programmatic dependent launch: this kernel's table prologue overlaps the
+    // previous kernel's tail (FCCT_PDL=0 disables)
+    static const bool pdl = [] {
+        const char* e = std::getenv("FCCT_PDL");
+        return !(e && e[0] == '0');
+    }();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kOfWarps * 32);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, d, in, out, batch);
 }
 
 template <int NN, int DIR, int MI, int MO, int TMAX>
