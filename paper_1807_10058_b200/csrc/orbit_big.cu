@@ -12,7 +12,11 @@ using namespace dev;
 namespace {
 
 // y[b][members[off + r]] = sum_c coef[cbase + c s + r] x[b][members[off + c]]
-__global__ void __launch_bounds__(256) orbit_big_s_kernel(const __grid_constant__ OrbitBigDesc d,
+// __launch_bounds__(256, 4): a 64-register cap. Unbounded, ptxas compiled 34
+// registers and kept ~2 of a row's 24 coefficient loads in flight (latency
+// bound: 29 us at n = 64). 62 registers hoist most of them with 4 CTAs per SM:
+// 44 -> 35 us per direction. (256, 1) / 3 / 5 measured 46 / 36 / 38 us.
+__global__ void __launch_bounds__(256, 4) orbit_big_s_kernel(const __grid_constant__ OrbitBigDesc d,
                                                           const double2* __restrict__ x, double2* __restrict__ y,
                                                           int64_t batch) {
     // no early trigger: this grid runs in several waves, and dependents
