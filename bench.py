@@ -179,7 +179,7 @@ CONFIGS = {
 
 def node_real_coords(n, dev):
     """Real coordinates ((x+z)/2, Re y, (x-z)/(2i)) of the canonical skew nodes
-    (real_coords, chebyshev.cpp:383-393), from the device-generated node set."""
+    (real_coords, chebyshev.cpp:87-97), from the device-generated node set."""
     from paper_1807_10058_b200 import SkewParams, skew_nodes
 
     nodes = skew_nodes(n, SkewParams.canonical(), device=dev)

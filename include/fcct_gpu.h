@@ -36,7 +36,7 @@ typedef enum {
     FCCT_INVALID_ARGUMENT = 1, /* std::invalid_argument (n < 1, bad params) */
     FCCT_SIZE_MISMATCH = 2,    /* SizeMismatch (transform.cpp:147-154,498-521) */
     FCCT_ODD_SIZE = 3,         /* OddSize (transform.cpp:173-175,315-317) */
-    FCCT_DEGENERATE_NODES = 4, /* DegenerateNodes (spectral.cpp:132-149) */
+    FCCT_DEGENERATE_NODES = 4, /* DegenerateNodes (spectral.cpp:26-43) */
     FCCT_ILL_CONDITIONED = 5,  /* IllConditioned (transform.cpp:113-117,377-378) */
     FCCT_PARAMS_MISMATCH = 6,  /* invalid_argument "different skew grid" (:163-165,515-517) */
     FCCT_IO = 7,               /* MalformedFile / IoFailure */
@@ -138,9 +138,9 @@ fcct_status fcct_radix_permutation(int n, uint64_t* out_host);
  * complex128, generated on the device into the caller's device buffer. */
 fcct_status fcct_dense_matrix(int n, double r, double s, double t, void* out_device, void* stream);
 
-/* Skew node set (skew_nodes, spectral.cpp:261-277) generated on the device:
+/* Skew node set (skew_nodes, spectral.cpp:155-171) generated on the device:
  * per node 6 complex128 values (u, v, w, x, y, z); runs the degeneracy check
- * for n <= 16 (spectral.cpp:132-149). */
+ * for n <= 16 (spectral.cpp:26-43). */
 fcct_status fcct_skew_nodes(int n, double r, double s, double t, void* out_device, void* stream);
 
 /* TransformPlan accessors (transform.hpp:71-84). kernel(): 8x8 column-major
@@ -200,12 +200,12 @@ fcct_status fcct_shard_range(int64_t total, int rank, int world, int64_t* begin,
  * outputs go to `path`, where NULL or "-" means stdout (fcct.cpp:44-54).
  * ------------------------------------------------------------------------- */
 
-/* parse_params / SkewParams::encode (spectral.cpp:79-128): "r,s,t" with
+/* parse_params / SkewParams::encode (spectral.cpp:77-117): "r,s,t" with
  * fields "a/b" or decimals. encode writes at most `len` bytes incl. the NUL. */
 fcct_status fcct_parse_params(const char* text, double* r, double* s, double* t);
 fcct_status fcct_encode_params(double r, double s, double t, char* buf, int64_t len);
 
-/* export_nodes_csv of skew_nodes(n, params) (spectral.cpp:155-188; CLI `zeros`):
+/* export_nodes_csv of skew_nodes(n, params) (spectral.cpp:155-171,180-188; CLI `zeros`):
  * "i,j,k,x,y,z" + one %.17g row per node. DEGENERATE_NODES as skew_nodes. */
 fcct_status fcct_export_nodes_csv(int n, double r, double s, double t, const char* path);
 

@@ -110,7 +110,7 @@ const std::vector<Elem>& group() {
     return g;
 }
 
-// --- unit phases: src/transform.cpp:28-30, src/spectral.cpp:124-126 ------
+// --- unit phases: src/transform.cpp:28-30, src/spectral.cpp:18-20 --------
 Complex unit_phase(double turns) {
     return Complex{std::cos(two_pi * turns), std::sin(two_pi * turns)};
 }
@@ -119,25 +119,25 @@ struct Params {
     double r, s, t;
 };
 
-// SkewParams::child, src/spectral.cpp:155-157
+// SkewParams::child, src/spectral.cpp:49-51
 Params child_params(const Params& p, int ir, int is, int it) {
     return Params{(p.r + ir) / 2.0, (p.s + is) / 2.0, (p.t + it) / 2.0};
 }
 
-// --- nodes: src/chebyshev.cpp:326-342, src/spectral.cpp:132-149,261-277 ---
+// --- nodes: src/chebyshev.cpp:30-46,76-85, src/spectral.cpp:26-43,136-171 -
 struct Node {
     Index3 ijk;
     Complex u, v, w;
     Complex x, y, z;
 };
 
-double wrap_turn(double a) {  // TorusPoint::wrapped, src/chebyshev.cpp:326-335
+double wrap_turn(double a) {  // TorusPoint::wrapped, src/chebyshev.cpp:30-39
     double f = a - std::floor(a);
     if (f >= 1.0 - 1e-15) f = 0.0;
     return f;
 }
 
-void coords_from_uvw(Node& nd) {  // src/chebyshev.cpp:372-381
+void coords_from_uvw(Node& nd) {  // src/chebyshev.cpp:76-85
     const Complex u = nd.u, v = nd.v, w = nd.w;
     const Complex ui = 1.0 / u, vi = 1.0 / v, wi = 1.0 / w;
     nd.x = 0.25 * (u + ui * v + vi * w + wi);
@@ -163,7 +163,7 @@ std::vector<Node> skew_nodes(int n, const Params& p, bool check) {
                 coords_from_uvw(nd);
                 nodes.push_back(nd);
             }
-    // check_not_degenerate: n <= 16 only (src/spectral.cpp:132-149)
+    // check_not_degenerate: n <= 16 only (src/spectral.cpp:26-43)
     if (check && n <= 16) {
         constexpr double th = 1e-9 * 1e-9;
         for (size_t a = 0; a < nodes.size(); ++a)
@@ -179,7 +179,7 @@ std::vector<Node> skew_nodes(int n, const Params& p, bool check) {
     return nodes;
 }
 
-// common_zeros, src/spectral.cpp:242-259
+// common_zeros, src/spectral.cpp:136-153
 std::vector<Node> common_zeros(int n) {
     std::vector<Node> nodes;
     for (int i = 0; i < n; ++i)
@@ -196,7 +196,7 @@ std::vector<Node> common_zeros(int n) {
     return nodes;
 }
 
-// --- Chebyshev evaluation: src/chebyshev.cpp:310-322,363-370 -------------
+// --- Chebyshev evaluation: src/chebyshev.cpp:14-26 (ipow), :67-74 --------
 Complex ipow(Complex base, int e) {
     if (e < 0) {
         base = 1.0 / base;
@@ -795,6 +795,56 @@ int oracle_forward_dense(int n, double r, double s, double t, int64_t batch,
             for (int64_t i = 0; i < n3; ++i) {
                 y[2 * n3 * b + 2 * i] = static_cast<double>(acc[i].real());
                 y[2 * n3 * b + 2 * i + 1] = static_cast<double>(acc[i].imag());
+            }
+        }
+    })
+}
+
+// Selected rows of y = D x in long double, without forming D: row i of D_n(p)
+// at node (i0, i1, i2) is (1/24) sum_w e^{2 pi i (w kappa).(p + (i0,i1,i2))/n}
+// (the ColumnEvaluator sum, src/transform.cpp:35-82, read along a row), so
+// y_i = sum_kappa x_kappa D[i, kappa] costs 24 N long-double products per row.
+// An oracle for n = 16 (and up) that shares nothing with the orbit/FFT route.
+// x: [batch][N], y: [batch][nrows] complex128.
+int oracle_dense_rows(int n, double r, double s, double t, int64_t nrows, const int64_t* rows,
+                      int64_t batch, const double* x, double* y) {
+    ORACLE_TRY({
+        const int64_t n3 = static_cast<int64_t>(n) * n * n;
+        const long double tp = 2 * std::numbers::pi_v<long double>;
+        const auto& G = group();
+        // prefac[w][kappa] = e^{2 pi i (w kappa).p / n}, exponent unreduced
+        std::vector<CLD> prefac(24 * n3);
+        std::vector<int> a(24 * n3 * 3);
+        for (int w = 0; w < 24; ++w)
+            for (int64_t c = 0; c < n3; ++c) {
+                const Index3 k = unflatten(c, n);
+                const Index3 wk = G[w].apply(k);
+                const long double ph = (static_cast<long double>(r) * wk[0] + static_cast<long double>(s) * wk[1] +
+                                        static_cast<long double>(t) * wk[2]) / n;
+                prefac[w * n3 + c] = CLD{std::cos(tp * ph), std::sin(tp * ph)};
+                for (int d = 0; d < 3; ++d) a[(w * n3 + c) * 3 + d] = ((wk[d] % n) + n) % n;
+            }
+        std::vector<CLD> omega(n);
+        for (int j = 0; j < n; ++j) omega[j] = CLD{std::cos(tp * j / n), std::sin(tp * j / n)};
+        std::vector<CLD> drow(n3);
+        for (int64_t ri = 0; ri < nrows; ++ri) {
+            const Index3 ijk = unflatten(rows[ri], n);
+            for (int64_t c = 0; c < n3; ++c) {
+                CLD acc{0, 0};
+                for (int w = 0; w < 24; ++w) {
+                    const int* aw = &a[(w * n3 + c) * 3];
+                    const int e = static_cast<int>((static_cast<int64_t>(aw[0]) * ijk[0] + static_cast<int64_t>(aw[1]) * ijk[1] +
+                                                    static_cast<int64_t>(aw[2]) * ijk[2]) % n);
+                    acc += prefac[w * n3 + c] * omega[e];
+                }
+                drow[c] = acc / static_cast<long double>(24);
+            }
+            for (int64_t b = 0; b < batch; ++b) {
+                const double* xb = x + 2 * n3 * b;
+                CLD acc{0, 0};
+                for (int64_t c = 0; c < n3; ++c) acc += drow[c] * CLD{xb[2 * c], xb[2 * c + 1]};
+                y[2 * (nrows * b + ri)] = static_cast<double>(acc.real());
+                y[2 * (nrows * b + ri) + 1] = static_cast<double>(acc.imag());
             }
         }
     })

@@ -46,6 +46,7 @@ def lib() -> ctypes.CDLL:
             "oracle_dense_transform": (c_int, [c_int, *d3, c_int, POINTER(c_double)]),
             "oracle_forward_dense": (c_int, [c_int, *d3, c_int64, POINTER(c_double), POINTER(c_double)]),
             "oracle_inverse_dense": (c_int, [c_int, *d3, c_int64, POINTER(c_double), POINTER(c_double)]),
+            "oracle_dense_rows": (c_int, [c_int, *d3, c_int64, POINTER(c_int64), c_int64, POINTER(c_double), POINTER(c_double)]),
             "oracle_condition_estimate": (c_int, [c_int, *d3, POINTER(c_double)]),
             "oracle_condition_estimate_matrix": (c_int, [c_int64, POINTER(c_double), POINTER(c_double)]),
             "oracle_radix_permutation": (c_int, [c_int, POINTER(c_uint64)]),
@@ -123,6 +124,17 @@ def forward_dense(n, p, x: np.ndarray) -> np.ndarray:
     batch = x.size // n**3
     y = np.zeros_like(x)
     _ck(lib().oracle_forward_dense(n, p[0], p[1], p[2], batch, _dp(x.view(np.float64)), _dp(y.view(np.float64))))
+    return y
+
+
+def dense_rows(n, p, rows, x: np.ndarray) -> np.ndarray:
+    """Rows `rows` of D_n(p) x, each row generated and accumulated in long
+    double (independent of the orbit / FFT route): [batch, len(rows)]."""
+    x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.complex128)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    y = np.zeros((x.shape[0], len(rows)), dtype=np.complex128)
+    _ck(lib().oracle_dense_rows(n, p[0], p[1], p[2], len(rows), rows.ctypes.data_as(POINTER(c_int64)), x.shape[0],
+                                _dp(x.view(np.float64)), _dp(y.view(np.float64))))
     return y
 
 
@@ -280,7 +292,7 @@ class OrbitRoute:
 
 def symmetrized_rows(n, p, node_idx, x):
     """Per-node direct evaluation sum_k x_k T_k(theta_node) with
-    T_k(theta) = (1/24) sum_w e^{2 pi i (w k).theta} (chebyshev.cpp:350-361);
+    T_k(theta) = (1/24) sum_w e^{2 pi i (w k).theta} (chebyshev.cpp:54-65);
     the acceptance #7 spot check (acceptance/main.cpp:368-388), vectorised."""
     G = group()
     kap = np.array(list(itertools.product(range(n), repeat=3)), dtype=np.int64)
@@ -293,3 +305,117 @@ def symmetrized_rows(n, p, node_idx, x):
         T = np.exp(2j * np.pi * (wk @ theta)).sum(axis=0) / 24.0
         out.append(T @ x)
     return np.array(out)
+
+
+# ---------------------------------------------------------------------------
+# The reference's own Eigen-free sources (weyl_s4.cpp, chebyshev.cpp,
+# spectral.cpp), compiled in place by oracle/ref.mk into oracle/_ref/ — the
+# checker of this oracle. Only available where /root/reference exists (this
+# build container); the GPU box uses the frozen fixtures in tests/golden/.
+# ---------------------------------------------------------------------------
+REF_DIR = HERE / "_ref"
+REF_LIB = REF_DIR / "libfcct_ref.so"
+REF_SRC = Path("/root/reference/proj")
+_ref = None
+
+
+def ref_available() -> bool:
+    return REF_LIB.exists() or (REF_SRC / "src" / "spectral.cpp").exists()
+
+
+def build_ref(force: bool = False) -> bool:
+    """Compile oracle/_ref/libfcct_ref.so from the reference sources; False
+    when the reference tree is absent and no prebuilt library exists."""
+    if not (REF_SRC / "src" / "spectral.cpp").exists():
+        return REF_LIB.exists()
+    srcs = [REF_SRC / "src" / f for f in ("weyl_s4.cpp", "chebyshev.cpp", "spectral.cpp")]
+    srcs += [HERE / "ref_shim.cpp", HERE / "ref.mk"]
+    if force or not REF_LIB.exists() or any(s.stat().st_mtime > REF_LIB.stat().st_mtime for s in srcs):
+        subprocess.run(["make", "-s", "-f", str(HERE / "ref.mk"), f"REF={REF_SRC}"], check=True, cwd=str(HERE.parent))
+    return True
+
+
+def ref_lib() -> ctypes.CDLL:
+    global _ref
+    if _ref is None:
+        if not build_ref():
+            raise FileNotFoundError("reference sources absent and oracle/_ref not built")
+        L = ctypes.CDLL(str(REF_LIB))
+        d3 = [c_double, c_double, c_double]
+        sig = {
+            "ref_group": (c_int, [POINTER(c_int)]),
+            "ref_skew_nodes": (c_int, [c_int, *d3, POINTER(c_double)]),
+            "ref_common_zeros": (c_int, [c_int, POINTER(c_double)]),
+            "ref_cheb_eval_uvw": (c_int, [c_int, c_int, c_int, POINTER(c_double), POINTER(c_double)]),
+            "ref_dense_columns": (c_int, [c_int, *d3, c_int64, c_int64, POINTER(c_double)]),
+            "ref_real_coords": (c_int, [c_int, *d3, POINTER(c_double)]),
+            "ref_child": (c_int, [*d3, c_int, c_int, c_int, POINTER(c_double)]),
+            "ref_encode_param": (c_int, [c_double, ctypes.c_char_p, c_int]),
+            "ref_last_error": (ctypes.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _ref = L
+    return _ref
+
+
+def _rck(st):
+    if st != 0:
+        raise OracleError(st, ref_lib().ref_last_error().decode())
+
+
+class Ref:
+    """The reference's own functions (oracle/_ref), numpy in / out."""
+
+    @staticmethod
+    def group() -> np.ndarray:
+        out = np.zeros(24 * 9, dtype=np.int32)
+        _rck(ref_lib().ref_group(out.ctypes.data_as(POINTER(c_int))))
+        return out.reshape(24, 3, 3)
+
+    @staticmethod
+    def skew_nodes(n, p) -> np.ndarray:
+        out = np.zeros(n**3 * 12)
+        _rck(ref_lib().ref_skew_nodes(n, p[0], p[1], p[2], _dp(out)))
+        return out.view(np.complex128).reshape(n**3, 6)
+
+    @staticmethod
+    def common_zeros(n) -> np.ndarray:
+        out = np.zeros(n**3 * 12)
+        _rck(ref_lib().ref_common_zeros(n, _dp(out)))
+        return out.view(np.complex128).reshape(n**3, 6)
+
+    @staticmethod
+    def cheb_eval_uvw(k, uvw) -> complex:
+        a = np.array([uvw[0].real, uvw[0].imag, uvw[1].real, uvw[1].imag, uvw[2].real, uvw[2].imag])
+        out = np.zeros(2)
+        _rck(ref_lib().ref_cheb_eval_uvw(int(k[0]), int(k[1]), int(k[2]), _dp(a), _dp(out)))
+        return complex(out[0], out[1])
+
+    @staticmethod
+    def dense_columns(n, p, c0, c1) -> np.ndarray:
+        """Columns [c0, c1) of D_n(p), [node, column] complex128."""
+        N = n**3
+        out = np.zeros(2 * N * (c1 - c0))
+        _rck(ref_lib().ref_dense_columns(n, p[0], p[1], p[2], c0, c1, _dp(out)))
+        return out.view(np.complex128).reshape(c1 - c0, N).T.copy()
+
+    @staticmethod
+    def real_coords(n, p) -> np.ndarray:
+        out = np.zeros(n**3 * 3)
+        _rck(ref_lib().ref_real_coords(n, p[0], p[1], p[2], _dp(out)))
+        return out.reshape(n**3, 3)
+
+    @staticmethod
+    def child(p, ir, is_, it):
+        out = np.zeros(3)
+        _rck(ref_lib().ref_child(p[0], p[1], p[2], ir, is_, it, _dp(out)))
+        return tuple(out)
+
+    @staticmethod
+    def encode_param(v) -> str:
+        buf = ctypes.create_string_buffer(64)
+        _rck(ref_lib().ref_encode_param(v, buf, 64))
+        return buf.value.decode()

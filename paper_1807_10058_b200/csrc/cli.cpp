@@ -554,7 +554,7 @@ std::vector<Check> run_checks(int n_max, double tol_override, bool perturb) {
         add("semigroup_composition", worst, tol(1e-11));
     }
     const Params canon;
-    {  // node_generator_residuals (sigma / tau / rho, spectral.cpp:130-151)
+    {  // node_generator_residuals (sigma / tau / rho, spectral.cpp:119-134)
         double worst = 0.0;
         const Params& p = canon;
         const Complex sx = 0.25 * (unit(p.r) + unit(p.s - p.r) + unit(p.t - p.s) + unit(-p.t));

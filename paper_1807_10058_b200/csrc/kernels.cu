@@ -1454,7 +1454,7 @@ __global__ void gen_dense_inv_realform_kernel(int n, OrbitDev od, R* Wt) {
     Wt[(2 * kap + 1) * K + 2 * node + 1] = static_cast<R>(re);
 }
 
-__device__ double wrap_turn(double a) {  // TorusPoint::wrapped (chebyshev.cpp:326-335)
+__device__ double wrap_turn(double a) {  // TorusPoint::wrapped (chebyshev.cpp:30-39)
     double f = a - floor(a);
     if (f >= 1.0 - 1e-15) f = 0.0;
     return f;
@@ -1480,7 +1480,7 @@ __global__ void gen_nodes_kernel(int n, double r, double s, double t, double2* o
     sincospi(2.0 * th2, &s2, &c2);
     const double2 u = make_double2(c0, s0), v = make_double2(c1, s1), w = make_double2(c2, s2);
     const double2 ui = crecip(u), vi = crecip(v), wi = crecip(w);
-    // coords_from_uvw (chebyshev.cpp:372-381)
+    // coords_from_uvw (chebyshev.cpp:76-85)
     const double2 x = cscale(cadd(cadd(u, cmul(ui, v)), cadd(cmul(vi, w), wi)), 0.25);
     const double2 y = cscale(cadd(cadd(cadd(vi, v), cadd(cmul(u, wi), cmul(cmul(ui, v), wi))),
                                   cadd(cmul(ui, w), cmul(cmul(u, vi), w))),
@@ -1495,7 +1495,7 @@ __global__ void gen_nodes_kernel(int n, double r, double s, double t, double2* o
     o[5] = z;
 }
 
-// check_not_degenerate (spectral.cpp:132-149): any pair closer than 1e-9.
+// check_not_degenerate (spectral.cpp:26-43): any pair closer than 1e-9.
 __global__ void degenerate_kernel(int64_t N, const double2* nodes, int* flag) {
     const int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (a >= N) return;

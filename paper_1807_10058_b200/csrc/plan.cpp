@@ -136,7 +136,7 @@ const std::array<std::array<int, 9>, 24>& s4_group() {
     return g;
 }
 
-std::string encode_param(double value) {  // spectral.cpp:159-181
+std::string encode_param(double value) {  // spectral.cpp:53-75
     if (value == 0.0) return "0";
     double x = value;
     long long p0 = 0, q0 = 1, p1 = 1, q1 = 0;

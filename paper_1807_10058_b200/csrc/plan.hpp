@@ -56,8 +56,8 @@ struct FcctError : std::runtime_error {
 struct Params {
     double r = 0.0, s = 0.0, t = 0.0;
     bool operator==(const Params& o) const { return r == o.r && s == o.s && t == o.t; }
-    static Params canonical() { return Params{0.125, 0.0, 0.375}; }  // spectral.cpp:153
-    // SkewParams::child (spectral.cpp:155-157)
+    static Params canonical() { return Params{0.125, 0.0, 0.375}; }  // spectral.cpp:47
+    // SkewParams::child (spectral.cpp:49-51)
     Params child(int ir, int is, int it) const {
         return Params{(r + ir) / 2.0, (s + is) / 2.0, (t + it) / 2.0};
     }
@@ -137,7 +137,7 @@ inline bool level_identity(const std::vector<const PlanNode*>& level, bool inver
 // *cond receives the exact 1-norm condition.
 std::vector<cld> dense_inverse(const std::vector<cld>& a, int64_t dim, double* cond);
 
-// Text encoding of an offset (encode_param, spectral.cpp:159-181).
+// Text encoding of an offset (encode_param, spectral.cpp:53-75).
 std::string encode_param(double value);
 
 // Builds the tree (PlanBuilder::make, transform.cpp:382-401): direct for odd n
@@ -158,7 +158,7 @@ cld dense_entry(int n, const Params& p, const Index3& node, const Index3& kappa)
 // (skew_nodes + coords_from_uvw, spectral.cpp:155-171, chebyshev.cpp:30-85).
 std::vector<std::array<std::complex<double>, 3>> node_coords(int n, const Params& p);
 
-// Node degeneracy check (check_not_degenerate, spectral.cpp:132-149), n <= 16.
+// Node degeneracy check (check_not_degenerate, spectral.cpp:26-43), n <= 16.
 void check_nodes(int n, const Params& p);
 
 // Tree statistics.

@@ -16,11 +16,11 @@
 
 namespace fcct::io {
 
-// parse_param / parse_params (spectral.cpp:84-128); std::invalid_argument
+// parse_param / parse_params (spectral.cpp:81-117); std::invalid_argument
 // semantics map to ST_INVALID_ARGUMENT.
 double parse_param(const std::string& text);
 Params parse_params(const std::string& text);
-std::string encode_params(const Params& p);  // SkewParams::encode (spectral.cpp:79-81)
+std::string encode_params(const Params& p);  // SkewParams::encode (spectral.cpp:77-79)
 
 // VoxelGrid (voxel_io.hpp:16-22).
 struct Grid {

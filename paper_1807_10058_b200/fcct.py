@@ -94,12 +94,12 @@ def _raise(status: int) -> None:
 
 
 # ---------------------------------------------------------------------------
-# SkewParams: fcct/spectral.hpp:13-27, src/spectral.cpp:153-223
+# SkewParams: fcct/spectral.hpp:13-27, src/spectral.cpp:47-117
 # ---------------------------------------------------------------------------
 
 
 def encode_param(value: float) -> str:
-    """Exact small rational as 'a/b', else %.17g (spectral.cpp:159-181)."""
+    """Exact small rational as 'a/b', else %.17g (spectral.cpp:53-75)."""
     if value == 0.0:
         return "0"
     x = value
@@ -123,7 +123,7 @@ def encode_param(value: float) -> str:
 
 
 def parse_param(text: str) -> float:
-    """Inverse of encode_param (spectral.cpp:187-209)."""
+    """Inverse of encode_param (spectral.cpp:81-103)."""
     if not text:
         raise ValueError("empty grid offset")
     try:
@@ -556,7 +556,7 @@ def with_perturbed_basis(plan: TransformPlan, delta: float) -> TransformPlan:
 
 
 def skew_nodes(n: int, p: SkewParams, device=None) -> torch.Tensor:
-    """Node set (spectral.cpp:261-277) generated on the device: [n^3, 6]
+    """Node set (spectral.cpp:155-171) generated on the device: [n^3, 6]
     complex128 columns (u, v, w, x, y, z). Raises DegenerateNodes for n <= 16."""
     dev = _device_index(device)
     out = torch.empty((n**3, 6), dtype=torch.complex128, device=f"cuda:{dev}")
@@ -686,7 +686,7 @@ def load_spectrum_csv(path) -> Spectrum:
 
 
 def export_nodes_csv(n: int, p: SkewParams, path=None) -> None:
-    """export_nodes_csv(skew_nodes(n, p)) (spectral.cpp:155-188; CLI `zeros`)."""
+    """export_nodes_csv(skew_nodes(n, p)) (spectral.cpp:155-171,180-188; CLI `zeros`)."""
     _raise(_capi.lib().fcct_export_nodes_csv(n, p.r, p.s, p.t, _path(path)))
 
 
