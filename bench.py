@@ -153,16 +153,67 @@ def launches_per_call(info):
     return (1, 1)
 
 
-def run_cpu_baseline(n: int, blocks: int, threads: int, method: str = "fast", min_seconds: float = 0.0) -> dict:
+def cpu_baseline_run(n: int, mode: str = "batched", method: str = "fast", blocks: int = 1, threads: int = 1,
+                     fanout: int = 1, repeats: int = 5, min_seconds: float = 0.0, reps: int = 1) -> dict:
+    """One run of oracle/cpu_baseline.cpp (built on this host with -march=native)."""
     from oracle import oracle  # CPU baseline / reference arm only
 
-    oracle.build()
+    exe = oracle.cpu_baseline_path()
     out = subprocess.run(
-        [str(oracle.CPU_BASELINE), "--n", str(n), "--blocks", str(blocks), "--threads", str(threads), "--method", method,
-         "--min-seconds", str(min_seconds)],
+        [str(exe), "--n", str(n), "--mode", mode, "--method", method, "--blocks", str(blocks), "--threads",
+         str(threads), "--fanout", str(fanout), "--repeats", str(repeats), "--min-seconds", str(min_seconds),
+         "--reps", str(reps)],
         check=True, capture_output=True, text=True,
     )
     return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline(config: str, n: int, method: str, sample: int, min_seconds: float) -> dict:
+    """The reference path timed on this host's cores, beside the GPU number
+    (BASELINE.md "CPU baseline plan"). value = transforms/s (forward + inverse
+    per transform pair, like the GPU metric)."""
+    threads = os.cpu_count() or 1
+    if n > 16:
+        r = cpu_baseline_run(n, "fftroute", repeats=3, min_seconds=min_seconds)
+        return {
+            "value": 2e6 / (r["forward_us"] + r["inverse_us"]), "unit": "transforms/s", "cores": 1, "kind": "port",
+            "sample": (f"one n={n} transform, forward + inverse, median of {r['repeats']} calls: the FFT-route oracle "
+                       "(D x = n^3 IFFT3(S x); inverse S^-1 FFT3(y)/n^3 with S's orbit blocks), NOT the reference "
+                       "path, which cannot build an n = 64 plan (~137 GB of dense child LUs, SURVEY.md 0.6)"),
+            "us_per_forward": r["forward_us"], "us_per_inverse": r["inverse_us"], "route": "fft",
+        }
+    # mode 1: one vector per call (fcct bench protocol), threads = 1 and the reference's threads = 8 fan-out
+    rows = {}
+    for tag, fan in (("threads1", 1), ("fanout8", 8)):
+        if method == "direct" and fan > 1:
+            continue  # the dense path has no fan-out
+        if method == "direct" and n > 8:
+            continue  # a fresh 4096^2 LU per inverse call: minutes per call (transform.cpp:158-169)
+        r = cpu_baseline_run(n, "faithful", method, fanout=fan, repeats=5)
+        rows[tag] = {"us_per_forward": r["forward_us"], "us_per_inverse": r["inverse_us"],
+                     "transforms_per_s": 2e6 / (r["forward_us"] + r["inverse_us"]), "cores": fan,
+                     "inner_loop": r["inner"]}
+    if config == "c1":
+        best = rows["threads1"]
+        return {
+            "value": best["transforms_per_s"], "unit": "transforms/s", "cores": 1, "kind": "port",
+            "sample": (f"one n={n} vector per call, {method} path, threads=1, the fcct bench protocol "
+                       f"(tools/fcct.cpp:508-521: warm-up, median of 5 repeats of a {best['inner_loop']}-call inner "
+                       "loop), reference-faithful C++ restatement (oracle/cpu_baseline.cpp, -O3 -march=native)"),
+            "us_per_forward": best["us_per_forward"], "us_per_inverse": best["us_per_inverse"], "mode1": rows,
+        }
+    # mode 2: batched, all cores
+    r = cpu_baseline_run(n, "batched", method, blocks=sample, threads=threads, min_seconds=min_seconds)
+    return {
+        "value": 2 * sample / (r["forward_s"] + r["inverse_s"]), "unit": "transforms/s", "cores": threads,
+        "kind": "port",
+        "sample": (f"{sample} blocks of n={n}, forward then inverse, {method} path, repeated {r.get('reps', 1)}x "
+                   f"(>= {min_seconds:g} s of CPU work), one block per call, std::thread over blocks; "
+                   "reference-faithful C++ restatement (oracle/cpu_baseline.cpp, -O3 -march=native)"
+                   + ("; the direct inverse reuses one LU factored at plan time (the reference refactors per "
+                      "call, transform.cpp:158-169: a lower bound on its time)" if method == "direct" else "")),
+        "mode1": rows,
+    }
 
 
 CONFIGS = {
@@ -262,25 +313,90 @@ def dist_env():
     return world, rank, local
 
 
+def launch_ranks(args) -> int:
+    """`bench.py --gpus N` (N > 1) outside torchrun: start N ranks, one per GPU,
+    with torch.distributed.run on 127.0.0.1 and the same arguments."""
+    if not args.emulate_cpu:
+        import torch
+
+        visible = torch.cuda.device_count()
+        if visible < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {visible} CUDA device(s) are visible", file=sys.stderr)
+            return 1
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def workload(args, world: int) -> dict:
+    """The configuration both arms measure (BASELINE.json configs restated on the
+    reference's n^3 index set); the JSON `config` object is built
+    here so the reference arm's equals the B200 arm's."""
+    cfg = CONFIGS[args.config]
+    n = args.n if args.n is not None else cfg["n"]
+    precision = args.precision or ("f32" if args.config == "c5" else "f64")
+    f32 = precision == "f32"
+    esize = 8 if f32 else 16
+    real_io = bool(args.real_io) if args.real_io is not None else args.config in ("c3", "c5")
+    in_esize = esize // 2 if real_io else esize
+    per_gpu = args.blocks if args.blocks is not None else cfg["blocks"]
+    total = per_gpu if cfg["scaling"] == "strong" else per_gpu * world
+    per_rank_max = -(-total // world)
+    N = n**3
+    subset = (f"; {args.blocks} blocks per GPU (a subset of the config's {cfg['blocks']:,}, labelled as such)"
+              if args.blocks is not None and args.blocks != cfg["blocks"] else "")
+    config = {
+        "workload": f"{args.config}: {cfg['desc']}; n={n} (N={N} points/block), {args.method} path, "
+                    f"forward then inverse per step{subset}",
+        "blocks_total": total,
+        "blocks_per_gpu_max": per_rank_max,
+        "points_per_block": N,
+        "params": "canonical (1/8, 0, 3/8)",
+        "precision": precision,
+        "io": ("real samples in and out (z_transform / grid_from_signal fused into the device pipeline)"
+               if real_io else "complex in and out"),
+        "input": cfg["desc"] + " (seeded, generated on device)",
+        "l2": (f"inputs larger than L2 ({per_rank_max * N * in_esize / 2**20:.0f} MiB per array vs 126 MB L2), "
+               "no flush needed" if per_rank_max * N * in_esize > 126e6 else
+               f"input {per_rank_max * N * in_esize / 2**20:.1f} MiB is L2-resident (single-transform latency config)"),
+        "parallelism": f"batch-sharded dp{world}, no collective on the data path",
+    }
+    return dict(cfg=cfg, n=n, N=N, precision=precision, f32=f32, esize=esize, real_io=real_io, in_esize=in_esize,
+                per_gpu=per_gpu, total=total, config=config)
+
+
 def reference_arm(args):
+    """--impl reference: the reference's CPU path (the oracle port; the reference
+    itself needs Eigen3 and cannot be built) on this host's cores,
+    rank 0 only, each step a bounded sample of the same workload."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
-    args.n = args.n if args.n is not None else cfg["n"]
-    args.precision = args.precision or ("f32" if args.config == "c5" else "f64")
-    if args.n > 16:
-        print(json.dumps({"impl": "reference", "unavailable": f"n={args.n}: the reference-faithful plan derivation needs dense child LUs of (n/2)^3 (~137 GB at n=64, SURVEY.md §0.6)"}), flush=True)
-        return
+    w = workload(args, world)
+    n = w["n"]
     threads = os.cpu_count() or 1
-    # each step: a bounded sample of the workload (forward + inverse of `sample` blocks)
-    sample = min(args.cpu_sample, max(1, 2**25 // args.n**3))
-    vals = []
-    res = None
-    for i in range(args.warmup + args.steps):
-        res = run_cpu_baseline(args.n, sample, threads, args.method)
-        if i >= args.warmup:
-            vals.append(2 * sample / (res["forward_s"] + res["inverse_s"]))
+    if n > 16 or args.config == "c1":
+        sample = 1
+        vals = []
+        for i in range(args.warmup + args.steps):
+            res = cpu_baseline(args.config, n, args.method, 1, 0.0)
+            if i >= args.warmup:
+                vals.append(res["value"])
+    else:
+        # one plan build, warmup + steps timed passes over the sample (the reference arm's steps)
+        sample = min(args.cpu_sample, max(1, (2**25 if args.method == "fast" else 2**17) // n**3))
+        r = cpu_baseline_run(n, "batched", args.method, blocks=sample, threads=threads, reps=args.warmup + args.steps)
+        vals = [2 * sample / t for t in r["rep_s"][args.warmup:]]
+        res = {"cores": threads, "kind": "port",
+               "sample": f"{sample} blocks of n={n} per step, forward then inverse, {args.method} path, one block "
+                         "per call (the reference API), std::thread over blocks; reference-faithful C++ "
+                         "restatement (oracle/cpu_baseline.cpp, -O3 -march=native)"}
     v = statistics.median(vals)
     line = {
         "impl": "reference",
@@ -290,24 +406,80 @@ def reference_arm(args):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": 1e3 * 2 * sample / v,
+        "ms_per_step": 1e3 * 2 * (sample if n <= 16 and args.config != "c1" else 1) / v,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": w["cfg"]["scaling"],
         "vs_baseline": None,
-        "dtype": "f64" if args.precision == "f64" else "f32",
+        "dtype": w["precision"],
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: {cfg['desc']}; n={args.n} (N={args.n**3} points/block), {args.method} path, forward+inverse; CPU sample of {sample} blocks per step"},
-        "points_per_s": v * args.n**3,
-        "cpu_baseline": {
-            "value": v,
-            "unit": "transforms/s",
-            "cores": threads,
-            "kind": "port",
-            "sample": f"{sample} blocks of n={args.n}, forward then inverse, {args.method} path, reference-faithful C++ restatement (oracle/cpu_baseline.cpp), std::thread over blocks",
-        },
+        "config": w["config"],
+        "points_per_s": v * n**3,
+        "cpu_baseline": {"value": v, "unit": "transforms/s", "cores": res["cores"], "kind": res["kind"],
+                         "sample": res["sample"]},
         "e2e": {"value": v, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def emulated_arm(args):
+    """--emulate-cpu: the multi-rank launcher end to end without a GPU (gloo).
+    Each rank transforms its shard through the host emulation of the orbit-FFT
+    executor's compiled tables (the exact kernel indexing); timing is wall clock,
+    max over ranks. Test infrastructure for the launcher, not a measurement."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1807_10058_b200 import _capi, shard_range
+
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+    w = workload(args, world)
+    n, N = w["n"], w["N"]
+    b0, b1 = shard_range(w["total"], rank, world)
+    rng = np.random.default_rng(1234 + rank)
+    x = rng.uniform(-1, 1, (b1 - b0, N)) + 1j * rng.uniform(-1, 1, (b1 - b0, N))
+    y, z = np.zeros_like(x), np.zeros_like(x)
+    L = _capi.lib()
+
+    def step():
+        if b1 > b0:
+            assert L.fcct_debug_emulate_orbit_fft(n, 0.125, 0.0, 0.375, 0, x.ctypes.data, y.ctypes.data, b1 - b0) == 0
+            assert L.fcct_debug_emulate_orbit_fft(n, 0.125, 0.0, 0.375, 1, y.ctypes.data, z.ctypes.data, b1 - b0) == 0
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    ms = 1e3 * (time.perf_counter() - t0)
+    err = float(np.linalg.norm(z - x) / max(np.linalg.norm(x), 1e-300))
+    shards = [(b0, b1)]
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+        e = torch.tensor([err], dtype=torch.float64)
+        dist.all_reduce(e, op=dist.ReduceOp.MAX)
+        err = e.item()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (b0, b1))
+        shards = gathered
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    value = 2.0 * w["total"] * args.steps / (ms / 1e3)
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": "transforms/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": w["cfg"]["scaling"], "vs_baseline": None, "dtype": w["precision"], "data": "synthetic",
+        "config": w["config"], "emulated": "CPU host emulation of the orbit-FFT tables over gloo (launcher test)",
+        "shards": shards, "roundtrip_rel_err": err, "gpu_launches": 0,
+    }), flush=True)
 
 
 def b200_arm(args):
@@ -317,38 +489,33 @@ def b200_arm(args):
     from paper_1807_10058_b200 import SkewParams, build_plan, dense_transform, shard_range
 
     world, rank, local = dist_env()
+    visible = torch.cuda.device_count()
+    if visible < max(1, world) or visible == 0:
+        raise SystemExit(f"bench.py: {world} rank(s) need {world} CUDA device(s), {visible} visible")
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", init_method="env://")
     dev = torch.device(f"cuda:{local if world > 1 else 0}")
     torch.cuda.set_device(dev)
-    cfg = CONFIGS[args.config]
-    n = args.n if args.n is not None else cfg["n"]
-    N = n**3
-    if args.config == "c5" and args.precision is None:
-        args.precision = "f32"
-    args.precision = args.precision or "f64"
-    f32 = args.precision == "f32"
+    w = workload(args, world)
+    cfg, n, N, f32 = w["cfg"], w["n"], w["N"], w["f32"]
+    esize, in_esize, real_io, total = w["esize"], w["in_esize"], w["real_io"], w["total"]
     cdt = torch.complex64 if f32 else torch.complex128
     rdt = torch.float32 if f32 else torch.float64
-    esize = 8 if f32 else 16
     p = SkewParams.canonical()
-    per_gpu = args.blocks if args.blocks is not None else cfg["blocks"]
-    total = per_gpu if cfg["scaling"] == "strong" else per_gpu * world
     b0, b1 = shard_range(total, rank, world)
     blocks = b1 - b0
 
     if args.method == "fast":
-        plan = build_plan(n, p, precision=args.precision)
+        plan = build_plan(n, p, precision=w["precision"])
     else:
-        plan = dense_transform(n, p, precision=args.precision)._plan
+        plan = dense_transform(n, p, precision=w["precision"])._plan
     info = plan.info
 
     # seeded synthetic input, resident in HBM before the timed region
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     # real fields (c3, c5) enter and leave as real samples: z_transform / grid_from_signal
     # fused into the device pipelines, as the reference CLI uses them (fcct.cpp:95-129)
-    real_io = args.real_io if args.real_io is not None else args.config in ("c3", "c5")
     if args.config == "c3":
         x = gaussian_blobs(n, blocks, g, dev, rdt)
     elif args.config == "c5":
@@ -365,7 +532,6 @@ def b200_arm(args):
     z = torch.empty_like(x)
     fwd_fn = "fcct_forward_real" if real_io else "fcct_forward"
     inv_fn = "fcct_inverse_real" if real_io else "fcct_inverse"
-    in_esize = esize // 2 if real_io else esize
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
     from paper_1807_10058_b200 import _capi
@@ -405,19 +571,24 @@ def b200_arm(args):
     ms = start.elapsed_time(end)
     fwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     inv_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    per_rank_ms = [ms]
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
+        gathered = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(gathered, t)
+        per_rank_ms = [float(v.item()) for v in gathered]
+        ms = max(per_rank_ms)
     value = 2.0 * total * args.steps / (ms / 1e3)
 
-    # e2e: the reference-facing host-buffer API (H2D + transform + D2H each call)
-    e2e = None
-    if not args.no_e2e:
+    # e2e: the reference-facing host-buffer API (H2D + transform + D2H in every
+    # call), from pinned and from pageable host memory (staged by the library)
+    def e2e_run(pinned: bool):
         eb = max(1, min(blocks, args.e2e_blocks))
-        xh = x[:eb].cpu().pin_memory()
-        yh = torch.empty((eb, N), dtype=cdt).pin_memory()
-        zh = torch.empty_like(xh).pin_memory()
+        xh = x[:eb].cpu()
+        yh = torch.empty((eb, N), dtype=cdt)
+        zh = torch.empty_like(xh)
+        if pinned:
+            xh, yh, zh = xh.pin_memory(), yh.pin_memory(), zh.pin_memory()
         fwd_host = getattr(L, fwd_fn + "_host")
         inv_host = getattr(L, inv_fn + "_host")
         for _ in range(2):
@@ -438,14 +609,31 @@ def b200_arm(args):
             t = torch.tensor([ems], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = t.item()
-        e2e = {
+        ok = bool(torch.allclose(zh.to(x.dtype), x[:eb].cpu(), rtol=0, atol=1e-4 if f32 else 1e-9))
+        return {
             "value": 2.0 * eb * world * args.e2e_steps / (ems / 1e3),
             "unit": "transforms/s",
             "h2d_bytes_per_step": eb * N * (in_esize + esize),
             "d2h_bytes_per_step": eb * N * (esize + in_esize),
             "blocks_per_step": eb,
+            "host_memory": "pinned (cudaHostAlloc)" if pinned else "pageable (staged through pinned bounce buffers)",
+            "roundtrip_ok": ok,
         }
 
+    e2e = e2e_pageable = None
+    if not args.no_e2e:
+        e2e = e2e_run(pinned=True)
+        e2e_pageable = e2e_run(pinned=False)
+    launches = args.steps * sum(launches_per_call(info))
+
+    if world > 1:
+        lt = torch.tensor([launches, blocks], device=dev, dtype=torch.int64)
+        lg = [torch.zeros_like(lt) for _ in range(world)]
+        dist.all_gather(lg, lt)
+        per_rank = [{"rank": r, "gpu_launches": int(v[0]), "blocks": int(v[1]), "ms": per_rank_ms[r]}
+                    for r, v in enumerate(lg)]
+    else:
+        per_rank = [{"rank": 0, "gpu_launches": launches, "blocks": blocks, "ms": ms}]
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -457,7 +645,7 @@ def b200_arm(args):
     # the plan tables streamed once (about half of table_bytes, which counts both
     # directions) — negligible for batched configs, dominant for a single n = 64
     data_bytes = float(N * (in_esize + esize) * blocks)
-    table_bytes_fwd = 0.5 * float(info.table_bytes)
+    table_bytes_fwd = 0.5 * float(info.table_bytes) if info.executor in (3, 7) else 0.0
     bytes_fwd = data_bytes + table_bytes_fwd
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6488.0)
@@ -465,68 +653,46 @@ def b200_arm(args):
     # the DMMA executors (fp32 plans there keep fp64 arithmetic, complex64 I/O)
     on_fp64_pipe = (not f32) or info.executor in (2, 4, 5, 6, 7)
     peak_tf = FP64_PEAK_TFLOPS if on_fp64_pipe else FP32_PEAK_TFLOPS
-    achieved_tf = flops_fwd / (fwd_ms / 1e3) / 1e12
+    exec_flops = (info.exec_flops_forward or info.flops_forward) * blocks
+    achieved_tf = exec_flops / (fwd_ms / 1e3) / 1e12
     achieved_gbs = bytes_fwd / (fwd_ms / 1e3) / 1e9
-    t_star = max(bytes_fwd / (hbm * 1e9), flops_fwd / (peak_tf * 1e12))
-    hbm_bound = bytes_fwd / (hbm * 1e9) > flops_fwd / (peak_tf * 1e12)
+    t_hbm, t_pipe = bytes_fwd / (hbm * 1e9), exec_flops / (peak_tf * 1e12)
+    hbm_bound = t_hbm >= t_pipe
+    # frac: the kernel against its OWN work (executed flops, algorithmic bytes)
     roof = {
         "bound": "hbm" if hbm_bound else "tensor",
         "achieved": achieved_gbs if hbm_bound else achieved_tf,
         "peak": hbm if hbm_bound else peak_tf,
         "unit": "GB/s" if hbm_bound else "TFLOP/s",
-        "frac": (achieved_gbs / hbm) if hbm_bound else (achieved_tf / peak_tf),
+        "frac": max(t_hbm, t_pipe) / (fwd_ms / 1e3),
         "traffic": args.traffic if args.traffic is not None else profiled_traffic(args.config, f32, info.executor),
-        "kernel": {0: "gemm_f64_kernel / gemm_f32_kernel (direct)", 1: "pipeline_kernel (tile interpreter)",
-                   2: "pipeline2_kernel (FP64 tensor pipe)", 3: "gstage_* kernels (global multi-pass)",
-                   4: "root pass + 8 x pipeline2_kernel (two-level, FP64 tensor pipe)",
-                   5: "orbit_fft_ws_kernel (S_n on the FP64 tensor pipe + radix-2 FFT, warp-specialised)",
-                   6: "orbit16_base_kernel + fft_cube_kernel (two-pass orbit-FFT: S_n on the FP64 tensor pipe, "
-                      "then the n^3 FFT)",
-                   7: "orbit_big_s_kernel + line_fft_kernel (large-n orbit-FFT: S_n then three line-FFT passes)"}[
-                       info.executor],
+        "kernel": KERNELS[info.executor],
+        "executed_flops_per_launch": exec_flops,
         "algorithmic_flops_per_launch": flops_fwd,
         "algorithmic_bytes_per_launch": bytes_fwd,
         "table_bytes_per_launch": table_bytes_fwd,
-        "achieved_tflops": achieved_tf,
+        "achieved_tflops_executed": achieved_tf,
         "achieved_gbs": achieved_gbs,
+        "hbm_frac": achieved_gbs / hbm,
         "hbm_peak_gbs": hbm,
-        "t_star_over_t": t_star / (fwd_ms / 1e3),
+        "pipe_peak_tflops": peak_tf,
+        "t_star_algorithmic_over_t": max(t_hbm, flops_fwd / (peak_tf * 1e12)) / (fwd_ms / 1e3),
         "peak_source": ("measured DMMA m8n8k4 f64 peak" if on_fp64_pipe else "measured FFMA fp32 peak")
-                       + " (tools/peak_fp.cu, profiles/r01_fp_peaks.txt); HBM: MEASURED_PEAKS.json",
+                       + " (tools/peak_fp.cu, profiles/r01_fp_peaks.txt); HBM: MEASURED_PEAKS.json hbm_gbs (burst)",
         "fwd_ms": fwd_ms,
         "inv_ms": inv_ms,
-        "inverse_achieved_tflops": info.flops_inverse * blocks / (inv_ms / 1e3) / 1e12,
+        "note": ("frac = max(algorithmic bytes / HBM peak, executed flops / pipe peak) / forward launch time: the "
+                 "kernel against its own work. t_star_algorithmic_over_t uses SURVEY.md 8(d)'s tree flop count "
+                 "instead (the orbit-FFT executors issue fewer flops than the tree, so that ratio can exceed frac)"),
     }
     if info.executor == 6 and roof["traffic"] is not None:
         roof["traffic_note"] = ("two kernels per forward call: the base change writes z (complex128, orbit order) "
                                 "and the cube FFT reads it back, 2 x 16 B per point by design on top of the "
-                                "algorithmic bytes (ncu: pass A 0.57 + 1.02 GB, pass B 1.13 + 1.03 GB)")
-    if info.exec_flops_forward > 0:
-        # what the executor really issues on the FP64 pipes (the orbit-FFT route
-        # telescopes the tree: fewer flops than SURVEY.md's algorithmic count)
-        exec_tf = info.exec_flops_forward * blocks / (fwd_ms / 1e3) / 1e12
-        roof["executed_flops_per_launch"] = info.exec_flops_forward * blocks
-        roof["executed_tflops"] = exec_tf
-        roof["executed_frac_of_fp64_peak"] = exec_tf / peak_tf
-        roof["hbm_frac"] = achieved_gbs / hbm
-        t_exec = max(bytes_fwd / (hbm * 1e9), info.exec_flops_forward * blocks / (peak_tf * 1e12))
-        roof["executed_t_star_over_t"] = t_exec / (fwd_ms / 1e3)
-        roof["note"] = ("achieved/frac use SURVEY.md 8(d)'s algorithmic flops of the stage-by-stage tree; the "
-                        "orbit-FFT executor telescopes the tree and issues executed_flops_per_launch, so against "
-                        "its own work the bound is max(HBM bytes, executed flops) -> executed_t_star_over_t")
+                                "algorithmic bytes")
     cpu = None
-    if not args.no_cpu and world >= 1:
-        threads = os.cpu_count() or 1
-        sample = min(args.cpu_sample, max(1, 2**24 // N))
-        r = run_cpu_baseline(n, sample, threads, args.method, args.cpu_seconds) if n <= 16 else None
-        cpu = None if r is None else {
-            "value": 2 * sample / (r["forward_s"] + r["inverse_s"]),
-            "unit": "transforms/s",
-            "cores": threads,
-            "kind": "port",
-            "sample": f"{sample} blocks of n={n}, forward then inverse, {args.method} path, repeated {r.get('reps', 1)}x "
-                      f"(>= {args.cpu_seconds:g} s of CPU work), reference-faithful C++ restatement (oracle/cpu_baseline.cpp)",
-        }
+    if not args.no_cpu:
+        sample = min(args.cpu_sample, max(1, (2**24 if args.method == "fast" else 2**16) // N))
+        cpu = cpu_baseline(args.config, n, args.method, sample, args.cpu_seconds)
     line = {
         "metric": METRIC,
         "value": value,
@@ -538,34 +704,33 @@ def b200_arm(args):
         "higher_is_better": True,
         "scaling": cfg["scaling"],
         "vs_baseline": None,
-        "dtype": "f64" if not f32 else "f32",
+        "dtype": w["precision"],
         "data": "synthetic",
-        "config": {
-            "workload": f"{args.config}: {cfg['desc']}; n={n} (N={N} points/block), {blocks} blocks on rank 0, {args.method} path, forward then inverse per step",
-            "blocks_total": total,
-            "points_per_block": N,
-            "params": "canonical (1/8, 0, 3/8)",
-            "io": ("real samples in and out (z_transform / grid_from_signal fused into the device pipeline)"
-                   if real_io else "complex in and out"),
-            "input": cfg["desc"] + " (seeded, generated on device)",
-            "l2": (f"inputs larger than L2 ({blocks * N * esize / 2**20:.0f} MiB per array vs 126 MB L2)"
-                   if blocks * N * esize > 126e6 else
-                   f"input {blocks * N * esize / 2**20:.1f} MiB is L2-resident (single-transform latency config)"),
-            "parallelism": f"batch-sharded dp{world}, no collective",
-        },
+        "config": w["config"],
         "points_per_s": value * N,
         "roundtrip_rel_err": err,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": args.steps * sum(launches_per_call(info)),
+        "e2e_pageable": e2e_pageable if not args.no_e2e else None,
+        "gpu_launches": launches,
+        "gpu_launches_per_rank": per_rank,
         "clocks": clk.summary(),
         "plan": {"tree_nnz": info.tree_nnz, "tree_nnz_inv": info.tree_nnz_inv, "table_bytes": info.table_bytes,
-                 "flops_forward_per_block": info.flops_forward, "flops_inverse_per_block": info.flops_inverse},
+                 "flops_forward_per_block": info.flops_forward, "flops_inverse_per_block": info.flops_inverse,
+                 "exec_flops_forward_per_block": info.exec_flops_forward, "executor": info.executor},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+KERNELS = {0: "gemm_f64_kernel / gemm_f32_kernel (direct)", 1: "pipeline_kernel (tile interpreter)",
+           2: "pipeline2_kernel (FP64 tensor pipe)", 3: "gstage_* kernels (global multi-pass)",
+           4: "root pass + 8 x pipeline2_kernel (two-level, FP64 tensor pipe)",
+           5: "orbit_fft_ws_kernel (S_n on the FP64 tensor pipe + radix-2 FFT, warp-specialised)",
+           6: "orbit16_base_kernel + fft_cube_kernel (two-pass orbit-FFT: S_n on the FP64 tensor pipe, then the n^3 FFT)",
+           7: "orbit_big_s_kernel + line_fft_kernel (large-n orbit-FFT: S_n then three line-FFT passes)"}
 
 
 def main():
@@ -576,7 +741,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--n", type=int, default=None)
-    ap.add_argument("--blocks", type=int, default=None)
+    ap.add_argument("--blocks", type=int, default=None, help="blocks per GPU (weak) / in total (strong)")
     ap.add_argument("--method", default="fast", choices=["fast", "direct"])
     ap.add_argument("--precision", default=None, choices=["f64", "f32"])
     ap.add_argument("--cpu-sample", type=int, default=65536)
@@ -586,11 +751,20 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--emulate-cpu", action="store_true", help="launcher test without a GPU (gloo, host emulation)")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch (from profiles/)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        sys.exit(launch_ranks(args))
+    if world and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} under a world of {world} ranks", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         reference_arm(args)
+    elif args.emulate_cpu:
+        emulated_arm(args)
     else:
         b200_arm(args)
 

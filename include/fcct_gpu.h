@@ -15,7 +15,11 @@
  *
  * Buffers passed to fcct_forward / fcct_inverse are DEVICE pointers owned by
  * the caller; the *_host variants take HOST pointers and do the copies
- * themselves (pinned memory is used internally for the staging). The plan
+ * themselves: the batch moves in chunks alternating over two streams, so the
+ * H2D copy, the transform and the D2H copy of neighbouring chunks overlap.
+ * Page-locked caller buffers are DMA'd directly; pageable ones (a std::vector,
+ * an Eigen::VectorXcd) are staged through plan-owned pinned bounce buffers,
+ * the host-side copies split over a small thread pool. The plan
  * owns its device tables. Calls on distinct streams are safe to run
  * concurrently; results are deterministic (no atomics in any reduction).
  */
@@ -137,6 +141,9 @@ fcct_status fcct_radix_permutation(int n, uint64_t* out_host);
 /* dense_transform(n, params).matrix (transform.hpp:39-46): column-major n^3 x n^3
  * complex128, generated on the device into the caller's device buffer. */
 fcct_status fcct_dense_matrix(int n, double r, double s, double t, void* out_device, void* stream);
+/* Same matrix into HOST memory (column-major n^3 x n^3 complex128), generated
+ * on `device`: the DenseTransform::matrix of the C++ shim (include/fcct_b200.hpp). */
+fcct_status fcct_dense_matrix_host(int n, double r, double s, double t, int device, void* out_host);
 
 /* Skew node set (skew_nodes, spectral.cpp:155-171) generated on the device:
  * per node 6 complex128 values (u, v, w, x, y, z); runs the degeneracy check

@@ -16,16 +16,41 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 BUILD = HERE / "_build"
 LIB = BUILD / "liboracle.so"
-CPU_BASELINE = BUILD / "cpu_baseline"
 
 
 def build(force: bool = False) -> None:
-    srcs = [HERE / "fcct_oracle.cpp", HERE / "cpu_baseline.cpp", HERE / "Makefile"]
-    if not force and LIB.exists() and CPU_BASELINE.exists():
-        t = min(LIB.stat().st_mtime, CPU_BASELINE.stat().st_mtime)
-        if all(s.stat().st_mtime <= t for s in srcs if s.exists()):
-            return
-    subprocess.run(["make", "-C", str(HERE), "-s"], check=True)
+    srcs = [HERE / "fcct_oracle.cpp", HERE / "Makefile"]
+    if not force and LIB.exists() and all(s.stat().st_mtime <= LIB.stat().st_mtime for s in srcs if s.exists()):
+        return
+    subprocess.run(["make", "-C", str(HERE), "-s", "all"], check=True)
+
+
+def _host_key() -> str:
+    """Key of this machine's CPU (model name + ISA flags): the -march=native
+    CPU baseline is built per host, never carried across machines."""
+    import hashlib
+    import platform
+
+    info = platform.machine()
+    try:
+        text = Path("/proc/cpuinfo").read_text()
+        model = next((ln for ln in text.splitlines() if ln.startswith("model name")), "")
+        flags = next((ln for ln in text.splitlines() if ln.startswith("flags")), "")
+        info += model + flags
+    except OSError:
+        pass
+    return hashlib.sha1(info.encode()).hexdigest()[:12]
+
+
+def cpu_baseline_path(force: bool = False) -> Path:
+    """oracle/_build/host-<key>/cpu_baseline, compiled here with -march=native
+    on first use (a few seconds)."""
+    hostdir = BUILD / f"host-{_host_key()}"
+    exe = hostdir / "cpu_baseline"
+    srcs = [HERE / "cpu_baseline.cpp", HERE / "fcct_oracle.cpp", HERE / "Makefile"]
+    if force or not exe.exists() or any(s.stat().st_mtime > exe.stat().st_mtime for s in srcs):
+        subprocess.run(["make", "-C", str(HERE), "-s", "baseline", f"HOSTDIR={hostdir}"], check=True)
+    return exe
 
 
 _lib = None

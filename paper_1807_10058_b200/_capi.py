@@ -84,6 +84,7 @@ def lib() -> ctypes.CDLL:
         "fcct_inverse_real_host": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
         "fcct_radix_permutation": (c_int, [c_int, POINTER(c_uint64)]),
         "fcct_dense_matrix": (c_int, [c_int, c_double, c_double, c_double, c_void_p, c_void_p]),
+        "fcct_dense_matrix_host": (c_int, [c_int, c_double, c_double, c_double, c_int, c_void_p]),
         "fcct_skew_nodes": (c_int, [c_int, c_double, c_double, c_double, c_void_p, c_void_p]),
         "fcct_plan_kernel": (c_int, [c_void_p, POINTER(c_double)]),
         "fcct_plan_basis": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_int32), POINTER(c_double)]),
@@ -144,6 +145,7 @@ HEADER_SYMBOLS = [
     "fcct_inverse_real_host",
     "fcct_radix_permutation",
     "fcct_dense_matrix",
+    "fcct_dense_matrix_host",
     "fcct_skew_nodes",
     "fcct_plan_kernel",
     "fcct_plan_basis",

@@ -18,6 +18,7 @@
 #include "kernels.hpp"
 #include "orbit16.hpp"
 #include "orbit_big.hpp"
+#include "host_stage.hpp"
 #include "orbit_fft.hpp"
 #include "plan.hpp"
 #include "plan_cache.hpp"
@@ -601,7 +602,14 @@ struct fcct_plan_s {
     std::shared_ptr<DevBuf> ws_in[2], ws_out[2];
     cudaStream_t hs[2] = {nullptr, nullptr};  // host-path copy/compute streams
     cudaEvent_t hev = nullptr;
+    // pinned bounce buffers for pageable host buffers (host_stage.hpp)
+    PinnedBuf pin_in[2], pin_out[2];
+    cudaEvent_t h2d_ev[2] = {nullptr, nullptr}, d2h_ev[2] = {nullptr, nullptr};
     ~fcct_plan_s() {
+        for (auto e : h2d_ev)
+            if (e) cudaEventDestroy(e);
+        for (auto e : d2h_ev)
+            if (e) cudaEventDestroy(e);
         for (auto& h : hs)
             if (h) cudaStreamDestroy(h);
         for (auto& h : cs)
@@ -1251,21 +1259,53 @@ void run_host_any(fcct_plan_s* pl, bool inverse, bool real_io, const void* in, v
     for (auto h : pl->hs) ck(cudaStreamWaitEvent(h, pl->hev, 0), "stream wait");
     const char* src = static_cast<const char*>(in);
     char* dst = static_cast<char*>(out);
-    int c = 0;
-    for (int64_t off = 0; off < batch; off += chunk, ++c) {
-        const int64_t nb = std::min(chunk, batch - off);
-        cudaStream_t h = pl->hs[c & 1];
-        void* wi = pl->ws_in[c & 1]->ptr;
-        void* wo = pl->ws_out[c & 1]->ptr;
-        ck(cudaMemcpyAsync(wi, src + off * N * in_eb, static_cast<size_t>(nb * N * in_eb), cudaMemcpyHostToDevice, h),
-           "H2D");
+    // Pageable caller memory (e.g. a std::vector / Eigen::VectorXcd) is staged
+    // through pinned bounce buffers: the host copy into slot c & 1 overlaps the
+    // device work of chunk c - 1, and the copy out of chunk c - 1 overlaps
+    // chunk c. Pinned caller memory is DMA'd directly.
+    const bool stage_in = is_pageable_host(in), stage_out = is_pageable_host(out);
+    if (stage_in || stage_out) {
+        for (int k = 0; k < 2; ++k) {
+            if (stage_in) pl->pin_in[k].reserve(static_cast<size_t>(chunk * N * in_eb));
+            if (stage_out) pl->pin_out[k].reserve(static_cast<size_t>(chunk * N * out_eb));
+            if (!pl->h2d_ev[k]) ck(cudaEventCreateWithFlags(&pl->h2d_ev[k], cudaEventDisableTiming), "event");
+            if (!pl->d2h_ev[k]) ck(cudaEventCreateWithFlags(&pl->d2h_ev[k], cudaEventDisableTiming), "event");
+        }
+    }
+    const int64_t nchunks = (batch + chunk - 1) / chunk;
+    auto copy_out = [&](int64_t c) {  // host side of chunk c's D2H (staged output only)
+        const int64_t off = c * chunk, nb = std::min(chunk, batch - off);
+        ck(cudaEventSynchronize(pl->d2h_ev[c & 1]), "D2H wait");
+        par_memcpy(dst + off * N * out_eb, pl->pin_out[c & 1].ptr, static_cast<size_t>(nb * N * out_eb));
+    };
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t off = c * chunk, nb = std::min(chunk, batch - off);
+        const int k = static_cast<int>(c & 1);
+        cudaStream_t h = pl->hs[k];
+        void* wi = pl->ws_in[k]->ptr;
+        void* wo = pl->ws_out[k]->ptr;
+        const size_t ib = static_cast<size_t>(nb * N * in_eb), ob = static_cast<size_t>(nb * N * out_eb);
+        const void* hsrc = src + off * N * in_eb;
+        if (stage_in) {
+            if (c >= 2) ck(cudaEventSynchronize(pl->h2d_ev[k]), "H2D wait");  // chunk c - 2 has left the slot
+            par_memcpy(pl->pin_in[k].ptr, hsrc, ib);
+            hsrc = pl->pin_in[k].ptr;
+        }
+        ck(cudaMemcpyAsync(wi, hsrc, ib, cudaMemcpyHostToDevice, h), "H2D");
+        if (stage_in) ck(cudaEventRecord(pl->h2d_ev[k], h), "event record");
         if (real_io)
             run_real(pl, inverse, wi, wo, nb, h);
         else
             run(pl, inverse, wi, wo, nb, h);
-        ck(cudaMemcpyAsync(dst + off * N * out_eb, wo, static_cast<size_t>(nb * N * out_eb), cudaMemcpyDeviceToHost, h),
+        ck(cudaMemcpyAsync(stage_out ? pl->pin_out[k].ptr : static_cast<void*>(dst + off * N * out_eb), wo, ob,
+                           cudaMemcpyDeviceToHost, h),
            "D2H");
+        if (stage_out) {
+            ck(cudaEventRecord(pl->d2h_ev[k], h), "event record");
+            if (c >= 1) copy_out(c - 1);  // slot (c - 1) & 1 is reused by chunk c + 1
+        }
     }
+    if (stage_out) copy_out(nchunks - 1);
     for (auto h : pl->hs) ck(cudaStreamSynchronize(h), "sync");
 }
 
@@ -1457,6 +1497,19 @@ fcct_status fcct_dense_matrix(int n, double r, double s, double t, void* out_dev
         check_nodes(n, Params{r, s, t});  // transform.cpp:132
         ck(gen_dense_colmajor(n, r, s, t, static_cast<double*>(out_device), static_cast<cudaStream_t>(stream)),
            "dense matrix");
+    });
+}
+
+fcct_status fcct_dense_matrix_host(int n, double r, double s, double t, int device, void* out_host) {
+    return guarded([&] {
+        if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "dense_transform: n must be >= 1");
+        if (!out_host) throw FcctError(ST_INVALID_ARGUMENT, "null output");
+        DeviceGuard guard(device);
+        check_nodes(n, Params{r, s, t});  // transform.cpp:132
+        const size_t bytes = static_cast<size_t>(cube(n)) * cube(n) * 16;
+        DevBuf d(bytes);
+        ck(gen_dense_colmajor(n, r, s, t, static_cast<double*>(d.ptr), nullptr), "dense matrix");
+        ck(cudaMemcpy(out_host, d.ptr, bytes, cudaMemcpyDeviceToHost), "D2H");
     });
 }
 

@@ -327,6 +327,8 @@ class TransformPlan:
         x = x.contiguous()
         out = torch.empty(x.shape, dtype=rdt if real_out else dt, device=x.device)
         if x.is_cuda:
+            if x.device.index != self.device:
+                raise ValueError(f"tensor on {x.device}, plan on cuda:{self.device}")
             stream = torch.cuda.current_stream(x.device).cuda_stream
             if real_in:
                 st = L.fcct_forward_real(self._h, x.data_ptr(), out.data_ptr(), batch, stream)

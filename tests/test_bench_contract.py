@@ -55,3 +55,57 @@ def test_own_arm_json_line():
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert line["gpu_launches"] > 0
     assert line["clocks"]["sm_max_mhz"] > 0
+
+
+@pytest.mark.timeout(300)
+def test_multi_rank_launcher_end_to_end_on_cpu():
+    """`bench.py --gpus 2` outside torchrun starts two ranks itself
+    (torch.distributed.run on 127.0.0.1); --emulate-cpu runs them over gloo on
+    the host emulation of the compiled orbit-FFT tables. c5 is the strong-scaling
+    config: the ragged 37-block volume is split 19 + 18 with no collective on the
+    data path, and rank 0 prints one line with n_gpus = 2."""
+    out = subprocess.run(
+        [sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--emulate-cpu", "--config", "c5", "--blocks", "37",
+         "--steps", "2", "--warmup", "3"],
+        check=True, capture_output=True, text=True, cwd=ROOT, timeout=280,
+    )
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["blocks_total"] == 37 and line["config"]["blocks_per_gpu_max"] == 19
+    assert [tuple(s) for s in line["shards"]] == [(0, 19), (19, 37)]
+    assert line["roundtrip_rel_err"] < 1e-12
+    assert line["value"] > 0
+
+
+def test_launcher_fails_loudly_without_enough_gpus():
+    import torch
+
+    if torch.cuda.device_count() >= 64:
+        pytest.skip("this host has 64 GPUs")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "64", "--steps", "1"],
+                       capture_output=True, text=True, cwd=ROOT, timeout=120)
+    assert r.returncode != 0
+    assert "visible" in r.stderr
+
+
+@pytest.mark.timeout(300)
+def test_reference_arm_config_equals_own_arm_config():
+    """The driver compares the two arms' `config` objects: both come from
+    bench.workload() with the same arguments."""
+    sys.path.insert(0, str(ROOT))
+    import argparse
+
+    import bench
+
+    out = subprocess.run(
+        [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "c1", "--steps", "1",
+         "--warmup", "3"],
+        check=True, capture_output=True, text=True, cwd=ROOT,
+    )
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    args = argparse.Namespace(config="c1", n=None, precision=None, real_io=None, blocks=None, method="fast")
+    assert line["config"] == bench.workload(args, 1)["config"]
+    cpu = line["cpu_baseline"]
+    assert cpu["cores"] == 1 and "threads=1" in cpu["sample"]
