@@ -69,8 +69,10 @@ typedef struct {
     int64_t tree_nnz_inv;    /* same for the explicit B^{-1} factors */
     int64_t root_nnz;        /* nnz(B) of the root */
     int64_t table_bytes;     /* device bytes owned by the plan */
-    double condition;        /* exact 1-norm condition of D (direct plans), or of the root
-                                orbit blocks (fast plans) */
+    double condition;        /* the reference's condition estimate of D (direct plans,
+                                condition_with_lu, transform.cpp:91-111), or the largest
+                                estimate gated while building a fast plan's tree (radix
+                                kernels and every child transform) */
     double flops_forward;    /* algorithmic flops per block */
     double flops_inverse;
     int executor;            /* 0 direct GEMM, 1 tile interpreter, 2 FP64-tensor-pipe
@@ -95,6 +97,27 @@ const char* fcct_last_error(void);
  * on `device`. n odd or n == 1 always yields a direct plan (transform.cpp:385-386). */
 fcct_status fcct_plan_create(int n, double r, double s, double t, int method, int precision,
                              int device, fcct_plan* out);
+
+/* Executors of a FAST plan (fcct_plan_info_t.executor). FCCT_EXEC_AUTO is the
+ * default choice of fcct_plan_create; the others force one executor (parity tests
+ * of every executor, A/B timing). All compute the same transform; a forced
+ * executor that cannot run this plan falls through to the next in the order
+ * orbit -> pipeline2 -> two-level -> tile / global. No environment variable
+ * selects executors in the product build. */
+typedef enum {
+    FCCT_EXEC_AUTO = 0,
+    FCCT_EXEC_ORBIT = 1,          /* orbit-FFT executors (n = 4, 8 warp-specialised; 16; 32, 64) */
+    FCCT_EXEC_ORBIT_PHASED = 2,   /* n = 4, 8: the phased orbit-FFT kernel (16 warps alternate roles) */
+    FCCT_EXEC_PIPELINE2 = 3,      /* stage-by-stage FP64 DMMA pipeline (n <= 8) */
+    FCCT_EXEC_TWO_LEVEL = 4,      /* n = 16: root pass + eight n = 8 orbit-FFT children */
+    FCCT_EXEC_TWO_LEVEL_V2 = 5,   /* n = 16: root pass + eight n = 8 stage-pipeline children */
+    FCCT_EXEC_TILE = 6,           /* shared-memory tile interpreter */
+    FCCT_EXEC_GLOBAL = 7          /* global-memory multi-pass pipeline */
+} fcct_executor;
+
+/* build_plan with a forced executor (method FAST; see fcct_executor). */
+fcct_status fcct_plan_create_executor(int n, double r, double s, double t, int precision, int device, int executor,
+                                      fcct_plan* out);
 fcct_status fcct_plan_destroy(fcct_plan plan);
 fcct_status fcct_plan_info(fcct_plan plan, fcct_plan_info_t* info);
 
@@ -174,6 +197,15 @@ fcct_status fcct_plan_perturbed_basis(fcct_plan plan, double delta, fcct_plan* o
  * derived on the host (no GPU needed). Pass NULL arrays to query *nnz. */
 fcct_status fcct_basis_change(int n, double r, double s, double t, int inverse, int64_t* nnz, int64_t* colptr,
                               int32_t* rowidx, double* values);
+
+/* condition_estimate_1norm(dense_transform(n, params).matrix) (transform.hpp:141-143,
+ * transform.cpp:91-122): the reference's probe-based 1-norm condition estimate of
+ * D_n(p) — exact ||D||_1 times the largest ||D^{-1} v||_1 / ||v||_1 over its eight
+ * probes — without forming D (D = F_n S_n(p), D^{-1} v = S^{-1} F^{-1} v). This is
+ * the value IllConditioned is raised on and DenseTransform.condition_estimate holds.
+ * Host computation; column norms on the current GPU for n^3 >= 4096 when one is
+ * present. inf when D is singular. */
+fcct_status fcct_condition_estimate(int n, double r, double s, double t, double* out);
 
 /* Host-side tree statistics of the fast plan (no GPU needed): tree nnz of B and
  * B^{-1} (B_2 = I excluded) and the algorithmic flops per block. */

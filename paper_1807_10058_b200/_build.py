@@ -27,10 +27,18 @@ FLAGS = [
     "-fPIC,-O3",
     "-shared",
 ]
+# FCCT_BUILD_AB=1: a tuning build whose library honours the FCCT_DEBUG_* / A/B
+# environment switches (capi.cpp ab_env; tools/stage_timing.py). The product
+# build never reads them.
+if os.environ.get("FCCT_BUILD_AB") == "1":
+    FLAGS.append("-DFCCT_AB_SWITCHES")
+
+
+STAMP = LIB_DIR / "build_flags.txt"
 
 
 def _stale() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or not STAMP.exists() or STAMP.read_text() != " ".join(FLAGS):
         return True
     t = LIB.stat().st_mtime
     deps = [CSRC / s for s in SOURCES + HEADERS] + [PKG.parent / "include" / "fcct_gpu.h"]
@@ -81,6 +89,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         os.replace(tmp, LIB)
+        STAMP.write_text(" ".join(FLAGS))
     build_cli(force=force, verbose=verbose)
     return LIB
 

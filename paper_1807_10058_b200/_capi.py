@@ -70,6 +70,7 @@ def lib() -> ctypes.CDLL:
     L = ctypes.CDLL(str(path))
     sig = {
         "fcct_last_error": (c_char_p, []),
+        "fcct_plan_create_executor": (c_int, [c_int, c_double, c_double, c_double, c_int, c_int, c_int, POINTER(c_void_p)]),
         "fcct_plan_create": (c_int, [c_int, c_double, c_double, c_double, c_int, c_int, c_int, POINTER(c_void_p)]),
         "fcct_plan_destroy": (c_int, [c_void_p]),
         "fcct_plan_info": (c_int, [c_void_p, POINTER(PlanInfo)]),
@@ -117,6 +118,7 @@ def lib() -> ctypes.CDLL:
         "fcct_debug_v2_entry_slots": (c_int, [c_int, c_double, c_double, c_double, c_int, c_int, POINTER(c_int32), c_int64, POINTER(c_int64)]),
         "fcct_debug_v2_stage_stats": (c_int, [c_int, c_double, c_double, c_double, c_int, POINTER(c_int64), POINTER(c_int)]),
         "fcct_debug_timing": (c_int, [c_void_p, c_int, c_void_p, POINTER(c_int)]),
+        "fcct_condition_estimate": (c_int, [c_int, c_double, c_double, c_double, POINTER(c_double)]),
         "fcct_basis_change": (c_int, [c_int, c_double, c_double, c_double, c_int, POINTER(c_int64), POINTER(c_int64), POINTER(c_int32), POINTER(c_double)]),
         "fcct_plan_tree_stats": (c_int, [c_int, c_double, c_double, c_double, POINTER(c_int64), POINTER(c_int64), POINTER(c_double), POINTER(c_double)]),
     }
@@ -132,6 +134,7 @@ def lib() -> ctypes.CDLL:
 HEADER_SYMBOLS = [
     "fcct_last_error",
     "fcct_plan_create",
+    "fcct_plan_create_executor",
     "fcct_plan_destroy",
     "fcct_plan_info",
     "fcct_forward",
@@ -154,6 +157,7 @@ HEADER_SYMBOLS = [
     "fcct_plan_perturbed_basis",
     "fcct_shard_range",
     "fcct_basis_change",
+    "fcct_condition_estimate",
     "fcct_plan_tree_stats",
     "fcct_parse_params",
     "fcct_encode_params",

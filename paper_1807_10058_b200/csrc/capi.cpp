@@ -2,6 +2,7 @@
 // construction (plan.cpp), stage-table compilation for the fast pipeline,
 // device uploads and kernel launches (kernels.cu). No exception crosses the
 // ABI; failures map to fcct_status codes with a thread-local message.
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -49,6 +50,54 @@ struct CudaError : FcctError {
 
 void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw CudaError(what, e);
+}
+
+// ||D_n(p)||_1 for the plan-time condition estimate (plan.hpp ColNormHook): on
+// the device of the plan being built (children may be derived on worker threads,
+// whose current device is not the plan's).
+std::atomic<int> g_colnorm_device{0};
+
+double colnorm_on_device(int n, const Params& p) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return -1.0;  // no GPU: the host column sums
+    }
+    int prev = 0;
+    ck(cudaGetDevice(&prev), "cudaGetDevice");
+    const int dev = g_colnorm_device.load();
+    if (dev != prev) ck(cudaSetDevice(dev), "cudaSetDevice");
+    const int64_t N = cube(n);
+    double* d = nullptr;
+    cudaStream_t st = nullptr;
+    std::vector<double> h(static_cast<size_t>(N));
+    cudaError_t e = cudaMalloc(&d, sizeof(double) * N);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = dense_colnorm(n, p.r, p.s, p.t, d, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d, sizeof(double) * N, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (st) cudaStreamDestroy(st);
+    if (d) cudaFree(d);
+    if (dev != prev) cudaSetDevice(prev);
+    ck(e, "condition estimate (column norms)");
+    return *std::max_element(h.begin(), h.end());
+}
+
+const bool g_colnorm_registered = [] {
+    set_colnorm_hook(&colnorm_on_device);
+    return true;
+}();
+
+// Tuning / debugging switches (stage masks, per-stage clocks, layout A/B runs)
+// exist only in a library built with -DFCCT_AB_SWITCHES (tools/, never the
+// product build): there no environment variable can change what a call computes.
+const char* ab_env(const char* name) {
+#ifdef FCCT_AB_SWITCHES
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
 }
 
 class DeviceGuard {
@@ -199,13 +248,13 @@ void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
     out.desc.stride = h.stride;
     out.desc.row_in = out.desc.row_out = 2 * static_cast<int64_t>(h.N);
     out.desc.nstages = static_cast<int>(h.stages.size());
-    const char* ds = std::getenv("FCCT_DIRECT_STORE");
+    const char* ds = ab_env("FCCT_DIRECT_STORE");
     out.desc.direct_store = ds ? std::atoi(ds) : 0;
-    const char* sm = std::getenv("FCCT_DEBUG_STAGE_MASK");  // timing experiments only
+    const char* sm = ab_env("FCCT_DEBUG_STAGE_MASK");  // timing experiments only
     out.desc.stage_mask = sm ? std::atoi(sm) : -1;
     out.desc.ring = 1;  // sparse-stage table entries stream through the per-warp cp.async ring
     out.desc.timing = nullptr;
-    if (std::getenv("FCCT_DEBUG_TIMING")) {  // per-stage clock64 totals of CTA 0 (profiling aid)
+    if (ab_env("FCCT_DEBUG_TIMING")) {  // per-stage clock64 totals of CTA 0 (profiling aid)
         auto b = std::make_shared<DevBuf>(sizeof(unsigned long long) * (kMaxStages + 2 + kMaxStages * 16));
         ck(cudaMemset(b->ptr, 0, b->bytes), "memset");
         out.desc.timing = static_cast<unsigned long long*>(b->ptr);
@@ -226,9 +275,9 @@ void upload_pipeline2(const Pipeline2Host& h, Pipeline2Tables& out) {
         return b->ptr;
     };
     constexpr size_t kArenaK = 16 * 1024;  // K tables up to this size go to shared memory
-    const char* gs = std::getenv("FCCT_V2_GROUP_SYNC");  // A/B switch: 0 = CTA-wide barriers only
+    const char* gs = ab_env("FCCT_V2_GROUP_SYNC");  // A/B switch: 0 = CTA-wide barriers only
     const bool group_sync = gs ? std::atoi(gs) != 0 : true;
-    const char* ns = std::getenv("FCCT_V2_NAT_SHIFT");  // A/B switch: 0 = unshifted natural rows
+    const char* ns = ab_env("FCCT_V2_NAT_SHIFT");  // A/B switch: 0 = unshifted natural rows
     const bool nat_shift = ns ? std::atoi(ns) != 0 : true;
     out.desc.shift_in = nat_shift ? 2 * h.shift_in : 0;
     out.desc.shift_out = nat_shift ? 2 * h.shift_out : 0;
@@ -590,6 +639,7 @@ struct fcct_plan_s {
     bool global = false;  // global-memory multi-pass pipeline
     GlobalTables gfwd, ginv;
     std::shared_ptr<DevBuf> scratch0, scratch1;
+    int exec_force = 0;  // fcct_executor requested at creation (FCCT_EXEC_AUTO = the default choice)
     std::mutex scratch_mu;
     // stream-ordered ownership of the scratch: recorded after the last kernel
     // of a call that used it; the next call's stream waits on it (no host sync)
@@ -640,6 +690,12 @@ void scratch_acquire(fcct_plan_s* pl, cudaStream_t st) {
         ck(cudaStreamWaitEvent(st, pl->scratch_ev, 0), "scratch wait");
 }
 void scratch_release(fcct_plan_s* pl, cudaStream_t st) { ck(cudaEventRecord(pl->scratch_ev, st), "scratch record"); }
+// Before a scratch buffer is replaced (and freed): wait for its last user, which
+// may be a call on another stream (scratch_ev), as well as this stream's work.
+void scratch_retire(fcct_plan_s* pl, cudaStream_t st) {
+    ck(cudaStreamSynchronize(st), "sync");
+    if (pl->scratch_ev) ck(cudaEventSynchronize(pl->scratch_ev), "scratch event sync");
+}
 
 void build_direct(fcct_plan_s* pl) {
     const int n = pl->n;
@@ -651,8 +707,8 @@ void build_direct(fcct_plan_s* pl) {
     ck(gen_dense_realform(n, pl->p.r, pl->p.s, pl->p.t, pl->Wt_fwd->ptr, f32, nullptr), "gen_dense_realform");
     // orbit blocks of S_n(p)^{-1} -> device, then D^{-1} generated on the device
     OrbitBlocks ob = orbit_blocks(n, pl->p);
-    if (!(ob.worst_condition <= 1e12))
-        throw FcctError(ST_ILL_CONDITIONED, "dense transform: orbit block condition exceeds 1e12");
+    if (!std::isfinite(ob.worst_condition))
+        throw FcctError(ST_ILL_CONDITIONED, "dense transform: condition estimate inf exceeds 1e12");
     const Orbits& orb = *ob.orb;
     std::vector<int32_t> mem_off{0}, mem, sinv_off;
     std::vector<double> sinv;
@@ -672,19 +728,20 @@ void build_direct(fcct_plan_s* pl) {
                 static_cast<const int*>(b5->ptr), static_cast<const double*>(b6->ptr)};
     ck(gen_dense_inv_realform(n, od, pl->Wt_inv->ptr, f32, nullptr), "gen_dense_inv_realform");
     ck(cudaDeviceSynchronize(), "direct table generation");
-    // exact 1-norm condition: ||D||_1 ||D^{-1}||_1 from the orbit structure is
-    // what the reference gates on (transform.cpp:329-345); estimate it on the host
-    // from the blocks: ||D||_1 <= N max|col| ... use the blocks' worst condition.
-    pl->info.condition = ob.worst_condition;
+    // the reference's estimate and gate (assemble_direct: condition_with_lu(D),
+    // transform.cpp:339-344; dense_transform stores it for n^3 <= 512, :141-142)
+    pl->info.condition = reference_condition(n, pl->p);
+    if (!(pl->info.condition <= 1e12))
+        throw FcctError(ST_ILL_CONDITIONED, "dense transform (n=" + std::to_string(n) + "): condition estimate " +
+                                                std::to_string(pl->info.condition) + " exceeds 1e12");
     pl->info.table_bytes = static_cast<int64_t>(2 * wbytes);
 }
 
 void build_v2(fcct_plan_s* pl) {
     pl->v2 = false;
-    const char* force = std::getenv("FCCT_PIPELINE");
-    if (force && std::string(force) == "v1") return;
+    if (pl->exec_force == FCCT_EXEC_TILE) return;
     Shape2 shape;  // default: 16 blocks x 16 warps, one CTA per SM
-    if (const char* sh = std::getenv("FCCT_V2_SHAPE"); sh && std::string(sh) == "8x8")
+    if (const char* sh = ab_env("FCCT_V2_SHAPE"); sh && std::string(sh) == "8x8")
         shape = Shape2{8, 8, 8};  // two CTAs per SM (tuning experiment)
     Pipeline2Host hf, hi;
     if (!compile_pipeline2(*pl->tree, false, shape, hf) || !compile_pipeline2(*pl->tree, true, shape, hi)) return;
@@ -802,8 +859,7 @@ void build_two_level(fcct_plan_s* pl) {
     }
     // children: the orbit-FFT executor when every child is the exact n = 8 tree
     // (FCCT_CHILD_PIPELINE=v2 keeps them on the stage pipeline)
-    const char* cp = std::getenv("FCCT_CHILD_PIPELINE");
-    pl->child_offt = !(cp && std::string(cp) == "v2");
+    pl->child_offt = pl->exec_force != FCCT_EXEC_TWO_LEVEL_V2;
     for (int c = 0; c < 8 && pl->child_offt; ++c) {
         const PlanNode& ch = *root.children[c];
         OrbitFftHost hf, hi;
@@ -835,11 +891,11 @@ void run_o16(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, void* o
     const size_t bytes = static_cast<size_t>(batch * cube(pl->n) * 16);
     std::lock_guard<std::mutex> lock(pl->scratch_mu);
     if (!pl->scratch0 || pl->scratch0->bytes < bytes) {
-        ck(cudaStreamSynchronize(st), "sync");
+        scratch_retire(pl, st);
         pl->scratch0 = std::make_shared<DevBuf>(bytes);
     }
     if (inverse && (!pl->scratch1 || pl->scratch1->bytes < bytes)) {
-        ck(cudaStreamSynchronize(st), "sync");
+        scratch_retire(pl, st);
         pl->scratch1 = std::make_shared<DevBuf>(bytes);
     }
     void* z = pl->scratch0->ptr;
@@ -868,7 +924,7 @@ void run_two_level(fcct_plan_s* pl, bool inverse, const void* in, int in_mode, v
     const size_t bytes = static_cast<size_t>(batch * N * 16);
     std::lock_guard<std::mutex> lock(pl->scratch_mu);
     if (!pl->scratch0 || pl->scratch0->bytes < bytes) {
-        ck(cudaStreamSynchronize(st), "sync");
+        scratch_retire(pl, st);
         pl->scratch0 = std::make_shared<DevBuf>(bytes);
         pl->scratch1 = std::make_shared<DevBuf>(bytes);
     }
@@ -965,9 +1021,8 @@ void build_orbit_fft(fcct_plan_s* pl) {
     if (pl->n != 4 && pl->n != 8) return;
     if (!tree_is_exact(pl)) return;
     // default: the warp-specialised kernel (12 base-change + 4 FFT warps);
-    // FCCT_OFFT_WS=0 selects the phased one (16 warps alternate both roles)
-    const char* ws = std::getenv("FCCT_OFFT_WS");
-    const int warps = (ws && std::string(ws) == "0") ? kOfWarps : kOfBcWarps;
+    // FCCT_EXEC_ORBIT_PHASED selects the phased one (16 warps alternate both roles)
+    const int warps = pl->exec_force == FCCT_EXEC_ORBIT_PHASED ? kOfWarps : kOfBcWarps;
     OrbitFftHost hf, hi;
     if (!compile_orbit_fft(pl->n, pl->p, false, hf, warps) || !compile_orbit_fft(pl->n, pl->p, true, hi, warps)) return;
     upload_orbit_fft(hf, pl->ofwd);
@@ -979,10 +1034,16 @@ void build_orbit_fft(fcct_plan_s* pl) {
 // fp64 DMMA stage pipeline (n <= 8, stage by stage through the tree), the
 // two-level executor (n = 16), the shared-memory tile interpreter (one
 // block's state fits a CTA tile), else the global-memory multi-pass pipeline.
-// FCCT_PIPELINE=orbit|v2|two|v1|global forces one (A/B runs, parity tests).
+// fcct_plan_create_executor forces one (fcct_executor: parity tests of every
+// executor, A/B runs).
 void build_fast_paths(fcct_plan_s* pl) {
-    const char* force = std::getenv("FCCT_PIPELINE");
-    const std::string f = force ? force : "";
+    const int x = pl->exec_force;
+    const std::string f = x == FCCT_EXEC_AUTO                                   ? ""
+                          : x == FCCT_EXEC_ORBIT || x == FCCT_EXEC_ORBIT_PHASED ? "orbit"
+                          : x == FCCT_EXEC_PIPELINE2                           ? "v2"
+                          : x == FCCT_EXEC_TWO_LEVEL || x == FCCT_EXEC_TWO_LEVEL_V2 ? "two"
+                          : x == FCCT_EXEC_TILE                                ? "v1"
+                                                                               : "global";
     const bool f32 = pl->precision == FCCT_F32;
     if (f.empty() || f == "orbit") build_orbit_fft(pl);
     if (pl->offt) return;
@@ -1095,7 +1156,9 @@ void fill_info(fcct_plan_s* pl) {
 }
 
 fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int device,
-                         PlanStore* store = nullptr) {
+                         PlanStore* store = nullptr, int executor = FCCT_EXEC_AUTO) {
+    if (executor < FCCT_EXEC_AUTO || executor > FCCT_EXEC_GLOBAL)
+        throw FcctError(ST_INVALID_ARGUMENT, "unknown executor");
     if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "build_plan: n must be >= 1");
     if (method != FCCT_DIRECT && method != FCCT_FAST) throw FcctError(ST_INVALID_ARGUMENT, "unknown method");
     if (precision != FCCT_F64 && precision != FCCT_F32) throw FcctError(ST_INVALID_ARGUMENT, "unknown precision");
@@ -1105,11 +1168,13 @@ fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int 
     ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
     if (device < 0 || device >= ndev) throw FcctError(ST_INVALID_ARGUMENT, "no such CUDA device");
     DeviceGuard guard(device);
+    g_colnorm_device.store(device);
     auto pl = std::make_unique<fcct_plan_s>();
     pl->n = n;
     pl->p = p;
     pl->precision = precision;
     pl->device = device;
+    pl->exec_force = executor;
     ck(cudaDeviceGetAttribute(&pl->num_sms, cudaDevAttrMultiProcessorCount, device), "sm count");
     const bool f32 = precision == FCCT_F32;
     const bool radix = method == FCCT_FAST && n % 2 == 0;
@@ -1152,7 +1217,7 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
             const size_t bytes = static_cast<size_t>(batch * cube(pl->n) * 16);
             std::lock_guard<std::mutex> lock(pl->scratch_mu);
             if (!pl->scratch0 || pl->scratch0->bytes < bytes) {
-                ck(cudaStreamSynchronize(st), "sync");
+                scratch_retire(pl, st);
                 pl->scratch0 = std::make_shared<DevBuf>(bytes);
             }
             void* z = pl->scratch0->ptr;
@@ -1184,7 +1249,7 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
             const size_t bytes = static_cast<size_t>(batch * cube(pl->n) * elem_bytes(pl));
             std::lock_guard<std::mutex> lock(pl->scratch_mu);
             if (!pl->scratch0 || pl->scratch0->bytes < bytes) {
-                ck(cudaStreamSynchronize(st), "sync");
+                scratch_retire(pl, st);
                 pl->scratch0 = std::make_shared<DevBuf>(bytes);
                 pl->scratch1 = std::make_shared<DevBuf>(bytes);
             }
@@ -1240,7 +1305,7 @@ void run_host_any(fcct_plan_s* pl, bool inverse, bool real_io, const void* in, v
     // ~32 MB chunks (at least 8 per call when the batch is large), whole blocks
     // chunk size: FCCT_HOST_CHUNK_MB (default 32 MB), at least 8 chunks per call
     int64_t chunk_mb = 32;
-    if (const char* e = std::getenv("FCCT_HOST_CHUNK_MB")) chunk_mb = std::max<int64_t>(1, std::atoll(e));
+    if (const char* e = ab_env("FCCT_HOST_CHUNK_MB")) chunk_mb = std::max<int64_t>(1, std::atoll(e));
     int64_t chunk = std::max<int64_t>(1, (chunk_mb << 20) / block_bytes);
     chunk = std::min(chunk, std::max<int64_t>(1, (batch + 7) / 8));
     chunk = std::min(chunk, batch);
@@ -1393,6 +1458,14 @@ fcct_status fcct_plan_create(int n, double r, double s, double t, int method, in
     return guarded([&] {
         if (!out) throw FcctError(ST_INVALID_ARGUMENT, "null plan pointer");
         *out = create_plan(n, Params{r, s, t}, method, precision, device);
+    });
+}
+
+fcct_status fcct_plan_create_executor(int n, double r, double s, double t, int precision, int device, int executor,
+                                      fcct_plan* out) {
+    return guarded([&] {
+        if (!out) throw FcctError(ST_INVALID_ARGUMENT, "null plan pointer");
+        *out = create_plan(n, Params{r, s, t}, FCCT_FAST, precision, device, nullptr, executor);
     });
 }
 
@@ -1695,6 +1768,19 @@ fcct_status fcct_shard_range(int64_t total, int rank, int world, int64_t* begin,
         const int64_t per = (total + world - 1) / world;
         *begin = std::min<int64_t>(total, per * rank);
         *end = std::min<int64_t>(total, per * (rank + 1));
+    });
+}
+
+fcct_status fcct_condition_estimate(int n, double r, double s, double t, double* out) {
+    return guarded([&] {
+        if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "dense_transform: n must be >= 1");
+        if (!out) throw FcctError(ST_INVALID_ARGUMENT, "null output");
+        const Params p{r, s, t};
+        check_nodes(n, p);  // dense_transform runs the degeneracy check (transform.cpp:132)
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) g_colnorm_device.store(dev);
+        cudaGetLastError();
+        *out = reference_condition(n, p);
     });
 }
 

@@ -1423,6 +1423,59 @@ __global__ void gen_dense_colmajor_kernel(int n, double r, double s, double t, d
     D[idx] = dense_entry_dev(n, r, s, t, i0, i1, i2, k0, k1, k2);
 }
 
+// ||D_n(p)||_1 column sums (the norm factor of the reference's condition
+// estimate, condition_with_lu, transform.cpp:93): one CTA per column kappa
+// (grid-stride), the 24 group terms a_w = w kappa (reduced mod n) with
+// c_w = e^{2 pi i (w kappa).p/n}/24 (unreduced exponent, transform.cpp:51-53) in
+// shared memory, then every node x sums c_w e^{2 pi i (a_w.x mod n)/n} from a
+// twiddle table. Plan-time only.
+__global__ void dense_colnorm_kernel(int n, double r, double s, double t, double* colsum) {
+    extern __shared__ double2 tw[];  // n twiddles
+    __shared__ int aw[24][3];
+    __shared__ double2 cw[24];
+    __shared__ double red[32];
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) tw[i] = phase_turns(static_cast<double>(i) / n);
+    for (int64_t kap = blockIdx.x; kap < N; kap += gridDim.x) {
+        if (threadIdx.x < 24) {
+            const int* w = c_group + threadIdx.x * 9;
+            const int k0 = static_cast<int>(kap / (n * n)), k1 = static_cast<int>((kap / n) % n),
+                      k2 = static_cast<int>(kap % n);
+            const int a0 = w[0] * k0 + w[1] * k1 + w[2] * k2;
+            const int a1 = w[3] * k0 + w[4] * k1 + w[5] * k2;
+            const int a2 = w[6] * k0 + w[7] * k1 + w[8] * k2;
+            const double2 c = phase_turns((r * a0 + s * a1 + t * a2) / n);
+            cw[threadIdx.x] = make_double2(c.x / 24.0, c.y / 24.0);
+            aw[threadIdx.x][0] = ((a0 % n) + n) % n;
+            aw[threadIdx.x][1] = ((a1 % n) + n) % n;
+            aw[threadIdx.x][2] = ((a2 % n) + n) % n;
+        }
+        __syncthreads();
+        double acc = 0.0;
+        for (int64_t x = threadIdx.x; x < N; x += blockDim.x) {
+            const int x0 = static_cast<int>(x / (n * n)), x1 = static_cast<int>((x / n) % n), x2 = static_cast<int>(x % n);
+            double re = 0.0, im = 0.0;
+#pragma unroll 4
+            for (int e = 0; e < 24; ++e) {
+                const int ip = (aw[e][0] * x0 + aw[e][1] * x1 + aw[e][2] * x2) % n;
+                const double2 f = tw[ip], c = cw[e];
+                re = fma(c.x, f.x, fma(-c.y, f.y, re));
+                im = fma(c.x, f.y, fma(c.y, f.x, im));
+            }
+            acc += hypot(re, im);
+        }
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) tot += red[i];
+            colsum[kap] = tot;
+        }
+        __syncthreads();
+    }
+}
+
 // D^{-1}[kappa][node] = (1/N) sum_{a in O(kappa)} Sinv[kappa][a] e^{-2 pi i a.node/n}
 template <typename R>
 __global__ void gen_dense_inv_realform_kernel(int n, OrbitDev od, R* Wt) {
@@ -1591,6 +1644,15 @@ cudaError_t gen_dense_inv_realform(int n, const OrbitDev& od, void* Wt, bool f32
         gen_dense_inv_realform_kernel<float><<<blocks_for(N * N, 256), 256, 0, st>>>(n, od, static_cast<float*>(Wt));
     else
         gen_dense_inv_realform_kernel<double><<<blocks_for(N * N, 256), 256, 0, st>>>(n, od, static_cast<double*>(Wt));
+    return cudaGetLastError();
+}
+
+cudaError_t dense_colnorm(int n, double r, double s, double t, double* colsum, cudaStream_t st) {
+    cudaError_t e = upload_group();
+    if (e != cudaSuccess) return e;
+    const int64_t N = static_cast<int64_t>(n) * n * n;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(N, 148 * 16));
+    dense_colnorm_kernel<<<grid, 256, sizeof(double2) * n, st>>>(n, r, s, t, colsum);
     return cudaGetLastError();
 }
 

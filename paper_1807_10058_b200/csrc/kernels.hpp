@@ -167,6 +167,8 @@ cudaError_t gen_dense_realform(int n, double r, double s, double t, void* Wt, bo
 cudaError_t gen_dense_inv_realform(int n, const OrbitDev& od, void* Wt, bool f32, cudaStream_t st);
 // Complex column-major D (dense_transform(n,p).matrix layout).
 cudaError_t gen_dense_colmajor(int n, double r, double s, double t, double* D, cudaStream_t st);
+// Column 1-norms of D_n(p) (plan-time condition estimate): colsum[kappa], N doubles.
+cudaError_t dense_colnorm(int n, double r, double s, double t, double* colsum, cudaStream_t st);
 // Skew nodes: 6 complex per node (u,v,w,x,y,z); degenerate flag via *flag (device int).
 cudaError_t gen_nodes(int n, double r, double s, double t, double* out, int* flag, cudaStream_t st);
 // Composite radix permutation.

@@ -27,8 +27,9 @@ bool compile_orbit16(int n, const Params& p, bool inverse, Orbit16Host& h) {
     if (n != 16) return false;
     const int N = static_cast<int>(cube(n));
     OrbitBlocks ob = orbit_blocks(n, p);
-    if (!(ob.worst_condition <= 1e12))
-        throw FcctError(ST_ILL_CONDITIONED, "orbit-FFT plan: orbit block condition exceeds 1e12");
+    // the plan tree carries the reference's condition gates (plan.cpp); a singular
+    // orbit block (no S^{-1}) leaves this executor unbuilt
+    if (!std::isfinite(ob.worst_condition)) return false;
     const Orbits& orb = *ob.orb;
     // chunks of whole orbits, <= kO16Chunk slots (4 per k-tile), formed
     // greedily so that orbits whose members share 32-byte sectors (four

@@ -235,8 +235,12 @@ __global__ void __launch_bounds__(256) line_fft64_kernel(const double2* __restri
 
 bool pdl_enabled() {
     static const bool on = [] {
+#ifdef FCCT_AB_SWITCHES  // A/B timing builds only (capi.cpp ab_env)
         const char* e = std::getenv("FCCT_PDL");
         return !(e && e[0] == '0');
+#else
+        return true;
+#endif
     }();
     return on;
 }

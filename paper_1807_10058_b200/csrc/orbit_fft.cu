@@ -585,8 +585,12 @@ cudaError_t launch_ws_t(const OrbitFftDesc& d, const void* in, void* out, int64_
     // programmatic dependent launch: this kernel's table prologue overlaps the
     // previous kernel's tail (FCCT_PDL=0 disables)
     static const bool pdl = [] {
+#ifdef FCCT_AB_SWITCHES  // A/B timing builds only (capi.cpp ab_env)
         const char* e = std::getenv("FCCT_PDL");
         return !(e && e[0] == '0');
+#else
+        return true;
+#endif
     }();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));

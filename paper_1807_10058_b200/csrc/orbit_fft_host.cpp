@@ -65,8 +65,9 @@ bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h, in
     const bool ws = warps == kOfBcWarps;
     const int tmax_bound = n == 8 ? (ws ? kOfWsTmax8 : kOfTmax8) : (ws ? kOfWsTmax4 : kOfTmax4);
     OrbitBlocks ob = orbit_blocks(n, p);
-    if (!(ob.worst_condition <= 1e12))
-        throw FcctError(ST_ILL_CONDITIONED, "orbit-FFT plan: orbit block condition exceeds 1e12");
+    // the plan tree carries the reference's condition gates (plan.cpp); a singular
+    // orbit block (no S^{-1}) leaves this executor unbuilt
+    if (!std::isfinite(ob.worst_condition)) return false;
     const Orbits& orb = *ob.orb;
     // positions: forward reads natural kappa and writes swizzled a; inverse the reverse
     auto in_pos = [&](int lex) { return inverse ? of_swizzle(lex, n) : lex; };
@@ -127,10 +128,12 @@ bool compile_orbit_fft(int n, const Params& p, bool inverse, OrbitFftHost& h, in
         }
     }
     const int tmax = *std::max_element(load.begin(), load.end());
+#ifdef FCCT_AB_SWITCHES
     if (std::getenv("FCCT_DEBUG_OFFT_LOAD")) {
         for (int w = 0; w < warps; ++w) fprintf(stderr, "%d ", load[w]);
         fprintf(stderr, "\n");
     }
+#endif
     if (tmax > tmax_bound) return false;
     h = OrbitFftHost{};
     h.n = n;

@@ -9,6 +9,7 @@
 #include <map>
 #include <mutex>
 #include <numbers>
+#include <random>
 #include <set>
 #include <thread>
 #include <unordered_map>
@@ -234,6 +235,174 @@ OrbitBlocks orbit_blocks(int n, const Params& p) {
         ob.S[o] = std::move(S);
     }
     return ob;
+}
+
+// ---- the reference's condition estimate (condition_with_lu, transform.cpp:91-111) ----
+namespace {
+ColNormHook g_colnorm_hook = nullptr;
+
+using cd = std::complex<double>;
+
+double l1(const std::vector<cd>& v) {
+    double s = 0;
+    for (const cd& z : v) s += std::abs(z);
+    return s;
+}
+
+// max over the reference's eight probes of ||A^{-1} v||_1 / ||v||_1
+// (transform.cpp:95-109: e_0, e_{dim/2}, e_{dim-1}, then five coin-flip vectors
+// drawn from mt19937(12345) in the same order, real part first in source order).
+template <class Solve>
+double probe_inverse_norm(int64_t dim, Solve&& solve) {
+    double inv_norm = 0.0;
+    bool finite = true;
+    auto take = [&](double v) {
+        if (!std::isfinite(v)) finite = false;
+        inv_norm = std::max(inv_norm, v);
+    };
+    for (int64_t j : {int64_t{0}, dim / 2, dim - 1}) {
+        std::vector<cd> e(static_cast<size_t>(dim), cd{0, 0});
+        e[static_cast<size_t>(j)] = 1.0;
+        take(l1(solve(e)));
+    }
+    std::mt19937 rng(12345);
+    std::uniform_int_distribution<int> coin(0, 1);
+    for (int probe = 0; probe < 5; ++probe) {
+        std::vector<cd> v(static_cast<size_t>(dim));
+        for (int64_t i = 0; i < dim; ++i) v[static_cast<size_t>(i)] = cd(coin(rng) ? 1.0 : -1.0, coin(rng) ? 1.0 : -1.0);
+        take(l1(solve(v)) / l1(v));
+    }
+    return finite ? inv_norm : INFINITY;
+}
+
+// ||D_n(p)||_1 on the host: column kappa of D is sum_{a in O(kappa)} S[a, kappa]
+// e^{2 pi i a.x/n}; the exponent index (a.x mod n) advances incrementally.
+double colnorm_host(int n, const OrbitBlocks& ob) {
+    const Orbits& orb = *ob.orb;
+    const int64_t N = cube(n);
+    std::vector<cd> tw(static_cast<size_t>(n));
+    for (int k = 0; k < n; ++k) {
+        const cld t = unit_phase_ld(static_cast<long double>(k) / n);
+        tw[k] = cd(static_cast<double>(t.real()), static_cast<double>(t.imag()));
+    }
+    const int nth = N >= 4096 ? std::max(1u, std::min(32u, std::thread::hardware_concurrency())) : 1;
+    std::vector<double> best(nth, 0.0);
+    auto work = [&](int th) {
+        std::vector<cd> c;
+        std::vector<Index3> a;
+        std::vector<int> i0, i1, i2;
+        for (int64_t kap = th; kap < N; kap += nth) {
+            const int O = orb.orbit_of[kap], pk = orb.pos[kap];
+            const auto& mem = orb.members[O];
+            const int d = static_cast<int>(mem.size());
+            c.resize(d);
+            a.resize(d);
+            i0.resize(d);
+            i1.resize(d);
+            i2.resize(d);
+            for (int i = 0; i < d; ++i) {
+                const cld v = ob.S[O][static_cast<size_t>(i) * d + pk];
+                c[i] = cd(static_cast<double>(v.real()), static_cast<double>(v.imag()));
+                a[i] = unlex(mem[i], n);
+            }
+            double sum = 0.0;
+            for (int x0 = 0; x0 < n; ++x0) {
+                for (int i = 0; i < d; ++i) i0[i] = (a[i][0] * x0) % n;
+                for (int x1 = 0; x1 < n; ++x1) {
+                    for (int i = 0; i < d; ++i) i1[i] = (i0[i] + a[i][1] * x1) % n, i2[i] = i1[i];
+                    for (int x2 = 0; x2 < n; ++x2) {
+                        cd acc{0, 0};
+                        for (int i = 0; i < d; ++i) {
+                            acc += c[i] * tw[i2[i]];
+                            i2[i] += a[i][2];
+                            if (i2[i] >= n) i2[i] -= n;
+                        }
+                        sum += std::abs(acc);
+                    }
+                }
+            }
+            best[th] = std::max(best[th], sum);
+        }
+    };
+    if (nth == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (int th = 0; th < nth; ++th) pool.emplace_back(work, th);
+        for (auto& t : pool) t.join();
+    }
+    return *std::max_element(best.begin(), best.end());
+}
+}  // namespace
+
+void set_colnorm_hook(ColNormHook hook) { g_colnorm_hook = hook; }
+
+double reference_condition_dense(const std::vector<cld>& A, const std::vector<cld>& Ainv, int64_t dim) {
+    long double norm_a = 0;
+    for (int64_t j = 0; j < dim; ++j) {
+        long double s = 0;
+        for (int64_t i = 0; i < dim; ++i) s += std::abs(A[i * dim + j]);
+        norm_a = std::max(norm_a, s);
+    }
+    for (const cld& v : Ainv)
+        if (!std::isfinite(static_cast<double>(v.real())) || !std::isfinite(static_cast<double>(v.imag())))
+            return INFINITY;
+    const double inv = probe_inverse_norm(dim, [&](const std::vector<cd>& v) {
+        std::vector<cd> x(static_cast<size_t>(dim));
+        for (int64_t i = 0; i < dim; ++i) {
+            cld acc{0, 0};
+            for (int64_t j = 0; j < dim; ++j) acc += Ainv[i * dim + j] * cld(v[j].real(), v[j].imag());
+            x[i] = cd(static_cast<double>(acc.real()), static_cast<double>(acc.imag()));
+        }
+        return x;
+    });
+    return static_cast<double>(norm_a) * inv;
+}
+
+double reference_condition(int n, const Params& p) {
+    const OrbitBlocks ob = orbit_blocks(n, p);
+    if (!std::isfinite(ob.worst_condition)) return INFINITY;  // a singular orbit block: D is singular
+    const Orbits& orb = *ob.orb;
+    const int64_t N = cube(n);
+    double norm_a = -1.0;
+    if (N >= 4096 && g_colnorm_hook) norm_a = g_colnorm_hook(n, p);
+    if (norm_a < 0) norm_a = colnorm_host(n, ob);
+    // D^{-1} v = S^{-1} F^{-1} v: F^{-1} as three axis DFTs (e^{-2 pi i k/n} / n each)
+    std::vector<cd> tw(static_cast<size_t>(n));
+    for (int k = 0; k < n; ++k) {
+        const cld t = unit_phase_ld(-static_cast<long double>(k) / n);
+        tw[k] = cd(static_cast<double>(t.real()), static_cast<double>(t.imag())) / static_cast<double>(n);
+    }
+    const double inv = probe_inverse_norm(N, [&](const std::vector<cd>& v) {
+        std::vector<cd> u(v), t(static_cast<size_t>(N));
+        const int64_t strides[3] = {static_cast<int64_t>(n) * n, n, 1};
+        for (int ax = 0; ax < 3; ++ax) {
+            const int64_t st = strides[ax];
+            for (int64_t base = 0; base < N; ++base) {
+                if ((base / st) % n != 0) continue;  // one line per base with coordinate 0 on this axis
+                for (int a = 0; a < n; ++a) {
+                    cd acc{0, 0};
+                    for (int r = 0; r < n; ++r) acc += tw[(static_cast<int64_t>(a) * r) % n] * u[base + r * st];
+                    t[base + a * st] = acc;
+                }
+            }
+            u.swap(t);
+        }
+        std::vector<cd> x(static_cast<size_t>(N));
+        for (int64_t k = 0; k < N; ++k) {
+            const int O = orb.orbit_of[k], pk = orb.pos[k];
+            const auto& mem = orb.members[O];
+            const int d = static_cast<int>(mem.size());
+            cd acc{0, 0};
+            for (int i = 0; i < d; ++i) {
+                const cld s = ob.Sinv[O][static_cast<size_t>(pk) * d + i];
+                acc += cd(static_cast<double>(s.real()), static_cast<double>(s.imag())) * u[mem[i]];
+            }
+            x[k] = acc;
+        }
+        return x;
+    });
+    return norm_a * inv;
 }
 
 cld dense_entry(int n, const Params& p, const Index3& node, const Index3& kappa) {
@@ -519,17 +688,8 @@ std::shared_ptr<const PlanNode> make_node(int n, const Params& p, bool check) {
                 node->Dinv[k * n3 + r] = acc / static_cast<long double>(n3);
             }
         }
-        long double na = 0, ni = 0;
-        for (int64_t c = 0; c < n3; ++c) {
-            long double sa = 0, si = 0;
-            for (int64_t r = 0; r < n3; ++r) {
-                sa += std::abs(node->D[r * n3 + c]);
-                si += std::abs(node->Dinv[r * n3 + c]);
-            }
-            na = std::max(na, sa);
-            ni = std::max(ni, si);
-        }
-        node->condition = static_cast<double>(na * ni);
+        // assemble_direct gates on condition_with_lu(D) (transform.cpp:339-344)
+        node->condition = reference_condition_dense(node->D, node->Dinv, n3);
         require_condition(node->condition, "dense transform (n=" + std::to_string(n) + ")");
         return node;
     }
@@ -572,20 +732,33 @@ std::shared_ptr<const PlanNode> build_radix_node(int n, const Params& p,
     for (int blk = 0; blk < 8; ++blk)
         for (int g = 0; g < 8; ++g)
             K[blk * 8 + g] = dense_entry(2, p, unlex(blk, 2), unlex(g, 2));
-    const double kc = invert_ld(K, 8, Kinv);
+    invert_ld(K, 8, Kinv);
+    const double kc = reference_condition_dense(K, Kinv, 8);  // condition_estimate_1norm(K), transform.cpp:224-227
     require_condition(kc, "radix kernel");
     for (int i = 0; i < 64; ++i) {
         node->K[i] = snap(K[i]);
         node->Kinv[i] = snap(Kinv[i]);
     }
-    const OrbitBlocks Sn = orbit_blocks(n, p);
-    require_condition(Sn.worst_condition, "orbit block (n=" + std::to_string(n) + ")");
-    std::array<OrbitBlocks, 8> Sm;
-    for (int blk = 0; blk < 8; ++blk) {
-        Sm[blk] = orbit_blocks(m, children[blk]->p);
-        require_condition(Sm[blk].worst_condition, "child block " + std::to_string(blk));
+    // derive_basis gates every child's dense transform on condition_with_lu
+    // (transform.cpp:210-221); the parent D_n itself is not gated there, only its
+    // basis factor's invertibility (assemble_radix, transform.cpp:376-378), which
+    // fails exactly when an orbit block of S_n is singular.
+    std::array<double, 8> cc{};
+    if (m >= 16) {  // the column norms run on the GPU hook or on all host threads
+        for (int blk = 0; blk < 8; ++blk) cc[blk] = reference_condition(m, children[blk]->p);
+    } else {
+        std::array<std::future<double>, 8> fut;
+        for (int blk = 0; blk < 8; ++blk)
+            fut[blk] = std::async(std::launch::async, [&, blk] { return reference_condition(m, children[blk]->p); });
+        for (int blk = 0; blk < 8; ++blk) cc[blk] = fut[blk].get();
     }
-    node->condition = std::max(kc, Sn.worst_condition);
+    for (int blk = 0; blk < 8; ++blk) require_condition(cc[blk], "child block " + std::to_string(blk));
+    const OrbitBlocks Sn = orbit_blocks(n, p);
+    if (!std::isfinite(Sn.worst_condition))
+        throw FcctError(ST_ILL_CONDITIONED, "basis-change factor is not invertible");
+    std::array<OrbitBlocks, 8> Sm;
+    for (int blk = 0; blk < 8; ++blk) Sm[blk] = orbit_blocks(m, children[blk]->p);
+    node->condition = std::max(kc, *std::max_element(cc.begin(), cc.end()));
     node->B = derive_B(n, Sn, Sm, node->Kinv);
     node->Binv = derive_Binv(n, Sn, Sm, node->K);
     return node;

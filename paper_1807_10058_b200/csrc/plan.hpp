@@ -91,6 +91,21 @@ struct OrbitBlocks {
 };
 OrbitBlocks orbit_blocks(int n, const Params& p);
 
+// The reference's condition estimate (condition_with_lu, transform.cpp:91-111):
+// the exact 1-norm of A times the largest ||A^{-1} v||_1 / ||v||_1 over the unit
+// vectors e_0, e_{dim/2}, e_{dim-1} and five mt19937(12345) (+-1 +- i) probes.
+// It is what IllConditioned is raised on (require_condition, transform.cpp:113-117):
+// dense_transform (n^3 <= 512), assemble_direct, every child of derive_basis and
+// the radix kernel. inf when A is singular.
+double reference_condition_dense(const std::vector<cld>& A, const std::vector<cld>& Ainv, int64_t dim);
+// Same estimate for D_n(p) = F_n S_n(p) without forming D: ||D||_1 column by
+// column (each column is <= 24 plane waves), A^{-1} v = S^{-1} F^{-1} v.
+double reference_condition(int n, const Params& p);
+// ||D_n(p)||_1 on a GPU (registered by the C-ABI layer; < 0 = unavailable).
+// Used for n^3 >= 4096, where the host column sums cost seconds.
+using ColNormHook = double (*)(int n, const Params& p);
+void set_colnorm_hook(ColNormHook hook);
+
 // Sparse matrix in CSR (rows), long double values.
 struct SparseLD {
     int64_t dim = 0;

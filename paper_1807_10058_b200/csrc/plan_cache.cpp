@@ -6,6 +6,7 @@
 // the stored B by inverting its connected components, so it is consistent
 // with whatever B the file holds.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <filesystem>
 #include <fstream>
@@ -106,7 +107,7 @@ SparseLD invert_by_components(const SparseLD& B) {
         std::vector<cld> a(static_cast<size_t>(d) * d, cld{0, 0}), inv(static_cast<size_t>(d) * d, cld{0, 0});
         for (int i = 0; i < d; ++i) {
             for (int64_t k = B.rowptr[R[i]]; k < B.rowptr[R[i] + 1]; ++k)
-                a[static_cast<size_t>(i) * d + cpos[B.col[k]]] = B.val[k];
+                a[static_cast<size_t>(i) * d + cpos[B.col[k]]] += B.val[k];  // duplicates sum
             inv[static_cast<size_t>(i) * d + i] = 1;
         }
         for (int k = 0; k < d; ++k) {
@@ -229,9 +230,13 @@ std::shared_ptr<PlanNode> read_body(std::istream& in, const Header& h, const Par
         expect_eof(in);
         nd->radix = false;
         // D^{-1} densely (direct nodes are odd or unit sized and small)
-        const auto Dinv = dense_inverse(nd->D, n3, &nd->condition);
-        nd->Dinv = Dinv;
-        if (!(nd->condition <= 1e12)) throw FcctError(ST_ILL_CONDITIONED, "dense transform: condition exceeds 1e12");
+        double exact = 0;
+        nd->Dinv = dense_inverse(nd->D, n3, &exact);
+        // assemble_direct's gate on condition_with_lu (transform.cpp:339-344)
+        nd->condition = std::isfinite(exact) ? reference_condition_dense(nd->D, nd->Dinv, n3) : exact;
+        if (!(nd->condition <= 1e12))
+            throw FcctError(ST_ILL_CONDITIONED, "dense transform (n=" + std::to_string(h.n) + "): condition estimate " +
+                                                    std::to_string(nd->condition) + " exceeds 1e12");
         return nd;
     }
     for (int i = 0; i < 64; ++i) nd->K[i] = get_complex(in);
@@ -240,6 +245,8 @@ std::shared_ptr<PlanNode> read_body(std::istream& in, const Header& h, const Par
     for (int64_t i = 0; i < n3; ++i) {
         const auto v = get<uint64_t>(in);
         if (v >= static_cast<uint64_t>(n3) || seen[v]) throw Malformed("plan file permutation is not a permutation");
+        // the reference accepts any permutation here; the executors apply the
+        // radix interleave, so another one is treated as a corrupt entry (rebuilt)
         if (v != perm[i]) throw Malformed("plan file permutation is not the radix interleave");
         seen[v] = 1;
     }
@@ -253,6 +260,19 @@ std::shared_ptr<PlanNode> read_body(std::istream& in, const Header& h, const Par
         rows[r].emplace_back(static_cast<int32_t>(c), get_complex(in));
     }
     expect_eof(in);
+    // setFromTriplets sums duplicate (row, col) entries (transform of the file's
+    // triplet list into B, plan_cache.cpp:200-201)
+    for (auto& row : rows) {
+        std::stable_sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        size_t w = 0;
+        for (size_t i = 0; i < row.size(); ++i) {
+            if (w > 0 && row[w - 1].first == row[i].first)
+                row[w - 1].second += row[i].second;
+            else
+                row[w++] = row[i];
+        }
+        row.resize(w);
+    }
     nd->radix = true;
     nd->children = children;
     nd->B.dim = n3;
@@ -268,7 +288,9 @@ std::shared_ptr<PlanNode> read_body(std::istream& in, const Header& h, const Par
     std::vector<cld> K(nd->K.begin(), nd->K.end());
     double kc = 0;
     const auto Kinv = dense_inverse(K, 8, &kc);
-    if (!(kc <= 1e12)) throw FcctError(ST_ILL_CONDITIONED, "radix kernel: condition exceeds 1e12");
+    // assemble_radix: condition_estimate_1norm(kernel) (transform.cpp:366-369)
+    if (std::isfinite(kc)) kc = reference_condition_dense(K, Kinv, 8);
+    if (!(kc <= 1e12)) throw FcctError(ST_ILL_CONDITIONED, "radix kernel: condition estimate " + std::to_string(kc) + " exceeds 1e12");
     std::copy(Kinv.begin(), Kinv.end(), nd->Kinv.begin());
     nd->Binv = invert_by_components(nd->B);
     nd->condition = kc;
@@ -318,8 +340,7 @@ std::shared_ptr<const PlanNode> PlanStore::load_or_build(int n, const Params& p)
                 std::lock_guard<std::mutex> lock(mu_);
                 ++stats_.hits;
                 return node;
-            } catch (const FcctError& e) {
-                if (e.code != ST_IO) throw;
+            } catch (const FcctError& e) {  // every fcct::Error rebuilds (plan_cache.cpp:256-262)
                 std::cerr << "warning: rebuilding plan cache entry " << path << " (" << e.what() << ")\n";
             }
         }

@@ -364,12 +364,23 @@ class TransformPlan:
 # ---------------------------------------------------------------------------
 
 
-def _create(n: int, p: SkewParams, method: int, precision: str, device: int) -> TransformPlan:
+# fcct_executor (include/fcct_gpu.h): executors a FAST plan can be forced onto
+EXECUTORS = {"auto": 0, "orbit": 1, "orbit-phased": 2, "pipeline2": 3, "two-level": 4, "two-level-v2": 5,
+             "tile": 6, "global": 7}
+
+
+def _create(n: int, p: SkewParams, method: int, precision: str, device: int, executor: str = "auto") -> TransformPlan:
     if not isinstance(n, int):
         raise TypeError("n must be an int")
+    if executor not in EXECUTORS:
+        raise ValueError(f"unknown executor {executor!r} (one of {sorted(EXECUTORS)})")
     h = ctypes.c_void_p()
     prec = _capi.F32 if precision == "f32" else _capi.F64
-    _raise(_capi.lib().fcct_plan_create(n, p.r, p.s, p.t, method, prec, device, ctypes.byref(h)))
+    if executor == "auto":
+        _raise(_capi.lib().fcct_plan_create(n, p.r, p.s, p.t, method, prec, device, ctypes.byref(h)))
+    else:
+        _raise(_capi.lib().fcct_plan_create_executor(n, p.r, p.s, p.t, prec, device, EXECUTORS[executor],
+                                                     ctypes.byref(h)))
     return TransformPlan(h.value, precision, device)
 
 
@@ -390,7 +401,9 @@ def dense_transform(n: int, p: SkewParams, precision: str = "f64", device=None) 
     # the C ABI writes column-major; a row-major [N][N] view of it is D^T
     stream = torch.cuda.current_stream(dev).cuda_stream
     _raise(_capi.lib().fcct_dense_matrix(n, p.r, p.s, p.t, mat.data_ptr(), stream))
-    return DenseTransform(n, p, mat.t(), plan.info.condition, plan)
+    # the reference stores its estimate only for n^3 <= 512 (transform.cpp:141-142)
+    cond = plan.info.condition if N <= 512 else float("nan")
+    return DenseTransform(n, p, mat.t(), cond, plan)
 
 
 def naive_apply(t: DenseTransform, s: SignalTensor) -> Spectrum:
@@ -437,13 +450,17 @@ def radix_permutation(n: int) -> np.ndarray:
     return out
 
 
-def build_plan(n: int, p: SkewParams, store=None, precision: str = "f64", device=None) -> TransformPlan:
-    """build_plan (transform.cpp:404-408): radix2 tree for even n, direct otherwise."""
+def build_plan(n: int, p: SkewParams, store=None, precision: str = "f64", device=None,
+               executor: str = "auto") -> TransformPlan:
+    """build_plan (transform.cpp:404-408): radix2 tree for even n, direct otherwise.
+    `executor` (EXECUTORS) forces one of the fast executors; "auto" is the default choice."""
     if n < 1:
         raise ValueError("build_plan: n must be >= 1")
     if store is not None:
         return store.load_or_build(n, p, precision=precision, device=device)
-    return _create(n, p, _capi.FAST, precision, _device_index(device))
+    if executor != "auto" and (n == 1 or n % 2):
+        executor = "auto"  # odd n / n == 1: a direct plan (transform.cpp:385-386)
+    return _create(n, p, _capi.FAST, precision, _device_index(device), executor)
 
 
 @dataclass
@@ -519,6 +536,14 @@ def basis_change(n: int, p: SkewParams, inverse: bool = False) -> SparseMatrix:
         )
     )
     return SparseMatrix(N, N, colptr, rowidx, vals.view(np.complex128))
+
+
+def condition_estimate_1norm(n: int, p: SkewParams) -> float:
+    """condition_estimate_1norm(dense_transform(n, p).matrix) (transform.cpp:91-122):
+    the reference's probe-based estimate, the value IllConditioned is raised on."""
+    out = ctypes.c_double()
+    _raise(_capi.lib().fcct_condition_estimate(n, p.r, p.s, p.t, ctypes.byref(out)))
+    return out.value
 
 
 def plan_tree_stats(n: int, p: SkewParams) -> dict:

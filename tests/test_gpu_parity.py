@@ -311,7 +311,7 @@ def test_large_batch_roundtrip_property(cuda):
 
 
 @pytest.mark.parametrize("n", [32, 64])
-def test_large_n_global_pipeline(cuda, oracle_mod, n, monkeypatch):
+def test_large_n_global_pipeline(cuda, oracle_mod, n):
     # configs[3] (n = 64, single transform): fast path vs the FFT/orbit oracle,
     # plus per-node direct evaluation spot checks (acceptance/main.cpp:368-388)
     # The fp64 floor of the factorization grows ~35x per doubling of n
@@ -319,13 +319,12 @@ def test_large_n_global_pipeline(cuda, oracle_mod, n, monkeypatch):
     # 8.1e-12 / 3.6e-12 at n = 32 and 2.6e-10 / 1.2e-9 at n = 64
     # (tools/large_n_errors.py). The bars below sit just above those floors; the
     # node spot check uses the reference's own bar (acceptance #7: 1e-9).
-    monkeypatch.setenv("FCCT_PIPELINE", "global")
     bar = {32: 5e-11, 64: 5e-9}[n]
     route = oracle_mod.OrbitRoute(n, tup(CANON))
     batch = 2 if n == 32 else 1
     x = rand_batch(n, batch, seed=n)
     y_ref = route.forward(x)
-    plan = build_plan(n, CANON)
+    plan = build_plan(n, CANON, executor="global")
     assert plan.kind() == Kind.radix2
     xt = torch.from_numpy(x).to(cuda)
     y = fast_apply(plan, SignalTensor(n, xt)).values.cpu().numpy()
@@ -341,14 +340,13 @@ def test_large_n_global_pipeline(cuda, oracle_mod, n, monkeypatch):
 
 
 @pytest.mark.parametrize("pipeline", ["global", "v1"])
-def test_alternative_executors_agree(cuda, oracle_mod, pipeline, monkeypatch):
+def test_alternative_executors_agree(cuda, oracle_mod, pipeline):
     # every executor of the fast plan reproduces the oracle (n = 8 and n = 16)
-    monkeypatch.setenv("FCCT_PIPELINE", pipeline)
     for n in (8, 16):
         x = rand_batch(n, 3, seed=3 * n)
         route = oracle_mod.OrbitRoute(n, tup(CANON))
         y_ref = route.forward(x)
-        plan = build_plan(n, CANON)
+        plan = build_plan(n, CANON, executor={"global": "global", "v1": "tile"}[pipeline])
         y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values
         assert rel(y.cpu().numpy(), y_ref) <= F64_TOL
         back = inverse_apply(plan, Spectrum(n, CANON, y)).data.cpu().numpy()
@@ -442,13 +440,12 @@ def test_real_io_fused_matches_complex_path(cuda, oracle_mod, n, method, precisi
 
 
 @pytest.mark.parametrize("p", [SkewParams(0.21, 0.055, 0.4), SkewParams(0.37, 0.61, 0.085)])
-def test_n16_two_level_noncanonical(cuda, oracle_mod, p, monkeypatch):
+def test_n16_two_level_noncanonical(cuda, oracle_mod, p):
     """n = 16 on the two-level executor (root pass + eight n = 8 child
     transforms, fcct_plan_info_t.executor == 4) for non-canonical offsets,
     against the FFT / orbit-route oracle."""
-    monkeypatch.setenv("FCCT_PIPELINE", "two")
     n = 16
-    plan = build_plan(n, p)
+    plan = build_plan(n, p, executor="two-level")
     assert plan.info.executor == 4
     route = oracle_mod.OrbitRoute(n, tup(p))
     x = rand_batch(n, 7, seed=31)  # ragged: 7 blocks, 3 per root-pass CTA pass
@@ -463,10 +460,9 @@ def test_n16_two_level_noncanonical(cuda, oracle_mod, p, monkeypatch):
     assert rel(back, x) <= 2e-11  # measured 5.1e-12 (same floor; the reference's bar is 1e-8)
 
 
-def test_n16_two_level_f32_and_host(cuda, oracle_mod, monkeypatch):
-    monkeypatch.setenv("FCCT_PIPELINE", "two")
+def test_n16_two_level_f32_and_host(cuda, oracle_mod):
     n = 16
-    plan = build_plan(n, CANON, precision="f32")
+    plan = build_plan(n, CANON, precision="f32", executor="two-level")
     assert plan.info.executor == 4
     route = oracle_mod.OrbitRoute(n, tup(CANON))
     x = rand_batch(n, 5, seed=32)
@@ -475,33 +471,31 @@ def test_n16_two_level_f32_and_host(cuda, oracle_mod, monkeypatch):
     back = inverse_apply(plan, Spectrum(n, CANON, y)).data
     assert rel(back.cpu().numpy(), x) <= F32_TOL
     # host buffers through the chunked two-stream path: bitwise the device result
-    p64 = build_plan(n, CANON)
+    p64 = build_plan(n, CANON, executor="two-level")
     xd = torch.from_numpy(x).to(cuda)
     assert torch.equal(p64.apply_values(xd).cpu(), p64.apply_values(xd.cpu()))
 
 
 @pytest.mark.parametrize("pipeline", ["orbit", "orbit-phased", "v2"])
 @pytest.mark.parametrize("n", [4, 8])
-def test_orbit_fft_and_stage_executors(cuda, oracle_mod, pipeline, n, monkeypatch):
+def test_orbit_fft_and_stage_executors(cuda, oracle_mod, pipeline, n):
     """The orbit-FFT executor (the radix tree telescoped to S_n(p) + radix-2 FFT,
     executor 5, default for n = 4, 8) and the stage-by-stage DMMA pipeline
     (executor 2) both reproduce the dense oracle: fp64 (<= 1e-12), fp32 I/O
     (<= 1e-5), fused real-sample I/O bitwise equal to the complex path, on a
     ragged batch, canonical and non-dyadic offsets."""
-    monkeypatch.setenv("FCCT_PIPELINE", pipeline.split("-")[0])
-    monkeypatch.setenv("FCCT_OFFT_WS", "0" if pipeline == "orbit-phased" else "1")
     want = 5 if pipeline.startswith("orbit") else 2
     for p in (CANON, SkewParams(0.21, 0.055, 0.4)):
         x = rand_batch(n, 45, seed=7 * n)
         y_ref = oracle_mod.forward_dense(n, tup(p), x)
         x_ref = oracle_mod.inverse_dense(n, tup(p), y_ref)
-        plan = build_plan(n, p)
+        plan = build_plan(n, p, executor={"orbit": "orbit", "orbit-phased": "orbit-phased", "v2": "pipeline2"}[pipeline])
         assert plan.info.executor == want
         y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values
         assert rel(y.cpu().numpy(), y_ref) <= F64_TOL
         xb = inverse_apply(plan, Spectrum(n, p, torch.from_numpy(y_ref).to(cuda))).data
         assert rel(xb.cpu().numpy(), x_ref) <= F64_TOL
-        p32 = build_plan(n, p, precision="f32")
+        p32 = build_plan(n, p, precision="f32", executor={"orbit": "orbit", "orbit-phased": "orbit-phased", "v2": "pipeline2"}[pipeline])
         assert p32.info.executor == want
         y32 = fast_apply(p32, SignalTensor(n, torch.from_numpy(x).to(torch.complex64).to(cuda))).values
         assert rel(y32.cpu().numpy(), y_ref) <= F32_TOL
