@@ -34,6 +34,9 @@ BLOCKS_PER_GPU = 65536
 METRIC = "FCC-DCT transforms/s and points/s (fp64) vs HBM/FP64-TC roofline, 1–8 GPU"
 FP64_PEAK_TFLOPS = 37.17  # measured DMMA peak on this pool's B200 (profiles/r01_fp_peaks.txt)
 FP32_PEAK_TFLOPS = 72.4  # measured FFMA peak (profiles/r01_fp_peaks.txt)
+# dense TF32 tensor-core peak: the fallback B200_PROFILING.md states (MEASURED_PEAKS.json
+# has no TF32 figure; its measured bf16 burst / 2 = 805 TF/s is reported beside it)
+TF32_PEAK_TFLOPS = 1100.0
 
 
 def measured_peaks():
@@ -652,7 +655,8 @@ def b200_arm(args):
     # the roofline of the pipe that executes the plan: the FP64 tensor pipe for
     # the DMMA executors (fp32 plans there keep fp64 arithmetic, complex64 I/O)
     on_fp64_pipe = (not f32) or info.executor in (2, 4, 5, 6, 7)
-    peak_tf = FP64_PEAK_TFLOPS if on_fp64_pipe else FP32_PEAK_TFLOPS
+    on_tcgen05 = info.executor == 8
+    peak_tf = TF32_PEAK_TFLOPS if on_tcgen05 else (FP64_PEAK_TFLOPS if on_fp64_pipe else FP32_PEAK_TFLOPS)
     exec_flops = (info.exec_flops_forward or info.flops_forward) * blocks
     achieved_tf = exec_flops / (fwd_ms / 1e3) / 1e12
     achieved_gbs = bytes_fwd / (fwd_ms / 1e3) / 1e9
@@ -677,8 +681,11 @@ def b200_arm(args):
         "hbm_peak_gbs": hbm,
         "pipe_peak_tflops": peak_tf,
         "t_star_algorithmic_over_t": max(t_hbm, flops_fwd / (peak_tf * 1e12)) / (fwd_ms / 1e3),
-        "peak_source": ("measured DMMA m8n8k4 f64 peak" if on_fp64_pipe else "measured FFMA fp32 peak")
-                       + " (tools/peak_fp.cu, profiles/r01_fp_peaks.txt); HBM: MEASURED_PEAKS.json hbm_gbs (burst)",
+        "peak_source": (("dense TF32 tensor-core peak 1.1 PFLOP/s, the B200_PROFILING.md fallback (no measured TF32 "
+                         "figure; MEASURED_PEAKS.json bf16 burst / 2 = %.0f TF/s)" % (peaks.get("bf16_tflops", 0) / 2))
+                        if on_tcgen05 else
+                        ("measured DMMA m8n8k4 f64 peak" if on_fp64_pipe else "measured FFMA fp32 peak")
+                        + " (tools/peak_fp.cu, profiles/r01_fp_peaks.txt)") + "; HBM: MEASURED_PEAKS.json hbm_gbs (burst)",
         "fwd_ms": fwd_ms,
         "inv_ms": inv_ms,
         "note": ("frac = max(algorithmic bytes / HBM peak, executed flops / pipe peak) / forward launch time: the "
@@ -730,7 +737,8 @@ KERNELS = {0: "gemm_f64_kernel / gemm_f32_kernel (direct)", 1: "pipeline_kernel 
            4: "root pass + 8 x pipeline2_kernel (two-level, FP64 tensor pipe)",
            5: "orbit_fft_ws_kernel (S_n on the FP64 tensor pipe + radix-2 FFT, warp-specialised)",
            6: "orbit16_base_kernel + fft_cube_kernel (two-pass orbit-FFT: S_n on the FP64 tensor pipe, then the n^3 FFT)",
-           7: "orbit_big_s_kernel + line_fft_kernel (large-n orbit-FFT: S_n then three line-FFT passes)"}
+           7: "orbit_big_s_kernel + line_fft_kernel (large-n orbit-FFT: S_n then three line-FFT passes)",
+           8: "gemm_tf32x3_kernel (direct, tcgen05.mma kind::tf32 x3 split, TMEM accumulator, TMA tensor maps)"}
 
 
 def main():

@@ -645,6 +645,8 @@ struct fcct_plan_s {
     // of a call that used it; the next call's stream waits on it (no host sync)
     cudaEvent_t scratch_ev = nullptr;
     std::shared_ptr<DevBuf> Wt_fwd, Wt_inv;
+    std::shared_ptr<DevBuf> Wt_fwd_lo, Wt_inv_lo;  // tcgen05 3xTF32 plans: Wt_* hold the rna_tf32 parts
+    bool tc32 = false;                              // fp32 direct plan on tcgen05 (gemm_tc.cu)
     std::vector<std::shared_ptr<DevBuf>> extra;
     fcct_plan_info_t info{};
     // workspace for host-buffer calls and in-place direct calls
@@ -702,9 +704,24 @@ void build_direct(fcct_plan_s* pl) {
     const int64_t N = cube(n);
     const bool f32 = pl->precision == FCCT_F32;
     const size_t wbytes = static_cast<size_t>(2 * N) * (2 * N) * (f32 ? 4 : 8);
+    // fp32 plans whose real form tiles by 128 run on tcgen05 (3xTF32): the tables
+    // are generated in fp64 and split into (W_hi, W_lo)
+    pl->tc32 = f32 && gemm_tf32x3_supported(static_cast<int>(2 * N), static_cast<int>(2 * N));
+    const size_t count = static_cast<size_t>(2 * N) * (2 * N);
+    std::shared_ptr<DevBuf> w64;
+    if (pl->tc32) w64 = std::make_shared<DevBuf>(count * 8);
     pl->Wt_fwd = std::make_shared<DevBuf>(wbytes);
     pl->Wt_inv = std::make_shared<DevBuf>(wbytes);
-    ck(gen_dense_realform(n, pl->p.r, pl->p.s, pl->p.t, pl->Wt_fwd->ptr, f32, nullptr), "gen_dense_realform");
+    if (pl->tc32) {
+        pl->Wt_fwd_lo = std::make_shared<DevBuf>(wbytes);
+        pl->Wt_inv_lo = std::make_shared<DevBuf>(wbytes);
+        ck(gen_dense_realform(n, pl->p.r, pl->p.s, pl->p.t, w64->ptr, false, nullptr), "gen_dense_realform");
+        ck(split_tf32(static_cast<const double*>(w64->ptr), static_cast<float*>(pl->Wt_fwd->ptr),
+                      static_cast<float*>(pl->Wt_fwd_lo->ptr), static_cast<int64_t>(count), nullptr),
+           "split_tf32");
+    } else {
+        ck(gen_dense_realform(n, pl->p.r, pl->p.s, pl->p.t, pl->Wt_fwd->ptr, f32, nullptr), "gen_dense_realform");
+    }
     // orbit blocks of S_n(p)^{-1} -> device, then D^{-1} generated on the device
     OrbitBlocks ob = orbit_blocks(n, pl->p);
     if (!std::isfinite(ob.worst_condition))
@@ -726,7 +743,14 @@ void build_direct(fcct_plan_s* pl) {
     OrbitDev od{static_cast<const int*>(b1->ptr), static_cast<const int*>(b2->ptr),
                 static_cast<const int*>(b3->ptr), static_cast<const int*>(b4->ptr),
                 static_cast<const int*>(b5->ptr), static_cast<const double*>(b6->ptr)};
-    ck(gen_dense_inv_realform(n, od, pl->Wt_inv->ptr, f32, nullptr), "gen_dense_inv_realform");
+    if (pl->tc32) {
+        ck(gen_dense_inv_realform(n, od, w64->ptr, false, nullptr), "gen_dense_inv_realform");
+        ck(split_tf32(static_cast<const double*>(w64->ptr), static_cast<float*>(pl->Wt_inv->ptr),
+                      static_cast<float*>(pl->Wt_inv_lo->ptr), static_cast<int64_t>(count), nullptr),
+           "split_tf32");
+    } else {
+        ck(gen_dense_inv_realform(n, od, pl->Wt_inv->ptr, f32, nullptr), "gen_dense_inv_realform");
+    }
     ck(cudaDeviceSynchronize(), "direct table generation");
     // the reference's estimate and gate (assemble_direct: condition_with_lu(D),
     // transform.cpp:339-344; dense_transform stores it for n^3 <= 512, :141-142)
@@ -734,7 +758,7 @@ void build_direct(fcct_plan_s* pl) {
     if (!(pl->info.condition <= 1e12))
         throw FcctError(ST_ILL_CONDITIONED, "dense transform (n=" + std::to_string(n) + "): condition estimate " +
                                                 std::to_string(pl->info.condition) + " exceeds 1e12");
-    pl->info.table_bytes = static_cast<int64_t>(2 * wbytes);
+    pl->info.table_bytes = static_cast<int64_t>((pl->tc32 ? 4 : 2) * wbytes);
 }
 
 void build_v2(fcct_plan_s* pl) {
@@ -1102,7 +1126,7 @@ void fill_info(fcct_plan_s* pl) {
     in.method = pl->radix ? FCCT_FAST : FCCT_DIRECT;
     in.precision = pl->precision;
     in.points = cube(pl->n);
-    in.executor = !pl->radix ? 0
+    in.executor = !pl->radix ? (pl->tc32 ? 8 : 0)
                              : (pl->offt ? 5
                                 : (pl->o16 ? 6
                                 : (pl->obig ? 7 : (pl->v2 ? 2 : (pl->two_level ? 4 : (pl->global ? 3 : 1))))));
@@ -1152,6 +1176,8 @@ void fill_info(fcct_plan_s* pl) {
     } else {
         in.levels = 0;
         in.flops_forward = in.flops_inverse = 8.0 * N * N;
+        // 3xTF32 on tcgen05: three tensor-core products per algorithmic one
+        if (pl->tc32) in.exec_flops_forward = in.exec_flops_inverse = 3.0 * 8.0 * N * N;
     }
 }
 
@@ -1271,7 +1297,13 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
         tmp = std::make_shared<DevBuf>(static_cast<size_t>(batch * N * elem_bytes(pl)));
         dst = tmp->ptr;
     }
-    if (f32)
+    if (pl->tc32)
+        ck(launch_gemm_tf32x3(static_cast<const float*>(in), static_cast<const float*>(W),
+                              static_cast<const float*>(inverse ? pl->Wt_inv_lo->ptr : pl->Wt_fwd_lo->ptr),
+                              static_cast<float*>(dst), batch, static_cast<int>(2 * N), static_cast<int>(2 * N),
+                              pl->num_sms, st),
+           "direct gemm tf32x3 (tcgen05)");
+    else if (f32)
         ck(launch_gemm_f32(static_cast<const float*>(in), static_cast<const float*>(W), static_cast<float*>(dst),
                            batch, static_cast<int>(2 * N), static_cast<int>(2 * N), st),
            "direct gemm f32");

@@ -1,0 +1,368 @@
+// fp32 direct transform on the 5th-generation tensor cores (tcgen05, sm_100a).
+//
+// naive_apply / inverse_apply(dense) (transform.cpp:146-169) for an fp32 plan is
+// the real-form GEMM  C[M][Nn] = A[M][K] . W[Nn][K]^T  (A = the batch of blocks,
+// complex64 interleaved, K = Nn = 2 n^3; W = D or D^{-1} in real form, both
+// K-major). TF32 alone carries 11 significant bits, short of the 1e-5 fp32 bar,
+// so the product runs split (3xTF32):
+//     A.W ~= A_hi.W_hi + A_hi.W_lo + A_lo.W_hi,   x_hi = rna_tf32(x), x_lo = x - x_hi
+// with W_hi / W_lo split from the fp64 table at plan time and A split in shared
+// memory as each stage lands. All three products accumulate into one fp32
+// accumulator in tensor memory.
+//
+// Persistent kernel, one CTA per SM, warp-specialised (320 threads):
+//   warp 0      TMA producer: A, W_hi, W_lo tiles (BK = 32 fp32 = one 128-byte
+//               swizzle row) into a 3-stage ring, mbarrier complete_tx
+//   warp 1      MMA issuer (one thread): 3 x 4 tcgen05.mma.kind::tf32 per stage,
+//               M = 128, N = 128, K = 8; TMEM (512 columns): two hi.hi chunk
+//               accumulators (ping-pong every K = 128) and two tile accumulators
+//               for the hi.lo + lo.hi corrections; tcgen05.commit frees the stage
+//               and hands finished accumulators to the epilogue
+//   warps 2-9   epilogue: every K = 128 the hi.hi chunk accumulator is read with
+//               tcgen05.ld 32x32b.x32 and added into fp32 registers (one row,
+//               64 columns per thread); the tile's hi.lo + lo.hi accumulator is
+//               added last, then fp32 stores
+//   warps 10-13 converter: A stage -> (A_hi in place, A_lo), fence.proxy.async
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "device.cuh"
+#include "kernels.hpp"
+
+namespace fcct {
+
+using namespace dev;
+
+namespace {
+
+constexpr int kBM = 128, kBN = 128, kBK = 32, kStages = 3;
+constexpr int kTileA = kBM * kBK * 4;                   // 16 KB
+constexpr int kTileB = kBN * kBK * 4;                   // 16 KB
+constexpr int kStageBytes = 2 * kTileA + 2 * kTileB;    // A_hi (landed raw), A_lo, W_hi, W_lo
+constexpr int kTxBytes = kTileA + 2 * kTileB;           // what TMA brings per stage
+constexpr int kTmemCols = 4 * kBN;                      // 2 main chunk + 2 correction fp32 accumulators
+// the hi.hi chain is promoted to fp32 registers every kChunkKb k-blocks (K = 128):
+// the tensor core's accumulator alignment rounding grows with the chain length
+// (forward error 2.8e-6 at K = 1024 with one chain, ~K-linear)
+constexpr int kChunkKb = 4;
+constexpr int kEpiThreads = 256, kConvThreads = 128;
+constexpr int kThreads = 64 + kEpiThreads + kConvThreads;  // producer, MMA, 8 epilogue, 4 converter warps
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /* barriers */ + 1024 /* alignment */;
+
+// smem matrix descriptor, K-major, 128-byte swizzle (8-row atoms of 1024 bytes)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16)  // LBO (unused for swizzled K-major)
+           | (static_cast<uint64_t>(1024 >> 4) << 32)                     // SBO: 8-row group stride
+           | (1ull << 46)                                                 // descriptor version (sm_100)
+           | (2ull << 61);                                                // SWIZZLE_128B
+}
+
+// instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
+                            (static_cast<uint32_t>(kBM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+    return r;
+}
+
+#define TMEM_LD_32(taddr, v)                                                                                      \
+    asm volatile(                                                                                                 \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"  \
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"                                     \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),        \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),  \
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),             \
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),             \
+          "=r"(v[30]), "=r"(v[31])                                                                                \
+        : "r"(taddr))
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmWhi,
+                       const __grid_constant__ CUtensorMap tmWlo, float* __restrict__ C, int64_t M, int Nn, int K) {
+    extern __shared__ uint8_t smem_raw[];
+    // 1024-byte alignment for the 128-byte swizzle atoms
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* conv = full + kStages;      // converter -> MMA: A_hi / A_lo written
+    uint64_t* empty = conv + kStages;     // MMA -> producer: stage read
+    uint64_t* cfull = empty + kStages;    // MMA -> epilogue: a main chunk accumulator is complete
+    uint64_t* cempty = cfull + 2;         // epilogue -> MMA: chunk accumulator drained
+    uint64_t* rfull = cempty + 2;         // MMA -> epilogue: the tile's correction accumulator
+    uint64_t* rempty = rfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_tiles = Nn / kBN;
+    const int64_t m_tiles = (M + kBM - 1) / kBM;
+    const int64_t tiles = m_tiles * n_tiles;
+    const int kblocks = K / kBK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&conv[s], kConvThreads);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&cfull[a], 1);
+            mbar_init(&cempty[a], kEpiThreads);
+            mbar_init(&rfull[a], 1);
+            mbar_init(&rempty[a], kEpiThreads);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {  // TMEM, owned (and freed) by this warp
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmWhi)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmWlo)) : "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    // TMEM columns: [0, 2 BN) two main chunk accumulators, [2 BN, 4 BN) two tile correction accumulators
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = static_cast<int>((t / n_tiles) * kBM), n0 = static_cast<int>((t % n_tiles) * kBN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    uint8_t* st = smem + s * kStageBytes;
+                    mbar_arrive_expect_tx(&full[s], kTxBytes);
+                    tma_load_2d(st, &tmA, kb * kBK, m0, &full[s]);
+                    tma_load_2d(st + 2 * kTileA, &tmWhi, kb * kBK, n0, &full[s]);
+                    tma_load_2d(st + 2 * kTileA + kTileB, &tmWlo, kb * kBK, n0, &full[s]);
+                    if (++s == kStages) s = 0, ph ^= 1u;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            int s = 0, cb = 0, rb = 0;
+            uint32_t ph = 0, cph = 0, rph = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+                mbar_wait(&rempty[rb], rph ^ 1u);  // the epilogue read this correction accumulator
+                const uint32_t dr = tmem_base + static_cast<uint32_t>((2 + rb) * kBN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    const bool chunk_start = kb % kChunkKb == 0;
+                    if (chunk_start) mbar_wait(&cempty[cb], cph ^ 1u);  // the epilogue drained this chunk buffer
+                    mbar_wait(&conv[s], ph);
+                    tc_fence_after();
+                    const uint32_t dm = tmem_base + static_cast<uint32_t>(cb * kBN);
+                    const uint32_t st = smem_u32(smem + s * kStageBytes);
+                    const uint64_t ahi = sw128_desc(st), alo = sw128_desc(st + kTileA);
+                    const uint64_t bhi = sw128_desc(st + 2 * kTileA), blo = sw128_desc(st + 2 * kTileA + kTileB);
+#pragma unroll
+                    for (int k = 0; k < kBK / 8; ++k) {  // K = 8 tf32 = 32 bytes along the swizzled row
+                        const uint64_t dk = static_cast<uint64_t>(k * 2);  // 32 bytes in 16-byte units
+                        mma_tf32(dm, ahi + dk, bhi + dk, !(chunk_start && k == 0));
+                        mma_tf32(dr, ahi + dk, blo + dk, (kb | k) != 0);
+                        mma_tf32(dr, alo + dk, bhi + dk, 1u);
+                    }
+                    mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+                    if (++s == kStages) s = 0, ph ^= 1u;
+                    if (kb % kChunkKb == kChunkKb - 1 || kb == kblocks - 1) {
+                        mma_commit(&cfull[cb]);  // chunk complete: promote to the epilogue's fp32 registers
+                        if (++cb == 2) cb = 0, cph ^= 1u;
+                    }
+                }
+                mma_commit(&rfull[rb]);
+                if (++rb == 2) rb = 0, rph ^= 1u;
+            }
+        }
+    } else if (warp < 2 + kEpiThreads / 32) {  // ---- epilogue: chunk promotion + store
+        const int e = warp - 2;
+        const int quarter = warp & 3;        // TMEM lanes 32*quarter .. +31 belong to this warp
+        const int half = e >> 2;             // columns half*64 .. +63 of the tile
+        int cb = 0, rb = 0;
+        uint32_t cph = 0, rph = 0;
+        const int nchunks = (kblocks + kChunkKb - 1) / kChunkKb;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+            const int64_t row = (t / n_tiles) * kBM + quarter * 32 + lane;
+            const int n0 = static_cast<int>((t % n_tiles) * kBN) + half * 64;
+            const uint32_t lanes = static_cast<uint32_t>(quarter * 32) << 16;
+            float sum[64];
+#pragma unroll
+            for (int j = 0; j < 64; ++j) sum[j] = 0.f;
+            for (int c = 0; c < nchunks; ++c) {
+                mbar_wait(&cfull[cb], cph);
+                tc_fence_after();
+                const uint32_t ta = tmem_base + lanes + cb * kBN + half * 64;
+                uint32_t v[32];
+                TMEM_LD_32(ta, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) sum[j] += __uint_as_float(v[j]);
+                TMEM_LD_32(ta + 32, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) sum[32 + j] += __uint_as_float(v[j]);
+                tc_fence_before();
+                mbar_arrive(&cempty[cb]);
+                if (++cb == 2) cb = 0, cph ^= 1u;
+            }
+            mbar_wait(&rfull[rb], rph);
+            tc_fence_after();
+            {
+                const uint32_t ta = tmem_base + lanes + (2 + rb) * kBN + half * 64;
+                uint32_t v[32];
+                TMEM_LD_32(ta, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) sum[j] += __uint_as_float(v[j]);
+                TMEM_LD_32(ta + 32, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) sum[32 + j] += __uint_as_float(v[j]);
+            }
+            tc_fence_before();
+            mbar_arrive(&rempty[rb]);
+            if (++rb == 2) rb = 0, rph ^= 1u;
+            if (row < M) {
+                float4* dst = reinterpret_cast<float4*>(C + row * Nn + n0);
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    dst[q] = make_float4(sum[4 * q], sum[4 * q + 1], sum[4 * q + 2], sum[4 * q + 3]);
+            }
+        }
+    } else {  // ---- converter: A stage -> A_hi (in place) + A_lo, then hand to the MMA issuer
+        const int ct = threadIdx.x - (2 * 32 + kEpiThreads);  // 0..127
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int kb = 0; kb < kblocks; ++kb) {
+                mbar_wait(&full[s], ph);
+                float4* a = reinterpret_cast<float4*>(smem + s * kStageBytes);
+                float4* lo = reinterpret_cast<float4*>(smem + s * kStageBytes + kTileA);
+#pragma unroll
+                for (int q = 0; q < kTileA / 16 / kConvThreads; ++q) {  // elementwise: the swizzle is irrelevant
+                    const int i = q * kConvThreads + ct;
+                    const float4 x = a[i];
+                    float4 h, l;
+                    h.x = __uint_as_float(to_tf32(x.x));
+                    h.y = __uint_as_float(to_tf32(x.y));
+                    h.z = __uint_as_float(to_tf32(x.z));
+                    h.w = __uint_as_float(to_tf32(x.w));
+                    l.x = __uint_as_float(to_tf32(x.x - h.x));  // rounded, not left to the MMA's truncation
+                    l.y = __uint_as_float(to_tf32(x.y - h.y));
+                    l.z = __uint_as_float(to_tf32(x.z - h.z));
+                    l.w = __uint_as_float(to_tf32(x.w - h.w));
+                    a[i] = h;
+                    lo[i] = l;
+                }
+                fence_proxy_async_smem();  // generic-proxy writes -> tensor-core (async proxy) reads
+                mbar_arrive(&conv[s]);
+                if (++s == kStages) s = 0, ph ^= 1u;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(kTmemCols)
+                     : "memory");
+    }
+}
+
+// W (fp64 real form) -> W_hi = rna_tf32(W), W_lo = W - W_hi (rounded to fp32)
+__global__ void split_tf32_kernel(const double* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo,
+                                  int64_t count) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= count) return;
+    const double v = w[i];
+    const float h = __uint_as_float(to_tf32(static_cast<float>(v)));
+    hi[i] = h;
+    lo[i] = __uint_as_float(to_tf32(static_cast<float>(v - static_cast<double>(h))));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// [rows][cols] fp32 row-major, box = 32 columns (128 bytes) x 128 rows, 128-byte swizzle
+bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 4};
+    const cuuint32_t box[2] = {kBK, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool gemm_tf32x3_supported(int Nn, int K) { return Nn % kBN == 0 && K % kBK == 0 && Nn >= kBN && K >= kBK; }
+
+cudaError_t split_tf32(const double* w, float* hi, float* lo, int64_t count, cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    split_tf32_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, st>>>(w, hi, lo, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_tf32x3(const float* A, const float* Whi, const float* Wlo, float* C, int64_t M, int Nn, int K,
+                               int num_sms, cudaStream_t st) {
+    if (M <= 0) return cudaSuccess;
+    if (!gemm_tf32x3_supported(Nn, K)) return cudaErrorInvalidValue;
+    CUtensorMap ma, mh, ml;
+    if (!make_map(&ma, A, M, K) || !make_map(&mh, Whi, Nn, K) || !make_map(&ml, Wlo, Nn, K))
+        return cudaErrorInvalidValue;
+    int per_sm = 0;
+    cudaError_t e = prepare_launch(reinterpret_cast<const void*>(gemm_tf32x3_kernel), kThreads, kSmemBytes, &per_sm);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int64_t tiles = ((M + kBM - 1) / kBM) * (Nn / kBN);
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(tiles, num_sms));
+    gemm_tf32x3_kernel<<<grid, kThreads, kSmemBytes, st>>>(ma, mh, ml, C, M, Nn, K);
+    return cudaGetLastError();
+}
+
+}  // namespace fcct

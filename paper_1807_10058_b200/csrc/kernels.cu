@@ -18,7 +18,6 @@
 
 namespace fcct {
 
-namespace {
 // Per (device, kernel, dynamic smem) cache of the smem attribute and the
 // occupancy query: both are host round trips that would otherwise cost
 // microseconds on every launch (the latency of single-transform calls).
@@ -57,6 +56,8 @@ cudaError_t prepare_launch(const void* kern, int threads, int smem, int* per_sm)
     if (per_sm) *per_sm = occ;
     return cudaSuccess;
 }
+
+namespace {
 }  // namespace
 
 using namespace dev;

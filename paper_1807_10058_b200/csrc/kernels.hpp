@@ -147,6 +147,19 @@ cudaError_t launch_pipeline(const PipelineDesc& d, bool f32, const void* in, voi
 int pipeline_smem_bytes(const PipelineDesc& d, bool f32);
 
 // Direct transform: out[b][:] = real-form GEMM of in[b][:] with Wt (2N x 2N, [col][k]).
+// Raises the kernel's dynamic shared-memory limit once per (device, kernel) and
+// caches the occupancy (CTAs per SM) for (threads, smem); host round trips that
+// would otherwise cost microseconds per launch.
+cudaError_t prepare_launch(const void* kern, int threads, int smem, int* per_sm);
+
+// fp32 direct GEMM on tcgen05 (gemm_tc.cu): C = A . W^T with W = W_hi + W_lo,
+// 3xTF32 (A split on chip). Needs Nn % 128 == 0 and K % 32 == 0.
+bool gemm_tf32x3_supported(int Nn, int K);
+cudaError_t launch_gemm_tf32x3(const float* A, const float* Whi, const float* Wlo, float* C, int64_t M, int Nn, int K,
+                               int num_sms, cudaStream_t st);
+// fp64 table -> (rna_tf32 part, fp32 remainder)
+cudaError_t split_tf32(const double* w, float* hi, float* lo, int64_t count, cudaStream_t st);
+
 cudaError_t launch_gemm_f64(const double* A, const double* Wt, double* C, int64_t M, int Nn, int K,
                             cudaStream_t stream);
 cudaError_t launch_gemm_f32(const float* A, const float* Wt, float* C, int64_t M, int Nn, int K,

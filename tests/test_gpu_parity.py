@@ -112,6 +112,36 @@ def test_direct_f32(cuda, oracle_mod, n):
     assert rel(back.cpu().numpy(), x) <= F32_TOL
 
 
+@pytest.mark.parametrize("n,batch", [(4, 1), (4, 389), (8, 130), (8, 1000)])
+def test_direct_f32_tcgen05(cuda, oracle_mod, n, batch):
+    """fp32 direct plans run on tcgen05 (executor 8: 3xTF32 split, TMEM accumulator,
+    TMA tensor maps; gemm_tc.cu), ragged batches (partial 128-row tiles, a single
+    block): <= 1e-5 vs the long-double dense oracle, both directions, and in place."""
+    x = rand_batch(n, batch, seed=90 + batch)
+    y_ref = oracle_mod.forward_dense(n, tup(CANON), x)
+    dense = dense_transform(n, CANON, precision="f32")
+    assert dense._plan.info.executor == 8
+    xt = torch.from_numpy(x).to(torch.complex64).to(cuda)
+    y = naive_apply(dense, SignalTensor(n, xt)).values
+    assert rel(y.cpu().numpy(), y_ref) <= F32_TOL
+    back = inverse_apply(dense, Spectrum(n, CANON, y)).data
+    assert rel(back.cpu().numpy(), x) <= F32_TOL
+    # TF32 alone would miss the bar by ~100x: the split must be doing its work
+    assert rel(y.cpu().numpy(), y_ref) <= 2e-6
+
+
+def test_direct_f32_tcgen05_n16(cuda, oracle_mod):
+    """n = 16 (K = Nn = 8192) on tcgen05 against 192 long-double rows of D per block."""
+    n = 16
+    x = rand_batch(n, 37, seed=1616)
+    dense = dense_transform(n, CANON, precision="f32")
+    assert dense._plan.info.executor == 8
+    y = naive_apply(dense, SignalTensor(n, torch.from_numpy(x).to(torch.complex64).to(cuda))).values.cpu().numpy()
+    rows = np.random.default_rng(161).choice(n**3, 192, replace=False)
+    want = oracle_mod.dense_rows(n, tup(CANON), rows, x)
+    assert rel(y[:, rows], want) <= F32_TOL
+
+
 def test_reference_seeds_fast_vs_naive(cuda, oracle_mod):
     # test_transform.cpp:138-151 (seeds 40+n) and acceptance #7 (seeds 700+16n+trial)
     for n in (2, 4, 8):
