@@ -648,7 +648,7 @@ def b200_arm(args):
     # the plan tables streamed once (about half of table_bytes, which counts both
     # directions) — negligible for batched configs, dominant for a single n = 64
     data_bytes = float(N * (in_esize + esize) * blocks)
-    table_bytes_fwd = 0.5 * float(info.table_bytes) if info.executor in (3, 7) else 0.0
+    table_bytes_fwd = float(info.table_bytes_forward) if info.executor in (3, 7) else 0.0
     bytes_fwd = data_bytes + table_bytes_fwd
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6488.0)

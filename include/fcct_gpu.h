@@ -86,6 +86,7 @@ typedef struct {
                                   tiles including their zero padding, plus FFT butterflies); 0 when
                                   equal to the algorithmic count */
     double exec_flops_inverse;
+    int64_t table_bytes_forward; /* device bytes of the forward executor's own tables (fast plans) */
 } fcct_plan_info_t;
 
 /* Last error message on this thread ("" if none). */

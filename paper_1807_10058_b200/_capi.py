@@ -51,6 +51,7 @@ class PlanInfo(ctypes.Structure):
         ("executor", c_int),
         ("exec_flops_forward", c_double),
         ("exec_flops_inverse", c_double),
+        ("table_bytes_forward", c_int64),
     ]
 
 

@@ -231,6 +231,25 @@ void upload_orbit_big(const OrbitBigHost& h, OrbitBigTables& out) {
     d.coef_off = static_cast<const int64_t*>(b4->ptr);
     d.members = static_cast<const int*>(b5->ptr);
     d.coef = static_cast<const double2*>(b6->ptr);
+    if (h.gen) {
+        // (mpack, the per-slot packing, is the host emulation's view; the kernel reads fpack / tail)
+        auto g2 = upload(h.ttab), g3 = upload(h.mtab), g4 = upload(h.grp), g5 = upload(h.fpack), g6 = upload(h.tail),
+             g7 = upload(h.fbase);
+        out.bufs.insert(out.bufs.end(), {g2, g3, g4, g5, g6, g7});
+        d.fbase = static_cast<const double2*>(g7->ptr);
+        d.fpack = static_cast<const uint32_t*>(g5->ptr);
+        d.nfree = static_cast<int>(h.fpack.size() / 24);
+        d.tail = static_cast<const int*>(g6->ptr);
+        d.ntail = static_cast<int>(h.tail.size());
+        d.gen = 1;
+        d.pr = h.pr;
+        d.ps = h.ps;
+        d.pt = h.pt;
+        d.ttab = static_cast<const double2*>(g2->ptr);
+        d.mtab = static_cast<const uint8_t*>(g3->ptr);
+        d.grp = static_cast<const int*>(g4->ptr);
+        d.ncarry = h.ncarry;
+    }
     out.exec_flops = h.exec_flops();
 }
 
@@ -1173,6 +1192,10 @@ void fill_info(fcct_plan_s* pl) {
                 for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         }
         in.table_bytes = bytes;
+        int64_t fwd = 0;
+        for (auto* pt : {&pl->obfwd.bufs, &pl->gfwd.bufs, &pl->o16fwd.bufs, &pl->ofwd.bufs, &pl->fwd2.bufs})
+            for (auto& b : *pt) fwd += static_cast<int64_t>(b->bytes);
+        in.table_bytes_forward = fwd;
     } else {
         in.levels = 0;
         in.flops_forward = in.flops_inverse = 8.0 * N * N;

@@ -60,6 +60,94 @@ __global__ void __launch_bounds__(256, 4) orbit_big_s_kernel(const __grid_consta
     }
 }
 
+// Forward S pass with generated coefficients (OrbitBigDesc::gen): rows of free
+// orbits form S[r][c] = base_r T[t_c][g_r g_c^{-1}] from two small shared-memory
+// tables instead of streaming the 104 MB coefficient stream (n = 64); rows of the
+// few non-free orbits keep their coefficient blocks. Persistent grid-stride rows.
+constexpr int kGenMaxCarry = 64;
+constexpr int kGenOrbits = 10;  // free orbits per CTA: 240 of 256 threads, one row each
+// CTAs after the tail: the members of 10 free orbits are staged in shared
+// memory (x values and their decoded (T row, g) words), then each thread forms
+// its row from shared memory only: y_r = base_r sum_c T[t_c][g_r g_c^-1] x_c.
+// The first CTAs run the non-free orbits' rows on their coefficient blocks.
+__global__ void __launch_bounds__(256, 4) orbit_big_sgen_kernel(const __grid_constant__ OrbitBigDesc d,
+                                                                const double2* __restrict__ x,
+                                                                double2* __restrict__ y, int64_t batch) {
+    __shared__ double2 T[kGenMaxCarry * 24];
+    __shared__ uint8_t Mt[24 * 24];
+    __shared__ double2 xs[kGenOrbits * 24];
+    __shared__ int2 ws[kGenOrbits * 24];  // (T row offset, g) of each member
+    // the non-free orbits' rows (long serial coefficient chains) are scheduled first
+    const int tail_ctas = (d.ntail + 255) / 256;
+    const int tid = threadIdx.x;
+    if (static_cast<int>(blockIdx.x) >= tail_ctas) {
+        const int fb = static_cast<int>(blockIdx.x) - tail_ctas;
+        for (int i = tid; i < d.ncarry * 24; i += blockDim.x) T[i] = d.ttab[i];
+        for (int i = tid; i < 24 * 24; i += blockDim.x) Mt[i] = d.mtab[i];
+        const int orbit = fb * kGenOrbits + tid / 24;
+        const bool live = tid < kGenOrbits * 24 && orbit < d.nfree;
+        const int64_t slot = static_cast<int64_t>(orbit) * 24 + tid % 24;
+        const uint32_t me = live ? __ldg(d.fpack + slot) : 0u;
+        const int nat = static_cast<int>(me & 0x3FFFFu), gr = static_cast<int>((me >> 24) & 31u);
+        double2 base = live ? __ldg(d.fbase + slot) : make_double2(0.0, 0.0);
+        const double br = base.x, bi = base.y;
+        if (live) ws[tid] = make_int2(static_cast<int>((me >> 18) & 63u) * 24, gr);
+        __syncthreads();
+        const int ob = tid - tid % 24;  // first slot of this thread's orbit in the stage
+        pdl_wait();  // x is the previous kernel's output (the tables above overlap its tail)
+        const uint8_t* mrow = Mt + gr * 24;
+        for (int64_t b = 0; b < batch; ++b) {
+            if (b > 0) __syncthreads();  // the previous block's stage is consumed
+            if (live) xs[tid] = __ldg(x + b * d.N + nat);
+            __syncthreads();
+            if (!live) continue;
+            double re = 0.0, im = 0.0;
+#pragma unroll 8
+            for (int c = 0; c < 24; ++c) {
+                const double2 v = xs[ob + c];
+                const int2 w = ws[ob + c];
+                const double2 m = T[w.x + mrow[w.y]];
+                re = fma(m.x, v.x, re);
+                re = fma(-m.y, v.y, re);
+                im = fma(m.x, v.y, im);
+                im = fma(m.y, v.x, im);
+            }
+            y[b * d.N + nat] = make_double2(br * re - bi * im, br * im + bi * re);
+        }
+        return;
+    }
+    // non-free orbits (<= 12 members): their coefficient blocks, all loads in flight
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
+    if (q >= d.ntail) return;
+    const int64_t row = __ldg(d.tail + q);
+    const int o = __ldg(d.row_orbit + row), r = __ldg(d.row_index + row);
+    const int off = __ldg(d.orbit_off + o), s = __ldg(d.orbit_off + o + 1) - off;
+    const double2* __restrict__ cf = d.coef + __ldg(d.coef_off + o) + r;
+    const int* __restrict__ mem = d.members + off;
+    const int out = __ldg(mem + r);
+    int mi[12];
+    double2 mc[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) {
+        mi[c] = c < s ? __ldg(mem + c) : 0;
+        mc[c] = c < s ? __ldg(cf + static_cast<int64_t>(c) * s) : make_double2(0.0, 0.0);
+    }
+    pdl_wait();
+    for (int64_t b = 0; b < batch; ++b) {
+        const double2* xb = x + b * d.N;
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int c = 0; c < 12; ++c) {
+            const double2 v = c < s ? __ldg(xb + mi[c]) : make_double2(0.0, 0.0);
+            re = fma(mc[c].x, v.x, re);
+            re = fma(-mc[c].y, v.y, re);
+            im = fma(mc[c].x, v.y, im);
+            im = fma(mc[c].y, v.x, im);
+        }
+        y[b * d.N + out] = make_double2(re, im);
+    }
+}
+
 constexpr int kLines = 8;  // lines per CTA (neighbours in the contiguous dimension)
 
 // One radix-2 DIF FFT along `axis` for kLines neighbouring lines of n points.
@@ -268,6 +356,12 @@ cudaError_t launch_pdl(void (*kern)(P...), unsigned grid, unsigned block, cudaSt
 cudaError_t launch_orbit_big_s(const OrbitBigDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st) {
     if (batch <= 0) return cudaSuccess;
     const int64_t blocks = (d.rows + 255) / 256;
+    if (d.gen) {
+        if (d.ncarry > kGenMaxCarry) return cudaErrorInvalidValue;
+        const int64_t grid = (d.nfree + kGenOrbits - 1) / kGenOrbits + (d.ntail + 255) / 256;
+        return launch_pdl(orbit_big_sgen_kernel, static_cast<unsigned>(grid), 256, st, d,
+                          static_cast<const double2*>(in), static_cast<double2*>(out), batch);
+    }
     return launch_pdl(orbit_big_s_kernel, static_cast<unsigned>(blocks), 256, st, d, static_cast<const double2*>(in),
                       static_cast<double2*>(out), batch);
 }

@@ -608,26 +608,29 @@ def test_n16_two_pass_orbit_fft(cuda, oracle_mod, p):
     assert rel(b32.cpu().numpy(), x) <= F32_TOL
 
 
-@pytest.mark.parametrize("n", [32, 64])
-def test_large_n_orbit_fft(cuda, oracle_mod, n):
+@pytest.mark.parametrize("n,p", [(32, CANON), (64, CANON), (32, SkewParams(0.21, 0.055, 0.4))])
+def test_large_n_orbit_fft(cuda, oracle_mod, n, p):
     """configs[3] (n = 64, single transform) on the large-n orbit-FFT executor
-    (executor 7: S_n(p) as coalesced orbit-block rows, then three line-FFT
-    passes): the telescoped factorisation has no tree-conditioning floor, so
-    the 1e-12 bar holds where the stage-by-stage tree measures 1e-9."""
-    route = oracle_mod.OrbitRoute(n, tup(CANON))
+    (executor 7: S_n(p) as orbit-block rows — forward coefficients of the free
+    orbits generated from the group structure, inverse blocks streamed — then
+    three line-FFT passes): the telescoped factorisation has no tree-conditioning
+    floor, so the 1e-12 bar holds where the stage-by-stage tree measures 1e-9."""
+    route = oracle_mod.OrbitRoute(n, tup(p))
     batch = 2 if n == 32 else 1
     x = rand_batch(n, batch, seed=n + 1)
     y_ref = route.forward(x)
-    plan = build_plan(n, CANON)
+    plan = build_plan(n, p)
     assert plan.info.executor == 7
+    # the forward streams (almost) no coefficients: only the non-free orbits' blocks
+    assert plan.info.table_bytes_forward < 0.25 * (plan.info.table_bytes - plan.info.table_bytes_forward)
     y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values.cpu().numpy()
     assert rel(y, y_ref) <= F64_TOL
     nodes = np.random.default_rng(777).integers(0, n**3, 8)
-    direct = oracle_mod.symmetrized_rows(n, tup(CANON), nodes, x[0])
+    direct = oracle_mod.symmetrized_rows(n, tup(p), nodes, x[0])
     assert np.abs(y[0, nodes] - direct).max() / np.abs(direct).max() <= 1e-12
-    xb = inverse_apply(plan, Spectrum(n, CANON, torch.from_numpy(y_ref).to(cuda))).data.cpu().numpy()
+    xb = inverse_apply(plan, Spectrum(n, p, torch.from_numpy(y_ref).to(cuda))).data.cpu().numpy()
     assert rel(xb, route.inverse(y_ref)) <= F64_TOL
-    back = inverse_apply(plan, Spectrum(n, CANON, torch.from_numpy(y).to(cuda))).data.cpu().numpy()
+    back = inverse_apply(plan, Spectrum(n, p, torch.from_numpy(y).to(cuda))).data.cpu().numpy()
     assert rel(back, x) <= F64_TOL
 
 
