@@ -73,46 +73,69 @@ constexpr int kGenOrbits = 10;  // free orbits per CTA: 240 of 256 threads, one 
 __global__ void __launch_bounds__(256, 4) orbit_big_sgen_kernel(const __grid_constant__ OrbitBigDesc d,
                                                                 const double2* __restrict__ x,
                                                                 double2* __restrict__ y, int64_t batch) {
-    __shared__ double2 T[kGenMaxCarry * 24];
-    __shared__ uint8_t Mt[24 * 24];
+    __shared__ __align__(16) double2 T[kGenMaxCarry * 24];
+    __shared__ __align__(16) uint8_t Mt[24 * 24];
     __shared__ double2 xs[kGenOrbits * 24];
     __shared__ int2 ws[kGenOrbits * 24];  // (T row offset, g) of each member
-    // the non-free orbits' rows (long serial coefficient chains) are scheduled first
+    // the non-free orbits' rows (long serial coefficient chains) are scheduled first;
+    // the remaining CTAs are persistent over groups of 10 free orbits, so the two
+    // tables are loaded once per CTA (bulk copies, overlapped with the first group's
+    // member words)
     const int tail_ctas = (d.ntail + 255) / 256;
     const int tid = threadIdx.x;
     if (static_cast<int>(blockIdx.x) >= tail_ctas) {
-        const int fb = static_cast<int>(blockIdx.x) - tail_ctas;
-        for (int i = tid; i < d.ncarry * 24; i += blockDim.x) T[i] = d.ttab[i];
-        for (int i = tid; i < 24 * 24; i += blockDim.x) Mt[i] = d.mtab[i];
-        const int orbit = fb * kGenOrbits + tid / 24;
-        const bool live = tid < kGenOrbits * 24 && orbit < d.nfree;
-        const int64_t slot = static_cast<int64_t>(orbit) * 24 + tid % 24;
-        const uint32_t me = live ? __ldg(d.fpack + slot) : 0u;
-        const int nat = static_cast<int>(me & 0x3FFFFu), gr = static_cast<int>((me >> 24) & 31u);
-        double2 base = live ? __ldg(d.fbase + slot) : make_double2(0.0, 0.0);
-        const double br = base.x, bi = base.y;
-        if (live) ws[tid] = make_int2(static_cast<int>((me >> 18) & 63u) * 24, gr);
-        __syncthreads();
+        __shared__ __align__(8) uint64_t tbar;
+        const int nfc = static_cast<int>(gridDim.x) - tail_ctas;  // free-orbit CTAs
+        const int groups = (d.nfree + kGenOrbits - 1) / kGenOrbits;
+        const uint32_t tbytes = static_cast<uint32_t>(d.ncarry) * 24 * 16;
+        if (tid == 0) {
+            mbar_init(&tbar, 1);
+            fence_mbar_init();
+            mbar_arrive_expect_tx(&tbar, tbytes + 24 * 24);
+            tma_load_1d(T, d.ttab, tbytes, &tbar);
+            tma_load_1d(Mt, d.mtab, 24 * 24, &tbar);
+        }
+        __syncthreads();  // the barrier is initialised before anyone waits on it
         const int ob = tid - tid % 24;  // first slot of this thread's orbit in the stage
-        pdl_wait();  // x is the previous kernel's output (the tables above overlap its tail)
-        const uint8_t* mrow = Mt + gr * 24;
-        for (int64_t b = 0; b < batch; ++b) {
-            if (b > 0) __syncthreads();  // the previous block's stage is consumed
-            if (live) xs[tid] = __ldg(x + b * d.N + nat);
-            __syncthreads();
-            if (!live) continue;
-            double re = 0.0, im = 0.0;
-#pragma unroll 8
-            for (int c = 0; c < 24; ++c) {
-                const double2 v = xs[ob + c];
-                const int2 w = ws[ob + c];
-                const double2 m = T[w.x + mrow[w.y]];
-                re = fma(m.x, v.x, re);
-                re = fma(-m.y, v.y, re);
-                im = fma(m.x, v.y, im);
-                im = fma(m.y, v.x, im);
+        bool waited = false;
+        for (int grp = static_cast<int>(blockIdx.x) - tail_ctas; grp < groups; grp += nfc) {
+            const int orbit = grp * kGenOrbits + tid / 24;
+            const bool live = tid < kGenOrbits * 24 && orbit < d.nfree;
+            const int64_t slot = static_cast<int64_t>(orbit) * 24 + tid % 24;
+            const uint32_t me = live ? __ldg(d.fpack + slot) : 0u;
+            const double2 base = live ? __ldg(d.fbase + slot) : make_double2(0.0, 0.0);
+            const int nat = static_cast<int>(me & 0x3FFFFu), gr = static_cast<int>((me >> 24) & 31u);
+            if (!waited) {
+                pdl_wait();  // x is the previous kernel's output
+                mbar_wait(&tbar, 0);
+                waited = true;
+            } else {
+                __syncthreads();  // the previous group's stage is consumed
             }
-            y[b * d.N + nat] = make_double2(br * re - bi * im, br * im + bi * re);
+            if (live) ws[tid] = make_int2(static_cast<int>((me >> 18) & 63u) * 24, gr);
+            const uint8_t* mrow = Mt + gr * 24;
+            for (int64_t b = 0; b < batch; ++b) {
+                if (b > 0) __syncthreads();
+                if (live) xs[tid] = __ldg(x + b * d.N + nat);
+                __syncthreads();
+                if (!live) continue;
+                double re = 0.0, im = 0.0;
+#pragma unroll 8
+                for (int c = 0; c < 24; ++c) {
+                    const double2 v = xs[ob + c];
+                    const int2 w = ws[ob + c];
+                    const double2 m = T[w.x + mrow[w.y]];
+                    re = fma(m.x, v.x, re);
+                    re = fma(-m.y, v.y, re);
+                    im = fma(m.x, v.y, im);
+                    im = fma(m.y, v.x, im);
+                }
+                y[b * d.N + nat] = make_double2(base.x * re - base.y * im, base.x * im + base.y * re);
+            }
+        }
+        if (!waited) {
+            pdl_wait();
+            mbar_wait(&tbar, 0);  // the bulk copies must land before the CTA exits
         }
         return;
     }
@@ -358,7 +381,10 @@ cudaError_t launch_orbit_big_s(const OrbitBigDesc& d, const void* in, void* out,
     const int64_t blocks = (d.rows + 255) / 256;
     if (d.gen) {
         if (d.ncarry > kGenMaxCarry) return cudaErrorInvalidValue;
-        const int64_t grid = (d.nfree + kGenOrbits - 1) / kGenOrbits + (d.ntail + 255) / 256;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t grid = std::min<int64_t>((d.nfree + kGenOrbits - 1) / kGenOrbits, 4LL * sms) + (d.ntail + 255) / 256;
         return launch_pdl(orbit_big_sgen_kernel, static_cast<unsigned>(grid), 256, st, d,
                           static_cast<const double2*>(in), static_cast<double2*>(out), batch);
     }
