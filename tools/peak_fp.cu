@@ -1,6 +1,7 @@
 // Microbenchmark: FP64 DFMA, FP64 DMMA (mma.sync.m8n8k4.f64), FP32 FFMA peaks
 // on B200 (the roofline denominators MEASURED_PEAKS.json does not carry).
 #include <cstdio>
+#include <cstdint>
 #include <cuda_runtime.h>
 
 template <int ILP>
@@ -69,6 +70,27 @@ __global__ void dmma16_kernel(double* out, int iters) {
     if (s == 12345.678) out[threadIdx.x] = s;
 }
 
+template <int ILP>
+__global__ void hmma_tf32_kernel(float* out, int iters) {
+    // mma.sync.m16n8k8 tf32 (legacy warp-level tensor op on sm_100a)
+    uint32_t a0 = __float_as_uint(1.0f + threadIdx.x * 1e-6f), a1 = __float_as_uint(0.5f), a2 = a0, a3 = a1;
+    uint32_t b0 = __float_as_uint(0.999f), b1 = b0;
+    float c[ILP][4];
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) { c[i][0] = i; c[i][1] = -i; c[i][2] = 0; c[i][3] = 1; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < ILP; ++i)
+            asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                         : "+f"(c[i][0]), "+f"(c[i][1]), "+f"(c[i][2]), "+f"(c[i][3])
+                         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
+    float s = 0;
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+    if (s == 12345.678f) out[threadIdx.x] = s;
+}
+
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -115,6 +137,15 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         mflops = 2.0 * 512 * 4 * (double)iters * grid * (threads / 32);
         printf("DMMA m16n8k4 bps=%d: %.2f TFLOP/s\n", blocksPerSM, mflops / ms / 1e9);
+
+        hmma_tf32_kernel<4><<<grid, threads>>>((float*)d, 100);
+        cudaEventRecord(e0);
+        hmma_tf32_kernel<4><<<grid, threads>>>((float*)d, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        mflops = 2.0 * 16 * 8 * 8 * 4 * (double)iters * grid * (threads / 32);
+        printf("HMMA m16n8k8 tf32 bps=%d: %.2f TFLOP/s\n", blocksPerSM, mflops / ms / 1e9);
     }
     cudaError_t err = cudaGetLastError();
     printf("err=%s\n", cudaGetErrorString(err));
