@@ -89,6 +89,37 @@ __device__ __forceinline__ void fft_line(double2 (&v)[NN]) {
 
 __host__ __device__ constexpr int mode_bytes(int m) { return m == OF_C128 ? 16 : (m == OF_R32 ? 4 : 8); }
 
+// fp32 versions for fp32 plans (complex64 FFT tile, FP32 FMA pipe)
+template <int NN, int SIGN>
+__device__ __forceinline__ float2 twiddle_f(float2 d, int e) {
+    if (e == 0) return d;
+    if (4 * e == NN) return SIGN > 0 ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);
+    const float c = static_cast<float>(cos16(e * (16 / NN))), s = SIGN * static_cast<float>(cos16(e * (16 / NN) - 4));
+    return make_float2(fmaf(d.x, c, -d.y * s), fmaf(d.x, s, d.y * c));
+}
+template <int NN, int SIGN>
+__device__ __forceinline__ void fft_line_f(float2 (&v)[NN]) {
+#pragma unroll
+    for (int half = NN / 2; half >= 1; half >>= 1) {
+#pragma unroll
+        for (int st = 0; st < NN; st += 2 * half) {
+#pragma unroll
+            for (int j = 0; j < half; ++j) {
+                const float2 a = v[st + j], b = v[st + j + half];
+                v[st + j] = make_float2(a.x + b.x, a.y + b.y);
+                v[st + j + half] = twiddle_f<NN, SIGN>(make_float2(a.x - b.x, a.y - b.y), j * (NN / (2 * half)));
+            }
+        }
+    }
+    float2 t[NN];
+#pragma unroll
+    for (int q = 0; q < NN; ++q) t[q] = v[bitrev(q, NN)];
+#pragma unroll
+    for (int q = 0; q < NN; ++q) v[q] = t[q];
+}
+
+
+
 template <int M>
 __device__ __forceinline__ void load_elem(const char* row, int pos, double& re, double& im) {
     if constexpr (M == OF_C128) {
@@ -118,6 +149,33 @@ __device__ __forceinline__ void store_elem(char* row, int pos, double re, double
         *reinterpret_cast<double*>(row + pos * 8) = re;
     } else {
         *reinterpret_cast<float*>(row + pos * 4) = static_cast<float>(re);
+    }
+}
+
+template <int M>
+__device__ __forceinline__ void load_elem_f(const char* row, int pos, float& re, float& im) {
+    if constexpr (M == OF_C64) {
+        const float2 v = *reinterpret_cast<const float2*>(row + pos * 8);
+        re = v.x;
+        im = v.y;
+    } else if constexpr (M == OF_R32) {
+        re = *reinterpret_cast<const float*>(row + pos * 4);
+        im = 0.0f;
+    } else {
+        double r, i;
+        load_elem<M>(row, pos, r, i);
+        re = static_cast<float>(r);
+        im = static_cast<float>(i);
+    }
+}
+template <int M>
+__device__ __forceinline__ void store_elem_f(char* row, int pos, float re, float im) {
+    if constexpr (M == OF_C64) {
+        *reinterpret_cast<float2*>(row + pos * 8) = make_float2(re, im);
+    } else if constexpr (M == OF_R32) {
+        *reinterpret_cast<float*>(row + pos * 4) = re;
+    } else {
+        store_elem<M>(row, pos, re, im);
     }
 }
 
@@ -378,12 +436,68 @@ __device__ __forceinline__ void base_change_lean(const double2 (&tab)[TMAX], con
     }
 }
 
+// fp32 plans: the FFT tile is complex64 and the butterflies run on the FP32 FMA
+// pipe (off the FP64 pipe the DMMA base change uses); same lines and layout.
+template <int NN, int SIGN, int TB, int AX, int SRCM, int DSTM>
+__device__ __forceinline__ void fft_pass_group_f(int ft, const char* src, int64_t srow, bool src_nat, char* dst,
+                                                 int64_t drow, bool dst_nat, int nvalid) {
+    constexpr int L = TB * NN * NN;
+    constexpr int P = 2;
+    static_assert(L % (P * kOfFftThreads) == 0, "lines per FFT thread");
+    // lines of blocks >= nvalid are skipped altogether (a ragged or single-block
+    // tile: the c1 latency config transforms 1 of the 64 blocks of an n = 4 tile)
+    const int Lv = nvalid * NN * NN < L ? nvalid * NN * NN : L;
+#pragma unroll 1
+    for (int base = ft; base < Lv; base += P * kOfFftThreads) {
+        float2 v[P][NN];
+        int bb[P], hh[P], ll[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const int line = base + q * kOfFftThreads;
+            bb[q] = line / (NN * NN);
+            const int l = line % (NN * NN);
+            hh[q] = l / NN;
+            ll[q] = l % NN;
+        }
+        auto pos = [&](int q, int x, bool natural) {
+            const int hi = hh[q], lo = ll[q];
+            const int i = AX == 0 ? x : hi, j = AX == 0 ? hi : (AX == 1 ? x : lo), kk = AX == 2 ? x : lo;
+            return (i * NN + j) * NN + (natural ? kk : (kk ^ (j & (NN - 1))));
+        };
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const char* sp = src + bb[q] * srow;
+            const bool ok = !src_nat || bb[q] < nvalid;  // shared-memory sides stay unconditional
+#pragma unroll
+            for (int x = 0; x < NN; ++x) {
+                if (ok)
+                    load_elem_f<SRCM>(sp, pos(q, x, src_nat), v[q][x].x, v[q][x].y);
+                else
+                    v[q][x] = make_float2(0.0f, 0.0f);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < P; ++q) fft_line_f<NN, SIGN>(v[q]);
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            if (dst_nat && bb[q] >= nvalid) continue;
+            char* dp = dst + bb[q] * drow;
+#pragma unroll
+            for (int x = 0; x < NN; ++x) store_elem_f<DSTM>(dp, pos(q, x, dst_nat), v[q][x].x, v[q][x].y);
+        }
+    }
+}
+
 // One FFT pass by the FFT group (128 threads), two lines per step for ILP.
 // Lines of blocks >= nvalid neither load from nor store to a natural
 // (global) side.
-template <int NN, int SIGN, int TB, int AX, int SRCM, int DSTM>
+template <int NN, int SIGN, int TB, int AX, int SRCM, int DSTM, bool F32 = false>
 __device__ __forceinline__ void fft_pass_group(int ft, const char* src, int64_t srow, bool src_nat, char* dst,
                                                int64_t drow, bool dst_nat, int nvalid) {
+    if constexpr (F32) {
+        fft_pass_group_f<NN, SIGN, TB, AX, SRCM, DSTM>(ft, src, srow, src_nat, dst, drow, dst_nat, nvalid);
+        return;
+    }
     constexpr int L = TB * NN * NN;
     constexpr int P = 2;
     static_assert(L % (P * kOfFftThreads) == 0, "lines per FFT thread");
@@ -436,8 +550,12 @@ struct OfWsCfg {
     static constexpr int N = NN * NN * NN;
     static constexpr int G = 512 / N >= 1 ? 512 / N : 1;
     static constexpr int TB = 8 * G;
+    // fp32 plans (complex64 / real f32 I/O): the FFT tile is complex64 and the FFT
+    // runs in fp32; the base change keeps fp64 DMMA arithmetic
+    static constexpr bool F32 = MI == OF_C64 || MI == OF_R32 || MO == OF_C64 || MO == OF_R32;
+    static constexpr int YM = F32 ? OF_C64 : OF_C128;
     static constexpr int XROW = N * mode_bytes(MI) + 4 * mode_bytes(MI);  // forward input rows (see OfCfg)
-    static constexpr int YROW = (N + 4) * 16;
+    static constexpr int YROW = (N + 4) * mode_bytes(YM);
     static constexpr int BUF = ((TB * (XROW > YROW ? XROW : YROW)) + 127) / 128 * 128;
     static constexpr int META = kOfBcWarps * TMAX * 4 * 8;
     static constexpr int SMEM = 128 + META + 3 * BUF;
@@ -508,13 +626,13 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                 const int bi = (3 - j % 3) % 3, bf = (4 - j % 3) % 3;
                 mbar_wait(bar + bi, (j / 3) & 1);
                 if (j > 0) named_sync(7, kOfBcThreads);  // BC(j - 1) has read buffer bf (= in(j - 1))
-                base_change_lean<TMAX, G, MI, OF_C128>(tab, meta_w, nt_w, buf(bi), C::XROW, buf(bf), C::YROW, r, k,
+                base_change_lean<TMAX, G, MI, C::YM>(tab, meta_w, nt_w, buf(bi), C::XROW, buf(bf), C::YROW, r, k,
                                                        nvalid_of(tile));
                 named_arrive(1 + j % 3, kOfWarps * 32);  // tile j's spectrum-side buffer is ready
             } else {
                 named_sync(1 + j % 2, kOfWarps * 32);    // FFT(j) has filled y(j mod 2)
                 char* dst = static_cast<char*>(out) + tile * TB * out_stride;
-                base_change_lean<TMAX, G, OF_C128, MO>(tab, meta_w, nt_w, buf(1 + j % 2), C::YROW, dst, out_stride, r,
+                base_change_lean<TMAX, G, C::YM, MO>(tab, meta_w, nt_w, buf(1 + j % 2), C::YROW, dst, out_stride, r,
                                                        k, nvalid);
                 named_arrive(4 + j % 2, kOfWarps * 32);  // y(j mod 2) may be refilled
             }
@@ -530,11 +648,11 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                 const int bf = (4 - j % 3) % 3;
                 char* Y = buf(bf);
                 named_sync(1 + j % 3, kOfWarps * 32);
-                fft_pass_group<NN, +1, TB, 2, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
+                fft_pass_group<NN, +1, TB, 2, C::YM, C::YM, C::F32>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
                 named_sync(8, kOfFftThreads);
-                fft_pass_group<NN, +1, TB, 1, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
+                fft_pass_group<NN, +1, TB, 1, C::YM, C::YM, C::F32>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
                 named_sync(8, kOfFftThreads);
-                fft_pass_group<NN, +1, TB, 0, OF_C128, MO>(ft, Y, C::YROW, false,
+                fft_pass_group<NN, +1, TB, 0, C::YM, MO, C::F32>(ft, Y, C::YROW, false,
                                                           static_cast<char*>(out) + tile * TB * out_stride,
                                                           out_stride, true, nvalid);
                 named_sync(8, kOfFftThreads);
@@ -551,15 +669,15 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                     prefetch_l2_bulk(static_cast<const char*>(in) + (tile_of(j + 2) * TB + ft) * in_stride, in_row);
                 mbar_wait(bar, j & 1);
                 if (j >= 2) named_sync(4 + j % 2, kOfWarps * 32);  // BC(j - 2) has read y(j mod 2)
-                fft_pass_group<NN, -1, TB, 0, MI, OF_C128>(ft, buf(0), C::XROW, true, Y, C::YROW, false, nvalid);
+                fft_pass_group<NN, -1, TB, 0, MI, C::YM, C::F32>(ft, buf(0), C::XROW, true, Y, C::YROW, false, nvalid);
                 named_sync(8, kOfFftThreads);
                 if (ft == 0 && tile_of(j + 1) < ntiles) {
                     fence_proxy_async_smem();
                     issue_load(0, tile_of(j + 1));
                 }
-                fft_pass_group<NN, -1, TB, 1, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
+                fft_pass_group<NN, -1, TB, 1, C::YM, C::YM, C::F32>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
                 named_sync(8, kOfFftThreads);
-                fft_pass_group<NN, -1, TB, 2, OF_C128, OF_C128>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
+                fft_pass_group<NN, -1, TB, 2, C::YM, C::YM, C::F32>(ft, Y, C::YROW, false, Y, C::YROW, false, nvalid);
                 named_arrive(1 + j % 2, kOfWarps * 32);
             }
         }
