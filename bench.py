@@ -37,6 +37,8 @@ FP32_PEAK_TFLOPS = 72.4  # measured FFMA peak (profiles/r01_fp_peaks.txt)
 # dense TF32 tensor-core peak: the fallback B200_PROFILING.md states (MEASURED_PEAKS.json
 # has no TF32 figure; its measured bf16 burst / 2 = 805 TF/s is reported beside it)
 TF32_PEAK_TFLOPS = 1100.0
+# dense INT8 tensor-core peak, the B200_PROFILING.md fallback (fp8 / int8 4.5 PFLOP/s dense)
+INT8_PEAK_TOPS = 4500.0
 
 
 def measured_peaks():
@@ -137,7 +139,7 @@ def profiled_traffic(cfg_name: str, f32: bool, executor: int):
         return None
 
 
-def launches_per_call(info):
+def launches_per_call(info):  # noqa: C901
     """Kernels one forward / one inverse call launches on each executor
     (fcct_plan_info_t.executor): orbit-FFT 1; two-pass n = 16: base change +
     cube FFT (+ un-permute on the inverse); large n: S pass + 3 line passes;
@@ -153,6 +155,8 @@ def launches_per_call(info):
     if ex == 3:
         k = 2 * info.levels + 1
         return (k, k)
+    if ex == 9:  # input slicing + the int8 GEMM
+        return (2, 2)
     return (1, 1)
 
 
@@ -655,8 +659,9 @@ def b200_arm(args):
     # the roofline of the pipe that executes the plan: the FP64 tensor pipe for
     # the DMMA executors (fp32 plans there keep fp64 arithmetic, complex64 I/O)
     on_fp64_pipe = (not f32) or info.executor in (2, 4, 5, 6, 7)
-    on_tcgen05 = info.executor == 8
-    peak_tf = TF32_PEAK_TFLOPS if on_tcgen05 else (FP64_PEAK_TFLOPS if on_fp64_pipe else FP32_PEAK_TFLOPS)
+    on_tcgen05 = info.executor in (8, 9)
+    peak_tf = (TF32_PEAK_TFLOPS if info.executor == 8 else INT8_PEAK_TOPS) if on_tcgen05 else (
+        FP64_PEAK_TFLOPS if on_fp64_pipe else FP32_PEAK_TFLOPS)
     exec_flops = (info.exec_flops_forward or info.flops_forward) * blocks
     achieved_tf = exec_flops / (fwd_ms / 1e3) / 1e12
     achieved_gbs = bytes_fwd / (fwd_ms / 1e3) / 1e9
@@ -683,7 +688,9 @@ def b200_arm(args):
         "t_star_algorithmic_over_t": max(t_hbm, flops_fwd / (peak_tf * 1e12)) / (fwd_ms / 1e3),
         "peak_source": (("dense TF32 tensor-core peak 1.1 PFLOP/s, the B200_PROFILING.md fallback (no measured TF32 "
                          "figure; MEASURED_PEAKS.json bf16 burst / 2 = %.0f TF/s)" % (peaks.get("bf16_tflops", 0) / 2))
-                        if on_tcgen05 else
+                        if info.executor == 8 else
+                        "dense INT8 tensor-core peak 4.5 POPS, the B200_PROFILING.md fallback (executed = 28 int8 slice "
+                        "products per algorithmic fp64 op; TOPS)" if info.executor == 9 else
                         ("measured DMMA m8n8k4 f64 peak" if on_fp64_pipe else "measured FFMA fp32 peak")
                         + " (tools/peak_fp.cu, profiles/r01_fp_peaks.txt)") + "; HBM: MEASURED_PEAKS.json hbm_gbs (burst)",
         "fwd_ms": fwd_ms,
@@ -738,7 +745,8 @@ KERNELS = {0: "gemm_f64_kernel / gemm_f32_kernel (direct)", 1: "pipeline_kernel 
            5: "orbit_fft_ws_kernel (S_n on the FP64 tensor pipe + radix-2 FFT, warp-specialised)",
            6: "orbit16_base_kernel + fft_cube_kernel (two-pass orbit-FFT: S_n on the FP64 tensor pipe, then the n^3 FFT)",
            7: "orbit_big_s_kernel + line_fft_kernel (large-n orbit-FFT: S_n then three line-FFT passes)",
-           8: "gemm_tf32x3_kernel (direct, tcgen05.mma kind::tf32 x3 split, TMEM accumulator, TMA tensor maps)"}
+           8: "gemm_tf32x3_kernel (direct, tcgen05.mma kind::tf32 x3 split, TMEM accumulator, TMA tensor maps)",
+           9: "ozaki_slice_kernel + gemm_ozaki_kernel (direct fp64, tcgen05.mma kind::i8 on 7 int8 slices, TMEM)"}
 
 
 def main():

@@ -81,7 +81,8 @@ typedef struct {
                                 5 orbit-FFT (the radix tree telescoped to S_n + radix-2 FFT),
                                 6 two-pass orbit-FFT (n = 16: S_n pass + cube FFT pass),
                                 7 large-n orbit-FFT (n = 32, 64: S_n pass + three line-FFT passes),
-                                8 direct GEMM on tcgen05 (fp32 plans, 3xTF32, gemm_tc.cu) */
+                                8 direct GEMM on tcgen05 (fp32 plans, 3xTF32, gemm_tc.cu),
+                                9 direct GEMM on tcgen05 (fp64 plans, Ozaki int8 slices, gemm_tc.cu) */
     double exec_flops_forward; /* flops the executor issues on the FP64 pipes per block (tensor-core
                                   tiles including their zero padding, plus FFT butterflies); 0 when
                                   equal to the algorithmic count */

@@ -666,6 +666,11 @@ struct fcct_plan_s {
     std::shared_ptr<DevBuf> Wt_fwd, Wt_inv;
     std::shared_ptr<DevBuf> Wt_fwd_lo, Wt_inv_lo;  // tcgen05 3xTF32 plans: Wt_* hold the rna_tf32 parts
     bool tc32 = false;                              // fp32 direct plan on tcgen05 (gemm_tc.cu)
+    // fp64 direct plans on tcgen05 (Ozaki int8 slices): W slices + row scales per direction,
+    // and a per-call workspace for the slices of the input batch
+    bool oz64 = false;
+    std::shared_ptr<DevBuf> oz_w[2], oz_ws[2];
+    std::shared_ptr<DevBuf> oz_in, oz_in_scale;
     std::vector<std::shared_ptr<DevBuf>> extra;
     fcct_plan_info_t info{};
     // workspace for host-buffer calls and in-place direct calls
@@ -769,6 +774,20 @@ void build_direct(fcct_plan_s* pl) {
            "split_tf32");
     } else {
         ck(gen_dense_inv_realform(n, od, pl->Wt_inv->ptr, f32, nullptr), "gen_dense_inv_realform");
+    }
+    // fp64 plans whose real form tiles by 64 (n = 4, 8, 16) run on tcgen05 by the
+    // Ozaki scheme: int8 slices of D / D^{-1} (real form, rows = outputs) with row scales
+    pl->oz64 = !f32 && gemm_ozaki_supported(static_cast<int>(2 * N), static_cast<int>(2 * N));
+    if (pl->oz64) {
+        const int K = static_cast<int>(2 * N);
+        for (int dir = 0; dir < 2; ++dir) {
+            pl->oz_w[dir] = std::make_shared<DevBuf>(static_cast<size_t>(ozaki_slices()) * K * K);
+            pl->oz_ws[dir] = std::make_shared<DevBuf>(static_cast<size_t>(K) * 8);
+            ck(ozaki_slice(static_cast<const double*>((dir ? pl->Wt_inv : pl->Wt_fwd)->ptr), K, K,
+                           static_cast<int8_t*>(pl->oz_w[dir]->ptr), static_cast<double*>(pl->oz_ws[dir]->ptr),
+                           nullptr),
+               "ozaki slices");
+        }
     }
     ck(cudaDeviceSynchronize(), "direct table generation");
     // the reference's estimate and gate (assemble_direct: condition_with_lu(D),
@@ -1145,7 +1164,7 @@ void fill_info(fcct_plan_s* pl) {
     in.method = pl->radix ? FCCT_FAST : FCCT_DIRECT;
     in.precision = pl->precision;
     in.points = cube(pl->n);
-    in.executor = !pl->radix ? (pl->tc32 ? 8 : 0)
+    in.executor = !pl->radix ? (pl->tc32 ? 8 : (pl->oz64 ? 9 : 0))
                              : (pl->offt ? 5
                                 : (pl->o16 ? 6
                                 : (pl->obig ? 7 : (pl->v2 ? 2 : (pl->two_level ? 4 : (pl->global ? 3 : 1))))));
@@ -1201,6 +1220,8 @@ void fill_info(fcct_plan_s* pl) {
         in.flops_forward = in.flops_inverse = 8.0 * N * N;
         // 3xTF32 on tcgen05: three tensor-core products per algorithmic one
         if (pl->tc32) in.exec_flops_forward = in.exec_flops_inverse = 3.0 * 8.0 * N * N;
+        // Ozaki: 28 int8 products per algorithmic one (ops, not fp64 flops)
+        if (pl->oz64) in.exec_flops_forward = in.exec_flops_inverse = 28.0 * 8.0 * N * N;
     }
 }
 
@@ -1320,7 +1341,28 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
         tmp = std::make_shared<DevBuf>(static_cast<size_t>(batch * N * elem_bytes(pl)));
         dst = tmp->ptr;
     }
-    if (pl->tc32)
+    if (pl->oz64) {
+        const int K = static_cast<int>(2 * N);
+        // the slice workspace is plan-owned scratch: ordered across streams by the
+        // plan's scratch event like the other executors' scratch
+        std::lock_guard<std::mutex> lock(pl->scratch_mu);
+        const size_t need = static_cast<size_t>(ozaki_slices()) * batch * K;
+        if (!pl->oz_in || pl->oz_in->bytes < need || pl->oz_in_scale->bytes < static_cast<size_t>(batch) * 8) {
+            scratch_retire(pl, st);
+            pl->oz_in = std::make_shared<DevBuf>(need);
+            pl->oz_in_scale = std::make_shared<DevBuf>(static_cast<size_t>(batch) * 8);
+        }
+        scratch_acquire(pl, st);
+        ck(ozaki_slice(static_cast<const double*>(in), batch, K, static_cast<int8_t*>(pl->oz_in->ptr),
+                       static_cast<double*>(pl->oz_in_scale->ptr), st),
+           "ozaki input slices");
+        ck(launch_gemm_ozaki(static_cast<const int8_t*>(pl->oz_in->ptr), static_cast<const double*>(pl->oz_in_scale->ptr),
+                             static_cast<const int8_t*>(pl->oz_w[inverse ? 1 : 0]->ptr),
+                             static_cast<const double*>(pl->oz_ws[inverse ? 1 : 0]->ptr), static_cast<double*>(dst),
+                             batch, K, K, pl->num_sms, st),
+           "direct gemm ozaki (tcgen05 int8)");
+        scratch_release(pl, st);
+    } else if (pl->tc32)
         ck(launch_gemm_tf32x3(static_cast<const float*>(in), static_cast<const float*>(W),
                               static_cast<const float*>(inverse ? pl->Wt_inv_lo->ptr : pl->Wt_fwd_lo->ptr),
                               static_cast<float*>(dst), batch, static_cast<int>(2 * N), static_cast<int>(2 * N),

@@ -302,6 +302,213 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ===========================================================================
+// fp64 direct transform on tcgen05: Ozaki-scheme split into int8 slices.
+//
+// Each row of A (a block) and of W (an output of D or D^{-1}) is scaled by a
+// power of two sigma >= its max |entry| and cut into kOzS int8 slices,
+//     a / sigma = sum_p 2^{-7p} a_p,   |a_p| <= 127   (round to nearest, p = 1..kOzS).
+// Every slice product a_p . w_q is an exact int8 GEMM with int32 accumulation
+// (K 127^2 * pairs < 2^31 up to K = 8192), and
+//     C = sigma_A sigma_W sum_{p+q <= kOzS+1} 2^{-7(p+q)} (a_p . w_q^T).
+// Products of equal p + q share a scale and one TMEM accumulator (kOzS of them,
+// 64 columns each). kOzS = 7 (28 products): forward 4.5e-15, inverse 1.6e-14
+// relative L2 at n = 8 against fp64 (6 slices: 5.5e-13 / 1.9e-12; tools/ozaki_sim.py).
+// ===========================================================================
+constexpr int kOzS = 7;
+constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 32;          // BK = 32 int8 = one 32-byte swizzle row
+constexpr int kOzStages = 4;
+constexpr int kOzTileA = kOzS * kOzBM * kOzBK;             // 28 KB: all slices of the A tile
+constexpr int kOzTileB = kOzS * kOzBN * kOzBK;             // 14 KB
+constexpr int kOzStage = kOzTileA + kOzTileB;
+constexpr int kOzThreads = 64 + 128;                       // producer, MMA issuer, 4 epilogue warps
+constexpr int kOzSmem = kOzStages * kOzStage + 1024 + 1024;
+constexpr int kOzTmemCols = 512;                           // kOzS x 64 = 448 used
+
+// smem descriptor, K-major, 32-byte swizzle (8-row atoms of 256 bytes)
+__device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (static_cast<uint64_t>(256 >> 4) << 32) |
+           (1ull << 46) | (6ull << 61);
+}
+// D s32, A/B signed int8, K-major, M = 128, N = 64
+constexpr uint32_t kOzIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kOzBN >> 3) << 17) |
+                              (static_cast<uint32_t>(kOzBM >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(kOzIdesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// rows of A [rows][K] fp64 -> slices [kOzS][rows][K] int8 and scale[rows] = 2^e >= max |row|.
+// One warp per row.
+__global__ void ozaki_slice_kernel(const double* __restrict__ a, int64_t rows, int K, int8_t* __restrict__ sl,
+                                   double* __restrict__ scale) {
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const double* r = a + row * K;
+    double m = 0.0;
+    for (int k = lane; k < K; k += 32) m = fmax(m, fabs(r[k]));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int e = 0;
+    if (m > 0.0) {
+        frexp(m, &e);                      // m = f 2^e, f in [0.5, 1): 2^e > m
+    }
+    const double inv = ldexp(1.0, -e), sig = ldexp(1.0, e);
+    if (lane == 0) scale[row] = m > 0.0 ? sig : 1.0;
+    const int64_t plane = rows * static_cast<int64_t>(K);
+    for (int k = lane; k < K; k += 32) {
+        double v = m > 0.0 ? r[k] * inv : 0.0;  // exact (power of two)
+#pragma unroll
+        for (int q = 1; q <= kOzS; ++q) {
+            const double sc = ldexp(1.0, 7 * q);
+            double t = rint(v * sc);
+            t = fmin(127.0, fmax(-127.0, t));
+            v -= t / sc;                       // exact: removes the leading part
+            sl[(q - 1) * plane + row * K + k] = static_cast<int8_t>(t);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kOzThreads, 1)
+    gemm_ozaki_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+                      const double* __restrict__ sa, const double* __restrict__ sw, double* __restrict__ C,
+                      int64_t M, int Nn, int K) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzStages * kOzStage);
+    uint64_t* empty = full + kOzStages;
+    uint64_t* tfull = empty + kOzStages;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_tiles = Nn / kOzBN;
+    const int64_t tiles = ((M + kOzBM - 1) / kOzBM) * n_tiles;
+    const int kblocks = K / kOzBK;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kOzStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 128);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kOzTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer: all kOzS slices of A and of W per stage (3-D boxes)
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = static_cast<int>((t / n_tiles) * kOzBM), n0 = static_cast<int>((t % n_tiles) * kOzBN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    uint8_t* st = smem + s * kOzStage;
+                    mbar_arrive_expect_tx(&full[s], kOzStage);
+                    tma_load_3d(st, &tmA, kb * kOzBK, m0, 0, &full[s]);
+                    tma_load_3d(st + kOzTileA, &tmW, kb * kOzBK, n0, 0, &full[s]);
+                    if (++s == kOzStages) s = 0, ph ^= 1u;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            int s = 0;
+            uint32_t ph = 0, tph = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+                mbar_wait(tempty, tph ^ 1u);  // the epilogue drained the accumulators
+                tph ^= 1u;
+                tc_fence_after();
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t st = smem_u32(smem + s * kOzStage);
+#pragma unroll
+                    for (int p = 0; p < kOzS; ++p)
+#pragma unroll
+                        for (int q = 0; q + p < kOzS; ++q) {  // p + q + 2 <= kOzS + 1
+                            const uint64_t a = sw32_desc(st + p * kOzBM * kOzBK);
+                            const uint64_t b = sw32_desc(st + kOzTileA + q * kOzBN * kOzBK);
+                            mma_i8(tmem_base + static_cast<uint32_t>((p + q) * kOzBN), a, b, (kb > 0 || p > 0) ? 1u : 0u);
+                        }
+                    mma_commit(&empty[s]);
+                    if (++s == kOzStages) s = 0, ph ^= 1u;
+                }
+                mma_commit(tfull);
+            }
+        }
+    } else {  // ---- epilogue: C = sigma_A sigma_W sum_d 2^{-7(d+2)} acc_d
+        const int quarter = warp & 3;
+        uint32_t tph = 0;
+        for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+            const int64_t row = (t / n_tiles) * kOzBM + quarter * 32 + lane;
+            const int n0 = static_cast<int>((t % n_tiles) * kOzBN);
+            mbar_wait(tfull, tph);
+            tph ^= 1u;
+            tc_fence_after();
+            const uint32_t tl = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
+            const double ra = row < M ? sa[row] : 0.0;
+#pragma unroll 1
+            for (int h = 0; h < kOzBN / 32; ++h) {
+                double acc[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+#pragma unroll 1
+                for (int d = kOzS - 1; d >= 0; --d) {  // smallest terms first
+                    uint32_t v[32];
+                    TMEM_LD_32(tl + d * kOzBN + h * 32, v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                    const double sc = ldexp(1.0, -7 * (d + 2));
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) acc[j] = fma(static_cast<double>(static_cast<int>(v[j])), sc, acc[j]);
+                }
+                if (row < M) {
+                    double2* dst = reinterpret_cast<double2*>(C + row * Nn + n0 + h * 32);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int c = n0 + h * 32 + 2 * j;
+                        dst[j] = make_double2(acc[2 * j] * ra * __ldg(sw + c), acc[2 * j + 1] * ra * __ldg(sw + c + 1));
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tempty);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(kOzTmemCols)
+                     : "memory");
+    }
+}
+
 // W (fp64 real form) -> W_hi = rna_tf32(W), W_lo = W - W_hi (rounded to fp32)
 __global__ void split_tf32_kernel(const double* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo,
                                   int64_t count) {
@@ -338,7 +545,49 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols) {
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// slices [S][rows][K] int8, box = 32 bytes x brows rows x S slices, 32-byte swizzle
+bool make_slice_map(CUtensorMap* m, const int8_t* base, int64_t rows, int64_t K, int brows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(kOzS)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(K) * static_cast<cuuint64_t>(rows)};
+    const cuuint32_t box[3] = {kOzBK, static_cast<cuuint32_t>(brows), kOzS};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
+
+int ozaki_slices() { return kOzS; }
+
+bool gemm_ozaki_supported(int Nn, int K) { return Nn % kOzBN == 0 && K % kOzBK == 0 && Nn >= kOzBN && K <= 8192; }
+
+cudaError_t ozaki_slice(const double* a, int64_t rows, int K, int8_t* slices, double* scale, cudaStream_t st) {
+    if (rows <= 0) return cudaSuccess;
+    const int64_t threads = rows * 32;
+    ozaki_slice_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(a, rows, K, slices, scale);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_ozaki(const int8_t* a_slices, const double* a_scale, const int8_t* w_slices,
+                              const double* w_scale, double* C, int64_t M, int Nn, int K, int num_sms,
+                              cudaStream_t st) {
+    if (M <= 0) return cudaSuccess;
+    if (!gemm_ozaki_supported(Nn, K)) return cudaErrorInvalidValue;
+    CUtensorMap ma, mw;
+    if (!make_slice_map(&ma, a_slices, M, K, kOzBM) || !make_slice_map(&mw, w_slices, Nn, K, kOzBN))
+        return cudaErrorInvalidValue;
+    int per_sm = 0;
+    cudaError_t e = prepare_launch(reinterpret_cast<const void*>(gemm_ozaki_kernel), kOzThreads, kOzSmem, &per_sm);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int64_t tiles = ((M + kOzBM - 1) / kOzBM) * (Nn / kOzBN);
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(tiles, num_sms));
+    gemm_ozaki_kernel<<<grid, kOzThreads, kOzSmem, st>>>(ma, mw, a_scale, w_scale, C, M, Nn, K);
+    return cudaGetLastError();
+}
 
 bool gemm_tf32x3_supported(int Nn, int K) { return Nn % kBN == 0 && K % kBK == 0 && Nn >= kBN && K >= kBK; }
 

@@ -142,6 +142,25 @@ def test_direct_f32_tcgen05_n16(cuda, oracle_mod):
     assert rel(y[:, rows], want) <= F32_TOL
 
 
+@pytest.mark.parametrize("n,batch", [(4, 1), (4, 300), (8, 130), (8, 1000)])
+def test_direct_f64_tcgen05_ozaki(cuda, oracle_mod, n, batch):
+    """fp64 direct plans run on tcgen05 (executor 9): the Ozaki scheme — 7 int8
+    slices of the block and of D / D^-1 per row, exact int8 products (int32 in
+    TMEM), fp64 epilogue — against the long-double oracle at the fp64 bar, both
+    directions, ragged batches."""
+    x = rand_batch(n, batch, seed=700 + batch)
+    y_ref = oracle_mod.forward_dense(n, tup(CANON), x)
+    dense = dense_transform(n, CANON)
+    assert dense._plan.info.executor == 9
+    xt = torch.from_numpy(x).to(cuda)
+    y = naive_apply(dense, SignalTensor(n, xt)).values
+    assert rel(y.cpu().numpy(), y_ref) <= F64_TOL
+    back = inverse_apply(dense, Spectrum(n, CANON, y)).data
+    assert rel(back.cpu().numpy(), x) <= F64_TOL
+    x_inv = inverse_apply(dense, Spectrum(n, CANON, torch.from_numpy(y_ref).to(cuda))).data.cpu().numpy()
+    assert rel(x_inv, oracle_mod.inverse_dense(n, tup(CANON), y_ref)) <= F64_TOL
+
+
 def test_reference_seeds_fast_vs_naive(cuda, oracle_mod):
     # test_transform.cpp:138-151 (seeds 40+n) and acceptance #7 (seeds 700+16n+trial)
     for n in (2, 4, 8):
