@@ -350,7 +350,8 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 }
 
 // rows of A [rows][K] fp64 -> slices [kOzS][rows][K] int8 and scale[rows] = 2^e >= max |row|.
-// One warp per row.
+// One warp per row; each lane takes 8 consecutive elements per step (two 32-byte
+// loads, one 8-byte store per slice: 256-byte warp stores). K % 8 == 0.
 __global__ void ozaki_slice_kernel(const double* __restrict__ a, int64_t rows, int K, int8_t* __restrict__ sl,
                                    double* __restrict__ scale) {
     const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -358,24 +359,37 @@ __global__ void ozaki_slice_kernel(const double* __restrict__ a, int64_t rows, i
     if (row >= rows) return;
     const double* r = a + row * K;
     double m = 0.0;
-    for (int k = lane; k < K; k += 32) m = fmax(m, fabs(r[k]));
+    for (int k = 8 * lane; k < K; k += 256) {
+        const double4* v = reinterpret_cast<const double4*>(r + k);
+        const double4 x0 = v[0], x1 = v[1];
+        m = fmax(m, fmax(fmax(fabs(x0.x), fabs(x0.y)), fmax(fabs(x0.z), fabs(x0.w))));
+        m = fmax(m, fmax(fmax(fabs(x1.x), fabs(x1.y)), fmax(fabs(x1.z), fabs(x1.w))));
+    }
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     int e = 0;
-    if (m > 0.0) {
-        frexp(m, &e);                      // m = f 2^e, f in [0.5, 1): 2^e > m
-    }
-    const double inv = ldexp(1.0, -e), sig = ldexp(1.0, e);
-    if (lane == 0) scale[row] = m > 0.0 ? sig : 1.0;
+    if (m > 0.0) frexp(m, &e);  // m = f 2^e, f in [0.5, 1): 2^e > m
+    const double inv = m > 0.0 ? ldexp(1.0, -e) : 0.0;
+    if (lane == 0) scale[row] = m > 0.0 ? ldexp(1.0, e) : 1.0;
     const int64_t plane = rows * static_cast<int64_t>(K);
-    for (int k = lane; k < K; k += 32) {
-        double v = m > 0.0 ? r[k] * inv : 0.0;  // exact (power of two)
+    for (int k = 8 * lane; k < K; k += 256) {
+        const double4* v4 = reinterpret_cast<const double4*>(r + k);
+        const double4 x0 = v4[0], x1 = v4[1];
+        double v[8] = {x0.x * inv, x0.y * inv, x0.z * inv, x0.w * inv, x1.x * inv, x1.y * inv, x1.z * inv, x1.w * inv};
 #pragma unroll
         for (int q = 1; q <= kOzS; ++q) {
-            const double sc = ldexp(1.0, 7 * q);
-            double t = rint(v * sc);
-            t = fmin(127.0, fmax(-127.0, t));
-            v -= t / sc;                       // exact: removes the leading part
-            sl[(q - 1) * plane + row * K + k] = static_cast<int8_t>(t);
+            const double sc = ldexp(1.0, 7 * q), isc = ldexp(1.0, -7 * q);
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const double t = fmin(127.0, fmax(-127.0, rint(v[j] * sc)));
+                v[j] = fma(-t, isc, v[j]);  // exact: removes the leading part
+                const uint32_t byte = static_cast<uint32_t>(static_cast<int>(t)) & 0xFFu;
+                if (j < 4)
+                    lo |= byte << (8 * j);
+                else
+                    hi |= byte << (8 * (j - 4));
+            }
+            *reinterpret_cast<uint2*>(sl + (q - 1) * plane + row * K + k) = make_uint2(lo, hi);
         }
     }
 }
@@ -563,6 +577,7 @@ bool make_slice_map(CUtensorMap* m, const int8_t* base, int64_t rows, int64_t K,
 int ozaki_slices() { return kOzS; }
 
 bool gemm_ozaki_supported(int Nn, int K) { return Nn % kOzBN == 0 && K % kOzBK == 0 && Nn >= kOzBN && K <= 8192; }
+// (the slicing kernel also needs K % 8 == 0 and 32-byte aligned rows: K % 32 == 0 holds)
 
 cudaError_t ozaki_slice(const double* a, int64_t rows, int K, int8_t* slices, double* scale, cudaStream_t st) {
     if (rows <= 0) return cudaSuccess;
