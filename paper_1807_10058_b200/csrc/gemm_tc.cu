@@ -311,26 +311,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Every slice product a_p . w_q is an exact int8 GEMM with int32 accumulation
 // (K 127^2 * pairs < 2^31 up to K = 8192), and
 //     C = sigma_A sigma_W sum_{p+q <= kOzS+1} 2^{-7(p+q)} (a_p . w_q^T).
-// Products of equal p + q share a scale and one TMEM accumulator (kOzS of them,
-// 64 columns each). kOzS = 7 (28 products): forward 4.5e-15, inverse 1.6e-14
-// relative L2 at n = 8 against fp64 (6 slices: 5.5e-13 / 1.9e-12; tools/ozaki_sim.py).
-// ===========================================================================
+// Products of equal order d = p + q share a scale and one int32 TMEM accumulator.
+// N = 128 per MMA (the A operand's shared-memory reads amortised over 128
+// columns); 512 TMEM columns hold four 128-column accumulators, so a tile runs
+// in two passes over K: orders d = 0..3 (10 products, slices 0..3), drained into
+// fp64 registers by the epilogue, then d = 4..6 (18 products, slices 0..6).
+// kOzS = 7 (28 products): forward 4.5e-15, inverse 1.6e-14 relative L2 at n = 8
+// against fp64 (6 slices: 5.5e-13 / 1.9e-12; tools/ozaki_sim.py).
 constexpr int kOzS = 7;
-constexpr int kOzBM = 128, kOzBN = 64, kOzBK = 32;          // BK = 32 int8 = one 32-byte swizzle row
-constexpr int kOzStages = 4;
+constexpr int kOzPass1 = 4;                                 // orders d = 0..3 in the first pass
+constexpr int kOzBM = 128, kOzBN = 128, kOzBK = 32;         // BK = 32 int8 = one 32-byte swizzle row
+constexpr int kOzStages = 3;
 constexpr int kOzTileA = kOzS * kOzBM * kOzBK;             // 28 KB: all slices of the A tile
-constexpr int kOzTileB = kOzS * kOzBN * kOzBK;             // 14 KB
+constexpr int kOzTileB = kOzS * kOzBN * kOzBK;             // 28 KB
 constexpr int kOzStage = kOzTileA + kOzTileB;
-constexpr int kOzThreads = 64 + 128;                       // producer, MMA issuer, 4 epilogue warps
+constexpr int kOzEpi = 256;                                 // 8 epilogue warps: lane quarter x column half
+constexpr int kOzThreads = 64 + kOzEpi;                     // producer, MMA issuer, epilogue
 constexpr int kOzSmem = kOzStages * kOzStage + 1024 + 1024;
-constexpr int kOzTmemCols = 512;                           // kOzS x 64 = 448 used
+constexpr int kOzTmemCols = 512;                           // 4 x 128
 
 // smem descriptor, K-major, 32-byte swizzle (8-row atoms of 256 bytes)
 __device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
     return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (static_cast<uint64_t>(256 >> 4) << 32) |
            (1ull << 46) | (6ull << 61);
 }
-// D s32, A/B signed int8, K-major, M = 128, N = 64
+// D s32, A/B signed int8, K-major, M = 128, N = 128
 constexpr uint32_t kOzIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kOzBN >> 3) << 17) |
                               (static_cast<uint32_t>(kOzBM >> 4) << 24);
 
@@ -395,7 +400,8 @@ __global__ void ozaki_slice_kernel(const double* __restrict__ a, int64_t rows, i
 }
 
 __global__ void __launch_bounds__(kOzThreads, 1)
-    gemm_ozaki_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+    gemm_ozaki_kernel(const __grid_constant__ CUtensorMap tmA4, const __grid_constant__ CUtensorMap tmA7,
+                      const __grid_constant__ CUtensorMap tmW4, const __grid_constant__ CUtensorMap tmW7,
                       const double* __restrict__ sa, const double* __restrict__ sw, double* __restrict__ C,
                       int64_t M, int Nn, int K) {
     extern __shared__ uint8_t smem_raw[];
@@ -403,8 +409,8 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzStages * kOzStage);
     uint64_t* empty = full + kOzStages;
-    uint64_t* tfull = empty + kOzStages;
-    uint64_t* tempty = tfull + 1;
+    uint64_t* tfull = empty + kOzStages;  // MMA -> epilogue: a pass's accumulators are complete
+    uint64_t* tempty = tfull + 1;         // epilogue -> MMA: drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_tiles = Nn / kOzBN;
@@ -416,7 +422,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
             mbar_init(&empty[s], 1);
         }
         mbar_init(tfull, 1);
-        mbar_init(tempty, 128);
+        mbar_init(tempty, kOzEpi);
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -426,8 +432,8 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     if (warp == 0 && lane == 0) {
-        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+        for (const CUtensorMap* m : {&tmA4, &tmA7, &tmW4, &tmW7})
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -435,18 +441,21 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---- TMA producer: all kOzS slices of A and of W per stage (3-D boxes)
+        if (lane == 0) {  // ---- TMA producer: pass 1 slices 0..3, pass 2 slices 0..6 (3-D boxes)
             int s = 0;
             uint32_t ph = 0;
             for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
                 const int m0 = static_cast<int>((t / n_tiles) * kOzBM), n0 = static_cast<int>((t % n_tiles) * kOzBN);
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(&empty[s], ph ^ 1u);
-                    uint8_t* st = smem + s * kOzStage;
-                    mbar_arrive_expect_tx(&full[s], kOzStage);
-                    tma_load_3d(st, &tmA, kb * kOzBK, m0, 0, &full[s]);
-                    tma_load_3d(st + kOzTileA, &tmW, kb * kOzBK, n0, 0, &full[s]);
-                    if (++s == kOzStages) s = 0, ph ^= 1u;
+                for (int pass = 0; pass < 2; ++pass) {
+                    const uint32_t tx = (pass ? kOzS : kOzPass1) * (kOzBM + kOzBN) * kOzBK;
+                    for (int kb = 0; kb < kblocks; ++kb) {
+                        mbar_wait(&empty[s], ph ^ 1u);
+                        uint8_t* st = smem + s * kOzStage;
+                        mbar_arrive_expect_tx(&full[s], tx);
+                        tma_load_3d(st, pass ? &tmA7 : &tmA4, kb * kOzBK, m0, 0, &full[s]);
+                        tma_load_3d(st + kOzTileA, pass ? &tmW7 : &tmW4, kb * kOzBK, n0, 0, &full[s]);
+                        if (++s == kOzStages) s = 0, ph ^= 1u;
+                    }
                 }
             }
         }
@@ -455,63 +464,80 @@ __global__ void __launch_bounds__(kOzThreads, 1)
             int s = 0;
             uint32_t ph = 0, tph = 0;
             for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-                mbar_wait(tempty, tph ^ 1u);  // the epilogue drained the accumulators
-                tph ^= 1u;
-                tc_fence_after();
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(&full[s], ph);
+                for (int pass = 0; pass < 2; ++pass) {
+                    mbar_wait(tempty, tph ^ 1u);  // the epilogue drained the accumulators
+                    tph ^= 1u;
                     tc_fence_after();
-                    const uint32_t st = smem_u32(smem + s * kOzStage);
+                    for (int kb = 0; kb < kblocks; ++kb) {
+                        mbar_wait(&full[s], ph);
+                        tc_fence_after();
+                        const uint32_t st = smem_u32(smem + s * kOzStage);
+                        if (pass == 0) {
 #pragma unroll
-                    for (int p = 0; p < kOzS; ++p)
+                            for (int d = 0; d < kOzPass1; ++d)
 #pragma unroll
-                        for (int q = 0; q + p < kOzS; ++q) {  // p + q + 2 <= kOzS + 1
-                            const uint64_t a = sw32_desc(st + p * kOzBM * kOzBK);
-                            const uint64_t b = sw32_desc(st + kOzTileA + q * kOzBN * kOzBK);
-                            mma_i8(tmem_base + static_cast<uint32_t>((p + q) * kOzBN), a, b, (kb > 0 || p > 0) ? 1u : 0u);
+                                for (int pq = 0; pq <= d; ++pq)
+                                    mma_i8(tmem_base + static_cast<uint32_t>(d * kOzBN),
+                                           sw32_desc(st + pq * kOzBM * kOzBK),
+                                           sw32_desc(st + kOzTileA + (d - pq) * kOzBN * kOzBK),
+                                           (kb > 0 || pq > 0) ? 1u : 0u);
+                        } else {
+#pragma unroll
+                            for (int d = kOzPass1; d < kOzS; ++d)
+#pragma unroll
+                                for (int pq = 0; pq <= d; ++pq)
+                                    mma_i8(tmem_base + static_cast<uint32_t>((d - kOzPass1) * kOzBN),
+                                           sw32_desc(st + pq * kOzBM * kOzBK),
+                                           sw32_desc(st + kOzTileA + (d - pq) * kOzBN * kOzBK),
+                                           (kb > 0 || pq > 0) ? 1u : 0u);
                         }
-                    mma_commit(&empty[s]);
-                    if (++s == kOzStages) s = 0, ph ^= 1u;
+                        mma_commit(&empty[s]);
+                        if (++s == kOzStages) s = 0, ph ^= 1u;
+                    }
+                    mma_commit(tfull);
                 }
-                mma_commit(tfull);
             }
         }
-    } else {  // ---- epilogue: C = sigma_A sigma_W sum_d 2^{-7(d+2)} acc_d
-        const int quarter = warp & 3;
+    } else {  // ---- epilogue: C = sigma_A sigma_W sum_d 2^{-7(d+2)} acc_d, 64 columns per thread
+        const int e = warp - 2, quarter = warp & 3, half = e >> 2;
         uint32_t tph = 0;
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
             const int64_t row = (t / n_tiles) * kOzBM + quarter * 32 + lane;
-            const int n0 = static_cast<int>((t % n_tiles) * kOzBN);
-            mbar_wait(tfull, tph);
-            tph ^= 1u;
-            tc_fence_after();
-            const uint32_t tl = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
-            const double ra = row < M ? sa[row] : 0.0;
+            const int n0 = static_cast<int>((t % n_tiles) * kOzBN) + half * 64;
+            const uint32_t tl = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + half * 64;
+            double acc[64];
+#pragma unroll
+            for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+            for (int pass = 0; pass < 2; ++pass) {
+                mbar_wait(tfull, tph);
+                tph ^= 1u;
+                tc_fence_after();
+                const int d0 = pass ? kOzPass1 : 0, nd = pass ? kOzS - kOzPass1 : kOzPass1;
 #pragma unroll 1
-            for (int h = 0; h < kOzBN / 32; ++h) {
-                double acc[32];
+                for (int dd = nd - 1; dd >= 0; --dd) {
+                    const double sc = ldexp(1.0, -7 * (d0 + dd + 2));
 #pragma unroll
-                for (int j = 0; j < 32; ++j) acc[j] = 0.0;
-#pragma unroll 1
-                for (int d = kOzS - 1; d >= 0; --d) {  // smallest terms first
-                    uint32_t v[32];
-                    TMEM_LD_32(tl + d * kOzBN + h * 32, v);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                    const double sc = ldexp(1.0, -7 * (d + 2));
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t v[32];
+                        TMEM_LD_32(tl + dd * kOzBN + c * 32, v);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) acc[j] = fma(static_cast<double>(static_cast<int>(v[j])), sc, acc[j]);
-                }
-                if (row < M) {
-                    double2* dst = reinterpret_cast<double2*>(C + row * Nn + n0 + h * 32);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int c = n0 + h * 32 + 2 * j;
-                        dst[j] = make_double2(acc[2 * j] * ra * __ldg(sw + c), acc[2 * j + 1] * ra * __ldg(sw + c + 1));
+                        for (int j = 0; j < 32; ++j)
+                            acc[c * 32 + j] = fma(static_cast<double>(static_cast<int>(v[j])), sc, acc[c * 32 + j]);
                     }
                 }
+                tc_fence_before();
+                mbar_arrive(tempty);
             }
-            tc_fence_before();
-            mbar_arrive(tempty);
+            if (row < M) {
+                const double ra = sa[row];
+                double2* dst = reinterpret_cast<double2*>(C + row * Nn + n0);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int c = n0 + 2 * j;
+                    dst[j] = make_double2(acc[2 * j] * ra * __ldg(sw + c), acc[2 * j + 1] * ra * __ldg(sw + c + 1));
+                }
+            }
         }
     }
     tc_fence_before();
@@ -560,12 +586,12 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols) {
 }
 
 // slices [S][rows][K] int8, box = 32 bytes x brows rows x S slices, 32-byte swizzle
-bool make_slice_map(CUtensorMap* m, const int8_t* base, int64_t rows, int64_t K, int brows) {
+bool make_slice_map(CUtensorMap* m, const int8_t* base, int64_t rows, int64_t K, int brows, int bslices) {
     auto fn = encode_fn();
     if (!fn) return false;
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(kOzS)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(K) * static_cast<cuuint64_t>(rows)};
-    const cuuint32_t box[3] = {kOzBK, static_cast<cuuint32_t>(brows), kOzS};
+    const cuuint32_t box[3] = {kOzBK, static_cast<cuuint32_t>(brows), static_cast<cuuint32_t>(bslices)};
     const cuuint32_t estr[3] = {1, 1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -591,8 +617,9 @@ cudaError_t launch_gemm_ozaki(const int8_t* a_slices, const double* a_scale, con
                               cudaStream_t st) {
     if (M <= 0) return cudaSuccess;
     if (!gemm_ozaki_supported(Nn, K)) return cudaErrorInvalidValue;
-    CUtensorMap ma, mw;
-    if (!make_slice_map(&ma, a_slices, M, K, kOzBM) || !make_slice_map(&mw, w_slices, Nn, K, kOzBN))
+    CUtensorMap ma4, ma7, mw4, mw7;
+    if (!make_slice_map(&ma4, a_slices, M, K, kOzBM, kOzPass1) || !make_slice_map(&ma7, a_slices, M, K, kOzBM, kOzS) ||
+        !make_slice_map(&mw4, w_slices, Nn, K, kOzBN, kOzPass1) || !make_slice_map(&mw7, w_slices, Nn, K, kOzBN, kOzS))
         return cudaErrorInvalidValue;
     int per_sm = 0;
     cudaError_t e = prepare_launch(reinterpret_cast<const void*>(gemm_ozaki_kernel), kOzThreads, kOzSmem, &per_sm);
@@ -600,7 +627,7 @@ cudaError_t launch_gemm_ozaki(const int8_t* a_slices, const double* a_scale, con
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int64_t tiles = ((M + kOzBM - 1) / kOzBM) * (Nn / kOzBN);
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(tiles, num_sms));
-    gemm_ozaki_kernel<<<grid, kOzThreads, kOzSmem, st>>>(ma, mw, a_scale, w_scale, C, M, Nn, K);
+    gemm_ozaki_kernel<<<grid, kOzThreads, kOzSmem, st>>>(ma4, ma7, mw4, mw7, a_scale, w_scale, C, M, Nn, K);
     return cudaGetLastError();
 }
 
