@@ -364,17 +364,23 @@ __global__ void ozaki_slice_kernel(const double* __restrict__ a, int64_t rows, i
     if (row >= rows) return;
     const double* r = a + row * K;
     double m = 0.0;
+    bool nan = false;  // fmax drops NaN operands: track them apart
     for (int k = 8 * lane; k < K; k += 256) {
         const double4* v = reinterpret_cast<const double4*>(r + k);
         const double4 x0 = v[0], x1 = v[1];
         m = fmax(m, fmax(fmax(fabs(x0.x), fabs(x0.y)), fmax(fabs(x0.z), fabs(x0.w))));
         m = fmax(m, fmax(fmax(fabs(x1.x), fabs(x1.y)), fmax(fabs(x1.z), fabs(x1.w))));
+        nan |= isnan(x0.x + x0.y + x0.z + x0.w + x1.x + x1.y + x1.z + x1.w);
     }
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    nan = __any_sync(0xffffffffu, nan);
     int e = 0;
-    if (m > 0.0) frexp(m, &e);  // m = f 2^e, f in [0.5, 1): 2^e > m
-    const double inv = m > 0.0 ? ldexp(1.0, -e) : 0.0;
-    if (lane == 0) scale[row] = m > 0.0 ? ldexp(1.0, e) : 1.0;
+    const bool finite = isfinite(m) && !nan;
+    if (m > 0.0 && finite) frexp(m, &e);  // m = f 2^e, f in [0.5, 1): 2^e > m
+    const double inv = (m > 0.0 && finite) ? ldexp(1.0, -e) : 0.0;
+    // a row holding inf / NaN gets a NaN scale: its outputs are NaN (the fp64
+    // GEMM would propagate them too) instead of silently finite
+    if (lane == 0) scale[row] = !finite ? __longlong_as_double(0x7FF8000000000000LL) : (m > 0.0 ? ldexp(1.0, e) : 1.0);
     const int64_t plane = rows * static_cast<int64_t>(K);
     for (int k = 8 * lane; k < K; k += 256) {
         const double4* v4 = reinterpret_cast<const double4*>(r + k);

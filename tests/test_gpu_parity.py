@@ -161,6 +161,42 @@ def test_direct_f64_tcgen05_ozaki(cuda, oracle_mod, n, batch):
     assert rel(x_inv, oracle_mod.inverse_dense(n, tup(CANON), y_ref)) <= F64_TOL
 
 
+def test_direct_tcgen05_edge_rows(cuda, oracle_mod):
+    """Edge rows of the tcgen05 direct paths: zero blocks stay exactly zero, a
+    block holding NaN or inf yields a NaN row (no silently finite output), tiny
+    and huge magnitudes (per-row power-of-two scales) keep the fp64 bar, and the
+    in-place call (in == out) equals the out-of-place one."""
+    n = 8
+    rng = np.random.default_rng(5)
+    x = (rng.uniform(-1, 1, (6, n**3)) + 1j * rng.uniform(-1, 1, (6, n**3)))
+    x[1] = 0
+    x[2] *= 1e-200
+    x[3] *= 1e200
+    x[4, 7] = np.nan
+    x[5, 3] = np.inf
+    dense = dense_transform(n, CANON)
+    y = naive_apply(dense, SignalTensor(n, torch.from_numpy(x).to(cuda))).values.cpu().numpy()
+    assert np.all(y[1] == 0)
+    assert np.all(np.isnan(y[4])) and np.all(np.isnan(y[5]))
+    for b in (0, 2, 3):  # compared at unit scale (norms of 1e-200 values underflow)
+        sc = np.abs(x[b]).max()
+        ref = oracle_mod.forward_dense(n, tup(CANON), x[b:b + 1] / sc)[0]
+        assert rel(y[b] / sc, ref) <= F64_TOL, b
+    # in place through the C ABI (fcct_forward with in == out)
+    from paper_1807_10058_b200 import _capi
+
+    xt = torch.from_numpy(x[[0, 2, 3]].copy()).to(cuda)
+    out_of_place = dense._plan.apply_values(xt)
+    stream = torch.cuda.current_stream().cuda_stream
+    assert _capi.lib().fcct_forward(dense._plan._h, xt.data_ptr(), xt.data_ptr(), 3, stream) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(xt, out_of_place)
+    d32 = dense_transform(n, CANON, precision="f32")
+    x32 = torch.from_numpy(x[:2]).to(torch.complex64).to(cuda)
+    y32 = naive_apply(d32, SignalTensor(n, x32)).values
+    assert torch.all(y32[1] == 0)
+
+
 def test_reference_seeds_fast_vs_naive(cuda, oracle_mod):
     # test_transform.cpp:138-151 (seeds 40+n) and acceptance #7 (seeds 700+16n+trial)
     for n in (2, 4, 8):
