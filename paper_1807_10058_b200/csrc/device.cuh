@@ -125,6 +125,13 @@ __device__ __forceinline__ void cp_async_wait() {
 //   A 8x4 row:  a = A[lane>>2][lane&3]
 //   B 4x8 col:  b = B[lane&3][lane>>2]
 //   C 8x8:      c0,c1 = C[lane>>2][2*(lane&3) + {0,1}]
+// m16n8k4: rows lane/4 and lane/4 + 8 of A (a0, a1) and of C (c0, c1 | c2, c3)
+__device__ __forceinline__ void dmma1684(double& c0, double& c1, double& c2, double& c3, double a0, double a1,
+                                         double b) {
+    asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+                 : "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
+                 : "d"(a0), "d"(a1), "d"(b));
+}
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
