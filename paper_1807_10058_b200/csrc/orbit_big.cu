@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256, 4) orbit_big_sgen_kernel(const __grid_con
     __shared__ __align__(16) double2 T[kGenMaxCarry * 24];
     __shared__ __align__(16) uint8_t Mt[24 * 24];
     __shared__ double2 xs[kGenOrbits * 24];
-    __shared__ int2 ws[kGenOrbits * 24];  // (T row offset, g) of each member
+    __shared__ int ws[kGenOrbits * 24];   // T row offset (carry id x 24) of each member
     // the non-free orbits' rows (long serial coefficient chains) are scheduled first;
     // the remaining CTAs are persistent over groups of 10 free orbits, so the two
     // tables are loaded once per CTA (bulk copies, overlapped with the first group's
@@ -97,6 +97,10 @@ __global__ void __launch_bounds__(256, 4) orbit_big_sgen_kernel(const __grid_con
         }
         __syncthreads();  // the barrier is initialised before anyone waits on it
         const int ob = tid - tid % 24;  // first slot of this thread's orbit in the stage
+        // slots are ordered by group element, so this row's g_r = tid % 24 and its
+        // 24 values w = g_r g_c^-1 are one fixed row of the product table: packed
+        // into registers once (bytes), no table lookup per term
+        uint32_t wp[6] = {0, 0, 0, 0, 0, 0};
         bool waited = false;
         for (int grp = static_cast<int>(blockIdx.x) - tail_ctas; grp < groups; grp += nfc) {
             const int orbit = grp * kGenOrbits + tid / 24;
@@ -109,22 +113,28 @@ __global__ void __launch_bounds__(256, 4) orbit_big_sgen_kernel(const __grid_con
                 pdl_wait();  // x is the previous kernel's output
                 mbar_wait(&tbar, 0);
                 waited = true;
+                const int g0 = tid % 24;
+#pragma unroll
+                for (int q = 0; q < 6; ++q)
+                    wp[q] = static_cast<uint32_t>(Mt[g0 * 24 + 4 * q]) | (static_cast<uint32_t>(Mt[g0 * 24 + 4 * q + 1]) << 8) |
+                            (static_cast<uint32_t>(Mt[g0 * 24 + 4 * q + 2]) << 16) |
+                            (static_cast<uint32_t>(Mt[g0 * 24 + 4 * q + 3]) << 24);
             } else {
                 __syncthreads();  // the previous group's stage is consumed
             }
-            if (live) ws[tid] = make_int2(static_cast<int>((me >> 18) & 63u) * 24, gr);
-            const uint8_t* mrow = Mt + gr * 24;
+            if (live) ws[tid] = static_cast<int>((me >> 18) & 63u) * 24;
+            (void)gr;
             for (int64_t b = 0; b < batch; ++b) {
                 if (b > 0) __syncthreads();
                 if (live) xs[tid] = __ldg(x + b * d.N + nat);
                 __syncthreads();
                 if (!live) continue;
                 double re = 0.0, im = 0.0;
-#pragma unroll 8
+#pragma unroll
                 for (int c = 0; c < 24; ++c) {
                     const double2 v = xs[ob + c];
-                    const int2 w = ws[ob + c];
-                    const double2 m = T[w.x + mrow[w.y]];
+                    const int w = static_cast<int>((wp[c >> 2] >> (8 * (c & 3))) & 0xFFu);
+                    const double2 m = T[ws[ob + c] + w];
                     re = fma(m.x, v.x, re);
                     re = fma(-m.y, v.y, re);
                     im = fma(m.x, v.y, im);

@@ -122,6 +122,11 @@ bool compile_orbit_big(int n, const Params& p, bool inverse, OrbitBigHost& h, bo
         }
         if (h.gen) {
             if (gen_orbit) {
+                // device order: slot g holds the member generated by group element g
+                // (slot index = g_r, so a row's w = g_r g_c^-1 comes from a fixed table row)
+                std::array<uint32_t, 24> by_g{};
+                for (int j = 0; j < 24; ++j) by_g[(pack[j] >> 24) & 31u] = pack[j];
+                std::copy(by_g.begin(), by_g.end(), pack.begin());
                 h.fpack.insert(h.fpack.end(), pack.begin(), pack.end());
                 // base_j = e^{2 pi i (g_j k0).p / n} / 24 in long double
                 const Index3 k0 = {static_cast<int>(mem[0] / (n * n)), static_cast<int>((mem[0] / n) % n),
