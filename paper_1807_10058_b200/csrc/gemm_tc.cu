@@ -5,7 +5,8 @@
 // complex64 interleaved, K = Nn = 2 n^3; W = D or D^{-1} in real form, both
 // K-major). TF32 alone carries 11 significant bits, short of the 1e-5 fp32 bar,
 // so the product runs split (3xTF32):
-//     A.W ~= A_hi.W_hi + A_hi.W_lo + A_lo.W_hi,   x_hi = rna_tf32(x), x_lo = x - x_hi
+//     A.W ~= A_hi.W_hi + A_hi.W_lo + A_lo.W_hi,   W_hi = rna_tf32(W), A_hi = trunc_tf32(A),
+//     x_lo = rna_tf32(x - x_hi)
 // with W_hi / W_lo split from the fp64 table at plan time and A split in shared
 // memory as each stage lands. All three products accumulate into one fp32
 // accumulator in tensor memory.
@@ -22,7 +23,8 @@
 //               tcgen05.ld 32x32b.x32 and added into fp32 registers (one row,
 //               64 columns per thread); the tile's hi.lo + lo.hi accumulator is
 //               added last, then fp32 stores
-//   warps 10-13 converter: A stage -> (A_hi in place, A_lo), fence.proxy.async
+//   warps 10-13 converter: A stage -> A_lo (A_hi is the landed tile: kind::tf32
+//               drops the low 13 bits), fence.proxy.async
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -274,17 +276,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int q = 0; q < kTileA / 16 / kConvThreads; ++q) {  // elementwise: the swizzle is irrelevant
                     const int i = q * kConvThreads + ct;
+                    // A_hi is the landed tile itself: kind::tf32 reads the upper 19 bits of
+                    // each fp32 (the low 13 are dropped), so only A_lo = x - trunc(x) is written
                     const float4 x = a[i];
-                    float4 h, l;
-                    h.x = __uint_as_float(to_tf32(x.x));
-                    h.y = __uint_as_float(to_tf32(x.y));
-                    h.z = __uint_as_float(to_tf32(x.z));
-                    h.w = __uint_as_float(to_tf32(x.w));
-                    l.x = __uint_as_float(to_tf32(x.x - h.x));  // rounded, not left to the MMA's truncation
-                    l.y = __uint_as_float(to_tf32(x.y - h.y));
-                    l.z = __uint_as_float(to_tf32(x.z - h.z));
-                    l.w = __uint_as_float(to_tf32(x.w - h.w));
-                    a[i] = h;
+                    float4 l;
+                    l.x = __uint_as_float(to_tf32(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u)));
+                    l.y = __uint_as_float(to_tf32(x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u)));
+                    l.z = __uint_as_float(to_tf32(x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u)));
+                    l.w = __uint_as_float(to_tf32(x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u)));
                     lo[i] = l;
                 }
                 fence_proxy_async_smem();  // generic-proxy writes -> tensor-core (async proxy) reads
