@@ -723,6 +723,10 @@ void scratch_retire(fcct_plan_s* pl, cudaStream_t st) {
     if (pl->scratch_ev) ck(cudaEventSynchronize(pl->scratch_ev), "scratch event sync");
 }
 
+// Ozaki slice counts: the inverse's error is amplified by the conditioning of
+// D^{-1}, so it carries one more slice (fp64-level accuracy, tools/ozaki_sim.py)
+constexpr int kOzaki_forward = 7, kOzaki_inverse = 8;
+
 void build_direct(fcct_plan_s* pl) {
     const int n = pl->n;
     const int64_t N = cube(n);
@@ -781,9 +785,10 @@ void build_direct(fcct_plan_s* pl) {
     if (pl->oz64) {
         const int K = static_cast<int>(2 * N);
         for (int dir = 0; dir < 2; ++dir) {
-            pl->oz_w[dir] = std::make_shared<DevBuf>(static_cast<size_t>(ozaki_slices()) * K * K);
+            const int S = dir ? kOzaki_inverse : kOzaki_forward;
+            pl->oz_w[dir] = std::make_shared<DevBuf>(static_cast<size_t>(S) * K * K);
             pl->oz_ws[dir] = std::make_shared<DevBuf>(static_cast<size_t>(K) * 8);
-            ck(ozaki_slice(static_cast<const double*>((dir ? pl->Wt_inv : pl->Wt_fwd)->ptr), K, K,
+            ck(ozaki_slice(static_cast<const double*>((dir ? pl->Wt_inv : pl->Wt_fwd)->ptr), K, K, S,
                            static_cast<int8_t*>(pl->oz_w[dir]->ptr), static_cast<double*>(pl->oz_ws[dir]->ptr),
                            nullptr),
                "ozaki slices");
@@ -1221,7 +1226,10 @@ void fill_info(fcct_plan_s* pl) {
         // 3xTF32 on tcgen05: three tensor-core products per algorithmic one
         if (pl->tc32) in.exec_flops_forward = in.exec_flops_inverse = 3.0 * 8.0 * N * N;
         // Ozaki: 28 int8 products per algorithmic one (ops, not fp64 flops)
-        if (pl->oz64) in.exec_flops_forward = in.exec_flops_inverse = 28.0 * 8.0 * N * N;
+        if (pl->oz64) {
+            in.exec_flops_forward = 28.0 * 8.0 * N * N;  // 7 slices: 28 int8 products
+            in.exec_flops_inverse = 36.0 * 8.0 * N * N;  // 8 slices: 36
+        }
     }
 }
 
@@ -1353,13 +1361,14 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
             pl->oz_in_scale = std::make_shared<DevBuf>(static_cast<size_t>(batch) * 8);
         }
         scratch_acquire(pl, st);
-        ck(ozaki_slice(static_cast<const double*>(in), batch, K, static_cast<int8_t*>(pl->oz_in->ptr),
+        const int S = inverse ? kOzaki_inverse : kOzaki_forward;
+        ck(ozaki_slice(static_cast<const double*>(in), batch, K, S, static_cast<int8_t*>(pl->oz_in->ptr),
                        static_cast<double*>(pl->oz_in_scale->ptr), st),
            "ozaki input slices");
         ck(launch_gemm_ozaki(static_cast<const int8_t*>(pl->oz_in->ptr), static_cast<const double*>(pl->oz_in_scale->ptr),
                              static_cast<const int8_t*>(pl->oz_w[inverse ? 1 : 0]->ptr),
                              static_cast<const double*>(pl->oz_ws[inverse ? 1 : 0]->ptr), static_cast<double*>(dst),
-                             batch, K, K, pl->num_sms, st),
+                             batch, K, K, S, pl->num_sms, st),
            "direct gemm ozaki (tcgen05 int8)");
         scratch_release(pl, st);
     } else if (pl->tc32)

@@ -315,14 +315,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 // columns); 512 TMEM columns hold four 128-column accumulators, so a tile runs
 // in two passes over K: orders d = 0..3 (10 products, slices 0..3), drained into
 // fp64 registers by the epilogue, then d = 4..6 (18 products, slices 0..6).
-// kOzS = 7 (28 products): forward 4.5e-15, inverse 1.6e-14 relative L2 at n = 8
-// against fp64 (6 slices: 5.5e-13 / 1.9e-12; tools/ozaki_sim.py).
-constexpr int kOzS = 7;
+// S = 7 slices (28 products): forward 4.5e-15, inverse 1.6e-14 relative L2 at
+// n = 8 against fp64; S = 8 (36 products): 6.5e-16 / 8.7e-16 (tools/ozaki_sim.py).
+// The inverse, whose error the conditioning of D^{-1} amplifies, runs S = 8.
+constexpr int kOzSMax = 8;                                  // 7 slices forward, 8 inverse (capi.cpp)
 constexpr int kOzPass1 = 4;                                 // orders d = 0..3 in the first pass
 constexpr int kOzBM = 128, kOzBN = 128, kOzBK = 32;         // BK = 32 int8 = one 32-byte swizzle row
 constexpr int kOzStages = 3;
-constexpr int kOzTileA = kOzS * kOzBM * kOzBK;             // 28 KB: all slices of the A tile
-constexpr int kOzTileB = kOzS * kOzBN * kOzBK;             // 28 KB
+constexpr int kOzTileA = kOzSMax * kOzBM * kOzBK;          // 32 KB: all slices of the A tile
+constexpr int kOzTileB = kOzSMax * kOzBN * kOzBK;          // 32 KB
 constexpr int kOzStage = kOzTileA + kOzTileB;
 constexpr int kOzEpi = 256;                                 // 8 epilogue warps: lane quarter x column half
 constexpr int kOzThreads = 64 + kOzEpi;                     // producer, MMA issuer, epilogue
@@ -356,6 +357,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 // rows of A [rows][K] fp64 -> slices [kOzS][rows][K] int8 and scale[rows] = 2^e >= max |row|.
 // One warp per row; each lane takes 8 consecutive elements per step (two 32-byte
 // loads, one 8-byte store per slice: 256-byte warp stores). K % 8 == 0.
+template <int S>
 __global__ void ozaki_slice_kernel(const double* __restrict__ a, int64_t rows, int K, int8_t* __restrict__ sl,
                                    double* __restrict__ scale) {
     const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -386,7 +388,7 @@ __global__ void ozaki_slice_kernel(const double* __restrict__ a, int64_t rows, i
         const double4 x0 = v4[0], x1 = v4[1];
         double v[8] = {x0.x * inv, x0.y * inv, x0.z * inv, x0.w * inv, x1.x * inv, x1.y * inv, x1.z * inv, x1.w * inv};
 #pragma unroll
-        for (int q = 1; q <= kOzS; ++q) {
+        for (int q = 1; q <= S; ++q) {
             const double sc = ldexp(1.0, 7 * q), isc = ldexp(1.0, -7 * q);
             uint32_t lo = 0, hi = 0;
 #pragma unroll
@@ -404,6 +406,7 @@ __global__ void ozaki_slice_kernel(const double* __restrict__ a, int64_t rows, i
     }
 }
 
+template <int S>
 __global__ void __launch_bounds__(kOzThreads, 1)
     gemm_ozaki_kernel(const __grid_constant__ CUtensorMap tmA4, const __grid_constant__ CUtensorMap tmA7,
                       const __grid_constant__ CUtensorMap tmW4, const __grid_constant__ CUtensorMap tmW7,
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
             for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
                 const int m0 = static_cast<int>((t / n_tiles) * kOzBM), n0 = static_cast<int>((t % n_tiles) * kOzBN);
                 for (int pass = 0; pass < 2; ++pass) {
-                    const uint32_t tx = (pass ? kOzS : kOzPass1) * (kOzBM + kOzBN) * kOzBK;
+                    const uint32_t tx = (pass ? S : kOzPass1) * (kOzBM + kOzBN) * kOzBK;
                     for (int kb = 0; kb < kblocks; ++kb) {
                         mbar_wait(&empty[s], ph ^ 1u);
                         uint8_t* st = smem + s * kOzStage;
@@ -488,7 +491,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                                            (kb > 0 || pq > 0) ? 1u : 0u);
                         } else {
 #pragma unroll
-                            for (int d = kOzPass1; d < kOzS; ++d)
+                            for (int d = kOzPass1; d < S; ++d)
 #pragma unroll
                                 for (int pq = 0; pq <= d; ++pq)
                                     mma_i8(tmem_base + static_cast<uint32_t>((d - kOzPass1) * kOzBN),
@@ -517,7 +520,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                 mbar_wait(tfull, tph);
                 tph ^= 1u;
                 tc_fence_after();
-                const int d0 = pass ? kOzPass1 : 0, nd = pass ? kOzS - kOzPass1 : kOzPass1;
+                const int d0 = pass ? kOzPass1 : 0, nd = pass ? S - kOzPass1 : kOzPass1;
 #pragma unroll 1
                 for (int dd = nd - 1; dd >= 0; --dd) {
                     const double sc = ldexp(1.0, -7 * (d0 + dd + 2));
@@ -591,10 +594,12 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols) {
 }
 
 // slices [S][rows][K] int8, box = 32 bytes x brows rows x S slices, 32-byte swizzle
-bool make_slice_map(CUtensorMap* m, const int8_t* base, int64_t rows, int64_t K, int brows, int bslices) {
+bool make_slice_map(CUtensorMap* m, const int8_t* base, int64_t rows, int64_t K, int brows, int bslices,
+                    int nslices) {
     auto fn = encode_fn();
     if (!fn) return false;
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(kOzS)};
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows),
+                                static_cast<cuuint64_t>(nslices)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(K) * static_cast<cuuint64_t>(rows)};
     const cuuint32_t box[3] = {kOzBK, static_cast<cuuint32_t>(brows), static_cast<cuuint32_t>(bslices)};
     const cuuint32_t estr[3] = {1, 1, 1};
@@ -605,35 +610,49 @@ bool make_slice_map(CUtensorMap* m, const int8_t* base, int64_t rows, int64_t K,
 
 }  // namespace
 
-int ozaki_slices() { return kOzS; }
+int ozaki_slices() { return kOzSMax; }
 
 bool gemm_ozaki_supported(int Nn, int K) { return Nn % kOzBN == 0 && K % kOzBK == 0 && Nn >= kOzBN && K <= 8192; }
 // (the slicing kernel also needs K % 8 == 0 and 32-byte aligned rows: K % 32 == 0 holds)
 
-cudaError_t ozaki_slice(const double* a, int64_t rows, int K, int8_t* slices, double* scale, cudaStream_t st) {
+cudaError_t ozaki_slice(const double* a, int64_t rows, int K, int S, int8_t* slices, double* scale, cudaStream_t st) {
     if (rows <= 0) return cudaSuccess;
     const int64_t threads = rows * 32;
-    ozaki_slice_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(a, rows, K, slices, scale);
+    const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
+    if (S == 7)
+        ozaki_slice_kernel<7><<<grid, 256, 0, st>>>(a, rows, K, slices, scale);
+    else if (S == 8)
+        ozaki_slice_kernel<8><<<grid, 256, 0, st>>>(a, rows, K, slices, scale);
+    else
+        return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 
-cudaError_t launch_gemm_ozaki(const int8_t* a_slices, const double* a_scale, const int8_t* w_slices,
-                              const double* w_scale, double* C, int64_t M, int Nn, int K, int num_sms,
-                              cudaStream_t st) {
-    if (M <= 0) return cudaSuccess;
-    if (!gemm_ozaki_supported(Nn, K)) return cudaErrorInvalidValue;
+template <int S>
+cudaError_t launch_ozaki_t(const int8_t* a_slices, const double* a_scale, const int8_t* w_slices, const double* w_scale,
+                           double* C, int64_t M, int Nn, int K, int num_sms, cudaStream_t st) {
     CUtensorMap ma4, ma7, mw4, mw7;
-    if (!make_slice_map(&ma4, a_slices, M, K, kOzBM, kOzPass1) || !make_slice_map(&ma7, a_slices, M, K, kOzBM, kOzS) ||
-        !make_slice_map(&mw4, w_slices, Nn, K, kOzBN, kOzPass1) || !make_slice_map(&mw7, w_slices, Nn, K, kOzBN, kOzS))
+    if (!make_slice_map(&ma4, a_slices, M, K, kOzBM, kOzPass1, S) || !make_slice_map(&ma7, a_slices, M, K, kOzBM, S, S) ||
+        !make_slice_map(&mw4, w_slices, Nn, K, kOzBN, kOzPass1, S) || !make_slice_map(&mw7, w_slices, Nn, K, kOzBN, S, S))
         return cudaErrorInvalidValue;
     int per_sm = 0;
-    cudaError_t e = prepare_launch(reinterpret_cast<const void*>(gemm_ozaki_kernel), kOzThreads, kOzSmem, &per_sm);
+    cudaError_t e = prepare_launch(reinterpret_cast<const void*>(gemm_ozaki_kernel<S>), kOzThreads, kOzSmem, &per_sm);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int64_t tiles = ((M + kOzBM - 1) / kOzBM) * (Nn / kOzBN);
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(tiles, num_sms));
-    gemm_ozaki_kernel<<<grid, kOzThreads, kOzSmem, st>>>(ma4, ma7, mw4, mw7, a_scale, w_scale, C, M, Nn, K);
+    gemm_ozaki_kernel<S><<<grid, kOzThreads, kOzSmem, st>>>(ma4, ma7, mw4, mw7, a_scale, w_scale, C, M, Nn, K);
     return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_ozaki(const int8_t* a_slices, const double* a_scale, const int8_t* w_slices,
+                              const double* w_scale, double* C, int64_t M, int Nn, int K, int S, int num_sms,
+                              cudaStream_t st) {
+    if (M <= 0) return cudaSuccess;
+    if (!gemm_ozaki_supported(Nn, K)) return cudaErrorInvalidValue;
+    if (S == 7) return launch_ozaki_t<7>(a_slices, a_scale, w_slices, w_scale, C, M, Nn, K, num_sms, st);
+    if (S == 8) return launch_ozaki_t<8>(a_slices, a_scale, w_slices, w_scale, C, M, Nn, K, num_sms, st);
+    return cudaErrorInvalidValue;
 }
 
 bool gemm_tf32x3_supported(int Nn, int K) { return Nn % kBN == 0 && K % kBK == 0 && Nn >= kBN && K >= kBK; }

@@ -161,9 +161,10 @@ cudaError_t launch_gemm_tf32x3(const float* A, const float* Whi, const float* Wl
 // A and W with per-row power-of-two scales, exact int8 products, fp64 epilogue.
 int ozaki_slices();
 bool gemm_ozaki_supported(int Nn, int K);
-cudaError_t ozaki_slice(const double* a, int64_t rows, int K, int8_t* slices, double* scale, cudaStream_t st);
+// S = 7 or 8 slices ([S][rows][K] int8); ozaki_slices() = the largest S
+cudaError_t ozaki_slice(const double* a, int64_t rows, int K, int S, int8_t* slices, double* scale, cudaStream_t st);
 cudaError_t launch_gemm_ozaki(const int8_t* a_slices, const double* a_scale, const int8_t* w_slices,
-                              const double* w_scale, double* C, int64_t M, int Nn, int K, int num_sms,
+                              const double* w_scale, double* C, int64_t M, int Nn, int K, int S, int num_sms,
                               cudaStream_t st);
 // fp64 table -> (rna_tf32 part, fp32 remainder)
 cudaError_t split_tf32(const double* w, float* hi, float* lo, int64_t count, cudaStream_t st);
