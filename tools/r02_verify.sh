@@ -23,7 +23,7 @@ run c3d --config c3 --method direct --blocks 1024
 run c4 --config c4
 run c5 --config c5
 run c2f32 --precision f32 --no-cpu
-run c2d --method direct --no-cpu
+run c2d --method direct
 run c2f32d --method direct --precision f32 --no-cpu
 timeout 600 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err; echo "reference rc=$?"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1; echo "ncu launches rc=$?"
