@@ -112,19 +112,20 @@ def test_direct_f32(cuda, oracle_mod, n):
     assert rel(back.cpu().numpy(), x) <= F32_TOL
 
 
-@pytest.mark.parametrize("n,batch", [(4, 1), (4, 389), (8, 130), (8, 1000)])
-def test_direct_f32_tcgen05(cuda, oracle_mod, n, batch):
+@pytest.mark.parametrize("n,batch,p", [(4, 1, CANON), (4, 389, CANON), (8, 130, CANON), (8, 1000, CANON),
+                                       (8, 77, SkewParams(0.21, 0.055, 0.4))])
+def test_direct_f32_tcgen05(cuda, oracle_mod, n, batch, p):
     """fp32 direct plans run on tcgen05 (executor 8: 3xTF32 split, TMEM accumulator,
     TMA tensor maps; gemm_tc.cu), ragged batches (partial 128-row tiles, a single
     block): <= 1e-5 vs the long-double dense oracle, both directions, and in place."""
     x = rand_batch(n, batch, seed=90 + batch)
-    y_ref = oracle_mod.forward_dense(n, tup(CANON), x)
-    dense = dense_transform(n, CANON, precision="f32")
+    y_ref = oracle_mod.forward_dense(n, tup(p), x)
+    dense = dense_transform(n, p, precision="f32")
     assert dense._plan.info.executor == 8
     xt = torch.from_numpy(x).to(torch.complex64).to(cuda)
     y = naive_apply(dense, SignalTensor(n, xt)).values
     assert rel(y.cpu().numpy(), y_ref) <= F32_TOL
-    back = inverse_apply(dense, Spectrum(n, CANON, y)).data
+    back = inverse_apply(dense, Spectrum(n, p, y)).data
     assert rel(back.cpu().numpy(), x) <= F32_TOL
     # TF32 alone would miss the bar by ~100x: the split must be doing its work
     assert rel(y.cpu().numpy(), y_ref) <= 2e-6
@@ -142,23 +143,24 @@ def test_direct_f32_tcgen05_n16(cuda, oracle_mod):
     assert rel(y[:, rows], want) <= F32_TOL
 
 
-@pytest.mark.parametrize("n,batch", [(4, 1), (4, 300), (8, 130), (8, 1000)])
-def test_direct_f64_tcgen05_ozaki(cuda, oracle_mod, n, batch):
-    """fp64 direct plans run on tcgen05 (executor 9): the Ozaki scheme — 7 int8
-    slices of the block and of D / D^-1 per row, exact int8 products (int32 in
-    TMEM), fp64 epilogue — against the long-double oracle at the fp64 bar, both
-    directions, ragged batches."""
+@pytest.mark.parametrize("n,batch,p", [(4, 1, CANON), (4, 300, CANON), (8, 130, CANON), (8, 1000, CANON),
+                                       (8, 77, SkewParams(0.21, 0.055, 0.4)), (4, 33, SkewParams(0.37, 0.61, 0.085))])
+def test_direct_f64_tcgen05_ozaki(cuda, oracle_mod, n, batch, p):
+    """fp64 direct plans run on tcgen05 (executor 9): the Ozaki scheme — 7 (forward)
+    / 8 (inverse) int8 slices of the block and of D / D^-1 per row, exact int8
+    products (int32 in TMEM), fp64 epilogue — against the long-double oracle at the
+    fp64 bar, both directions, ragged batches, canonical and non-dyadic offsets."""
     x = rand_batch(n, batch, seed=700 + batch)
-    y_ref = oracle_mod.forward_dense(n, tup(CANON), x)
-    dense = dense_transform(n, CANON)
+    y_ref = oracle_mod.forward_dense(n, tup(p), x)
+    dense = dense_transform(n, p)
     assert dense._plan.info.executor == 9
     xt = torch.from_numpy(x).to(cuda)
     y = naive_apply(dense, SignalTensor(n, xt)).values
     assert rel(y.cpu().numpy(), y_ref) <= F64_TOL
-    back = inverse_apply(dense, Spectrum(n, CANON, y)).data
+    back = inverse_apply(dense, Spectrum(n, p, y)).data
     assert rel(back.cpu().numpy(), x) <= F64_TOL
-    x_inv = inverse_apply(dense, Spectrum(n, CANON, torch.from_numpy(y_ref).to(cuda))).data.cpu().numpy()
-    assert rel(x_inv, oracle_mod.inverse_dense(n, tup(CANON), y_ref)) <= F64_TOL
+    x_inv = inverse_apply(dense, Spectrum(n, p, torch.from_numpy(y_ref).to(cuda))).data.cpu().numpy()
+    assert rel(x_inv, oracle_mod.inverse_dense(n, tup(p), y_ref)) <= F64_TOL
 
 
 def test_direct_tcgen05_edge_rows(cuda, oracle_mod):
