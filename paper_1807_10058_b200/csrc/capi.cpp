@@ -1276,11 +1276,35 @@ fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int 
     return pl.release();
 }
 
+void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st);
+void run_real(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st);
+
+// Device buffers that are not 16-byte aligned (a caller's sub-range at an odd
+// complex64 / real offset) cannot feed the TMA row copies and vector loads of
+// the executors: such calls run on aligned staging copies (the result is the
+// same; the staging is the caller's cost). Returns true when it handled the call.
+bool run_staged_if_unaligned(fcct_plan_s* pl, bool inverse, bool real_io, const void* in, void* out, int64_t batch,
+                             cudaStream_t st) {
+    if (((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) return false;
+    const int64_t N = cube(pl->n), eb = elem_bytes(pl);
+    const int64_t in_eb = (real_io && !inverse) ? eb / 2 : eb, out_eb = (real_io && inverse) ? eb / 2 : eb;
+    DevBuf si(static_cast<size_t>(batch * N * in_eb)), so(static_cast<size_t>(batch * N * out_eb));
+    ck(cudaMemcpyAsync(si.ptr, in, si.bytes, cudaMemcpyDeviceToDevice, st), "stage input");
+    if (real_io)
+        run_real(pl, inverse, si.ptr, so.ptr, batch, st);
+    else
+        run(pl, inverse, si.ptr, so.ptr, batch, st);
+    ck(cudaMemcpyAsync(out, so.ptr, so.bytes, cudaMemcpyDeviceToDevice, st), "copy back");
+    ck(cudaStreamSynchronize(st), "sync");  // before the staging buffers are freed
+    return true;
+}
+
 void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st) {
     if (batch < 0) throw FcctError(ST_SIZE_MISMATCH, "batch must be >= 0");
     if (batch == 0) return;
     if (!in || !out) throw FcctError(ST_INVALID_ARGUMENT, "null buffer");
     DeviceGuard guard(pl->device);
+    if (run_staged_if_unaligned(pl, inverse, false, in, out, batch, st)) return;
     const bool f32 = pl->precision == FCCT_F32;
     if (pl->radix) {
         if (pl->two_level) {
@@ -1344,9 +1368,19 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
     const int64_t N = cube(pl->n);
     const void* W = inverse ? pl->Wt_inv->ptr : pl->Wt_fwd->ptr;
     void* dst = out;
-    std::shared_ptr<DevBuf> tmp;
-    if (in == out) {
-        tmp = std::make_shared<DevBuf>(static_cast<size_t>(batch * N * elem_bytes(pl)));
+    std::shared_ptr<DevBuf> tmp, tmp_in;
+    const size_t io_bytes = static_cast<size_t>(batch * N * elem_bytes(pl));
+    // the tcgen05 paths read rows with TMA / 32-byte vector loads: buffers that are
+    // not 32-byte aligned (a caller's sub-range at an odd offset) are staged
+    const bool misaligned = (pl->oz64 || pl->tc32) &&
+                            ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 31) != 0;
+    if (misaligned && (reinterpret_cast<uintptr_t>(in) & 31) != 0) {
+        tmp_in = std::make_shared<DevBuf>(io_bytes);
+        ck(cudaMemcpyAsync(tmp_in->ptr, in, io_bytes, cudaMemcpyDeviceToDevice, st), "stage input");
+        in = tmp_in->ptr;
+    }
+    if (in == out || (misaligned && (reinterpret_cast<uintptr_t>(out) & 31) != 0)) {
+        tmp = std::make_shared<DevBuf>(io_bytes);
         dst = tmp->ptr;
     }
     if (pl->oz64) {
@@ -1385,11 +1419,10 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
         ck(launch_gemm_f64(static_cast<const double*>(in), static_cast<const double*>(W), static_cast<double*>(dst),
                            batch, static_cast<int>(2 * N), static_cast<int>(2 * N), st),
            "direct gemm f64");
-    if (tmp) {
+    if (tmp)
         ck(cudaMemcpyAsync(out, tmp->ptr, static_cast<size_t>(batch * N * elem_bytes(pl)), cudaMemcpyDeviceToDevice, st),
            "copy back");
-        ck(cudaStreamSynchronize(st), "sync");
-    }
+    if (tmp || tmp_in) ck(cudaStreamSynchronize(st), "sync");  // before the staging buffers are freed
 }
 
 void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch, cudaStream_t st);
@@ -1493,6 +1526,7 @@ void run_real(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t 
     if (batch == 0) return;
     if (!in || !out) throw FcctError(ST_INVALID_ARGUMENT, "null buffer");
     DeviceGuard guard(pl->device);
+    if (run_staged_if_unaligned(pl, inverse, true, in, out, batch, st)) return;
     const bool f32 = pl->precision == FCCT_F32;
     if (pl->radix && pl->two_level) {
         const int cm = f32 ? 1 : 0, rm = f32 ? 3 : 2;

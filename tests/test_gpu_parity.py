@@ -197,6 +197,45 @@ def test_direct_tcgen05_edge_rows(cuda, oracle_mod):
     x32 = torch.from_numpy(x[:2]).to(torch.complex64).to(cuda)
     y32 = naive_apply(d32, SignalTensor(n, x32)).values
     assert torch.all(y32[1] == 0)
+    # buffers at an 8 / 16-byte offset (not 32-byte aligned) are staged, same result
+    for plan, dt, esz in ((dense._plan, torch.complex128, 16), (d32._plan, torch.complex64, 8)):
+        xb = torch.from_numpy(x[[0, 2]].copy()).to(dt).to(cuda)
+        want = plan.apply_values(xb)
+        raw_in = torch.zeros(2 * n**3 + 4, dtype=dt, device=cuda)
+        raw_out = torch.zeros_like(raw_in)
+        raw_in[1:1 + 2 * n**3] = xb.reshape(-1)
+        assert _capi.lib().fcct_forward(plan._h, raw_in.data_ptr() + esz, raw_out.data_ptr() + esz, 2, stream) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(raw_out[1:1 + 2 * n**3].reshape(2, -1), want)
+
+
+@pytest.mark.parametrize("n", [4, 8, 16])
+def test_fast_f32_unaligned_buffers(cuda, n):
+    """fp32 fast plans on buffers at an 8-byte offset (a caller's sub-range; TMA
+    needs 16-byte rows): same result as aligned buffers."""
+    from paper_1807_10058_b200 import _capi
+
+    plan = build_plan(n, CANON, precision="f32")
+    x = torch.from_numpy(rand_batch(n, 3, seed=n)).to(torch.complex64).to(cuda)
+    want = plan.apply_values(x)
+    raw_in = torch.zeros(3 * n**3 + 4, dtype=torch.complex64, device=cuda)
+    raw_out = torch.zeros_like(raw_in)
+    raw_in[1:1 + 3 * n**3] = x.reshape(-1)
+    stream = torch.cuda.current_stream().cuda_stream
+    st = _capi.lib().fcct_forward(plan._h, raw_in.data_ptr() + 8, raw_out.data_ptr() + 8, 3, stream)
+    torch.cuda.synchronize()
+    assert st == 0, _capi.lib().fcct_last_error()
+    assert torch.equal(raw_out[1:1 + 3 * n**3].reshape(3, -1), want)
+    # real f32 samples at a 4-byte offset (fused real-sample entry)
+    xr = x.real.contiguous()
+    want_r = plan.apply_values(xr)
+    raw_r = torch.zeros(3 * n**3 + 4, dtype=torch.float32, device=cuda)
+    raw_r[1:1 + 3 * n**3] = xr.reshape(-1)
+    out_r = torch.zeros(3 * n**3 + 4, dtype=torch.complex64, device=cuda)
+    st = _capi.lib().fcct_forward_real(plan._h, raw_r.data_ptr() + 4, out_r.data_ptr() + 8, 3, stream)
+    torch.cuda.synchronize()
+    assert st == 0, _capi.lib().fcct_last_error()
+    assert torch.equal(out_r[1:1 + 3 * n**3].reshape(3, -1), want_r)
 
 
 def test_reference_seeds_fast_vs_naive(cuda, oracle_mod):
