@@ -50,16 +50,25 @@ for n, ex, b in cases:
     err = float((xb - x).abs().max())
     print(f"n={n:2d} {ex:13s} batch={b:3d} executor={plan.info.executor} repeat-equal={ok} roundtrip={err:.1e}")
     failures += (not ok) or err > 1e-9
-for n, prec in [(4, "f64"), (8, "f64"), (8, "f32")]:
+for n, prec in [(4, "f64"), (8, "f64"), (8, "f32"), (2, "f64")]:
+    # tcgen05 direct plans (executors 8, 9) share a per-plan slice workspace across
+    # calls and streams; n = 2 runs the DMMA GEMM
     dt = dense_transform(n, P, precision=prec)
-    x = rnd(n, 33, 5)
+    x = rnd(n, 333, 5)
     if prec == "f32":
         x = x.to(torch.complex64)
     y = naive_apply(dt, SignalTensor(n, x)).values
+    y1 = naive_apply(dt, SignalTensor(n, x)).values
+    s2 = torch.cuda.Stream()
+    with torch.cuda.stream(s2):
+        y2 = naive_apply(dt, SignalTensor(n, x)).values
+        x2 = inverse_apply(dt, Spectrum(n, P, y2)).data
+    s2.synchronize()
     xb = inverse_apply(dt, Spectrum(n, P, y)).data
     torch.cuda.synchronize()
+    ok = torch.equal(y, y1) and torch.equal(y, y2) and torch.equal(xb, x2)
     err = float((xb - x).abs().max())
-    print(f"n={n:2d} direct {prec} roundtrip={err:.1e}")
-    failures += err > (1e-4 if prec == "f32" else 1e-9)
+    print(f"n={n:2d} direct {prec} executor={dt._plan.info.executor} repeat-equal={ok} roundtrip={err:.1e}")
+    failures += (not ok) or err > (1e-4 if prec == "f32" else 1e-9)
 print("FAILURES", failures)
 sys.exit(1 if failures else 0)
