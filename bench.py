@@ -514,7 +514,7 @@ def b200_arm(args):
     blocks = b1 - b0
 
     if args.method == "fast":
-        plan = build_plan(n, p, precision=w["precision"])
+        plan = build_plan(n, p, precision=w["precision"], executor=args.executor)
     else:
         plan = dense_transform(n, p, precision=w["precision"])._plan
     info = plan.info
@@ -658,7 +658,7 @@ def b200_arm(args):
     hbm = peaks.get("hbm_gbs", 6488.0)
     # the roofline of the pipe that executes the plan: the FP64 tensor pipe for
     # the DMMA executors (fp32 plans there keep fp64 arithmetic, complex64 I/O)
-    on_fp64_pipe = (not f32) or info.executor in (2, 4, 5, 6, 7)
+    on_fp64_pipe = (not f32) or info.executor in (2, 4, 5, 6, 7, 10)
     on_tcgen05 = info.executor in (8, 9)
     peak_tf = (TF32_PEAK_TFLOPS if info.executor == 8 else INT8_PEAK_TOPS) if on_tcgen05 else (
         FP64_PEAK_TFLOPS if on_fp64_pipe else FP32_PEAK_TFLOPS)
@@ -746,7 +746,9 @@ KERNELS = {0: "gemm_f64_kernel / gemm_f32_kernel (direct)", 1: "pipeline_kernel 
            6: "orbit16_base_kernel + fft_cube_kernel (two-pass orbit-FFT: S_n on the FP64 tensor pipe, then the n^3 FFT)",
            7: "orbit_big_s_kernel + line_fft_kernel (large-n orbit-FFT: S_n then three line-FFT passes)",
            8: "gemm_tf32x3_kernel (direct, tcgen05.mma kind::tf32 x3 split, TMEM accumulator, TMA tensor maps)",
-           9: "ozaki_slice_kernel + gemm_ozaki_kernel (direct fp64, tcgen05.mma kind::i8 on 7 int8 slices, TMEM)"}
+           9: "ozaki_slice_kernel + gemm_ozaki_kernel (direct fp64, tcgen05.mma kind::i8 on 7 int8 slices, TMEM)",
+           10: "orbit_pat_kernel (single pass: the block resident in shared memory, constant-operator DMMA base change "
+               "over the block's own orbits + the n^3 FFT)"}
 
 
 def main():
@@ -768,6 +770,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--emulate-cpu", action="store_true", help="launcher test without a GPU (gloo, host emulation)")
+    ap.add_argument("--executor", default="auto", help="force a fast executor (fcct.EXECUTORS; A/B runs)")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch (from profiles/)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

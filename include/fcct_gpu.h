@@ -82,7 +82,9 @@ typedef struct {
                                 6 two-pass orbit-FFT (n = 16: S_n pass + cube FFT pass),
                                 7 large-n orbit-FFT (n = 32, 64: S_n pass + three line-FFT passes),
                                 8 direct GEMM on tcgen05 (fp32 plans, 3xTF32, gemm_tc.cu),
-                                9 direct GEMM on tcgen05 (fp64 plans, Ozaki int8 slices, gemm_tc.cu) */
+                                9 direct GEMM on tcgen05 (fp64 plans, Ozaki int8 slices, gemm_tc.cu),
+                                10 single-pass orbit-pattern executor (n = 16: the block resident in
+                                   shared memory, constant-operator DMMA base change + cube FFT, orbit_pat.hpp) */
     double exec_flops_forward; /* flops the executor issues on the FP64 pipes per block (tensor-core
                                   tiles including their zero padding, plus FFT butterflies); 0 when
                                   equal to the algorithmic count */
@@ -109,13 +111,14 @@ fcct_status fcct_plan_create(int n, double r, double s, double t, int method, in
  * selects executors in the product build. */
 typedef enum {
     FCCT_EXEC_AUTO = 0,
-    FCCT_EXEC_ORBIT = 1,          /* orbit-FFT executors (n = 4, 8 warp-specialised; 16; 32, 64) */
+    FCCT_EXEC_ORBIT = 1,          /* orbit-FFT executors (n = 4, 8 warp-specialised; 16 single pass; 32, 64) */
     FCCT_EXEC_ORBIT_PHASED = 2,   /* n = 4, 8: the phased orbit-FFT kernel (16 warps alternate roles) */
     FCCT_EXEC_PIPELINE2 = 3,      /* stage-by-stage FP64 DMMA pipeline (n <= 8) */
     FCCT_EXEC_TWO_LEVEL = 4,      /* n = 16: root pass + eight n = 8 orbit-FFT children */
     FCCT_EXEC_TWO_LEVEL_V2 = 5,   /* n = 16: root pass + eight n = 8 stage-pipeline children */
     FCCT_EXEC_TILE = 6,           /* shared-memory tile interpreter */
-    FCCT_EXEC_GLOBAL = 7          /* global-memory multi-pass pipeline */
+    FCCT_EXEC_GLOBAL = 7,         /* global-memory multi-pass pipeline */
+    FCCT_EXEC_ORBIT_TWO_PASS = 8  /* n = 16: the two-pass orbit-FFT executor (S_n pass + cube FFT pass through HBM) */
 } fcct_executor;
 
 /* build_plan with a forced executor (method FAST; see fcct_executor). */

@@ -14,8 +14,8 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libfcct_b200.so"
 CLI = LIB_DIR / "fcct"  # command-line front end (csrc/cli.cpp), a client of the C ABI
-SOURCES = ["kernels.cu", "gemm_tc.cu", "host_stage.cpp", "orbit_fft.cu", "orbit_fft_host.cpp", "orbit16.cu", "orbit16_host.cpp", "orbit_big.cu", "orbit_big_host.cpp", "capi.cpp", "plan.cpp", "tiling.cpp", "plan_cache.cpp", "voxel_io.cpp"]
-HEADERS = ["kernels.hpp", "host_stage.hpp", "orbit_fft.hpp", "orbit16.hpp", "orbit_big.hpp", "device.cuh", "plan.hpp", "tiling.hpp", "plan_cache.hpp", "voxel_io.hpp"]
+SOURCES = ["kernels.cu", "gemm_tc.cu", "host_stage.cpp", "orbit_fft.cu", "orbit_fft_host.cpp", "orbit16.cu", "orbit16_host.cpp", "orbit_pat.cu", "orbit_pat_host.cpp", "orbit_big.cu", "orbit_big_host.cpp", "capi.cpp", "plan.cpp", "tiling.cpp", "plan_cache.cpp", "voxel_io.cpp"]
+HEADERS = ["kernels.hpp", "host_stage.hpp", "orbit_fft.hpp", "orbit16.hpp", "orbit_pat.hpp", "orbit_dev.cuh", "orbit_big.hpp", "device.cuh", "plan.hpp", "tiling.hpp", "plan_cache.hpp", "voxel_io.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3",

@@ -114,6 +114,7 @@ def lib() -> ctypes.CDLL:
         "fcct_debug_emulate_v2": (c_int, [c_int, c_double, c_double, c_double, c_int, c_void_p, c_void_p, c_int64]),
         "fcct_debug_emulate_orbit_fft": (c_int, [c_int, c_double, c_double, c_double, c_int, c_void_p, c_void_p, c_int64]),
         "fcct_debug_emulate_orbit16": (c_int, [c_int, c_double, c_double, c_double, c_int, c_void_p, c_void_p, c_int64]),
+        "fcct_debug_emulate_orbit_pat": (c_int, [c_int, c_double, c_double, c_double, c_int, c_void_p, c_void_p, c_int64, POINTER(c_int64)]),
         "fcct_debug_emulate_orbit_big": (c_int, [c_int, c_double, c_double, c_double, c_int, c_void_p, c_void_p, c_int64]),
         "fcct_debug_v2_stats": (c_int, [c_int, c_double, c_double, c_double, c_int, POINTER(c_int64)]),
         "fcct_debug_v2_entry_slots": (c_int, [c_int, c_double, c_double, c_double, c_int, c_int, POINTER(c_int32), c_int64, POINTER(c_int64)]),

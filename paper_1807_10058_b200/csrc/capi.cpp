@@ -18,6 +18,7 @@
 #include "../../include/fcct_gpu.h"
 #include "kernels.hpp"
 #include "orbit16.hpp"
+#include "orbit_pat.hpp"
 #include "orbit_big.hpp"
 #include "host_stage.hpp"
 #include "orbit_fft.hpp"
@@ -205,6 +206,44 @@ void upload_orbit16(const Orbit16Host& h, Orbit16Tables& out) {
     d.gather = static_cast<const int*>(bg->ptr);
     d.chunk_slots = static_cast<const int*>(bc->ptr);
     d.zperm = static_cast<const int*>(bz->ptr);
+    out.exec_flops = h.exec_flops();
+}
+
+// Single-pass orbit-pattern executor (n = 16, orbit_pat.hpp).
+struct OrbitPatTables {
+    OrbitPatDesc desc{};
+    std::vector<std::shared_ptr<DevBuf>> bufs;
+    double exec_flops = 0;
+};
+
+void upload_orbit_pat(const OrbitPatHost& h, OrbitPatTables& out) {
+    out = OrbitPatTables{};
+    OrbitPatDesc& d = out.desc;
+    d.n = h.n;
+    d.N = h.N;
+    d.dir = h.dir;
+    for (int c = 0; c < 2; ++c) {
+        d.cnt[c] = h.cnt[c];
+        d.ntiles[c] = h.ntiles[c];
+        if (h.op[c].empty()) continue;
+        auto bo = upload(h.op[c]), bl = upload(h.lam[c]);
+        out.bufs.insert(out.bufs.end(), {bo, bl});
+        d.op[c] = static_cast<const double2*>(bo->ptr);
+        d.lam[c] = static_cast<const double2*>(bl->ptr);
+    }
+    auto bi = upload(h.idx), bw = upload(h.warp_tiles);
+    out.bufs.insert(out.bufs.end(), {bi, bw});
+    d.idx = static_cast<const uint16_t*>(bi->ptr);
+    d.idx_count = static_cast<int>(h.idx.size());
+    d.warp_tiles = static_cast<const int2*>(bw->ptr);
+    d.nrare = static_cast<int>(h.rare_rows.size() / 2);
+    if (d.nrare > 0) {
+        auto br = upload(h.rare_rows), bn = upload(h.rare_in), bc = upload(h.rare_coef);
+        out.bufs.insert(out.bufs.end(), {br, bn, bc});
+        d.rare_rows = static_cast<const int2*>(br->ptr);
+        d.rare_in = static_cast<const uint16_t*>(bn->ptr);
+        d.rare_coef = static_cast<const double2*>(bc->ptr);
+    }
     out.exec_flops = h.exec_flops();
 }
 
@@ -644,6 +683,8 @@ struct fcct_plan_s {
     OrbitFftTables ofwd, ofinv;
     bool o16 = false;  // two-pass orbit-FFT executor (n = 16, orbit16.hpp)
     Orbit16Tables o16fwd, o16inv;
+    bool opat = false;  // single-pass orbit-pattern executor (n = 16, orbit_pat.hpp)
+    OrbitPatTables opfwd, opinv;
     bool obig = false;  // large-n orbit-FFT executor (n = 32, 64, fp64, orbit_big.hpp)
     OrbitBigTables obfwd, obinv;
     bool v2 = false;  // fp64 DMMA pipeline (tiling.hpp)
@@ -1106,7 +1147,7 @@ void build_orbit_fft(fcct_plan_s* pl) {
 void build_fast_paths(fcct_plan_s* pl) {
     const int x = pl->exec_force;
     const std::string f = x == FCCT_EXEC_AUTO                                   ? ""
-                          : x == FCCT_EXEC_ORBIT || x == FCCT_EXEC_ORBIT_PHASED ? "orbit"
+                          : x == FCCT_EXEC_ORBIT || x == FCCT_EXEC_ORBIT_PHASED || x == FCCT_EXEC_ORBIT_TWO_PASS ? "orbit"
                           : x == FCCT_EXEC_PIPELINE2                           ? "v2"
                           : x == FCCT_EXEC_TWO_LEVEL || x == FCCT_EXEC_TWO_LEVEL_V2 ? "two"
                           : x == FCCT_EXEC_TILE                                ? "v1"
@@ -1114,6 +1155,17 @@ void build_fast_paths(fcct_plan_s* pl) {
     const bool f32 = pl->precision == FCCT_F32;
     if (f.empty() || f == "orbit") build_orbit_fft(pl);
     if (pl->offt) return;
+    if ((f.empty() || f == "orbit") && x != FCCT_EXEC_ORBIT_TWO_PASS) {  // n = 16: one pass, block resident in shared memory
+        pl->opat = false;
+        OrbitPatHost hf, hi;
+        if (pl->n == 16 && tree_is_exact(pl) && compile_orbit_pat(pl->n, pl->p, false, hf) &&
+            compile_orbit_pat(pl->n, pl->p, true, hi)) {
+            upload_orbit_pat(hf, pl->opfwd);
+            upload_orbit_pat(hi, pl->opinv);
+            pl->opat = true;
+            return;
+        }
+    }
     if (f.empty() || f == "orbit") {  // n = 16: the two-pass orbit-FFT executor
         pl->o16 = false;
         Orbit16Host hf, hi;
@@ -1171,8 +1223,9 @@ void fill_info(fcct_plan_s* pl) {
     in.points = cube(pl->n);
     in.executor = !pl->radix ? (pl->tc32 ? 8 : (pl->oz64 ? 9 : 0))
                              : (pl->offt ? 5
+                                : (pl->opat ? 10
                                 : (pl->o16 ? 6
-                                : (pl->obig ? 7 : (pl->v2 ? 2 : (pl->two_level ? 4 : (pl->global ? 3 : 1))))));
+                                : (pl->obig ? 7 : (pl->v2 ? 2 : (pl->two_level ? 4 : (pl->global ? 3 : 1)))))));
     const double N = static_cast<double>(in.points);
     if (pl->radix) {
         in.levels = tree_levels(pl->n);
@@ -1190,6 +1243,10 @@ void fill_info(fcct_plan_s* pl) {
             in.exec_flops_forward = pl->o16fwd.exec_flops;
             in.exec_flops_inverse = pl->o16inv.exec_flops;
         }
+        if (pl->opat) {
+            in.exec_flops_forward = pl->opfwd.exec_flops;
+            in.exec_flops_inverse = pl->opinv.exec_flops;
+        }
         if (pl->obig) {
             in.exec_flops_forward = pl->obfwd.exec_flops;
             in.exec_flops_inverse = pl->obinv.exec_flops;
@@ -1205,6 +1262,8 @@ void fill_info(fcct_plan_s* pl) {
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->obfwd, &pl->obinv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+        for (auto* pt : {&pl->opfwd, &pl->opinv})
+            for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->gfwd, &pl->ginv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->rfwd, &pl->rinv})
@@ -1217,7 +1276,7 @@ void fill_info(fcct_plan_s* pl) {
         }
         in.table_bytes = bytes;
         int64_t fwd = 0;
-        for (auto* pt : {&pl->obfwd.bufs, &pl->gfwd.bufs, &pl->o16fwd.bufs, &pl->ofwd.bufs, &pl->fwd2.bufs})
+        for (auto* pt : {&pl->obfwd.bufs, &pl->gfwd.bufs, &pl->o16fwd.bufs, &pl->opfwd.bufs, &pl->ofwd.bufs, &pl->fwd2.bufs})
             for (auto& b : *pt) fwd += static_cast<int64_t>(b->bytes);
         in.table_bytes_forward = fwd;
     } else {
@@ -1235,7 +1294,7 @@ void fill_info(fcct_plan_s* pl) {
 
 fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int device,
                          PlanStore* store = nullptr, int executor = FCCT_EXEC_AUTO) {
-    if (executor < FCCT_EXEC_AUTO || executor > FCCT_EXEC_GLOBAL)
+    if (executor < FCCT_EXEC_AUTO || executor > FCCT_EXEC_ORBIT_TWO_PASS)
         throw FcctError(ST_INVALID_ARGUMENT, "unknown executor");
     if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "build_plan: n must be >= 1");
     if (method != FCCT_DIRECT && method != FCCT_FAST) throw FcctError(ST_INVALID_ARGUMENT, "unknown method");
@@ -1309,6 +1368,12 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
     if (pl->radix) {
         if (pl->two_level) {
             run_two_level(pl, inverse, in, f32 ? 1 : 0, out, f32 ? 1 : 0, batch, st);
+            return;
+        }
+        if (pl->opat) {
+            ck(launch_orbit_pat(inverse ? pl->opinv.desc : pl->opfwd.desc, f32 ? OF_C64 : OF_C128,
+                                f32 ? OF_C64 : OF_C128, in, out, batch, st, pl->num_sms),
+               "orbit-pattern executor");
             return;
         }
         if (pl->o16) {
@@ -1531,6 +1596,13 @@ void run_real(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t 
     if (pl->radix && pl->two_level) {
         const int cm = f32 ? 1 : 0, rm = f32 ? 3 : 2;
         run_two_level(pl, inverse, in, inverse ? cm : rm, out, inverse ? rm : cm, batch, st);
+        return;
+    }
+    if (pl->radix && pl->opat) {
+        const int cm = f32 ? OF_C64 : OF_C128, rm = f32 ? OF_R32 : OF_R64;
+        ck(launch_orbit_pat(inverse ? pl->opinv.desc : pl->opfwd.desc, inverse ? cm : rm, inverse ? rm : cm, in, out,
+                            batch, st, pl->num_sms),
+           "orbit-pattern executor (real I/O)");
         return;
     }
     if (pl->radix && pl->o16) {
@@ -1984,6 +2056,27 @@ fcct_status fcct_debug_emulate_orbit_big(int n, double r, double s, double t, in
         if (!compile_orbit_big(n, Params{r, s, t}, inverse != 0, h))
             throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by the large-n orbit-FFT executor");
         emulate_orbit_big(h, in, out, batch);
+    });
+}
+
+// Host emulation of the single-pass orbit-pattern executor's tables (n = 16, CPU
+// tests); stats (optional, 6 values): shapes, class sizes, DMMA count, modelled
+// shared-memory wavefronts of the gathers / scatters and their floor.
+fcct_status fcct_debug_emulate_orbit_pat(int n, double r, double s, double t, int inverse, const double* in,
+                                         double* out, int64_t batch, int64_t* stats) {
+    return guarded([&] {
+        OrbitPatHost h;
+        if (!compile_orbit_pat(n, Params{r, s, t}, inverse != 0, h))
+            throw FcctError(ST_INVALID_ARGUMENT, "plan not supported by the orbit-pattern executor");
+        if (stats) {
+            stats[0] = h.patterns;
+            stats[1] = h.cnt[0];
+            stats[2] = h.cnt[1];
+            stats[3] = h.dmma;
+            stats[4] = h.wavefronts;
+            stats[5] = h.wavefronts_floor;
+        }
+        if (batch > 0) emulate_orbit_pat(h, in, out, batch);
     });
 }
 

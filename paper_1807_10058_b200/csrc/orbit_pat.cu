@@ -1,0 +1,277 @@
+// Single-pass orbit-pattern executor (orbit_pat.hpp): one transform block per
+// CTA iteration, resident in a 64 KB shared tile from load to store — the base
+// change as a register-resident constant-operator DMMA over the block's own
+// orbits, in place, and the 16^3 radix-2 FFT in the same tile.
+#include <algorithm>
+
+#include "orbit_dev.cuh"
+#include "orbit_pat.hpp"
+
+namespace fcct {
+
+using namespace dev;
+using namespace odev;
+
+namespace {
+
+constexpr int kPatThreads = kPatWarps * 32;
+
+// One DMMA class: orbits of D members sharing the operator M (D x D complex).
+// MMA roles: A = data, 8 orbits x 4 members per k-step (lane: orbit lane / 4,
+// member 4 q + lane % 4); B = M^T fragments in registers (k = member, n = output
+// row); C[orbit][row]: this lane's rows 8 nt + 2 (lane % 4) + {0, 1}.
+// An orbit is read and written by this warp only, and every fragment of a tile
+// is loaded before its last DMMA issues, so the tile is updated in place.
+template <int D, int DIR, bool RIN, bool ROUT>
+__device__ __forceinline__ void pat_class(double2* X, const uint16_t* ix0, const double2* __restrict__ op,
+                                          const double2* __restrict__ lam, int first, int count, int cnt, int lane) {
+    constexpr int KT = D / 4, NT = (D + 7) / 8;
+    if (count == 0) return;
+    double br[KT][NT], bi[KT][NT];
+#pragma unroll
+    for (int q = 0; q < KT; ++q)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const double2 v = __ldg(op + (q * NT + nt) * 32 + lane);
+            br[q][nt] = v.x;
+            bi[q][nt] = v.y;
+        }
+    const int o = lane >> 2, k = lane & 3;
+    for (int t = first; t < first + count; ++t) {
+        const uint16_t* ix = ix0 + t * (D * 8);
+        double cr[NT][2], ci[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) cr[nt][0] = cr[nt][1] = ci[nt][0] = ci[nt][1] = 0.0;
+        double2 lf[NT][2];  // forward: Lambda of this lane's outputs, requested ahead of the chain
+        if constexpr (DIR == 0) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                lf[nt][0] = __ldg(lam + ((t * NT + nt) * 32 + lane) * 2);
+                lf[nt][1] = __ldg(lam + ((t * NT + nt) * 32 + lane) * 2 + 1);
+            }
+        }
+        double2 li[KT];  // inverse: 24 n^-3 conj(Lambda) of this lane's fragment elements
+        if constexpr (DIR == 1) {
+#pragma unroll
+            for (int q = 0; q < KT; ++q) li[q] = __ldg(lam + (t * KT + q) * 32 + lane);
+        }
+        double ar[KT], ai[KT];
+#pragma unroll
+        for (int q = 0; q < KT; ++q) {
+            const int slot = ix[(4 * q + k) * 8 + o];
+            if constexpr (RIN) {
+                ar[q] = X[slot].x;
+                ai[q] = 0.0;
+            } else {
+                const double2 v = X[slot];
+                ar[q] = v.x;
+                ai[q] = v.y;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < KT; ++q) {
+            double xr = ar[q], xi = ai[q];
+            if constexpr (DIR == 1) {
+                const double tr = fma(xr, li[q].x, -xi * li[q].y), ti = fma(xr, li[q].y, xi * li[q].x);
+                xr = tr;
+                xi = ti;
+            }
+            const double nxi = neg_hi16(xi);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                dmma884(cr[nt][0], cr[nt][1], xr, br[q][nt]);
+                if constexpr (!ROUT) dmma884(ci[nt][0], ci[nt][1], xr, bi[q][nt]);
+                if constexpr (!RIN) {
+                    dmma884(cr[nt][0], cr[nt][1], nxi, bi[q][nt]);
+                    if constexpr (!ROUT) dmma884(ci[nt][0], ci[nt][1], xi, br[q][nt]);
+                }
+            }
+        }
+        const bool valid = t * 8 + o < cnt;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = 8 * nt + 2 * k + e;
+                if ((D % 8 == 0 || row < D) && valid) {
+                    const int slot = ix[row * 8 + o];
+                    const double vr = cr[nt][e], vi = ci[nt][e];
+                    if constexpr (DIR == 0) {
+                        const double2 l = lf[nt][e];
+                        X[slot] = make_double2(fma(vr, l.x, -vi * l.y), fma(vr, l.y, vi * l.x));
+                    } else if constexpr (ROUT) {
+                        X[slot].x = vr;
+                    } else {
+                        X[slot] = make_double2(vr, vi);
+                    }
+                }
+            }
+    }
+}
+
+template <int DIR, int MI, int MO>
+__global__ void __launch_bounds__(kPatThreads, 3)
+    orbit_pat_kernel(const __grid_constant__ OrbitPatDesc d, const void* __restrict__ in, void* __restrict__ out,
+                     int64_t batch) {
+    constexpr int NN = 16, N = NN * NN * NN, SIGN = DIR == 0 ? +1 : -1;
+    constexpr bool RIN = DIR == 0 && (MI == OF_R64 || MI == OF_R32);
+    constexpr bool ROUT = DIR == 1 && (MO == OF_R64 || MO == OF_R32);
+    extern __shared__ __align__(128) unsigned char smem[];
+    double2* X = reinterpret_cast<double2*>(smem);
+    uint16_t* ix_s = reinterpret_cast<uint16_t*>(smem + N * 16);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int i = tid; i < d.idx_count / 2; i += kPatThreads)
+        reinterpret_cast<uint32_t*>(ix_s)[i] = __ldg(reinterpret_cast<const uint32_t*>(d.idx) + i);
+    const int2 wa = __ldg(d.warp_tiles + warp), wb = __ldg(d.warp_tiles + kPatWarps + warp);
+    // this thread's rare rows (SIMT)
+    int2 rr[kPatMaxRare];
+#pragma unroll
+    for (int u = 0; u < kPatMaxRare; ++u)
+        rr[u] = tid + u * kPatThreads < d.nrare ? __ldg(d.rare_rows + tid + u * kPatThreads) : make_int2(0, 0);
+    __syncthreads();
+    constexpr int64_t in_row = int64_t{N} * eb_of(MI), out_row = int64_t{N} * eb_of(MO);
+    auto swz = [](int i, int j, int k) { return (i * NN + j) * NN + (k ^ j); };
+    for (int64_t blk = blockIdx.x; blk < batch; blk += gridDim.x) {
+        const char* src = static_cast<const char*>(in) + blk * in_row;
+        char* dst = static_cast<char*>(out) + blk * out_row;
+#pragma unroll 8
+        for (int a = tid; a < N; a += kPatThreads) {
+            if constexpr (MI == OF_C128) {
+                cp_async_n<16>(X + pat_slot(a), src + static_cast<int64_t>(a) * 16, true);
+            } else if constexpr (MI == OF_R64) {
+                cp_async_n<8>(&X[pat_slot(a)].x, src + static_cast<int64_t>(a) * 8, true);
+            } else {
+                double re, im;
+                ld_el<MI>(src, a, re, im);
+                X[pat_slot(a)] = make_double2(re, im);
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        double2 v[NN];
+        auto pass = [&](auto at) {  // one in-place line pass: two lines per thread
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
+#pragma unroll
+                for (int x = 0; x < NN; ++x) v[x] = X[at(hi, lo, x)];
+                fft_line16<NN, SIGN>(v);
+#pragma unroll
+                for (int x = 0; x < NN; ++x) X[at(hi, lo, x)] = v[x];
+            }
+            __syncthreads();
+        };
+        if constexpr (DIR == 1) {
+            pass([&](int hi, int lo, int x) { return swz(x, hi, lo); });
+            pass([&](int hi, int lo, int x) { return swz(hi, x, lo); });
+            pass([&](int hi, int lo, int x) { return swz(hi, lo, x); });
+        }
+        // base change, in place
+        double2 racc[kPatMaxRare];
+#pragma unroll
+        for (int u = 0; u < kPatMaxRare; ++u) {
+            racc[u] = make_double2(0.0, 0.0);
+            const int terms = rr[u].x >> 16;
+            for (int t = 0; t < terms; ++t) {
+                const double2 c = __ldg(d.rare_coef + rr[u].y + t);
+                const int slot = __ldg(d.rare_in + rr[u].y + t);
+                if constexpr (RIN) {
+                    const double xr = X[slot].x;
+                    racc[u].x = fma(c.x, xr, racc[u].x);
+                    racc[u].y = fma(c.y, xr, racc[u].y);
+                } else {
+                    const double2 x = X[slot];
+                    racc[u].x = fma(c.x, x.x, racc[u].x);
+                    racc[u].x = fma(-c.y, x.y, racc[u].x);
+                    racc[u].y = fma(c.x, x.y, racc[u].y);
+                    racc[u].y = fma(c.y, x.x, racc[u].y);
+                }
+            }
+        }
+        pat_class<24, DIR, RIN, ROUT>(X, ix_s, d.op[0], d.lam[0], wa.x, wa.y, d.cnt[0], lane);
+        pat_class<12, DIR, RIN, ROUT>(X, ix_s + d.ntiles[0] * (24 * 8), d.op[1], d.lam[1], wb.x, wb.y, d.cnt[1], lane);
+        __syncthreads();  // the rare rows have been read by everyone
+#pragma unroll
+        for (int u = 0; u < kPatMaxRare; ++u)
+            if ((rr[u].x >> 16) != 0) X[rr[u].x & 0xFFFF] = racc[u];
+        __syncthreads();
+        if constexpr (DIR == 0) {
+            pass([&](int hi, int lo, int x) { return swz(hi, lo, x); });
+            pass([&](int hi, int lo, int x) { return swz(hi, x, lo); });
+            // i axis, stored to HBM from registers (lanes vary k: coalesced)
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
+#pragma unroll
+                for (int x = 0; x < NN; ++x) v[x] = X[swz(x, hi, lo)];
+                fft_line16<NN, SIGN>(v);
+#pragma unroll
+                for (int x = 0; x < NN; ++x) st_el<MO>(dst, (x * NN + hi) * NN + lo, v[x].x, v[x].y);
+            }
+        } else {
+#pragma unroll 8
+            for (int a = tid; a < N; a += kPatThreads) {
+                const double2 r = X[pat_slot(a)];
+                st_el<MO>(dst, a, r.x, r.y);
+            }
+        }
+        __syncthreads();  // the tile is refilled by the next block
+    }
+}
+
+template <int DIR, int MI, int MO>
+cudaError_t launch_pat(const OrbitPatDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st, int num_sms) {
+    const int smem = 16 * 16 * 16 * 16 + ((d.idx_count * 2 + 15) / 16) * 16;
+    auto kern = orbit_pat_kernel<DIR, MI, MO>;
+    static thread_local int prepared = -1;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (prepared != dev) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        prepared = dev;
+    }
+    kern<<<static_cast<unsigned>(std::min<int64_t>(batch, 3 * static_cast<int64_t>(num_sms))), kPatThreads, smem, st>>>(
+        d, in, out, batch);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_orbit_pat(const OrbitPatDesc& d, int in_mode, int out_mode, const void* in, void* out,
+                             int64_t batch, cudaStream_t st, int num_sms) {
+    if (batch <= 0) return cudaSuccess;
+    if (d.n != 16 || d.nrare > kPatMaxRare * kPatThreads) return cudaErrorInvalidValue;
+    if (d.dir == 0) {
+        if (out_mode == OF_C128) switch (in_mode) {
+                case OF_C128: return launch_pat<0, OF_C128, OF_C128>(d, in, out, batch, st, num_sms);
+                case OF_C64: return launch_pat<0, OF_C64, OF_C128>(d, in, out, batch, st, num_sms);
+                case OF_R64: return launch_pat<0, OF_R64, OF_C128>(d, in, out, batch, st, num_sms);
+                case OF_R32: return launch_pat<0, OF_R32, OF_C128>(d, in, out, batch, st, num_sms);
+            }
+        if (out_mode == OF_C64) switch (in_mode) {
+                case OF_C128: return launch_pat<0, OF_C128, OF_C64>(d, in, out, batch, st, num_sms);
+                case OF_C64: return launch_pat<0, OF_C64, OF_C64>(d, in, out, batch, st, num_sms);
+                case OF_R64: return launch_pat<0, OF_R64, OF_C64>(d, in, out, batch, st, num_sms);
+                case OF_R32: return launch_pat<0, OF_R32, OF_C64>(d, in, out, batch, st, num_sms);
+            }
+    } else {
+        if (in_mode == OF_C128) switch (out_mode) {
+                case OF_C128: return launch_pat<1, OF_C128, OF_C128>(d, in, out, batch, st, num_sms);
+                case OF_C64: return launch_pat<1, OF_C128, OF_C64>(d, in, out, batch, st, num_sms);
+                case OF_R64: return launch_pat<1, OF_C128, OF_R64>(d, in, out, batch, st, num_sms);
+                case OF_R32: return launch_pat<1, OF_C128, OF_R32>(d, in, out, batch, st, num_sms);
+            }
+        if (in_mode == OF_C64) switch (out_mode) {
+                case OF_C128: return launch_pat<1, OF_C64, OF_C128>(d, in, out, batch, st, num_sms);
+                case OF_C64: return launch_pat<1, OF_C64, OF_C64>(d, in, out, batch, st, num_sms);
+                case OF_R64: return launch_pat<1, OF_C64, OF_R64>(d, in, out, batch, st, num_sms);
+                case OF_R32: return launch_pat<1, OF_C64, OF_R32>(d, in, out, batch, st, num_sms);
+            }
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace fcct

@@ -1,0 +1,87 @@
+// Single-pass orbit-pattern executor for n = 16 (executor 10): D_n(p) = F_n S_n(p)
+// with one transform block resident in shared memory from load to store.
+//
+// The orbit blocks of S_n(p) (ColumnEvaluator's symmetrised plane waves,
+// transform.cpp:46-68, restated in orbit_fft.hpp) come in very few shapes.
+// List an orbit's members in group order from its lexicographically smallest
+// member k0 (member r = g_r k0 mod n, first appearance), and split off the
+// separable phase of the reduced index,
+//     S_O = diag(Lambda[a_r]) M,  Lambda[a] = e^{2 pi i a.p/n} / 24,
+// then M holds only the carry phases e^{2 pi i t.p} (g k = a + n t) and is the
+// SAME matrix for every free orbit (24 members), and one of two matrices for the
+// 12-member orbits, ... : 8 distinct M for any n and p (measured n = 8..32).
+// So the base change of a block is a GEMM with a constant 24 x 24 (and a
+// 12 x 12) complex operator over the block's OWN orbits:
+//   - the operator lives in registers as DMMA m8n8k4 B fragments (36 doubles);
+//   - the M dimension of the MMA is 8 orbits of the same block, so a CTA needs
+//     one block (64 KB complex128), not 8 — the block stays in shared memory,
+//     the base change runs in place (an orbit is read and written by one warp),
+//     and the 16^3 FFT follows (forward) or precedes (inverse) it in the same
+//     tile. HBM sees every sample once: no z round trip (orbit16.hpp moves z
+//     through HBM twice), no operator stream from L2, no tile metadata;
+//   - Lambda (forward: on the accumulators; inverse: 24 n^-3 conj(Lambda) on
+//     the loaded fragments) is a 64 KB table in fragment order, L2 resident;
+//   - the few orbits of the rare shapes (28 of 245 at n = 16) are SIMT rows.
+// Real samples in (forward) and out (inverse) halve the DMMA count.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+namespace fcct {
+
+struct Params;
+
+constexpr int kPatWarps = 4;     // warps per CTA (three CTAs per SM)
+constexpr int kPatMaxRare = 2;   // rare rows per thread
+
+// physical slot of Fourier / sample index a = (i, j, k) in the shared tile:
+// (i, j, k ^ j) — the k, j and i line passes of the FFT are conflict-free
+__host__ __device__ constexpr int pat_slot(int a) { return (a & ~15) | ((a ^ (a >> 4)) & 15); }
+
+struct OrbitPatDesc {
+    int n = 0, N = 0, dir = 0;
+    int cnt[2] = {0, 0};      // orbits of the two DMMA classes (24 and 12 members)
+    int ntiles[2] = {0, 0};   // tiles of 8 orbits
+    int idx_count = 0;        // uint16 entries of idx (copied to shared memory)
+    int nrare = 0;            // SIMT rows
+    const double2* op[2] = {nullptr, nullptr};   // [q][nt][32] B fragments (Re, Im) of M (or M^-1)
+    const double2* lam[2] = {nullptr, nullptr};  // forward [tile][nt][32][2]; inverse [tile][q][32]
+    const uint16_t* idx = nullptr;               // class 0: [tile][24][8], then class 1: [tile][12][8] slots
+    const int2* warp_tiles = nullptr;            // [2][kPatWarps]: (first tile, tiles) of a warp per class
+    const int2* rare_rows = nullptr;             // [nrare]: (out slot | terms << 16, first term)
+    const uint16_t* rare_in = nullptr;           // [terms] slots
+    const double2* rare_coef = nullptr;          // [terms]
+};
+
+struct OrbitPatHost {
+    int n = 0, N = 0, dir = 0;
+    int cnt[2] = {0, 0}, ntiles[2] = {0, 0};
+    std::vector<double> op[2], lam[2];
+    std::vector<uint16_t> idx;
+    std::vector<int32_t> warp_tiles;  // [2][kPatWarps][2]
+    std::vector<int32_t> rare_rows;   // [nrare][2]
+    std::vector<uint16_t> rare_in;
+    std::vector<double> rare_coef;
+    int patterns = 0;                 // distinct shapes found
+    int64_t dmma = 0;                 // complex-input DMMA count per block
+    double exec_flops() const;        // FP64-pipe flops per block (complex in / out)
+    // modelled shared-memory wavefronts per block of the fragment gathers and
+    // result scatters (16-byte accesses, quarter-warps), and their conflict-free floor
+    int64_t wavefronts = 0, wavefronts_floor = 0;
+};
+
+// Compiles S_n(p) (forward) or S_n(p)^{-1} / n^3 (inverse); false when n is not
+// 16, an orbit block is singular or the shapes do not fit the kernel.
+bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h);
+
+// Host emulation on the compiled tables, complex128 rows (CPU tests).
+void emulate_orbit_pat(const OrbitPatHost& h, const double* in, double* out, int64_t batch);
+
+// in / out modes as OfMode (orbit_fft.hpp).
+cudaError_t launch_orbit_pat(const OrbitPatDesc& d, int in_mode, int out_mode, const void* in, void* out,
+                             int64_t batch, cudaStream_t st, int num_sms);
+
+}  // namespace fcct

@@ -1,0 +1,359 @@
+// Host side of the single-pass orbit-pattern executor (orbit_pat.hpp): the
+// orbit blocks of S_n(p) classified by shape, the two big shapes compiled into
+// DMMA fragment tables, the rare ones into SIMT rows.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <complex>
+#include <numbers>
+
+#include "orbit_pat.hpp"
+#include "plan.hpp"
+
+namespace fcct {
+
+namespace {
+
+using cd = std::complex<double>;
+
+struct Shape {
+    int d = 0;
+    std::vector<cld> M, Minv;  // d x d row-major, members in group order
+    std::vector<int> orbits;
+};
+
+long double max_diff(const std::vector<cld>& a, const std::vector<cld>& b) {
+    long double m = 0;
+    for (size_t i = 0; i < a.size(); ++i) m = std::max(m, std::abs(a[i] - b[i]));
+    return m;
+}
+
+// wavefronts of one 16-byte access per lane: quarter-warps of 8 lanes, 8 bank
+// groups of 16 bytes; equal addresses are one broadcast
+int wavefronts16(const std::array<int, 32>& slot, const std::array<bool, 32>& on) {
+    int total = 0;
+    for (int h = 0; h < 4; ++h) {
+        int worst = 0;
+        bool any = false;
+        for (int bg = 0; bg < 8; ++bg) {
+            std::array<int, 8> seen{};
+            int ns = 0;
+            for (int l = 8 * h; l < 8 * h + 8; ++l) {
+                if (!on[l] || (slot[l] & 7) != bg) continue;
+                any = true;
+                if (std::find(seen.begin(), seen.begin() + ns, slot[l]) == seen.begin() + ns) seen[ns++] = slot[l];
+            }
+            worst = std::max(worst, ns);
+        }
+        total += any ? worst : 0;
+    }
+    return total;
+}
+
+}  // namespace
+
+bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
+    if (n != 16) return false;
+    const int N = static_cast<int>(cube(n));
+    OrbitBlocks ob = orbit_blocks(n, p);
+    if (!std::isfinite(ob.worst_condition)) return false;
+    const Orbits& orb = *ob.orb;
+    const auto& grp = s4_group();
+    const long double pr = p.r, ps = p.s, pt = p.t;
+    auto lam = [&](int a) {  // Lambda[a] = e^{2 pi i a.p/n} / 24
+        const int i = a / (n * n), j = (a / n) % n, k = a % n;
+        return unit_phase_ld((pr * i + ps * j + pt * k) / n) / 24.0L;
+    };
+    const int norb = static_cast<int>(orb.members.size());
+    // members in group order from the smallest member
+    std::vector<std::vector<int>> L(norb);
+    std::vector<Shape> shapes;
+    for (int o = 0; o < norb; ++o) {
+        const auto& mem = orb.members[o];
+        const int d = static_cast<int>(mem.size());
+        const int a0 = mem[0];
+        const int k0[3] = {a0 / (n * n), (a0 / n) % n, a0 % n};
+        for (const auto& w : grp) {
+            int b[3];
+            for (int i = 0; i < 3; ++i) {
+                const int v = w[3 * i] * k0[0] + w[3 * i + 1] * k0[1] + w[3 * i + 2] * k0[2];
+                b[i] = ((v % n) + n) % n;
+            }
+            const int a = (b[0] * n + b[1]) * n + b[2];
+            if (std::find(L[o].begin(), L[o].end(), a) == L[o].end()) L[o].push_back(a);
+        }
+        if (static_cast<int>(L[o].size()) != d) return false;
+        std::vector<cld> M(static_cast<size_t>(d) * d), Mi(static_cast<size_t>(d) * d);
+        for (int r = 0; r < d; ++r)
+            for (int c = 0; c < d; ++c) {
+                const size_t src = static_cast<size_t>(orb.pos[L[o][r]]) * d + orb.pos[L[o][c]];
+                M[static_cast<size_t>(r) * d + c] = ob.S[o][src] / lam(L[o][r]);
+                Mi[static_cast<size_t>(r) * d + c] = ob.Sinv[o][src] * lam(L[o][c]);
+            }
+        bool found = false;
+        for (Shape& s : shapes)
+            if (s.d == d && max_diff(s.M, M) < 1e-12L && max_diff(s.Minv, Mi) < 1e-10L) {
+                s.orbits.push_back(o);
+                found = true;
+                break;
+            }
+        if (!found) shapes.push_back(Shape{d, std::move(M), std::move(Mi), {o}});
+    }
+    h = OrbitPatHost{};
+    h.n = n;
+    h.N = N;
+    h.dir = inverse ? 1 : 0;
+    h.patterns = static_cast<int>(shapes.size());
+    // DMMA classes: the most populated shape of 24 and of 12 members
+    const int cls_d[2] = {24, 12};
+    int cls[2] = {-1, -1};
+    for (int c = 0; c < 2; ++c)
+        for (size_t s = 0; s < shapes.size(); ++s)
+            if (shapes[s].d == cls_d[c] && (cls[c] < 0 || shapes[s].orbits.size() > shapes[cls[c]].orbits.size()))
+                cls[c] = static_cast<int>(s);
+    if (cls[0] < 0) return false;
+    std::vector<char> in_class(norb, 0);
+    for (int c = 0; c < 2; ++c) {
+        if (cls[c] < 0) continue;
+        h.cnt[c] = static_cast<int>(shapes[cls[c]].orbits.size());
+        h.ntiles[c] = (h.cnt[c] + 7) / 8;
+        for (int o : shapes[cls[c]].orbits) in_class[o] = 1;
+    }
+    const long double inv_scale = 1.0L / N;
+    for (int c = 0; c < 2; ++c) {
+        if (cls[c] < 0) continue;
+        const Shape& sh = shapes[cls[c]];
+        const int d = sh.d, KT = d / 4, NT = (d + 7) / 8;
+        const std::vector<cld>& M = inverse ? sh.Minv : sh.M;
+        h.op[c].assign(static_cast<size_t>(KT) * NT * 32 * 2, 0.0);
+        for (int q = 0; q < KT; ++q)
+            for (int nt = 0; nt < NT; ++nt)
+                for (int l = 0; l < 32; ++l) {
+                    const int row = 8 * nt + l / 4, col = 4 * q + l % 4;
+                    const cld v = row < d ? M[static_cast<size_t>(row) * d + col] : cld{0, 0};
+                    h.op[c][((static_cast<size_t>(q) * NT + nt) * 32 + l) * 2] = static_cast<double>(v.real());
+                    h.op[c][((static_cast<size_t>(q) * NT + nt) * 32 + l) * 2 + 1] = static_cast<double>(v.imag());
+                }
+        const int T = h.ntiles[c];
+        auto orbit_at = [&](int t, int o) {  // padding slots of the last tile repeat its first orbit
+            const int i = t * 8 + o;
+            return sh.orbits[i < h.cnt[c] ? i : t * 8];
+        };
+        for (int t = 0; t < T; ++t)
+            for (int m = 0; m < d; ++m)
+                for (int o = 0; o < 8; ++o) h.idx.push_back(static_cast<uint16_t>(pat_slot(L[orbit_at(t, o)][m])));
+        if (!inverse) {
+            h.lam[c].assign(static_cast<size_t>(T) * NT * 32 * 2 * 2, 0.0);
+            for (int t = 0; t < T; ++t)
+                for (int nt = 0; nt < NT; ++nt)
+                    for (int l = 0; l < 32; ++l)
+                        for (int e = 0; e < 2; ++e) {
+                            const int row = 8 * nt + 2 * (l % 4) + e;
+                            if (row >= d) continue;
+                            const cld v = lam(L[orbit_at(t, l / 4)][row]);
+                            const size_t at = (((static_cast<size_t>(t) * NT + nt) * 32 + l) * 2 + e) * 2;
+                            h.lam[c][at] = static_cast<double>(v.real());
+                            h.lam[c][at + 1] = static_cast<double>(v.imag());
+                        }
+        } else {
+            h.lam[c].assign(static_cast<size_t>(T) * KT * 32 * 2, 0.0);
+            for (int t = 0; t < T; ++t)
+                for (int q = 0; q < KT; ++q)
+                    for (int l = 0; l < 32; ++l) {
+                        const cld v = inv_scale / lam(L[orbit_at(t, l / 4)][4 * q + l % 4]);
+                        const size_t at = ((static_cast<size_t>(t) * KT + q) * 32 + l) * 2;
+                        h.lam[c][at] = static_cast<double>(v.real());
+                        h.lam[c][at + 1] = static_cast<double>(v.imag());
+                    }
+        }
+        h.dmma += static_cast<int64_t>(T) * KT * NT * 4;
+        // shared-memory conflict model of the gathers and scatters
+        for (int t = 0; t < T; ++t) {
+            std::array<int, 32> slot{};
+            std::array<bool, 32> on{};
+            for (int q = 0; q < KT; ++q) {
+                for (int l = 0; l < 32; ++l) {
+                    slot[l] = pat_slot(L[orbit_at(t, l / 4)][4 * q + l % 4]);
+                    on[l] = true;
+                }
+                h.wavefronts += wavefronts16(slot, on);
+                h.wavefronts_floor += 4;
+            }
+            for (int nt = 0; nt < NT; ++nt)
+                for (int e = 0; e < 2; ++e) {
+                    int live = 0;
+                    for (int l = 0; l < 32; ++l) {
+                        const int row = 8 * nt + 2 * (l % 4) + e;
+                        on[l] = row < d && t * 8 + l / 4 < h.cnt[c];
+                        slot[l] = on[l] ? pat_slot(L[orbit_at(t, l / 4)][row]) : 0;
+                        live += on[l];
+                    }
+                    h.wavefronts += wavefronts16(slot, on);
+                    h.wavefronts_floor += (live + 7) / 8;
+                }
+        }
+    }
+    // tiles to warps: class 0 round robin, class 1 to the least loaded warp
+    {
+        int na[kPatWarps] = {}, nb[kPatWarps] = {}, load[kPatWarps] = {};
+        for (int t = 0; t < h.ntiles[0]; ++t) {
+            ++na[t % kPatWarps];
+            load[t % kPatWarps] += 72;
+        }
+        for (int t = 0; t < h.ntiles[1]; ++t) {
+            const int w = static_cast<int>(std::min_element(load, load + kPatWarps) - load);
+            ++nb[w];
+            load[w] += 24;
+        }
+        h.warp_tiles.assign(2 * kPatWarps * 2, 0);
+        int fa = 0, fb = 0;
+        for (int w = 0; w < kPatWarps; ++w) {
+            h.warp_tiles[(0 * kPatWarps + w) * 2] = fa;
+            h.warp_tiles[(0 * kPatWarps + w) * 2 + 1] = na[w];
+            h.warp_tiles[(1 * kPatWarps + w) * 2] = fb;
+            h.warp_tiles[(1 * kPatWarps + w) * 2 + 1] = nb[w];
+            fa += na[w];
+            fb += nb[w];
+        }
+    }
+    // rare shapes: one SIMT row per output member, full S / S^-1 n^-3 entries
+    for (int o = 0; o < norb; ++o) {
+        if (in_class[o]) continue;
+        const auto& mem = orb.members[o];
+        const int d = static_cast<int>(mem.size());
+        const std::vector<cld>& M = inverse ? ob.Sinv[o] : ob.S[o];
+        for (int r = 0; r < d; ++r) {
+            const int first = static_cast<int>(h.rare_in.size());
+            int terms = 0;
+            for (int c = 0; c < d; ++c) {
+                const cld v = M[static_cast<size_t>(r) * d + c] * (inverse ? inv_scale : 1.0L);
+                if (v == cld{0, 0}) continue;
+                h.rare_in.push_back(static_cast<uint16_t>(pat_slot(mem[c])));
+                h.rare_coef.push_back(static_cast<double>(v.real()));
+                h.rare_coef.push_back(static_cast<double>(v.imag()));
+                ++terms;
+            }
+            h.rare_rows.push_back(pat_slot(mem[r]) | (terms << 16));
+            h.rare_rows.push_back(first);
+        }
+    }
+    if (static_cast<int>(h.rare_rows.size() / 2) > kPatMaxRare * kPatWarps * 32) return false;
+    if (h.idx.size() * 2 > 10 * 1024) return false;  // the slot lists share the CTA's shared memory with the tile
+    return true;
+}
+
+double OrbitPatHost::exec_flops() const {
+    int lg = 0;
+    while ((1 << lg) < n) ++lg;
+    double twiddles = 0;
+    for (int half = n / 2; half >= 1; half /= 2)
+        for (int j = 0; j < half; ++j) {
+            const int e = j * (n / (2 * half));
+            if (e != 0 && 4 * e != n) twiddles += n / (2 * half);
+        }
+    const double fft = 3.0 * n * n * ((n / 2.0) * lg * 4.0 + 6.0 * twiddles);
+    return static_cast<double>(dmma) * 512.0 + fft + 8.0 * static_cast<double>(rare_in.size()) + 6.0 * N;
+}
+
+namespace {
+
+void dft3(std::vector<cd>& buf, int n, int sign) {
+    std::vector<cd> line(n), res(n);
+    for (int axis = 0; axis < 3; ++axis)
+        for (int u = 0; u < n; ++u)
+            for (int v = 0; v < n; ++v) {
+                auto at = [&](int x) {
+                    int ijk[3];
+                    ijk[axis] = x;
+                    ijk[axis == 0 ? 1 : 0] = u;
+                    ijk[axis == 2 ? 1 : 2] = v;
+                    return (ijk[0] * n + ijk[1]) * n + ijk[2];
+                };
+                for (int x = 0; x < n; ++x) line[x] = buf[at(x)];
+                for (int q = 0; q < n; ++q) {
+                    cd acc{0, 0};
+                    for (int x = 0; x < n; ++x) {
+                        const double ang = sign * 2.0 * std::numbers::pi * ((x * q) % n) / n;
+                        acc += line[x] * cd{std::cos(ang), std::sin(ang)};
+                    }
+                    res[q] = acc;
+                }
+                for (int x = 0; x < n; ++x) buf[at(x)] = res[x];
+            }
+}
+
+// the base change on the tile X (physical slots), as the kernel indexes its tables
+void base_change(const OrbitPatHost& h, std::vector<cd>& X) {
+    const int nrare = static_cast<int>(h.rare_rows.size() / 2);
+    std::vector<cd> rare(nrare);
+    for (int r = 0; r < nrare; ++r) {
+        const int terms = h.rare_rows[2 * r] >> 16, first = h.rare_rows[2 * r + 1];
+        cd acc{0, 0};
+        for (int t = 0; t < terms; ++t)
+            acc += cd{h.rare_coef[2 * (first + t)], h.rare_coef[2 * (first + t) + 1]} * X[h.rare_in[first + t]];
+        rare[r] = acc;
+    }
+    size_t idx_base = 0;
+    const int cls_d[2] = {24, 12};
+    for (int c = 0; c < 2; ++c) {
+        const int d = cls_d[c], KT = d / 4, NT = (d + 7) / 8;
+        for (int w = 0; w < kPatWarps; ++w) {
+            const int first = h.warp_tiles[(c * kPatWarps + w) * 2], count = h.warp_tiles[(c * kPatWarps + w) * 2 + 1];
+            for (int t = first; t < first + count; ++t) {
+                const uint16_t* ix = h.idx.data() + idx_base + static_cast<size_t>(t) * d * 8;
+                cd acc[8][24];
+                for (int o = 0; o < 8; ++o)
+                    for (int nt = 0; nt < NT; ++nt)
+                        for (int nl = 0; nl < 8; ++nl) {
+                            cd s{0, 0};
+                            for (int q = 0; q < KT; ++q)
+                                for (int k = 0; k < 4; ++k) {
+                                    cd a = X[ix[(4 * q + k) * 8 + o]];
+                                    if (h.dir == 1) {
+                                        const size_t at = ((static_cast<size_t>(t) * KT + q) * 32 + o * 4 + k) * 2;
+                                        a *= cd{h.lam[c][at], h.lam[c][at + 1]};
+                                    }
+                                    const size_t ot = ((static_cast<size_t>(q) * NT + nt) * 32 + nl * 4 + k) * 2;
+                                    s += a * cd{h.op[c][ot], h.op[c][ot + 1]};
+                                }
+                            acc[o][8 * nt + nl] = s;
+                        }
+                for (int o = 0; o < 8; ++o) {
+                    if (t * 8 + o >= h.cnt[c]) continue;
+                    for (int row = 0; row < d; ++row) {
+                        cd v = acc[o][row];
+                        if (h.dir == 0) {
+                            const int nt = row / 8, kk = (row % 8) / 2, e = row % 2;
+                            const size_t at = (((static_cast<size_t>(t) * NT + nt) * 32 + o * 4 + kk) * 2 + e) * 2;
+                            v *= cd{h.lam[c][at], h.lam[c][at + 1]};
+                        }
+                        X[ix[row * 8 + o]] = v;
+                    }
+                }
+            }
+        }
+        idx_base += static_cast<size_t>(h.ntiles[c]) * d * 8;
+    }
+    for (int r = 0; r < nrare; ++r) X[h.rare_rows[2 * r] & 0xFFFF] = rare[r];
+}
+
+}  // namespace
+
+void emulate_orbit_pat(const OrbitPatHost& h, const double* in, double* out, int64_t batch) {
+    const int N = h.N;
+    std::vector<cd> x(N), X(N);
+    for (int64_t b = 0; b < batch; ++b) {
+        for (int a = 0; a < N; ++a) x[a] = cd{in[2 * (b * N + a)], in[2 * (b * N + a) + 1]};
+        if (h.dir == 1) dft3(x, h.n, -1);
+        for (int a = 0; a < N; ++a) X[pat_slot(a)] = x[a];
+        base_change(h, X);
+        for (int a = 0; a < N; ++a) x[a] = X[pat_slot(a)];
+        if (h.dir == 0) dft3(x, h.n, +1);
+        for (int a = 0; a < N; ++a) {
+            out[2 * (b * N + a)] = x[a].real();
+            out[2 * (b * N + a) + 1] = x[a].imag();
+        }
+    }
+}
+
+}  // namespace fcct

@@ -656,15 +656,19 @@ def test_orbit_fft_full_batch_properties(cuda, oracle_mod):
     assert float(torch.linalg.norm(ya - lin) / torch.linalg.norm(lin)) <= F64_TOL
 
 
+@pytest.mark.parametrize("exe,eid", [("auto", 10), ("orbit-two-pass", 6)])
 @pytest.mark.parametrize("p", [CANON, SkewParams(0.21, 0.055, 0.4), SkewParams(0.37, 0.61, 0.085)])
-def test_n16_two_pass_orbit_fft(cuda, oracle_mod, p):
-    """n = 16 on the two-pass orbit-FFT executor (executor 6: S_16(p) on the
-    FP64 tensor pipe over gathered 8-block chunks, then the 16^3 FFT) against
-    the FFT / orbit-route oracle, ragged batch; fp32 I/O; fused real I/O
-    bitwise equal to the complex path; host buffers; acceptance #7 node rows."""
+def test_n16_orbit_executors(cuda, oracle_mod, p, exe, eid):
+    """n = 16 on the single-pass orbit-pattern executor (executor 10, the default:
+    the block resident in shared memory, S_16(p) as a constant-operator DMMA over
+    the block's own orbits, then the 16^3 FFT in the same tile) and on the
+    two-pass orbit-FFT executor (executor 6: S_16(p) over gathered 8-block
+    chunks, z through HBM, then the 16^3 FFT) against the FFT / orbit-route
+    oracle, ragged batch; fp32 I/O; fused real I/O bitwise equal to the complex
+    path; host buffers; acceptance #7 node rows."""
     n = 16
-    plan = build_plan(n, p)
-    assert plan.info.executor == 6
+    plan = build_plan(n, p, executor=exe)
+    assert plan.info.executor == eid
     route = oracle_mod.OrbitRoute(n, tup(p))
     x = rand_batch(n, 11, seed=61)  # ragged: 8 + 3 blocks
     y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values
@@ -696,8 +700,8 @@ def test_n16_two_pass_orbit_fft(cuda, oracle_mod, p):
     torch.cuda.synchronize()
     assert torch.equal(buf[1:].view(yr.shape[0], n**3), xr_back)
     # fp32 I/O (complex64 in HBM, fp64 arithmetic)
-    p32 = build_plan(n, p, precision="f32")
-    assert p32.info.executor == 6
+    p32 = build_plan(n, p, precision="f32", executor=exe)
+    assert p32.info.executor == eid
     y32 = fast_apply(p32, SignalTensor(n, torch.from_numpy(x).to(torch.complex64).to(cuda))).values
     assert rel(y32.cpu().numpy(), y_ref) <= F32_TOL
     b32 = inverse_apply(p32, Spectrum(n, p, y32)).data
@@ -736,7 +740,7 @@ def test_scratch_executors_concurrent_streams(cuda, n):
     order concurrent calls on different streams on the device (a per-plan
     event, no host sync): two forward and two inverse calls issued back to back
     on two streams give bitwise the results of isolated calls."""
-    plan = build_plan(n, CANON)
+    plan = build_plan(n, CANON, executor="orbit-two-pass" if n == 16 else "auto")
     assert plan.info.executor in (6, 7)
     a = torch.from_numpy(rand_batch(n, 9, seed=5)).to(cuda)
     b = torch.from_numpy(rand_batch(n, 9, seed=6)).to(cuda)

@@ -134,6 +134,34 @@ def test_orbit16_tables_emulated(p):
 
 
 @pytest.mark.parametrize("p", [CANON, P2])
+def test_orbit_pat_tables_emulated(p):
+    """The single-pass orbit-pattern executor (n = 16): the orbit blocks fall into
+    8 shapes for any offsets; the two big ones (all 112 free orbits share ONE
+    24 x 24 operator, 105 of the 108 twelve-member orbits another) are emulated as
+    the kernel indexes its fragment tables (8 orbits per DMMA tile, Lambda in
+    fragment order, in-place slots), the rare ones as SIMT rows, plus the cube
+    FFT; against the FFT / orbit-route oracle."""
+    import ctypes
+
+    n = 16
+    L = _capi.lib()
+    rng = np.random.default_rng(161)
+    x = rng.uniform(-1, 1, (2, n**3)) + 1j * rng.uniform(-1, 1, (2, n**3))
+    pt = (p.r, p.s, p.t)
+    route = oracle.OrbitRoute(n, pt)
+    y = np.zeros_like(x)
+    st = (ctypes.c_int64 * 6)()
+    assert L.fcct_debug_emulate_orbit_pat(n, *pt, 0, x.ctypes.data, y.ctypes.data, 2, st) == 0
+    assert list(st)[:4] == [8, 112, 105, 14 * 72 + 14 * 24]
+    assert st[5] <= st[4] <= 4 * st[5]  # modelled gather / scatter wavefronts vs their floor
+    yr = route.forward(x)
+    assert np.linalg.norm(y - yr) / np.linalg.norm(yr) < 1e-13
+    xi = np.zeros_like(x)
+    assert L.fcct_debug_emulate_orbit_pat(n, *pt, 1, yr.ctypes.data, xi.ctypes.data, 2, None) == 0
+    assert np.linalg.norm(xi - x) / np.linalg.norm(x) < 1e-13
+
+
+@pytest.mark.parametrize("p", [CANON, P2])
 def test_orbit_big_tables_emulated(p):
     """The large-n orbit-FFT executor (n = 32): column-major orbit-block rows of
     S_n(p) / S_n(p)^{-1} n^-3 emulated as the kernel indexes them, plus the three
