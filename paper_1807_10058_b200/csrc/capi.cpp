@@ -226,21 +226,23 @@ void upload_orbit_pat(const OrbitPatHost& h, OrbitPatTables& out) {
         d.cnt[c] = h.cnt[c];
         d.ntiles[c] = h.ntiles[c];
         if (h.op[c].empty()) continue;
-        auto bo = upload(h.op[c]), bl = upload(h.lam[c]);
-        out.bufs.insert(out.bufs.end(), {bo, bl});
+        auto bo = upload(h.op[c]);
+        out.bufs.push_back(bo);
         d.op[c] = static_cast<const double2*>(bo->ptr);
-        d.lam[c] = static_cast<const double2*>(bl->ptr);
     }
     auto bi = upload(h.idx), bw = upload(h.warp_tiles);
     out.bufs.insert(out.bufs.end(), {bi, bw});
     d.idx = static_cast<const uint16_t*>(bi->ptr);
     d.idx_count = static_cast<int>(h.idx.size());
     d.warp_tiles = static_cast<const int2*>(bw->ptr);
-    d.nrare = static_cast<int>(h.rare_rows.size() / 2);
+    d.nrare = h.nrare;
+    d.rare_pitch = h.rare_pitch;
+    for (int ax = 0; ax < 3; ++ax)
+        for (int x = 0; x < 16; ++x) d.lax[ax][x] = make_double2(h.lax[ax][x][0], h.lax[ax][x][1]);
     if (d.nrare > 0) {
-        auto br = upload(h.rare_rows), bn = upload(h.rare_in), bc = upload(h.rare_coef);
+        auto br = upload(h.rare_out), bn = upload(h.rare_in), bc = upload(h.rare_coef);
         out.bufs.insert(out.bufs.end(), {br, bn, bc});
-        d.rare_rows = static_cast<const int2*>(br->ptr);
+        d.rare_out = static_cast<const uint16_t*>(br->ptr);
         d.rare_in = static_cast<const uint16_t*>(bn->ptr);
         d.rare_coef = static_cast<const double2*>(bc->ptr);
     }

@@ -22,39 +22,32 @@ constexpr int kPatThreads = kPatWarps * 32;
 // row); C[orbit][row]: this lane's rows 8 nt + 2 (lane % 4) + {0, 1}.
 // An orbit is read and written by this warp only, and every fragment of a tile
 // is loaded before its last DMMA issues, so the tile is updated in place.
-template <int D, int DIR, bool RIN, bool ROUT>
-__device__ __forceinline__ void pat_class(double2* X, const uint16_t* ix0, const double2* __restrict__ op,
-                                          const double2* __restrict__ lam, int first, int count, int cnt, int lane) {
-    constexpr int KT = D / 4, NT = (D + 7) / 8;
-    if (count == 0) return;
+template <int D>
+struct PatOp {
+    static constexpr int KT = D / 4, NT = (D + 7) / 8;
     double br[KT][NT], bi[KT][NT];
+    __device__ __forceinline__ void load(const double2* __restrict__ op, int lane) {
 #pragma unroll
-    for (int q = 0; q < KT; ++q)
+        for (int q = 0; q < KT; ++q)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            const double2 v = __ldg(op + (q * NT + nt) * 32 + lane);
-            br[q][nt] = v.x;
-            bi[q][nt] = v.y;
-        }
+            for (int nt = 0; nt < NT; ++nt) {
+                const double2 v = __ldg(op + (q * NT + nt) * 32 + lane);
+                br[q][nt] = v.x;
+                bi[q][nt] = v.y;
+            }
+    }
+};
+
+template <int D, bool RIN, bool ROUT>
+__device__ __forceinline__ void pat_class(double2* X, const uint16_t* ix0, const PatOp<D>& op, int first, int count,
+                                          int cnt, int lane) {
+    constexpr int KT = D / 4, NT = (D + 7) / 8;
     const int o = lane >> 2, k = lane & 3;
     for (int t = first; t < first + count; ++t) {
         const uint16_t* ix = ix0 + t * (D * 8);
         double cr[NT][2], ci[NT][2];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) cr[nt][0] = cr[nt][1] = ci[nt][0] = ci[nt][1] = 0.0;
-        double2 lf[NT][2];  // forward: Lambda of this lane's outputs, requested ahead of the chain
-        if constexpr (DIR == 0) {
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                lf[nt][0] = __ldg(lam + ((t * NT + nt) * 32 + lane) * 2);
-                lf[nt][1] = __ldg(lam + ((t * NT + nt) * 32 + lane) * 2 + 1);
-            }
-        }
-        double2 li[KT];  // inverse: 24 n^-3 conj(Lambda) of this lane's fragment elements
-        if constexpr (DIR == 1) {
-#pragma unroll
-            for (int q = 0; q < KT; ++q) li[q] = __ldg(lam + (t * KT + q) * 32 + lane);
-        }
         double ar[KT], ai[KT];
 #pragma unroll
         for (int q = 0; q < KT; ++q) {
@@ -70,20 +63,14 @@ __device__ __forceinline__ void pat_class(double2* X, const uint16_t* ix0, const
         }
 #pragma unroll
         for (int q = 0; q < KT; ++q) {
-            double xr = ar[q], xi = ai[q];
-            if constexpr (DIR == 1) {
-                const double tr = fma(xr, li[q].x, -xi * li[q].y), ti = fma(xr, li[q].y, xi * li[q].x);
-                xr = tr;
-                xi = ti;
-            }
-            const double nxi = neg_hi16(xi);
+            const double xr = ar[q], xi = ai[q], nxi = neg_hi16(xi);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
-                dmma884(cr[nt][0], cr[nt][1], xr, br[q][nt]);
-                if constexpr (!ROUT) dmma884(ci[nt][0], ci[nt][1], xr, bi[q][nt]);
+                dmma884(cr[nt][0], cr[nt][1], xr, op.br[q][nt]);
+                if constexpr (!ROUT) dmma884(ci[nt][0], ci[nt][1], xr, op.bi[q][nt]);
                 if constexpr (!RIN) {
-                    dmma884(cr[nt][0], cr[nt][1], nxi, bi[q][nt]);
-                    if constexpr (!ROUT) dmma884(ci[nt][0], ci[nt][1], xi, br[q][nt]);
+                    dmma884(cr[nt][0], cr[nt][1], nxi, op.bi[q][nt]);
+                    if constexpr (!ROUT) dmma884(ci[nt][0], ci[nt][1], xi, op.br[q][nt]);
                 }
             }
         }
@@ -95,15 +82,10 @@ __device__ __forceinline__ void pat_class(double2* X, const uint16_t* ix0, const
                 const int row = 8 * nt + 2 * k + e;
                 if ((D % 8 == 0 || row < D) && valid) {
                     const int slot = ix[row * 8 + o];
-                    const double vr = cr[nt][e], vi = ci[nt][e];
-                    if constexpr (DIR == 0) {
-                        const double2 l = lf[nt][e];
-                        X[slot] = make_double2(fma(vr, l.x, -vi * l.y), fma(vr, l.y, vi * l.x));
-                    } else if constexpr (ROUT) {
-                        X[slot].x = vr;
-                    } else {
-                        X[slot] = make_double2(vr, vi);
-                    }
+                    if constexpr (ROUT)
+                        X[slot].x = cr[nt][e];
+                    else
+                        X[slot] = make_double2(cr[nt][e], ci[nt][e]);
                 }
             }
     }
@@ -123,14 +105,36 @@ __global__ void __launch_bounds__(kPatThreads, 3)
     for (int i = tid; i < d.idx_count / 2; i += kPatThreads)
         reinterpret_cast<uint32_t*>(ix_s)[i] = __ldg(reinterpret_cast<const uint32_t*>(d.idx) + i);
     const int2 wa = __ldg(d.warp_tiles + warp), wb = __ldg(d.warp_tiles + kPatWarps + warp);
-    // this thread's rare rows (SIMT)
-    int2 rr[kPatMaxRare];
+    const uint16_t* ix_b = ix_s + d.ntiles[0] * (24 * 8);
+    // this thread's rare rows (SIMT): output slots
+    int rout[kPatMaxRare];
 #pragma unroll
     for (int u = 0; u < kPatMaxRare; ++u)
-        rr[u] = tid + u * kPatThreads < d.nrare ? __ldg(d.rare_rows + tid + u * kPatThreads) : make_int2(0, 0);
+        rout[u] = tid + u * kPatThreads < d.nrare ? __ldg(d.rare_out + tid + u * kPatThreads) : -1;
     __syncthreads();
     constexpr int64_t in_row = int64_t{N} * eb_of(MI), out_row = int64_t{N} * eb_of(MO);
     auto swz = [](int i, int j, int k) { return (i * NN + j) * NN + (k ^ j); };
+    // one in-place line pass of the cube FFT, two lines per thread; the axis'
+    // share of Lambda multiplies the line before (forward) or after (inverse)
+    // the butterflies, its 16 constants read from the parameter bank
+    auto pass = [&](auto at, const double2 (&lax)[16]) {
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
+            double2 v[NN];
+#pragma unroll
+            for (int x = 0; x < NN; ++x) {
+                v[x] = X[at(hi, lo, x)];
+                if constexpr (DIR == 0) v[x] = make_double2(fma(v[x].x, lax[x].x, -v[x].y * lax[x].y), fma(v[x].x, lax[x].y, v[x].y * lax[x].x));
+            }
+            fft_line16<NN, SIGN>(v);
+#pragma unroll
+            for (int x = 0; x < NN; ++x) {
+                if constexpr (DIR == 1) v[x] = make_double2(fma(v[x].x, lax[x].x, -v[x].y * lax[x].y), fma(v[x].x, lax[x].y, v[x].y * lax[x].x));
+                X[at(hi, lo, x)] = v[x];
+            }
+        }
+    };
     for (int64_t blk = blockIdx.x; blk < batch; blk += gridDim.x) {
         const char* src = static_cast<const char*>(in) + blk * in_row;
         char* dst = static_cast<char*>(out) + blk * out_row;
@@ -147,64 +151,78 @@ __global__ void __launch_bounds__(kPatThreads, 3)
             }
         }
         cp_async_commit();
+        PatOp<24> opa;
+        PatOp<12> opb;
+        if constexpr (DIR == 0) {  // the operator fragments arrive while the tile loads
+            opa.load(d.op[0], lane);
+            opb.load(d.op[1], lane);
+        }
         cp_async_wait<0>();
         __syncthreads();
-        double2 v[NN];
-        auto pass = [&](auto at) {  // one in-place line pass: two lines per thread
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
-#pragma unroll
-                for (int x = 0; x < NN; ++x) v[x] = X[at(hi, lo, x)];
-                fft_line16<NN, SIGN>(v);
-#pragma unroll
-                for (int x = 0; x < NN; ++x) X[at(hi, lo, x)] = v[x];
-            }
-            __syncthreads();
-        };
         if constexpr (DIR == 1) {
-            pass([&](int hi, int lo, int x) { return swz(x, hi, lo); });
-            pass([&](int hi, int lo, int x) { return swz(hi, x, lo); });
-            pass([&](int hi, int lo, int x) { return swz(hi, lo, x); });
+            pass([&](int hi, int lo, int x) { return swz(x, hi, lo); }, d.lax[0]);
+            __syncthreads();
+            pass([&](int hi, int lo, int x) { return swz(hi, x, lo); }, d.lax[1]);
+            __syncthreads();
+            pass([&](int hi, int lo, int x) { return swz(hi, lo, x); }, d.lax[2]);
+            opa.load(d.op[0], lane);
+            opb.load(d.op[1], lane);
+            __syncthreads();
         }
-        // base change, in place
+        // base change, in place: the rare rows first (into registers, all their
+        // loads in flight at once), then the two DMMA classes
         double2 racc[kPatMaxRare];
 #pragma unroll
         for (int u = 0; u < kPatMaxRare; ++u) {
             racc[u] = make_double2(0.0, 0.0);
-            const int terms = rr[u].x >> 16;
-            for (int t = 0; t < terms; ++t) {
-                const double2 c = __ldg(d.rare_coef + rr[u].y + t);
-                const int slot = __ldg(d.rare_in + rr[u].y + t);
-                if constexpr (RIN) {
-                    const double xr = X[slot].x;
-                    racc[u].x = fma(c.x, xr, racc[u].x);
-                    racc[u].y = fma(c.y, xr, racc[u].y);
-                } else {
-                    const double2 x = X[slot];
-                    racc[u].x = fma(c.x, x.x, racc[u].x);
-                    racc[u].x = fma(-c.y, x.y, racc[u].x);
-                    racc[u].y = fma(c.x, x.y, racc[u].y);
-                    racc[u].y = fma(c.y, x.x, racc[u].y);
+            if (rout[u] >= 0) {
+                const int r = tid + u * kPatThreads;
+                double2 c[kPatRareTerms];
+                int sl[kPatRareTerms];
+#pragma unroll
+                for (int t = 0; t < kPatRareTerms; ++t) {
+                    c[t] = __ldg(d.rare_coef + t * d.rare_pitch + r);
+                    sl[t] = __ldg(d.rare_in + t * d.rare_pitch + r);
+                }
+#pragma unroll
+                for (int t = 0; t < kPatRareTerms; ++t) {
+                    if constexpr (RIN) {
+                        const double xr = X[sl[t]].x;
+                        racc[u].x = fma(c[t].x, xr, racc[u].x);
+                        racc[u].y = fma(c[t].y, xr, racc[u].y);
+                    } else {
+                        const double2 x = X[sl[t]];
+                        racc[u].x = fma(c[t].x, x.x, racc[u].x);
+                        racc[u].x = fma(-c[t].y, x.y, racc[u].x);
+                        racc[u].y = fma(c[t].x, x.y, racc[u].y);
+                        racc[u].y = fma(c[t].y, x.x, racc[u].y);
+                    }
                 }
             }
         }
-        pat_class<24, DIR, RIN, ROUT>(X, ix_s, d.op[0], d.lam[0], wa.x, wa.y, d.cnt[0], lane);
-        pat_class<12, DIR, RIN, ROUT>(X, ix_s + d.ntiles[0] * (24 * 8), d.op[1], d.lam[1], wb.x, wb.y, d.cnt[1], lane);
+        pat_class<24, RIN, ROUT>(X, ix_s, opa, wa.x, wa.y, d.cnt[0], lane);
+        pat_class<12, RIN, ROUT>(X, ix_b, opb, wb.x, wb.y, d.cnt[1], lane);
         __syncthreads();  // the rare rows have been read by everyone
 #pragma unroll
         for (int u = 0; u < kPatMaxRare; ++u)
-            if ((rr[u].x >> 16) != 0) X[rr[u].x & 0xFFFF] = racc[u];
+            if (rout[u] >= 0) X[rout[u]] = racc[u];
         __syncthreads();
         if constexpr (DIR == 0) {
-            pass([&](int hi, int lo, int x) { return swz(hi, lo, x); });
-            pass([&](int hi, int lo, int x) { return swz(hi, x, lo); });
+            pass([&](int hi, int lo, int x) { return swz(hi, lo, x); }, d.lax[2]);
+            __syncthreads();
+            pass([&](int hi, int lo, int x) { return swz(hi, x, lo); }, d.lax[1]);
+            __syncthreads();
             // i axis, stored to HBM from registers (lanes vary k: coalesced)
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
+                double2 v[NN];
 #pragma unroll
-                for (int x = 0; x < NN; ++x) v[x] = X[swz(x, hi, lo)];
+                for (int x = 0; x < NN; ++x) {
+                    v[x] = X[swz(x, hi, lo)];
+                    v[x] = make_double2(fma(v[x].x, d.lax[0][x].x, -v[x].y * d.lax[0][x].y),
+                                        fma(v[x].x, d.lax[0][x].y, v[x].y * d.lax[0][x].x));
+                }
                 fft_line16<NN, SIGN>(v);
 #pragma unroll
                 for (int x = 0; x < NN; ++x) st_el<MO>(dst, (x * NN + hi) * NN + lo, v[x].x, v[x].y);

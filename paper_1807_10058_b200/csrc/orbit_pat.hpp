@@ -19,9 +19,13 @@
 //     and the 16^3 FFT follows (forward) or precedes (inverse) it in the same
 //     tile. HBM sees every sample once: no z round trip (orbit16.hpp moves z
 //     through HBM twice), no operator stream from L2, no tile metadata;
-//   - Lambda (forward: on the accumulators; inverse: 24 n^-3 conj(Lambda) on
-//     the loaded fragments) is a 64 KB table in fragment order, L2 resident;
-//   - the few orbits of the rare shapes (28 of 245 at n = 16) are SIMT rows.
+//   - Lambda is separable, Lambda[(i, j, k)] = L0[i] L1[j] L2[k]: each axis pass of
+//     the FFT multiplies its line by 16 constants read from the kernel
+//     parameters (constant bank operands: no load instructions, no table) —
+//     before the butterflies in the forward, after them (conjugated, 24 n^-3
+//     folded into axis 0) in the inverse;
+//   - the few orbits of the rare shapes (28 of 245 at n = 16) are SIMT rows,
+//     their coefficients stored term-major so a warp's loads are coalesced.
 // Real samples in (forward) and out (inverse) halve the DMMA count.
 #pragma once
 
@@ -36,6 +40,7 @@ struct Params;
 
 constexpr int kPatWarps = 4;     // warps per CTA (three CTAs per SM)
 constexpr int kPatMaxRare = 2;   // rare rows per thread
+constexpr int kPatRareTerms = 12;  // terms of a rare row (padded with zero coefficients)
 
 // physical slot of Fourier / sample index a = (i, j, k) in the shared tile:
 // (i, j, k ^ j) — the k, j and i line passes of the FFT are conflict-free
@@ -48,23 +53,27 @@ struct OrbitPatDesc {
     int idx_count = 0;        // uint16 entries of idx (copied to shared memory)
     int nrare = 0;            // SIMT rows
     const double2* op[2] = {nullptr, nullptr};   // [q][nt][32] B fragments (Re, Im) of M (or M^-1)
-    const double2* lam[2] = {nullptr, nullptr};  // forward [tile][nt][32][2]; inverse [tile][q][32]
     const uint16_t* idx = nullptr;               // class 0: [tile][24][8], then class 1: [tile][12][8] slots
     const int2* warp_tiles = nullptr;            // [2][kPatWarps]: (first tile, tiles) of a warp per class
-    const int2* rare_rows = nullptr;             // [nrare]: (out slot | terms << 16, first term)
-    const uint16_t* rare_in = nullptr;           // [terms] slots
-    const double2* rare_coef = nullptr;          // [terms]
+    int rare_pitch = 0;                          // nrare rounded up to a warp
+    const uint16_t* rare_out = nullptr;          // [nrare] output slots
+    const uint16_t* rare_in = nullptr;           // [kPatRareTerms][rare_pitch] input slots
+    const double2* rare_coef = nullptr;          // [kPatRareTerms][rare_pitch]
+    double2 lax[3][16];                          // per-axis phases of Lambda (forward) / its scaled inverse
 };
 
 struct OrbitPatHost {
     int n = 0, N = 0, dir = 0;
     int cnt[2] = {0, 0}, ntiles[2] = {0, 0};
-    std::vector<double> op[2], lam[2];
+    std::vector<double> op[2];
+    double lax[3][16][2] = {};        // per-axis phases (Re, Im)
     std::vector<uint16_t> idx;
     std::vector<int32_t> warp_tiles;  // [2][kPatWarps][2]
-    std::vector<int32_t> rare_rows;   // [nrare][2]
-    std::vector<uint16_t> rare_in;
-    std::vector<double> rare_coef;
+    int nrare = 0, rare_pitch = 0;
+    std::vector<uint16_t> rare_out;   // [nrare]
+    std::vector<uint16_t> rare_in;    // [kPatRareTerms][rare_pitch]
+    std::vector<double> rare_coef;    // [kPatRareTerms][rare_pitch][2]
+    int64_t rare_terms = 0;           // non-zero terms
     int patterns = 0;                 // distinct shapes found
     int64_t dmma = 0;                 // complex-input DMMA count per block
     double exec_flops() const;        // FP64-pipe flops per block (complex in / out)

@@ -120,6 +120,16 @@ bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
         for (int o : shapes[cls[c]].orbits) in_class[o] = 1;
     }
     const long double inv_scale = 1.0L / N;
+    {  // Lambda[(i, j, k)] = L0[i] L1[j] L2[k]; 1/24 (forward) or 24 / N (inverse, conjugated) on axis 0
+        const long double off[3] = {pr, ps, pt};
+        for (int ax = 0; ax < 3; ++ax)
+            for (int x = 0; x < n; ++x) {
+                cld v = unit_phase_ld((inverse ? -off[ax] : off[ax]) * x / n);
+                if (ax == 0) v *= inverse ? 24.0L * inv_scale : 1.0L / 24.0L;
+                h.lax[ax][x][0] = static_cast<double>(v.real());
+                h.lax[ax][x][1] = static_cast<double>(v.imag());
+            }
+    }
     for (int c = 0; c < 2; ++c) {
         if (cls[c] < 0) continue;
         const Shape& sh = shapes[cls[c]];
@@ -142,30 +152,6 @@ bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
         for (int t = 0; t < T; ++t)
             for (int m = 0; m < d; ++m)
                 for (int o = 0; o < 8; ++o) h.idx.push_back(static_cast<uint16_t>(pat_slot(L[orbit_at(t, o)][m])));
-        if (!inverse) {
-            h.lam[c].assign(static_cast<size_t>(T) * NT * 32 * 2 * 2, 0.0);
-            for (int t = 0; t < T; ++t)
-                for (int nt = 0; nt < NT; ++nt)
-                    for (int l = 0; l < 32; ++l)
-                        for (int e = 0; e < 2; ++e) {
-                            const int row = 8 * nt + 2 * (l % 4) + e;
-                            if (row >= d) continue;
-                            const cld v = lam(L[orbit_at(t, l / 4)][row]);
-                            const size_t at = (((static_cast<size_t>(t) * NT + nt) * 32 + l) * 2 + e) * 2;
-                            h.lam[c][at] = static_cast<double>(v.real());
-                            h.lam[c][at + 1] = static_cast<double>(v.imag());
-                        }
-        } else {
-            h.lam[c].assign(static_cast<size_t>(T) * KT * 32 * 2, 0.0);
-            for (int t = 0; t < T; ++t)
-                for (int q = 0; q < KT; ++q)
-                    for (int l = 0; l < 32; ++l) {
-                        const cld v = inv_scale / lam(L[orbit_at(t, l / 4)][4 * q + l % 4]);
-                        const size_t at = ((static_cast<size_t>(t) * KT + q) * 32 + l) * 2;
-                        h.lam[c][at] = static_cast<double>(v.real());
-                        h.lam[c][at + 1] = static_cast<double>(v.imag());
-                    }
-        }
         h.dmma += static_cast<int64_t>(T) * KT * NT * 4;
         // shared-memory conflict model of the gathers and scatters
         for (int t = 0; t < T; ++t) {
@@ -216,28 +202,48 @@ bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
             fb += nb[w];
         }
     }
-    // rare shapes: one SIMT row per output member, full S / S^-1 n^-3 entries
-    for (int o = 0; o < norb; ++o) {
-        if (in_class[o]) continue;
-        const auto& mem = orb.members[o];
-        const int d = static_cast<int>(mem.size());
-        const std::vector<cld>& M = inverse ? ob.Sinv[o] : ob.S[o];
-        for (int r = 0; r < d; ++r) {
-            const int first = static_cast<int>(h.rare_in.size());
-            int terms = 0;
-            for (int c = 0; c < d; ++c) {
-                const cld v = M[static_cast<size_t>(r) * d + c] * (inverse ? inv_scale : 1.0L);
-                if (v == cld{0, 0}) continue;
-                h.rare_in.push_back(static_cast<uint16_t>(pat_slot(mem[c])));
-                h.rare_coef.push_back(static_cast<double>(v.real()));
-                h.rare_coef.push_back(static_cast<double>(v.imag()));
-                ++terms;
+    // rare shapes: one SIMT row per output member, the entries of S / S^-1 with Lambda divided out,
+    // term-major and padded to kPatRareTerms (zero coefficient on the row's own
+    // first input)
+    {
+        struct Row { int out; std::vector<std::pair<int, cld>> terms; };
+        std::vector<Row> rows;
+        for (int o = 0; o < norb; ++o) {
+            if (in_class[o]) continue;
+            const auto& mem = orb.members[o];
+            const int d = static_cast<int>(mem.size());
+            const std::vector<cld>& M = inverse ? ob.Sinv[o] : ob.S[o];
+            for (int r = 0; r < d; ++r) {
+                Row row{pat_slot(mem[r]), {}};
+                for (int c = 0; c < d; ++c) {
+                    // Lambda is applied by the FFT passes to every element: divide it out
+                    const cld v = inverse ? M[static_cast<size_t>(r) * d + c] * lam(mem[c])
+                                          : M[static_cast<size_t>(r) * d + c] / lam(mem[r]);
+                    if (v != cld{0, 0}) row.terms.emplace_back(pat_slot(mem[c]), v);
+                }
+                if (row.terms.empty()) row.terms.emplace_back(pat_slot(mem[0]), cld{0, 0});
+                if (static_cast<int>(row.terms.size()) > kPatRareTerms) return false;
+                h.rare_terms += static_cast<int64_t>(row.terms.size());
+                rows.push_back(std::move(row));
             }
-            h.rare_rows.push_back(pat_slot(mem[r]) | (terms << 16));
-            h.rare_rows.push_back(first);
+        }
+        h.nrare = static_cast<int>(rows.size());
+        if (h.nrare > kPatMaxRare * kPatWarps * 32) return false;
+        h.rare_pitch = (h.nrare + 31) / 32 * 32;
+        h.rare_out.assign(h.nrare, 0);
+        h.rare_in.assign(static_cast<size_t>(kPatRareTerms) * h.rare_pitch, 0);
+        h.rare_coef.assign(static_cast<size_t>(kPatRareTerms) * h.rare_pitch * 2, 0.0);
+        for (int r = 0; r < h.nrare; ++r) {
+            h.rare_out[r] = static_cast<uint16_t>(rows[r].out);
+            for (int t = 0; t < kPatRareTerms; ++t) {
+                const bool on = t < static_cast<int>(rows[r].terms.size());
+                const size_t at = static_cast<size_t>(t) * h.rare_pitch + r;
+                h.rare_in[at] = static_cast<uint16_t>(on ? rows[r].terms[t].first : rows[r].terms[0].first);
+                h.rare_coef[2 * at] = on ? static_cast<double>(rows[r].terms[t].second.real()) : 0.0;
+                h.rare_coef[2 * at + 1] = on ? static_cast<double>(rows[r].terms[t].second.imag()) : 0.0;
+            }
         }
     }
-    if (static_cast<int>(h.rare_rows.size() / 2) > kPatMaxRare * kPatWarps * 32) return false;
     if (h.idx.size() * 2 > 10 * 1024) return false;  // the slot lists share the CTA's shared memory with the tile
     return true;
 }
@@ -252,7 +258,7 @@ double OrbitPatHost::exec_flops() const {
             if (e != 0 && 4 * e != n) twiddles += n / (2 * half);
         }
     const double fft = 3.0 * n * n * ((n / 2.0) * lg * 4.0 + 6.0 * twiddles);
-    return static_cast<double>(dmma) * 512.0 + fft + 8.0 * static_cast<double>(rare_in.size()) + 6.0 * N;
+    return static_cast<double>(dmma) * 512.0 + fft + 8.0 * static_cast<double>(rare_terms) + 3.0 * 6.0 * N;
 }
 
 namespace {
@@ -284,13 +290,14 @@ void dft3(std::vector<cd>& buf, int n, int sign) {
 
 // the base change on the tile X (physical slots), as the kernel indexes its tables
 void base_change(const OrbitPatHost& h, std::vector<cd>& X) {
-    const int nrare = static_cast<int>(h.rare_rows.size() / 2);
+    const int nrare = h.nrare;
     std::vector<cd> rare(nrare);
     for (int r = 0; r < nrare; ++r) {
-        const int terms = h.rare_rows[2 * r] >> 16, first = h.rare_rows[2 * r + 1];
         cd acc{0, 0};
-        for (int t = 0; t < terms; ++t)
-            acc += cd{h.rare_coef[2 * (first + t)], h.rare_coef[2 * (first + t) + 1]} * X[h.rare_in[first + t]];
+        for (int t = 0; t < kPatRareTerms; ++t) {
+            const size_t at = static_cast<size_t>(t) * h.rare_pitch + r;
+            acc += cd{h.rare_coef[2 * at], h.rare_coef[2 * at + 1]} * X[h.rare_in[at]];
+        }
         rare[r] = acc;
     }
     size_t idx_base = 0;
@@ -308,11 +315,7 @@ void base_change(const OrbitPatHost& h, std::vector<cd>& X) {
                             cd s{0, 0};
                             for (int q = 0; q < KT; ++q)
                                 for (int k = 0; k < 4; ++k) {
-                                    cd a = X[ix[(4 * q + k) * 8 + o]];
-                                    if (h.dir == 1) {
-                                        const size_t at = ((static_cast<size_t>(t) * KT + q) * 32 + o * 4 + k) * 2;
-                                        a *= cd{h.lam[c][at], h.lam[c][at + 1]};
-                                    }
+                                    const cd a = X[ix[(4 * q + k) * 8 + o]];
                                     const size_t ot = ((static_cast<size_t>(q) * NT + nt) * 32 + nl * 4 + k) * 2;
                                     s += a * cd{h.op[c][ot], h.op[c][ot + 1]};
                                 }
@@ -321,20 +324,14 @@ void base_change(const OrbitPatHost& h, std::vector<cd>& X) {
                 for (int o = 0; o < 8; ++o) {
                     if (t * 8 + o >= h.cnt[c]) continue;
                     for (int row = 0; row < d; ++row) {
-                        cd v = acc[o][row];
-                        if (h.dir == 0) {
-                            const int nt = row / 8, kk = (row % 8) / 2, e = row % 2;
-                            const size_t at = (((static_cast<size_t>(t) * NT + nt) * 32 + o * 4 + kk) * 2 + e) * 2;
-                            v *= cd{h.lam[c][at], h.lam[c][at + 1]};
-                        }
-                        X[ix[row * 8 + o]] = v;
+                        X[ix[row * 8 + o]] = acc[o][row];
                     }
                 }
             }
         }
         idx_base += static_cast<size_t>(h.ntiles[c]) * d * 8;
     }
-    for (int r = 0; r < nrare; ++r) X[h.rare_rows[2 * r] & 0xFFFF] = rare[r];
+    for (int r = 0; r < nrare; ++r) X[h.rare_out[r]] = rare[r];
 }
 
 }  // namespace
@@ -344,11 +341,23 @@ void emulate_orbit_pat(const OrbitPatHost& h, const double* in, double* out, int
     std::vector<cd> x(N), X(N);
     for (int64_t b = 0; b < batch; ++b) {
         for (int a = 0; a < N; ++a) x[a] = cd{in[2 * (b * N + a)], in[2 * (b * N + a) + 1]};
-        if (h.dir == 1) dft3(x, h.n, -1);
+        auto phases = [&]() {  // the axis passes' constant multiplies
+            for (int a = 0; a < N; ++a) {
+                const int ijk[3] = {a / 256, (a / 16) % 16, a % 16};
+                for (int ax = 0; ax < 3; ++ax) x[a] *= cd{h.lax[ax][ijk[ax]][0], h.lax[ax][ijk[ax]][1]};
+            }
+        };
+        if (h.dir == 1) {
+            dft3(x, h.n, -1);
+            phases();
+        }
         for (int a = 0; a < N; ++a) X[pat_slot(a)] = x[a];
         base_change(h, X);
         for (int a = 0; a < N; ++a) x[a] = X[pat_slot(a)];
-        if (h.dir == 0) dft3(x, h.n, +1);
+        if (h.dir == 0) {
+            phases();
+            dft3(x, h.n, +1);
+        }
         for (int a = 0; a < N; ++a) {
             out[2 * (b * N + a)] = x[a].real();
             out[2 * (b * N + a) + 1] = x[a].imag();
