@@ -39,8 +39,8 @@ struct PatOp {
 };
 
 template <int D, bool RIN, bool ROUT>
-__device__ __forceinline__ void pat_class(double2* X, const uint16_t* ix0, const PatOp<D>& op, int first, int count,
-                                          int cnt, int lane) {
+__device__ __forceinline__ void pat_class(double* Re, double* Im, const uint16_t* ix0, const PatOp<D>& op, int first,
+                                          int count, int cnt, int lane) {
     constexpr int KT = D / 4, NT = (D + 7) / 8;
     const int o = lane >> 2, k = lane & 3;
     for (int t = first; t < first + count; ++t) {
@@ -52,14 +52,8 @@ __device__ __forceinline__ void pat_class(double2* X, const uint16_t* ix0, const
 #pragma unroll
         for (int q = 0; q < KT; ++q) {
             const int slot = ix[(4 * q + k) * 8 + o];
-            if constexpr (RIN) {
-                ar[q] = X[slot].x;
-                ai[q] = 0.0;
-            } else {
-                const double2 v = X[slot];
-                ar[q] = v.x;
-                ai[q] = v.y;
-            }
+            ar[q] = Re[slot];
+            ai[q] = RIN ? 0.0 : Im[slot];
         }
 #pragma unroll
         for (int q = 0; q < KT; ++q) {
@@ -82,15 +76,22 @@ __device__ __forceinline__ void pat_class(double2* X, const uint16_t* ix0, const
                 const int row = 8 * nt + 2 * k + e;
                 if ((D % 8 == 0 || row < D) && valid) {
                     const int slot = ix[row * 8 + o];
-                    if constexpr (ROUT)
-                        X[slot].x = cr[nt][e];
-                    else
-                        X[slot] = make_double2(cr[nt][e], ci[nt][e]);
+                    Re[slot] = cr[nt][e];
+                    if constexpr (!ROUT) Im[slot] = ci[nt][e];
                 }
             }
     }
 }
 
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+// The tile: two planes of n^3 doubles (Re, Im). Natural order (slot = lexicographic
+// index) while the base change runs and on the load / store side, so a real block
+// is ONE bulk copy (TMA) into / out of the Re plane; (i, j, k ^ j) for the k-axis
+// pass. The j-axis pass converts between the two for free: a row (i, j, .) is
+// read and written by the 16 lanes of one instruction.
 template <int DIR, int MI, int MO>
 __global__ void __launch_bounds__(kPatThreads, 3)
     orbit_pat_kernel(const __grid_constant__ OrbitPatDesc d, const void* __restrict__ in, void* __restrict__ out,
@@ -98,73 +99,116 @@ __global__ void __launch_bounds__(kPatThreads, 3)
     constexpr int NN = 16, N = NN * NN * NN, SIGN = DIR == 0 ? +1 : -1;
     constexpr bool RIN = DIR == 0 && (MI == OF_R64 || MI == OF_R32);
     constexpr bool ROUT = DIR == 1 && (MO == OF_R64 || MO == OF_R32);
+    constexpr bool TMA_IN = DIR == 0 && MI == OF_R64, TMA_OUT = DIR == 1 && MO == OF_R64;
     extern __shared__ __align__(128) unsigned char smem[];
-    double2* X = reinterpret_cast<double2*>(smem);
-    uint16_t* ix_s = reinterpret_cast<uint16_t*>(smem + N * 16);
+    double* Re = reinterpret_cast<double*>(smem);
+    double* Im = Re + N;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + N * 16);
+    uint16_t* ix_s = reinterpret_cast<uint16_t*>(smem + N * 16 + 16);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (TMA_IN && tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
     for (int i = tid; i < d.idx_count / 2; i += kPatThreads)
         reinterpret_cast<uint32_t*>(ix_s)[i] = __ldg(reinterpret_cast<const uint32_t*>(d.idx) + i);
     const int2 wa = __ldg(d.warp_tiles + warp), wb = __ldg(d.warp_tiles + kPatWarps + warp);
     const uint16_t* ix_b = ix_s + d.ntiles[0] * (24 * 8);
-    // this thread's rare rows (SIMT): output slots
-    int rout[kPatMaxRare];
+    int rout[kPatMaxRare];  // this thread's rare rows (SIMT): output slots
 #pragma unroll
     for (int u = 0; u < kPatMaxRare; ++u)
         rout[u] = tid + u * kPatThreads < d.nrare ? __ldg(d.rare_out + tid + u * kPatThreads) : -1;
     __syncthreads();
     constexpr int64_t in_row = int64_t{N} * eb_of(MI), out_row = int64_t{N} * eb_of(MO);
+    auto nat = [](int i, int j, int k) { return (i * NN + j) * NN + k; };
     auto swz = [](int i, int j, int k) { return (i * NN + j) * NN + (k ^ j); };
-    // one in-place line pass of the cube FFT, two lines per thread; the axis'
-    // share of Lambda multiplies the line before (forward) or after (inverse)
-    // the butterflies, its 16 constants read from the parameter bank
-    auto pass = [&](auto at, const double2 (&lax)[16]) {
+    // one line of the cube FFT in registers; the axis' share of Lambda multiplies
+    // it before (forward) or after (inverse) the butterflies
+    auto line_fft = [&](double2 (&v)[NN], const double2 (&lax)[16]) {
+        if constexpr (DIR == 0) {
+#pragma unroll
+            for (int x = 0; x < NN; ++x) v[x] = cmul(v[x], lax[x]);
+        }
+        fft_line16<NN, SIGN>(v);
+        if constexpr (DIR == 1) {
+#pragma unroll
+            for (int x = 0; x < NN; ++x) v[x] = cmul(v[x], lax[x]);
+        }
+    };
+    // in-place pass over the tile, two lines per thread: rd / wr give the slot of
+    // element x of line (hi, lo)
+    auto pass = [&](auto rd, auto wr, const double2 (&lax)[16]) {
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
             const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
             double2 v[NN];
 #pragma unroll
-            for (int x = 0; x < NN; ++x) {
-                v[x] = X[at(hi, lo, x)];
-                if constexpr (DIR == 0) v[x] = make_double2(fma(v[x].x, lax[x].x, -v[x].y * lax[x].y), fma(v[x].x, lax[x].y, v[x].y * lax[x].x));
-            }
-            fft_line16<NN, SIGN>(v);
+            for (int x = 0; x < NN; ++x) v[x] = make_double2(Re[rd(hi, lo, x)], Im[rd(hi, lo, x)]);
+            line_fft(v, lax);
 #pragma unroll
             for (int x = 0; x < NN; ++x) {
-                if constexpr (DIR == 1) v[x] = make_double2(fma(v[x].x, lax[x].x, -v[x].y * lax[x].y), fma(v[x].x, lax[x].y, v[x].y * lax[x].x));
-                X[at(hi, lo, x)] = v[x];
+                Re[wr(hi, lo, x)] = v[x].x;
+                Im[wr(hi, lo, x)] = v[x].y;
             }
         }
     };
+    uint32_t phase = 0;
     for (int64_t blk = blockIdx.x; blk < batch; blk += gridDim.x) {
         const char* src = static_cast<const char*>(in) + blk * in_row;
         char* dst = static_cast<char*>(out) + blk * out_row;
-#pragma unroll 8
-        for (int a = tid; a < N; a += kPatThreads) {
-            if constexpr (MI == OF_C128) {
-                cp_async_n<16>(X + pat_slot(a), src + static_cast<int64_t>(a) * 16, true);
-            } else if constexpr (MI == OF_R64) {
-                cp_async_n<8>(&X[pat_slot(a)].x, src + static_cast<int64_t>(a) * 8, true);
-            } else {
-                double re, im;
-                ld_el<MI>(src, a, re, im);
-                X[pat_slot(a)] = make_double2(re, im);
-            }
-        }
-        cp_async_commit();
         PatOp<24> opa;
         PatOp<12> opb;
-        if constexpr (DIR == 0) {  // the operator fragments arrive while the tile loads
-            opa.load(d.op[0], lane);
+        if constexpr (DIR == 0) {
+            if constexpr (TMA_IN) {  // a real block: one bulk copy into the Re plane
+                if (tid == 0) {
+                    mbar_arrive_expect_tx(bar, N * 8);
+                    tma_load_1d(Re, src, N * 8, bar);
+                }
+            } else {
+#pragma unroll 8
+                for (int a = tid; a < N; a += kPatThreads) {
+                    if constexpr (MI == OF_C128) {
+                        cp_async_n<8>(Re + a, src + static_cast<int64_t>(a) * 16, true);
+                        cp_async_n<8>(Im + a, src + static_cast<int64_t>(a) * 16 + 8, true);
+                    } else {
+                        double re, im;
+                        ld_el<MI>(src, a, re, im);
+                        Re[a] = re;
+                        if constexpr (!RIN) Im[a] = im;
+                    }
+                }
+                cp_async_commit();
+            }
+            opa.load(d.op[0], lane);  // the operator fragments arrive while the tile loads
             opb.load(d.op[1], lane);
-        }
-        cp_async_wait<0>();
-        __syncthreads();
-        if constexpr (DIR == 1) {
-            pass([&](int hi, int lo, int x) { return swz(x, hi, lo); }, d.lax[0]);
+            if constexpr (TMA_IN) {
+                mbar_wait(bar, phase);
+                phase ^= 1;
+            } else {
+                cp_async_wait<0>();
+                __syncthreads();
+            }
+        } else {
+            // i axis straight from HBM (lanes vary k: coalesced), written in the k-pass layout
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
+                double2 v[NN];
+#pragma unroll
+                for (int x = 0; x < NN; ++x) ld_el<MI>(src, nat(x, hi, lo), v[x].x, v[x].y);
+                line_fft(v, d.lax[0]);
+#pragma unroll
+                for (int x = 0; x < NN; ++x) {
+                    Re[swz(x, hi, lo)] = v[x].x;
+                    Im[swz(x, hi, lo)] = v[x].y;
+                }
+            }
             __syncthreads();
-            pass([&](int hi, int lo, int x) { return swz(hi, x, lo); }, d.lax[1]);
+            pass([&](int hi, int lo, int x) { return swz(hi, lo, x); }, [&](int hi, int lo, int x) { return swz(hi, lo, x); },
+                 d.lax[2]);
             __syncthreads();
-            pass([&](int hi, int lo, int x) { return swz(hi, lo, x); }, d.lax[2]);
+            pass([&](int hi, int lo, int x) { return swz(hi, x, lo); }, [&](int hi, int lo, int x) { return nat(hi, x, lo); },
+                 d.lax[1]);
             opa.load(d.op[0], lane);
             opb.load(d.op[1], lane);
             __syncthreads();
@@ -186,31 +230,34 @@ __global__ void __launch_bounds__(kPatThreads, 3)
                 }
 #pragma unroll
                 for (int t = 0; t < kPatRareTerms; ++t) {
-                    if constexpr (RIN) {
-                        const double xr = X[sl[t]].x;
-                        racc[u].x = fma(c[t].x, xr, racc[u].x);
-                        racc[u].y = fma(c[t].y, xr, racc[u].y);
-                    } else {
-                        const double2 x = X[sl[t]];
-                        racc[u].x = fma(c[t].x, x.x, racc[u].x);
-                        racc[u].x = fma(-c[t].y, x.y, racc[u].x);
-                        racc[u].y = fma(c[t].x, x.y, racc[u].y);
-                        racc[u].y = fma(c[t].y, x.x, racc[u].y);
+                    const double xr = Re[sl[t]];
+                    racc[u].x = fma(c[t].x, xr, racc[u].x);
+                    racc[u].y = fma(c[t].y, xr, racc[u].y);
+                    if constexpr (!RIN) {
+                        const double xi = Im[sl[t]];
+                        racc[u].x = fma(-c[t].y, xi, racc[u].x);
+                        racc[u].y = fma(c[t].x, xi, racc[u].y);
                     }
                 }
             }
         }
-        pat_class<24, RIN, ROUT>(X, ix_s, opa, wa.x, wa.y, d.cnt[0], lane);
-        pat_class<12, RIN, ROUT>(X, ix_b, opb, wb.x, wb.y, d.cnt[1], lane);
+        pat_class<24, RIN, ROUT>(Re, Im, ix_s, opa, wa.x, wa.y, d.cnt[0], lane);
+        pat_class<12, RIN, ROUT>(Re, Im, ix_b, opb, wb.x, wb.y, d.cnt[1], lane);
         __syncthreads();  // the rare rows have been read by everyone
 #pragma unroll
         for (int u = 0; u < kPatMaxRare; ++u)
-            if (rout[u] >= 0) X[rout[u]] = racc[u];
+            if (rout[u] >= 0) {
+                Re[rout[u]] = racc[u].x;
+                if constexpr (!ROUT) Im[rout[u]] = racc[u].y;
+            }
+        if constexpr (TMA_OUT) fence_proxy_async_smem();
         __syncthreads();
         if constexpr (DIR == 0) {
-            pass([&](int hi, int lo, int x) { return swz(hi, lo, x); }, d.lax[2]);
+            pass([&](int hi, int lo, int x) { return nat(hi, x, lo); }, [&](int hi, int lo, int x) { return swz(hi, x, lo); },
+                 d.lax[1]);
             __syncthreads();
-            pass([&](int hi, int lo, int x) { return swz(hi, x, lo); }, d.lax[1]);
+            pass([&](int hi, int lo, int x) { return swz(hi, lo, x); }, [&](int hi, int lo, int x) { return swz(hi, lo, x); },
+                 d.lax[2]);
             __syncthreads();
             // i axis, stored to HBM from registers (lanes vary k: coalesced)
 #pragma unroll 1
@@ -218,29 +265,30 @@ __global__ void __launch_bounds__(kPatThreads, 3)
                 const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
                 double2 v[NN];
 #pragma unroll
-                for (int x = 0; x < NN; ++x) {
-                    v[x] = X[swz(x, hi, lo)];
-                    v[x] = make_double2(fma(v[x].x, d.lax[0][x].x, -v[x].y * d.lax[0][x].y),
-                                        fma(v[x].x, d.lax[0][x].y, v[x].y * d.lax[0][x].x));
-                }
-                fft_line16<NN, SIGN>(v);
+                for (int x = 0; x < NN; ++x) v[x] = make_double2(Re[swz(x, hi, lo)], Im[swz(x, hi, lo)]);
+                line_fft(v, d.lax[0]);
 #pragma unroll
-                for (int x = 0; x < NN; ++x) st_el<MO>(dst, (x * NN + hi) * NN + lo, v[x].x, v[x].y);
+                for (int x = 0; x < NN; ++x) st_el<MO>(dst, nat(x, hi, lo), v[x].x, v[x].y);
             }
+            __syncthreads();  // the tile is refilled by the next block
+        } else if constexpr (TMA_OUT) {  // a real block: one bulk copy out of the Re plane
+            if (tid == 0) {
+                tma_store_1d(dst, Re, N * 8);
+                tma_store_commit();
+                tma_store_wait_read0();
+            }
+            __syncthreads();
         } else {
 #pragma unroll 8
-            for (int a = tid; a < N; a += kPatThreads) {
-                const double2 r = X[pat_slot(a)];
-                st_el<MO>(dst, a, r.x, r.y);
-            }
+            for (int a = tid; a < N; a += kPatThreads) st_el<MO>(dst, a, Re[a], ROUT ? 0.0 : Im[a]);
+            __syncthreads();
         }
-        __syncthreads();  // the tile is refilled by the next block
     }
 }
 
 template <int DIR, int MI, int MO>
 cudaError_t launch_pat(const OrbitPatDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st, int num_sms) {
-    const int smem = 16 * 16 * 16 * 16 + ((d.idx_count * 2 + 15) / 16) * 16;
+    const int smem = 16 * 16 * 16 * 16 + 16 + ((d.idx_count * 2 + 15) / 16) * 16;
     auto kern = orbit_pat_kernel<DIR, MI, MO>;
     static thread_local int prepared = -1;
     int dev = 0;

@@ -42,9 +42,10 @@ constexpr int kPatWarps = 4;     // warps per CTA (three CTAs per SM)
 constexpr int kPatMaxRare = 2;   // rare rows per thread
 constexpr int kPatRareTerms = 12;  // terms of a rare row (padded with zero coefficients)
 
-// physical slot of Fourier / sample index a = (i, j, k) in the shared tile:
-// (i, j, k ^ j) — the k, j and i line passes of the FFT are conflict-free
-__host__ __device__ constexpr int pat_slot(int a) { return (a & ~15) | ((a ^ (a >> 4)) & 15); }
+// slot of Fourier / sample index a = (i, j, k) in the shared tile's Re / Im planes
+// while the base change runs: natural order (the FFT's j-axis pass converts to and
+// from the conflict-free (i, j, k ^ j) layout of the k-axis pass)
+__host__ __device__ constexpr int pat_slot(int a) { return a; }
 
 struct OrbitPatDesc {
     int n = 0, N = 0, dir = 0;
@@ -77,8 +78,8 @@ struct OrbitPatHost {
     int patterns = 0;                 // distinct shapes found
     int64_t dmma = 0;                 // complex-input DMMA count per block
     double exec_flops() const;        // FP64-pipe flops per block (complex in / out)
-    // modelled shared-memory wavefronts per block of the fragment gathers and
-    // result scatters (16-byte accesses, quarter-warps), and their conflict-free floor
+    // modelled shared-memory wavefronts per block and plane of the fragment gathers
+    // and result scatters (8-byte accesses, half-warps), and their conflict-free floor
     int64_t wavefronts = 0, wavefronts_floor = 0;
 };
 

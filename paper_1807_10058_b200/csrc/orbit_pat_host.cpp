@@ -5,6 +5,8 @@
 #include <array>
 #include <cmath>
 #include <complex>
+#include <map>
+#include <mutex>
 #include <numbers>
 
 #include "orbit_pat.hpp"
@@ -28,27 +30,122 @@ long double max_diff(const std::vector<cld>& a, const std::vector<cld>& b) {
     return m;
 }
 
-// wavefronts of one 16-byte access per lane: quarter-warps of 8 lanes, 8 bank
-// groups of 16 bytes; equal addresses are one broadcast
-int wavefronts16(const std::array<int, 32>& slot, const std::array<bool, 32>& on) {
+// wavefronts of one 8-byte access per lane into a plane of doubles: half-warps
+// of 16 lanes, 16 banks of 8 bytes; equal addresses are one broadcast
+int wavefronts8(const std::array<int, 32>& slot, const std::array<bool, 32>& on) {
     int total = 0;
-    for (int h = 0; h < 4; ++h) {
+    for (int h = 0; h < 2; ++h) {
         int worst = 0;
-        bool any = false;
-        for (int bg = 0; bg < 8; ++bg) {
-            std::array<int, 8> seen{};
+        for (int bank = 0; bank < 16; ++bank) {
+            std::array<int, 16> seen{};
             int ns = 0;
-            for (int l = 8 * h; l < 8 * h + 8; ++l) {
-                if (!on[l] || (slot[l] & 7) != bg) continue;
-                any = true;
+            for (int l = 16 * h; l < 16 * h + 16; ++l) {
+                if (!on[l] || (slot[l] & 15) != bank) continue;
                 if (std::find(seen.begin(), seen.begin() + ns, slot[l]) == seen.begin() + ns) seen[ns++] = slot[l];
             }
             worst = std::max(worst, ns);
         }
-        total += any ? worst : 0;
+        total += worst;
     }
     return total;
 }
+
+// Bank-conflict search for one DMMA class. The kernel's fragment gather of
+// k-step q touches, per half-warp, members pi[4 q .. 4 q + 3] of 4 orbits (16
+// doubles of one plane), its scatter of n-tile nt members pi[8 nt + e + 2 kk];
+// banks are slot mod 16. Free choices: the order of the orbits (which 4 share a
+// half-warp) and the member order pi (shared by the class: it permutes the
+// operator's rows and columns). Deterministic hill climbing: orbit swaps
+// between half-warps, now and then a swap inside pi.
+struct ConflictSearch {
+    int d = 0;
+    const std::vector<std::vector<int>>* L = nullptr;
+    std::vector<int> ord;  // orbit ids; slots beyond ord.size() in the last tile are padding
+    std::vector<int> pi;   // member order
+    int wl = 1, ws = 1;    // planes read by a gather / written by a scatter
+    std::vector<std::array<int, 4>> quads_ld, quads_st;
+    std::vector<int> st_live;  // live members of a store quad (d = 12: rows 8..11 only)
+
+    void quads() {
+        quads_ld.clear();
+        quads_st.clear();
+        st_live.clear();
+        for (int q = 0; q < d / 4; ++q) quads_ld.push_back({pi[4 * q], pi[4 * q + 1], pi[4 * q + 2], pi[4 * q + 3]});
+        for (int nt = 0; nt < (d + 7) / 8; ++nt)
+            for (int e = 0; e < 2; ++e) {
+                std::array<int, 4> qd{};
+                int live = 0;
+                for (int kk = 0; kk < 4; ++kk)
+                    if (8 * nt + e + 2 * kk < d) qd[live++] = pi[8 * nt + e + 2 * kk];
+                quads_st.push_back(qd);
+                st_live.push_back(live);
+            }
+    }
+    int quad_cost(int g, const std::array<int, 4>& qd, int live) const {  // half-warp g: orbits ord[4 g ..]
+        int cnt[16] = {};
+        int worst = 0;
+        for (int o = 4 * g; o < 4 * g + 4 && o < static_cast<int>(ord.size()); ++o)
+            for (int m = 0; m < live; ++m) worst = std::max(worst, ++cnt[(*L)[ord[o]][qd[m]] & 15]);
+        return worst;
+    }
+    int group_cost(int g) const {
+        int c = 0;
+        for (const auto& qd : quads_ld) c += wl * quad_cost(g, qd, 4);
+        for (size_t i = 0; i < quads_st.size(); ++i) c += ws * quad_cost(g, quads_st[i], st_live[i]);
+        return c;
+    }
+    int groups() const { return (static_cast<int>(ord.size()) + 3) / 4; }
+    int total() const {
+        int c = 0;
+        for (int g = 0; g < groups(); ++g) c += group_cost(g);
+        return c;
+    }
+    void run(int rounds, int swaps_per_round) {
+        uint64_t rng = 0x9E3779B97F4A7C15ull;
+        auto next = [&](int mod) {
+            rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+            return static_cast<int>((rng >> 33) % static_cast<uint64_t>(mod));
+        };
+        quads();
+        const int G = groups(), n_orb = static_cast<int>(ord.size());
+        std::vector<int> gc(G);
+        for (int g = 0; g < G; ++g) gc[g] = group_cost(g);
+        auto sweep = [&]() {
+            for (int it = 0; it < swaps_per_round; ++it) {
+                const int a = next(n_orb), b = next(n_orb), ga = a / 4, gb = b / 4;
+                if (ga == gb) continue;
+                std::swap(ord[a], ord[b]);
+                const int ca = group_cost(ga), cb = group_cost(gb);
+                if (ca + cb <= gc[ga] + gc[gb]) {
+                    gc[ga] = ca;
+                    gc[gb] = cb;
+                } else {
+                    std::swap(ord[a], ord[b]);
+                }
+            }
+        };
+        sweep();
+        for (int r = 0; r < rounds; ++r) {
+            const std::vector<int> ord0 = ord, gc0 = gc;
+            int before = 0;
+            for (int g = 0; g < G; ++g) before += gc[g];
+            const int a = next(d), b = next(d);
+            if (a == b) continue;
+            std::swap(pi[a], pi[b]);
+            quads();
+            for (int g = 0; g < G; ++g) gc[g] = group_cost(g);
+            sweep();
+            int after = 0;
+            for (int g = 0; g < G; ++g) after += gc[g];
+            if (after > before) {
+                std::swap(pi[a], pi[b]);
+                quads();
+                ord = ord0;
+                gc = gc0;
+            }
+        }
+    }
+};
 
 }  // namespace
 
@@ -134,7 +231,34 @@ bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
         if (cls[c] < 0) continue;
         const Shape& sh = shapes[cls[c]];
         const int d = sh.d, KT = d / 4, NT = (d + 7) / 8;
-        const std::vector<cld>& M = inverse ? sh.Minv : sh.M;
+        // orbit order and member order with the fewest modelled bank conflicts
+        ConflictSearch cs;
+        cs.d = d;
+        cs.L = &L;
+        cs.ord = sh.orbits;
+        cs.pi.resize(d);
+        for (int m = 0; m < d; ++m) cs.pi[m] = m;
+        cs.wl = 2;  // planes (Re, Im) a gather reads / a scatter writes; real I/O halves one side
+        cs.ws = 2;
+        {  // the search does not depend on the direction or the offsets: once per (n, class)
+            static std::mutex mu;
+            static std::map<std::pair<int, int>, std::pair<std::vector<int>, std::vector<int>>> cache;
+            std::lock_guard<std::mutex> lock(mu);
+            auto it = cache.find({n, d});
+            if (it == cache.end() || it->second.first.size() != cs.ord.size()) {
+                cs.run(300, 2000);
+                cache[{n, d}] = {cs.ord, cs.pi};
+            } else {
+                cs.ord = it->second.first;
+                cs.pi = it->second.second;
+            }
+        }
+        const std::vector<int>& pi = cs.pi;
+        std::vector<cld> M(static_cast<size_t>(d) * d);
+        for (int r = 0; r < d; ++r)
+            for (int cc = 0; cc < d; ++cc)
+                M[static_cast<size_t>(r) * d + cc] = (inverse ? sh.Minv : sh.M)[static_cast<size_t>(pi[r]) * d + pi[cc]];
+        auto member = [&](int o, int m) { return L[o][pi[m]]; };
         h.op[c].assign(static_cast<size_t>(KT) * NT * 32 * 2, 0.0);
         for (int q = 0; q < KT; ++q)
             for (int nt = 0; nt < NT; ++nt)
@@ -147,11 +271,11 @@ bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
         const int T = h.ntiles[c];
         auto orbit_at = [&](int t, int o) {  // padding slots of the last tile repeat its first orbit
             const int i = t * 8 + o;
-            return sh.orbits[i < h.cnt[c] ? i : t * 8];
+            return cs.ord[i < h.cnt[c] ? i : t * 8];
         };
         for (int t = 0; t < T; ++t)
             for (int m = 0; m < d; ++m)
-                for (int o = 0; o < 8; ++o) h.idx.push_back(static_cast<uint16_t>(pat_slot(L[orbit_at(t, o)][m])));
+                for (int o = 0; o < 8; ++o) h.idx.push_back(static_cast<uint16_t>(pat_slot(member(orbit_at(t, o), m))));
         h.dmma += static_cast<int64_t>(T) * KT * NT * 4;
         // shared-memory conflict model of the gathers and scatters
         for (int t = 0; t < T; ++t) {
@@ -159,11 +283,11 @@ bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
             std::array<bool, 32> on{};
             for (int q = 0; q < KT; ++q) {
                 for (int l = 0; l < 32; ++l) {
-                    slot[l] = pat_slot(L[orbit_at(t, l / 4)][4 * q + l % 4]);
+                    slot[l] = pat_slot(member(orbit_at(t, l / 4), 4 * q + l % 4));
                     on[l] = true;
                 }
-                h.wavefronts += wavefronts16(slot, on);
-                h.wavefronts_floor += 4;
+                h.wavefronts += wavefronts8(slot, on);
+                h.wavefronts_floor += 2;
             }
             for (int nt = 0; nt < NT; ++nt)
                 for (int e = 0; e < 2; ++e) {
@@ -171,11 +295,11 @@ bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
                     for (int l = 0; l < 32; ++l) {
                         const int row = 8 * nt + 2 * (l % 4) + e;
                         on[l] = row < d && t * 8 + l / 4 < h.cnt[c];
-                        slot[l] = on[l] ? pat_slot(L[orbit_at(t, l / 4)][row]) : 0;
+                        slot[l] = on[l] ? pat_slot(member(orbit_at(t, l / 4), row)) : 0;
                         live += on[l];
                     }
-                    h.wavefronts += wavefronts16(slot, on);
-                    h.wavefronts_floor += (live + 7) / 8;
+                    h.wavefronts += wavefronts8(slot, on);
+                    h.wavefronts_floor += (live + 15) / 16;
                 }
         }
     }
