@@ -158,6 +158,8 @@ __global__ void __launch_bounds__(kPatThreads, 3)
         char* dst = static_cast<char*>(out) + blk * out_row;
         PatOp<24> opa;
         PatOp<12> opb;
+        if (tid == 0 && blk + gridDim.x < batch)  // the block after this one, into L2
+            prefetch_l2_bulk(src + static_cast<int64_t>(gridDim.x) * in_row, static_cast<uint32_t>(in_row));
         if constexpr (DIR == 0) {
             if constexpr (TMA_IN) {  // a real block: one bulk copy into the Re plane
                 if (tid == 0) {
@@ -167,10 +169,7 @@ __global__ void __launch_bounds__(kPatThreads, 3)
             } else {
 #pragma unroll 8
                 for (int a = tid; a < N; a += kPatThreads) {
-                    if constexpr (MI == OF_C128) {
-                        cp_async_n<8>(Re + a, src + static_cast<int64_t>(a) * 16, true);
-                        cp_async_n<8>(Im + a, src + static_cast<int64_t>(a) * 16 + 8, true);
-                    } else {
+                    {
                         double re, im;
                         ld_el<MI>(src, a, re, im);
                         Re[a] = re;
@@ -190,17 +189,24 @@ __global__ void __launch_bounds__(kPatThreads, 3)
             }
         } else {
             // i axis straight from HBM (lanes vary k: coalesced), written in the k-pass layout
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
-                double2 v[NN];
+            {
+                const int hi = tid >> 4, lo = tid & 15;  // lines tid and tid + 128: (hi, lo) and (hi + 8, lo)
+                double2 v[NN], w[NN];
 #pragma unroll
                 for (int x = 0; x < NN; ++x) ld_el<MI>(src, nat(x, hi, lo), v[x].x, v[x].y);
+#pragma unroll
+                for (int x = 0; x < NN; ++x) ld_el<MI>(src, nat(x, hi + 8, lo), w[x].x, w[x].y);
                 line_fft(v, d.lax[0]);
 #pragma unroll
                 for (int x = 0; x < NN; ++x) {
                     Re[swz(x, hi, lo)] = v[x].x;
                     Im[swz(x, hi, lo)] = v[x].y;
+                }
+                line_fft(w, d.lax[0]);
+#pragma unroll
+                for (int x = 0; x < NN; ++x) {
+                    Re[swz(x, hi + 8, lo)] = w[x].x;
+                    Im[swz(x, hi + 8, lo)] = w[x].y;
                 }
             }
             __syncthreads();
