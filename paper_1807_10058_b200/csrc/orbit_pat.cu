@@ -15,6 +15,8 @@ using namespace odev;
 namespace {
 
 constexpr int kPatThreads = kPatWarps * 32;
+constexpr int kPatCtas = kPatWarps == 4 ? 3 : 2;        // CTAs per SM
+constexpr int kPatLines = 256 / kPatThreads;             // FFT lines per thread per pass
 
 // One DMMA class: orbits of D members sharing the operator M (D x D complex).
 // MMA roles: A = data, 8 orbits x 4 members per k-step (lane: orbit lane / 4,
@@ -93,7 +95,7 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 // pass. The j-axis pass converts between the two for free: a row (i, j, .) is
 // read and written by the 16 lanes of one instruction.
 template <int DIR, int MI, int MO>
-__global__ void __launch_bounds__(kPatThreads, 3)
+__global__ void __launch_bounds__(kPatThreads, kPatCtas)
     orbit_pat_kernel(const __grid_constant__ OrbitPatDesc d, const void* __restrict__ in, void* __restrict__ out,
                      int64_t batch) {
     constexpr int NN = 16, N = NN * NN * NN, SIGN = DIR == 0 ? +1 : -1;
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(kPatThreads, 3)
     // element x of line (hi, lo)
     auto pass = [&](auto rd, auto wr, const double2 (&lax)[16]) {
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kPatLines; ++h) {
             const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
             double2 v[NN];
 #pragma unroll
@@ -157,7 +159,6 @@ __global__ void __launch_bounds__(kPatThreads, 3)
         const char* src = static_cast<const char*>(in) + blk * in_row;
         char* dst = static_cast<char*>(out) + blk * out_row;
         PatOp<24> opa;
-        PatOp<12> opb;
         if (tid == 0 && blk + gridDim.x < batch)  // the block after this one, into L2
             prefetch_l2_bulk(src + static_cast<int64_t>(gridDim.x) * in_row, static_cast<uint32_t>(in_row));
         if constexpr (DIR == 0) {
@@ -179,7 +180,6 @@ __global__ void __launch_bounds__(kPatThreads, 3)
                 cp_async_commit();
             }
             opa.load(d.op[0], lane);  // the operator fragments arrive while the tile loads
-            opb.load(d.op[1], lane);
             if constexpr (TMA_IN) {
                 mbar_wait(bar, phase);
                 phase ^= 1;
@@ -189,7 +189,18 @@ __global__ void __launch_bounds__(kPatThreads, 3)
             }
         } else {
             // i axis straight from HBM (lanes vary k: coalesced), written in the k-pass layout
-            {
+            if constexpr (kPatLines == 1) {
+                const int hi = tid >> 4, lo = tid & 15;
+                double2 v[NN];
+#pragma unroll
+                for (int x = 0; x < NN; ++x) ld_el<MI>(src, nat(x, hi, lo), v[x].x, v[x].y);
+                line_fft(v, d.lax[0]);
+#pragma unroll
+                for (int x = 0; x < NN; ++x) {
+                    Re[swz(x, hi, lo)] = v[x].x;
+                    Im[swz(x, hi, lo)] = v[x].y;
+                }
+            } else {
                 const int hi = tid >> 4, lo = tid & 15;  // lines tid and tid + 128: (hi, lo) and (hi + 8, lo)
                 double2 v[NN], w[NN];
 #pragma unroll
@@ -216,7 +227,6 @@ __global__ void __launch_bounds__(kPatThreads, 3)
             pass([&](int hi, int lo, int x) { return swz(hi, x, lo); }, [&](int hi, int lo, int x) { return nat(hi, x, lo); },
                  d.lax[1]);
             opa.load(d.op[0], lane);
-            opb.load(d.op[1], lane);
             __syncthreads();
         }
         // base change, in place: the rare rows first (into registers, all their
@@ -248,6 +258,8 @@ __global__ void __launch_bounds__(kPatThreads, 3)
             }
         }
         pat_class<24, RIN, ROUT>(Re, Im, ix_s, opa, wa.x, wa.y, d.cnt[0], lane);
+        PatOp<12> opb;
+        opb.load(d.op[1], lane);
         pat_class<12, RIN, ROUT>(Re, Im, ix_b, opb, wb.x, wb.y, d.cnt[1], lane);
         __syncthreads();  // the rare rows have been read by everyone
 #pragma unroll
@@ -267,7 +279,7 @@ __global__ void __launch_bounds__(kPatThreads, 3)
             __syncthreads();
             // i axis, stored to HBM from registers (lanes vary k: coalesced)
 #pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kPatLines; ++h) {
                 const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
                 double2 v[NN];
 #pragma unroll
@@ -305,7 +317,7 @@ cudaError_t launch_pat(const OrbitPatDesc& d, const void* in, void* out, int64_t
         if (e != cudaSuccess) return e;
         prepared = dev;
     }
-    kern<<<static_cast<unsigned>(std::min<int64_t>(batch, 3 * static_cast<int64_t>(num_sms))), kPatThreads, smem, st>>>(
+    kern<<<static_cast<unsigned>(std::min<int64_t>(batch, kPatCtas * static_cast<int64_t>(num_sms))), kPatThreads, smem, st>>>(
         d, in, out, batch);
     return cudaGetLastError();
 }

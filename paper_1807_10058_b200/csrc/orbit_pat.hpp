@@ -38,7 +38,7 @@ namespace fcct {
 
 struct Params;
 
-constexpr int kPatWarps = 4;     // warps per CTA (three CTAs per SM)
+constexpr int kPatWarps = 4;     // warps per CTA (4: three CTAs per SM; 8: two)
 constexpr int kPatMaxRare = 2;   // rare rows per thread
 constexpr int kPatRareTerms = 12;  // terms of a rare row (padded with zero coefficients)
 
