@@ -118,7 +118,9 @@ typedef enum {
     FCCT_EXEC_TWO_LEVEL_V2 = 5,   /* n = 16: root pass + eight n = 8 stage-pipeline children */
     FCCT_EXEC_TILE = 6,           /* shared-memory tile interpreter */
     FCCT_EXEC_GLOBAL = 7,         /* global-memory multi-pass pipeline */
-    FCCT_EXEC_ORBIT_TWO_PASS = 8  /* n = 16: the two-pass orbit-FFT executor (S_n pass + cube FFT pass through HBM) */
+    FCCT_EXEC_ORBIT_TWO_PASS = 8, /* n = 16: the two-pass orbit-FFT executor (S_n pass + cube FFT pass through HBM) */
+    FCCT_EXEC_ORBIT_STREAMED = 9  /* n = 32, 64: the S pass on streamed / generated orbit blocks (one thread per row)
+                                     instead of the constant-operator DMMA tiles (orbit_pat.hpp) */
 } fcct_executor;
 
 /* build_plan with a forced executor (method FAST; see fcct_executor). */

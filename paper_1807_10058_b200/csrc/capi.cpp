@@ -230,7 +230,8 @@ void upload_orbit_pat(const OrbitPatHost& h, OrbitPatTables& out) {
         out.bufs.push_back(bo);
         d.op[c] = static_cast<const double2*>(bo->ptr);
     }
-    auto bi = upload(h.idx), bw = upload(h.warp_tiles);
+    auto narrow = [](const std::vector<int32_t>& v) { return std::vector<uint16_t>(v.begin(), v.end()); };
+    auto bi = upload(narrow(h.idx)), bw = upload(h.warp_tiles);
     out.bufs.insert(out.bufs.end(), {bi, bw});
     d.idx = static_cast<const uint16_t*>(bi->ptr);
     d.idx_count = static_cast<int>(h.idx.size());
@@ -240,10 +241,54 @@ void upload_orbit_pat(const OrbitPatHost& h, OrbitPatTables& out) {
     for (int ax = 0; ax < 3; ++ax)
         for (int x = 0; x < 16; ++x) d.lax[ax][x] = make_double2(h.lax[ax][x][0], h.lax[ax][x][1]);
     if (d.nrare > 0) {
-        auto br = upload(h.rare_out), bn = upload(h.rare_in), bc = upload(h.rare_coef);
+        auto br = upload(narrow(h.rare_out)), bn = upload(narrow(h.rare_in)), bc = upload(h.rare_coef);
         out.bufs.insert(out.bufs.end(), {br, bn, bc});
         d.rare_out = static_cast<const uint16_t*>(br->ptr);
         d.rare_in = static_cast<const uint16_t*>(bn->ptr);
+        d.rare_coef = static_cast<const double2*>(bc->ptr);
+    }
+    out.exec_flops = h.exec_flops();
+}
+
+// Large-n S pass on the orbit-pattern tables (n = 32, 64, orbit_pat.hpp).
+struct OrbitPatBigTables {
+    OrbitPatBigDesc desc{};
+    std::vector<std::shared_ptr<DevBuf>> bufs;
+    double exec_flops = 0;
+};
+
+void upload_orbit_pat_big(const OrbitPatHost& h, OrbitPatBigTables& out) {
+    out = OrbitPatBigTables{};
+    OrbitPatBigDesc& d = out.desc;
+    d.n = h.n;
+    d.N = h.N;
+    d.dir = h.dir;
+    while ((1 << d.log2n) < h.n) ++d.log2n;
+    for (int c = 0; c < 2; ++c) {
+        d.cnt[c] = h.cnt[c];
+        d.ntiles[c] = h.ntiles[c];
+        if (h.op[c].empty()) continue;
+        auto bo = upload(h.op[c]);
+        out.bufs.push_back(bo);
+        d.op[c] = static_cast<const double2*>(bo->ptr);
+    }
+    std::vector<double> lax(static_cast<size_t>(3) * h.n * 2);
+    for (int ax = 0; ax < 3; ++ax)
+        for (int x = 0; x < h.n; ++x) {
+            lax[(static_cast<size_t>(ax) * h.n + x) * 2] = h.lax[ax][x][0];
+            lax[(static_cast<size_t>(ax) * h.n + x) * 2 + 1] = h.lax[ax][x][1];
+        }
+    auto bi = upload(h.idx), bl = upload(lax);
+    out.bufs.insert(out.bufs.end(), {bi, bl});
+    d.idx = static_cast<const int32_t*>(bi->ptr);
+    d.lax = static_cast<const double2*>(bl->ptr);
+    d.nrare = h.nrare;
+    d.rare_pitch = h.rare_pitch;
+    if (d.nrare > 0) {
+        auto br = upload(h.rare_out), bn = upload(h.rare_in), bc = upload(h.rare_coef);
+        out.bufs.insert(out.bufs.end(), {br, bn, bc});
+        d.rare_out = static_cast<const int32_t*>(br->ptr);
+        d.rare_in = static_cast<const int32_t*>(bn->ptr);
         d.rare_coef = static_cast<const double2*>(bc->ptr);
     }
     out.exec_flops = h.exec_flops();
@@ -689,6 +734,8 @@ struct fcct_plan_s {
     OrbitPatTables opfwd, opinv;
     bool obig = false;  // large-n orbit-FFT executor (n = 32, 64, fp64, orbit_big.hpp)
     OrbitBigTables obfwd, obinv;
+    bool obpat = false;  // ... its S pass on the orbit-pattern tables (constant operator in registers)
+    OrbitPatBigTables obpfwd, obpinv;
     bool v2 = false;  // fp64 DMMA pipeline (tiling.hpp)
     Pipeline2Tables fwd2, inv2;
     bool two_level = false;  // n = 16: root pass + eight n = 8 child pipelines
@@ -1149,7 +1196,9 @@ void build_orbit_fft(fcct_plan_s* pl) {
 void build_fast_paths(fcct_plan_s* pl) {
     const int x = pl->exec_force;
     const std::string f = x == FCCT_EXEC_AUTO                                   ? ""
-                          : x == FCCT_EXEC_ORBIT || x == FCCT_EXEC_ORBIT_PHASED || x == FCCT_EXEC_ORBIT_TWO_PASS ? "orbit"
+                          : x == FCCT_EXEC_ORBIT || x == FCCT_EXEC_ORBIT_PHASED || x == FCCT_EXEC_ORBIT_TWO_PASS ||
+                                  x == FCCT_EXEC_ORBIT_STREAMED
+                              ? "orbit"
                           : x == FCCT_EXEC_PIPELINE2                           ? "v2"
                           : x == FCCT_EXEC_TWO_LEVEL || x == FCCT_EXEC_TWO_LEVEL_V2 ? "two"
                           : x == FCCT_EXEC_TILE                                ? "v1"
@@ -1157,11 +1206,10 @@ void build_fast_paths(fcct_plan_s* pl) {
     const bool f32 = pl->precision == FCCT_F32;
     if (f.empty() || f == "orbit") build_orbit_fft(pl);
     if (pl->offt) return;
-    if ((f.empty() || f == "orbit") && x != FCCT_EXEC_ORBIT_TWO_PASS) {  // n = 16: one pass, block resident in shared memory
+    if ((f.empty() || f == "orbit") && x != FCCT_EXEC_ORBIT_TWO_PASS && x != FCCT_EXEC_ORBIT_STREAMED) {  // n = 16: one pass, block resident in shared memory
         pl->opat = false;
         OrbitPatHost hf, hi;
-        if (pl->n == 16 && tree_is_exact(pl) && compile_orbit_pat(pl->n, pl->p, false, hf) &&
-            compile_orbit_pat(pl->n, pl->p, true, hi)) {
+        if (pl->n == 16 && tree_is_exact(pl) && compile_orbit_pat_pair(pl->n, pl->p, hf, hi)) {
             upload_orbit_pat(hf, pl->opfwd);
             upload_orbit_pat(hi, pl->opinv);
             pl->opat = true;
@@ -1178,7 +1226,16 @@ void build_fast_paths(fcct_plan_s* pl) {
             pl->o16 = true;
             return;
         }
-        pl->obig = false;
+        pl->obig = pl->obpat = false;
+        if ((pl->n == 32 || pl->n == 64) && !f32 && x != FCCT_EXEC_ORBIT_STREAMED && tree_is_exact(pl)) {
+            OrbitPatHost hf, hi;
+            if (compile_orbit_pat_pair(pl->n, pl->p, hf, hi)) {
+                upload_orbit_pat_big(hf, pl->obpfwd);
+                upload_orbit_pat_big(hi, pl->obpinv);
+                pl->obig = pl->obpat = true;
+                return;
+            }
+        }
         if ((pl->n == 32 || pl->n == 64) && !f32 && tree_is_exact(pl)) {
             OrbitBigHost h;
             if (compile_orbit_big(pl->n, pl->p, false, h)) {
@@ -1250,8 +1307,8 @@ void fill_info(fcct_plan_s* pl) {
             in.exec_flops_inverse = pl->opinv.exec_flops;
         }
         if (pl->obig) {
-            in.exec_flops_forward = pl->obfwd.exec_flops;
-            in.exec_flops_inverse = pl->obinv.exec_flops;
+            in.exec_flops_forward = pl->obpat ? pl->obpfwd.exec_flops : pl->obfwd.exec_flops;
+            in.exec_flops_inverse = pl->obpat ? pl->obpinv.exec_flops : pl->obinv.exec_flops;
         }
         int64_t bytes = 0;
         for (auto* pt : {&pl->fwd, &pl->inv})
@@ -1266,6 +1323,8 @@ void fill_info(fcct_plan_s* pl) {
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->opfwd, &pl->opinv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
+        for (auto* pt : {&pl->obpfwd, &pl->obpinv})
+            for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->gfwd, &pl->ginv})
             for (auto& b : pt->bufs) bytes += static_cast<int64_t>(b->bytes);
         for (auto* pt : {&pl->rfwd, &pl->rinv})
@@ -1278,7 +1337,7 @@ void fill_info(fcct_plan_s* pl) {
         }
         in.table_bytes = bytes;
         int64_t fwd = 0;
-        for (auto* pt : {&pl->obfwd.bufs, &pl->gfwd.bufs, &pl->o16fwd.bufs, &pl->opfwd.bufs, &pl->ofwd.bufs, &pl->fwd2.bufs})
+        for (auto* pt : {&pl->obfwd.bufs, &pl->gfwd.bufs, &pl->o16fwd.bufs, &pl->opfwd.bufs, &pl->obpfwd.bufs, &pl->ofwd.bufs, &pl->fwd2.bufs})
             for (auto& b : *pt) fwd += static_cast<int64_t>(b->bytes);
         in.table_bytes_forward = fwd;
     } else {
@@ -1296,7 +1355,7 @@ void fill_info(fcct_plan_s* pl) {
 
 fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int device,
                          PlanStore* store = nullptr, int executor = FCCT_EXEC_AUTO) {
-    if (executor < FCCT_EXEC_AUTO || executor > FCCT_EXEC_ORBIT_TWO_PASS)
+    if (executor < FCCT_EXEC_AUTO || executor > FCCT_EXEC_ORBIT_STREAMED)
         throw FcctError(ST_INVALID_ARGUMENT, "unknown executor");
     if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "build_plan: n must be >= 1");
     if (method != FCCT_DIRECT && method != FCCT_FAST) throw FcctError(ST_INVALID_ARGUMENT, "unknown method");
@@ -1392,7 +1451,9 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
             void* z = pl->scratch0->ptr;
             scratch_acquire(pl, st);
             if (!inverse) {
-                ck(launch_orbit_big_s(pl->obfwd.desc, in, z, batch, st), "orbit base change");
+                ck(pl->obpat ? launch_orbit_pat_big(pl->obpfwd.desc, in, z, batch, st)
+                             : launch_orbit_big_s(pl->obfwd.desc, in, z, batch, st),
+                   "orbit base change");
                 ck(launch_line_fft(pl->n, 2, +1, z, z, batch, st), "line FFT");
                 ck(launch_line_fft(pl->n, 1, +1, z, z, batch, st), "line FFT");
                 ck(launch_line_fft(pl->n, 0, +1, z, out, batch, st), "line FFT");
@@ -1400,7 +1461,9 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
                 ck(launch_line_fft(pl->n, 0, -1, in, z, batch, st), "line FFT");
                 ck(launch_line_fft(pl->n, 1, -1, z, z, batch, st), "line FFT");
                 ck(launch_line_fft(pl->n, 2, -1, z, z, batch, st), "line FFT");
-                ck(launch_orbit_big_s(pl->obinv.desc, z, out, batch, st), "orbit base change");
+                ck(pl->obpat ? launch_orbit_pat_big(pl->obpinv.desc, z, out, batch, st)
+                             : launch_orbit_big_s(pl->obinv.desc, z, out, batch, st),
+                   "orbit base change");
             }
             scratch_release(pl, st);
             return;

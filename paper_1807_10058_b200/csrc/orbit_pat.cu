@@ -322,7 +322,142 @@ cudaError_t launch_pat(const OrbitPatDesc& d, const void* in, void* out, int64_t
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Large n (32, 64): the S pass of a transform that lives in L2. One warp per
+// tile of 8 orbits: fragments gathered from global memory, the constant
+// operator in registers, results scattered to the output row; Lambda from
+// three n-entry tables in shared memory. The CTAs after the tile CTAs run the
+// rare shapes' rows, one thread per row.
+// ---------------------------------------------------------------------------
+struct LamTab {
+    const double2* t;  // shared: [3][n]
+    int n, lg;
+    __device__ __forceinline__ double2 operator()(int a) const {
+        const int k = a & (n - 1), j = (a >> lg) & (n - 1), i = a >> (2 * lg);
+        return cmul(cmul(t[i], t[n + j]), t[2 * n + k]);
+    }
+};
+
+template <int D, int DIR>
+__device__ __forceinline__ void pat_big_tile(const OrbitPatBigDesc& d, const LamTab& lam, const int32_t* __restrict__ ix,
+                                             const double2* __restrict__ opt, int valid_orbits,
+                                             const double2* __restrict__ x, double2* __restrict__ y, int64_t batch,
+                                             int lane) {
+    constexpr int KT = D / 4, NT = (D + 7) / 8;
+    PatOp<D> op;
+    op.load(opt, lane);
+    const int o = lane >> 2, k = lane & 3;
+    int gs[KT], ss[NT][2];
+#pragma unroll
+    for (int q = 0; q < KT; ++q) gs[q] = __ldg(ix + (4 * q + k) * 8 + o);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int row = 8 * nt + 2 * k + e;
+            ss[nt][e] = (D % 8 == 0 || row < D) && o < valid_orbits ? __ldg(ix + row * 8 + o) : -1;
+        }
+    pdl_wait();  // x is the previous kernel's output; the tables above are the plan's
+    for (int64_t b = 0; b < batch; ++b) {
+        const double2* xb = x + b * d.N;
+        double2* yb = y + b * d.N;
+        double2 a[KT];
+#pragma unroll
+        for (int q = 0; q < KT; ++q) a[q] = __ldg(xb + gs[q]);
+        double cr[NT][2], ci[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) cr[nt][0] = cr[nt][1] = ci[nt][0] = ci[nt][1] = 0.0;
+#pragma unroll
+        for (int q = 0; q < KT; ++q) {
+            if constexpr (DIR == 1) a[q] = cmul(a[q], lam(gs[q]));
+            const double xr = a[q].x, xi = a[q].y, nxi = neg_hi16(xi);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                dmma884(cr[nt][0], cr[nt][1], xr, op.br[q][nt]);
+                dmma884(ci[nt][0], ci[nt][1], xr, op.bi[q][nt]);
+                dmma884(cr[nt][0], cr[nt][1], nxi, op.bi[q][nt]);
+                dmma884(ci[nt][0], ci[nt][1], xi, op.br[q][nt]);
+            }
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                if (ss[nt][e] >= 0) {
+                    double2 v = make_double2(cr[nt][e], ci[nt][e]);
+                    if constexpr (DIR == 0) v = cmul(v, lam(ss[nt][e]));
+                    yb[ss[nt][e]] = v;
+                }
+    }
+}
+
+template <int DIR>
+__global__ void __launch_bounds__(128, 3)
+    orbit_pat_big_kernel(const __grid_constant__ OrbitPatBigDesc d, const double2* __restrict__ x,
+                         double2* __restrict__ y, int64_t batch, int tile_ctas) {
+    __shared__ double2 lax_s[3 * 64];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int i = tid; i < 3 * d.n; i += 128) lax_s[i] = __ldg(d.lax + i);
+    __syncthreads();
+    const LamTab lam{lax_s, d.n, d.log2n};
+    if (static_cast<int>(blockIdx.x) < tile_ctas) {
+        const int t = blockIdx.x * 4 + warp, ta = d.ntiles[0];
+        if (t < ta)
+            pat_big_tile<24, DIR>(d, lam, d.idx + static_cast<int64_t>(t) * (24 * 8), d.op[0], d.cnt[0] - t * 8, x, y,
+                                  batch, lane);
+        else if (t < ta + d.ntiles[1])
+            pat_big_tile<12, DIR>(d, lam, d.idx + static_cast<int64_t>(ta) * (24 * 8) + static_cast<int64_t>(t - ta) * (12 * 8),
+                                  d.op[1], d.cnt[1] - (t - ta) * 8, x, y, batch, lane);
+        return;
+    }
+    const int r = (blockIdx.x - tile_ctas) * 128 + tid;
+    if (r >= d.nrare) return;
+    double2 c[kPatRareTerms];
+    int sl[kPatRareTerms];
+#pragma unroll
+    for (int t = 0; t < kPatRareTerms; ++t) {
+        c[t] = __ldg(d.rare_coef + static_cast<int64_t>(t) * d.rare_pitch + r);
+        sl[t] = __ldg(d.rare_in + static_cast<int64_t>(t) * d.rare_pitch + r);
+    }
+    const int out = __ldg(d.rare_out + r);
+    pdl_wait();
+    for (int64_t b = 0; b < batch; ++b) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < kPatRareTerms; ++t) {
+            double2 v = __ldg(x + b * d.N + sl[t]);
+            if constexpr (DIR == 1) v = cmul(v, lam(sl[t]));
+            acc.x = fma(c[t].x, v.x, acc.x);
+            acc.x = fma(-c[t].y, v.y, acc.x);
+            acc.y = fma(c[t].x, v.y, acc.y);
+            acc.y = fma(c[t].y, v.x, acc.y);
+        }
+        if constexpr (DIR == 0) acc = cmul(acc, lam(out));
+        y[b * d.N + out] = acc;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_orbit_pat_big(const OrbitPatBigDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st) {
+    if (batch <= 0) return cudaSuccess;
+    if (d.n > 64 || in == out) return cudaErrorInvalidValue;
+    const int tile_ctas = (d.ntiles[0] + d.ntiles[1] + 3) / 4, rare_ctas = (d.nrare + 127) / 128;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(tile_ctas + rare_ctas));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    auto* x = static_cast<const double2*>(in);
+    auto* y = static_cast<double2*>(out);
+    return d.dir == 0 ? cudaLaunchKernelEx(&cfg, orbit_pat_big_kernel<0>, d, x, y, batch, tile_ctas)
+                      : cudaLaunchKernelEx(&cfg, orbit_pat_big_kernel<1>, d, x, y, batch, tile_ctas);
+}
 
 cudaError_t launch_orbit_pat(const OrbitPatDesc& d, int in_mode, int out_mode, const void* in, void* out,
                              int64_t batch, cudaStream_t st, int num_sms) {

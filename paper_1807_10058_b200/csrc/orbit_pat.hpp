@@ -63,16 +63,33 @@ struct OrbitPatDesc {
     double2 lax[3][16];                          // per-axis phases of Lambda (forward) / its scaled inverse
 };
 
+// Large n (32, 64; orbit_big.hpp's executor): the same tables drive the S pass of
+// a single transform that lives in L2 — one warp per tile of 8 orbits, fragments
+// gathered from / scattered to global memory, Lambda from three n-entry tables
+// in shared memory. Nothing is streamed: the 104 MB coefficient stream of
+// S_64^-1 (and S_64's generated coefficients) become a 9 KB register operand.
+struct OrbitPatBigDesc {
+    int n = 0, N = 0, dir = 0, log2n = 0;
+    int cnt[2] = {0, 0}, ntiles[2] = {0, 0};
+    const double2* op[2] = {nullptr, nullptr};
+    const int32_t* idx = nullptr;        // class 0: [tile][24][8], then class 1: [tile][12][8] natural positions
+    int nrare = 0, rare_pitch = 0;
+    const int32_t* rare_out = nullptr;   // [nrare]
+    const int32_t* rare_in = nullptr;    // [kPatRareTerms][rare_pitch]
+    const double2* rare_coef = nullptr;  // [kPatRareTerms][rare_pitch]
+    const double2* lax = nullptr;        // [3][n] per-axis phases
+};
+
 struct OrbitPatHost {
     int n = 0, N = 0, dir = 0;
     int cnt[2] = {0, 0}, ntiles[2] = {0, 0};
     std::vector<double> op[2];
-    double lax[3][16][2] = {};        // per-axis phases (Re, Im)
-    std::vector<uint16_t> idx;
+    double lax[3][64][2] = {};        // per-axis phases (Re, Im), n entries per axis
+    std::vector<int32_t> idx;
     std::vector<int32_t> warp_tiles;  // [2][kPatWarps][2]
     int nrare = 0, rare_pitch = 0;
-    std::vector<uint16_t> rare_out;   // [nrare]
-    std::vector<uint16_t> rare_in;    // [kPatRareTerms][rare_pitch]
+    std::vector<int32_t> rare_out;    // [nrare]
+    std::vector<int32_t> rare_in;     // [kPatRareTerms][rare_pitch]
     std::vector<double> rare_coef;    // [kPatRareTerms][rare_pitch][2]
     int64_t rare_terms = 0;           // non-zero terms
     int patterns = 0;                 // distinct shapes found
@@ -84,8 +101,10 @@ struct OrbitPatHost {
 };
 
 // Compiles S_n(p) (forward) or S_n(p)^{-1} / n^3 (inverse); false when n is not
-// 16, an orbit block is singular or the shapes do not fit the kernel.
+// 16, 32 or 64, an orbit block is singular or the shapes do not fit the kernel.
 bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h);
+// Both directions from one derivation of the orbit blocks.
+bool compile_orbit_pat_pair(int n, const Params& p, OrbitPatHost& fwd, OrbitPatHost& inv);
 
 // Host emulation on the compiled tables, complex128 rows (CPU tests).
 void emulate_orbit_pat(const OrbitPatHost& h, const double* in, double* out, int64_t batch);
@@ -93,5 +112,8 @@ void emulate_orbit_pat(const OrbitPatHost& h, const double* in, double* out, int
 // in / out modes as OfMode (orbit_fft.hpp).
 cudaError_t launch_orbit_pat(const OrbitPatDesc& d, int in_mode, int out_mode, const void* in, void* out,
                              int64_t batch, cudaStream_t st, int num_sms);
+
+// Large-n S pass (complex128 in and out, [batch][N] rows; in != out).
+cudaError_t launch_orbit_pat_big(const OrbitPatBigDesc& d, const void* in, void* out, int64_t batch, cudaStream_t st);
 
 }  // namespace fcct

@@ -149,10 +149,26 @@ struct ConflictSearch {
 
 }  // namespace
 
+namespace {
+bool compile_from_blocks(int n, const Params& p, const OrbitBlocks& ob, bool inverse, OrbitPatHost& h);
+}
+
 bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
-    if (n != 16) return false;
+    if (n != 16 && n != 32 && n != 64) return false;
+    const OrbitBlocks ob = orbit_blocks(n, p);
+    return compile_from_blocks(n, p, ob, inverse, h);
+}
+
+bool compile_orbit_pat_pair(int n, const Params& p, OrbitPatHost& fwd, OrbitPatHost& inv) {
+    if (n != 16 && n != 32 && n != 64) return false;
+    const OrbitBlocks ob = orbit_blocks(n, p);  // the long-double blocks once for both directions
+    return compile_from_blocks(n, p, ob, false, fwd) && compile_from_blocks(n, p, ob, true, inv);
+}
+
+namespace {
+
+bool compile_from_blocks(int n, const Params& p, const OrbitBlocks& ob, bool inverse, OrbitPatHost& h) {
     const int N = static_cast<int>(cube(n));
-    OrbitBlocks ob = orbit_blocks(n, p);
     if (!std::isfinite(ob.worst_condition)) return false;
     const Orbits& orb = *ob.orb;
     const auto& grp = s4_group();
@@ -180,12 +196,13 @@ bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
             if (std::find(L[o].begin(), L[o].end(), a) == L[o].end()) L[o].push_back(a);
         }
         if (static_cast<int>(L[o].size()) != d) return false;
-        std::vector<cld> M(static_cast<size_t>(d) * d), Mi(static_cast<size_t>(d) * d);
+        std::vector<cld> M(static_cast<size_t>(d) * d), Mi(static_cast<size_t>(d) * d), lv(d);
+        for (int r = 0; r < d; ++r) lv[r] = lam(L[o][r]);
         for (int r = 0; r < d; ++r)
             for (int c = 0; c < d; ++c) {
                 const size_t src = static_cast<size_t>(orb.pos[L[o][r]]) * d + orb.pos[L[o][c]];
-                M[static_cast<size_t>(r) * d + c] = ob.S[o][src] / lam(L[o][r]);
-                Mi[static_cast<size_t>(r) * d + c] = ob.Sinv[o][src] * lam(L[o][c]);
+                M[static_cast<size_t>(r) * d + c] = ob.S[o][src] / lv[r];
+                Mi[static_cast<size_t>(r) * d + c] = ob.Sinv[o][src] * lv[c];
             }
         bool found = false;
         for (Shape& s : shapes)
@@ -245,7 +262,9 @@ bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
             static std::map<std::pair<int, int>, std::pair<std::vector<int>, std::vector<int>>> cache;
             std::lock_guard<std::mutex> lock(mu);
             auto it = cache.find({n, d});
-            if (it == cache.end() || it->second.first.size() != cs.ord.size()) {
+            if (n > 16) {
+                // large n gathers from global memory (L2): no banks to avoid
+            } else if (it == cache.end() || it->second.first.size() != cs.ord.size()) {
                 cs.run(300, 2000);
                 cache[{n, d}] = {cs.ord, cs.pi};
             } else {
@@ -275,7 +294,7 @@ bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
         };
         for (int t = 0; t < T; ++t)
             for (int m = 0; m < d; ++m)
-                for (int o = 0; o < 8; ++o) h.idx.push_back(static_cast<uint16_t>(pat_slot(member(orbit_at(t, o), m))));
+                for (int o = 0; o < 8; ++o) h.idx.push_back(pat_slot(member(orbit_at(t, o), m)));
         h.dmma += static_cast<int64_t>(T) * KT * NT * 4;
         // shared-memory conflict model of the gathers and scatters
         for (int t = 0; t < T; ++t) {
@@ -352,25 +371,27 @@ bool compile_orbit_pat(int n, const Params& p, bool inverse, OrbitPatHost& h) {
             }
         }
         h.nrare = static_cast<int>(rows.size());
-        if (h.nrare > kPatMaxRare * kPatWarps * 32) return false;
+        if (n == 16 && h.nrare > kPatMaxRare * kPatWarps * 32) return false;
         h.rare_pitch = (h.nrare + 31) / 32 * 32;
         h.rare_out.assign(h.nrare, 0);
         h.rare_in.assign(static_cast<size_t>(kPatRareTerms) * h.rare_pitch, 0);
         h.rare_coef.assign(static_cast<size_t>(kPatRareTerms) * h.rare_pitch * 2, 0.0);
         for (int r = 0; r < h.nrare; ++r) {
-            h.rare_out[r] = static_cast<uint16_t>(rows[r].out);
+            h.rare_out[r] = rows[r].out;
             for (int t = 0; t < kPatRareTerms; ++t) {
                 const bool on = t < static_cast<int>(rows[r].terms.size());
                 const size_t at = static_cast<size_t>(t) * h.rare_pitch + r;
-                h.rare_in[at] = static_cast<uint16_t>(on ? rows[r].terms[t].first : rows[r].terms[0].first);
+                h.rare_in[at] = on ? rows[r].terms[t].first : rows[r].terms[0].first;
                 h.rare_coef[2 * at] = on ? static_cast<double>(rows[r].terms[t].second.real()) : 0.0;
                 h.rare_coef[2 * at + 1] = on ? static_cast<double>(rows[r].terms[t].second.imag()) : 0.0;
             }
         }
     }
-    if (h.idx.size() * 2 > 10 * 1024) return false;  // the slot lists share the CTA's shared memory with the tile
+    if (n == 16 && h.idx.size() * 2 > 10 * 1024) return false;  // the slot lists share the CTA's shared memory with the tile
     return true;
 }
+
+}  // namespace
 
 double OrbitPatHost::exec_flops() const {
     int lg = 0;
@@ -431,7 +452,7 @@ void base_change(const OrbitPatHost& h, std::vector<cd>& X) {
         for (int w = 0; w < kPatWarps; ++w) {
             const int first = h.warp_tiles[(c * kPatWarps + w) * 2], count = h.warp_tiles[(c * kPatWarps + w) * 2 + 1];
             for (int t = first; t < first + count; ++t) {
-                const uint16_t* ix = h.idx.data() + idx_base + static_cast<size_t>(t) * d * 8;
+                const int32_t* ix = h.idx.data() + idx_base + static_cast<size_t>(t) * d * 8;
                 cd acc[8][24];
                 for (int o = 0; o < 8; ++o)
                     for (int nt = 0; nt < NT; ++nt)
@@ -467,7 +488,7 @@ void emulate_orbit_pat(const OrbitPatHost& h, const double* in, double* out, int
         for (int a = 0; a < N; ++a) x[a] = cd{in[2 * (b * N + a)], in[2 * (b * N + a) + 1]};
         auto phases = [&]() {  // the axis passes' constant multiplies
             for (int a = 0; a < N; ++a) {
-                const int ijk[3] = {a / 256, (a / 16) % 16, a % 16};
+                const int ijk[3] = {a / (h.n * h.n), (a / h.n) % h.n, a % h.n};
                 for (int ax = 0; ax < 3; ++ax) x[a] *= cd{h.lax[ax][ijk[ax]][0], h.lax[ax][ijk[ax]][1]};
             }
         };

@@ -366,7 +366,7 @@ class TransformPlan:
 
 # fcct_executor (include/fcct_gpu.h): executors a FAST plan can be forced onto
 EXECUTORS = {"auto": 0, "orbit": 1, "orbit-phased": 2, "pipeline2": 3, "two-level": 4, "two-level-v2": 5,
-             "tile": 6, "global": 7, "orbit-two-pass": 8}
+             "tile": 6, "global": 7, "orbit-two-pass": 8, "orbit-streamed": 9}
 
 
 def _create(n: int, p: SkewParams, method: int, precision: str, device: int, executor: str = "auto") -> TransformPlan:

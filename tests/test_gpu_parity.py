@@ -708,21 +708,27 @@ def test_n16_orbit_executors(cuda, oracle_mod, p, exe, eid):
     assert rel(b32.cpu().numpy(), x) <= F32_TOL
 
 
+@pytest.mark.parametrize("exe", ["auto", "orbit-streamed"])
 @pytest.mark.parametrize("n,p", [(32, CANON), (64, CANON), (32, SkewParams(0.21, 0.055, 0.4))])
-def test_large_n_orbit_fft(cuda, oracle_mod, n, p):
+def test_large_n_orbit_fft(cuda, oracle_mod, n, p, exe):
     """configs[3] (n = 64, single transform) on the large-n orbit-FFT executor
-    (executor 7: S_n(p) as orbit-block rows — forward coefficients of the free
-    orbits generated from the group structure, inverse blocks streamed — then
-    three line-FFT passes): the telescoped factorisation has no tree-conditioning
-    floor, so the 1e-12 bar holds where the stage-by-stage tree measures 1e-9."""
+    (executor 7: S_n(p), then three line-FFT passes). The S pass runs on the
+    orbit-pattern tables (default: one warp per tile of 8 orbits, the constant
+    24 x 24 / 12 x 12 operator in registers as DMMA fragments, nothing streamed)
+    or, forced, on the orbit-block rows (forward coefficients of the free orbits
+    generated from the group structure, inverse blocks streamed). The telescoped
+    factorisation has no tree-conditioning floor, so the 1e-12 bar holds where
+    the stage-by-stage tree measures 1e-9."""
     route = oracle_mod.OrbitRoute(n, tup(p))
     batch = 2 if n == 32 else 1
     x = rand_batch(n, batch, seed=n + 1)
     y_ref = route.forward(x)
-    plan = build_plan(n, p)
+    plan = build_plan(n, p, executor=exe)
     assert plan.info.executor == 7
-    # the forward streams (almost) no coefficients: only the non-free orbits' blocks
-    assert plan.info.table_bytes_forward < 0.25 * (plan.info.table_bytes - plan.info.table_bytes_forward)
+    if exe == "auto":  # the pattern tables: slot lists and two register operands, ~1 MB at n = 64
+        assert plan.info.table_bytes < 4 * n**3 * 16
+    else:  # the forward streams (almost) no coefficients: only the non-free orbits' blocks
+        assert plan.info.table_bytes_forward < 0.25 * (plan.info.table_bytes - plan.info.table_bytes_forward)
     y = fast_apply(plan, SignalTensor(n, torch.from_numpy(x).to(cuda))).values.cpu().numpy()
     assert rel(y, y_ref) <= F64_TOL
     nodes = np.random.default_rng(777).integers(0, n**3, 8)

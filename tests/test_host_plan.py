@@ -161,6 +161,29 @@ def test_orbit_pat_tables_emulated(p):
     assert np.linalg.norm(xi - x) / np.linalg.norm(x) < 1e-13
 
 
+def test_orbit_pat_tables_emulated_n32():
+    """The same pattern tables drive the large-n S pass (n = 32, 64: one warp per
+    tile of 8 orbits gathering from global memory): 1,120 free orbits on one
+    operator, 465 of the 472 twelve-member orbits on another, emulated at n = 32."""
+    import ctypes
+
+    n = 32
+    L = _capi.lib()
+    rng = np.random.default_rng(321)
+    x = rng.uniform(-1, 1, (1, n**3)) + 1j * rng.uniform(-1, 1, (1, n**3))
+    pt = (P2.r, P2.s, P2.t)
+    route = oracle.OrbitRoute(n, pt)
+    y = np.zeros_like(x)
+    st = (ctypes.c_int64 * 6)()
+    assert L.fcct_debug_emulate_orbit_pat(n, *pt, 0, x.ctypes.data, y.ctypes.data, 1, st) == 0
+    assert list(st)[:3] == [8, 1120, 465]
+    yr = route.forward(x)
+    assert np.linalg.norm(y - yr) / np.linalg.norm(yr) < 1e-13
+    xi = np.zeros_like(x)
+    assert L.fcct_debug_emulate_orbit_pat(n, *pt, 1, yr.ctypes.data, xi.ctypes.data, 1, None) == 0
+    assert np.linalg.norm(xi - x) / np.linalg.norm(x) < 1e-13
+
+
 @pytest.mark.parametrize("p", [CANON, P2])
 def test_orbit_big_tables_emulated(p):
     """The large-n orbit-FFT executor (n = 32): column-major orbit-block rows of
