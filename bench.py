@@ -662,7 +662,7 @@ def b200_arm(args):
     on_tcgen05 = info.executor in (8, 9)
     peak_tf = (TF32_PEAK_TFLOPS if info.executor == 8 else INT8_PEAK_TOPS) if on_tcgen05 else (
         FP64_PEAK_TFLOPS if on_fp64_pipe else FP32_PEAK_TFLOPS)
-    exec_flops = (info.exec_flops_forward or info.flops_forward) * blocks
+    exec_flops = ((w["real_io"] and info.exec_flops_forward_real) or info.exec_flops_forward or info.flops_forward) * blocks
     achieved_tf = exec_flops / (fwd_ms / 1e3) / 1e12
     achieved_gbs = bytes_fwd / (fwd_ms / 1e3) / 1e9
     t_hbm, t_pipe = bytes_fwd / (hbm * 1e9), exec_flops / (peak_tf * 1e12)

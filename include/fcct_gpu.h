@@ -90,6 +90,10 @@ typedef struct {
                                   equal to the algorithmic count */
     double exec_flops_inverse;
     int64_t table_bytes_forward; /* device bytes of the forward executor's own tables (fast plans) */
+    double exec_flops_forward_real; /* same as exec_flops_*, for real samples in (fcct_forward_real) / out
+                                       (fcct_inverse_real) where the executor skips the imaginary half of its
+                                       tensor-core products (executor 10); 0 when equal to exec_flops_* */
+    double exec_flops_inverse_real;
 } fcct_plan_info_t;
 
 /* Last error message on this thread ("" if none). */

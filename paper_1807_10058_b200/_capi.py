@@ -52,6 +52,8 @@ class PlanInfo(ctypes.Structure):
         ("exec_flops_forward", c_double),
         ("exec_flops_inverse", c_double),
         ("table_bytes_forward", c_int64),
+        ("exec_flops_forward_real", c_double),
+        ("exec_flops_inverse_real", c_double),
     ]
 
 

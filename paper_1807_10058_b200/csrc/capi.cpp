@@ -213,7 +213,7 @@ void upload_orbit16(const Orbit16Host& h, Orbit16Tables& out) {
 struct OrbitPatTables {
     OrbitPatDesc desc{};
     std::vector<std::shared_ptr<DevBuf>> bufs;
-    double exec_flops = 0;
+    double exec_flops = 0, exec_flops_real = 0;
 };
 
 void upload_orbit_pat(const OrbitPatHost& h, OrbitPatTables& out) {
@@ -248,6 +248,7 @@ void upload_orbit_pat(const OrbitPatHost& h, OrbitPatTables& out) {
         d.rare_coef = static_cast<const double2*>(bc->ptr);
     }
     out.exec_flops = h.exec_flops();
+    out.exec_flops_real = h.exec_flops(true);
 }
 
 // Large-n S pass on the orbit-pattern tables (n = 32, 64, orbit_pat.hpp).
@@ -1305,6 +1306,8 @@ void fill_info(fcct_plan_s* pl) {
         if (pl->opat) {
             in.exec_flops_forward = pl->opfwd.exec_flops;
             in.exec_flops_inverse = pl->opinv.exec_flops;
+            in.exec_flops_forward_real = pl->opfwd.exec_flops_real;
+            in.exec_flops_inverse_real = pl->opinv.exec_flops_real;
         }
         if (pl->obig) {
             in.exec_flops_forward = pl->obpat ? pl->obpfwd.exec_flops : pl->obfwd.exec_flops;

@@ -94,7 +94,9 @@ struct OrbitPatHost {
     int64_t rare_terms = 0;           // non-zero terms
     int patterns = 0;                 // distinct shapes found
     int64_t dmma = 0;                 // complex-input DMMA count per block
-    double exec_flops() const;        // FP64-pipe flops per block (complex in / out)
+    // FP64-pipe flops per block; real_io: real samples in (forward) / out
+    // (inverse), where half of the DMMA products are not issued
+    double exec_flops(bool real_io = false) const;
     // modelled shared-memory wavefronts per block and plane of the fragment gathers
     // and result scatters (8-byte accesses, half-warps), and their conflict-free floor
     int64_t wavefronts = 0, wavefronts_floor = 0;

@@ -393,7 +393,7 @@ bool compile_from_blocks(int n, const Params& p, const OrbitBlocks& ob, bool inv
 
 }  // namespace
 
-double OrbitPatHost::exec_flops() const {
+double OrbitPatHost::exec_flops(bool real_io) const {
     int lg = 0;
     while ((1 << lg) < n) ++lg;
     double twiddles = 0;
@@ -403,7 +403,7 @@ double OrbitPatHost::exec_flops() const {
             if (e != 0 && 4 * e != n) twiddles += n / (2 * half);
         }
     const double fft = 3.0 * n * n * ((n / 2.0) * lg * 4.0 + 6.0 * twiddles);
-    return static_cast<double>(dmma) * 512.0 + fft + 8.0 * static_cast<double>(rare_terms) + 3.0 * 6.0 * N;
+    return static_cast<double>(real_io ? dmma / 2 : dmma) * 512.0 + fft + 8.0 * static_cast<double>(rare_terms) + 3.0 * 6.0 * N;
 }
 
 namespace {
