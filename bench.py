@@ -110,14 +110,16 @@ def profiled_traffic(cfg_name: str, f32: bool, executor: int):
     the run is not a captured configuration.
     c2 fp64 (tools/prof_run.py, 65,536 blocks): profiles/r01_orbit_fft_ws_raw.csv
     (orbit-FFT executor) or profiles/r01_pipeline2_raw.csv (stage pipeline).
-    c3 (16,384 blocks, real f64 input): the forward base change from
-    profiles/r01_orbit16_passA_raw.csv (`prof_run.py --n 16 --real`) plus the
+    c3 (16,384 blocks, real f64 input): the single-pass kernel's forward launch from
+    profiles/r02_orbit_pat_raw.csv (`prof_run.py --n 16 --real`); on the two-pass
+    executor the forward base change from profiles/r01_orbit16_passA_raw.csv plus the
     forward cube FFT from profiles/r01_orbit16_raw.csv (z is complex128 either way)."""
     parts = {
         ("c2", 2): [("r01_pipeline2_raw.csv", None)],
         ("c2", 5): [("r01_orbit_fft_ws_raw.csv", None)],
         ("c3", 6): [("r01_orbit16_passA_raw.csv", "orbit16_base_kernel<0, 2, 0>"),
                     ("r01_orbit16_raw.csv", "fft_cube_kernel<16, 1,")],
+        ("c3", 10): [("r02_orbit_pat_raw.csv", "orbit_pat_kernel<0, 2, 0>")],
     }.get((cfg_name, executor))
     if f32 or parts is None:
         return None

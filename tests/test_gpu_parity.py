@@ -708,6 +708,29 @@ def test_n16_orbit_executors(cuda, oracle_mod, p, exe, eid):
     assert rel(b32.cpu().numpy(), x) <= F32_TOL
 
 
+def test_n16_orbit_pat_many_blocks(cuda, oracle_mod):
+    """More blocks than resident CTAs (3 per SM): every CTA of the single-pass
+    executor walks several blocks (tile reuse, the TMA mbarrier's phase, the bulk
+    store's read-completion wait). 1,000 blocks against the two-pass executor,
+    the first and last block against the orbit-route oracle; real and complex I/O."""
+    n, nb = 16, 1000
+    pat, two = build_plan(n, CANON), build_plan(n, CANON, executor="orbit-two-pass")
+    assert pat.info.executor == 10 and two.info.executor == 6
+    g = torch.Generator(device="cpu").manual_seed(1610)
+    xr = torch.rand(nb, n**3, dtype=torch.float64, generator=g).mul_(2).sub_(1).to(cuda)
+    xc = torch.complex(xr, torch.rand(nb, n**3, dtype=torch.float64, generator=g).mul_(2).sub_(1).to(cuda))
+    route = oracle_mod.OrbitRoute(n, tup(CANON))
+    for x in (xr, xc):
+        y, y2 = pat.apply_values(x), two.apply_values(x)
+        assert float(torch.linalg.norm(y - y2) / torch.linalg.norm(y2)) <= 1e-13
+        ends = x[[0, nb - 1]].cpu().numpy().astype(np.complex128)
+        assert rel(y[[0, nb - 1]].cpu().numpy(), route.forward(ends)) <= F64_TOL
+        back = pat._run(y, True, real_out=not x.is_complex())
+        assert float(torch.linalg.norm(back - x) / torch.linalg.norm(x)) <= F64_TOL
+        back2 = two._run(y, True, real_out=not x.is_complex())
+        assert float(torch.linalg.norm(back - back2) / torch.linalg.norm(back2)) <= 1e-13
+
+
 @pytest.mark.parametrize("exe", ["auto", "orbit-streamed"])
 @pytest.mark.parametrize("n,p", [(32, CANON), (64, CANON), (32, SkewParams(0.21, 0.055, 0.4))])
 def test_large_n_orbit_fft(cuda, oracle_mod, n, p, exe):

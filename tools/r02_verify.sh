@@ -27,3 +27,7 @@ run c2d --method direct
 run c2f32d --method direct --precision f32 --no-cpu
 timeout 600 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err; echo "reference rc=$?"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1; echo "ncu launches rc=$?"
+# c3's dominant kernel: one ncu --set full capture (forward + inverse launch) and the raw page
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:orbit_pat_kernel -c 2 -o $O/orbit_pat_full -f python tools/prof_run.py --n 16 --blocks 16384 --real > $O/ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv python bench.py --config c3 --steps 2 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1; echo "ncu launches c3 rc=$?"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c4.csv python bench.py --config c4 --steps 2 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1; echo "ncu launches c4 rc=$?"

@@ -21,7 +21,8 @@ quick = "--quick" in sys.argv
 P = SkewParams.canonical()
 dev = torch.device("cuda:0")
 cases = [(4, "orbit", 37), (8, "orbit", 37), (8, "orbit-phased", 19), (8, "pipeline2", 19), (16, "orbit", 5),
-         (16, "two-level", 4), (32, "orbit", 1), (8, "tile", 9), (8, "global", 9)]
+         (16, "orbit", 1200), (16, "orbit-two-pass", 5), (16, "two-level", 4), (32, "orbit", 1), (32, "orbit-streamed", 1),
+         (8, "tile", 9), (8, "global", 9)]
 if not quick:
     cases += [(64, "orbit", 1), (16, "global", 2)]
 
