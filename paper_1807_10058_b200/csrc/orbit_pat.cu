@@ -163,9 +163,7 @@ __global__ void __launch_bounds__(kPatThreads, kPatCtas)
             prefetch_l2_bulk(src + static_cast<int64_t>(gridDim.x) * in_row, static_cast<uint32_t>(in_row));
         if constexpr (DIR == 0) {
             if constexpr (TMA_IN) {  // a real block: one bulk copy into the Re plane
-                // (blocks after the CTA's first were requested by the previous
-                // iteration, as soon as its last pass had read the tile)
-                if (tid == 0 && blk == static_cast<int64_t>(blockIdx.x)) {
+                if (tid == 0) {
                     mbar_arrive_expect_tx(bar, N * 8);
                     tma_load_1d(Re, src, N * 8, bar);
                 }
@@ -197,10 +195,6 @@ __global__ void __launch_bounds__(kPatThreads, kPatCtas)
 #pragma unroll
                 for (int x = 0; x < NN; ++x) ld_el<MI>(src, nat(x, hi, lo), v[x].x, v[x].y);
                 line_fft(v, d.lax[0]);
-                if constexpr (TMA_OUT) {  // the previous block's bulk store has read the Re plane
-                    if (tid == 0) tma_store_wait_read0();
-                    __syncthreads();
-                }
 #pragma unroll
                 for (int x = 0; x < NN; ++x) {
                     Re[swz(x, hi, lo)] = v[x].x;
@@ -214,10 +208,6 @@ __global__ void __launch_bounds__(kPatThreads, kPatCtas)
 #pragma unroll
                 for (int x = 0; x < NN; ++x) ld_el<MI>(src, nat(x, hi + 8, lo), w[x].x, w[x].y);
                 line_fft(v, d.lax[0]);
-                if constexpr (TMA_OUT) {  // the previous block's bulk store has read the Re plane
-                    if (tid == 0) tma_store_wait_read0();
-                    __syncthreads();
-                }
 #pragma unroll
                 for (int x = 0; x < NN; ++x) {
                     Re[swz(x, hi, lo)] = v[x].x;
@@ -288,53 +278,29 @@ __global__ void __launch_bounds__(kPatThreads, kPatCtas)
                  d.lax[2]);
             __syncthreads();
             // i axis, stored to HBM from registers (lanes vary k: coalesced)
-            if constexpr (TMA_IN && kPatLines == 2) {
-                // both lines into registers first: the tile is free after one
-                // barrier and the next block's bulk copy overlaps the butterflies
-                // and the stores
-                const int hi = tid >> 4, lo = tid & 15;
-                double2 v[NN], w[NN];
+#pragma unroll 1
+            for (int h = 0; h < kPatLines; ++h) {
+                const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
+                double2 v[NN];
 #pragma unroll
                 for (int x = 0; x < NN; ++x) v[x] = make_double2(Re[swz(x, hi, lo)], Im[swz(x, hi, lo)]);
-#pragma unroll
-                for (int x = 0; x < NN; ++x) w[x] = make_double2(Re[swz(x, hi + 8, lo)], Im[swz(x, hi + 8, lo)]);
-                __syncthreads();
-                if (tid == 0 && blk + gridDim.x < batch) {
-                    mbar_arrive_expect_tx(bar, N * 8);
-                    tma_load_1d(Re, src + static_cast<int64_t>(gridDim.x) * in_row, N * 8, bar);
-                }
                 line_fft(v, d.lax[0]);
 #pragma unroll
                 for (int x = 0; x < NN; ++x) st_el<MO>(dst, nat(x, hi, lo), v[x].x, v[x].y);
-                line_fft(w, d.lax[0]);
-#pragma unroll
-                for (int x = 0; x < NN; ++x) st_el<MO>(dst, nat(x, hi + 8, lo), w[x].x, w[x].y);
-            } else {
-#pragma unroll 1
-                for (int h = 0; h < kPatLines; ++h) {
-                    const int line = tid + h * kPatThreads, hi = line >> 4, lo = line & 15;
-                    double2 v[NN];
-#pragma unroll
-                    for (int x = 0; x < NN; ++x) v[x] = make_double2(Re[swz(x, hi, lo)], Im[swz(x, hi, lo)]);
-                    line_fft(v, d.lax[0]);
-#pragma unroll
-                    for (int x = 0; x < NN; ++x) st_el<MO>(dst, nat(x, hi, lo), v[x].x, v[x].y);
-                }
-                __syncthreads();  // the tile is refilled by the next block
             }
+            __syncthreads();  // the tile is refilled by the next block
         } else if constexpr (TMA_OUT) {  // a real block: one bulk copy out of the Re plane
-            if (tid == 0) {  // it drains while the next block's first pass loads and transforms (store_pending)
+            if (tid == 0) {
                 tma_store_1d(dst, Re, N * 8);
                 tma_store_commit();
+                tma_store_wait_read0();
             }
+            __syncthreads();
         } else {
 #pragma unroll 8
             for (int a = tid; a < N; a += kPatThreads) st_el<MO>(dst, a, Re[a], ROUT ? 0.0 : Im[a]);
             __syncthreads();
         }
-    }
-    if constexpr (TMA_OUT) {  // shared memory stays valid until the last bulk store has read it
-        if (tid == 0) tma_store_wait_read0();
     }
 }
 
