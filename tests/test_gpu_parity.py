@@ -530,7 +530,8 @@ def test_plan_store_load_or_build(cuda, oracle_mod, tmp_path):
 
 
 @pytest.mark.parametrize("n,method,precision", [(4, "fast", "f64"), (8, "fast", "f64"), (8, "fast", "f32"),
-                                                (16, "fast", "f64"), (8, "direct", "f64"), (3, "fast", "f64"),
+                                                (16, "fast", "f64"), (16, "fast", "f32"), (8, "direct", "f64"),
+                                                (3, "fast", "f64"),
                                                 (8, "direct", "f32")])
 def test_real_io_fused_matches_complex_path(cuda, oracle_mod, n, method, precision):
     """z_transform fused into the tile load (fcct_forward_real) and
