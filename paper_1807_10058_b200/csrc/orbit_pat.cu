@@ -312,8 +312,8 @@ cudaError_t launch_pat(const OrbitPatDesc& d, const void* in, void* out, int64_t
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    if (prepared != dev) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (prepared != dev) {  // the bound compile_orbit_pat enforces on the slot lists (10 KB), not this plan's size
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 16 * 16 * 16 + 16 + 10 * 1024);
         if (e != cudaSuccess) return e;
         prepared = dev;
     }
