@@ -9,7 +9,8 @@
 //     S_O = diag(Lambda[a_r]) M,  Lambda[a] = e^{2 pi i a.p/n} / 24,
 // then M holds only the carry phases e^{2 pi i t.p} (g k = a + n t) and is the
 // SAME matrix for every free orbit (24 members), and one of two matrices for the
-// 12-member orbits, ... : 8 distinct M for any n and p (measured n = 8..32).
+// 12-member orbits, ... : 8 distinct M for any n and p (measured n = 8 .. 64;
+// tools/orbit_shapes.py counts them from the group alone).
 // So the base change of a block is a GEMM with a constant 24 x 24 (and a
 // 12 x 12) complex operator over the block's OWN orbits:
 //   - the operator lives in registers as DMMA m8n8k4 B fragments (36 doubles);

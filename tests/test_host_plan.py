@@ -161,6 +161,24 @@ def test_orbit_pat_tables_emulated(p):
     assert np.linalg.norm(xi - x) / np.linalg.norm(x) < 1e-13
 
 
+@pytest.mark.parametrize("n,expect", [(8, {1: [1], 3: [1], 4: [7], 6: [3, 1], 12: [21, 1], 24: [8]}),
+                                      (16, {1: [1], 3: [1], 4: [15], 6: [7, 1], 12: [105, 3], 24: [112]})])
+def test_orbit_block_shapes_from_the_group_alone(n, expect):
+    """The structural fact the orbit-pattern executors rest on, checked without any of
+    the product's code: built from the oracle's group table with numpy, the orbit
+    blocks of S_n(p) — members in group order from the smallest member, the reduced
+    index's phase divided out — coincide in 8 matrices, all free orbits in ONE, for
+    canonical and generic offsets (tools/orbit_shapes.py)."""
+    import importlib.util
+    from pathlib import Path
+
+    spec = importlib.util.spec_from_file_location("orbit_shapes", Path(__file__).resolve().parents[1] / "tools" / "orbit_shapes.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    for p in (CANON, P2):
+        assert mod.summary(n, (p.r, p.s, p.t)) == expect
+
+
 def test_orbit_pat_tables_emulated_n32():
     """The same pattern tables drive the large-n S pass (n = 32, 64: one warp per
     tile of 8 orbits gathering from global memory): 1,120 free orbits on one
