@@ -608,7 +608,15 @@ struct OfWsCfg {
     static constexpr int YROW = (N + 4) * mode_bytes(YM);
     static constexpr int BUF = ((TB * (XROW > YROW ? XROW : YROW)) + 127) / 128 * 128;
     static constexpr int META = kOfBcWarps * TMAX * 4 * 8;
-    static constexpr int SMEM = 128 + META + 3 * BUF;
+    // fp32 plans, inverse with real f32 output: the base change's rows (scattered 4-byte
+    // elements at natural positions) are staged in shared memory and leave by TMA bulk
+    // copies, whole sectors at a time; two stages alternate. Measured: c5 inverse 0.668 ->
+    // 0.643 ms; complex64 output (8-byte elements) was slower staged (c2 fp32 inverse
+    // 0.281 -> 0.297 ms) and fp64 tiles leave no room for a stage.
+    static constexpr bool STAGE_OUT = F32 && DIR == 1 && MO == OF_R32;
+    static constexpr int SROW = N * mode_bytes(MO) + 16;  // +16: the 8 block rows start 4 banks apart
+    static constexpr int STG = STAGE_OUT ? (TB * SROW + 127) / 128 * 128 : 0;
+    static constexpr int SMEM = 128 + META + 3 * BUF + 2 * STG;
 };
 
 template <int NN, int DIR, int MI, int MO, int TMAX>
@@ -622,6 +630,7 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
     int2* meta_s = reinterpret_cast<int2*>(smem + 128);
     char* buf0 = reinterpret_cast<char*>(smem + 128 + C::META);
     auto buf = [&](int b) { return buf0 + b * C::BUF; };
+    auto stg = [&](int b) { return buf0 + 3 * C::BUF + b * C::STG; };
     const int tid = threadIdx.x, warp = tid >> 5;
     pdl_trigger();  // one CTA per SM: the next launch's CTAs take SMs as these exit
     const int64_t ntiles = (batch + TB - 1) / TB;
@@ -686,7 +695,20 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
             } else {
                 named_sync(1 + j % 2, kOfWarps * 32);    // FFT(j) has filled y(j mod 2)
                 char* dst = static_cast<char*>(out) + tile * TB * out_stride;
-                if constexpr (C::T16)
+                if constexpr (C::STAGE_OUT) {
+                    // stage j mod 2 is free once the bulk copies of tile j - 2 have read it
+                    if (tid == 0) tma_store_wait_read<1>();
+                    named_sync(7, kOfBcThreads);
+                    base_change_lean<TMAX, G, C::YM, MO>(tab, meta_w, nt_w, buf(1 + j % 2), C::YROW, stg(j % 2), C::SROW,
+                                                         r, k, nvalid);
+                    fence_proxy_async_smem();
+                    named_sync(7, kOfBcThreads);
+                    if (tid == 0) {
+                        for (int q = 0; q < nvalid; ++q)
+                            tma_store_1d(dst + q * out_stride, stg(j % 2) + q * C::SROW, out_row);
+                        tma_store_commit();
+                    }
+                } else if constexpr (C::T16)
                     base_change_lean16<TMAX, C::YM, MO>(tab, meta_w, nt_w, buf(1 + j % 2), C::YROW, dst, out_stride, r,
                                                         k, nvalid);
                 else
@@ -694,6 +716,9 @@ __global__ void __launch_bounds__(kOfWarps * 32, 1)
                                                          r, k, nvalid);
                 named_arrive(4 + j % 2, kOfWarps * 32);  // y(j mod 2) may be refilled
             }
+        }
+        if constexpr (C::STAGE_OUT) {  // shared memory stays valid until the last bulk copies have read it
+            if (tid == 0) tma_store_wait_read<0>();
         }
     } else {
         // ---------------- FFT group ----------------
