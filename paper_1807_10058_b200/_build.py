@@ -34,6 +34,12 @@ if os.environ.get("FCCT_BUILD_AB") == "1":
     FLAGS.append("-DFCCT_AB_SWITCHES")
 
 
+# FCCT_NVTX=1: NVTX ranges around the forward / inverse calls too (plan construction
+# always carries one).
+if os.environ.get("FCCT_NVTX") == "1":
+    FLAGS.append("-DFCCT_NVTX")
+
+
 STAMP = LIB_DIR / "build_flags.txt"
 
 

@@ -4,6 +4,7 @@
 // ABI; failures map to fcct_status codes with a thread-local message.
 #include <atomic>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1356,8 +1357,19 @@ void fill_info(fcct_plan_s* pl) {
     }
 }
 
+// NVTX ranges: plan construction always; the forward / inverse calls in a build with
+// FCCT_NVTX=1 (-DFCCT_NVTX: the single-transform latency config is a few microseconds per
+// call, so the apply path carries no instrumentation by default).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 fcct_plan_s* create_plan(int n, const Params& p, int method, int precision, int device,
                          PlanStore* store = nullptr, int executor = FCCT_EXEC_AUTO) {
+    NvtxRange range(method == FCCT_FAST ? "fcct build_plan" : "fcct dense_transform");
     if (executor < FCCT_EXEC_AUTO || executor > FCCT_EXEC_ORBIT_STREAMED)
         throw FcctError(ST_INVALID_ARGUMENT, "unknown executor");
     if (n < 1) throw FcctError(ST_INVALID_ARGUMENT, "build_plan: n must be >= 1");
@@ -1426,6 +1438,9 @@ void run(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t batch
     if (batch < 0) throw FcctError(ST_SIZE_MISMATCH, "batch must be >= 0");
     if (batch == 0) return;
     if (!in || !out) throw FcctError(ST_INVALID_ARGUMENT, "null buffer");
+#ifdef FCCT_NVTX
+    NvtxRange range(inverse ? "fcct inverse" : "fcct forward");
+#endif
     DeviceGuard guard(pl->device);
     if (run_staged_if_unaligned(pl, inverse, false, in, out, batch, st)) return;
     const bool f32 = pl->precision == FCCT_F32;
@@ -1658,6 +1673,9 @@ void run_real(fcct_plan_s* pl, bool inverse, const void* in, void* out, int64_t 
     if (batch < 0) throw FcctError(ST_SIZE_MISMATCH, "batch must be >= 0");
     if (batch == 0) return;
     if (!in || !out) throw FcctError(ST_INVALID_ARGUMENT, "null buffer");
+#ifdef FCCT_NVTX
+    NvtxRange range(inverse ? "fcct inverse (real output)" : "fcct forward (real input)");
+#endif
     DeviceGuard guard(pl->device);
     if (run_staged_if_unaligned(pl, inverse, true, in, out, batch, st)) return;
     const bool f32 = pl->precision == FCCT_F32;
