@@ -106,12 +106,18 @@ class DeviceGuard {
 public:
     explicit DeviceGuard(int dev) {
         ck(cudaGetDevice(&prev_), "cudaGetDevice");
-        if (prev_ != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+        if (prev_ != dev) {
+            ck(cudaSetDevice(dev), "cudaSetDevice");
+            switched_ = true;
+        }
     }
-    ~DeviceGuard() { cudaSetDevice(prev_); }
+    ~DeviceGuard() {  // nothing to restore on the caller's own device (a driver call per transform otherwise)
+        if (switched_) cudaSetDevice(prev_);
+    }
 
 private:
     int prev_ = 0;
+    bool switched_ = false;
 };
 
 // Device allocation owned by a plan.
