@@ -388,6 +388,40 @@ bool compile_from_blocks(int n, const Params& p, const OrbitBlocks& ob, bool inv
         }
     }
     if (n == 16 && h.idx.size() * 2 > 10 * 1024) return false;  // the slot lists share the CTA's shared memory with the tile
+    // structural check of the tables (the kernels index shared / global memory through
+    // them unchecked): every slot in range, and every position of the block written
+    // exactly once — by one live orbit slot of a tile or by one rare row
+    {
+        std::vector<int> written(N, 0);
+        size_t base = 0;
+        for (int c = 0; c < 2; ++c) {
+            const int d = cls_d[c];
+            for (int t = 0; t < h.ntiles[c]; ++t)
+                for (int m = 0; m < d; ++m)
+                    for (int o = 0; o < 8; ++o) {
+                        const int slot = h.idx[base + (static_cast<size_t>(t) * d + m) * 8 + o];
+                        if (slot < 0 || slot >= N) return false;
+                        if (t * 8 + o < h.cnt[c]) ++written[slot];
+                    }
+            base += static_cast<size_t>(h.ntiles[c]) * d * 8;
+        }
+        if (base != h.idx.size()) return false;
+        for (int r = 0; r < h.nrare; ++r) {
+            if (h.rare_out[r] < 0 || h.rare_out[r] >= N) return false;
+            ++written[h.rare_out[r]];
+        }
+        for (int v : h.rare_in)
+            if (v < 0 || v >= N) return false;
+        for (int a = 0; a < N; ++a)
+            if (written[a] != 1) return false;
+        int tiles[2] = {0, 0};
+        for (int c = 0; c < 2; ++c)
+            for (int w = 0; w < kPatWarps; ++w) {
+                if (h.warp_tiles[(c * kPatWarps + w) * 2] != tiles[c]) return false;  // contiguous, complete
+                tiles[c] += h.warp_tiles[(c * kPatWarps + w) * 2 + 1];
+            }
+        if (tiles[0] != h.ntiles[0] || tiles[1] != h.ntiles[1]) return false;
+    }
     return true;
 }
 
